@@ -1,0 +1,395 @@
+// extern "C" surface for the octree build side of libvtx (include/vtx.h).
+#include <algorithm>
+#include <cstring>
+
+#include "tree.cuh"
+
+using namespace vtx;
+
+namespace vtx {
+const char* last_error();
+}
+
+namespace {
+
+__global__ void k_scatter_stats(const int64_t* __restrict__ nodes, int n,
+                                const int32_t* __restrict__ in, int32_t* stats) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n * ST_N * kMaxC) return;
+  int r = i / (ST_N * kMaxC), w = i % (ST_N * kMaxC);
+  stats[nodes[r] * ST_N * kMaxC + w] = in[i];
+}
+
+// standalone halfsample_block (octree.py:58-92) on int32 values
+__global__ void k_halfsample(const int32_t* __restrict__ v, int mz, int my, int mx, int C, int cx,
+                             int cy, int cz, int kx, int ky, int kz, int bg, int32_t* out) {
+  int oz = mz / kz, oy = my / ky, ox = mx / kx;
+  int64_t n = (int64_t)oz * oy * ox * C;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int c = (int)(e % C);
+    int64_t p = e / C;
+    int x = (int)(p % ox), y = (int)((p / ox) % oy), z = (int)(p / ((int64_t)ox * oy));
+    long long s = 0;
+    int cnt = 0;
+    for (int dz = 0; dz < kz; ++dz)
+      for (int dy = 0; dy < ky; ++dy)
+        for (int dx = 0; dx < kx; ++dx) {
+          int sz = kz * z + dz, sy = ky * y + dy, sx = kx * x + dx;
+          if (sx < cx && sy < cy && sz < cz) {
+            s += v[(((int64_t)sz * my + sy) * mx + sx) * C + c];
+            ++cnt;
+          }
+        }
+    out[e] = cnt ? (int32_t)((2 * s + cnt) / (2 * cnt)) : bg;
+  }
+}
+
+// synthetic volumes: bit-identical twins of oracle/voxtree_oracle.py
+__device__ __forceinline__ uint32_t hash4(uint32_t x, uint32_t y, uint32_t z, uint32_t c,
+                                          uint32_t seed) {
+  uint32_t h = x * 0x9E3779B1u;
+  h ^= y * 0x85EBCA77u;
+  h *= 0xC2B2AE3Du;
+  h ^= z * 0x27D4EB2Fu;
+  h ^= c * 0x165667B1u + seed;
+  h ^= h >> 15;
+  h *= 0x2C1B3C6Du;
+  h ^= h >> 12;
+  h *= 0x297A2D39u;
+  h ^= h >> 15;
+  return h;
+}
+
+template <class T>
+__global__ void k_synth(T* out, int kind, int dx, int dy, int dz, int C, int fmax, uint32_t seed,
+                        int z0, int z1) {
+  const int64_t n = (int64_t)(z1 - z0) * dy * dx;
+  const bool big = fmax > 255;
+  const int amp = big ? 40000 : 220, base = big ? 100 : 8, nmask = big ? 15 : 3;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int x = (int)(e % dx);
+    int y = (int)((e / dx) % dy);
+    int z = z0 + (int)(e / ((int64_t)dx * dy));
+    T* o = out + e * C;
+    if (kind == 0) {
+      for (int c = 0; c < C; ++c) o[c] = (T)(hash4(x, y, z, c, seed) % (uint32_t)(fmax + 1));
+      continue;
+    }
+    long long ex = (long long)(2 * x - dx) * (2 * x - dx) * 10000 / max((long long)dx * dx, 1LL);
+    long long ey = (long long)(2 * y - dy) * (2 * y - dy) * 10000 / max((long long)dy * dy, 1LL);
+    long long ez = (long long)(2 * z - dz) * (2 * z - dz) * 10000 / max((long long)dz * dz, 1LL);
+    bool inside = ex + ey + ez <= 8100;
+    int lx = (x & 31) - 16, ly = (y & 31) - 16, lz = (z & 31) - 16;
+    int d2 = lx * lx + ly * ly + lz * lz;
+    for (int c = 0; c < C; ++c) {
+      long long v = base + (hash4(x, y, z, c, seed) & (uint32_t)nmask);
+      uint32_t hc = hash4(x >> 5, y >> 5, z >> 5, c + 7, seed);
+      if (inside && (hc % 4u) == 0) {
+        long long r = 4 + (hc >> 8) % 9u;
+        long long r2 = r * r;
+        long long b = r2 - d2;
+        v += b > 0 ? (long long)amp * b / r2 : 0;
+      }
+      o[c] = (T)(v < 0 ? 0 : (v > fmax ? fmax : v));
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* vt_last_error(void) { return vtx::last_error(); }
+int32_t vt_abi_version(void) { return 1; }
+
+vt_status vt_tree_create(const vt_tree_desc* desc, vt_tree** out) {
+  return guarded([&] {
+    VT_REQUIRE(desc && out, VT_EINVAL, "null argument");
+    *out = new vt_tree(*desc);
+  });
+}
+
+vt_status vt_tree_destroy(vt_tree* tree) {
+  return guarded([&] { delete tree; });
+}
+
+vt_status vt_tree_set_stream(vt_tree* tree, void* stream) {
+  return guarded([&] {
+    Tree& t = tree->t;
+    VT_CUDA(cudaStreamSynchronize(t.stream));
+    if (t.own_stream) VT_CUDA(cudaStreamDestroy(t.stream));
+    t.own_stream = false;
+    t.stream = (cudaStream_t)stream;
+  });
+}
+
+vt_status vt_tree_insert(vt_tree* tree, int32_t channel, const int32_t origin[3],
+                         const int32_t dims[3], const void* samples, int32_t mem_kind) {
+  return guarded([&] {
+    VT_REQUIRE(channel >= 0, VT_EINVAL, "channel " + std::to_string(channel) + " out of range");
+    tree->t.insert(channel, origin, dims, samples, mem_kind);
+  });
+}
+
+vt_status vt_tree_insert_channels(vt_tree* tree, const int32_t origin[3], const int32_t dims[3],
+                                  const void* samples, int32_t mem_kind) {
+  return guarded([&] { tree->t.insert(-1, origin, dims, samples, mem_kind); });
+}
+
+vt_status vt_tree_take_events(vt_tree* tree, int32_t* kinds, int64_t* indices, int64_t cap,
+                              int64_t* n, int32_t* more) {
+  return guarded([&] {
+    auto& ev = tree->t.events;
+    int64_t m = std::min<int64_t>(cap, (int64_t)ev.size());
+    for (int64_t i = 0; i < m; ++i) {
+      kinds[i] = ev[i].first;
+      indices[i] = ev[i].second;
+    }
+    ev.erase(ev.begin(), ev.begin() + m);
+    *n = m;
+    *more = ev.empty() ? 0 : 1;
+  });
+}
+
+vt_status vt_tree_finalize(vt_tree* tree) {
+  return guarded([&] { tree->t.finished = true; });
+}
+
+vt_status vt_tree_fill_borders(vt_tree* tree) {
+  return guarded([&] { tree->t.fill_borders(); });
+}
+
+vt_status vt_tree_sync(vt_tree* tree) {
+  return guarded([&] { tree->t.sync(); });
+}
+
+vt_status vt_tree_info_get(vt_tree* tree, vt_tree_info* o) {
+  return guarded([&] {
+    const Tree& t = tree->t;
+    o->node_count = t.node_count;
+    o->brick_count = t.brick_count;
+    o->pruned_bricks = t.pruned;
+    o->inserted_voxels = t.inserted;
+    o->capacity = t.g.capacity;
+    o->pool_slots = t.pool_slots;
+    o->depth = t.g.depth;
+    for (int a = 0; a < 3; ++a) o->virtual_dims[a] = t.g.virt[a];
+    o->finished = t.finished;
+    o->borders_filled = t.borders;
+  });
+}
+
+vt_status vt_tree_node(vt_tree* tree, int64_t index, vt_node* out, int32_t* exists) {
+  return guarded([&] {
+    Tree& t = tree->t;
+    *exists = 0;
+    if (index < 0 || index >= t.g.capacity || !(t.flags[index] & NF_EXISTS)) return;
+    t.flush();
+    t.gather_stats({index});
+    *exists = 1;
+    out->flags = t.flags[index];
+    out->level = t.g.level_of(index);
+    t.g.box_lo(index, out->box_lo);
+    out->slot = t.slot[index];
+    for (int c = 0; c < kMaxC; ++c)
+      for (int s = 0; s < ST_N; ++s) out->stats[c][s] = c < t.g.C ? t.stat(index, s, c) : 0;
+  });
+}
+
+vt_status vt_tree_list_nodes(vt_tree* tree, int64_t* out, int32_t* fl, int64_t cap,
+                             int64_t* n) {
+  return guarded([&] {
+    const Tree& t = tree->t;
+    int64_t m = 0;
+    for (int64_t i = 0; i < t.g.capacity; ++i)
+      if (t.flags[i] & NF_EXISTS) {
+        if (m < cap) {
+          if (out) out[m] = i;
+          if (fl) fl[m] = t.flags[i];
+        }
+        ++m;
+      }
+    *n = m;
+  });
+}
+
+vt_status vt_tree_find_node(vt_tree* tree, const double point[3], int32_t target, int64_t* index) {
+  return guarded([&] { *index = tree->t.find_node(point, target); });
+}
+
+vt_status vt_tree_read_brick(vt_tree* tree, int64_t index, void* out) {
+  return guarded([&] {
+    Tree& t = tree->t;
+    VT_REQUIRE(index >= 0 && index < t.g.capacity && (t.flags[index] & NF_BRICK), VT_EINVAL,
+               "node has no brick");
+    t.flush();
+    const int64_t bytes = t.g.brick_elems * t.g.sb;
+    VT_CUDA(cudaMemcpyAsync(out, t.d_pool + (int64_t)t.slot[index] * bytes, bytes,
+                            cudaMemcpyDeviceToHost, t.stream));
+    VT_CUDA(cudaStreamSynchronize(t.stream));
+  });
+}
+
+vt_status vt_tree_export(vt_tree* tree, int64_t n, const int64_t* indices, int32_t* stats,
+                         void* bricks) {
+  return guarded([&] {
+    Tree& t = tree->t;
+    t.flush();
+    std::vector<int64_t> nodes(indices, indices + n);
+    for (int64_t i : nodes)
+      VT_REQUIRE(i >= 0 && i < t.g.capacity && (t.flags[i] & NF_EXISTS), VT_EINVAL,
+                 "export of a node that does not exist");
+    t.gather_stats(nodes);
+    const int C = t.g.C;
+    for (int64_t r = 0; r < n; ++r)
+      for (int c = 0; c < C; ++c)
+        for (int s = 0; s < ST_N; ++s) stats[(r * C + c) * ST_N + s] = t.stat(nodes[r], s, c);
+    if (!bricks) return;
+    std::vector<int32_t> slots;
+    for (int64_t i : nodes)
+      if (t.flags[i] & NF_BRICK) slots.push_back(t.slot[i]);
+    const int64_t bb = t.g.brick_elems * t.g.sb;
+    const int64_t batch = std::max<int64_t>(1, (256LL << 20) / bb);
+    uint8_t* dbuf = nullptr;
+    VT_CUDA(cudaMallocAsync(&dbuf, std::min<int64_t>(batch, std::max<size_t>(1, slots.size())) * bb,
+                            t.stream));
+    for (size_t o = 0; o < slots.size(); o += batch) {
+      int m = (int)std::min<int64_t>(batch, slots.size() - o);
+      std::vector<int32_t> part(slots.begin() + o, slots.begin() + o + m);
+      int32_t* ds = upload(t, part);
+      launch_gather_bricks(t, ds, m, dbuf);
+      VT_CUDA(cudaMemcpyAsync((uint8_t*)bricks + o * bb, dbuf, m * bb, cudaMemcpyDeviceToHost,
+                              t.stream));
+      release(t, ds);
+      VT_CUDA(cudaStreamSynchronize(t.stream));
+    }
+    release(t, dbuf);
+    VT_CUDA(cudaStreamSynchronize(t.stream));
+  });
+}
+
+vt_status vt_tree_import(vt_tree* tree, int64_t n, const int64_t* indices, const int32_t* nflags,
+                         const int32_t* stats, const void* bricks, int32_t finished,
+                         int32_t borders_filled, int64_t pruned_bricks) {
+  return guarded([&] {
+    Tree& t = tree->t;
+    VT_REQUIRE(t.node_count == 1 && t.brick_count == 0, VT_ESTATE, "import into a non-empty tree");
+    const int C = t.g.C;
+    std::vector<int64_t> nodes(indices, indices + n);
+    std::vector<int32_t> st(n * ST_N * kMaxC, 0);
+    std::vector<int32_t> slots;
+    t.node_count = 0;
+    for (int64_t r = 0; r < n; ++r) {
+      int64_t i = nodes[r];
+      VT_REQUIRE(i >= 0 && i < t.g.capacity, VT_EINVAL, "node index outside the tree");
+      int f = nflags[r];
+      uint8_t hf = NF_EXISTS;
+      if (f & VT_NODE_CHILDREN) hf |= NF_CHILDREN;
+      if (f & VT_NODE_IN_VOLUME) hf |= NF_INVOL;
+      t.flags[i] = hf;
+      t.slot[i] = -1;
+      if (f & VT_NODE_BRICK) {
+        t.flags[i] |= NF_BRICK;
+        t.slot[i] = t.alloc_slot();
+        slots.push_back(t.slot[i]);
+        ++t.brick_count;
+      }
+      t.mark_struct(i);
+      ++t.node_count;
+      for (int c = 0; c < C; ++c)
+        for (int s = 0; s < ST_N; ++s) {
+          int v = stats[(r * C + c) * ST_N + s];
+          st[(r * ST_N + s) * kMaxC + c] = v;
+          t.h_stats[st_index(i, s, c)] = v;
+        }
+    }
+    t.flush_structure();
+    int64_t* dn = upload(t, nodes);
+    int32_t* dst = upload(t, st);
+    if (n) {
+      int work = (int)(n * ST_N * kMaxC);
+      k_scatter_stats<<<(work + 255) / 256, 256, 0, t.stream>>>(dn, (int)n, dst, t.d_stats);
+      VT_CUDA(cudaGetLastError());
+    }
+    release(t, dn);
+    release(t, dst);
+    const int64_t bb = t.g.brick_elems * t.g.sb;
+    if (!slots.empty()) {
+      uint8_t* dbuf = nullptr;
+      VT_CUDA(cudaMallocAsync(&dbuf, slots.size() * bb, t.stream));
+      VT_CUDA(cudaMemcpyAsync(dbuf, bricks, slots.size() * bb, cudaMemcpyHostToDevice, t.stream));
+      int32_t* ds = upload(t, slots);
+      launch_scatter_bricks(t, ds, (int)slots.size(), dbuf);
+      release(t, ds);
+      release(t, dbuf);
+    }
+    // plane partials for later incremental insertions
+    std::vector<PlaneJob> planes;
+    for (int64_t i : nodes)
+      if (t.flags[i] & NF_BRICK) {
+        int ce[3];
+        t.node_in_extent(i, ce);
+        if (ce[0] > 0 && ce[1] > 0)
+          for (int z = 0; z < ce[2]; ++z) planes.push_back({t.slot[i], z, ce[0], ce[1]});
+      }
+    PlaneJob* dp = upload(t, planes);
+    launch_plane(t, dp, (int)planes.size());
+    release(t, dp);
+    t.finished = finished != 0;
+    t.borders = borders_filled != 0;
+    t.pruned = pruned_bricks;
+    VT_CUDA(cudaStreamSynchronize(t.stream));
+  });
+}
+
+vt_status vt_halfsample(const int32_t* values, const int32_t shape[4], const int32_t ext[3],
+                        const int32_t split[3], int32_t background, int32_t* out,
+                        int32_t device) {
+  return guarded([&] {
+    VT_CUDA(cudaSetDevice(device));
+    int mz = shape[0], my = shape[1], mx = shape[2], C = shape[3];
+    int kx = split[0] ? 2 : 1, ky = split[1] ? 2 : 1, kz = split[2] ? 2 : 1;
+    int64_t nin = (int64_t)mz * my * mx * C;
+    int64_t nout = (int64_t)(mz / kz) * (my / ky) * (mx / kx) * C;
+    int32_t *din = nullptr, *dout = nullptr;
+    VT_CUDA(cudaMalloc(&din, std::max<int64_t>(1, nin) * 4));
+    VT_CUDA(cudaMalloc(&dout, std::max<int64_t>(1, nout) * 4));
+    VT_CUDA(cudaMemcpy(din, values, nin * 4, cudaMemcpyHostToDevice));
+    if (nout) {
+      k_halfsample<<<(unsigned)std::min<int64_t>((nout + 255) / 256, 4096), 256>>>(
+          din, mz, my, mx, C, ext[0], ext[1], ext[2], kx, ky, kz, background, dout);
+      VT_CUDA(cudaGetLastError());
+    }
+    VT_CUDA(cudaMemcpy(out, dout, nout * 4, cudaMemcpyDeviceToHost));
+    cudaFree(din);
+    cudaFree(dout);
+  });
+}
+
+vt_status vt_synth(void* out, int32_t kind, const int32_t dims[3], int32_t C, int32_t sb,
+                   uint32_t seed, int32_t z0, int32_t z1, void* stream) {
+  return guarded([&] {
+    VT_REQUIRE(sb == 1 || sb == 2, VT_EINVAL, "sample bytes must be 1 or 2");
+    int64_t n = (int64_t)(z1 - z0) * dims[1] * dims[0];
+    unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32);
+    if (n <= 0) return;
+    if (sb == 1)
+      k_synth<uint8_t><<<grid, 256, 0, (cudaStream_t)stream>>>(
+          (uint8_t*)out, kind, dims[0], dims[1], dims[2], C, 255, seed, z0, z1);
+    else
+      k_synth<uint16_t><<<grid, 256, 0, (cudaStream_t)stream>>>(
+          (uint16_t*)out, kind, dims[0], dims[1], dims[2], C, 65535, seed, z0, z1);
+    VT_CUDA(cudaGetLastError());
+  });
+}
+
+vt_status vt_last_kernel_ms(vt_tree* tree, double* render_ms, double* build_ms) {
+  return guarded([&] {
+    if (render_ms) *render_ms = tree->t.last_render_ms;
+    if (build_ms) *build_ms = tree->t.last_build_ms;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,1037 @@
+// Device mirror (DeviceState, device.py:124-386) and the octree ray caster
+// (render/raycast.py:40-339, render/core.py:34-187) for sm_100a.
+//
+// One thread per ray, one warp per 8x4 pixel tile.  Every ray is
+// independent within a pass (the node buffer and brick buffer are frozen,
+// flags are idempotent ORs, counters are sums), so marching each ray to
+// completion reproduces the reference's wavefront `march` exactly.
+//
+// Arithmetic: FP64 throughout, compiled with -fmad=false, following the
+// reference's numpy operation order (sampling positions, LOD, trilinear
+// weights, np.interp transfer functions, compositing), so images match the
+// CPU reference to ~1e-15 rather than merely within the 1/255 tolerance.
+// The gather (8 corners x C channels per pos-sample from the brick buffer)
+// is the bandwidth limiter; FP64 on B200 runs at half the FP32 rate, which
+// this kernel never approaches.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+
+#include "tree.cuh"
+
+using namespace vtx;
+
+struct vt_mirror {
+  vt_tree* tree = nullptr;
+  bool zero_copy = false;
+  int64_t slots = 0;
+  uint64_t* d_nb = nullptr;
+  uint8_t* d_fb = nullptr;
+  uint8_t* d_bb = nullptr;   // own brick buffer (bounded mode)
+  int32_t* d_res = nullptr;  // node -> brick-buffer slot or -1 (bounded mode)
+};
+
+namespace {
+
+constexpr int kMaxLevels = kMaxDepth + 1;
+
+struct RenderParams {
+  Geo g;
+  double dims[3], spacing[3], box_hi[3];
+  double ext[kMaxLevels][3], scl[kMaxLevels][3];
+  double base_voxel;
+  double fmax;
+  double qmax;
+  int avg_w;
+  int borders_filled;
+  int zero_copy;
+  // scene
+  double cam[3], fwd[3], right[3], up[3];
+  double tan_half, aspect, pfs;  // pixel_footprint_scale
+  int W, H;
+  int mip;
+  double step, corr, et, lod_scale;
+  int has_et;
+  int tf_n[kMaxC];
+  double tf_x[kMaxC][VT_MAX_TF_POINTS];
+  double tf_v[kMaxC][VT_MAX_TF_POINTS][4];
+  int n_clips;
+  double clip_n[3][3], clip_o[3];
+  int has_tr;
+  double tr[kMaxC][12];
+  // tile restriction
+  int rect[4];  // x0, y0, x1, y1
+};
+
+// per-launch scene + geometry; render entry points serialise on g_render_mu
+__constant__ RenderParams c_P;
+
+struct RayOut {
+  double rgb[3], a;
+  double mip[kMaxC];
+};
+
+struct Counters {
+  long long samples, tf, avgfb, coarse, req, used;
+};
+
+__device__ __forceinline__ double clampd(double v, double lo, double hi) {
+  return fmin(fmax(v, lo), hi);
+}
+
+// np.clip(a, lo, hi) == minimum(maximum(a, lo), hi)
+__device__ __forceinline__ double npclip(double v, double lo, double hi) {
+  double m = v > lo ? v : (v != v ? v : lo);
+  return m < hi ? m : (m != m ? m : hi);
+}
+
+// camera.py:41-53
+__device__ void ray_dir(int i, int j, double d[3]) {
+  const RenderParams& P = c_P;
+  double xs = (2.0 * ((double)i + 0.5) / (double)P.W - 1.0) * P.tan_half * P.aspect;
+  double ys = (1.0 - 2.0 * ((double)j + 0.5) / (double)P.H) * P.tan_half;
+  for (int a = 0; a < 3; ++a) d[a] = P.fwd[a] + xs * P.right[a] + ys * P.up[a];
+  double n = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+  for (int a = 0; a < 3; ++a) d[a] = d[a] / n;
+}
+
+// compute_ray_bounds (core.py:34-67) + RayBatch step count (core.py:79-89)
+__device__ void ray_setup(const double d[3], double& t0o, long long& n) {
+  const RenderParams& P = c_P;
+  double t0 = 0.0, t1 = INFINITY;
+  for (int a = 0; a < 3; ++a) {
+    double o = P.cam[a], dd = d[a];
+    double near_, far_;
+    if (dd == 0.0) {
+      bool in = o >= 0.0 && o <= P.box_hi[a];
+      near_ = in ? -INFINITY : INFINITY;
+      far_ = in ? INFINITY : -INFINITY;
+    } else {
+      double ta = (0.0 - o) / dd, tb = (P.box_hi[a] - o) / dd;
+      near_ = fmin(ta, tb);
+      far_ = fmax(ta, tb);
+    }
+    t0 = fmax(t0, near_);
+    t1 = fmin(t1, far_);
+  }
+  for (int q = 0; q < P.n_clips; ++q) {
+    const double* nn = P.clip_n[q];
+    double num = P.clip_o[q] - (P.cam[0] * nn[0] + P.cam[1] * nn[1] + P.cam[2] * nn[2]);
+    double den = d[0] * nn[0] + d[1] * nn[1] + d[2] * nn[2];
+    double tc = num / den;
+    bool keep = den == 0.0 && num >= 0.0;
+    bool kill = den == 0.0 && num < 0.0;
+    if (den > 0.0)
+      t1 = fmin(t1, tc);
+    else if (!keep && !kill)
+      t0 = fmax(t0, tc);
+    if (kill) t1 = -INFINITY;
+  }
+  bool hit = t0 < t1;
+  double span = fmax(t1 - t0, 0.0);
+  t0o = hit ? t0 : 0.0;
+  n = hit ? (long long)ceil(span / P.step - 1e-12) : 0;
+}
+
+// np.interp on sorted control points (transfer.py:34-41)
+__device__ double interp(int c, int comp, double x) {
+  const RenderParams& P = c_P;
+  const int n = P.tf_n[c];
+  const double* xp = P.tf_x[c];
+  if (!(x >= xp[0])) {
+    if (x != x) return x;
+    return P.tf_v[c][0][comp];
+  }
+  if (x >= xp[n - 1]) return P.tf_v[c][n - 1][comp];
+  int j = 0;
+  while (j + 1 < n && !(x < xp[j + 1])) ++j;
+  double y0 = P.tf_v[c][j][comp], y1 = P.tf_v[c][j + 1][comp];
+  double slope = (y1 - y0) / (xp[j + 1] - xp[j]);
+  double r = slope * (x - xp[j]) + y0;
+  if (r != r) {
+    r = slope * (x - xp[j + 1]) + y1;
+    if (r != r && y0 == y1) r = y0;
+  }
+  return r;
+}
+
+struct DescentCache {
+  int target = -1;
+  int lvl;
+  long long idx;
+  double lo[3];
+  long long a_idx[2];
+  int a_lvl[2];
+  double a_lo[2][3];
+};
+
+#define P c_P
+template <class T>
+struct Sampler {
+  const uint64_t* __restrict__ nb;
+  uint8_t* fb;
+  const T* __restrict__ bb;
+  bool fullframe;
+  Counters& cnt;
+  long long last_used = -1, last_req = -1;
+  DescentCache cache[kMaxC];
+
+  __device__ Sampler(const uint64_t* n, uint8_t* f, const T* b, bool ff, Counters& c)
+      : nb(n), fb(f), bb(b), fullframe(ff), cnt(c) {}
+
+  __device__ void mark(long long idx, unsigned flag) {
+    long long& last = flag == 1 ? last_used : last_req;
+    if (last == idx) return;
+    last = idx;
+    unsigned* w = reinterpret_cast<unsigned*>(fb + (idx & ~3LL));
+    unsigned bit = flag << ((idx & 3) * 8);
+    if (!(__ldcg(w) & bit)) atomicOr(w, bit);
+  }
+
+  __device__ double avg_of(uint64_t e, int c) const {
+    uint64_t q = (e >> (24 + c * P.avg_w)) & ((1ULL << P.avg_w) - 1);
+    return rint((double)q * P.fmax / P.qmax);
+  }
+
+  __device__ double trilerp(uint64_t e, int lvl, const double lo[3], const double pv[3],
+                            int c) const {
+    const long long slot = (long long)((e >> 24) & 0xFFFFFFFFULL);
+    const T* b = bb + slot * P.g.brick_elems;
+    int i0[3];
+    double w1[3], w0[3];
+    for (int a = 0; a < 3; ++a) {
+      double m = (double)P.g.brick[a];
+      double f = (pv[a] - lo[a]) / P.scl[lvl][a] + 0.5;
+      f = P.borders_filled ? npclip(f, 0.0, m + 1.0) : npclip(f, 1.0, m);
+      long long fi = (long long)floor(f);
+      fi = fi < 0 ? 0 : (fi > P.g.brick[a] ? P.g.brick[a] : fi);
+      i0[a] = (int)fi;
+      w1[a] = npclip(f - (double)fi, 0.0, 1.0);
+      w0[a] = 1.0 - w1[a];
+    }
+    const int sx = P.g.stored[0], sy = P.g.stored[1], C = P.g.C;
+    const int64_t sxC = (int64_t)sx * C, sxyC = (int64_t)sx * sy * C;
+    const T* p = b + i0[2] * sxyC + i0[1] * sxC + (int64_t)i0[0] * C + c;
+    double v = 0.0;
+#pragma unroll
+    for (int dz = 0; dz < 2; ++dz) {
+      double wz = dz ? w1[2] : w0[2];
+#pragma unroll
+      for (int dy = 0; dy < 2; ++dy) {
+        double wy = dy ? w1[1] : w0[1];
+#pragma unroll
+        for (int dx = 0; dx < 2; ++dx) {
+          double wx = dx ? w1[0] : w0[0];
+          double corner = (double)__ldg(p + dz * sxyC + dy * sxC + dx * C);
+          v = v + wz * wy * wx * corner;
+        }
+      }
+    }
+    return v;
+  }
+
+  // raycast.py:86-123 with a per-channel-group descent cache
+  __device__ void descend(const double pv[3], int target, DescentCache& dc) {
+    if (dc.target == target) {
+      bool ok = true;
+      for (int a = 0; a < 3; ++a)
+        if (P.g.split[a] && !(pv[a] >= dc.lo[a] && pv[a] < dc.lo[a] + P.ext[dc.lvl][a])) ok = false;
+      if (ok) return;
+    }
+    long long idx = 0;
+    int lvl = P.g.depth;
+    double lo[3] = {0.0, 0.0, 0.0};
+    long long a1 = -1, a2 = -1;
+    int a1l = 0, a2l = 0;
+    double a1lo[3] = {0, 0, 0}, a2lo[3] = {0, 0, 0};
+    for (int it = 0; it < P.g.depth; ++it) {
+      uint64_t e = __ldg(nb + idx);
+      long long ptr = (long long)((e >> 2) & 0x3FFFFFULL);
+      if (!(ptr != 0 && lvl > target)) break;
+      int k = 0;
+      double nlo[3];
+      for (int a = 0; a < 3; ++a) {
+        double half = P.ext[lvl - 1][a];
+        bool bit = (pv[a] >= lo[a] + half) && P.g.split[a];
+        k |= bit ? (1 << a) : 0;
+        nlo[a] = lo[a] + (bit ? half : 0.0);
+      }
+      a2 = a1;
+      a2l = a1l;
+      for (int a = 0; a < 3; ++a) a2lo[a] = a1lo[a];
+      a1 = idx;
+      a1l = lvl;
+      for (int a = 0; a < 3; ++a) {
+        a1lo[a] = lo[a];
+        lo[a] = nlo[a];
+      }
+      idx = 8 * (ptr - 1) + 1 + k;
+      --lvl;
+    }
+    dc.target = target;
+    dc.idx = idx;
+    dc.lvl = lvl;
+    for (int a = 0; a < 3; ++a) {
+      dc.lo[a] = lo[a];
+      dc.a_lo[0][a] = a1lo[a];
+      dc.a_lo[1][a] = a2lo[a];
+    }
+    dc.a_idx[0] = a1;
+    dc.a_idx[1] = a2;
+    dc.a_lvl[0] = a1l;
+    dc.a_lvl[1] = a2l;
+  }
+
+  // optimal_lod (raycast.py:40-50)
+  __device__ int lod(const double p[3]) const {
+    double z = (p[0] - P.cam[0]) * P.fwd[0] + (p[1] - P.cam[1]) * P.fwd[1] +
+               (p[2] - P.cam[2]) * P.fwd[2];
+    double fp = fmax(z, 1e-12) * P.pfs;
+    fp = fp * P.lod_scale;
+    double l = floor(log2(fmax(fp / P.base_voxel, 1e-300)));
+    l = fmin(fmax(l, 0.0), (double)P.g.depth);
+    return (int)l;
+  }
+
+  // _resolve + _fullframe_fallback (raycast.py:167-238) for channels [c0, c1)
+  __device__ bool resolve(const double pv[3], int target, int c0, int c1, double* out,
+                          DescentCache& dc) {
+    descend(pv, target, dc);
+    const uint64_t e = __ldg(nb + dc.idx);
+    const bool resident = e & 1, nh = e & 2;
+    if (!nh) {
+      for (int c = c0; c < c1; ++c) out[c] = avg_of(e, c);
+      return false;
+    }
+    if (resident) {
+      for (int c = c0; c < c1; ++c) out[c] = trilerp(e, dc.lvl, dc.lo, pv, c);
+      mark(dc.idx, 1);
+      cnt.used++;
+      return false;
+    }
+    mark(dc.idx, 2);
+    cnt.req++;
+    if (!fullframe) return true;
+    for (int q = 0; q < 2; ++q) {
+      long long ai = dc.a_idx[q];
+      if (ai < 0) continue;
+      uint64_t ae = __ldg(nb + ai);
+      if (ae & 1) {
+        for (int c = c0; c < c1; ++c) out[c] = trilerp(ae, dc.a_lvl[q], dc.a_lo[q], pv, c);
+        mark(ai, 1);
+        cnt.used++;
+        cnt.coarse++;
+        return false;
+      }
+      if (ae & 2) {
+        mark(ai, 2);
+        cnt.req++;
+      }
+    }
+    for (int c = c0; c < c1; ++c) out[c] = avg_of(e, c);
+    cnt.avgfb++;
+    return false;
+  }
+
+  // sampler (raycast.py:242-278); returns missing
+  __device__ bool sample(const double p[3], double* vals) {
+    const int C = P.g.C;
+    for (int c = 0; c < C; ++c) vals[c] = (double)P.g.bg;
+    if (!P.has_tr) {
+      double pv[3];
+      bool in = true;
+      for (int a = 0; a < 3; ++a) {
+        pv[a] = p[a] / P.spacing[a];
+        in = in && pv[a] >= 0.0 && pv[a] <= P.dims[a];
+      }
+      if (!in) return false;
+      int target = lod(p);
+      for (int a = 0; a < 3; ++a) pv[a] = npclip(pv[a], 0.0, P.dims[a] - 1e-9);
+      return resolve(pv, target, 0, C, vals, cache[0]);
+    }
+    bool missing = false;
+    for (int c = 0; c < C; ++c) {
+      const double* m = P.tr[c];
+      double q[3], pv[3];
+      bool in = true;
+      for (int r = 0; r < 3; ++r) {
+        q[r] = p[0] * m[r * 4 + 0] + p[1] * m[r * 4 + 1] + p[2] * m[r * 4 + 2] + m[r * 4 + 3];
+        pv[r] = q[r] / P.spacing[r];
+        in = in && pv[r] >= 0.0 && pv[r] <= P.dims[r];
+      }
+      if (!in) continue;
+      int target = lod(q);
+      for (int a = 0; a < 3; ++a) pv[a] = npclip(pv[a], 0.0, P.dims[a] - 1e-9);
+      missing |= resolve(pv, target, c, c + 1, vals, cache[c]);
+    }
+    return missing;
+  }
+};
+
+#undef P
+
+// composite_step (core.py:110-134); returns terminated
+__device__ bool composite(const double* vals, RayOut& o, Counters& cnt) {
+  const RenderParams& P = c_P;
+  const int C = P.g.C;
+  if (P.mip) {
+    for (int c = 0; c < C; ++c) o.mip[c] = fmax(o.mip[c], vals[c]);
+    return false;
+  }
+  double srgb[3] = {0.0, 0.0, 0.0};
+  double trans = 1.0;
+  for (int c = 0; c < C; ++c) {
+    double x = vals[c] / P.fmax;
+    double alpha_tf = interp(c, 3, x);
+    cnt.tf++;
+    double alpha = 1.0 - (P.corr == 1.0 ? (1.0 - alpha_tf) : pow(1.0 - alpha_tf, P.corr));
+    for (int a = 0; a < 3; ++a) srgb[a] = srgb[a] + interp(c, a, x) * alpha;
+    trans = trans * (1.0 - alpha);
+  }
+  for (int a = 0; a < 3; ++a) srgb[a] = npclip(srgb[a], 0.0, 1.0);
+  double sa = 1.0 - trans;
+  double w = 1.0 - o.a;
+  for (int a = 0; a < 3; ++a) o.rgb[a] = o.rgb[a] + w * srgb[a];
+  o.a = o.a + w * sa;
+  return P.has_et && o.a >= P.et;
+}
+
+// finalize_image (core.py:137-155)
+__device__ void finalize(const RayOut& o, double px[4], Counters& cnt) {
+  const RenderParams& P = c_P;
+  if (!P.mip) {
+    px[0] = o.rgb[0];
+    px[1] = o.rgb[1];
+    px[2] = o.rgb[2];
+    px[3] = o.a;
+    return;
+  }
+  double rgb[3] = {0, 0, 0}, trans = 1.0;
+  for (int c = 0; c < P.g.C; ++c) {
+    double x = o.mip[c] / P.fmax;
+    double al = interp(c, 3, x);
+    cnt.tf++;
+    for (int a = 0; a < 3; ++a) rgb[a] = rgb[a] + interp(c, a, x) * al;
+    trans = trans * (1.0 - al);
+  }
+  for (int a = 0; a < 3; ++a) px[a] = npclip(rgb[a], 0.0, 1.0);
+  px[3] = 1.0 - trans;
+}
+
+__device__ void warp_add_counters(const Counters& c, unsigned long long* out) {
+  long long v[6] = {c.samples, c.tf, c.avgfb, c.coarse, c.req, c.used};
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    long long x = v[i];
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+    if ((threadIdx.x & 31) == 0 && x) atomicAdd(out + i, (unsigned long long)x);
+  }
+}
+
+__device__ __forceinline__ bool pixel_of(int& i, int& j) {
+  const RenderParams& P = c_P;
+  // warp = 8x4 pixel tile; block = 4 warps stacked vertically (8x16)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  i = blockIdx.x * 8 + (lane & 7);
+  j = (blockIdx.y * 4 + warp) * 4 + (lane >> 3);
+  i += P.rect[0];
+  j += P.rect[1];
+  return i < P.rect[2] && j < P.rect[3];
+}
+
+template <class T>
+__device__ void store_px(void* out, int kind, int64_t r, const double px[4]) {
+  if (kind == 0) {
+    double* o = (double*)out + r * 4;
+    for (int a = 0; a < 4; ++a) o[a] = px[a];
+  } else if (kind == 1) {
+    float* o = (float*)out + r * 4;
+    for (int a = 0; a < 4; ++a) o[a] = (float)px[a];
+  } else {
+    uint8_t* o = (uint8_t*)out + r * 4;
+    for (int a = 0; a < 4; ++a) o[a] = (uint8_t)npclip(rint(px[a] * 255.0), 0.0, 255.0);
+  }
+}
+
+// fused full-frame pass: ray setup + march + finalize, no per-ray state
+template <class T>
+__global__ void __launch_bounds__(128) k_render_fullframe(const uint64_t* __restrict__ nb,
+                                                          uint8_t* fb, const T* __restrict__ bb,
+                                                          void* out, int out_kind, int out_w,
+                                                          unsigned long long* counters) {
+  const RenderParams& P = c_P;
+  Counters cnt{0, 0, 0, 0, 0, 0};
+  int i, j;
+  bool active = pixel_of(i, j);
+  if (active) {
+    double d[3];
+    ray_dir(i, j, d);
+    double t0;
+    long long n;
+    ray_setup(d, t0, n);
+    RayOut o{};
+    Sampler<T> s(nb, fb, bb, true, cnt);
+    double vals[kMaxC];
+    for (long long k = 0; k < n; ++k) {
+      double t = t0 + (double)k * P.step;
+      double p[3];
+      for (int a = 0; a < 3; ++a) p[a] = P.cam[a] + t * d[a];
+      s.sample(p, vals);
+      cnt.samples++;
+      if (composite(vals, o, cnt)) break;
+    }
+    double px[4];
+    finalize(o, px, cnt);
+    store_px<T>(out, out_kind, (int64_t)(j - P.rect[1]) * out_w + (i - P.rect[0]), px);
+  }
+  warp_add_counters(cnt, counters);
+}
+
+// ---- stateful passes (RefinementSession, raycast.py:298-339) ---------------
+
+struct RayState {
+  double* t0;
+  long long* n;
+  long long* k;
+  uint8_t* flags;  // bit0 suspended, bit1 terminated
+  double* acc;     // [rays][4]: rgb, a
+  double* mip;     // [rays][4]
+};
+
+__global__ void k_rays_init(RayState S) {
+  const RenderParams& P = c_P;
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P.W * P.H) return;
+  int x = i % P.W, y = i / P.W;
+  double d[3];
+  ray_dir(x, y, d);
+  double t0;
+  long long n;
+  ray_setup(d, t0, n);
+  bool in_tile = x >= P.rect[0] && x < P.rect[2] && y >= P.rect[1] && y < P.rect[3];
+  S.t0[i] = t0;
+  S.n[i] = in_tile ? n : 0;
+  S.k[i] = 0;
+  S.flags[i] = 0;
+  for (int a = 0; a < 4; ++a) {
+    S.acc[i * 4 + a] = 0.0;
+    S.mip[i * 4 + a] = 0.0;
+  }
+}
+
+template <class T>
+__global__ void __launch_bounds__(128) k_rays_march(RayState S,
+                                                    const uint64_t* __restrict__ nb, uint8_t* fb,
+                                                    const T* __restrict__ bb, int fullframe,
+                                                    unsigned long long* counters,
+                                                    unsigned long long* n_susp) {
+  const RenderParams& P = c_P;
+  Counters cnt{0, 0, 0, 0, 0, 0};
+  int i, j;
+  // stateful passes cover the whole frame; rect = full
+  bool active = pixel_of(i, j);
+  bool susp = false;
+  if (active) {
+    const int64_t r = (int64_t)j * P.W + i;
+    uint8_t fl = S.flags[r] & ~1;  // suspended flags reset each pass
+    long long k = S.k[r];
+    const long long n = S.n[r];
+    if (!(fl & 2) && k < n) {
+      double d[3];
+      ray_dir(i, j, d);
+      RayOut o;
+      for (int a = 0; a < 3; ++a) o.rgb[a] = S.acc[r * 4 + a];
+      o.a = S.acc[r * 4 + 3];
+      for (int c = 0; c < kMaxC; ++c) o.mip[c] = S.mip[r * 4 + c];
+      Sampler<T> s(nb, fb, bb, fullframe != 0, cnt);
+      double vals[kMaxC];
+      const double t0 = S.t0[r];
+      for (; k < n; ++k) {
+        double t = t0 + (double)k * P.step;
+        double p[3];
+        for (int a = 0; a < 3; ++a) p[a] = P.cam[a] + t * d[a];
+        bool miss = s.sample(p, vals);
+        cnt.samples++;
+        if (miss) {
+          susp = true;
+          fl |= 1;
+          break;
+        }
+        bool term = composite(vals, o, cnt);
+        if (term) {
+          fl |= 2;
+          ++k;
+          break;
+        }
+      }
+      for (int a = 0; a < 3; ++a) S.acc[r * 4 + a] = o.rgb[a];
+      S.acc[r * 4 + 3] = o.a;
+      for (int c = 0; c < kMaxC; ++c) S.mip[r * 4 + c] = o.mip[c];
+      S.k[r] = k;
+    }
+    S.flags[r] = fl;
+  }
+  warp_add_counters(cnt, counters);
+  unsigned b = __ballot_sync(0xffffffffu, susp);
+  if ((threadIdx.x & 31) == 0 && b) atomicAdd(n_susp, (unsigned long long)__popc(b));
+}
+
+__global__ void k_rays_image(RayState S, double* out,
+                             unsigned long long* counters) {
+  const RenderParams& P = c_P;
+  Counters cnt{0, 0, 0, 0, 0, 0};
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < P.W * P.H) {
+    RayOut o;
+    for (int a = 0; a < 3; ++a) o.rgb[a] = S.acc[i * 4 + a];
+    o.a = S.acc[i * 4 + 3];
+    for (int c = 0; c < kMaxC; ++c) o.mip[c] = S.mip[i * 4 + c];
+    double px[4];
+    finalize(o, px, cnt);
+    for (int a = 0; a < 4; ++a) out[(int64_t)i * 4 + a] = px[a];
+  }
+  warp_add_counters(cnt, counters);
+}
+
+// ---- mirror kernels ------------------------------------------------------------
+
+// _entry_for / pack_node (device.py:51-87, 168-178)
+__global__ void k_repack(Geo g, const uint8_t* __restrict__ flags,
+                         const int32_t* __restrict__ pslot, const int32_t* __restrict__ stats,
+                         const int32_t* __restrict__ res, int zero_copy, double fmax, int w,
+                         uint64_t* nb) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= g.capacity) return;
+  uint8_t f = flags[i];
+  if (!(f & NF_EXISTS)) {
+    nb[i] = 0;
+    return;
+  }
+  uint64_t e = (f & NF_BRICK) ? 2ULL : 0ULL;
+  if (f & NF_CHILDREN) e |= (uint64_t)(i + 1) << 2;
+  int32_t s = zero_copy ? ((f & NF_BRICK) ? pslot[i] : -1) : res[i];
+  if (s >= 0) {
+    e |= 1ULL | ((uint64_t)(uint32_t)s << 24);
+  } else {
+    double qmax = (double)((1LL << w) - 1);
+    for (int c = 0; c < g.C; ++c) {
+      double v = (double)stats[st_index(i, ST_AVG, c)];
+      uint64_t q = (uint64_t)rint(v * qmax / fmax);
+      e |= q << (24 + c * w);
+    }
+  }
+  nb[i] = e;
+}
+
+__global__ void k_set_res(const int64_t* __restrict__ nodes, const int32_t* __restrict__ slots,
+                          int n, int32_t* res) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) res[nodes[i]] = slots[i];
+}
+
+__global__ void k_upload(const int32_t* __restrict__ src_slots, const int32_t* __restrict__ dst_slots,
+                         int n, const uint8_t* __restrict__ pool, uint8_t* bb, int64_t bytes) {
+  int b = blockIdx.y;
+  if (b >= n || dst_slots[b] < 0) return;
+  const uint32_t* s = reinterpret_cast<const uint32_t*>(pool + (int64_t)src_slots[b] * bytes);
+  uint32_t* d = reinterpret_cast<uint32_t*>(bb + (int64_t)dst_slots[b] * bytes);
+  if ((bytes & 3) == 0) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < bytes / 4;
+         e += (int64_t)gridDim.x * blockDim.x)
+      d[e] = s[e];
+  } else {
+    const uint8_t* s1 = pool + (int64_t)src_slots[b] * bytes;
+    uint8_t* d1 = bb + (int64_t)dst_slots[b] * bytes;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < bytes;
+         e += (int64_t)gridDim.x * blockDim.x)
+      d1[e] = s1[e];
+  }
+}
+
+// c_P is one symbol per device: render entry points hold this lock from
+// the parameter upload until their kernels have completed
+std::mutex g_render_mu;
+
+void set_params(const RenderParams& P, cudaStream_t st) {
+  VT_CUDA(cudaMemcpyToSymbolAsync(c_P, &P, sizeof(RenderParams), 0, cudaMemcpyHostToDevice, st));
+}
+
+void fill_params(const vt_mirror* m, const vt_scene* s, RenderParams& P) {
+  const Tree& t = m->tree->t;
+  std::memset(&P, 0, sizeof(P));
+  P.g = t.g;
+  for (int a = 0; a < 3; ++a) {
+    P.dims[a] = (double)t.g.dims[a];
+    P.spacing[a] = s->spacing[a];
+    P.box_hi[a] = P.dims[a] * P.spacing[a];
+  }
+  for (int l = 0; l <= t.g.depth; ++l)
+    for (int a = 0; a < 3; ++a) {
+      P.ext[l][a] = (double)t.g.extent(a, l);
+      P.scl[l][a] = (double)t.g.scale(a, l);
+    }
+  bool any_split = t.g.split[0] || t.g.split[1] || t.g.split[2];
+  double bv = INFINITY;
+  for (int a = 0; a < 3; ++a)
+    if (!any_split || t.g.split[a]) bv = std::min(bv, s->spacing[a]);
+  P.base_voxel = bv;
+  P.fmax = (double)t.fmax;
+  P.avg_w = 40 / t.g.C;
+  P.qmax = (double)((1LL << P.avg_w) - 1);
+  P.borders_filled = t.borders ? 1 : 0;
+  P.zero_copy = m->zero_copy;
+  // camera basis from the host shim (numpy-identical, camera.py:33-57)
+  for (int a = 0; a < 3; ++a) {
+    P.cam[a] = s->position[a];
+    P.fwd[a] = s->fwd[a];
+    P.right[a] = s->right[a];
+    P.up[a] = s->up[a];
+  }
+  P.aspect = s->aspect;
+  P.pfs = s->footprint_scale;
+  P.W = s->width;
+  P.H = s->height;
+  P.tan_half = s->tan_half;
+  P.mip = s->mode_mip;
+  P.step = s->step;
+  P.corr = s->corr_exp;
+  P.et = s->et_limit;
+  P.has_et = (s->et_limit >= 0.0 && s->et_limit < 1.0) ? 1 : 0;
+  P.lod_scale = s->lod_scale;
+  for (int c = 0; c < t.g.C; ++c) {
+    P.tf_n[c] = s->tf_count[c];
+    VT_REQUIRE(P.tf_n[c] >= 2 && P.tf_n[c] <= VT_MAX_TF_POINTS, VT_EINVAL,
+               "transfer function needs 2..16 control points");
+    for (int q = 0; q < P.tf_n[c]; ++q) {
+      P.tf_x[c][q] = s->tf_x[c][q];
+      for (int a = 0; a < 4; ++a) P.tf_v[c][q][a] = s->tf_rgba[c][q][a];
+    }
+  }
+  P.n_clips = s->n_clips;
+  VT_REQUIRE(P.n_clips >= 0 && P.n_clips <= 3, VT_EINVAL, "at most 3 clip planes supported");
+  for (int q = 0; q < P.n_clips; ++q) {
+    for (int a = 0; a < 3; ++a) P.clip_n[q][a] = s->clip_normal[q][a];
+    P.clip_o[q] = s->clip_offset[q];
+  }
+  P.has_tr = s->has_transforms;
+  for (int c = 0; c < kMaxC; ++c)
+    for (int q = 0; q < 12; ++q) P.tr[c][q] = s->transforms[c][q];
+  P.rect[0] = 0;
+  P.rect[1] = 0;
+  P.rect[2] = P.W;
+  P.rect[3] = P.H;
+}
+
+}  // namespace
+
+struct vt_rays {
+  vt_mirror* m;
+  RenderParams P;
+  RayState S{};
+  int64_t n = 0;
+};
+
+extern "C" {
+
+vt_status vt_mirror_create(vt_tree* tree, int64_t slot_count, vt_mirror** out) {
+  return guarded([&] {
+    Tree& t = tree->t;
+    t.flush();
+    auto* m = new vt_mirror();
+    m->tree = tree;
+    const int64_t cap = t.g.capacity;
+    const int64_t cap4 = (cap + 3) & ~3LL;
+    try {
+      VT_CUDA(cudaMalloc(&m->d_nb, cap * sizeof(uint64_t)));
+      VT_CUDA(cudaMalloc(&m->d_fb, cap4));
+      VT_CUDA(cudaMemsetAsync(m->d_fb, 0, cap4, t.stream));
+      if (slot_count < 0) {
+        m->zero_copy = true;
+        m->slots = t.pool_slots;
+      } else {
+        m->slots = std::max<int64_t>(1, slot_count);
+        VT_CUDA(cudaMalloc(&m->d_bb, m->slots * t.g.brick_elems * t.g.sb));
+        VT_CUDA(cudaMemsetAsync(m->d_bb, 0, m->slots * t.g.brick_elems * t.g.sb, t.stream));
+        VT_CUDA(cudaMalloc(&m->d_res, cap * sizeof(int32_t)));
+        VT_CUDA(cudaMemsetAsync(m->d_res, 0xFF, cap * sizeof(int32_t), t.stream));
+      }
+    } catch (...) {
+      cudaFree(m->d_nb);
+      cudaFree(m->d_fb);
+      cudaFree(m->d_bb);
+      cudaFree(m->d_res);
+      delete m;
+      throw;
+    }
+    *out = m;
+  });
+}
+
+vt_status vt_mirror_destroy(vt_mirror* m) {
+  return guarded([&] {
+    if (!m) return;
+    cudaStreamSynchronize(m->tree->t.stream);
+    cudaFree(m->d_nb);
+    cudaFree(m->d_fb);
+    cudaFree(m->d_bb);
+    cudaFree(m->d_res);
+    delete m;
+  });
+}
+
+vt_status vt_mirror_buffers(vt_mirror* m, void** nbp, void** fbp, void** bbp, int64_t* cap,
+                            int64_t* slots) {
+  return guarded([&] {
+    Tree& t = m->tree->t;
+    if (nbp) *nbp = m->d_nb;
+    if (fbp) *fbp = m->d_fb;
+    if (bbp) *bbp = m->zero_copy ? t.d_pool : m->d_bb;
+    if (cap) *cap = t.g.capacity;
+    if (slots) *slots = m->zero_copy ? t.pool_slots : m->slots;
+  });
+}
+
+vt_status vt_mirror_set_resident(vt_mirror* m, int64_t n, const int64_t* nodes,
+                                 const int32_t* slots, int32_t copy) {
+  return guarded([&] {
+    Tree& t = m->tree->t;
+    VT_REQUIRE(!m->zero_copy, VT_ESTATE, "zero-copy mirror: every brick is resident");
+    if (n <= 0) return;
+    t.flush();
+    std::vector<int64_t> nv(nodes, nodes + n);
+    std::vector<int32_t> sv(slots, slots + n);
+    std::vector<int32_t> src(n, 0);
+    for (int64_t i = 0; i < n; ++i) {
+      VT_REQUIRE(sv[i] < m->slots, VT_EINVAL, "brick-buffer slot out of range");
+      if (sv[i] >= 0) {
+        VT_REQUIRE(t.flags[nv[i]] & NF_BRICK, VT_EINVAL, "upload of a node without a brick");
+        src[i] = t.slot[nv[i]];
+      }
+    }
+    int64_t* dn = upload(t, nv);
+    int32_t* ds = upload(t, sv);
+    k_set_res<<<(unsigned)((n + 255) / 256), 256, 0, t.stream>>>(dn, ds, (int)n, m->d_res);
+    VT_CUDA(cudaGetLastError());
+    if (copy) {
+      int32_t* dsrc = upload(t, src);
+      const int64_t bytes = t.g.brick_elems * t.g.sb;
+      for (int64_t o = 0; o < n; o += 65535) {
+        int cnt = (int)std::min<int64_t>(65535, n - o);
+        dim3 grid(16, cnt);
+        k_upload<<<grid, 256, 0, t.stream>>>(dsrc + o, ds + o, cnt, t.d_pool, m->d_bb, bytes);
+        VT_CUDA(cudaGetLastError());
+      }
+      release(t, dsrc);
+    }
+    release(t, dn);
+    release(t, ds);
+  });
+}
+
+vt_status vt_mirror_repack(vt_mirror* m) {
+  return guarded([&] {
+    Tree& t = m->tree->t;
+    t.flush();
+    const int64_t cap = t.g.capacity;
+    k_repack<<<(unsigned)((cap + 255) / 256), 256, 0, t.stream>>>(
+        t.g, t.d_flags, t.d_slot, t.d_stats, m->d_res, m->zero_copy ? 1 : 0, (double)t.fmax,
+        40 / t.g.C, m->d_nb);
+    VT_CUDA(cudaGetLastError());
+  });
+}
+
+vt_status vt_mirror_read_flags(vt_mirror* m, uint8_t* out, int32_t clear) {
+  return guarded([&] {
+    Tree& t = m->tree->t;
+    const int64_t cap = t.g.capacity;
+    VT_CUDA(cudaMemcpyAsync(out, m->d_fb, cap, cudaMemcpyDeviceToHost, t.stream));
+    if (clear) VT_CUDA(cudaMemsetAsync(m->d_fb, 0, (cap + 3) & ~3LL, t.stream));
+    VT_CUDA(cudaStreamSynchronize(t.stream));
+  });
+}
+
+static const void* brick_ptr(vt_mirror* m) {
+  Tree& t = m->tree->t;
+  return m->zero_copy ? (const void*)t.d_pool : (const void*)m->d_bb;
+}
+
+static void add_counters(vt_counters* cnt, const unsigned long long* h) {
+  if (!cnt) return;
+  cnt->samples += (int64_t)h[0];
+  cnt->tf_lookups += (int64_t)h[1];
+  cnt->avg_fallbacks += (int64_t)h[2];
+  cnt->coarse_fallbacks += (int64_t)h[3];
+  cnt->bricks_requested += (int64_t)h[4];
+  cnt->bricks_used_marks += (int64_t)h[5];
+}
+
+static void render_rect(vt_mirror* m, const vt_scene* scene, const int32_t* rect, void* out,
+                        int32_t out_kind, int32_t out_on_device, vt_counters* cnt) {
+  std::lock_guard<std::mutex> lk(g_render_mu);
+  Tree& t = m->tree->t;
+  t.flush();
+  RenderParams P;
+  fill_params(m, scene, P);
+  if (rect) {
+    VT_REQUIRE(rect[0] >= 0 && rect[1] >= 0 && rect[2] <= P.W && rect[3] <= P.H &&
+                   rect[0] <= rect[2] && rect[1] <= rect[3],
+               VT_EINVAL, "tile rectangle outside the viewport");
+    for (int a = 0; a < 4; ++a) P.rect[a] = rect[a];
+  }
+  const int rw = P.rect[2] - P.rect[0], rh = P.rect[3] - P.rect[1];
+  const int64_t px = (int64_t)rw * rh;
+  const int esz = out_kind == 0 ? 8 : (out_kind == 1 ? 4 : 1);
+  void* dout = out;
+  if (!out_on_device) VT_CUDA(cudaMallocAsync(&dout, std::max<int64_t>(1, px) * 4 * esz, t.stream));
+  unsigned long long* dc = nullptr;
+  VT_CUDA(cudaMallocAsync(&dc, 6 * sizeof(unsigned long long), t.stream));
+  VT_CUDA(cudaMemsetAsync(dc, 0, 6 * sizeof(unsigned long long), t.stream));
+  dim3 grid((rw + 7) / 8, (rh + 15) / 16);
+  VT_CUDA(cudaEventRecord(t.ev0, t.stream));
+  set_params(P, t.stream);
+  if (px > 0) {
+    if (t.g.sb == 1)
+      k_render_fullframe<uint8_t><<<grid, 128, 0, t.stream>>>(
+          m->d_nb, m->d_fb, (const uint8_t*)brick_ptr(m), dout, out_kind, rw, dc);
+    else
+      k_render_fullframe<uint16_t><<<grid, 128, 0, t.stream>>>(
+          m->d_nb, m->d_fb, (const uint16_t*)brick_ptr(m), dout, out_kind, rw, dc);
+    VT_CUDA(cudaGetLastError());
+  }
+  VT_CUDA(cudaEventRecord(t.ev1, t.stream));
+  unsigned long long h[6];
+  VT_CUDA(cudaMemcpyAsync(h, dc, sizeof(h), cudaMemcpyDeviceToHost, t.stream));
+  if (!out_on_device) {
+    VT_CUDA(cudaMemcpyAsync(out, dout, px * 4 * esz, cudaMemcpyDeviceToHost, t.stream));
+    release(t, dout);
+  }
+  release(t, dc);
+  VT_CUDA(cudaStreamSynchronize(t.stream));
+  float ms = 0;
+  if (cudaEventElapsedTime(&ms, t.ev0, t.ev1) == cudaSuccess) t.last_render_ms = ms;
+  add_counters(cnt, h);
+}
+
+vt_status vt_render_fullframe(vt_mirror* m, const vt_scene* scene, void* out, int32_t out_kind,
+                              int32_t out_on_device, vt_counters* cnt) {
+  return guarded([&] { render_rect(m, scene, nullptr, out, out_kind, out_on_device, cnt); });
+}
+
+vt_status vt_render_tile(vt_mirror* m, const vt_scene* scene, const int32_t rect[4], void* out,
+                         int32_t out_kind, int32_t out_on_device, vt_counters* cnt) {
+  return guarded([&] { render_rect(m, scene, rect, out, out_kind, out_on_device, cnt); });
+}
+
+vt_status vt_rays_create(vt_mirror* m, const vt_scene* scene, const int32_t* tile, vt_rays** out) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(g_render_mu);
+    Tree& t = m->tree->t;
+    auto* r = new vt_rays();
+    r->m = m;
+    fill_params(m, scene, r->P);
+    if (tile)
+      for (int a = 0; a < 4; ++a) r->P.rect[a] = tile[a];
+    r->n = (int64_t)r->P.W * r->P.H;
+    const int64_t n = std::max<int64_t>(1, r->n);
+    VT_CUDA(cudaMalloc(&r->S.t0, n * 8));
+    VT_CUDA(cudaMalloc(&r->S.n, n * 8));
+    VT_CUDA(cudaMalloc(&r->S.k, n * 8));
+    VT_CUDA(cudaMalloc(&r->S.flags, n));
+    VT_CUDA(cudaMalloc(&r->S.acc, n * 32));
+    VT_CUDA(cudaMalloc(&r->S.mip, n * 32));
+    set_params(r->P, t.stream);
+    k_rays_init<<<(unsigned)((n + 127) / 128), 128, 0, t.stream>>>(r->S);
+    VT_CUDA(cudaGetLastError());
+    VT_CUDA(cudaStreamSynchronize(t.stream));
+    *out = r;
+  });
+}
+
+vt_status vt_rays_destroy(vt_rays* r) {
+  return guarded([&] {
+    if (!r) return;
+    cudaStreamSynchronize(r->m->tree->t.stream);
+    cudaFree(r->S.t0);
+    cudaFree(r->S.n);
+    cudaFree(r->S.k);
+    cudaFree(r->S.flags);
+    cudaFree(r->S.acc);
+    cudaFree(r->S.mip);
+    delete r;
+  });
+}
+
+vt_status vt_rays_march(vt_rays* r, int32_t strategy, vt_counters* cnt, int64_t* suspended) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(g_render_mu);
+    vt_mirror* m = r->m;
+    Tree& t = m->tree->t;
+    t.flush();
+    RenderParams P = r->P;
+    P.borders_filled = t.borders ? 1 : 0;
+    P.rect[0] = 0;
+    P.rect[1] = 0;
+    P.rect[2] = P.W;
+    P.rect[3] = P.H;
+    unsigned long long* dc = nullptr;
+    VT_CUDA(cudaMallocAsync(&dc, 7 * sizeof(unsigned long long), t.stream));
+    VT_CUDA(cudaMemsetAsync(dc, 0, 7 * sizeof(unsigned long long), t.stream));
+    dim3 grid((P.W + 7) / 8, (P.H + 15) / 16);
+    set_params(P, t.stream);
+    if (t.g.sb == 1)
+      k_rays_march<uint8_t><<<grid, 128, 0, t.stream>>>(r->S, m->d_nb, m->d_fb,
+                                                        (const uint8_t*)brick_ptr(m),
+                                                        strategy == 0, dc, dc + 6);
+    else
+      k_rays_march<uint16_t><<<grid, 128, 0, t.stream>>>(r->S, m->d_nb, m->d_fb,
+                                                         (const uint16_t*)brick_ptr(m),
+                                                         strategy == 0, dc, dc + 6);
+    VT_CUDA(cudaGetLastError());
+    unsigned long long h[7];
+    VT_CUDA(cudaMemcpyAsync(h, dc, sizeof(h), cudaMemcpyDeviceToHost, t.stream));
+    release(t, dc);
+    VT_CUDA(cudaStreamSynchronize(t.stream));
+    add_counters(cnt, h);
+    if (suspended) *suspended = (int64_t)h[6];
+  });
+}
+
+vt_status vt_rays_image(vt_rays* r, double* out_host, vt_counters* cnt) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(g_render_mu);
+    Tree& t = r->m->tree->t;
+    double* dout = nullptr;
+    const int64_t n = std::max<int64_t>(1, r->n);
+    VT_CUDA(cudaMallocAsync(&dout, n * 32, t.stream));
+    unsigned long long* dc = nullptr;
+    VT_CUDA(cudaMallocAsync(&dc, 6 * sizeof(unsigned long long), t.stream));
+    VT_CUDA(cudaMemsetAsync(dc, 0, 6 * sizeof(unsigned long long), t.stream));
+    set_params(r->P, t.stream);
+    k_rays_image<<<(unsigned)((n + 127) / 128), 128, 0, t.stream>>>(r->S, dout, dc);
+    VT_CUDA(cudaGetLastError());
+    unsigned long long h[6];
+    VT_CUDA(cudaMemcpyAsync(out_host, dout, r->n * 32, cudaMemcpyDeviceToHost, t.stream));
+    VT_CUDA(cudaMemcpyAsync(h, dc, sizeof(h), cudaMemcpyDeviceToHost, t.stream));
+    release(t, dout);
+    release(t, dc);
+    VT_CUDA(cudaStreamSynchronize(t.stream));
+    add_counters(cnt, h);
+  });
+}
+
+vt_status vt_rays_state(vt_rays* r, int64_t* k, int64_t* n_steps, uint8_t* suspended) {
+  return guarded([&] {
+    Tree& t = r->m->tree->t;
+    std::vector<uint8_t> fl(r->n);
+    if (k) VT_CUDA(cudaMemcpyAsync(k, r->S.k, r->n * 8, cudaMemcpyDeviceToHost, t.stream));
+    if (n_steps)
+      VT_CUDA(cudaMemcpyAsync(n_steps, r->S.n, r->n * 8, cudaMemcpyDeviceToHost, t.stream));
+    VT_CUDA(cudaMemcpyAsync(fl.data(), r->S.flags, r->n, cudaMemcpyDeviceToHost, t.stream));
+    VT_CUDA(cudaStreamSynchronize(t.stream));
+    if (suspended)
+      for (int64_t i = 0; i < r->n; ++i) suspended[i] = fl[i] & 1;
+  });
+}
+
+}  // extern "C"

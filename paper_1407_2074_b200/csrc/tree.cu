@@ -1,0 +1,625 @@
+// Host control plane of the incremental octree (octree.py:143-614) over the
+// device pool.  The host owns the tree STRUCTURE (which nodes exist, which
+// own bricks, pool slots, change events, prune decisions); all sample data
+// and node statistics live in HBM and are computed by build_kernels.cu.
+//
+// One insertion = (a) a host walk that creates nodes / bricks and records
+// dirty boxes, (b) stream-ordered kernels: structure mirror, child seeding,
+// brick seeding, block scatter, then (c) per-level propagation:
+// plane stats -> reduce (leaves), octant half-sample -> plane stats ->
+// reduce (levels 1..N).  With tau == 0 (nothing is ever pruned, every seed is
+// the background, every brick a pure function of the data) (c) is deferred
+// and batched across insertions until something reads the tree.  With
+// tau > 0 it runs per insertion, followed by a stats gather and the exact
+// reference prune (octree.py:456-493).
+#include <algorithm>
+#include <cstring>
+#include <map>
+
+#include "tree.cuh"
+
+namespace vtx {
+
+static thread_local std::string g_last_error;
+void set_last_error(const std::string& m) { g_last_error = m; }
+const char* last_error() { return g_last_error.c_str(); }
+
+// ---------------------------------------------------------------------------
+// construction
+// ---------------------------------------------------------------------------
+
+static void build_geo(const vt_tree_desc& d, Geo& g) {
+  int ns[3];
+  int depth = 0;
+  for (int a = 0; a < 3; ++a) {
+    VT_REQUIRE(d.dims[a] > 0 && d.brick[a] > 0, VT_EINVAL, "dims and brick_dims must be positive");
+    int n = 0;
+    int64_t ext = d.brick[a];
+    while (ext < d.dims[a]) {
+      ext *= 2;
+      ++n;
+    }
+    ns[a] = n;
+    depth = std::max(depth, n);
+  }
+  VT_REQUIRE(depth <= kMaxDepth, VT_EINVAL,
+             "tree needs " + std::to_string(depth + 1) +
+                 " levels; child pointers address at most 9 (volume too large for this brick "
+                 "resolution)");
+  for (int a = 0; a < 3; ++a) {
+    g.dims[a] = d.dims[a];
+    g.brick[a] = d.brick[a];
+    g.stored[a] = d.brick[a] + 2;
+    g.virt[a] = ns[a] == 0 ? d.brick[a] : d.brick[a] << depth;
+    g.split[a] = g.virt[a] > d.brick[a];
+  }
+  g.depth = depth;
+  g.C = d.channels;
+  g.sb = d.sample_bytes;
+  g.bg = d.background;
+  int64_t s = 0, w = 1;
+  for (int i = 0; i < kMaxDepth + 2; ++i) {
+    g.level_start[i] = s;
+    s += w;
+    w *= 8;
+  }
+  g.capacity = g.level_start[depth + 1];
+  g.brick_elems = (int64_t)g.stored[0] * g.stored[1] * g.stored[2] * g.C;
+}
+
+Tree::Tree(const vt_tree_desc& d) {
+  VT_REQUIRE(d.channels >= 1 && d.channels <= kMaxC, VT_EINVAL, "channels must be in [1, 4]");
+  VT_REQUIRE(d.sample_bytes == 1 || d.sample_bytes == 2, VT_EINVAL, "unsupported sample format");
+  for (int a = 0; a < 3; ++a)
+    VT_REQUIRE(d.brick[a] >= 1 && (d.brick[a] == 1 || d.brick[a] % 2 == 0), VT_EINVAL,
+               "brick dims must be even (or 1)");
+  build_geo(d, g);
+  tau = d.threshold;
+  fmax = d.sample_bytes == 1 ? 255 : 65535;
+  VT_REQUIRE(d.background >= 0 && d.background <= fmax, VT_EINVAL,
+             "background_value outside the sample format range");
+  device = d.device;
+  VT_CUDA(cudaSetDevice(device));
+  VT_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  own_stream = true;
+  {
+    cudaMemPool_t pool;
+    VT_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thr = UINT64_MAX;
+    VT_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  }
+  const int64_t cap = g.capacity;
+  flags.assign(cap, 0);
+  slot.assign(cap, -1);
+  struct_mark.assign(cap, 0);
+  h_stats.assign(cap * ST_N * kMaxC, 0);
+  flags[0] = NF_EXISTS | NF_INVOL;
+  for (int c = 0; c < g.C; ++c)
+    for (int s2 = 0; s2 < ST_N; ++s2) h_stats[st_index(0, s2, c)] = g.bg;
+  VT_CUDA(cudaMalloc(&d_flags, cap));
+  VT_CUDA(cudaMalloc(&d_slot, cap * sizeof(int32_t)));
+  VT_CUDA(cudaMalloc(&d_stats, cap * ST_N * kMaxC * sizeof(int32_t)));
+  VT_CUDA(cudaMemset(d_flags, 0, cap));
+  VT_CUDA(cudaMemset(d_slot, 0xFF, cap * sizeof(int32_t)));
+  VT_CUDA(cudaMemcpy(d_flags, flags.data(), 1, cudaMemcpyHostToDevice));
+  VT_CUDA(cudaMemcpy(d_stats, h_stats.data(), ST_N * kMaxC * sizeof(int32_t),
+                     cudaMemcpyHostToDevice));
+  pending.assign(g.depth + 1, {});
+  VT_CUDA(cudaEventCreate(&ev0));
+  VT_CUDA(cudaEventCreate(&ev1));
+  int64_t reserve = d.reserve_slots > 0 ? d.reserve_slots : 64;
+  ensure_pool(reserve);
+}
+
+Tree::~Tree() {
+  if (stream) cudaStreamSynchronize(stream);
+  cudaFree(d_pool);
+  cudaFree(d_flags);
+  cudaFree(d_slot);
+  cudaFree(d_stats);
+  cudaFree(d_pmin);
+  cudaFree(d_pmax);
+  cudaFree(d_psum);
+  if (ev0) cudaEventDestroy(ev0);
+  if (ev1) cudaEventDestroy(ev1);
+  if (own_stream && stream) cudaStreamDestroy(stream);
+}
+
+void Tree::ensure_pool(int64_t need) {
+  if (need <= pool_slots) return;
+  int64_t n = std::max<int64_t>(need, pool_slots * 2);
+  const int64_t bb = g.brick_elems * g.sb;
+  const int64_t pe = (int64_t)g.brick[2] * g.C;
+  uint8_t* np = nullptr;
+  int32_t *nmin = nullptr, *nmax = nullptr;
+  unsigned long long* nsum = nullptr;
+  VT_CUDA(cudaMalloc(&np, n * bb));
+  VT_CUDA(cudaMalloc(&nmin, n * pe * sizeof(int32_t)));
+  VT_CUDA(cudaMalloc(&nmax, n * pe * sizeof(int32_t)));
+  VT_CUDA(cudaMalloc(&nsum, n * pe * sizeof(unsigned long long)));
+  if (pool_slots) {
+    VT_CUDA(cudaMemcpyAsync(np, d_pool, pool_slots * bb, cudaMemcpyDeviceToDevice, stream));
+    VT_CUDA(cudaMemcpyAsync(nmin, d_pmin, pool_slots * pe * 4, cudaMemcpyDeviceToDevice, stream));
+    VT_CUDA(cudaMemcpyAsync(nmax, d_pmax, pool_slots * pe * 4, cudaMemcpyDeviceToDevice, stream));
+    VT_CUDA(cudaMemcpyAsync(nsum, d_psum, pool_slots * pe * 8, cudaMemcpyDeviceToDevice, stream));
+    VT_CUDA(cudaStreamSynchronize(stream));
+    cudaFree(d_pool);
+    cudaFree(d_pmin);
+    cudaFree(d_pmax);
+    cudaFree(d_psum);
+  }
+  d_pool = np;
+  d_pmin = nmin;
+  d_pmax = nmax;
+  d_psum = nsum;
+  pool_slots = n;
+}
+
+// ---------------------------------------------------------------------------
+// structure helpers
+// ---------------------------------------------------------------------------
+
+bool Tree::in_volume(int64_t idx) const {
+  int lo[3];
+  g.box_lo(idx, lo);
+  int level = g.level_of(idx);
+  for (int a = 0; a < 3; ++a)
+    if (!(lo[a] < g.dims[a] && lo[a] + g.extent(a, level) > 0)) return false;
+  return true;
+}
+
+void Tree::node_in_extent(int64_t idx, int c[3]) const {
+  int lo[3];
+  g.box_lo(idx, lo);
+  g.in_extent(lo, g.level_of(idx), c);
+}
+
+void Tree::mark_struct(int64_t idx) {
+  if (!struct_mark[idx]) {
+    struct_mark[idx] = 1;
+    struct_dirty.push_back(idx);
+  }
+}
+
+int32_t Tree::alloc_slot() {
+  // BrickStore.allocate: recycle the lowest freed slot, else open a new one
+  // (paging.py:213-228)
+  int32_t s;
+  if (!free_slots.empty()) {
+    s = free_slots.top();
+    free_slots.pop();
+  } else {
+    VT_REQUIRE(cursor < INT32_MAX, VT_EOVERFLOW, "brick pool exhausted");
+    s = (int32_t)cursor++;
+    ensure_pool(cursor);
+  }
+  return s;
+}
+
+void Tree::ensure_children(int64_t p) {
+  if (flags[p] & NF_CHILDREN) return;
+  flags[p] |= NF_CHILDREN;
+  mark_struct(p);
+  auto it = created_seed.find(p);
+  int64_t src = it == created_seed.end() ? p : it->second;
+  creates.push_back({p, src});
+  for (int k = 0; k < 8; ++k) {
+    if (!g.octant_real(k)) continue;
+    int64_t c = 8 * p + 1 + k;
+    bool inv = in_volume(c);
+    flags[c] = NF_EXISTS | (inv ? NF_INVOL : 0);
+    slot[c] = -1;
+    mark_struct(c);
+    created_seed[c] = src;
+    ++node_count;
+    events.emplace_back(VT_EV_CREATED, c);
+  }
+}
+
+bool Tree::ensure_brick(int64_t n) {
+  if (flags[n] & NF_BRICK) return false;
+  int32_t s = alloc_slot();
+  flags[n] |= NF_BRICK;
+  slot[n] = s;
+  mark_struct(n);
+  SeedJob j{};
+  j.node = n;
+  j.slot = s;
+  node_in_extent(n, j.cext);
+  seeds.push_back(j);
+  ++brick_count;
+  return true;
+}
+
+void Tree::free_brick(int64_t n) {
+  if (!(flags[n] & NF_BRICK)) return;
+  free_slots.push(slot[n]);
+  flags[n] &= ~NF_BRICK;
+  slot[n] = -1;
+  mark_struct(n);
+  --brick_count;
+  ++pruned;
+}
+
+void Tree::flush_structure() {
+  if (struct_dirty.empty()) return;
+  std::vector<StructUpd> upd;
+  upd.reserve(struct_dirty.size());
+  for (int64_t i : struct_dirty) {
+    upd.push_back({i, flags[i], slot[i]});
+    struct_mark[i] = 0;
+  }
+  struct_dirty.clear();
+  StructUpd* d = upload(*this, upd);
+  launch_struct_update(*this, d, (int)upd.size());
+  release(*this, d);
+}
+
+// ---------------------------------------------------------------------------
+// insertion (octree.py:323-397)
+// ---------------------------------------------------------------------------
+
+static inline void box_union(Pending& p, const Box& b) {
+  if (!p.has_box) {
+    p.box = b;
+    p.has_box = true;
+    return;
+  }
+  for (int a = 0; a < 3; ++a) {
+    p.box.lo[a] = std::min(p.box.lo[a], b.lo[a]);
+    p.box.hi[a] = std::max(p.box.hi[a], b.hi[a]);
+  }
+}
+
+void Tree::insert(int channel, const int origin[3], const int dims[3], const void* samples,
+                  int mem_kind) {
+  // validation exactly as octree.py:331-341 (channel -1 = all channels interleaved)
+  VT_REQUIRE(channel == -1 || (channel >= 0 && channel < g.C), VT_EINVAL,
+             "channel " + std::to_string(channel) + " out of range");
+  for (int a = 0; a < 3; ++a) {
+    VT_REQUIRE(dims[a] >= 0, VT_EINVAL, "block dims must be non-negative");
+    VT_REQUIRE(origin[a] >= 0 && (int64_t)origin[a] + dims[a] <= g.dims[a], VT_EINVAL,
+               "block [" + std::to_string(origin[0]) + "," + std::to_string(origin[1]) + "," +
+                   std::to_string(origin[2]) + "] outside volume");
+  }
+  const int64_t nvox = (int64_t)dims[0] * dims[1] * dims[2];
+  VT_CUDA(cudaSetDevice(device));
+  const int nch = channel < 0 ? g.C : 1;
+  if (nvox == 0) {
+    // an empty block touches nothing: the reference still emits no events
+    return;
+  }
+  const int64_t bytes = nvox * nch * g.sb;
+  // stage the block on the device (stream ordered)
+  const void* dsrc = samples;
+  void* staged = nullptr;
+  if (mem_kind == VT_MEM_HOST) {
+    VT_CUDA(cudaMallocAsync(&staged, bytes, stream));
+    VT_CUDA(cudaMemcpyAsync(staged, samples, bytes, cudaMemcpyHostToDevice, stream));
+    dsrc = staged;
+  }
+  if (channel >= 0) {
+    insert_staged(channel, origin, dims, dsrc, 1, 0, 1);
+  } else if (tau > 0) {
+    // exact sequential semantics: C successive single-channel insertions
+    for (int c = 0; c < g.C; ++c) insert_staged(c, origin, dims, dsrc, g.C, c, 1);
+  } else {
+    // tau == 0: one fused pass; events as for C successive insertions
+    insert_staged(-1, origin, dims, dsrc, g.C, 0, g.C);
+  }
+  if (staged) release(*this, staged);
+  if (mem_kind == VT_MEM_HOST) {
+    // a pinned source is read asynchronously: keep the borrow contract
+    cudaPointerAttributes attr{};
+    if (cudaPointerGetAttributes(&attr, samples) == cudaSuccess &&
+        attr.type == cudaMemoryTypeHost)
+      VT_CUDA(cudaStreamSynchronize(stream));
+    else
+      cudaGetLastError();
+  }
+}
+
+void Tree::insert_staged(int channel, const int origin[3], const int dims[3], const void* dsrc,
+                         int src_stride, int src_off, int reps) {
+  const int64_t nvox = (int64_t)dims[0] * dims[1] * dims[2];
+  creates.clear();
+  seeds.clear();
+  created_seed.clear();
+  const int* M = g.brick;
+  int g0[3], g1[3], gn[3];
+  for (int a = 0; a < 3; ++a) {
+    g0[a] = origin[a] / M[a];
+    g1[a] = (origin[a] + dims[a] - 1) / M[a];
+    gn[a] = g1[a] - g0[a] + 1;
+  }
+  std::vector<int32_t> leaf_slots((size_t)gn[0] * gn[1] * gn[2]);
+  std::vector<std::vector<int64_t>> touched(g.depth + 1);
+
+  // leaves (octree.py:351-360): descend, create, ensure brick, dirty box
+  for (int gz = g0[2]; gz <= g1[2]; ++gz)
+    for (int gy = g0[1]; gy <= g1[1]; ++gy)
+      for (int gx = g0[0]; gx <= g1[0]; ++gx) {
+        int gg[3] = {gx, gy, gz};
+        int64_t idx = 0;
+        for (int lvl = g.depth; lvl > 0; --lvl) {
+          ensure_children(idx);
+          int k = 0;
+          for (int a = 0; a < 3; ++a)
+            if (g.split[a] && ((gg[a] >> (lvl - 1)) & 1)) k |= 1 << a;
+          idx = 8 * idx + 1 + k;
+        }
+        bool fresh = ensure_brick(idx);
+        leaf_slots[((size_t)(gz - g0[2]) * gn[1] + (gy - g0[1])) * gn[0] + (gx - g0[0])] =
+            slot[idx];
+        Box b;
+        for (int a = 0; a < 3; ++a) {
+          int lo = gg[a] * M[a];
+          b.lo[a] = fresh ? 0 : std::max(origin[a], lo) - lo;
+          b.hi[a] = fresh ? M[a] : std::min(origin[a] + dims[a], lo + M[a]) - lo;
+        }
+        Pending& p = pending[0][idx];
+        box_union(p, b);
+        p.fresh |= fresh;
+        touched[0].push_back(idx);
+      }
+  // ancestors (octree.py:363-387): ensure parent bricks, record freshness
+  for (int lvl = 1; lvl <= g.depth; ++lvl) {
+    std::vector<int64_t>& par = touched[lvl];
+    for (int64_t c : touched[lvl - 1]) par.push_back((c - 1) >> 3);
+    std::sort(par.begin(), par.end());
+    par.erase(std::unique(par.begin(), par.end()), par.end());
+    for (int64_t p : par) {
+      bool fresh = ensure_brick(p);
+      pending[lvl][p].fresh |= fresh;
+    }
+  }
+  std::sort(touched[0].begin(), touched[0].end());
+  has_pending = true;
+
+  // device pre-work for this insertion
+  flush_structure();
+  CreateJob* dc = upload(*this, creates);
+  launch_create(*this, dc, (int)creates.size());
+  SeedJob* ds = upload(*this, seeds);
+  launch_seed(*this, ds, (int)seeds.size());
+  int32_t* dl = upload(*this, leaf_slots);
+  launch_scatter(*this, dsrc, channel, src_stride, src_off, origin, dims, g0, gn, dl);
+  release(*this, dc);
+  release(*this, ds);
+  release(*this, dl);
+  inserted += nvox * reps;
+
+  std::vector<char> dmark;
+  std::vector<int64_t> deleted;
+  if (tau > 0) {
+    propagate();
+    std::vector<int64_t> all;
+    for (auto& v : touched) all.insert(all.end(), v.begin(), v.end());
+    gather_stats(all);
+    prune(touched, dmark, deleted);
+    flush_structure();
+  }
+  // NODE_UPDATED for every touched, non-deleted node, sorted (octree.py:393-395)
+  std::vector<int64_t> upd;
+  for (auto& v : touched) upd.insert(upd.end(), v.begin(), v.end());
+  std::sort(upd.begin(), upd.end());
+  upd.erase(std::unique(upd.begin(), upd.end()), upd.end());
+  for (int r = 0; r < reps; ++r)
+    for (int64_t i : upd)
+      if (flags[i] & NF_EXISTS) events.emplace_back(VT_EV_UPDATED, i);
+}
+
+// ---------------------------------------------------------------------------
+// propagation of dirty boxes up the tree
+// ---------------------------------------------------------------------------
+
+void Tree::propagate() {
+  if (!has_pending) return;
+  VT_CUDA(cudaEventRecord(ev0, stream));
+  const int* M = g.brick;
+  for (int lvl = 0; lvl <= g.depth; ++lvl) {
+    auto& pm = pending[lvl];
+    if (pm.empty()) continue;
+    std::vector<int64_t> nodes;
+    nodes.reserve(pm.size());
+    for (auto& kv : pm) nodes.push_back(kv.first);
+    std::sort(nodes.begin(), nodes.end());
+    std::vector<OctJob> oct;
+    if (lvl > 0) {
+      // group dirty children by parent
+      std::map<int64_t, std::vector<int64_t>> kids;
+      for (auto& kv : pending[lvl - 1]) kids[(kv.first - 1) >> 3].push_back(kv.first);
+      for (int64_t p : nodes) {
+        Pending& pp = pm[p];
+        auto emit = [&](int64_t c, const Box* cb) {
+          OctJob j{};
+          j.pslot = slot[p];
+          j.cslot = (flags[c] & NF_BRICK) ? slot[c] : -1;
+          j.child = c;
+          j.k = (int)((c - 1) & 7);
+          node_in_extent(c, j.cext);
+          Box pb;
+          for (int a = 0; a < 3; ++a) {
+            int kk = g.split[a] ? 2 : 1;
+            int off = (((j.k >> a) & 1) && g.split[a]) ? M[a] / 2 : 0;
+            if (cb) {
+              j.r0[a] = cb->lo[a] / kk;
+              j.r1[a] = (cb->hi[a] + kk - 1) / kk;
+            } else {
+              j.r0[a] = 0;
+              j.r1[a] = M[a] / kk;
+            }
+            pb.lo[a] = off + j.r0[a];
+            pb.hi[a] = off + j.r1[a];
+          }
+          if (j.r1[0] > j.r0[0] && j.r1[1] > j.r0[1] && j.r1[2] > j.r0[2]) {
+            oct.push_back(j);
+            box_union(pp, pb);
+          }
+        };
+        if (pp.fresh) {
+          // fresh parent brick: every real octant (octree.py:375-377)
+          for (int k = 0; k < 8; ++k) {
+            if (!g.octant_real(k)) continue;
+            emit(8 * p + 1 + k, nullptr);
+          }
+          pp.box = Box{{0, 0, 0}, {M[0], M[1], M[2]}};
+          pp.has_box = true;
+        } else {
+          auto it = kids.find(p);
+          if (it != kids.end()) {
+            std::sort(it->second.begin(), it->second.end());
+            for (int64_t c : it->second) {
+              Pending& cp = pending[lvl - 1][c];
+              if (cp.has_box) emit(c, &cp.box);
+            }
+          }
+        }
+      }
+      OctJob* d = upload(*this, oct);
+      launch_octant(*this, d, (int)oct.size());
+      release(*this, d);
+    }
+    // stats of this level's dirty nodes
+    std::vector<PlaneJob> planes;
+    std::vector<ReduceJob> reds;
+    for (int64_t n : nodes) {
+      Pending& p = pm[n];
+      ReduceJob r{};
+      r.node = n;
+      r.slot = slot[n];
+      node_in_extent(n, r.cext);
+      r.leafish = (lvl == 0 || !(flags[n] & NF_CHILDREN)) ? 1 : 0;
+      if (p.has_box && r.cext[0] > 0 && r.cext[1] > 0) {
+        int z1 = std::min(p.box.hi[2], r.cext[2]);
+        for (int z = p.box.lo[2]; z < z1; ++z) planes.push_back({r.slot, z, r.cext[0], r.cext[1]});
+      }
+      reds.push_back(r);
+    }
+    PlaneJob* dp = upload(*this, planes);
+    launch_plane(*this, dp, (int)planes.size());
+    ReduceJob* dr = upload(*this, reds);
+    launch_reduce(*this, dr, (int)reds.size());
+    release(*this, dp);
+    release(*this, dr);
+  }
+  for (int lvl = 0; lvl <= g.depth; ++lvl) pending[lvl].clear();
+  has_pending = false;
+  VT_CUDA(cudaEventRecord(ev1, stream));
+}
+
+void Tree::flush() {
+  VT_CUDA(cudaSetDevice(device));
+  flush_structure();
+  propagate();
+}
+
+void Tree::sync() {
+  flush();
+  VT_CUDA(cudaStreamSynchronize(stream));
+  float ms = 0;
+  if (cudaEventElapsedTime(&ms, ev0, ev1) == cudaSuccess) last_build_ms = ms;
+}
+
+void Tree::gather_stats(const std::vector<int64_t>& nodes) {
+  if (nodes.empty()) return;
+  const size_t row = ST_N * kMaxC;
+  int64_t* dn = upload(*this, nodes);
+  int32_t* dout = nullptr;
+  VT_CUDA(cudaMallocAsync(&dout, nodes.size() * row * sizeof(int32_t), stream));
+  launch_gather_stats(*this, dn, (int)nodes.size(), dout);
+  std::vector<int32_t> host(nodes.size() * row);
+  VT_CUDA(cudaMemcpyAsync(host.data(), dout, host.size() * sizeof(int32_t),
+                          cudaMemcpyDeviceToHost, stream));
+  release(*this, dn);
+  release(*this, dout);
+  VT_CUDA(cudaStreamSynchronize(stream));
+  for (size_t i = 0; i < nodes.size(); ++i)
+    std::memcpy(&h_stats[nodes[i] * row], &host[i * row], row * sizeof(int32_t));
+}
+
+// ---------------------------------------------------------------------------
+// pruning (octree.py:446-493), on the gathered statistics
+// ---------------------------------------------------------------------------
+
+void Tree::delete_below(int64_t p, std::vector<char>& mark, std::vector<int64_t>& deleted) {
+  for (int k = 0; k < 8; ++k) {
+    if (!g.octant_real(k)) continue;
+    int64_t c = 8 * p + 1 + k;
+    if (!(flags[c] & NF_EXISTS)) continue;
+    if (flags[c] & NF_CHILDREN) delete_below(c, mark, deleted);
+    free_brick(c);
+    --node_count;
+    flags[c] = 0;
+    slot[c] = -1;
+    mark_struct(c);
+    deleted.push_back(c);
+    events.emplace_back(VT_EV_DELETED, c);
+  }
+  flags[p] &= ~NF_CHILDREN;
+  mark_struct(p);
+}
+
+void Tree::prune(std::vector<std::vector<int64_t>>& touched, std::vector<char>& mark,
+                 std::vector<int64_t>& deleted) {
+  auto homog = [&](int64_t n, int lo_stat, int hi_stat) {
+    for (int c = 0; c < g.C; ++c)
+      if (!((double)(stat(n, hi_stat, c) - stat(n, lo_stat, c)) < tau)) return false;
+    return true;
+  };
+  // pass 1: bricks (ascending level, index)
+  for (int lvl = 0; lvl <= g.depth; ++lvl)
+    for (int64_t n : touched[lvl]) {
+      if (n == 0 || !(flags[n] & NF_BRICK)) continue;
+      if (homog(n, ST_MIN, ST_MAX)) free_brick(n);
+    }
+  // pass 2: homogeneous subtrees
+  for (int lvl = 1; lvl <= g.depth; ++lvl)
+    for (int64_t n : touched[lvl]) {
+      if (n == 0 || !(flags[n] & NF_EXISTS) || !(flags[n] & NF_CHILDREN)) continue;
+      bool sub_h = !(flags[n] & NF_INVOL) || homog(n, ST_SUBMIN, ST_SUBMAX);
+      if (sub_h) delete_below(n, mark, deleted);
+    }
+  // root: collapse only when the whole tree is homogeneous
+  if (homog(0, ST_SUBMIN, ST_SUBMAX) && ((flags[0] & NF_CHILDREN) || (flags[0] & NF_BRICK))) {
+    if (flags[0] & NF_CHILDREN) delete_below(0, mark, deleted);
+    free_brick(0);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// borders (octree.py:540-614)
+// ---------------------------------------------------------------------------
+
+void Tree::fill_borders() {
+  flush();
+  std::vector<BorderJob> jobs;
+  for (int64_t i = 0; i < g.capacity; ++i)
+    if ((flags[i] & NF_EXISTS) && (flags[i] & NF_BRICK)) jobs.push_back({i, slot[i]});
+  BorderJob* d = upload(*this, jobs);
+  launch_borders(*this, d, (int)jobs.size());
+  release(*this, d);
+  for (auto& j : jobs) events.emplace_back(VT_EV_UPDATED, j.node);
+  borders = true;
+}
+
+int64_t Tree::find_node(const double pt[3], int target) const {
+  int64_t idx = 0;
+  int lvl = g.depth;
+  int lo[3] = {0, 0, 0};
+  while (lvl > target && (flags[idx] & NF_CHILDREN)) {
+    int k = 0;
+    for (int a = 0; a < 3; ++a) {
+      int half = g.extent(a, lvl - 1);
+      if (g.split[a] && pt[a] >= lo[a] + half) {
+        k |= 1 << a;
+        lo[a] += half;
+      }
+    }
+    idx = 8 * idx + 1 + k;
+    --lvl;
+  }
+  return idx;
+}
+
+}  // namespace vtx

@@ -1,0 +1,138 @@
+// Host-side octree control plane (structure, slots, events, pruning) over a
+// device-resident brick pool and node-stat arrays.  Replaces voxtree's
+// Octree (octree.py:143-614) + BrickStore (paging.py) for the hot path.
+#pragma once
+
+#include <queue>
+#include <unordered_map>
+#include <vector>
+
+#include "vtx_common.cuh"
+
+namespace vtx {
+
+struct Box {
+  int lo[3], hi[3];  // brick-interior voxel coords, [lo, hi)
+};
+
+struct Pending {
+  Box box;
+  bool has_box = false;
+  bool fresh = false;
+};
+
+struct Tree {
+  Geo g{};
+  double tau = 0;
+  int fmax = 255;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+
+  // -- host structure (authoritative) --
+  std::vector<uint8_t> flags;
+  std::vector<int32_t> slot;
+  int64_t node_count = 1, brick_count = 0, pruned = 0, inserted = 0;
+  bool finished = false, borders = false;
+  std::priority_queue<int32_t, std::vector<int32_t>, std::greater<int32_t>> free_slots;
+  int64_t cursor = 0;
+
+  // -- device state --
+  uint8_t* d_pool = nullptr;  // [pool_slots][Sz][Sy][Sx][C] samples
+  int64_t pool_slots = 0;
+  uint8_t* d_flags = nullptr;
+  int32_t* d_slot = nullptr;
+  int32_t* d_stats = nullptr;  // [capacity][5][4]
+  int32_t* d_pmin = nullptr;   // [pool_slots][Mz][C] plane partials
+  int32_t* d_pmax = nullptr;
+  unsigned long long* d_psum = nullptr;
+
+  // -- host stat cache (valid for nodes gathered since last device change) --
+  std::vector<int32_t> h_stats;
+
+  // -- events (octree.py:41-50) --
+  std::vector<std::pair<int32_t, int64_t>> events;
+
+  // -- deferred propagation (tau == 0 batches; tau > 0 per insertion) --
+  std::vector<std::unordered_map<int64_t, Pending>> pending;
+  bool has_pending = false;
+
+  // -- per-insertion device work lists --
+  std::vector<int64_t> struct_dirty;
+  std::vector<uint8_t> struct_mark;
+  std::vector<CreateJob> creates;
+  std::vector<SeedJob> seeds;
+  std::unordered_map<int64_t, int64_t> created_seed;  // node created this insertion -> seed src
+
+  // timing of the last build flush (CUDA events)
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  double last_build_ms = 0, last_render_ms = 0;
+
+  Tree(const vt_tree_desc& d);
+  ~Tree();
+
+  // structure helpers
+  bool in_volume(int64_t idx) const;
+  void mark_struct(int64_t idx);
+  int32_t alloc_slot();
+  void ensure_pool(int64_t slots_needed);
+  void ensure_children(int64_t p);
+  bool ensure_brick(int64_t n);
+  void node_in_extent(int64_t idx, int c[3]) const;
+
+  // insertion / propagation
+  void insert(int channel, const int origin[3], const int dims[3], const void* samples,
+              int mem_kind);
+  void insert_staged(int channel, const int origin[3], const int dims[3], const void* dsrc,
+                     int src_stride, int src_off, int reps);
+  void flush_structure();
+  void propagate();
+  void flush();  // propagate pending + structure
+  void sync();
+  void gather_stats(const std::vector<int64_t>& nodes);
+  void prune(std::vector<std::vector<int64_t>>& touched, std::vector<char>& deleted_mark,
+             std::vector<int64_t>& deleted);
+  void delete_below(int64_t p, std::vector<char>& mark, std::vector<int64_t>& deleted);
+  void free_brick(int64_t n);
+  void fill_borders();
+  int64_t find_node(const double pt[3], int target) const;
+
+  int32_t stat(int64_t node, int s, int c) const { return h_stats[st_index(node, s, c)]; }
+};
+
+// launch helpers implemented in build_kernels.cu
+void launch_struct_update(const Tree& t, const StructUpd* d_upd, int n);
+void launch_create(const Tree& t, const CreateJob* d_jobs, int n);
+void launch_seed(const Tree& t, const SeedJob* d_jobs, int n);
+void launch_scatter(const Tree& t, const void* src, int channel, int src_stride, int src_off,
+                    const int origin[3],
+                    const int dims[3], const int g0[3], const int gn[3], const int32_t* d_leaf_slots);
+void launch_octant(const Tree& t, const OctJob* d_jobs, int n);
+void launch_plane(const Tree& t, const PlaneJob* d_jobs, int n);
+void launch_reduce(const Tree& t, const ReduceJob* d_jobs, int n);
+void launch_borders(const Tree& t, const BorderJob* d_jobs, int n);
+void launch_gather_stats(const Tree& t, const int64_t* d_nodes, int n, int32_t* d_out);
+void launch_gather_bricks(const Tree& t, const int32_t* d_slots, int n, uint8_t* d_out);
+void launch_scatter_bricks(const Tree& t, const int32_t* d_slots, int n, const uint8_t* d_in);
+void launch_pool_fill(const Tree& t, int64_t first_slot, int64_t n_slots);
+
+// device scratch: stream-ordered allocation of a host vector's copy
+template <class T>
+T* upload(const Tree& t, const std::vector<T>& v) {
+  if (v.empty()) return nullptr;
+  void* p = nullptr;
+  VT_CUDA(cudaMallocAsync(&p, v.size() * sizeof(T), t.stream));
+  VT_CUDA(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, t.stream));
+  return static_cast<T*>(p);
+}
+inline void release(const Tree& t, void* p) {
+  if (p) VT_CUDA(cudaFreeAsync(p, t.stream));
+}
+
+}  // namespace vtx
+
+// the opaque ABI handle (include/vtx.h)
+struct vt_tree {
+  vtx::Tree t;
+  explicit vt_tree(const vt_tree_desc& d) : t(d) {}
+};

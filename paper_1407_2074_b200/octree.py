@@ -1,0 +1,394 @@
+"""Incremental octree over a device-resident (HBM) brick pool — drop-in for
+voxtree.octree (octree.py:143-614).
+
+``Octree`` keeps the reference's constructor, ``insert_block`` /
+``finalize`` / ``fill_borders`` / ``drain_events`` / ``find_node`` /
+``node_by_index`` / ``iter_nodes`` API, exceptions and events.  All data
+work runs in libvtx (csrc/): the host keeps only the lock the reference
+holds (octree.py:153) and the event list.  Node objects returned by the
+queries are snapshots (the reference hands out live objects; callers in the
+reference only read them).
+"""
+
+from __future__ import annotations
+
+import ctypes as ct
+import threading
+from dataclasses import dataclass
+from enum import IntEnum
+
+import numpy as np
+
+from . import _lib
+from .volume import BrickPoolConfig, TreeGeometry, VolumeDescriptor
+
+
+class ChangeKind(IntEnum):
+    NODE_CREATED = 1
+    NODE_DELETED = 2
+    NODE_UPDATED = 3
+
+
+@dataclass(frozen=True)
+class ChangeEvent:
+    kind: ChangeKind
+    node_index: int
+
+
+@dataclass(frozen=True)
+class BrickLocator:
+    """Handle of a node's brick: the node index plus its HBM pool slot."""
+    node_index: int
+    slot: int
+
+
+def round_mean(sums, counts):
+    """(2*sum + n) // (2n), ties up (octree.py:53-55) — host helper for
+    scalar bookkeeping; the bulk means are computed on the device."""
+    s = np.asarray(sums, dtype=np.int64)
+    n = np.asarray(counts, dtype=np.int64)
+    return (2 * s + n) // (2 * n)
+
+
+def halfsample_block(values: np.ndarray, in_extent, split, background: int) -> np.ndarray:
+    """halfsample_block (octree.py:58-92) executed by the device kernel."""
+    v = np.ascontiguousarray(values, dtype=np.int32)
+    if v.ndim != 4:
+        raise ValueError("values must be (mz, my, mx, C)")
+    mz, my, mx, nc = v.shape
+    k = [2 if s else 1 for s in split]
+    out = np.empty((mz // k[2], my // k[1], mx // k[0], nc), dtype=np.int32)
+    shape = (ct.c_int32 * 4)(mz, my, mx, nc)
+    _lib.call("vt_halfsample", _lib.ptr(v, ct.c_int32), shape, _lib.i32x3(in_extent),
+              _lib.i32x3([1 if s else 0 for s in split]), int(background),
+              _lib.ptr(out, ct.c_int32), 0)
+    return out.astype(np.int64)
+
+
+def classify_homogeneous(smin, smax, threshold: float):
+    """Per-channel ``max - min < threshold`` and the overall verdict
+    (octree.py:95-99)."""
+    per = [(hi - lo) < threshold for lo, hi in zip(smin, smax)]
+    return per, all(per)
+
+
+class OctreeNode:
+    """Snapshot of one node (OctreeNode, octree.py:102-140)."""
+
+    __slots__ = ("_tree", "level", "index", "box_lo", "avg", "smin", "smax", "sub_min",
+                 "sub_max", "in_volume", "_flags", "_slot")
+
+    def __init__(self, tree: "Octree", index: int, rec: _lib.vt_node):
+        C = tree.descriptor.channels
+        self._tree = tree
+        self.index = index
+        self.level = int(rec.level)
+        self.box_lo = tuple(int(v) for v in rec.box_lo)
+        self._flags = int(rec.flags)
+        self._slot = int(rec.slot)
+        st = [[int(rec.stats[c][s]) for s in range(5)] for c in range(C)]
+        self.avg = [st[c][0] for c in range(C)]
+        self.smin = [st[c][1] for c in range(C)]
+        self.smax = [st[c][2] for c in range(C)]
+        self.in_volume = bool(self._flags & _lib.NODE_IN_VOLUME)
+        self.sub_min = [st[c][3] for c in range(C)] if self.in_volume else None
+        self.sub_max = [st[c][4] for c in range(C)] if self.in_volume else None
+
+    @property
+    def brick(self):
+        return BrickLocator(self.index, self._slot) if self._flags & _lib.NODE_BRICK else None
+
+    @property
+    def has_children(self) -> bool:
+        return bool(self._flags & _lib.NODE_CHILDREN)
+
+    @property
+    def children(self):
+        if not self.has_children:
+            return None
+        geo = self._tree.geometry
+        out = [None] * 8
+        for k in geo.real_octants:
+            out[k] = self._tree.node_by_index(8 * self.index + 1 + k)
+        return out
+
+    def child_nodes(self):
+        return [c for c in (self.children or []) if c is not None]
+
+    def __repr__(self):
+        kind = "brick" if self.brick else "avg"
+        return f"<node {self.index} L{self.level} {kind} avg={self.avg}>"
+
+
+class _PoolView:
+    """``tree.store`` facade: brick reads go to HBM (BrickStore.read_brick,
+    paging.py:398-403)."""
+
+    def __init__(self, tree: "Octree"):
+        self._tree = tree
+
+    def read_brick(self, loc: BrickLocator) -> np.ndarray:
+        return self._tree.read_brick(loc.node_index)
+
+    @property
+    def live_bricks(self) -> int:
+        return self._tree.brick_count
+
+    @property
+    def payload_nbytes(self) -> int:
+        t = self._tree
+        return t.brick_count * t.config.brick_nbytes(t.descriptor)
+
+    def close(self) -> None:
+        pass
+
+
+class Octree:
+    """Incrementally constructed octree with its brick pool in HBM."""
+
+    def __init__(self, desc: VolumeDescriptor, cfg: BrickPoolConfig, store=None, *,
+                 device: int = 0, reserve_slots: int = 0):
+        self.descriptor = desc
+        self.config = cfg
+        self.geometry = TreeGeometry.build(desc, cfg)
+        self.threshold = cfg.resolve_threshold(desc)
+        self.lock = threading.RLock()
+        self._events: list[ChangeEvent] = []
+        self._closed = False
+        d = _lib.vt_tree_desc()
+        d.dims[:] = list(desc.dims)
+        d.channels = desc.channels
+        d.sample_bytes = desc.dtype.itemsize
+        d.background = desc.background_value
+        d.brick[:] = list(cfg.brick_dims)
+        d.threshold = float(self.threshold)
+        d.reserve_slots = int(reserve_slots)
+        d.device = int(device)
+        self.device = int(device)
+        h = ct.c_void_p()
+        _lib.call("vt_tree_create", ct.byref(d), ct.byref(h))
+        self._h = h
+        self.store = _PoolView(self)
+
+    # -- factories ---------------------------------------------------------
+    @classmethod
+    def create(cls, desc: VolumeDescriptor, cfg: BrickPoolConfig, pool_path=None, **kw):
+        """Octree.create (octree.py:166-176); the pool lives in HBM, so
+        ``pool_path`` is accepted for signature compatibility only."""
+        return cls(desc, cfg, None, **kw)
+
+    def close(self):
+        if not self._closed and self._h:
+            _lib.call("vt_tree_destroy", self._h)
+            self._closed = True
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    # -- events --------------------------------------------------------------
+    def _collect(self) -> list[ChangeEvent]:
+        out = []
+        cap = 1 << 16
+        kinds = np.empty(cap, np.int32)
+        idx = np.empty(cap, np.int64)
+        n, more = ct.c_int64(), ct.c_int32(1)
+        while more.value:
+            _lib.call("vt_tree_take_events", self._h, _lib.ptr(kinds, ct.c_int32),
+                      _lib.ptr(idx, ct.c_int64), cap, ct.byref(n), ct.byref(more))
+            out.extend(ChangeEvent(ChangeKind(int(k)), int(i))
+                       for k, i in zip(kinds[:n.value], idx[:n.value]))
+        self._events.extend(out)
+        return out
+
+    def drain_events(self) -> list[ChangeEvent]:
+        with self.lock:
+            self._collect()
+            ev, self._events = self._events, []
+            return ev
+
+    # -- insertion -------------------------------------------------------------
+    def insert_block(self, channel: int, origin, values) -> list[ChangeEvent]:
+        """Octree.insert_block (octree.py:323-397).  ``values`` (dz, dy, dx)
+        numpy array (host) or a CUDA tensor/array exposing
+        ``__cuda_array_interface__`` (device, stream-ordered)."""
+        desc = self.descriptor
+        if not 0 <= channel < desc.channels:
+            raise ValueError(f"channel {channel} out of range")
+        origin = tuple(int(v) for v in origin)
+        src, kind, shape, keep = self._source(values, 3)
+        bdims = (shape[2], shape[1], shape[0])
+        for a in range(3):
+            if origin[a] < 0 or origin[a] + bdims[a] > desc.dims[a]:
+                raise ValueError(f"block [{origin} + {bdims}) outside volume {desc.dims}")
+        with self.lock:
+            _lib.call("vt_tree_insert", self._h, int(channel), _lib.i32x3(origin),
+                      _lib.i32x3(bdims), src, kind)
+            del keep
+            return self._collect()
+
+    def insert_channels(self, origin, values) -> list[ChangeEvent]:
+        """All channels at once: values (dz, dy, dx, C) interleaved; same
+        tree and events as C successive insert_block calls."""
+        desc = self.descriptor
+        origin = tuple(int(v) for v in origin)
+        src, kind, shape, keep = self._source(values, 4)
+        if shape[3] != desc.channels:
+            raise ValueError("last axis must hold every channel")
+        bdims = (shape[2], shape[1], shape[0])
+        for a in range(3):
+            if origin[a] < 0 or origin[a] + bdims[a] > desc.dims[a]:
+                raise ValueError(f"block [{origin} + {bdims}) outside volume {desc.dims}")
+        with self.lock:
+            _lib.call("vt_tree_insert_channels", self._h, _lib.i32x3(origin),
+                      _lib.i32x3(bdims), src, kind)
+            del keep
+            return self._collect()
+
+    def _source(self, values, ndim):
+        dt = self.descriptor.dtype
+        cai = getattr(values, "__cuda_array_interface__", None)
+        if cai is not None:
+            import torch
+            t = torch.as_tensor(values, device="cuda") if not isinstance(values, torch.Tensor) \
+                else values
+            if t.dim() != ndim:
+                raise ValueError(f"block values must be {ndim}-D")
+            want = torch.uint8 if dt == np.uint8 else torch.uint16
+            t = t.to(want).contiguous()
+            # device work runs on the tree's own stream: order it after torch's
+            torch.cuda.current_stream(t.device).synchronize()
+            return ct.c_void_p(t.data_ptr()), _lib.VT_MEM_DEVICE, tuple(t.shape), t
+        arr = np.asarray(values)
+        if arr.ndim != ndim:
+            raise ValueError("block values must be 3-D (z, y, x)" if ndim == 3 else
+                             "block values must be 4-D (z, y, x, c)")
+        arr = np.ascontiguousarray(arr.astype(dt, copy=False))
+        return ct.c_void_p(arr.ctypes.data), _lib.VT_MEM_HOST, arr.shape, arr
+
+    # -- state ---------------------------------------------------------------
+    def _info(self) -> _lib.vt_tree_info:
+        info = _lib.vt_tree_info()
+        _lib.call("vt_tree_info_get", self._h, ct.byref(info))
+        return info
+
+    @property
+    def node_count(self) -> int:
+        return int(self._info().node_count)
+
+    @property
+    def brick_count(self) -> int:
+        return int(self._info().brick_count)
+
+    @property
+    def pruned_bricks(self) -> int:
+        return int(self._info().pruned_bricks)
+
+    @property
+    def inserted_voxels(self) -> int:
+        return int(self._info().inserted_voxels)
+
+    @property
+    def construction_finished(self) -> bool:
+        return bool(self._info().finished)
+
+    @property
+    def borders_filled(self) -> bool:
+        return bool(self._info().borders_filled)
+
+    @property
+    def root(self) -> OctreeNode:
+        return self.node_by_index(0)
+
+    def sync(self) -> None:
+        """Complete deferred device work (tau == 0 batches)."""
+        _lib.call("vt_tree_sync", self._h)
+
+    # -- finalization ----------------------------------------------------------
+    def finalize(self) -> None:
+        with self.lock:
+            _lib.call("vt_tree_finalize", self._h)
+
+    def fill_borders(self) -> None:
+        """octree.py:540-549; emits NODE_UPDATED per brick."""
+        with self.lock:
+            _lib.call("vt_tree_fill_borders", self._h)
+            self._collect()
+
+    def fill_borders_async(self) -> threading.Thread:
+        th = threading.Thread(target=self.fill_borders, name="border-fill", daemon=True)
+        th.start()
+        return th
+
+    # -- lookup ------------------------------------------------------------------
+    def node_by_index(self, index: int) -> OctreeNode | None:
+        rec = _lib.vt_node()
+        ex = ct.c_int32()
+        _lib.call("vt_tree_node", self._h, int(index), ct.byref(rec), ct.byref(ex))
+        return OctreeNode(self, int(index), rec) if ex.value else None
+
+    def find_node(self, point, target_level: int = 0) -> OctreeNode:
+        p = (ct.c_double * 3)(*[float(v) for v in point])
+        out = ct.c_int64()
+        _lib.call("vt_tree_find_node", self._h, p, int(target_level), ct.byref(out))
+        return self.node_by_index(out.value)
+
+    def node_indices(self, with_flags: bool = False):
+        n = ct.c_int64()
+        _lib.call("vt_tree_list_nodes", self._h, None, None, 0, ct.byref(n))
+        idx = np.empty(n.value, np.int64)
+        fl = np.empty(n.value, np.int32)
+        _lib.call("vt_tree_list_nodes", self._h, _lib.ptr(idx, ct.c_int64),
+                  _lib.ptr(fl, ct.c_int32), n.value, ct.byref(n))
+        return (idx, fl) if with_flags else idx
+
+    def iter_nodes(self):
+        """Breadth-first (== ascending index) snapshots (octree.py:507-513)."""
+        idx, flags, stats, _ = self.export(with_bricks=False)
+        geo = self.geometry
+        for r, i in enumerate(idx):
+            rec = _lib.vt_node()
+            rec.flags = int(flags[r])
+            rec.level = geo.level_of_index(int(i))
+            rec.box_lo[:] = list(geo.box_lo_of_index(int(i)))
+            rec.slot = -1
+            for c in range(self.descriptor.channels):
+                for s in range(5):
+                    rec.stats[c][s] = int(stats[r, c, s])
+            yield OctreeNode(self, int(i), rec)
+
+    def read_brick(self, index: int) -> np.ndarray:
+        cfg, desc = self.config, self.descriptor
+        bz, by, bx = tuple(reversed(cfg.stored_brick_dims))
+        out = np.empty((bz, by, bx, desc.channels), dtype=desc.dtype)
+        _lib.call("vt_tree_read_brick", self._h, int(index), ct.c_void_p(out.ctypes.data))
+        return out
+
+    def export(self, indices=None, with_bricks=True):
+        """Bulk snapshot for serialization: (indices, VT_NODE_* flags, stats
+        (n, C, 5) as [avg, smin, smax, sub_min, sub_max], bricks of the
+        bricked nodes in index order)."""
+        all_idx, all_fl = self.node_indices(with_flags=True)
+        if indices is None:
+            idx, flags = all_idx, all_fl
+        else:
+            idx = np.asarray(indices, np.int64)
+            lut = dict(zip(all_idx.tolist(), all_fl.tolist()))
+            flags = np.asarray([lut[int(i)] for i in idx], np.int32)
+        C = self.descriptor.channels
+        stats = np.empty((len(idx), C, 5), np.int32)
+        nbrick = int(np.count_nonzero(flags & _lib.NODE_BRICK))
+        bricks = None
+        if with_bricks:
+            bz, by, bx = tuple(reversed(self.config.stored_brick_dims))
+            bricks = np.empty((nbrick, bz, by, bx, C), dtype=self.descriptor.dtype)
+        _lib.call("vt_tree_export", self._h, len(idx), _lib.ptr(idx, ct.c_int64),
+                  _lib.ptr(stats, ct.c_int32),
+                  ct.c_void_p(bricks.ctypes.data) if bricks is not None and nbrick else None)
+        return idx, flags, stats, bricks

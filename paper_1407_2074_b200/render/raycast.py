@@ -1,0 +1,187 @@
+"""Octree ray caster — drop-in for voxtree.render.raycast (raycast.py:53-339).
+
+``OutOfCoreRenderer.render_fullframe`` launches the fused full-frame kernel
+(ray setup + march + finalize in one pass); ``RefinementSession`` keeps the
+per-ray state (k, accumulated colour, maxima, terminated/suspended) in HBM
+between passes.  No CPU path exists.
+"""
+
+from __future__ import annotations
+
+import ctypes as ct
+
+import numpy as np
+
+from .. import _lib
+from ..device import DeviceState
+from .core import RenderCounters
+from .settings import Scene
+
+OUT_F64, OUT_F32, OUT_RGBA8 = 0, 1, 2
+
+
+def scene_to_vt(scene: Scene, descriptor) -> _lib.vt_scene:
+    """Pack a Scene for the kernel.  Transcendental / BLAS-dependent camera
+    constants are computed with numpy exactly as the reference computes them
+    (camera.py:33-57, settings.py:60-67)."""
+    cam, st = scene.camera, scene.settings
+    C = descriptor.channels
+    if len(scene.transfer_functions) != C:
+        raise ValueError(f"need one transfer function per channel ({C})")
+    s = _lib.vt_scene()
+    pos, fwd, right, up = cam.basis()
+    s.position[:] = list(pos)
+    s.fwd[:] = list(fwd)
+    s.right[:] = list(right)
+    s.up[:] = list(up)
+    s.tan_half = float(np.tan(cam.fov_y / 2.0))
+    s.aspect = cam.width / cam.height
+    s.footprint_scale = float(cam.pixel_footprint_scale())
+    s.width, s.height = int(cam.width), int(cam.height)
+    s.mode_mip = 1 if st.mode == "mip" else 0
+    step = st.resolve_step(descriptor.spacing)
+    s.step = step
+    s.corr_exp = st.opacity_exponent(step)
+    et = st.early_termination_alpha
+    s.et_limit = -1.0 if et is None else float(et)
+    s.lod_scale = float(2.0 ** st.lod_bias)
+    for c, tf in enumerate(scene.transfer_functions):
+        n = len(tf.xs)
+        s.tf_count[c] = n
+        for q in range(n):
+            s.tf_x[c][q] = float(tf.xs[q])
+            for a in range(4):
+                s.tf_rgba[c][q][a] = float(tf.rgba[q, a])
+    planes = list(scene.clips)
+    s.n_clips = len(planes)
+    for q, p in enumerate(planes):
+        s.clip_normal[q][:] = [float(v) for v in p.normal]
+        s.clip_offset[q] = float(p.offset)
+    s.spacing[:] = list(descriptor.spacing)
+    s.has_transforms = 1 if descriptor.has_channel_transforms else 0
+    if s.has_transforms:
+        for c in range(C):
+            m = np.asarray(descriptor.channel_transforms[c], dtype=np.float64)
+            s.transforms[c][:] = [float(v) for v in m[:3, :4].reshape(-1)]
+    return s
+
+
+class OutOfCoreRenderer:
+    """Full-frame and refinement passes over a DeviceState (raycast.py:53-295)."""
+
+    def __init__(self, device: DeviceState):
+        self.device = device
+        self.descriptor = device.octree.descriptor
+        self.geometry = device.octree.geometry
+        self.channels = self.descriptor.channels
+
+    def render_fullframe(self, scene: Scene, out_kind: int = OUT_F64):
+        """One complete pass; returns ((H, W, 4) image, RenderCounters)."""
+        s = scene_to_vt(scene, self.descriptor)
+        cam = scene.camera
+        dtype = {OUT_F64: np.float64, OUT_F32: np.float32, OUT_RGBA8: np.uint8}[out_kind]
+        img = np.empty((cam.height, cam.width, 4), dtype=dtype)
+        cnt = _lib.vt_counters()
+        _lib.call("vt_render_fullframe", self.device.handle, ct.byref(s),
+                  ct.c_void_p(img.ctypes.data), out_kind, 0, ct.byref(cnt))
+        return img, RenderCounters.from_vt(cnt)
+
+    def render_tile(self, scene: Scene, rect, out_kind: int = OUT_F64):
+        """Pixels [x0,x1) x [y0,y1) of the full-frame image (sort-first tile)."""
+        s = scene_to_vt(scene, self.descriptor)
+        x0, y0, x1, y1 = (int(v) for v in rect)
+        dtype = {OUT_F64: np.float64, OUT_F32: np.float32, OUT_RGBA8: np.uint8}[out_kind]
+        img = np.empty((y1 - y0, x1 - x0, 4), dtype=dtype)
+        cnt = _lib.vt_counters()
+        r = (ct.c_int32 * 4)(x0, y0, x1, y1)
+        _lib.call("vt_render_tile", self.device.handle, ct.byref(s), r,
+                  ct.c_void_p(img.ctypes.data), out_kind, 0, ct.byref(cnt))
+        return img, RenderCounters.from_vt(cnt)
+
+    def start_refinement(self, scene: Scene, tile=None) -> "RefinementSession":
+        return RefinementSession(self, scene, tile=tile)
+
+
+class _RayView:
+    """``session.rays`` view: n_steps / k / suspended copied from HBM."""
+
+    def __init__(self, session: "RefinementSession"):
+        self._s = session
+
+    def _state(self):
+        n = self._s._n
+        k = np.empty(n, np.int64)
+        ns = np.empty(n, np.int64)
+        sus = np.empty(n, np.uint8)
+        _lib.call("vt_rays_state", self._s._h, _lib.ptr(k, ct.c_int64),
+                  _lib.ptr(ns, ct.c_int64), ct.c_void_p(sus.ctypes.data))
+        return k, ns, sus.astype(bool)
+
+    @property
+    def k(self):
+        return self._state()[0]
+
+    @property
+    def n_steps(self):
+        return self._state()[1]
+
+    @property
+    def suspended(self):
+        return self._state()[2]
+
+
+class RefinementSession:
+    """Progressive refinement with per-ray state cached in HBM between
+    passes (raycast.py:298-339); complete when a pass requests nothing."""
+
+    def __init__(self, renderer: OutOfCoreRenderer, scene: Scene, tile=None):
+        self.renderer = renderer
+        self.scene = scene
+        self.scene_key = scene.key()
+        s = scene_to_vt(scene, renderer.descriptor)
+        cam = scene.camera
+        self._n = cam.width * cam.height
+        h = ct.c_void_p()
+        t = None
+        if tile is not None:
+            x0, y0, x1, y1 = (int(v) for v in tile)
+            t = (ct.c_int32 * 4)(max(0, x0), max(0, y0), min(cam.width, x1), min(cam.height, y1))
+        _lib.call("vt_rays_create", renderer.device.handle, ct.byref(s), t, ct.byref(h))
+        self._h = h
+        self.rays = _RayView(self)
+        self.counters = RenderCounters()
+        self.passes = 0
+        self.complete = False
+        self._last_suspended = 0
+
+    def __del__(self):
+        try:
+            if self._h:
+                _lib.call("vt_rays_destroy", self._h)
+                self._h = None
+        except Exception:
+            pass
+
+    def run_pass(self) -> bool:
+        if self.complete:
+            return True
+        cnt = _lib.vt_counters()
+        sus = ct.c_int64()
+        _lib.call("vt_rays_march", self._h, 1, ct.byref(cnt), ct.byref(sus))
+        self.passes += 1
+        pc = RenderCounters.from_vt(cnt)
+        self.counters = self.counters.merged(pc)
+        self._last_suspended = int(sus.value)
+        self.complete = pc.bricks_requested == 0
+        return self.complete
+
+    @property
+    def suspended_rays(self) -> int:
+        return self._last_suspended
+
+    def image(self) -> np.ndarray:
+        cam = self.scene.camera
+        out = np.empty((cam.height, cam.width, 4), np.float64)
+        cnt = _lib.vt_counters()
+        _lib.call("vt_rays_image", self._h, ct.c_void_p(out.ctypes.data), ct.byref(cnt))
+        return out
