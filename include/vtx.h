@@ -230,6 +230,16 @@ vt_status vt_render_fullframe(vt_mirror* m, const vt_scene* scene, void* out,
 vt_status vt_render_tile(vt_mirror* m, const vt_scene* scene, const int32_t rect[4], void* out,
                          int32_t out_kind, int32_t out_on_device, vt_counters* cnt);
 
+/* sort-first strip partition (multi-GPU): render the rows of
+ * strips part, part + n_parts, part + 2 n_parts, ... (strip_rows rows each,
+ * full width) into a compact (vt_strip_part_rows(H, strip_rows, n_parts), W, 4)
+ * buffer; rows past the frame are zero.  Interleaving balances the per-GPU
+ * sample load; n_parts == 1 equals vt_render_fullframe. */
+vt_status vt_render_strips(vt_mirror* m, const vt_scene* scene, int32_t strip_rows,
+                           int32_t n_parts, int32_t part, void* out, int32_t out_kind,
+                           int32_t out_on_device, vt_counters* cnt);
+int32_t vt_strip_part_rows(int32_t height, int32_t strip_rows, int32_t n_parts);
+
 /* synthetic volumes (oracle/voxtree_oracle.py synth_*): device fill of
  * z in [z0,z1) as (z,y,x,C) interleaved samples; kind 0 uniform, 1 spim */
 vt_status vt_synth(void* out_device, int32_t kind, const int32_t dims[3], int32_t channels,

@@ -100,6 +100,9 @@ SIGNATURES = {
     "vt_rays_state": [P, PI64, PI64, P],
     "vt_render_fullframe": [P, ct.POINTER(vt_scene), P, I32, I32, ct.POINTER(vt_counters)],
     "vt_render_tile": [P, ct.POINTER(vt_scene), PI32, P, I32, I32, ct.POINTER(vt_counters)],
+    "vt_render_strips": [P, ct.POINTER(vt_scene), I32, I32, I32, P, I32, I32,
+                         ct.POINTER(vt_counters)],
+    "vt_strip_part_rows": [I32, I32, I32],
     "vt_synth": [P, I32, PI32, I32, I32, U32, I32, I32, P],
     "vt_last_kernel_ms": [P, ct.POINTER(ct.c_double), ct.POINTER(ct.c_double)],
 }

@@ -112,7 +112,7 @@ vt_status vt_tree_create(const vt_tree_desc* desc, vt_tree** out) {
 }
 
 vt_status vt_tree_destroy(vt_tree* tree) {
-  return guarded([&] { delete tree; });
+  return guarded([&] { vt_tree_release(tree); });
 }
 
 vt_status vt_tree_set_stream(vt_tree* tree, void* stream) {

@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 
 #include "tree.cuh"
@@ -24,6 +25,7 @@ using namespace vtx;
 
 struct vt_mirror {
   vt_tree* tree = nullptr;
+  std::atomic<int> refs{1};  // ray sessions keep their mirror alive
   bool zero_copy = false;
   int64_t slots = 0;
   uint64_t* d_nb = nullptr;
@@ -62,6 +64,9 @@ struct RenderParams {
   double tr[kMaxC][12];
   // tile restriction
   int rect[4];  // x0, y0, x1, y1
+  // sort-first strip interleave: this launch renders the rows of strips
+  // part, part + n_parts, ... (strip_rows rows each), written compactly
+  int strip_rows, n_parts, part;
 };
 
 // per-launch scene + geometry; render entry points serialise on g_render_mu
@@ -429,14 +434,20 @@ __device__ void warp_add_counters(const Counters& c, unsigned long long* out) {
   }
 }
 
-__device__ __forceinline__ bool pixel_of(int& i, int& j) {
+// pixel of this thread: i (column), j (frame row), jl (output row)
+__device__ __forceinline__ bool pixel_of(int& i, int& j, int& jl) {
   const RenderParams& P = c_P;
   // warp = 8x4 pixel tile; block = 4 warps stacked vertically (8x16)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   i = blockIdx.x * 8 + (lane & 7);
-  j = (blockIdx.y * 4 + warp) * 4 + (lane >> 3);
+  jl = (blockIdx.y * 4 + warp) * 4 + (lane >> 3);
   i += P.rect[0];
-  j += P.rect[1];
+  if (P.n_parts > 1) {
+    const int s = jl / P.strip_rows;
+    j = (s * P.n_parts + P.part) * P.strip_rows + (jl - s * P.strip_rows);
+  } else {
+    j = jl + P.rect[1];
+  }
   return i < P.rect[2] && j < P.rect[3];
 }
 
@@ -459,11 +470,12 @@ template <class T>
 __global__ void __launch_bounds__(128) k_render_fullframe(const uint64_t* __restrict__ nb,
                                                           uint8_t* fb, const T* __restrict__ bb,
                                                           void* out, int out_kind, int out_w,
+                                                          int out_rows,
                                                           unsigned long long* counters) {
   const RenderParams& P = c_P;
   Counters cnt{0, 0, 0, 0, 0, 0};
-  int i, j;
-  bool active = pixel_of(i, j);
+  int i, j, jl;
+  bool active = pixel_of(i, j, jl);
   if (active) {
     double d[3];
     ray_dir(i, j, d);
@@ -483,7 +495,11 @@ __global__ void __launch_bounds__(128) k_render_fullframe(const uint64_t* __rest
     }
     double px[4];
     finalize(o, px, cnt);
-    store_px<T>(out, out_kind, (int64_t)(j - P.rect[1]) * out_w + (i - P.rect[0]), px);
+    store_px<T>(out, out_kind, (int64_t)jl * out_w + (i - P.rect[0]), px);
+  } else if (P.n_parts > 1 && i < P.rect[2] && jl < out_rows) {
+    // padding rows of the last strip: deterministic zeros
+    const double z[4] = {0.0, 0.0, 0.0, 0.0};
+    store_px<T>(out, out_kind, (int64_t)jl * out_w + (i - P.rect[0]), z);
   }
   warp_add_counters(cnt, counters);
 }
@@ -528,9 +544,9 @@ __global__ void __launch_bounds__(128) k_rays_march(RayState S,
                                                     unsigned long long* n_susp) {
   const RenderParams& P = c_P;
   Counters cnt{0, 0, 0, 0, 0, 0};
-  int i, j;
+  int i, j, jl;
   // stateful passes cover the whole frame; rect = full
-  bool active = pixel_of(i, j);
+  bool active = pixel_of(i, j, jl);
   bool susp = false;
   if (active) {
     const int64_t r = (int64_t)j * P.W + i;
@@ -653,6 +669,13 @@ __global__ void k_upload(const int32_t* __restrict__ src_slots, const int32_t* _
 // the parameter upload until their kernels have completed
 std::mutex g_render_mu;
 
+// rows of one part's compact output: ceil(strips / n_parts) whole strips
+int strip_part_rows(int H, int strip_rows, int n_parts) {
+  if (n_parts <= 1) return H;
+  const int strips = (H + strip_rows - 1) / strip_rows;
+  return (strips + n_parts - 1) / n_parts * strip_rows;
+}
+
 void set_params(const RenderParams& P, cudaStream_t st) {
   VT_CUDA(cudaMemcpyToSymbolAsync(c_P, &P, sizeof(RenderParams), 0, cudaMemcpyHostToDevice, st));
 }
@@ -721,6 +744,9 @@ void fill_params(const vt_mirror* m, const vt_scene* s, RenderParams& P) {
   P.rect[1] = 0;
   P.rect[2] = P.W;
   P.rect[3] = P.H;
+  P.strip_rows = P.H > 0 ? P.H : 1;
+  P.n_parts = 1;
+  P.part = 0;
 }
 
 }  // namespace
@@ -740,6 +766,7 @@ vt_status vt_mirror_create(vt_tree* tree, int64_t slot_count, vt_mirror** out) {
     t.flush();
     auto* m = new vt_mirror();
     m->tree = tree;
+    vt_tree_retain(tree);
     const int64_t cap = t.g.capacity;
     const int64_t cap4 = (cap + 3) & ~3LL;
     try {
@@ -761,6 +788,7 @@ vt_status vt_mirror_create(vt_tree* tree, int64_t slot_count, vt_mirror** out) {
       cudaFree(m->d_fb);
       cudaFree(m->d_bb);
       cudaFree(m->d_res);
+      vt_tree_release(m->tree);
       delete m;
       throw;
     }
@@ -768,16 +796,19 @@ vt_status vt_mirror_create(vt_tree* tree, int64_t slot_count, vt_mirror** out) {
   });
 }
 
+static void mirror_release(vt_mirror* m) {
+  if (!m || m->refs.fetch_sub(1) != 1) return;
+  cudaStreamSynchronize(m->tree->t.stream);
+  cudaFree(m->d_nb);
+  cudaFree(m->d_fb);
+  cudaFree(m->d_bb);
+  cudaFree(m->d_res);
+  vt_tree_release(m->tree);
+  delete m;
+}
+
 vt_status vt_mirror_destroy(vt_mirror* m) {
-  return guarded([&] {
-    if (!m) return;
-    cudaStreamSynchronize(m->tree->t.stream);
-    cudaFree(m->d_nb);
-    cudaFree(m->d_fb);
-    cudaFree(m->d_bb);
-    cudaFree(m->d_res);
-    delete m;
-  });
+  return guarded([&] { mirror_release(m); });
 }
 
 vt_status vt_mirror_buffers(vt_mirror* m, void** nbp, void** fbp, void** bbp, int64_t* cap,
@@ -867,19 +898,29 @@ static void add_counters(vt_counters* cnt, const unsigned long long* h) {
 }
 
 static void render_rect(vt_mirror* m, const vt_scene* scene, const int32_t* rect, void* out,
-                        int32_t out_kind, int32_t out_on_device, vt_counters* cnt) {
+                        int32_t out_kind, int32_t out_on_device, vt_counters* cnt,
+                        int strip_rows = 0, int n_parts = 1, int part = 0) {
   std::lock_guard<std::mutex> lk(g_render_mu);
   Tree& t = m->tree->t;
   t.flush();
   RenderParams P;
   fill_params(m, scene, P);
+  VT_REQUIRE(out_kind >= 0 && out_kind <= 2, VT_EINVAL, "out_kind must be 0, 1 or 2");
   if (rect) {
     VT_REQUIRE(rect[0] >= 0 && rect[1] >= 0 && rect[2] <= P.W && rect[3] <= P.H &&
                    rect[0] <= rect[2] && rect[1] <= rect[3],
                VT_EINVAL, "tile rectangle outside the viewport");
     for (int a = 0; a < 4; ++a) P.rect[a] = rect[a];
   }
-  const int rw = P.rect[2] - P.rect[0], rh = P.rect[3] - P.rect[1];
+  int rw = P.rect[2] - P.rect[0], rh = P.rect[3] - P.rect[1];
+  if (n_parts > 1) {
+    VT_REQUIRE(strip_rows > 0 && part >= 0 && part < n_parts, VT_EINVAL,
+               "strip partition needs strip_rows > 0 and 0 <= part < n_parts");
+    P.strip_rows = strip_rows;
+    P.n_parts = n_parts;
+    P.part = part;
+    rh = strip_part_rows(P.H, strip_rows, n_parts);
+  }
   const int64_t px = (int64_t)rw * rh;
   const int esz = out_kind == 0 ? 8 : (out_kind == 1 ? 4 : 1);
   void* dout = out;
@@ -893,10 +934,10 @@ static void render_rect(vt_mirror* m, const vt_scene* scene, const int32_t* rect
   if (px > 0) {
     if (t.g.sb == 1)
       k_render_fullframe<uint8_t><<<grid, 128, 0, t.stream>>>(
-          m->d_nb, m->d_fb, (const uint8_t*)brick_ptr(m), dout, out_kind, rw, dc);
+          m->d_nb, m->d_fb, (const uint8_t*)brick_ptr(m), dout, out_kind, rw, rh, dc);
     else
       k_render_fullframe<uint16_t><<<grid, 128, 0, t.stream>>>(
-          m->d_nb, m->d_fb, (const uint16_t*)brick_ptr(m), dout, out_kind, rw, dc);
+          m->d_nb, m->d_fb, (const uint16_t*)brick_ptr(m), dout, out_kind, rw, rh, dc);
     VT_CUDA(cudaGetLastError());
   }
   VT_CUDA(cudaEventRecord(t.ev1, t.stream));
@@ -923,12 +964,27 @@ vt_status vt_render_tile(vt_mirror* m, const vt_scene* scene, const int32_t rect
   return guarded([&] { render_rect(m, scene, rect, out, out_kind, out_on_device, cnt); });
 }
 
+vt_status vt_render_strips(vt_mirror* m, const vt_scene* scene, int32_t strip_rows,
+                           int32_t n_parts, int32_t part, void* out, int32_t out_kind,
+                           int32_t out_on_device, vt_counters* cnt) {
+  return guarded([&] {
+    VT_REQUIRE(n_parts >= 1, VT_EINVAL, "n_parts must be >= 1");
+    render_rect(m, scene, nullptr, out, out_kind, out_on_device, cnt, strip_rows, n_parts, part);
+  });
+}
+
+int32_t vt_strip_part_rows(int32_t height, int32_t strip_rows, int32_t n_parts) {
+  if (height <= 0 || strip_rows <= 0 || n_parts <= 0) return 0;
+  return strip_part_rows(height, strip_rows, n_parts);
+}
+
 vt_status vt_rays_create(vt_mirror* m, const vt_scene* scene, const int32_t* tile, vt_rays** out) {
   return guarded([&] {
     std::lock_guard<std::mutex> lk(g_render_mu);
     Tree& t = m->tree->t;
     auto* r = new vt_rays();
     r->m = m;
+    m->refs.fetch_add(1);
     fill_params(m, scene, r->P);
     if (tile)
       for (int a = 0; a < 4; ++a) r->P.rect[a] = tile[a];
@@ -958,6 +1014,7 @@ vt_status vt_rays_destroy(vt_rays* r) {
     cudaFree(r->S.flags);
     cudaFree(r->S.acc);
     cudaFree(r->S.mip);
+    mirror_release(r->m);
     delete r;
   });
 }

@@ -3,6 +3,7 @@
 // Octree (octree.py:143-614) + BrickStore (paging.py) for the hot path.
 #pragma once
 
+#include <atomic>
 #include <queue>
 #include <unordered_map>
 #include <vector>
@@ -132,7 +133,14 @@ inline void release(const Tree& t, void* p) {
 }  // namespace vtx
 
 // the opaque ABI handle (include/vtx.h)
+// Reference counted: a mirror (and its ray sessions) keep the tree alive, so
+// Python finalizers may run in any order (GC of reference cycles).
 struct vt_tree {
   vtx::Tree t;
+  std::atomic<int> refs{1};
   explicit vt_tree(const vt_tree_desc& d) : t(d) {}
 };
+inline void vt_tree_retain(vt_tree* t) { t->refs.fetch_add(1); }
+inline void vt_tree_release(vt_tree* t) {
+  if (t && t->refs.fetch_sub(1) == 1) delete t;
+}
