@@ -18,6 +18,7 @@
 #include <cstring>
 #include <atomic>
 #include <mutex>
+#include <type_traits>
 
 #include "tree.cuh"
 
@@ -58,6 +59,12 @@ struct RenderParams {
   int tf_n[kMaxC];
   double tf_x[kMaxC][VT_MAX_TF_POINTS];
   double tf_v[kMaxC][VT_MAX_TF_POINTS][4];
+  double tf_s[kMaxC][VT_MAX_TF_POINTS][4];  // segment slopes (host FP64)
+  double inv_fmax;
+  double inv_scl[kMaxLevels][3];  // exact: scales are powers of two
+  int unit_spacing;               // spacing == (1, 1, 1): p / spacing == p
+  int base_pow2;                  // base_voxel a power of two: exact reciprocal
+  double inv_base;
   int n_clips;
   double clip_n[3][3], clip_o[3];
   int has_tr;
@@ -139,30 +146,43 @@ __device__ void ray_setup(const double d[3], double& t0o, long long& n) {
   n = hit ? (long long)ceil(span / P.step - 1e-12) : 0;
 }
 
-// np.interp on sorted control points (transfer.py:34-41)
-__device__ double interp(int c, int comp, double x) {
+// np.interp on sorted control points (transfer.py:34-41), all four RGBA
+// components from one segment search.  Segment slopes are precomputed on
+// the host in FP64 with the same operation numpy uses, so every result is
+// bit-identical to numpy's: slope * (x - xp[j]) + fp[j].
+__device__ __forceinline__ void interp4(int c, double x, double out[4]) {
   const RenderParams& P = c_P;
   const int n = P.tf_n[c];
   const double* xp = P.tf_x[c];
   if (!(x >= xp[0])) {
-    if (x != x) return x;
-    return P.tf_v[c][0][comp];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) out[q] = x != x ? x : P.tf_v[c][0][q];
+    return;
   }
-  if (x >= xp[n - 1]) return P.tf_v[c][n - 1][comp];
+  if (x >= xp[n - 1]) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) out[q] = P.tf_v[c][n - 1][q];
+    return;
+  }
   int j = 0;
-  while (j + 1 < n && !(x < xp[j + 1])) ++j;
-  double y0 = P.tf_v[c][j][comp], y1 = P.tf_v[c][j + 1][comp];
-  double slope = (y1 - y0) / (xp[j + 1] - xp[j]);
-  double r = slope * (x - xp[j]) + y0;
-  if (r != r) {
-    r = slope * (x - xp[j + 1]) + y1;
-    if (r != r && y0 == y1) r = y0;
+  while (j + 2 < n && !(x < xp[j + 1])) ++j;
+  const double dx = x - xp[j];
+  const bool exact = x == xp[j];  // numpy returns fp[j] on an exact knot
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const double y0 = P.tf_v[c][j][q];
+    double r = exact ? y0 : P.tf_s[c][j][q] * dx + y0;
+    if (r != r) {
+      const double y1 = P.tf_v[c][j + 1][q];
+      r = P.tf_s[c][j][q] * (x - xp[j + 1]) + y1;
+      if (r != r && y0 == y1) r = y0;
+    }
+    out[q] = r;
   }
-  return r;
 }
 
 struct DescentCache {
-  int target = -1;
+  int target;
   int lvl;
   long long idx;
   double lo[3];
@@ -171,20 +191,30 @@ struct DescentCache {
   double a_lo[2][3];
 };
 
+// floor(log2(v)) for a positive normal double: its unbiased exponent
+__device__ __forceinline__ int floor_log2(double v) {
+  return (int)((__double_as_longlong(v) >> 52) & 0x7FF) - 1023;
+}
+
 #define P c_P
-template <class T>
+template <class T, int NC, bool TR>
 struct Sampler {
   const uint64_t* __restrict__ nb;
   uint8_t* fb;
   const T* __restrict__ bb;
   bool fullframe;
-  Counters& cnt;
+  Counters cnt;  // by value: stays in registers
   long long last_used = -1, last_req = -1;
-  DescentCache cache[kMaxC];
+  DescentCache cache[TR ? NC : 1];
 
-  __device__ Sampler(const uint64_t* n, uint8_t* f, const T* b, bool ff, Counters& c)
-      : nb(n), fb(f), bb(b), fullframe(ff), cnt(c) {}
+  __device__ Sampler(const uint64_t* n, uint8_t* f, const T* b, bool ff)
+      : nb(n), fb(f), bb(b), fullframe(ff), cnt{0, 0, 0, 0, 0, 0} {
+#pragma unroll
+    for (int q = 0; q < (TR ? NC : 1); ++q) cache[q].target = -1;
+  }
 
+  // feedback flag: idempotent OR into the byte of the node (device.py:35-36,
+  // raycast.py:161-163); skipped when this thread already marked the node
   __device__ void mark(long long idx, unsigned flag) {
     long long& last = flag == 1 ? last_used : last_req;
     if (last == idx) return;
@@ -199,47 +229,58 @@ struct Sampler {
     return rint((double)q * P.fmax / P.qmax);
   }
 
-  __device__ double trilerp(uint64_t e, int lvl, const double lo[3], const double pv[3],
-                            int c) const {
+  // _trilerp (raycast.py:133-159) for channels [c0, c1): cell index and
+  // weights once per sample, then the 8 corners of every channel
+  __device__ void trilerp(uint64_t e, int lvl, const double lo[3], const double pv[3], int c0,
+                          int c1, double* out) const {
     const long long slot = (long long)((e >> 24) & 0xFFFFFFFFULL);
-    const T* b = bb + slot * P.g.brick_elems;
     int i0[3];
     double w1[3], w0[3];
+#pragma unroll
     for (int a = 0; a < 3; ++a) {
-      double m = (double)P.g.brick[a];
-      double f = (pv[a] - lo[a]) / P.scl[lvl][a] + 0.5;
+      const double m = (double)P.g.brick[a];
+      // scale is a power of two: multiplying by its reciprocal is exact
+      double f = (pv[a] - lo[a]) * P.inv_scl[lvl][a] + 0.5;
       f = P.borders_filled ? npclip(f, 0.0, m + 1.0) : npclip(f, 1.0, m);
-      long long fi = (long long)floor(f);
+      int fi = (int)floor(f);
       fi = fi < 0 ? 0 : (fi > P.g.brick[a] ? P.g.brick[a] : fi);
-      i0[a] = (int)fi;
+      i0[a] = fi;
       w1[a] = npclip(f - (double)fi, 0.0, 1.0);
       w0[a] = 1.0 - w1[a];
     }
-    const int sx = P.g.stored[0], sy = P.g.stored[1], C = P.g.C;
-    const int64_t sxC = (int64_t)sx * C, sxyC = (int64_t)sx * sy * C;
-    const T* p = b + i0[2] * sxyC + i0[1] * sxC + (int64_t)i0[0] * C + c;
-    double v = 0.0;
+    constexpr int C = NC;
+    const int64_t sxC = (int64_t)P.g.stored[0] * C, sxyC = sxC * P.g.stored[1];
+    const T* p = bb + slot * P.g.brick_elems + i0[2] * sxyC + i0[1] * sxC + (int64_t)i0[0] * C;
+    // the 8 weight products in the reference's order: (wz * wy) * wx
+    double w[8];
 #pragma unroll
-    for (int dz = 0; dz < 2; ++dz) {
-      double wz = dz ? w1[2] : w0[2];
+    for (int dz = 0; dz < 2; ++dz)
 #pragma unroll
-      for (int dy = 0; dy < 2; ++dy) {
-        double wy = dy ? w1[1] : w0[1];
+      for (int dy = 0; dy < 2; ++dy)
 #pragma unroll
-        for (int dx = 0; dx < 2; ++dx) {
-          double wx = dx ? w1[0] : w0[0];
-          double corner = (double)__ldg(p + dz * sxyC + dy * sxC + dx * C);
-          v = v + wz * wy * wx * corner;
-        }
+        for (int dx = 0; dx < 2; ++dx)
+          w[dz * 4 + dy * 2 + dx] = ((dz ? w1[2] : w0[2]) * (dy ? w1[1] : w0[1])) *
+                                    (dx ? w1[0] : w0[0]);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      if (c < c0 || c >= c1) continue;
+      double v = 0.0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int dz = q >> 2, dy = (q >> 1) & 1, dx = q & 1;
+        const double corner = (double)__ldg(p + dz * sxyC + dy * sxC + dx * C + c);
+        v = v + w[q] * corner;
       }
+      out[c] = v;
     }
-    return v;
   }
 
-  // raycast.py:86-123 with a per-channel-group descent cache
+  // raycast.py:86-123 with a per-channel-group descent cache: a sample that
+  // stays inside the cached node box at the same target level reuses it
   __device__ void descend(const double pv[3], int target, DescentCache& dc) {
     if (dc.target == target) {
       bool ok = true;
+#pragma unroll
       for (int a = 0; a < 3; ++a)
         if (P.g.split[a] && !(pv[a] >= dc.lo[a] && pv[a] < dc.lo[a] + P.ext[dc.lvl][a])) ok = false;
       if (ok) return;
@@ -256,6 +297,7 @@ struct Sampler {
       if (!(ptr != 0 && lvl > target)) break;
       int k = 0;
       double nlo[3];
+#pragma unroll
       for (int a = 0; a < 3; ++a) {
         double half = P.ext[lvl - 1][a];
         bool bit = (pv[a] >= lo[a] + half) && P.g.split[a];
@@ -264,9 +306,11 @@ struct Sampler {
       }
       a2 = a1;
       a2l = a1l;
+#pragma unroll
       for (int a = 0; a < 3; ++a) a2lo[a] = a1lo[a];
       a1 = idx;
       a1l = lvl;
+#pragma unroll
       for (int a = 0; a < 3; ++a) {
         a1lo[a] = lo[a];
         lo[a] = nlo[a];
@@ -277,6 +321,7 @@ struct Sampler {
     dc.target = target;
     dc.idx = idx;
     dc.lvl = lvl;
+#pragma unroll
     for (int a = 0; a < 3; ++a) {
       dc.lo[a] = lo[a];
       dc.a_lo[0][a] = a1lo[a];
@@ -288,15 +333,17 @@ struct Sampler {
     dc.a_lvl[1] = a2l;
   }
 
-  // optimal_lod (raycast.py:40-50)
+  // optimal_lod (raycast.py:40-50): floor(log2(.)) is the exponent of the
+  // positive normal footprint ratio (no transcendental per sample)
   __device__ int lod(const double p[3]) const {
     double z = (p[0] - P.cam[0]) * P.fwd[0] + (p[1] - P.cam[1]) * P.fwd[1] +
                (p[2] - P.cam[2]) * P.fwd[2];
     double fp = fmax(z, 1e-12) * P.pfs;
     fp = fp * P.lod_scale;
-    double l = floor(log2(fmax(fp / P.base_voxel, 1e-300)));
-    l = fmin(fmax(l, 0.0), (double)P.g.depth);
-    return (int)l;
+    const double v = P.base_pow2 ? fp * P.inv_base : fp / P.base_voxel;
+    int l = v >= 2.2250738585072014e-308 ? floor_log2(v) : -1;
+    l = l < 0 ? 0 : (l > P.g.depth ? P.g.depth : l);
+    return l;
   }
 
   // _resolve + _fullframe_fallback (raycast.py:167-238) for channels [c0, c1)
@@ -306,11 +353,13 @@ struct Sampler {
     const uint64_t e = __ldg(nb + dc.idx);
     const bool resident = e & 1, nh = e & 2;
     if (!nh) {
-      for (int c = c0; c < c1; ++c) out[c] = avg_of(e, c);
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+        if (c >= c0 && c < c1) out[c] = avg_of(e, c);
       return false;
     }
     if (resident) {
-      for (int c = c0; c < c1; ++c) out[c] = trilerp(e, dc.lvl, dc.lo, pv, c);
+      trilerp(e, dc.lvl, dc.lo, pv, c0, c1, out);
       mark(dc.idx, 1);
       cnt.used++;
       return false;
@@ -318,12 +367,13 @@ struct Sampler {
     mark(dc.idx, 2);
     cnt.req++;
     if (!fullframe) return true;
+#pragma unroll
     for (int q = 0; q < 2; ++q) {
       long long ai = dc.a_idx[q];
       if (ai < 0) continue;
       uint64_t ae = __ldg(nb + ai);
       if (ae & 1) {
-        for (int c = c0; c < c1; ++c) out[c] = trilerp(ae, dc.a_lvl[q], dc.a_lo[q], pv, c);
+        trilerp(ae, dc.a_lvl[q], dc.a_lo[q], pv, c0, c1, out);
         mark(ai, 1);
         cnt.used++;
         cnt.coarse++;
@@ -334,41 +384,49 @@ struct Sampler {
         cnt.req++;
       }
     }
-    for (int c = c0; c < c1; ++c) out[c] = avg_of(e, c);
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+      if (c >= c0 && c < c1) out[c] = avg_of(e, c);
     cnt.avgfb++;
     return false;
   }
 
+  __device__ __forceinline__ void to_voxels(const double q[3], double pv[3]) const {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) pv[a] = P.unit_spacing ? q[a] : q[a] / P.spacing[a];
+  }
+
   // sampler (raycast.py:242-278); returns missing
   __device__ bool sample(const double p[3], double* vals) {
-    const int C = P.g.C;
+    constexpr int C = NC;
+#pragma unroll
     for (int c = 0; c < C; ++c) vals[c] = (double)P.g.bg;
-    if (!P.has_tr) {
+    if (!TR) {
       double pv[3];
+      to_voxels(p, pv);
       bool in = true;
-      for (int a = 0; a < 3; ++a) {
-        pv[a] = p[a] / P.spacing[a];
-        in = in && pv[a] >= 0.0 && pv[a] <= P.dims[a];
-      }
+#pragma unroll
+      for (int a = 0; a < 3; ++a) in = in && pv[a] >= 0.0 && pv[a] <= P.dims[a];
       if (!in) return false;
       int target = lod(p);
+#pragma unroll
       for (int a = 0; a < 3; ++a) pv[a] = npclip(pv[a], 0.0, P.dims[a] - 1e-9);
       return resolve(pv, target, 0, C, vals, cache[0]);
     }
     bool missing = false;
+#pragma unroll
     for (int c = 0; c < C; ++c) {
       const double* m = P.tr[c];
       double q[3], pv[3];
       bool in = true;
-      for (int r = 0; r < 3; ++r) {
+      for (int r = 0; r < 3; ++r)
         q[r] = p[0] * m[r * 4 + 0] + p[1] * m[r * 4 + 1] + p[2] * m[r * 4 + 2] + m[r * 4 + 3];
-        pv[r] = q[r] / P.spacing[r];
-        in = in && pv[r] >= 0.0 && pv[r] <= P.dims[r];
-      }
+      to_voxels(q, pv);
+      for (int r = 0; r < 3; ++r) in = in && pv[r] >= 0.0 && pv[r] <= P.dims[r];
       if (!in) continue;
       int target = lod(q);
       for (int a = 0; a < 3; ++a) pv[a] = npclip(pv[a], 0.0, P.dims[a] - 1e-9);
-      missing |= resolve(pv, target, c, c + 1, vals, cache[c]);
+      missing |= resolve(pv, target, c, c + 1, vals, cache[TR ? c : 0]);
     }
     return missing;
   }
@@ -377,32 +435,40 @@ struct Sampler {
 #undef P
 
 // composite_step (core.py:110-134); returns terminated
+template <int NC>
 __device__ bool composite(const double* vals, RayOut& o, Counters& cnt) {
   const RenderParams& P = c_P;
-  const int C = P.g.C;
+  constexpr int C = NC;
   if (P.mip) {
+#pragma unroll
     for (int c = 0; c < C; ++c) o.mip[c] = fmax(o.mip[c], vals[c]);
     return false;
   }
   double srgb[3] = {0.0, 0.0, 0.0};
   double trans = 1.0;
+#pragma unroll
   for (int c = 0; c < C; ++c) {
-    double x = vals[c] / P.fmax;
-    double alpha_tf = interp(c, 3, x);
+    const double x = vals[c] * P.inv_fmax;
+    double rgba[4];
+    interp4(c, x, rgba);
     cnt.tf++;
-    double alpha = 1.0 - (P.corr == 1.0 ? (1.0 - alpha_tf) : pow(1.0 - alpha_tf, P.corr));
-    for (int a = 0; a < 3; ++a) srgb[a] = srgb[a] + interp(c, a, x) * alpha;
+    const double alpha = 1.0 - (P.corr == 1.0 ? (1.0 - rgba[3]) : pow(1.0 - rgba[3], P.corr));
+#pragma unroll
+    for (int a = 0; a < 3; ++a) srgb[a] = srgb[a] + rgba[a] * alpha;
     trans = trans * (1.0 - alpha);
   }
+#pragma unroll
   for (int a = 0; a < 3; ++a) srgb[a] = npclip(srgb[a], 0.0, 1.0);
-  double sa = 1.0 - trans;
-  double w = 1.0 - o.a;
+  const double sa = 1.0 - trans;
+  const double w = 1.0 - o.a;
+#pragma unroll
   for (int a = 0; a < 3; ++a) o.rgb[a] = o.rgb[a] + w * srgb[a];
   o.a = o.a + w * sa;
   return P.has_et && o.a >= P.et;
 }
 
 // finalize_image (core.py:137-155)
+template <int NC>
 __device__ void finalize(const RayOut& o, double px[4], Counters& cnt) {
   const RenderParams& P = c_P;
   if (!P.mip) {
@@ -413,12 +479,14 @@ __device__ void finalize(const RayOut& o, double px[4], Counters& cnt) {
     return;
   }
   double rgb[3] = {0, 0, 0}, trans = 1.0;
-  for (int c = 0; c < P.g.C; ++c) {
-    double x = o.mip[c] / P.fmax;
-    double al = interp(c, 3, x);
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const double x = o.mip[c] * P.inv_fmax;
+    double rgba[4];
+    interp4(c, x, rgba);
     cnt.tf++;
-    for (int a = 0; a < 3; ++a) rgb[a] = rgb[a] + interp(c, a, x) * al;
-    trans = trans * (1.0 - al);
+    for (int a = 0; a < 3; ++a) rgb[a] = rgb[a] + rgba[a] * rgba[3];
+    trans = trans * (1.0 - rgba[3]);
   }
   for (int a = 0; a < 3; ++a) px[a] = npclip(rgb[a], 0.0, 1.0);
   px[3] = 1.0 - trans;
@@ -466,14 +534,15 @@ __device__ void store_px(void* out, int kind, int64_t r, const double px[4]) {
 }
 
 // fused full-frame pass: ray setup + march + finalize, no per-ray state
-template <class T>
+template <class T, int NC, bool TR>
 __global__ void __launch_bounds__(128) k_render_fullframe(const uint64_t* __restrict__ nb,
                                                           uint8_t* fb, const T* __restrict__ bb,
                                                           void* out, int out_kind, int out_w,
                                                           int out_rows,
                                                           unsigned long long* counters) {
   const RenderParams& P = c_P;
-  Counters cnt{0, 0, 0, 0, 0, 0};
+  Sampler<T, NC, TR> s(nb, fb, bb, true);
+  Counters& cnt = s.cnt;
   int i, j, jl;
   bool active = pixel_of(i, j, jl);
   if (active) {
@@ -483,18 +552,18 @@ __global__ void __launch_bounds__(128) k_render_fullframe(const uint64_t* __rest
     long long n;
     ray_setup(d, t0, n);
     RayOut o{};
-    Sampler<T> s(nb, fb, bb, true, cnt);
-    double vals[kMaxC];
+    double vals[NC];
     for (long long k = 0; k < n; ++k) {
       double t = t0 + (double)k * P.step;
       double p[3];
+#pragma unroll
       for (int a = 0; a < 3; ++a) p[a] = P.cam[a] + t * d[a];
       s.sample(p, vals);
       cnt.samples++;
-      if (composite(vals, o, cnt)) break;
+      if (composite<NC>(vals, o, cnt)) break;
     }
     double px[4];
-    finalize(o, px, cnt);
+    finalize<NC>(o, px, cnt);
     store_px<T>(out, out_kind, (int64_t)jl * out_w + (i - P.rect[0]), px);
   } else if (P.n_parts > 1 && i < P.rect[2] && jl < out_rows) {
     // padding rows of the last strip: deterministic zeros
@@ -536,14 +605,15 @@ __global__ void k_rays_init(RayState S) {
   }
 }
 
-template <class T>
+template <class T, int NC, bool TR>
 __global__ void __launch_bounds__(128) k_rays_march(RayState S,
                                                     const uint64_t* __restrict__ nb, uint8_t* fb,
                                                     const T* __restrict__ bb, int fullframe,
                                                     unsigned long long* counters,
                                                     unsigned long long* n_susp) {
   const RenderParams& P = c_P;
-  Counters cnt{0, 0, 0, 0, 0, 0};
+  Sampler<T, NC, TR> s(nb, fb, bb, fullframe != 0);
+  Counters& cnt = s.cnt;
   int i, j, jl;
   // stateful passes cover the whole frame; rect = full
   bool active = pixel_of(i, j, jl);
@@ -559,9 +629,9 @@ __global__ void __launch_bounds__(128) k_rays_march(RayState S,
       RayOut o;
       for (int a = 0; a < 3; ++a) o.rgb[a] = S.acc[r * 4 + a];
       o.a = S.acc[r * 4 + 3];
+#pragma unroll
       for (int c = 0; c < kMaxC; ++c) o.mip[c] = S.mip[r * 4 + c];
-      Sampler<T> s(nb, fb, bb, fullframe != 0, cnt);
-      double vals[kMaxC];
+      double vals[NC];
       const double t0 = S.t0[r];
       for (; k < n; ++k) {
         double t = t0 + (double)k * P.step;
@@ -574,7 +644,7 @@ __global__ void __launch_bounds__(128) k_rays_march(RayState S,
           fl |= 1;
           break;
         }
-        bool term = composite(vals, o, cnt);
+        bool term = composite<NC>(vals, o, cnt);
         if (term) {
           fl |= 2;
           ++k;
@@ -593,6 +663,7 @@ __global__ void __launch_bounds__(128) k_rays_march(RayState S,
   if ((threadIdx.x & 31) == 0 && b) atomicAdd(n_susp, (unsigned long long)__popc(b));
 }
 
+template <int NC>
 __global__ void k_rays_image(RayState S, double* out,
                              unsigned long long* counters) {
   const RenderParams& P = c_P;
@@ -604,7 +675,7 @@ __global__ void k_rays_image(RayState S, double* out,
     o.a = S.acc[i * 4 + 3];
     for (int c = 0; c < kMaxC; ++c) o.mip[c] = S.mip[i * 4 + c];
     double px[4];
-    finalize(o, px, cnt);
+    finalize<NC>(o, px, cnt);
     for (int a = 0; a < 4; ++a) out[(int64_t)i * 4 + a] = px[a];
   }
   warp_add_counters(cnt, counters);
@@ -669,6 +740,25 @@ __global__ void k_upload(const int32_t* __restrict__ src_slots, const int32_t* _
 // the parameter upload until their kernels have completed
 std::mutex g_render_mu;
 
+// kernel instantiation for (sample type, channel count, transforms)
+template <class F>
+void dispatch(int sb, int C, bool tr, F&& f) {
+  auto by_c = [&](auto tag, auto trc) {
+    switch (C) {
+      case 1: f(tag, std::integral_constant<int, 1>{}, trc); break;
+      case 2: f(tag, std::integral_constant<int, 2>{}, trc); break;
+      case 3: f(tag, std::integral_constant<int, 3>{}, trc); break;
+      default: f(tag, std::integral_constant<int, 4>{}, trc); break;
+    }
+  };
+  auto by_tr = [&](auto tag) {
+    if (tr) by_c(tag, std::true_type{});
+    else by_c(tag, std::false_type{});
+  };
+  if (sb == 1) by_tr(uint8_t{});
+  else by_tr(uint16_t{});
+}
+
 // rows of one part's compact output: ceil(strips / n_parts) whole strips
 int strip_part_rows(int H, int strip_rows, int n_parts) {
   if (n_parts <= 1) return H;
@@ -700,6 +790,16 @@ void fill_params(const vt_mirror* m, const vt_scene* s, RenderParams& P) {
     if (!any_split || t.g.split[a]) bv = std::min(bv, s->spacing[a]);
   P.base_voxel = bv;
   P.fmax = (double)t.fmax;
+  P.inv_fmax = 1.0 / P.fmax;
+  for (int l = 0; l <= t.g.depth; ++l)
+    for (int a = 0; a < 3; ++a) P.inv_scl[l][a] = 1.0 / P.scl[l][a];
+  P.unit_spacing = s->spacing[0] == 1.0 && s->spacing[1] == 1.0 && s->spacing[2] == 1.0;
+  {
+    int ex = 0;
+    const double mant = std::frexp(bv, &ex);
+    P.base_pow2 = (std::isfinite(bv) && mant == 0.5) ? 1 : 0;
+    P.inv_base = P.base_pow2 ? 1.0 / bv : 0.0;
+  }
   P.avg_w = 40 / t.g.C;
   P.qmax = (double)((1LL << P.avg_w) - 1);
   P.borders_filled = t.borders ? 1 : 0;
@@ -730,6 +830,10 @@ void fill_params(const vt_mirror* m, const vt_scene* s, RenderParams& P) {
       P.tf_x[c][q] = s->tf_x[c][q];
       for (int a = 0; a < 4; ++a) P.tf_v[c][q][a] = s->tf_rgba[c][q][a];
     }
+    // np.interp's slope, (fp[j+1] - fp[j]) / (xp[j+1] - xp[j]), in FP64
+    for (int q = 0; q + 1 < P.tf_n[c]; ++q)
+      for (int a = 0; a < 4; ++a)
+        P.tf_s[c][q][a] = (P.tf_v[c][q + 1][a] - P.tf_v[c][q][a]) / (P.tf_x[c][q + 1] - P.tf_x[c][q]);
   }
   P.n_clips = s->n_clips;
   VT_REQUIRE(P.n_clips >= 0 && P.n_clips <= 3, VT_EINVAL, "at most 3 clip planes supported");
@@ -932,12 +1036,11 @@ static void render_rect(vt_mirror* m, const vt_scene* scene, const int32_t* rect
   VT_CUDA(cudaEventRecord(t.ev0, t.stream));
   set_params(P, t.stream);
   if (px > 0) {
-    if (t.g.sb == 1)
-      k_render_fullframe<uint8_t><<<grid, 128, 0, t.stream>>>(
-          m->d_nb, m->d_fb, (const uint8_t*)brick_ptr(m), dout, out_kind, rw, rh, dc);
-    else
-      k_render_fullframe<uint16_t><<<grid, 128, 0, t.stream>>>(
-          m->d_nb, m->d_fb, (const uint16_t*)brick_ptr(m), dout, out_kind, rw, rh, dc);
+    dispatch(t.g.sb, t.g.C, P.has_tr != 0, [&](auto tag, auto nc, auto tr) {
+      using T = decltype(tag);
+      k_render_fullframe<T, decltype(nc)::value, decltype(tr)::value><<<grid, 128, 0, t.stream>>>(
+          m->d_nb, m->d_fb, (const T*)brick_ptr(m), dout, out_kind, rw, rh, dc);
+    });
     VT_CUDA(cudaGetLastError());
   }
   VT_CUDA(cudaEventRecord(t.ev1, t.stream));
@@ -1036,14 +1139,11 @@ vt_status vt_rays_march(vt_rays* r, int32_t strategy, vt_counters* cnt, int64_t*
     VT_CUDA(cudaMemsetAsync(dc, 0, 7 * sizeof(unsigned long long), t.stream));
     dim3 grid((P.W + 7) / 8, (P.H + 15) / 16);
     set_params(P, t.stream);
-    if (t.g.sb == 1)
-      k_rays_march<uint8_t><<<grid, 128, 0, t.stream>>>(r->S, m->d_nb, m->d_fb,
-                                                        (const uint8_t*)brick_ptr(m),
-                                                        strategy == 0, dc, dc + 6);
-    else
-      k_rays_march<uint16_t><<<grid, 128, 0, t.stream>>>(r->S, m->d_nb, m->d_fb,
-                                                         (const uint16_t*)brick_ptr(m),
-                                                         strategy == 0, dc, dc + 6);
+    dispatch(t.g.sb, t.g.C, P.has_tr != 0, [&](auto tag, auto nc, auto tr) {
+      using T = decltype(tag);
+      k_rays_march<T, decltype(nc)::value, decltype(tr)::value><<<grid, 128, 0, t.stream>>>(
+          r->S, m->d_nb, m->d_fb, (const T*)brick_ptr(m), strategy == 0, dc, dc + 6);
+    });
     VT_CUDA(cudaGetLastError());
     unsigned long long h[7];
     VT_CUDA(cudaMemcpyAsync(h, dc, sizeof(h), cudaMemcpyDeviceToHost, t.stream));
@@ -1065,7 +1165,10 @@ vt_status vt_rays_image(vt_rays* r, double* out_host, vt_counters* cnt) {
     VT_CUDA(cudaMallocAsync(&dc, 6 * sizeof(unsigned long long), t.stream));
     VT_CUDA(cudaMemsetAsync(dc, 0, 6 * sizeof(unsigned long long), t.stream));
     set_params(r->P, t.stream);
-    k_rays_image<<<(unsigned)((n + 127) / 128), 128, 0, t.stream>>>(r->S, dout, dc);
+    dispatch(2, t.g.C, false, [&](auto, auto nc, auto) {
+      k_rays_image<decltype(nc)::value><<<(unsigned)((n + 127) / 128), 128, 0, t.stream>>>(
+          r->S, dout, dc);
+    });
     VT_CUDA(cudaGetLastError());
     unsigned long long h[6];
     VT_CUDA(cudaMemcpyAsync(out_host, dout, r->n * 32, cudaMemcpyDeviceToHost, t.stream));
