@@ -92,10 +92,33 @@ __device__ __forceinline__ double clampd(double v, double lo, double hi) {
   return fmin(fmax(v, lo), hi);
 }
 
-// np.clip(a, lo, hi) == minimum(maximum(a, lo), hi)
+// np.clip(a, lo, hi) == minimum(maximum(a, lo), hi) for non-NaN a (every
+// clipped quantity on the sampling path is finite)
 __device__ __forceinline__ double npclip(double v, double lo, double hi) {
-  double m = v > lo ? v : (v != v ? v : lo);
-  return m < hi ? m : (m != m ? m : hi);
+  return fmin(fmax(v, lo), hi);
+}
+
+// transfer-function tables staged in shared memory per block: lanes index
+// different segments, which the constant cache would serialise
+struct TFTable {
+  double x[kMaxC][VT_MAX_TF_POINTS];
+  double v[kMaxC][VT_MAX_TF_POINTS][4];
+  double s[kMaxC][VT_MAX_TF_POINTS][4];
+  int n[kMaxC];
+};
+
+__device__ void load_tf(TFTable& T) {
+  const RenderParams& P = c_P;
+  const double* src_x = &P.tf_x[0][0];
+  const double* src_v = &P.tf_v[0][0][0];
+  const double* src_s = &P.tf_s[0][0][0];
+  for (int e = threadIdx.x; e < kMaxC * VT_MAX_TF_POINTS; e += blockDim.x) (&T.x[0][0])[e] = src_x[e];
+  for (int e = threadIdx.x; e < kMaxC * VT_MAX_TF_POINTS * 4; e += blockDim.x) {
+    (&T.v[0][0][0])[e] = src_v[e];
+    (&T.s[0][0][0])[e] = src_s[e];
+  }
+  if (threadIdx.x < kMaxC) T.n[threadIdx.x] = P.tf_n[threadIdx.x];
+  __syncthreads();
 }
 
 // camera.py:41-53
@@ -150,18 +173,17 @@ __device__ void ray_setup(const double d[3], double& t0o, long long& n) {
 // components from one segment search.  Segment slopes are precomputed on
 // the host in FP64 with the same operation numpy uses, so every result is
 // bit-identical to numpy's: slope * (x - xp[j]) + fp[j].
-__device__ __forceinline__ void interp4(int c, double x, double out[4]) {
-  const RenderParams& P = c_P;
-  const int n = P.tf_n[c];
-  const double* xp = P.tf_x[c];
+__device__ __forceinline__ void interp4(const TFTable& T, int c, double x, double out[4]) {
+  const int n = T.n[c];
+  const double* xp = T.x[c];
   if (!(x >= xp[0])) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) out[q] = x != x ? x : P.tf_v[c][0][q];
+    for (int q = 0; q < 4; ++q) out[q] = x != x ? x : T.v[c][0][q];
     return;
   }
   if (x >= xp[n - 1]) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) out[q] = P.tf_v[c][n - 1][q];
+    for (int q = 0; q < 4; ++q) out[q] = T.v[c][n - 1][q];
     return;
   }
   int j = 0;
@@ -170,11 +192,11 @@ __device__ __forceinline__ void interp4(int c, double x, double out[4]) {
   const bool exact = x == xp[j];  // numpy returns fp[j] on an exact knot
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    const double y0 = P.tf_v[c][j][q];
-    double r = exact ? y0 : P.tf_s[c][j][q] * dx + y0;
+    const double y0 = T.v[c][j][q];
+    double r = exact ? y0 : T.s[c][j][q] * dx + y0;
     if (r != r) {
-      const double y1 = P.tf_v[c][j + 1][q];
-      r = P.tf_s[c][j][q] * (x - xp[j + 1]) + y1;
+      const double y1 = T.v[c][j + 1][q];
+      r = T.s[c][j][q] * (x - xp[j + 1]) + y1;
       if (r != r && y0 == y1) r = y0;
     }
     out[q] = r;
@@ -436,7 +458,7 @@ struct Sampler {
 
 // composite_step (core.py:110-134); returns terminated
 template <int NC>
-__device__ bool composite(const double* vals, RayOut& o, Counters& cnt) {
+__device__ bool composite(const TFTable& T, const double* vals, RayOut& o, Counters& cnt) {
   const RenderParams& P = c_P;
   constexpr int C = NC;
   if (P.mip) {
@@ -450,7 +472,7 @@ __device__ bool composite(const double* vals, RayOut& o, Counters& cnt) {
   for (int c = 0; c < C; ++c) {
     const double x = vals[c] * P.inv_fmax;
     double rgba[4];
-    interp4(c, x, rgba);
+    interp4(T, c, x, rgba);
     cnt.tf++;
     const double alpha = 1.0 - (P.corr == 1.0 ? (1.0 - rgba[3]) : pow(1.0 - rgba[3], P.corr));
 #pragma unroll
@@ -469,7 +491,7 @@ __device__ bool composite(const double* vals, RayOut& o, Counters& cnt) {
 
 // finalize_image (core.py:137-155)
 template <int NC>
-__device__ void finalize(const RayOut& o, double px[4], Counters& cnt) {
+__device__ void finalize(const TFTable& T, const RayOut& o, double px[4], Counters& cnt) {
   const RenderParams& P = c_P;
   if (!P.mip) {
     px[0] = o.rgb[0];
@@ -483,7 +505,7 @@ __device__ void finalize(const RayOut& o, double px[4], Counters& cnt) {
   for (int c = 0; c < NC; ++c) {
     const double x = o.mip[c] * P.inv_fmax;
     double rgba[4];
-    interp4(c, x, rgba);
+    interp4(T, c, x, rgba);
     cnt.tf++;
     for (int a = 0; a < 3; ++a) rgb[a] = rgb[a] + rgba[a] * rgba[3];
     trans = trans * (1.0 - rgba[3]);
@@ -534,13 +556,18 @@ __device__ void store_px(void* out, int kind, int64_t r, const double px[4]) {
 }
 
 // fused full-frame pass: ray setup + march + finalize, no per-ray state
+#ifndef VT_RENDER_MINB
+#define VT_RENDER_MINB 4
+#endif
 template <class T, int NC, bool TR>
-__global__ void __launch_bounds__(128) k_render_fullframe(const uint64_t* __restrict__ nb,
+__global__ void __launch_bounds__(128, VT_RENDER_MINB) k_render_fullframe(const uint64_t* __restrict__ nb,
                                                           uint8_t* fb, const T* __restrict__ bb,
                                                           void* out, int out_kind, int out_w,
                                                           int out_rows,
                                                           unsigned long long* counters) {
   const RenderParams& P = c_P;
+  __shared__ TFTable tf;
+  load_tf(tf);
   Sampler<T, NC, TR> s(nb, fb, bb, true);
   Counters& cnt = s.cnt;
   int i, j, jl;
@@ -560,10 +587,10 @@ __global__ void __launch_bounds__(128) k_render_fullframe(const uint64_t* __rest
       for (int a = 0; a < 3; ++a) p[a] = P.cam[a] + t * d[a];
       s.sample(p, vals);
       cnt.samples++;
-      if (composite<NC>(vals, o, cnt)) break;
+      if (composite<NC>(tf, vals, o, cnt)) break;
     }
     double px[4];
-    finalize<NC>(o, px, cnt);
+    finalize<NC>(tf, o, px, cnt);
     store_px<T>(out, out_kind, (int64_t)jl * out_w + (i - P.rect[0]), px);
   } else if (P.n_parts > 1 && i < P.rect[2] && jl < out_rows) {
     // padding rows of the last strip: deterministic zeros
@@ -612,6 +639,8 @@ __global__ void __launch_bounds__(128) k_rays_march(RayState S,
                                                     unsigned long long* counters,
                                                     unsigned long long* n_susp) {
   const RenderParams& P = c_P;
+  __shared__ TFTable tf;
+  load_tf(tf);
   Sampler<T, NC, TR> s(nb, fb, bb, fullframe != 0);
   Counters& cnt = s.cnt;
   int i, j, jl;
@@ -644,7 +673,7 @@ __global__ void __launch_bounds__(128) k_rays_march(RayState S,
           fl |= 1;
           break;
         }
-        bool term = composite<NC>(vals, o, cnt);
+        bool term = composite<NC>(tf, vals, o, cnt);
         if (term) {
           fl |= 2;
           ++k;
@@ -667,6 +696,8 @@ template <int NC>
 __global__ void k_rays_image(RayState S, double* out,
                              unsigned long long* counters) {
   const RenderParams& P = c_P;
+  __shared__ TFTable tf;
+  load_tf(tf);
   Counters cnt{0, 0, 0, 0, 0, 0};
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < P.W * P.H) {
@@ -675,7 +706,7 @@ __global__ void k_rays_image(RayState S, double* out,
     o.a = S.acc[i * 4 + 3];
     for (int c = 0; c < kMaxC; ++c) o.mip[c] = S.mip[i * 4 + c];
     double px[4];
-    finalize<NC>(o, px, cnt);
+    finalize<NC>(tf, o, px, cnt);
     for (int a = 0; a < 4; ++a) out[(int64_t)i * 4 + a] = px[a];
   }
   warp_add_counters(cnt, counters);
