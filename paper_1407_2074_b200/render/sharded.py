@@ -73,14 +73,15 @@ class SortFirstRenderer:
         self.root = int(root)
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
-        self.descriptor = device.octree.descriptor
+        self.descriptor = device.octree.descriptor if device is not None else None
         self._bufs = {}
 
-    def _buffer(self, key, shape, dtype):
+    def _buffer(self, key, shape, dtype, device="cuda"):
         import torch
         b = self._bufs.get(key)
-        if b is None or tuple(b.shape) != tuple(shape) or b.dtype != dtype:
-            b = torch.empty(shape, dtype=dtype, device="cuda")
+        if (b is None or tuple(b.shape) != tuple(shape) or b.dtype != dtype
+                or b.device != torch.device(device)):
+            b = torch.empty(shape, dtype=dtype, device=device)
             self._bufs[key] = b
         return b
 
@@ -107,7 +108,8 @@ class SortFirstRenderer:
             return local
         parts = None
         if self.rank == self.root:
-            parts = self._buffer("parts", (self.world,) + tuple(local.shape), local.dtype)
+            parts = self._buffer("parts", (self.world,) + tuple(local.shape), local.dtype,
+                                 local.device)
             plist = list(parts.unbind(0))
         dist.gather(local, plist if self.rank == self.root else None, dst=self.root,
                     group=self.group)

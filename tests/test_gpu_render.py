@@ -164,3 +164,35 @@ def test_rgba8_output_matches_image_to_rgba8():
     f64, _ = r.render_fullframe(scene)
     u8, _ = r.render_fullframe(scene, out_kind=OUT_RGBA8)
     assert np.array_equal(u8, image_to_rgba8(f64))
+
+
+@pytest.mark.parametrize("G,strip", [(2, 8), (3, 4), (8, 8)])
+def test_strip_partition_equals_fullframe(G, strip):
+    """sort-first strips (vt_render_strips) of G parts re-interleaved on the
+    host == the single-GPU full frame; counters sum to the full frame's."""
+    import ctypes as ct
+    import torch
+    from paper_1407_2074_b200 import DeviceState, _lib
+    from paper_1407_2074_b200.render import OutOfCoreRenderer
+    from paper_1407_2074_b200.render.raycast import OUT_F64, scene_to_vt
+    from paper_1407_2074_b200.render.sharded import assemble, part_rows
+    rc = scenarios.render_case("spim_u8_dvr")
+    _, tree, _ = build_scenario(rc["build"], borders=True)
+    dev = DeviceState(tree, resident_all=True)
+    scene = to_scene(rc["scene"])
+    full, fcnt = OutOfCoreRenderer(dev).render_fullframe(scene)
+    H, W = full.shape[:2]
+    rows = part_rows(H, strip, G)
+    assert _lib.lib().vt_strip_part_rows(H, strip, G) == rows
+    parts, total = [], 0
+    for p in range(G):
+        buf = torch.full((rows, W, 4), -1.0, dtype=torch.float64, device="cuda")
+        cnt = _lib.vt_counters()
+        s = scene_to_vt(scene, tree.descriptor)
+        _lib.call("vt_render_strips", dev.handle, ct.byref(s), strip, G, p,
+                  ct.c_void_p(buf.data_ptr()), OUT_F64, 1, ct.byref(cnt))
+        parts.append(buf)
+        total += cnt.samples
+    img = assemble(torch.stack(parts), H, strip).cpu().numpy()
+    assert np.array_equal(img, full)
+    assert total == fcnt.samples
