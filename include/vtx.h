@@ -115,6 +115,8 @@ vt_status vt_tree_insert_channels(vt_tree* tree, const int32_t origin[3],
  * *n returns the number written (<= cap); call again while *more != 0 */
 vt_status vt_tree_take_events(vt_tree* tree, int32_t* kinds, int64_t* indices, int64_t cap,
                               int64_t* n, int32_t* more);
+/* number of pending change events (size the take_events buffers) */
+vt_status vt_tree_event_count(vt_tree* tree, int64_t* n);
 /* Octree.finalize / fill_borders (octree.py:536-614) */
 vt_status vt_tree_finalize(vt_tree* tree);
 vt_status vt_tree_fill_borders(vt_tree* tree);

@@ -153,6 +153,10 @@ vt_status vt_tree_take_events(vt_tree* tree, int32_t* kinds, int64_t* indices, i
   });
 }
 
+vt_status vt_tree_event_count(vt_tree* tree, int64_t* n) {
+  return guarded([&] { *n = (int64_t)tree->t.events.size(); });
+}
+
 vt_status vt_tree_finalize(vt_tree* tree) {
   return guarded([&] { tree->t.finished = true; });
 }

@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import ctypes as ct
 import threading
+from collections.abc import Sequence
 from dataclasses import dataclass
 from enum import IntEnum
 
@@ -70,6 +71,50 @@ def classify_homogeneous(smin, smax, threshold: float):
     (octree.py:95-99)."""
     per = [(hi - lo) < threshold for lo, hi in zip(smin, smax)]
     return per, all(per)
+
+
+class EventBatch(Sequence):
+    """The change events of one or more insertions, in order: a read-only
+    sequence of ChangeEvent (what insert_block / drain_events return in the
+    reference, octree.py:180-183, 393-395) backed by two arrays, so a slab
+    that creates and updates thousands of nodes costs no Python objects
+    until a caller indexes it.  ``kinds`` / ``indices`` expose the arrays."""
+
+    __slots__ = ("kinds", "indices")
+
+    def __init__(self, kinds, indices):
+        self.kinds = np.asarray(kinds, np.int32)
+        self.indices = np.asarray(indices, np.int64)
+
+    @staticmethod
+    def concat(batches) -> "EventBatch":
+        batches = list(batches)
+        if not batches:
+            return EventBatch(np.empty(0, np.int32), np.empty(0, np.int64))
+        if len(batches) == 1:
+            return batches[0]
+        return EventBatch(np.concatenate([b.kinds for b in batches]),
+                          np.concatenate([b.indices for b in batches]))
+
+    def __len__(self):
+        return len(self.kinds)
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return EventBatch(self.kinds[i], self.indices[i])
+        return ChangeEvent(ChangeKind(int(self.kinds[i])), int(self.indices[i]))
+
+    def __eq__(self, other):
+        if isinstance(other, EventBatch):
+            return (np.array_equal(self.kinds, other.kinds)
+                    and np.array_equal(self.indices, other.indices))
+        try:
+            return list(self) == list(other)
+        except TypeError:
+            return NotImplemented
+
+    def __repr__(self):
+        return f"EventBatch({len(self)} events)"
 
 
 class OctreeNode:
@@ -153,7 +198,7 @@ class Octree:
         self.geometry = TreeGeometry.build(desc, cfg)
         self.threshold = cfg.resolve_threshold(desc)
         self.lock = threading.RLock()
-        self._events: list[ChangeEvent] = []
+        self._events: list[EventBatch] = []
         self._closed = False
         d = _lib.vt_tree_desc()
         d.dims[:] = list(desc.dims)
@@ -193,28 +238,28 @@ class Octree:
         return self._h
 
     # -- events --------------------------------------------------------------
-    def _collect(self) -> list[ChangeEvent]:
-        out = []
-        cap = 1 << 16
-        kinds = np.empty(cap, np.int32)
-        idx = np.empty(cap, np.int64)
-        n, more = ct.c_int64(), ct.c_int32(1)
-        while more.value:
+    def _collect(self) -> "EventBatch":
+        n = ct.c_int64()
+        _lib.call("vt_tree_event_count", self._h, ct.byref(n))
+        kinds = np.empty(n.value, np.int32)
+        idx = np.empty(n.value, np.int64)
+        if n.value:
+            got, more = ct.c_int64(), ct.c_int32()
             _lib.call("vt_tree_take_events", self._h, _lib.ptr(kinds, ct.c_int32),
-                      _lib.ptr(idx, ct.c_int64), cap, ct.byref(n), ct.byref(more))
-            out.extend(ChangeEvent(ChangeKind(int(k)), int(i))
-                       for k, i in zip(kinds[:n.value], idx[:n.value]))
-        self._events.extend(out)
+                      _lib.ptr(idx, ct.c_int64), n.value, ct.byref(got), ct.byref(more))
+        out = EventBatch(kinds, idx)
+        if len(out):
+            self._events.append(out)
         return out
 
-    def drain_events(self) -> list[ChangeEvent]:
+    def drain_events(self) -> "EventBatch":
         with self.lock:
             self._collect()
-            ev, self._events = self._events, []
+            ev, self._events = EventBatch.concat(self._events), []
             return ev
 
     # -- insertion -------------------------------------------------------------
-    def insert_block(self, channel: int, origin, values) -> list[ChangeEvent]:
+    def insert_block(self, channel: int, origin, values) -> EventBatch:
         """Octree.insert_block (octree.py:323-397).  ``values`` (dz, dy, dx)
         numpy array (host) or a CUDA tensor/array exposing
         ``__cuda_array_interface__`` (device, stream-ordered)."""
@@ -233,7 +278,7 @@ class Octree:
             del keep
             return self._collect()
 
-    def insert_channels(self, origin, values) -> list[ChangeEvent]:
+    def insert_channels(self, origin, values) -> EventBatch:
         """All channels at once: values (dz, dy, dx, C) interleaved; same
         tree and events as C successive insert_block calls."""
         desc = self.descriptor
