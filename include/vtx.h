@@ -102,6 +102,10 @@ vt_status vt_tree_destroy(vt_tree* tree);
 /* order all device work on a caller stream (cudaStream_t as void*) */
 vt_status vt_tree_set_stream(vt_tree* tree, void* stream);
 
+/* order the tree's device work after everything already queued on
+ * `stream` (e.g. the producer of a device-resident block), without a host
+ * synchronisation */
+vt_status vt_tree_wait_stream(vt_tree* tree, void* stream);
 /* Octree.insert_block (octree.py:323-397): one channel, values (dz,dy,dx)
  * x-fastest.  Errors exactly as octree.py:331-341 (VT_EINVAL). */
 vt_status vt_tree_insert(vt_tree* tree, int32_t channel, const int32_t origin[3],

@@ -153,6 +153,16 @@ vt_status vt_tree_take_events(vt_tree* tree, int32_t* kinds, int64_t* indices, i
   });
 }
 
+vt_status vt_tree_wait_stream(vt_tree* tree, void* stream) {
+  return guarded([&] {
+    Tree& t = tree->t;
+    if ((cudaStream_t)stream == t.stream) return;
+    if (!t.ev_wait) VT_CUDA(cudaEventCreateWithFlags(&t.ev_wait, cudaEventDisableTiming));
+    VT_CUDA(cudaEventRecord(t.ev_wait, (cudaStream_t)stream));
+    VT_CUDA(cudaStreamWaitEvent(t.stream, t.ev_wait, 0));
+  });
+}
+
 vt_status vt_tree_event_count(vt_tree* tree, int64_t* n) {
   return guarded([&] { *n = (int64_t)tree->t.events.size(); });
 }
@@ -278,6 +288,7 @@ vt_status vt_tree_import(vt_tree* tree, int64_t n, const int64_t* indices, const
                          const int32_t* stats, const void* bricks, int32_t finished,
                          int32_t borders_filled, int64_t pruned_bricks) {
   return guarded([&] {
+    ++tree->t.data_version;
     Tree& t = tree->t;
     VT_REQUIRE(t.node_count == 1 && t.brick_count == 0, VT_ESTATE, "import into a non-empty tree");
     const int C = t.g.C;
@@ -335,8 +346,7 @@ vt_status vt_tree_import(vt_tree* tree, int64_t n, const int64_t* indices, const
       if (t.flags[i] & NF_BRICK) {
         int ce[3];
         t.node_in_extent(i, ce);
-        if (ce[0] > 0 && ce[1] > 0)
-          for (int z = 0; z < ce[2]; ++z) planes.push_back({t.slot[i], z, ce[0], ce[1]});
+        if (ce[0] > 0 && ce[1] > 0 && ce[2] > 0) planes.push_back({t.slot[i], 0, ce[2], ce[0], ce[1]});
       }
     PlaneJob* dp = upload(t, planes);
     launch_plane(t, dp, (int)planes.size());

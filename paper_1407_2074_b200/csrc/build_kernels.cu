@@ -4,6 +4,7 @@
 // All integer arithmetic reproduces voxtree bit-exactly:
 //   means (2*sum + n) // (2n)     octree.py:53-55, 82, 91
 //   homogeneity / extents         octree.py:95-99, 190-199
+#include <algorithm>
 #include <climits>
 
 #include "tree.cuh"
@@ -14,7 +15,6 @@ namespace {
 
 constexpr int kThreads = 256;
 
-__device__ __forceinline__ int div_up(int a, int b) { return (a + b - 1) / b; }
 
 __global__ void k_struct_update(const StructUpd* __restrict__ u, int n, uint8_t* flags,
                                 int32_t* slot) {
@@ -44,95 +44,221 @@ __global__ void k_create(const CreateJob* __restrict__ jobs, int n, Geo g,
 }
 
 // _ensure_brick (octree.py:225-241): bg everywhere, node AVG on the
-// in-volume interior
+// in-volume interior — except the cover box, which later work of the same
+// insertion overwrites with every channel.  One warp per stored row.
 template <class T>
-__global__ void k_seed(const SeedJob* __restrict__ jobs, Geo g, T* pool,
+__global__ void k_seed(const SeedJob* __restrict__ jobs, int n, Geo g, T* pool,
                        const int32_t* __restrict__ stats) {
-  const SeedJob j = jobs[blockIdx.y];
-  T* b = pool + (int64_t)j.slot * g.brick_elems;
-  T avg[kMaxC];
-  for (int c = 0; c < g.C; ++c) avg[c] = (T)stats[st_index(j.node, ST_AVG, c)];
-  const int sx = g.stored[0], sy = g.stored[1];
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < g.brick_elems;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    int c = (int)(e % g.C);
-    int64_t v = e / g.C;
-    int x = (int)(v % sx);
-    int y = (int)((v / sx) % sy);
-    int z = (int)(v / ((int64_t)sx * sy));
-    bool in = x >= 1 && x <= j.cext[0] && y >= 1 && y <= j.cext[1] && z >= 1 && z <= j.cext[2];
-    b[e] = in ? avg[c] : (T)g.bg;
+  const int lane = threadIdx.x & 31;
+  const int C = g.C;
+  const int sx = g.stored[0], sy = g.stored[1], sz = g.stored[2];
+  const int rowlen = sx * C;
+  // x = e / C by multiply-shift (e < 2^12, C <= 4)
+  const uint32_t inv = (65536u + (uint32_t)C - 1) / (uint32_t)C;
+  for (int job = blockIdx.x; job < n; job += gridDim.x) {
+    const SeedJob j = jobs[job];
+    T* b = pool + (int64_t)j.slot * g.brick_elems;
+    T avg[kMaxC];
+#pragma unroll
+    for (int c = 0; c < kMaxC; ++c) avg[c] = c < C ? (T)stats[st_index(j.node, ST_AVG, c)] : (T)0;
+    const T bg = (T)g.bg;
+    auto val = [&](int x, int c, bool yz_in) {
+      const bool in = yz_in && x >= 1 && x <= j.cext[0];
+      T v = bg;
+#pragma unroll
+      for (int q = 0; q < kMaxC; ++q)
+        if (in && q == c) v = avg[q];
+      return v;
+    };
+    const bool cov = j.cov_hi[0] > j.cov_lo[0] && j.cov_hi[1] > j.cov_lo[1] &&
+                     j.cov_hi[2] > j.cov_lo[2];
+    // rows outside the cover: whole rows, one warp each
+    for (int row = threadIdx.x >> 5; row < sy * sz; row += blockDim.x >> 5) {
+      const int y = row % sy, z = row / sy;
+      const bool yz_cov = cov && y >= 1 + j.cov_lo[1] && y < 1 + j.cov_hi[1] &&
+                          z >= 1 + j.cov_lo[2] && z < 1 + j.cov_hi[2];
+      if (yz_cov) continue;
+      const bool yz_in = y >= 1 && y <= j.cext[1] && z >= 1 && z <= j.cext[2];
+      T* dst = b + (int64_t)row * rowlen;
+      for (int e = lane; e < rowlen; e += 32) {
+        const int x = (int)(((uint32_t)e * inv) >> 16);
+        dst[e] = val(x, e - x * C, yz_in);
+      }
+    }
+    if (!cov) continue;
+    // covered rows: only the x ends outside the cover, one thread per row
+    const int cy = j.cov_hi[1] - j.cov_lo[1], cz = j.cov_hi[2] - j.cov_lo[2];
+    for (int r = threadIdx.x; r < cy * cz; r += blockDim.x) {
+      const int y = 1 + j.cov_lo[1] + r % cy, z = 1 + j.cov_lo[2] + r / cy;
+      const bool yz_in = y <= j.cext[1] && z <= j.cext[2];
+      T* dst = b + ((int64_t)z * sy + y) * rowlen;
+      for (int x = 0; x < 1 + j.cov_lo[0]; ++x)
+        for (int c = 0; c < C; ++c) dst[x * C + c] = val(x, c, yz_in);
+      for (int x = 1 + j.cov_hi[0]; x < sx; ++x)
+        for (int c = 0; c < C; ++c) dst[x * C + c] = val(x, c, yz_in);
+    }
   }
 }
 
-// _write_leaf (octree.py:420-442): block (dz,dy,dx[,C]) -> leaf bricks at +1
+// _write_leaf (octree.py:420-442): block (dz,dy,dx[,C]) -> leaf bricks at +1.
+// One CTA per (brick column, block z): warps over rows, lanes over the
+// contiguous samples of a row (coalesced on both sides).  When the block
+// holds every channel and covers the brick's whole in-volume plane, the CTA
+// also emits that plane's partial stats (_recompute_stats, octree.py:248-263)
+// so the plane is never re-read.
+__device__ __forceinline__ bool owns_stats(const Geo& g, int channel, int ox, int oy, int dx,
+                                           int dy, int gx, int gy) {
+  if (!(channel < 0 || g.C == 1)) return false;
+  const int bx0 = gx * g.brick[0], by0 = gy * g.brick[1];
+  const int ix1 = min(g.dims[0], bx0 + g.brick[0]), iy1 = min(g.dims[1], by0 + g.brick[1]);
+  return ox <= bx0 && ox + dx >= ix1 && oy <= by0 && oy + dy >= iy1;
+}
+
 template <class T>
-__global__ void k_scatter(const T* __restrict__ src, int channel, int src_stride, int src_off,
-                          int ox, int oy, int oz, int dx,
-                          int dy, int dz, int g0x, int g0y, int g0z, int gnx, int gny,
-                          const int32_t* __restrict__ leaf_slots, Geo g, T* pool) {
-  const int64_t rows = (int64_t)dy * dz;
-  const int mx = g.brick[0], my = g.brick[1], mz = g.brick[2];
-  for (int64_t row = blockIdx.y; row < rows; row += gridDim.y) {
-    int y = (int)(row % dy), z = (int)(row / dy);
-    int Y = oy + y, Z = oz + z;
-    int gy = Y / my, gz = Z / mz;
-    int ly = Y - gy * my, lz = Z - gz * mz;
-    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < dx; x += gridDim.x * blockDim.x) {
-      int X = ox + x;
-      int gx = X / mx, lx = X - gx * mx;
-      int32_t s = leaf_slots[((int64_t)(gz - g0z) * gny + (gy - g0y)) * gnx + (gx - g0x)];
-      T* dst = pool + (int64_t)s * g.brick_elems + g.voxel_offset(lz + 1, ly + 1, lx + 1);
-      if (channel >= 0) {
-        dst[channel] = src[(row * dx + x) * src_stride + src_off];
-      } else {
-        const T* sp = src + (row * dx + x) * g.C;
-        for (int c = 0; c < g.C; ++c) dst[c] = sp[c];
+__global__ void __launch_bounds__(256) k_scatter(const T* __restrict__ src, int channel,
+                                                 int src_stride, int src_off, int ox, int oy,
+                                                 int oz, int zb, int dx, int dy, int g0x, int g0y,
+                                                 int g0z, int gnx, int gny,
+                                                 const int32_t* __restrict__ leaf_slots, Geo g,
+                                                 T* pool, int32_t* pmin, int32_t* pmax,
+                                                 unsigned long long* psum) {
+  const int mx = g.brick[0], my = g.brick[1], mz = g.brick[2], C = g.C;
+  const int gx = g0x + (int)(blockIdx.x % gnx), gy = g0y + (int)(blockIdx.x / gnx);
+  const int Z = oz + zb + (int)blockIdx.y;
+  const int gz = Z / mz, lz = Z - gz * mz;
+  const int32_t s = leaf_slots[((int64_t)(gz - g0z) * gny + (gy - g0y)) * gnx + (gx - g0x)];
+  const int X0 = max(ox, gx * mx), X1 = min(ox + dx, (gx + 1) * mx);
+  const int Y0 = max(oy, gy * my), Y1 = min(oy + dy, (gy + 1) * my);
+  const bool fused = channel < 0;
+  T* brick = pool + (int64_t)s * g.brick_elems;
+  const bool stats = owns_stats(g, channel, ox, oy, dx, dy, gx, gy);
+  int mn[kMaxC], mxv[kMaxC];
+  unsigned long long sm[kMaxC];
+#pragma unroll
+  for (int c = 0; c < kMaxC; ++c) {
+    mn[c] = INT_MAX;
+    mxv[c] = INT_MIN;
+    sm[c] = 0;
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int64_t zrow = (int64_t)(Z - oz) * dy;
+  const int nvox = X1 - X0;
+  unsigned int sm32[kMaxC] = {0, 0, 0, 0};
+  for (int y = Y0 + warp; y < Y1; y += nw) {
+    const int64_t svox = (zrow + (y - oy)) * dx + (X0 - ox);
+    T* drow = brick + g.voxel_offset(lz + 1, y - gy * my + 1, X0 - gx * mx + 1);
+    if (fused) {
+      // lane per voxel: its C samples are contiguous on both sides
+      const T* srow = src + svox * C;
+      for (int v = lane; v < nvox; v += 32) {
+#pragma unroll
+        for (int c = 0; c < kMaxC; ++c) {
+          if (c < C) {
+            const T val = srow[v * C + c];
+            drow[v * C + c] = val;
+            mn[c] = min(mn[c], (int)val);
+            mxv[c] = max(mxv[c], (int)val);
+            sm32[c] += val;
+          }
+        }
+      }
+    } else {
+      for (int v = lane; v < nvox; v += 32) {
+        const T val = src[(svox + v) * src_stride + src_off];
+        drow[(int64_t)v * C + channel] = val;
+        mn[0] = min(mn[0], (int)val);
+        mxv[0] = max(mxv[0], (int)val);
+        sm32[0] += val;
       }
     }
+  }
+#pragma unroll
+  for (int c = 0; c < kMaxC; ++c) sm[c] = sm32[c];
+  if (!stats) return;
+  __shared__ int s_mn[8][kMaxC], s_mx[8][kMaxC];
+  __shared__ unsigned long long s_sm[8][kMaxC];
+#pragma unroll
+  for (int c = 0; c < kMaxC; ++c) {
+    for (int o = 16; o > 0; o >>= 1) {
+      mn[c] = min(mn[c], __shfl_xor_sync(0xffffffffu, mn[c], o));
+      mxv[c] = max(mxv[c], __shfl_xor_sync(0xffffffffu, mxv[c], o));
+      sm[c] += __shfl_xor_sync(0xffffffffu, sm[c], o);
+    }
+    if (lane == 0) {
+      s_mn[warp][c] = mn[c];
+      s_mx[warp][c] = mxv[c];
+      s_sm[warp][c] = sm[c];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < C) {
+    const int c = threadIdx.x;
+    int a = INT_MAX, b = INT_MIN;
+    unsigned long long t = 0;
+    for (int w = 0; w < nw; ++w) {
+      a = min(a, s_mn[w][c]);
+      b = max(b, s_mx[w][c]);
+      t += s_sm[w][c];
+    }
+    const int64_t off = ((int64_t)s * mz + lz) * C + c;
+    pmin[off] = a;
+    pmax[off] = b;
+    psum[off] = t;
   }
 }
 
 // per-plane partial statistics of the in-volume interior (feeds
-// _recompute_stats, octree.py:248-263); blockDim multiple of C
+// _recompute_stats, octree.py:248-263): one warp per plane of a brick job,
+// one lane per voxel of a row, warp-shuffle reductions per channel
 template <class T>
-__global__ void __launch_bounds__(192) k_plane(const PlaneJob* __restrict__ jobs, Geo g,
+__global__ void __launch_bounds__(256) k_plane(const PlaneJob* __restrict__ jobs, int n, Geo g,
                                                const T* __restrict__ pool, int32_t* pmin,
                                                int32_t* pmax, unsigned long long* psum) {
-  const PlaneJob j = jobs[blockIdx.x];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int C = g.C;
-  const int t = threadIdx.x;
-  const int c = t % C;
-  const T* base = pool + (int64_t)j.slot * g.brick_elems + g.voxel_offset(j.z + 1, 1, 1);
-  const int rowlen = j.cx * C;
   const int64_t rowstride = (int64_t)g.stored[0] * C;
-  const int n = j.cy * rowlen;
-  int mn = INT_MAX, mx = INT_MIN;
-  unsigned long long s = 0;
-  for (int e = t; e < n; e += blockDim.x) {
-    int y = e / rowlen;
-    int r = e - y * rowlen;
-    int v = base[y * rowstride + r];
-    mn = min(mn, v);
-    mx = max(mx, v);
-    s += (unsigned)v;
-  }
-  __shared__ int smn[192], smx[192];
-  __shared__ unsigned long long ss[192];
-  smn[t] = mn;
-  smx[t] = mx;
-  ss[t] = s;
-  __syncthreads();
-  if (t < C) {
-    for (int u = t + C; u < blockDim.x; u += C) {
-      mn = min(mn, smn[u]);
-      mx = max(mx, smx[u]);
-      s += ss[u];
+  for (int job = blockIdx.x; job < n; job += gridDim.x) {
+    const PlaneJob j = jobs[job];
+    for (int z = j.z0 + warp; z < j.z1; z += nw) {
+      const T* base = pool + (int64_t)j.slot * g.brick_elems + g.voxel_offset(z + 1, 1, 1);
+      int mn[kMaxC], mx[kMaxC];
+      unsigned long long sm[kMaxC];
+#pragma unroll
+      for (int c = 0; c < kMaxC; ++c) {
+        mn[c] = INT_MAX;
+        mx[c] = INT_MIN;
+        sm[c] = 0;
+      }
+      for (int y = 0; y < j.cy; ++y) {
+        const T* row = base + y * rowstride;
+        for (int x = lane; x < j.cx; x += 32) {
+#pragma unroll
+          for (int c = 0; c < kMaxC; ++c) {
+            if (c < C) {
+              const int v = row[x * C + c];
+              mn[c] = min(mn[c], v);
+              mx[c] = max(mx[c], v);
+              sm[c] += (unsigned)v;
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < kMaxC; ++c) {
+        if (c >= C) continue;
+        for (int o = 16; o > 0; o >>= 1) {
+          mn[c] = min(mn[c], __shfl_xor_sync(0xffffffffu, mn[c], o));
+          mx[c] = max(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], o));
+          sm[c] += __shfl_xor_sync(0xffffffffu, sm[c], o);
+        }
+        if (lane == 0) {
+          const int64_t off = ((int64_t)j.slot * g.brick[2] + z) * C + c;
+          pmin[off] = mn[c];
+          pmax[off] = mx[c];
+          psum[off] = sm[c];
+        }
+      }
     }
-    int64_t o = ((int64_t)j.slot * g.brick[2] + j.z) * C + t;
-    pmin[o] = mn;
-    pmax[o] = mx;
-    psum[o] = s;
   }
 }
 
@@ -187,54 +313,85 @@ __global__ void k_reduce(const ReduceJob* __restrict__ jobs, int n, Geo g,
 }
 
 // child contribution to its parent's octant: halfsample_block or AVG fill
-// (octree.py:58-92, 281-319)
+// (octree.py:58-92, 281-319).  One CTA per job; a thread owns one output
+// voxel (all channels) of a plane and walks the planes, so a warp reads
+// 2 x 32 consecutive child voxels per (dz, dy) row — coalesced.
 template <class T>
-__global__ void k_octant(const OctJob* __restrict__ jobs, Geo g, T* pool,
-                         const int32_t* __restrict__ stats) {
-  const OctJob j = jobs[blockIdx.y];
+__global__ void __launch_bounds__(256) k_octant(const OctJob* __restrict__ jobs, int n, Geo g,
+                                                T* pool, const int32_t* __restrict__ stats) {
   const int C = g.C;
-  int kk[3], off[3];
-  for (int a = 0; a < 3; ++a) {
-    kk[a] = g.split[a] ? 2 : 1;
-    off[a] = (((j.k >> a) & 1) && g.split[a]) ? g.brick[a] / 2 : 0;
-  }
-  const int wx = j.r1[0] - j.r0[0], wy = j.r1[1] - j.r0[1], wz = j.r1[2] - j.r0[2];
-  const int64_t n = (int64_t)wx * wy * wz * C;
-  T* parent = pool + (int64_t)j.pslot * g.brick_elems;
-  const T* child = j.cslot >= 0 ? pool + (int64_t)j.cslot * g.brick_elems : nullptr;
-  int lim[3];
-  for (int a = 0; a < 3; ++a) lim[a] = div_up(j.cext[a], kk[a]);
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    int c = (int)(e % C);
-    int64_t v = e / C;
-    int ox = j.r0[0] + (int)(v % wx);
-    int oy = j.r0[1] + (int)((v / wx) % wy);
-    int oz = j.r0[2] + (int)(v / ((int64_t)wx * wy));
-    int val;
-    if (child) {
-      long long s = 0;
+  for (int job = blockIdx.x; job < n; job += gridDim.x) {
+    const OctJob j = jobs[job];
+    int kk[3], off[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      kk[a] = g.split[a] ? 2 : 1;
+      off[a] = (((j.k >> a) & 1) && g.split[a]) ? g.brick[a] / 2 : 0;
+    }
+    const int wx = j.r1[0] - j.r0[0], wy = j.r1[1] - j.r0[1], wz = j.r1[2] - j.r0[2];
+    T* parent = pool + (int64_t)j.pslot * g.brick_elems;
+    const T* child = j.cslot >= 0 ? pool + (int64_t)j.cslot * g.brick_elems : nullptr;
+    const int per_plane = wx * wy;
+    int avgv[kMaxC];
+    int lim[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) lim[a] = (j.cext[a] + kk[a] - 1) / kk[a];
+    if (!child) {
+#pragma unroll
+      for (int c = 0; c < kMaxC; ++c) avgv[c] = c < C ? stats[st_index(j.child, ST_AVG, c)] : 0;
+    }
+    // fast path: the 2x2x2 (or 2x2 / 2) source block is fully in volume
+    const bool full = child && j.cext[0] >= kk[0] * j.r1[0] && j.cext[1] >= kk[1] * j.r1[1] &&
+                      j.cext[2] >= kk[2] * j.r1[2];
+    const int n_out = kk[0] * kk[1] * kk[2];
+    for (int e = threadIdx.x; e < per_plane * wz; e += blockDim.x) {
+      const int oz = j.r0[2] + e / per_plane;
+      const int rem = e - (e / per_plane) * per_plane;
+      const int oy = j.r0[1] + rem / wx, ox = j.r0[0] + rem % wx;
+      T* dst = parent + g.voxel_offset(1 + off[2] + oz, 1 + off[1] + oy, 1 + off[0] + ox);
+      if (!child) {
+        const bool in = ox < lim[0] && oy < lim[1] && oz < lim[2];
+#pragma unroll
+        for (int c = 0; c < kMaxC; ++c)
+          if (c < C) dst[c] = (T)(in ? avgv[c] : g.bg);
+        continue;
+      }
+      long long sum[kMaxC] = {0, 0, 0, 0};
       int cnt = 0;
-      for (int dz = 0; dz < kk[2]; ++dz) {
-        int sz = kk[2] * oz + dz;
-        if (sz >= j.cext[2]) continue;
-        for (int dy = 0; dy < kk[1]; ++dy) {
-          int sy = kk[1] * oy + dy;
-          if (sy >= j.cext[1]) continue;
-          for (int dx = 0; dx < kk[0]; ++dx) {
-            int sx = kk[0] * ox + dx;
-            if (sx >= j.cext[0]) continue;
-            s += child[g.voxel_offset(1 + sz, 1 + sy, 1 + sx) + c];
-            ++cnt;
+      if (full) {
+        for (int dz = 0; dz < kk[2]; ++dz)
+          for (int dy = 0; dy < kk[1]; ++dy) {
+            const T* row = child + g.voxel_offset(1 + kk[2] * oz + dz, 1 + kk[1] * oy + dy,
+                                                  1 + kk[0] * ox);
+            for (int dx = 0; dx < kk[0]; ++dx)
+#pragma unroll
+              for (int c = 0; c < kMaxC; ++c)
+                if (c < C) sum[c] += row[dx * C + c];
+          }
+        cnt = n_out;
+      } else {
+        for (int dz = 0; dz < kk[2]; ++dz) {
+          const int sz = kk[2] * oz + dz;
+          if (sz >= j.cext[2]) continue;
+          for (int dy = 0; dy < kk[1]; ++dy) {
+            const int sy = kk[1] * oy + dy;
+            if (sy >= j.cext[1]) continue;
+            for (int dx = 0; dx < kk[0]; ++dx) {
+              const int sx = kk[0] * ox + dx;
+              if (sx >= j.cext[0]) continue;
+              const T* v = child + g.voxel_offset(1 + sz, 1 + sy, 1 + sx);
+#pragma unroll
+              for (int c = 0; c < kMaxC; ++c)
+                if (c < C) sum[c] += v[c];
+              ++cnt;
+            }
           }
         }
       }
-      val = cnt ? (int)((2 * s + cnt) / (2 * cnt)) : g.bg;
-    } else {
-      bool in = ox < lim[0] && oy < lim[1] && oz < lim[2];
-      val = in ? stats[st_index(j.child, ST_AVG, c)] : g.bg;
+#pragma unroll
+      for (int c = 0; c < kMaxC; ++c)
+        if (c < C) dst[c] = (T)(cnt ? (2 * sum[c] + cnt) / (2 * cnt) : g.bg);
     }
-    parent[g.voxel_offset(1 + off[2] + oz, 1 + off[1] + oy, 1 + off[0] + ox) + c] = (T)val;
   }
 }
 
@@ -387,56 +544,61 @@ void launch_create(const Tree& t, const CreateJob* d, int n) {
 
 constexpr int kMaxGridY = 65535;
 
-void launch_seed(const Tree& t, const SeedJob* d_all, int n_all) {
-  for (int o = 0; o < n_all; o += kMaxGridY) {
-  const SeedJob* d = d_all + o;
-  int n = n_all - o < kMaxGridY ? n_all - o : kMaxGridY;
-  dim3 grid(grid_for(t.g.brick_elems, kThreads, 64), n);
+void launch_seed(const Tree& t, const SeedJob* d, int n) {
+  if (n <= 0) return;
+  const unsigned grid = (unsigned)std::min<int64_t>(n, 148 * 64);
   if (t.g.sb == 1)
-    k_seed<uint8_t><<<grid, kThreads, 0, t.stream>>>(d, t.g, t.d_pool, t.d_stats);
+    k_seed<uint8_t><<<grid, 256, 0, t.stream>>>(d, n, t.g, t.d_pool, t.d_stats);
   else
-    k_seed<uint16_t><<<grid, kThreads, 0, t.stream>>>(d, t.g, (uint16_t*)t.d_pool, t.d_stats);
+    k_seed<uint16_t><<<grid, 256, 0, t.stream>>>(d, n, t.g, (uint16_t*)t.d_pool, t.d_stats);
   VT_CHECK_LAUNCH();
-  }
+}
+
+bool scatter_owns_stats(const Geo& g, int channel, const int o[3], const int d[3], int gx,
+                        int gy) {
+  if (!(channel < 0 || g.C == 1)) return false;
+  const int bx0 = gx * g.brick[0], by0 = gy * g.brick[1];
+  const int ix1 = std::min(g.dims[0], bx0 + g.brick[0]), iy1 = std::min(g.dims[1], by0 + g.brick[1]);
+  return o[0] <= bx0 && o[0] + d[0] >= ix1 && o[1] <= by0 && o[1] + d[1] >= iy1;
 }
 
 void launch_scatter(const Tree& t, const void* src, int channel, int ss, int so, const int o[3],
-                    const int d[3],
-                    const int g0[3], const int gn[3], const int32_t* slots) {
-  int64_t rows = (int64_t)d[1] * d[2];
-  dim3 grid((d[0] + kThreads - 1) / kThreads, (unsigned)(rows > 65535 ? 65535 : rows));
-  if (t.g.sb == 1)
-    k_scatter<uint8_t><<<grid, kThreads, 0, t.stream>>>((const uint8_t*)src, channel, ss, so, o[0], o[1],
-                                                        o[2], d[0], d[1], d[2], g0[0], g0[1],
-                                                        g0[2], gn[0], gn[1], slots, t.g, t.d_pool);
-  else
-    k_scatter<uint16_t><<<grid, kThreads, 0, t.stream>>>(
-        (const uint16_t*)src, channel, ss, so, o[0], o[1], o[2], d[0], d[1], d[2], g0[0], g0[1], g0[2],
-        gn[0], gn[1], slots, t.g, (uint16_t*)t.d_pool);
-  VT_CHECK_LAUNCH();
+                    const int d[3], const int g0[3], const int gn[3], const int32_t* slots) {
+  if ((int64_t)d[0] * d[1] * d[2] == 0) return;
+  for (int z = 0; z < d[2]; z += 65535) {
+    const int nz = std::min(65535, d[2] - z);
+    dim3 grid((unsigned)(gn[0] * gn[1]), (unsigned)nz);
+    if (t.g.sb == 1)
+      k_scatter<uint8_t><<<grid, 256, 0, t.stream>>>(
+          (const uint8_t*)src, channel, ss, so, o[0], o[1], o[2], z, d[0], d[1], g0[0], g0[1],
+          g0[2], gn[0], gn[1], slots, t.g, t.d_pool, t.d_pmin, t.d_pmax, t.d_psum);
+    else
+      k_scatter<uint16_t><<<grid, 256, 0, t.stream>>>(
+          (const uint16_t*)src, channel, ss, so, o[0], o[1], o[2], z, d[0], d[1], g0[0], g0[1],
+          g0[2], gn[0], gn[1], slots, t.g, (uint16_t*)t.d_pool, t.d_pmin, t.d_pmax, t.d_psum);
+    VT_CHECK_LAUNCH();
+  }
 }
 
-void launch_octant(const Tree& t, const OctJob* d_all, int n_all) {
-  for (int o = 0; o < n_all; o += kMaxGridY) {
-  const OctJob* d = d_all + o;
-  int n = n_all - o < kMaxGridY ? n_all - o : kMaxGridY;
-  int64_t per = (int64_t)t.g.brick[0] * t.g.brick[1] * t.g.brick[2] * t.g.C / 8;
-  dim3 grid(grid_for(per, kThreads, 32), n);
+void launch_octant(const Tree& t, const OctJob* d, int n) {
+  if (n <= 0) return;
+  const unsigned grid = (unsigned)std::min<int64_t>(n, 148 * 32);
   if (t.g.sb == 1)
-    k_octant<uint8_t><<<grid, kThreads, 0, t.stream>>>(d, t.g, t.d_pool, t.d_stats);
+    k_octant<uint8_t><<<grid, 256, 0, t.stream>>>(d, n, t.g, t.d_pool, t.d_stats);
   else
-    k_octant<uint16_t><<<grid, kThreads, 0, t.stream>>>(d, t.g, (uint16_t*)t.d_pool, t.d_stats);
+    k_octant<uint16_t><<<grid, 256, 0, t.stream>>>(d, n, t.g, (uint16_t*)t.d_pool, t.d_stats);
   VT_CHECK_LAUNCH();
-  }
 }
 
 void launch_plane(const Tree& t, const PlaneJob* d, int n) {
   if (n <= 0) return;
+  const unsigned grid = (unsigned)std::min<int64_t>(n, 148 * 64);
   if (t.g.sb == 1)
-    k_plane<uint8_t><<<n, 192, 0, t.stream>>>(d, t.g, t.d_pool, t.d_pmin, t.d_pmax, t.d_psum);
+    k_plane<uint8_t><<<grid, 256, 0, t.stream>>>(d, n, t.g, t.d_pool, t.d_pmin, t.d_pmax,
+                                                  t.d_psum);
   else
-    k_plane<uint16_t><<<n, 192, 0, t.stream>>>(d, t.g, (const uint16_t*)t.d_pool, t.d_pmin,
-                                               t.d_pmax, t.d_psum);
+    k_plane<uint16_t><<<grid, 256, 0, t.stream>>>(d, n, t.g, (const uint16_t*)t.d_pool, t.d_pmin,
+                                                   t.d_pmax, t.d_psum);
   VT_CHECK_LAUNCH();
 }
 

@@ -33,6 +33,12 @@ struct vt_mirror {
   uint8_t* d_fb = nullptr;
   uint8_t* d_bb = nullptr;   // own brick buffer (bounded mode)
   int32_t* d_res = nullptr;  // node -> brick-buffer slot or -1 (bounded mode)
+  // per brick-buffer slot, per channel: max sample over the stored brick
+  // (borders included) — empty-space skipping bound; valid for slots < bmax_n
+  int32_t* d_bmax = nullptr;
+  int64_t bmax_cap = 0;
+  bool bmax_valid = false;
+  int64_t bmax_version = -1;  // tree data_version the zero-copy maxima reflect
 };
 
 namespace {
@@ -74,6 +80,12 @@ struct RenderParams {
   // sort-first strip interleave: this launch renders the rows of strips
   // part, part + n_parts, ... (strip_rows rows each), written compactly
   int strip_rows, n_parts, part;
+  // exact empty-space skipping (DVR, no channel transforms): a sample whose
+  // every channel value v satisfies v <= ess_thr[c] has transfer-function
+  // alpha exactly 0 and composites to a no-op
+  int ess;
+  int ess_thr[kMaxC];
+  const int32_t* bmax;
 };
 
 // per-launch scene + geometry; render entry points serialise on g_render_mu
@@ -227,6 +239,9 @@ struct Sampler {
   bool fullframe;
   Counters cnt;  // by value: stays in registers
   long long last_used = -1, last_req = -1;
+  // the last sample resolved to a node that is transparent for the scene's
+  // transfer functions: 1 resident brick, 2 homogeneous (AVG) node
+  int hint = 0;
   DescentCache cache[TR ? NC : 1];
 
   __device__ Sampler(const uint64_t* n, uint8_t* f, const T* b, bool ff)
@@ -375,15 +390,27 @@ struct Sampler {
     const uint64_t e = __ldg(nb + dc.idx);
     const bool resident = e & 1, nh = e & 2;
     if (!nh) {
+      bool clear = true;
 #pragma unroll
       for (int c = 0; c < NC; ++c)
-        if (c >= c0 && c < c1) out[c] = avg_of(e, c);
+        if (c >= c0 && c < c1) {
+          out[c] = avg_of(e, c);
+          clear = clear && out[c] <= (double)P.ess_thr[c];
+        }
+      hint = (!TR && P.ess && clear) ? 2 : 0;
       return false;
     }
     if (resident) {
       trilerp(e, dc.lvl, dc.lo, pv, c0, c1, out);
       mark(dc.idx, 1);
       cnt.used++;
+      if (!TR && P.ess) {
+        const int32_t* bm = P.bmax + ((e >> 24) & 0xFFFFFFFFULL) * kMaxC;
+        bool clear = true;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) clear = clear && __ldg(bm + c) <= P.ess_thr[c];
+        hint = clear ? 1 : 0;
+      }
       return false;
     }
     mark(dc.idx, 2);
@@ -418,9 +445,55 @@ struct Sampler {
     for (int a = 0; a < 3; ++a) pv[a] = P.unit_spacing ? q[a] : q[a] / P.spacing[a];
   }
 
+  // samples k+1 .. k+m provably resolve to the same transparent node with
+  // the same target level, inside the volume and the ray: returns m (exact
+  // empty-space skip; each skipped sample still counts as the reference
+  // counts it).  Positions are monotone in k, so checking the last one
+  // suffices; the analytic estimate is verified with the sampling code.
+  __device__ long long skip_count(long long k, long long n, double t0, const double d[3]) {
+    const DescentCache& dc = cache[0];
+    double tl = INFINITY;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      double lo = 0.0, hi = P.dims[a];
+      if (P.g.split[a]) {
+        lo = fmax(lo, dc.lo[a]);
+        hi = fmin(hi, dc.lo[a] + P.ext[dc.lvl][a]);
+      }
+      if (d[a] > 0.0) tl = fmin(tl, (hi * P.spacing[a] - P.cam[a]) / d[a]);
+      else if (d[a] < 0.0) tl = fmin(tl, (lo * P.spacing[a] - P.cam[a]) / d[a]);
+    }
+    if (dc.target < P.g.depth) {
+      const double df = d[0] * P.fwd[0] + d[1] * P.fwd[1] + d[2] * P.fwd[2];
+      if (df > 0.0)
+        tl = fmin(tl, ldexp(1.0, dc.target + 1) * P.base_voxel / (P.pfs * P.lod_scale) / df);
+    }
+    long long m = (long long)floor((tl - t0) / P.step) - 1 - k;
+    m = m < n - 1 - k ? m : n - 1 - k;
+    for (int tries = 0; tries < 3 && m > 0; ++tries, m >>= 1) {
+      const double t = t0 + (double)(k + m) * P.step;
+      double p[3], pv[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) p[a] = P.cam[a] + t * d[a];
+      to_voxels(p, pv);
+      bool ok = true;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) ok = ok && pv[a] >= 0.0 && pv[a] <= P.dims[a];
+      if (!ok || lod(p) != dc.target) continue;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const double q = npclip(pv[a], 0.0, P.dims[a] - 1e-9);
+        if (P.g.split[a] && !(q >= dc.lo[a] && q < dc.lo[a] + P.ext[dc.lvl][a])) ok = false;
+      }
+      if (ok) return m;
+    }
+    return 0;
+  }
+
   // sampler (raycast.py:242-278); returns missing
   __device__ bool sample(const double p[3], double* vals) {
     constexpr int C = NC;
+    hint = 0;
 #pragma unroll
     for (int c = 0; c < C; ++c) vals[c] = (double)P.g.bg;
     if (!TR) {
@@ -588,6 +661,13 @@ __global__ void __launch_bounds__(128, VT_RENDER_MINB) k_render_fullframe(const 
       s.sample(p, vals);
       cnt.samples++;
       if (composite<NC>(tf, vals, o, cnt)) break;
+      if (s.hint) {
+        const long long m = s.skip_count(k, n, t0, d);
+        cnt.samples += m;
+        cnt.tf += m * NC;
+        if (s.hint == 1) cnt.used += m;
+        k += m;
+      }
     }
     double px[4];
     finalize<NC>(tf, o, px, cnt);
@@ -679,6 +759,13 @@ __global__ void __launch_bounds__(128) k_rays_march(RayState S,
           ++k;
           break;
         }
+        if (s.hint) {
+          const long long m = s.skip_count(k, n, t0, d);
+          cnt.samples += m;
+          cnt.tf += m * NC;
+          if (s.hint == 1) cnt.used += m;
+          k += m;
+        }
       }
       for (int a = 0; a < 3; ++a) S.acc[r * 4 + a] = o.rgb[a];
       S.acc[r * 4 + 3] = o.a;
@@ -713,6 +800,39 @@ __global__ void k_rays_image(RayState S, double* out,
 }
 
 // ---- mirror kernels ------------------------------------------------------------
+
+// per-slot, per-channel maximum over the whole stored brick (borders too):
+// the bound the empty-space skip tests against.  slots == nullptr: slot = job
+template <class T>
+__global__ void __launch_bounds__(256) k_brick_max(const T* __restrict__ bb, const int32_t* slots,
+                                                   int n, Geo g, int32_t* bmax) {
+  const int C = g.C;
+  const int64_t nvox = g.brick_elems / C;
+  __shared__ int red[8][kMaxC];
+  for (int job = blockIdx.x; job < n; job += gridDim.x) {
+    const int64_t slot = slots ? slots[job] : job;
+    if (slot < 0) continue;
+    const T* b = bb + slot * g.brick_elems;
+    int mx[kMaxC] = {0, 0, 0, 0};
+    for (int64_t v = threadIdx.x; v < nvox; v += blockDim.x) {
+#pragma unroll
+      for (int c = 0; c < kMaxC; ++c)
+        if (c < C) mx[c] = max(mx[c], (int)b[v * C + c]);
+    }
+#pragma unroll
+    for (int c = 0; c < kMaxC; ++c) {
+      for (int o = 16; o > 0; o >>= 1) mx[c] = max(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], o));
+      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][c] = mx[c];
+    }
+    __syncthreads();
+    if (threadIdx.x < kMaxC) {
+      int r = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r = max(r, red[w][threadIdx.x]);
+      bmax[slot * kMaxC + threadIdx.x] = r;
+    }
+    __syncthreads();
+  }
+}
 
 // _entry_for / pack_node (device.py:51-87, 168-178)
 __global__ void k_repack(Geo g, const uint8_t* __restrict__ flags,
@@ -879,12 +999,64 @@ void fill_params(const vt_mirror* m, const vt_scene* s, RenderParams& P) {
   P.rect[1] = 0;
   P.rect[2] = P.W;
   P.rect[3] = P.H;
+  // empty-space skip thresholds: x*_c = sup{x : TF alpha == 0 on [0, x]};
+  // a sample value v is transparent when v + 0.5 <= x*_c * fmax
+  P.ess = (!P.mip && !P.has_tr && m->bmax_valid && m->d_bmax) ? 1 : 0;
+  P.bmax = m->d_bmax;
+  for (int c = 0; c < kMaxC; ++c) P.ess_thr[c] = -1;
+  for (int c = 0; c < t.g.C; ++c) {
+    const int n = P.tf_n[c];
+    double xs = -1.0;
+    if (P.tf_v[c][0][3] == 0.0) {
+      xs = INFINITY;
+      for (int q = 0; q + 1 < n; ++q) {
+        if (P.tf_v[c][q + 1][3] != 0.0) {
+          xs = P.tf_x[c][q];
+          break;
+        }
+      }
+      if (n == 1) xs = INFINITY;
+    }
+    if (xs < 0.0) P.ess_thr[c] = -1;
+    else if (!std::isfinite(xs)) P.ess_thr[c] = t.fmax;
+    else P.ess_thr[c] = (int)std::max(-1.0, std::floor(xs * P.fmax - 0.5));
+  }
   P.strip_rows = P.H > 0 ? P.H : 1;
   P.n_parts = 1;
   P.part = 0;
 }
 
 }  // namespace
+
+// (re)compute brick maxima: every pool slot in use (zero copy) or the listed
+// brick-buffer slots (bounded mode, after uploads)
+static void update_bmax(vt_mirror* m, const int32_t* d_slots, int n) {
+  Tree& t = m->tree->t;
+  const int64_t need = m->zero_copy ? t.pool_slots : m->slots;
+  if (need > m->bmax_cap) {
+    VT_CUDA(cudaStreamSynchronize(t.stream));
+    cudaFree(m->d_bmax);
+    m->d_bmax = nullptr;
+    VT_CUDA(cudaMalloc(&m->d_bmax, std::max<int64_t>(1, need) * kMaxC * sizeof(int32_t)));
+    VT_CUDA(cudaMemsetAsync(m->d_bmax, 0x7F, std::max<int64_t>(1, need) * kMaxC * sizeof(int32_t),
+                            t.stream));  // unknown slots never qualify as empty
+    m->bmax_cap = need;
+  }
+  const int jobs = d_slots ? n : (int)(m->zero_copy ? t.cursor : m->slots);
+  if (jobs > 0) {
+    const unsigned grid = (unsigned)std::min<int64_t>(jobs, 148 * 16);
+    const void* bb = m->zero_copy ? (const void*)t.d_pool : (const void*)m->d_bb;
+    if (t.g.sb == 1)
+      k_brick_max<uint8_t><<<grid, 256, 0, t.stream>>>((const uint8_t*)bb, d_slots, jobs, t.g,
+                                                       m->d_bmax);
+    else
+      k_brick_max<uint16_t><<<grid, 256, 0, t.stream>>>((const uint16_t*)bb, d_slots, jobs, t.g,
+                                                        m->d_bmax);
+    VT_CUDA(cudaGetLastError());
+  }
+  m->bmax_valid = true;
+  if (m->zero_copy) m->bmax_version = t.data_version;
+}
 
 struct vt_rays {
   vt_mirror* m;
@@ -938,6 +1110,7 @@ static void mirror_release(vt_mirror* m) {
   cudaFree(m->d_fb);
   cudaFree(m->d_bb);
   cudaFree(m->d_res);
+  cudaFree(m->d_bmax);
   vt_tree_release(m->tree);
   delete m;
 }
@@ -988,6 +1161,7 @@ vt_status vt_mirror_set_resident(vt_mirror* m, int64_t n, const int64_t* nodes,
         k_upload<<<grid, 256, 0, t.stream>>>(dsrc + o, ds + o, cnt, t.d_pool, m->d_bb, bytes);
         VT_CUDA(cudaGetLastError());
       }
+      update_bmax(m, ds, (int)n);
       release(t, dsrc);
     }
     release(t, dn);
@@ -1004,6 +1178,8 @@ vt_status vt_mirror_repack(vt_mirror* m) {
         t.g, t.d_flags, t.d_slot, t.d_stats, m->d_res, m->zero_copy ? 1 : 0, (double)t.fmax,
         40 / t.g.C, m->d_nb);
     VT_CUDA(cudaGetLastError());
+    if (m->zero_copy) update_bmax(m, nullptr, 0);
+    else if (!m->bmax_valid) update_bmax(m, nullptr, 0);
   });
 }
 
@@ -1038,6 +1214,7 @@ static void render_rect(vt_mirror* m, const vt_scene* scene, const int32_t* rect
   std::lock_guard<std::mutex> lk(g_render_mu);
   Tree& t = m->tree->t;
   t.flush();
+  if (m->zero_copy && m->bmax_version != t.data_version) update_bmax(m, nullptr, 0);
   RenderParams P;
   fill_params(m, scene, P);
   VT_REQUIRE(out_kind >= 0 && out_kind <= 2, VT_EINVAL, "out_kind must be 0, 1 or 2");
@@ -1159,8 +1336,11 @@ vt_status vt_rays_march(vt_rays* r, int32_t strategy, vt_counters* cnt, int64_t*
     vt_mirror* m = r->m;
     Tree& t = m->tree->t;
     t.flush();
+    if (m->zero_copy && m->bmax_version != t.data_version) update_bmax(m, nullptr, 0);
     RenderParams P = r->P;
     P.borders_filled = t.borders ? 1 : 0;
+    P.bmax = m->d_bmax;
+    P.ess = (!P.mip && !P.has_tr && m->bmax_valid && m->d_bmax) ? 1 : 0;
     P.rect[0] = 0;
     P.rect[1] = 0;
     P.rect[2] = P.W;

@@ -13,8 +13,10 @@
 // tau > 0 it runs per insertion, followed by a stats gather and the exact
 // reference prune (octree.py:456-493).
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <mutex>
 #include <cstring>
-#include <map>
 
 #include "tree.cuh"
 
@@ -68,6 +70,7 @@ static void build_geo(const vt_tree_desc& d, Geo& g) {
 }
 
 Tree::Tree(const vt_tree_desc& d) {
+  if (const char* e = std::getenv("VT_HOST_PROFILE")) prof.on = e[0] == '1';
   VT_REQUIRE(d.channels >= 1 && d.channels <= kMaxC, VT_EINVAL, "channels must be in [1, 4]");
   VT_REQUIRE(d.sample_bytes == 1 || d.sample_bytes == 2, VT_EINVAL, "unsupported sample format");
   for (int a = 0; a < 3; ++a)
@@ -104,15 +107,79 @@ Tree::Tree(const vt_tree_desc& d) {
   VT_CUDA(cudaMemcpy(d_flags, flags.data(), 1, cudaMemcpyHostToDevice));
   VT_CUDA(cudaMemcpy(d_stats, h_stats.data(), ST_N * kMaxC * sizeof(int32_t),
                      cudaMemcpyHostToDevice));
-  pending.assign(g.depth + 1, {});
+  pend_nodes.assign(g.depth + 1, {});
+  pend_pool.assign(g.depth + 1, {});
+  pend_slot.assign(cap, -1);
   VT_CUDA(cudaEventCreate(&ev0));
   VT_CUDA(cudaEventCreate(&ev1));
   int64_t reserve = d.reserve_slots > 0 ? d.reserve_slots : 64;
   ensure_pool(reserve);
 }
 
+// process-wide cache of pinned staging blocks: page-locking costs
+// milliseconds, so blocks outlive the trees that used them
+namespace {
+std::mutex g_pin_mu;
+std::vector<std::pair<uint8_t*, size_t>> g_pin_free;
+
+uint8_t* pinned_get(size_t& cap) {
+  {
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    for (size_t i = 0; i < g_pin_free.size(); ++i)
+      if (g_pin_free[i].second >= cap) {
+        uint8_t* p = g_pin_free[i].first;
+        cap = g_pin_free[i].second;
+        g_pin_free.erase(g_pin_free.begin() + i);
+        return p;
+      }
+  }
+  uint8_t* p = nullptr;
+  VT_CUDA(cudaMallocHost(&p, cap));
+  return p;
+}
+
+void pinned_put(uint8_t* p, size_t cap) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  g_pin_free.emplace_back(p, cap);
+}
+}  // namespace
+
+void* Tree::stage_copy(const void* src, size_t bytes) const {
+  const size_t need = (bytes + 255) & ~(size_t)255;
+  if (need > stage.cap) {
+    VT_CUDA(cudaStreamSynchronize(stream));
+    pinned_put(stage.h, stage.cap);
+    if (stage.d) cudaFree(stage.d);
+    stage.h = nullptr;
+    stage.d = nullptr;
+    size_t cap = std::max<size_t>(need * 2, (size_t)8 << 20);
+    stage.h = pinned_get(cap);
+    VT_CUDA(cudaMalloc(&stage.d, cap));
+    stage.cap = cap;
+    stage.head = 0;
+  } else if (stage.head + need > stage.cap) {
+    // wrap: every earlier copy (and kernel reading the ring) must be done
+    VT_CUDA(cudaStreamSynchronize(stream));
+    stage.head = 0;
+  }
+  uint8_t* h = stage.h + stage.head;
+  uint8_t* d = stage.d + stage.head;
+  std::memcpy(h, src, bytes);
+  VT_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, stream));
+  stage.head += need;
+  return d;
+}
+
 Tree::~Tree() {
+  if (prof.on) {
+    std::fprintf(stderr, "[vtx host profile ms]");
+    for (int i = 0; i < 8; ++i) std::fprintf(stderr, " %s=%.2f", HostProf::name(i), prof.t[i]);
+    std::fprintf(stderr, "\n");
+  }
   if (stream) cudaStreamSynchronize(stream);
+  pinned_put(stage.h, stage.cap);
+  if (stage.d) cudaFree(stage.d);
   cudaFree(d_pool);
   cudaFree(d_flags);
   cudaFree(d_slot);
@@ -122,6 +189,7 @@ Tree::~Tree() {
   cudaFree(d_psum);
   if (ev0) cudaEventDestroy(ev0);
   if (ev1) cudaEventDestroy(ev1);
+  if (ev_wait) cudaEventDestroy(ev_wait);
   if (own_stream && stream) cudaStreamDestroy(stream);
 }
 
@@ -226,6 +294,7 @@ bool Tree::ensure_brick(int64_t n) {
   j.node = n;
   j.slot = s;
   node_in_extent(n, j.cext);
+  // no cover by default (set by the caller when it overwrites a region)
   seeds.push_back(j);
   ++brick_count;
   return true;
@@ -273,6 +342,7 @@ static inline void box_union(Pending& p, const Box& b) {
 
 void Tree::insert(int channel, const int origin[3], const int dims[3], const void* samples,
                   int mem_kind) {
+  ProfScope ps(prof, 0);
   // validation exactly as octree.py:331-341 (channel -1 = all channels interleaved)
   VT_REQUIRE(channel == -1 || (channel >= 0 && channel < g.C), VT_EINVAL,
              "channel " + std::to_string(channel) + " out of range");
@@ -322,6 +392,7 @@ void Tree::insert(int channel, const int origin[3], const int dims[3], const voi
 void Tree::insert_staged(int channel, const int origin[3], const int dims[3], const void* dsrc,
                          int src_stride, int src_off, int reps) {
   const int64_t nvox = (int64_t)dims[0] * dims[1] * dims[2];
+  ++data_version;
   creates.clear();
   seeds.clear();
   created_seed.clear();
@@ -334,6 +405,7 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
   }
   std::vector<int32_t> leaf_slots((size_t)gn[0] * gn[1] * gn[2]);
   std::vector<std::vector<int64_t>> touched(g.depth + 1);
+  auto* walk_scope = new ProfScope(prof, 1);
 
   // leaves (octree.py:351-360): descend, create, ensure brick, dirty box
   for (int gz = g0[2]; gz <= g1[2]; ++gz)
@@ -357,9 +429,33 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
           b.lo[a] = fresh ? 0 : std::max(origin[a], lo) - lo;
           b.hi[a] = fresh ? M[a] : std::min(origin[a] + dims[a], lo + M[a]) - lo;
         }
-        Pending& p = pending[0][idx];
+        if (fresh && (channel < 0 || g.C == 1)) {
+          // the scatter below writes every channel of block ∩ brick
+          SeedJob& sj = seeds.back();
+          for (int a = 0; a < 3; ++a) {
+            int lo = gg[a] * M[a];
+            sj.cov_lo[a] = std::max(origin[a], lo) - lo;
+            sj.cov_hi[a] = std::min(origin[a] + dims[a], lo + M[a]) - lo;
+          }
+        }
+        Pending& p = pend(0, idx);
         box_union(p, b);
         p.fresh |= fresh;
+        if (g.brick[2] <= 128) {
+          int ce[3];
+          node_in_extent(idx, ce);
+          if (!p.masked) {
+            // first touch since the last propagation: nothing owed yet
+            p.masked = true;
+            p.need[0] = p.need[1] = 0;
+          }
+          if (fresh)
+            for (int z = 0; z < ce[2]; ++z) p.set_need(z, true);
+          const bool own = scatter_owns_stats(g, channel, origin, dims, gx, gy);
+          const int z0 = std::max(origin[2], gz * M[2]) - gz * M[2];
+          const int z1 = std::min(std::min(origin[2] + dims[2], (gz + 1) * M[2]) - gz * M[2], ce[2]);
+          for (int z = z0; z < z1; ++z) p.set_need(z, !own);
+        }
         touched[0].push_back(idx);
       }
   // ancestors (octree.py:363-387): ensure parent bricks, record freshness
@@ -370,20 +466,39 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
     par.erase(std::unique(par.begin(), par.end()), par.end());
     for (int64_t p : par) {
       bool fresh = ensure_brick(p);
-      pending[lvl][p].fresh |= fresh;
+      if (fresh) {
+        // a fresh parent recomputes every real octant: its whole interior
+        SeedJob& sj = seeds.back();
+        for (int a = 0; a < 3; ++a) {
+          sj.cov_lo[a] = 0;
+          sj.cov_hi[a] = M[a];
+        }
+      }
+      pend(lvl, p).fresh |= fresh;
     }
   }
   std::sort(touched[0].begin(), touched[0].end());
   has_pending = true;
+  delete walk_scope;
+  ProfScope enq_scope(prof, 2);
 
   // device pre-work for this insertion
-  flush_structure();
-  CreateJob* dc = upload(*this, creates);
-  launch_create(*this, dc, (int)creates.size());
-  SeedJob* ds = upload(*this, seeds);
-  launch_seed(*this, ds, (int)seeds.size());
-  int32_t* dl = upload(*this, leaf_slots);
-  launch_scatter(*this, dsrc, channel, src_stride, src_off, origin, dims, g0, gn, dl);
+  { ProfScope q(prof, 5); flush_structure(); }
+  CreateJob* dc;
+  SeedJob* ds;
+  {
+    ProfScope q(prof, 6);
+    dc = upload(*this, creates);
+    launch_create(*this, dc, (int)creates.size());
+    ds = upload(*this, seeds);
+    launch_seed(*this, ds, (int)seeds.size());
+  }
+  int32_t* dl;
+  {
+    ProfScope q(prof, 7);
+    dl = upload(*this, leaf_slots);
+    launch_scatter(*this, dsrc, channel, src_stride, src_off, origin, dims, g0, gn, dl);
+  }
   release(*this, dc);
   release(*this, ds);
   release(*this, dl);
@@ -415,22 +530,20 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
 
 void Tree::propagate() {
   if (!has_pending) return;
+  ProfScope ps(prof, 4);
   VT_CUDA(cudaEventRecord(ev0, stream));
   const int* M = g.brick;
   for (int lvl = 0; lvl <= g.depth; ++lvl) {
-    auto& pm = pending[lvl];
-    if (pm.empty()) continue;
-    std::vector<int64_t> nodes;
-    nodes.reserve(pm.size());
-    for (auto& kv : pm) nodes.push_back(kv.first);
+    std::vector<int64_t>& nodes = pend_nodes[lvl];
+    if (nodes.empty()) continue;
     std::sort(nodes.begin(), nodes.end());
     std::vector<OctJob> oct;
     if (lvl > 0) {
-      // group dirty children by parent
-      std::map<int64_t, std::vector<int64_t>> kids;
-      for (auto& kv : pending[lvl - 1]) kids[(kv.first - 1) >> 3].push_back(kv.first);
+      // dirty children are sorted: those of parent p are a contiguous run
+      const std::vector<int64_t>& kids = pend_nodes[lvl - 1];
+      size_t ci = 0;
       for (int64_t p : nodes) {
-        Pending& pp = pm[p];
+        Pending& pp = *pend_find(p, lvl);
         auto emit = [&](int64_t c, const Box* cb) {
           OctJob j{};
           j.pslot = slot[p];
@@ -457,6 +570,7 @@ void Tree::propagate() {
             box_union(pp, pb);
           }
         };
+        while (ci < kids.size() && ((kids[ci] - 1) >> 3) < p) ++ci;
         if (pp.fresh) {
           // fresh parent brick: every real octant (octree.py:375-377)
           for (int k = 0; k < 8; ++k) {
@@ -466,13 +580,9 @@ void Tree::propagate() {
           pp.box = Box{{0, 0, 0}, {M[0], M[1], M[2]}};
           pp.has_box = true;
         } else {
-          auto it = kids.find(p);
-          if (it != kids.end()) {
-            std::sort(it->second.begin(), it->second.end());
-            for (int64_t c : it->second) {
-              Pending& cp = pending[lvl - 1][c];
-              if (cp.has_box) emit(c, &cp.box);
-            }
+          for (size_t q = ci; q < kids.size() && ((kids[q] - 1) >> 3) == p; ++q) {
+            const Pending& cp = *pend_find(kids[q], lvl - 1);
+            if (cp.has_box) emit(kids[q], &cp.box);
           }
         }
       }
@@ -483,16 +593,33 @@ void Tree::propagate() {
     // stats of this level's dirty nodes
     std::vector<PlaneJob> planes;
     std::vector<ReduceJob> reds;
+    planes.reserve(nodes.size());
+    reds.reserve(nodes.size());
     for (int64_t n : nodes) {
-      Pending& p = pm[n];
+      const Pending& p = *pend_find(n, lvl);
       ReduceJob r{};
       r.node = n;
       r.slot = slot[n];
       node_in_extent(n, r.cext);
       r.leafish = (lvl == 0 || !(flags[n] & NF_CHILDREN)) ? 1 : 0;
       if (p.has_box && r.cext[0] > 0 && r.cext[1] > 0) {
-        int z1 = std::min(p.box.hi[2], r.cext[2]);
-        for (int z = p.box.lo[2]; z < z1; ++z) planes.push_back({r.slot, z, r.cext[0], r.cext[1]});
+        if (lvl == 0 && p.masked) {
+          // runs of planes whose stats the scatter did not compute
+          int z = 0;
+          while (z < r.cext[2]) {
+            if (!p.needs(z)) {
+              ++z;
+              continue;
+            }
+            int e = z;
+            while (e < r.cext[2] && p.needs(e)) ++e;
+            planes.push_back({r.slot, z, e, r.cext[0], r.cext[1]});
+            z = e;
+          }
+        } else {
+          int z1 = std::min(p.box.hi[2], r.cext[2]);
+          if (z1 > p.box.lo[2]) planes.push_back({r.slot, p.box.lo[2], z1, r.cext[0], r.cext[1]});
+        }
       }
       reds.push_back(r);
     }
@@ -503,7 +630,11 @@ void Tree::propagate() {
     release(*this, dp);
     release(*this, dr);
   }
-  for (int lvl = 0; lvl <= g.depth; ++lvl) pending[lvl].clear();
+  for (int lvl = 0; lvl <= g.depth; ++lvl) {
+    for (int64_t i : pend_nodes[lvl]) pend_slot[i] = -1;
+    pend_nodes[lvl].clear();
+    pend_pool[lvl].clear();
+  }
   has_pending = false;
   VT_CUDA(cudaEventRecord(ev1, stream));
 }
@@ -593,6 +724,7 @@ void Tree::prune(std::vector<std::vector<int64_t>>& touched, std::vector<char>& 
 
 void Tree::fill_borders() {
   flush();
+  ++data_version;
   std::vector<BorderJob> jobs;
   for (int64_t i = 0; i < g.capacity; ++i)
     if ((flags[i] & NF_EXISTS) && (flags[i] & NF_BRICK)) jobs.push_back({i, slot[i]});

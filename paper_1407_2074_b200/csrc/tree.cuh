@@ -4,6 +4,7 @@
 #pragma once
 
 #include <atomic>
+#include <chrono>
 #include <queue>
 #include <unordered_map>
 #include <vector>
@@ -20,9 +21,45 @@ struct Pending {
   Box box;
   bool has_box = false;
   bool fresh = false;
+  // leaves: planes whose partial stats are still owed (bit z); planes whose
+  // stats the scatter computed in-kernel are cleared (requires Mz <= 128)
+  bool masked = false;
+  uint64_t need[2] = {0, 0};
+  void set_need(int z, bool v) {
+    uint64_t bit = 1ULL << (z & 63);
+    if (v) need[z >> 6] |= bit;
+    else need[z >> 6] &= ~bit;
+  }
+  bool needs(int z) const { return (need[z >> 6] >> (z & 63)) & 1; }
+};
+
+// optional host-side phase timing (env VT_HOST_PROFILE=1), printed when the
+// tree is destroyed
+struct HostProf {
+  bool on = false;
+  double t[8] = {0};
+  static const char* name(int i) {
+    static const char* n[8] = {"insert", "walk", "enqueue", "events", "propagate", "prop_jobs",
+                               "borders", "other"};
+    return n[i];
+  }
+};
+struct ProfScope {
+  HostProf& p;
+  int i;
+  std::chrono::steady_clock::time_point t0;
+  ProfScope(HostProf& p_, int i_) : p(p_), i(i_) {
+    if (p.on) t0 = std::chrono::steady_clock::now();
+  }
+  ~ProfScope() {
+    if (p.on)
+      p.t[i] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+                    .count();
+  }
 };
 
 struct Tree {
+  HostProf prof;
   Geo g{};
   double tau = 0;
   int fmax = 255;
@@ -37,6 +74,7 @@ struct Tree {
   bool finished = false, borders = false;
   std::priority_queue<int32_t, std::vector<int32_t>, std::greater<int32_t>> free_slots;
   int64_t cursor = 0;
+  int64_t data_version = 0;  // bumped by every pool mutation
 
   // -- device state --
   uint8_t* d_pool = nullptr;  // [pool_slots][Sz][Sy][Sx][C] samples
@@ -55,8 +93,25 @@ struct Tree {
   std::vector<std::pair<int32_t, int64_t>> events;
 
   // -- deferred propagation (tau == 0 batches; tau > 0 per insertion) --
-  std::vector<std::unordered_map<int64_t, Pending>> pending;
+  // dirty nodes per level: pend_nodes[lvl] lists them, pend_slot[node]
+  // indexes pend_pool[lvl] (-1 = clean); flat arrays, no hashing
+  std::vector<std::vector<int64_t>> pend_nodes;
+  std::vector<std::vector<Pending>> pend_pool;
+  std::vector<int32_t> pend_slot;
   bool has_pending = false;
+  Pending& pend(int lvl, int64_t idx) {
+    int32_t& k = pend_slot[idx];
+    if (k < 0) {
+      k = (int32_t)pend_pool[lvl].size();
+      pend_pool[lvl].emplace_back();
+      pend_nodes[lvl].push_back(idx);
+    }
+    return pend_pool[lvl][k];
+  }
+  Pending* pend_find(int64_t idx, int lvl) {
+    int32_t k = pend_slot[idx];
+    return k < 0 ? nullptr : &pend_pool[lvl][k];
+  }
 
   // -- per-insertion device work lists --
   std::vector<int64_t> struct_dirty;
@@ -65,8 +120,22 @@ struct Tree {
   std::vector<SeedJob> seeds;
   std::unordered_map<int64_t, int64_t> created_seed;  // node created this insertion -> seed src
 
+  // pinned host -> device staging ring for job lists (no implicit syncs of
+  // pageable copies; wraps only after the stream has drained the old data)
+  struct Staging {
+    uint8_t* h = nullptr;
+    uint8_t* d = nullptr;
+    size_t cap = 0, head = 0;
+  };
+  mutable Staging stage;
+  void* stage_copy(const void* src, size_t bytes) const;
+  bool is_staged(const void* p) const {
+    return stage.d && p >= (const void*)stage.d && p < (const void*)(stage.d + stage.cap);
+  }
+
   // timing of the last build flush (CUDA events)
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev_wait = nullptr;  // cross-stream ordering (vt_tree_wait_stream)
   double last_build_ms = 0, last_render_ms = 0;
 
   Tree(const vt_tree_desc& d);
@@ -108,6 +177,9 @@ void launch_seed(const Tree& t, const SeedJob* d_jobs, int n);
 void launch_scatter(const Tree& t, const void* src, int channel, int src_stride, int src_off,
                     const int origin[3],
                     const int dims[3], const int g0[3], const int gn[3], const int32_t* d_leaf_slots);
+// the scatter computes a leaf plane's partial stats itself iff this holds
+bool scatter_owns_stats(const Geo& g, int channel, const int origin[3], const int dims[3], int gx,
+                        int gy);
 void launch_octant(const Tree& t, const OctJob* d_jobs, int n);
 void launch_plane(const Tree& t, const PlaneJob* d_jobs, int n);
 void launch_reduce(const Tree& t, const ReduceJob* d_jobs, int n);
@@ -121,13 +193,11 @@ void launch_pool_fill(const Tree& t, int64_t first_slot, int64_t n_slots);
 template <class T>
 T* upload(const Tree& t, const std::vector<T>& v) {
   if (v.empty()) return nullptr;
-  void* p = nullptr;
-  VT_CUDA(cudaMallocAsync(&p, v.size() * sizeof(T), t.stream));
-  VT_CUDA(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, t.stream));
-  return static_cast<T*>(p);
+  return static_cast<T*>(t.stage_copy(v.data(), v.size() * sizeof(T)));
 }
+// frees stream-ordered allocations; staging-ring pointers are recycled by the ring
 inline void release(const Tree& t, void* p) {
-  if (p) VT_CUDA(cudaFreeAsync(p, t.stream));
+  if (p && !t.is_staged(p)) VT_CUDA(cudaFreeAsync(p, t.stream));
 }
 
 }  // namespace vtx

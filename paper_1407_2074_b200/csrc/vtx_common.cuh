@@ -124,7 +124,10 @@ __host__ __device__ inline int64_t st_index(int64_t node, int stat, int c) {
 // ---------------------------------------------------------------------------
 struct StructUpd { int64_t node; int32_t flags; int32_t slot; };
 struct CreateJob { int64_t parent; int64_t seed_src; };   // seed children of parent
-struct SeedJob { int64_t node; int32_t slot; int32_t cext[3]; };
+// cov_lo/cov_hi: interior box [lo, hi) that later work of the same insertion
+// overwrites with every channel (scatter of a fused all-channel block, or the
+// octant rewrite of a fresh parent) — the seed skips it
+struct SeedJob { int64_t node; int32_t slot; int32_t cext[3]; int32_t cov_lo[3], cov_hi[3]; };
 struct OctJob {
   int32_t pslot, cslot;  // cslot < 0: brickless child, AVG fill
   int64_t child;
@@ -132,7 +135,7 @@ struct OctJob {
   int32_t cext[3];       // child in-volume extent
   int32_t r0[3], r1[3];  // region in octant-local output voxels
 };
-struct PlaneJob { int32_t slot, z, cx, cy; };
+struct PlaneJob { int32_t slot, z0, z1, cx, cy; };  // planes [z0, z1) of one brick
 struct ReduceJob { int64_t node; int32_t slot; int32_t cext[3]; int32_t leafish; };
 struct BorderJob { int64_t node; int32_t slot; };
 

@@ -73,6 +73,28 @@ def classify_homogeneous(smin, smax, threshold: float):
     return per, all(per)
 
 
+class _Pinned:
+    """Keeps a converted device temporary alive until every stream is done
+    with it (released through a device synchronisation)."""
+
+    def __init__(self, t):
+        self.t = t
+
+    def data_ptr(self):
+        return self.t.data_ptr()
+
+    @property
+    def shape(self):
+        return self.t.shape
+
+    def __del__(self):
+        try:
+            import torch
+            torch.cuda.synchronize(self.t.device)
+        except Exception:
+            pass
+
+
 class EventBatch(Sequence):
     """The change events of one or more insertions, in order: a read-only
     sequence of ChangeEvent (what insert_block / drain_events return in the
@@ -306,9 +328,15 @@ class Octree:
             if t.dim() != ndim:
                 raise ValueError(f"block values must be {ndim}-D")
             want = torch.uint8 if dt == np.uint8 else torch.uint16
+            orig = t
             t = t.to(want).contiguous()
-            # device work runs on the tree's own stream: order it after torch's
-            torch.cuda.current_stream(t.device).synchronize()
+            if t.data_ptr() != orig.data_ptr():
+                # a converted temporary must outlive the tree stream's reads
+                t = _Pinned(t)
+            # device work runs on the tree's stream: order it after torch's
+            # current stream (event wait, no host synchronisation)
+            _lib.call("vt_tree_wait_stream", self._h,
+                      ct.c_void_p(torch.cuda.current_stream(t.device).cuda_stream))
             return ct.c_void_p(t.data_ptr()), _lib.VT_MEM_DEVICE, tuple(t.shape), t
         arr = np.asarray(values)
         if arr.ndim != ndim:
@@ -350,6 +378,12 @@ class Octree:
     @property
     def root(self) -> OctreeNode:
         return self.node_by_index(0)
+
+    def use_stream(self, stream) -> None:
+        """Run this tree's device work on ``stream`` (a torch.cuda.Stream or
+        a raw cudaStream_t handle)."""
+        h = getattr(stream, "cuda_stream", stream)
+        _lib.call("vt_tree_set_stream", self._h, ct.c_void_p(int(h)))
 
     def sync(self) -> None:
         """Complete deferred device work (tau == 0 batches)."""
