@@ -211,6 +211,9 @@ typedef struct {
 typedef struct {
   int64_t samples, tf_lookups, avg_fallbacks, coarse_fallbacks, bricks_requested,
       bricks_used_marks; /* RenderCounters, render/core.py:20-31 */
+  /* not a reference counter: of `samples`, those the exact empty-space skip
+   * accounted without computing them (transfer-function alpha provably 0) */
+  int64_t samples_skipped;
 } vt_counters;
 
 /* RayBatch + CompositeState on the device (render/core.py:75-97, 100-107);

@@ -61,7 +61,8 @@ class vt_scene(ct.Structure):
 class vt_counters(ct.Structure):
     _fields_ = [("samples", ct.c_int64), ("tf_lookups", ct.c_int64),
                 ("avg_fallbacks", ct.c_int64), ("coarse_fallbacks", ct.c_int64),
-                ("bricks_requested", ct.c_int64), ("bricks_used_marks", ct.c_int64)]
+                ("bricks_requested", ct.c_int64), ("bricks_used_marks", ct.c_int64),
+                ("samples_skipped", ct.c_int64)]
 
 
 P = ct.c_void_p

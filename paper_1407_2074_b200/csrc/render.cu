@@ -15,6 +15,7 @@
 // this kernel never approaches.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <atomic>
 #include <mutex>
@@ -35,7 +36,8 @@ struct vt_mirror {
   int32_t* d_res = nullptr;  // node -> brick-buffer slot or -1 (bounded mode)
   // per brick-buffer slot, per channel: max sample over the stored brick
   // (borders included) — empty-space skipping bound; valid for slots < bmax_n
-  int32_t* d_bmax = nullptr;
+  uint16_t* d_bmax = nullptr;        // sub-brick maxima, then brick maxima
+  uint16_t* d_bmax_brick = nullptr;  // = d_bmax + bmax_cap * kMaxC
   int64_t bmax_cap = 0;
   bool bmax_valid = false;
   int64_t bmax_version = -1;  // tree data_version the zero-copy maxima reflect
@@ -66,6 +68,7 @@ struct RenderParams {
   double tf_x[kMaxC][VT_MAX_TF_POINTS];
   double tf_v[kMaxC][VT_MAX_TF_POINTS][4];
   double tf_s[kMaxC][VT_MAX_TF_POINTS][4];  // segment slopes (host FP64)
+  double tf_xzero[kMaxC];                   // alpha == 0 on [0, xzero]
   double inv_fmax;
   double inv_scl[kMaxLevels][3];  // exact: scales are powers of two
   int unit_spacing;               // spacing == (1, 1, 1): p / spacing == p
@@ -85,7 +88,10 @@ struct RenderParams {
   // alpha exactly 0 and composites to a no-op
   int ess;
   int ess_thr[kMaxC];
-  const int32_t* bmax;
+  const uint16_t* bmax;        // [slot][nsb][kMaxC] sub-brick maxima
+  const uint16_t* bmax_brick;  // [slot][kMaxC] whole-brick maxima
+  double inv_step;
+  int sbk[3], nsub[3], nsb;  // sub-brick edge, count per axis, total
 };
 
 // per-launch scene + geometry; render entry points serialise on g_render_mu
@@ -98,6 +104,7 @@ struct RayOut {
 
 struct Counters {
   long long samples, tf, avgfb, coarse, req, used;
+  long long skipped;  // samples accounted by the empty-space skip (not computed)
 };
 
 __device__ __forceinline__ double clampd(double v, double lo, double hi) {
@@ -113,6 +120,7 @@ __device__ __forceinline__ double npclip(double v, double lo, double hi) {
 // transfer-function tables staged in shared memory per block: lanes index
 // different segments, which the constant cache would serialise
 struct TFTable {
+  double xzero[kMaxC];  // TF alpha is exactly 0 for every x <= xzero (or -inf)
   double x[kMaxC][VT_MAX_TF_POINTS];
   double v[kMaxC][VT_MAX_TF_POINTS][4];
   double s[kMaxC][VT_MAX_TF_POINTS][4];
@@ -129,7 +137,10 @@ __device__ void load_tf(TFTable& T) {
     (&T.v[0][0][0])[e] = src_v[e];
     (&T.s[0][0][0])[e] = src_s[e];
   }
-  if (threadIdx.x < kMaxC) T.n[threadIdx.x] = P.tf_n[threadIdx.x];
+  if (threadIdx.x < kMaxC) {
+    T.n[threadIdx.x] = P.tf_n[threadIdx.x];
+    T.xzero[threadIdx.x] = P.tf_xzero[threadIdx.x];
+  }
   __syncthreads();
 }
 
@@ -217,6 +228,7 @@ __device__ __forceinline__ void interp4(const TFTable& T, int c, double x, doubl
 
 struct DescentCache {
   int target;
+  int clear;  // the node is transparent for the scene (empty-space skip)
   int lvl;
   long long idx;
   double lo[3];
@@ -240,14 +252,19 @@ struct Sampler {
   Counters cnt;  // by value: stays in registers
   long long last_used = -1, last_req = -1;
   // the last sample resolved to a node that is transparent for the scene's
-  // transfer functions: 1 resident brick, 2 homogeneous (AVG) node
+  // transfer functions: 1 resident brick (sub-brick), 2 homogeneous (AVG)
+  // node; box_lo/box_hi: the voxel-space box that stays transparent
   int hint = 0;
+  double box_lo[3], box_hi[3];
   DescentCache cache[TR ? NC : 1];
 
   __device__ Sampler(const uint64_t* n, uint8_t* f, const T* b, bool ff)
-      : nb(n), fb(f), bb(b), fullframe(ff), cnt{0, 0, 0, 0, 0, 0} {
+      : nb(n), fb(f), bb(b), fullframe(ff), cnt{0, 0, 0, 0, 0, 0, 0} {
 #pragma unroll
-    for (int q = 0; q < (TR ? NC : 1); ++q) cache[q].target = -1;
+    for (int q = 0; q < (TR ? NC : 1); ++q) {
+      cache[q].target = -1;
+      cache[q].clear = 0;
+    }
   }
 
   // feedback flag: idempotent OR into the byte of the node (device.py:35-36,
@@ -269,7 +286,7 @@ struct Sampler {
   // _trilerp (raycast.py:133-159) for channels [c0, c1): cell index and
   // weights once per sample, then the 8 corners of every channel
   __device__ void trilerp(uint64_t e, int lvl, const double lo[3], const double pv[3], int c0,
-                          int c1, double* out) const {
+                          int c1, double* out, int* cell = nullptr) const {
     const long long slot = (long long)((e >> 24) & 0xFFFFFFFFULL);
     int i0[3];
     double w1[3], w0[3];
@@ -282,6 +299,7 @@ struct Sampler {
       int fi = (int)floor(f);
       fi = fi < 0 ? 0 : (fi > P.g.brick[a] ? P.g.brick[a] : fi);
       i0[a] = fi;
+      if (cell) cell[a] = fi;
       w1[a] = npclip(f - (double)fi, 0.0, 1.0);
       w0[a] = 1.0 - w1[a];
     }
@@ -314,13 +332,14 @@ struct Sampler {
 
   // raycast.py:86-123 with a per-channel-group descent cache: a sample that
   // stays inside the cached node box at the same target level reuses it
-  __device__ void descend(const double pv[3], int target, DescentCache& dc) {
+  // returns true when it re-descended (a different node than the cached one)
+  __device__ bool descend(const double pv[3], int target, DescentCache& dc) {
     if (dc.target == target) {
       bool ok = true;
 #pragma unroll
       for (int a = 0; a < 3; ++a)
         if (P.g.split[a] && !(pv[a] >= dc.lo[a] && pv[a] < dc.lo[a] + P.ext[dc.lvl][a])) ok = false;
-      if (ok) return;
+      if (ok) return false;
     }
     long long idx = 0;
     int lvl = P.g.depth;
@@ -368,6 +387,32 @@ struct Sampler {
     dc.a_idx[1] = a2;
     dc.a_lvl[0] = a1l;
     dc.a_lvl[1] = a2l;
+    return true;
+  }
+
+  // transparency of the node just entered: every sample in it has TF alpha 0
+  __device__ int node_clear(uint64_t e, int c0, int c1) const {
+    if (TR || !P.ess) return 0;
+    bool clear = true;
+    if (!(e & 2)) {
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+        if (c >= c0 && c < c1) clear = clear && avg_of(e, c) <= (double)P.ess_thr[c];
+      return clear ? 2 : 0;
+    }
+    if (!(e & 1)) return 0;
+    const uint16_t* bm = P.bmax_brick + ((e >> 24) & 0xFFFFFFFFULL) * kMaxC;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) clear = clear && (int)__ldg(bm + c) <= P.ess_thr[c];
+    return clear ? 1 : 0;
+  }
+
+  __device__ void node_box(const DescentCache& dc) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      box_lo[a] = P.g.split[a] ? dc.lo[a] : -INFINITY;
+      box_hi[a] = P.g.split[a] ? dc.lo[a] + P.ext[dc.lvl][a] : INFINITY;
+    }
   }
 
   // optimal_lod (raycast.py:40-50): floor(log2(.)) is the exponent of the
@@ -386,30 +431,61 @@ struct Sampler {
   // _resolve + _fullframe_fallback (raycast.py:167-238) for channels [c0, c1)
   __device__ bool resolve(const double pv[3], int target, int c0, int c1, double* out,
                           DescentCache& dc) {
-    descend(pv, target, dc);
+    const bool moved = descend(pv, target, dc);
     const uint64_t e = __ldg(nb + dc.idx);
     const bool resident = e & 1, nh = e & 2;
+    if (moved) dc.clear = node_clear(e, c0, c1);
     if (!nh) {
-      bool clear = true;
+      if (dc.clear) {
+        // transparent homogeneous node: value irrelevant, skip its samples
+        hint = 2;
+        node_box(dc);
+        return false;
+      }
 #pragma unroll
       for (int c = 0; c < NC; ++c)
-        if (c >= c0 && c < c1) {
-          out[c] = avg_of(e, c);
-          clear = clear && out[c] <= (double)P.ess_thr[c];
-        }
-      hint = (!TR && P.ess && clear) ? 2 : 0;
+        if (c >= c0 && c < c1) out[c] = avg_of(e, c);
       return false;
     }
     if (resident) {
-      trilerp(e, dc.lvl, dc.lo, pv, c0, c1, out);
       mark(dc.idx, 1);
       cnt.used++;
-      if (!TR && P.ess) {
-        const int32_t* bm = P.bmax + ((e >> 24) & 0xFFFFFFFFULL) * kMaxC;
+      if (dc.clear) {
+        hint = 1;
+        node_box(dc);
+        return false;
+      }
+      int cell[3];
+      trilerp(e, dc.lvl, dc.lo, pv, c0, c1, out, cell);
+      if (!TR && P.ess >= 2) {
+        // sub-brick of the sample's trilinear cell: its maxima bound every
+        // corner of every sample whose cell lies in the sub-brick
+        const uint64_t slot = (e >> 24) & 0xFFFFFFFFULL;
+        int sb[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          const int q = cell[a] / P.sbk[a];
+          sb[a] = q >= P.nsub[a] ? P.nsub[a] - 1 : q;
+        }
+        const int sbi = (sb[2] * P.nsub[1] + sb[1]) * P.nsub[0] + sb[0];
+        const uint16_t* sm = P.bmax + (slot * P.nsb + sbi) * kMaxC;
         bool clear = true;
 #pragma unroll
-        for (int c = 0; c < NC; ++c) clear = clear && __ldg(bm + c) <= P.ess_thr[c];
-        hint = clear ? 1 : 0;
+        for (int c = 0; c < NC; ++c) clear = clear && (int)__ldg(sm + c) <= P.ess_thr[c];
+        if (clear) {
+          hint = 1;
+          // cells [sB, sB + B) <=> (pv - lo) / scale in [sB - 0.5, sB + B - 0.5)
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            const double sc = P.scl[dc.lvl][a];
+            const double base = dc.lo[a] - 0.5 * sc;
+            box_lo[a] = sb[a] == 0 ? (P.g.split[a] ? dc.lo[a] : -INFINITY)
+                                   : base + (double)(sb[a] * P.sbk[a]) * sc;
+            box_hi[a] = sb[a] == P.nsub[a] - 1
+                            ? (P.g.split[a] ? dc.lo[a] + P.ext[dc.lvl][a] : INFINITY)
+                            : base + (double)((sb[a] + 1) * P.sbk[a]) * sc;
+          }
+        }
       }
       return false;
     }
@@ -450,25 +526,25 @@ struct Sampler {
   // empty-space skip; each skipped sample still counts as the reference
   // counts it).  Positions are monotone in k, so checking the last one
   // suffices; the analytic estimate is verified with the sampling code.
+  // per-ray constants of the skip estimate
+  double inv_d[3], t_lod;
+  __device__ void set_ray(const double d[3]) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) inv_d[a] = d[a] != 0.0 ? 1.0 / d[a] : 0.0;
+    const double df = d[0] * P.fwd[0] + d[1] * P.fwd[1] + d[2] * P.fwd[2];
+    t_lod = df > 0.0 ? P.base_voxel / (P.pfs * P.lod_scale * df) : INFINITY;
+  }
+
   __device__ long long skip_count(long long k, long long n, double t0, const double d[3]) {
-    const DescentCache& dc = cache[0];
-    double tl = INFINITY;
+    const int target = cache[0].target;
+    double tl = target < P.g.depth ? ldexp(t_lod, target + 1) : INFINITY;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-      double lo = 0.0, hi = P.dims[a];
-      if (P.g.split[a]) {
-        lo = fmax(lo, dc.lo[a]);
-        hi = fmin(hi, dc.lo[a] + P.ext[dc.lvl][a]);
-      }
-      if (d[a] > 0.0) tl = fmin(tl, (hi * P.spacing[a] - P.cam[a]) / d[a]);
-      else if (d[a] < 0.0) tl = fmin(tl, (lo * P.spacing[a] - P.cam[a]) / d[a]);
+      const double lo = fmax(0.0, box_lo[a]), hi = fmin(P.dims[a], box_hi[a]);
+      if (d[a] > 0.0) tl = fmin(tl, (hi * P.spacing[a] - P.cam[a]) * inv_d[a]);
+      else if (d[a] < 0.0) tl = fmin(tl, (lo * P.spacing[a] - P.cam[a]) * inv_d[a]);
     }
-    if (dc.target < P.g.depth) {
-      const double df = d[0] * P.fwd[0] + d[1] * P.fwd[1] + d[2] * P.fwd[2];
-      if (df > 0.0)
-        tl = fmin(tl, ldexp(1.0, dc.target + 1) * P.base_voxel / (P.pfs * P.lod_scale) / df);
-    }
-    long long m = (long long)floor((tl - t0) / P.step) - 1 - k;
+    long long m = (long long)floor((tl - t0) * P.inv_step) - 1 - k;
     m = m < n - 1 - k ? m : n - 1 - k;
     for (int tries = 0; tries < 3 && m > 0; ++tries, m >>= 1) {
       const double t = t0 + (double)(k + m) * P.step;
@@ -479,11 +555,11 @@ struct Sampler {
       bool ok = true;
 #pragma unroll
       for (int a = 0; a < 3; ++a) ok = ok && pv[a] >= 0.0 && pv[a] <= P.dims[a];
-      if (!ok || lod(p) != dc.target) continue;
+      if (!ok || lod(p) != target) continue;
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
         const double q = npclip(pv[a], 0.0, P.dims[a] - 1e-9);
-        if (P.g.split[a] && !(q >= dc.lo[a] && q < dc.lo[a] + P.ext[dc.lvl][a])) ok = false;
+        if (!(q >= box_lo[a] && q < box_hi[a])) ok = false;
       }
       if (ok) return m;
     }
@@ -541,17 +617,22 @@ __device__ bool composite(const TFTable& T, const double* vals, RayOut& o, Count
   }
   double srgb[3] = {0.0, 0.0, 0.0};
   double trans = 1.0;
+  bool any = false;
 #pragma unroll
   for (int c = 0; c < C; ++c) {
     const double x = vals[c] * P.inv_fmax;
+    cnt.tf++;
+    // alpha exactly 0: rgb * 0 and (1 - 0) change nothing — skip the lookup
+    if (x <= T.xzero[c]) continue;
+    any = true;
     double rgba[4];
     interp4(T, c, x, rgba);
-    cnt.tf++;
     const double alpha = 1.0 - (P.corr == 1.0 ? (1.0 - rgba[3]) : pow(1.0 - rgba[3], P.corr));
 #pragma unroll
     for (int a = 0; a < 3; ++a) srgb[a] = srgb[a] + rgba[a] * alpha;
     trans = trans * (1.0 - alpha);
   }
+  if (!any) return false;  // the sample composites to a no-op
 #pragma unroll
   for (int a = 0; a < 3; ++a) srgb[a] = npclip(srgb[a], 0.0, 1.0);
   const double sa = 1.0 - trans;
@@ -588,9 +669,9 @@ __device__ void finalize(const TFTable& T, const RayOut& o, double px[4], Counte
 }
 
 __device__ void warp_add_counters(const Counters& c, unsigned long long* out) {
-  long long v[6] = {c.samples, c.tf, c.avgfb, c.coarse, c.req, c.used};
+  long long v[7] = {c.samples, c.tf, c.avgfb, c.coarse, c.req, c.used, c.skipped};
 #pragma unroll
-  for (int i = 0; i < 6; ++i) {
+  for (int i = 0; i < 7; ++i) {
     long long x = v[i];
     for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
     if ((threadIdx.x & 31) == 0 && x) atomicAdd(out + i, (unsigned long long)x);
@@ -653,6 +734,7 @@ __global__ void __launch_bounds__(128, VT_RENDER_MINB) k_render_fullframe(const 
     ray_setup(d, t0, n);
     RayOut o{};
     double vals[NC];
+    if (P.ess) s.set_ray(d);
     for (long long k = 0; k < n; ++k) {
       double t = t0 + (double)k * P.step;
       double p[3];
@@ -660,14 +742,18 @@ __global__ void __launch_bounds__(128, VT_RENDER_MINB) k_render_fullframe(const 
       for (int a = 0; a < 3; ++a) p[a] = P.cam[a] + t * d[a];
       s.sample(p, vals);
       cnt.samples++;
-      if (composite<NC>(tf, vals, o, cnt)) break;
       if (s.hint) {
+        // transparent (TF alpha exactly 0): compositing is a no-op; account
+        // this sample and the provably transparent run after it
         const long long m = s.skip_count(k, n, t0, d);
         cnt.samples += m;
-        cnt.tf += m * NC;
+        cnt.skipped += m;
+        cnt.tf += (m + 1) * NC;
         if (s.hint == 1) cnt.used += m;
         k += m;
+        continue;
       }
+      if (composite<NC>(tf, vals, o, cnt)) break;
     }
     double px[4];
     finalize<NC>(tf, o, px, cnt);
@@ -742,6 +828,7 @@ __global__ void __launch_bounds__(128) k_rays_march(RayState S,
       for (int c = 0; c < kMaxC; ++c) o.mip[c] = S.mip[r * 4 + c];
       double vals[NC];
       const double t0 = S.t0[r];
+      if (P.ess) s.set_ray(d);
       for (; k < n; ++k) {
         double t = t0 + (double)k * P.step;
         double p[3];
@@ -753,18 +840,20 @@ __global__ void __launch_bounds__(128) k_rays_march(RayState S,
           fl |= 1;
           break;
         }
+        if (s.hint) {
+          const long long m = s.skip_count(k, n, t0, d);
+          cnt.samples += m;
+          cnt.skipped += m;
+          cnt.tf += (m + 1) * NC;
+          if (s.hint == 1) cnt.used += m;
+          k += m;
+          continue;
+        }
         bool term = composite<NC>(tf, vals, o, cnt);
         if (term) {
           fl |= 2;
           ++k;
           break;
-        }
-        if (s.hint) {
-          const long long m = s.skip_count(k, n, t0, d);
-          cnt.samples += m;
-          cnt.tf += m * NC;
-          if (s.hint == 1) cnt.used += m;
-          k += m;
         }
       }
       for (int a = 0; a < 3; ++a) S.acc[r * 4 + a] = o.rgb[a];
@@ -785,7 +874,7 @@ __global__ void k_rays_image(RayState S, double* out,
   const RenderParams& P = c_P;
   __shared__ TFTable tf;
   load_tf(tf);
-  Counters cnt{0, 0, 0, 0, 0, 0};
+  Counters cnt{0, 0, 0, 0, 0, 0, 0};
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < P.W * P.H) {
     RayOut o;
@@ -801,36 +890,58 @@ __global__ void k_rays_image(RayState S, double* out,
 
 // ---- mirror kernels ------------------------------------------------------------
 
-// per-slot, per-channel maximum over the whole stored brick (borders too):
-// the bound the empty-space skip tests against.  slots == nullptr: slot = job
+// per-slot, per-sub-brick, per-channel maximum over the stored voxels any
+// trilinear corner of a sample inside the sub-brick can touch (stored
+// indices [s*B, s*B + B + 1] per axis, borders included): the bound the
+// empty-space skip tests against.  One warp per sub-brick.
 template <class T>
 __global__ void __launch_bounds__(256) k_brick_max(const T* __restrict__ bb, const int32_t* slots,
-                                                   int n, Geo g, int32_t* bmax) {
+                                                   int n, Geo g, int sb0, int sb1, int sb2,
+                                                   int nx, int ny, int nz, uint16_t* bmax,
+                                                   uint16_t* bmax_brick) {
   const int C = g.C;
-  const int64_t nvox = g.brick_elems / C;
-  __shared__ int red[8][kMaxC];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int nsb = nx * ny * nz;
+  const int ex = sb0 + 2, ey = sb1 + 2, ez = sb2 + 2;  // voxels per sub-brick range
   for (int job = blockIdx.x; job < n; job += gridDim.x) {
     const int64_t slot = slots ? slots[job] : job;
     if (slot < 0) continue;
     const T* b = bb + slot * g.brick_elems;
-    int mx[kMaxC] = {0, 0, 0, 0};
-    for (int64_t v = threadIdx.x; v < nvox; v += blockDim.x) {
+    __shared__ int s_all[kMaxC];
+    if (threadIdx.x < kMaxC) s_all[threadIdx.x] = 0;
+    __syncthreads();
+    for (int q = warp; q < nsb; q += nw) {
+      const int qx = q % nx, qy = (q / nx) % ny, qz = q / (nx * ny);
+      int mx[kMaxC] = {0, 0, 0, 0};
+      for (int v = lane; v < ex * ey * ez; v += 32) {
+        const int x = qx * sb0 + v % ex, y = qy * sb1 + (v / ex) % ey, z = qz * sb2 + v / (ex * ey);
+        if (x >= g.stored[0] || y >= g.stored[1] || z >= g.stored[2]) continue;
+        const T* p = b + g.voxel_offset(z, y, x);
 #pragma unroll
-      for (int c = 0; c < kMaxC; ++c)
-        if (c < C) mx[c] = max(mx[c], (int)b[v * C + c]);
-    }
+        for (int c = 0; c < kMaxC; ++c)
+          if (c < C) mx[c] = max(mx[c], (int)p[c]);
+      }
 #pragma unroll
-    for (int c = 0; c < kMaxC; ++c) {
-      for (int o = 16; o > 0; o >>= 1) mx[c] = max(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], o));
-      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][c] = mx[c];
+      for (int c = 0; c < kMaxC; ++c) {
+        for (int o = 16; o > 0; o >>= 1) mx[c] = max(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], o));
+        if (lane == 0) {
+          bmax[(slot * nsb + q) * kMaxC + c] = (uint16_t)mx[c];
+          atomicMax(&s_all[c], mx[c]);
+        }
+      }
     }
     __syncthreads();
-    if (threadIdx.x < kMaxC) {
-      int r = 0;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r = max(r, red[w][threadIdx.x]);
-      bmax[slot * kMaxC + threadIdx.x] = r;
-    }
+    if (threadIdx.x < kMaxC) bmax_brick[slot * kMaxC + threadIdx.x] = (uint16_t)s_all[threadIdx.x];
     __syncthreads();
+  }
+}
+
+// sub-brick edge per axis: a quarter of the brick when that divides evenly
+// into edges of at least 2 voxels, else the whole brick
+inline void sub_bricks(const Geo& g, int sbk[3], int nsub[3]) {
+  for (int a = 0; a < 3; ++a) {
+    sbk[a] = (g.brick[a] % 4 == 0 && g.brick[a] >= 8) ? g.brick[a] / 4 : g.brick[a];
+    nsub[a] = g.brick[a] / sbk[a];
   }
 }
 
@@ -890,6 +1001,16 @@ __global__ void k_upload(const int32_t* __restrict__ src_slots, const int32_t* _
 // c_P is one symbol per device: render entry points hold this lock from
 // the parameter upload until their kernels have completed
 std::mutex g_render_mu;
+
+// empty-space skip granularity: 0 off, 1 bricks, 2 bricks + sub-bricks
+// (env VT_ESS overrides the default)
+int ess_level() {
+  static int lvl = [] {
+    const char* e = std::getenv("VT_ESS");
+    return e ? std::atoi(e) : 1;
+  }();
+  return lvl;
+}
 
 // kernel instantiation for (sample type, channel count, transforms)
 template <class F>
@@ -1001,8 +1122,12 @@ void fill_params(const vt_mirror* m, const vt_scene* s, RenderParams& P) {
   P.rect[3] = P.H;
   // empty-space skip thresholds: x*_c = sup{x : TF alpha == 0 on [0, x]};
   // a sample value v is transparent when v + 0.5 <= x*_c * fmax
-  P.ess = (!P.mip && !P.has_tr && m->bmax_valid && m->d_bmax) ? 1 : 0;
+  P.ess = (!P.mip && !P.has_tr && m->bmax_valid && m->d_bmax) ? ess_level() : 0;
   P.bmax = m->d_bmax;
+  P.bmax_brick = m->d_bmax_brick;
+  P.inv_step = 1.0 / P.step;
+  sub_bricks(t.g, P.sbk, P.nsub);
+  P.nsb = P.nsub[0] * P.nsub[1] * P.nsub[2];
   for (int c = 0; c < kMaxC; ++c) P.ess_thr[c] = -1;
   for (int c = 0; c < t.g.C; ++c) {
     const int n = P.tf_n[c];
@@ -1012,11 +1137,14 @@ void fill_params(const vt_mirror* m, const vt_scene* s, RenderParams& P) {
       for (int q = 0; q + 1 < n; ++q) {
         if (P.tf_v[c][q + 1][3] != 0.0) {
           xs = P.tf_x[c][q];
+          // duplicate knot: the jump may already apply at x == xp[q]
+          if (!(P.tf_x[c][q + 1] > xs)) xs = std::nextafter(xs, -INFINITY);
           break;
         }
       }
       if (n == 1) xs = INFINITY;
     }
+    P.tf_xzero[c] = xs < 0.0 ? -INFINITY : xs;
     if (xs < 0.0) P.ess_thr[c] = -1;
     else if (!std::isfinite(xs)) P.ess_thr[c] = t.fmax;
     else P.ess_thr[c] = (int)std::max(-1.0, std::floor(xs * P.fmax - 0.5));
@@ -1032,15 +1160,20 @@ void fill_params(const vt_mirror* m, const vt_scene* s, RenderParams& P) {
 // brick-buffer slots (bounded mode, after uploads)
 static void update_bmax(vt_mirror* m, const int32_t* d_slots, int n) {
   Tree& t = m->tree->t;
-  const int64_t need = m->zero_copy ? t.pool_slots : m->slots;
+  int sbk[3], nsub[3];
+  sub_bricks(t.g, sbk, nsub);
+  const int64_t nsb = (int64_t)nsub[0] * nsub[1] * nsub[2];
+  const int64_t nslots = std::max<int64_t>(1, m->zero_copy ? t.pool_slots : m->slots);
+  const int64_t need = nslots * nsb;
   if (need > m->bmax_cap) {
     VT_CUDA(cudaStreamSynchronize(t.stream));
     cudaFree(m->d_bmax);
     m->d_bmax = nullptr;
-    VT_CUDA(cudaMalloc(&m->d_bmax, std::max<int64_t>(1, need) * kMaxC * sizeof(int32_t)));
-    VT_CUDA(cudaMemsetAsync(m->d_bmax, 0x7F, std::max<int64_t>(1, need) * kMaxC * sizeof(int32_t),
-                            t.stream));  // unknown slots never qualify as empty
+    const size_t bytes = (need + nslots) * kMaxC * sizeof(uint16_t);
+    VT_CUDA(cudaMalloc(&m->d_bmax, bytes));
+    VT_CUDA(cudaMemsetAsync(m->d_bmax, 0xFF, bytes, t.stream));  // unknown: never empty
     m->bmax_cap = need;
+    m->d_bmax_brick = m->d_bmax + need * kMaxC;
   }
   const int jobs = d_slots ? n : (int)(m->zero_copy ? t.cursor : m->slots);
   if (jobs > 0) {
@@ -1048,10 +1181,12 @@ static void update_bmax(vt_mirror* m, const int32_t* d_slots, int n) {
     const void* bb = m->zero_copy ? (const void*)t.d_pool : (const void*)m->d_bb;
     if (t.g.sb == 1)
       k_brick_max<uint8_t><<<grid, 256, 0, t.stream>>>((const uint8_t*)bb, d_slots, jobs, t.g,
-                                                       m->d_bmax);
+                                                       sbk[0], sbk[1], sbk[2], nsub[0], nsub[1],
+                                                       nsub[2], m->d_bmax, m->d_bmax_brick);
     else
       k_brick_max<uint16_t><<<grid, 256, 0, t.stream>>>((const uint16_t*)bb, d_slots, jobs, t.g,
-                                                        m->d_bmax);
+                                                        sbk[0], sbk[1], sbk[2], nsub[0], nsub[1],
+                                                        nsub[2], m->d_bmax, m->d_bmax_brick);
     VT_CUDA(cudaGetLastError());
   }
   m->bmax_valid = true;
@@ -1206,6 +1341,7 @@ static void add_counters(vt_counters* cnt, const unsigned long long* h) {
   cnt->coarse_fallbacks += (int64_t)h[3];
   cnt->bricks_requested += (int64_t)h[4];
   cnt->bricks_used_marks += (int64_t)h[5];
+  cnt->samples_skipped += (int64_t)h[6];
 }
 
 static void render_rect(vt_mirror* m, const vt_scene* scene, const int32_t* rect, void* out,
@@ -1238,8 +1374,8 @@ static void render_rect(vt_mirror* m, const vt_scene* scene, const int32_t* rect
   void* dout = out;
   if (!out_on_device) VT_CUDA(cudaMallocAsync(&dout, std::max<int64_t>(1, px) * 4 * esz, t.stream));
   unsigned long long* dc = nullptr;
-  VT_CUDA(cudaMallocAsync(&dc, 6 * sizeof(unsigned long long), t.stream));
-  VT_CUDA(cudaMemsetAsync(dc, 0, 6 * sizeof(unsigned long long), t.stream));
+  VT_CUDA(cudaMallocAsync(&dc, 7 * sizeof(unsigned long long), t.stream));
+  VT_CUDA(cudaMemsetAsync(dc, 0, 7 * sizeof(unsigned long long), t.stream));
   dim3 grid((rw + 7) / 8, (rh + 15) / 16);
   VT_CUDA(cudaEventRecord(t.ev0, t.stream));
   set_params(P, t.stream);
@@ -1252,7 +1388,7 @@ static void render_rect(vt_mirror* m, const vt_scene* scene, const int32_t* rect
     VT_CUDA(cudaGetLastError());
   }
   VT_CUDA(cudaEventRecord(t.ev1, t.stream));
-  unsigned long long h[6];
+  unsigned long long h[7];
   VT_CUDA(cudaMemcpyAsync(h, dc, sizeof(h), cudaMemcpyDeviceToHost, t.stream));
   if (!out_on_device) {
     VT_CUDA(cudaMemcpyAsync(out, dout, px * 4 * esz, cudaMemcpyDeviceToHost, t.stream));
@@ -1340,28 +1476,29 @@ vt_status vt_rays_march(vt_rays* r, int32_t strategy, vt_counters* cnt, int64_t*
     RenderParams P = r->P;
     P.borders_filled = t.borders ? 1 : 0;
     P.bmax = m->d_bmax;
-    P.ess = (!P.mip && !P.has_tr && m->bmax_valid && m->d_bmax) ? 1 : 0;
+    P.bmax_brick = m->d_bmax_brick;
+    P.ess = (!P.mip && !P.has_tr && m->bmax_valid && m->d_bmax) ? ess_level() : 0;
     P.rect[0] = 0;
     P.rect[1] = 0;
     P.rect[2] = P.W;
     P.rect[3] = P.H;
     unsigned long long* dc = nullptr;
-    VT_CUDA(cudaMallocAsync(&dc, 7 * sizeof(unsigned long long), t.stream));
-    VT_CUDA(cudaMemsetAsync(dc, 0, 7 * sizeof(unsigned long long), t.stream));
+    VT_CUDA(cudaMallocAsync(&dc, 8 * sizeof(unsigned long long), t.stream));
+    VT_CUDA(cudaMemsetAsync(dc, 0, 8 * sizeof(unsigned long long), t.stream));
     dim3 grid((P.W + 7) / 8, (P.H + 15) / 16);
     set_params(P, t.stream);
     dispatch(t.g.sb, t.g.C, P.has_tr != 0, [&](auto tag, auto nc, auto tr) {
       using T = decltype(tag);
       k_rays_march<T, decltype(nc)::value, decltype(tr)::value><<<grid, 128, 0, t.stream>>>(
-          r->S, m->d_nb, m->d_fb, (const T*)brick_ptr(m), strategy == 0, dc, dc + 6);
+          r->S, m->d_nb, m->d_fb, (const T*)brick_ptr(m), strategy == 0, dc, dc + 7);
     });
     VT_CUDA(cudaGetLastError());
-    unsigned long long h[7];
+    unsigned long long h[8];
     VT_CUDA(cudaMemcpyAsync(h, dc, sizeof(h), cudaMemcpyDeviceToHost, t.stream));
     release(t, dc);
     VT_CUDA(cudaStreamSynchronize(t.stream));
     add_counters(cnt, h);
-    if (suspended) *suspended = (int64_t)h[6];
+    if (suspended) *suspended = (int64_t)h[7];
   });
 }
 
@@ -1373,15 +1510,15 @@ vt_status vt_rays_image(vt_rays* r, double* out_host, vt_counters* cnt) {
     const int64_t n = std::max<int64_t>(1, r->n);
     VT_CUDA(cudaMallocAsync(&dout, n * 32, t.stream));
     unsigned long long* dc = nullptr;
-    VT_CUDA(cudaMallocAsync(&dc, 6 * sizeof(unsigned long long), t.stream));
-    VT_CUDA(cudaMemsetAsync(dc, 0, 6 * sizeof(unsigned long long), t.stream));
+    VT_CUDA(cudaMallocAsync(&dc, 7 * sizeof(unsigned long long), t.stream));
+    VT_CUDA(cudaMemsetAsync(dc, 0, 7 * sizeof(unsigned long long), t.stream));
     set_params(r->P, t.stream);
     dispatch(2, t.g.C, false, [&](auto, auto nc, auto) {
       k_rays_image<decltype(nc)::value><<<(unsigned)((n + 127) / 128), 128, 0, t.stream>>>(
           r->S, dout, dc);
     });
     VT_CUDA(cudaGetLastError());
-    unsigned long long h[6];
+    unsigned long long h[7];
     VT_CUDA(cudaMemcpyAsync(out_host, dout, r->n * 32, cudaMemcpyDeviceToHost, t.stream));
     VT_CUDA(cudaMemcpyAsync(h, dc, sizeof(h), cudaMemcpyDeviceToHost, t.stream));
     release(t, dout);

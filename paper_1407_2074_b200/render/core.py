@@ -17,14 +17,23 @@ class RenderCounters:
     bricks_requested: int = 0
     bricks_used_marks: int = 0
 
+    # not a reference counter (kept out of the dataclass fields, so equality
+    # and field lists match voxtree's): of ``samples``, how many the exact
+    # empty-space skip accounted without computing them
+    samples_skipped = 0
+
     def merged(self, other: "RenderCounters") -> "RenderCounters":
-        return RenderCounters(*(getattr(self, f) + getattr(other, f)
-                                for f in self.__dataclass_fields__))
+        out = RenderCounters(*(getattr(self, f) + getattr(other, f)
+                               for f in self.__dataclass_fields__))
+        out.samples_skipped = self.samples_skipped + other.samples_skipped
+        return out
 
     @classmethod
     def from_vt(cls, c) -> "RenderCounters":
-        return cls(int(c.samples), int(c.tf_lookups), int(c.avg_fallbacks),
-                   int(c.coarse_fallbacks), int(c.bricks_requested), int(c.bricks_used_marks))
+        out = cls(int(c.samples), int(c.tf_lookups), int(c.avg_fallbacks),
+                  int(c.coarse_fallbacks), int(c.bricks_requested), int(c.bricks_used_marks))
+        out.samples_skipped = int(c.samples_skipped)
+        return out
 
 
 def image_to_rgba8(image: np.ndarray) -> np.ndarray:

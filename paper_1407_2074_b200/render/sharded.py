@@ -124,9 +124,13 @@ class SortFirstRenderer:
             return cnt
         fields = list(RenderCounters.__dataclass_fields__)
         dev = "cuda" if dist.get_backend(self.group) == "nccl" else "cpu"
-        v = torch.tensor([getattr(cnt, f) for f in fields], dtype=torch.int64, device=dev)
+        v = torch.tensor([getattr(cnt, f) for f in fields] + [cnt.samples_skipped],
+                         dtype=torch.int64, device=dev)
         dist.all_reduce(v, group=self.group)
-        return RenderCounters(**{f: int(x) for f, x in zip(fields, v.tolist())})
+        vals = v.tolist()
+        out = RenderCounters(**{f: int(x) for f, x in zip(fields, vals)})
+        out.samples_skipped = int(vals[-1])
+        return out
 
     def render_fullframe(self, scene, out_kind: int = OUT_RGBA8, to_host: bool = False):
         local, cnt = self.render_part(scene, out_kind)
