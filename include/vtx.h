@@ -148,6 +148,21 @@ vt_status vt_tree_import(vt_tree* tree, int64_t n, const int64_t* indices,
                          const int32_t* flags, const int32_t* stats, const void* bricks,
                          int32_t finished, int32_t borders_filled, int64_t pruned_bricks);
 
+/* z-slab sharded build (no reference counterpart).  Export the
+ * records of the given nodes: VT_NODE_* flags, stats as vt_tree_export, and
+ * the bricks of the bricked ones in the given order into host or device
+ * memory (bricks_mem_kind). */
+vt_status vt_tree_export_nodes(vt_tree* tree, int64_t n, const int64_t* indices, int32_t* flags,
+                               int32_t* stats, void* bricks, int32_t bricks_mem_kind);
+/* Splice complete subtrees (records as exported above, parents before
+ * children not required) into this tree: ancestor chains are created as an
+ * insertion walk would create them, every ancestor above the records is
+ * given a brick and recomputed from all of its children.  With tau == 0 the
+ * result is byte-identical to inserting the subtrees' data here. */
+vt_status vt_tree_merge(vt_tree* tree, int64_t n, const int64_t* indices, const int32_t* flags,
+                        const int32_t* stats, const void* bricks, int32_t bricks_mem_kind,
+                        int64_t inserted_voxels);
+
 /* halfsample_block (octree.py:58-92) as a standalone device op on host
  * buffers: values (mz,my,mx,C) int32 -> out (mz/kz,my/ky,mx/kx,C) int32 */
 vt_status vt_halfsample(const int32_t* values, const int32_t shape[4],

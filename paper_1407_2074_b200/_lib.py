@@ -78,6 +78,8 @@ SIGNATURES = {
     "vt_tree_insert_channels": [P, PI32, PI32, P, I32],
     "vt_tree_take_events": [P, PI32, PI64, I64, PI64, PI32],
     "vt_tree_event_count": [P, PI64],
+    "vt_tree_export_nodes": [P, I64, PI64, PI32, PI32, P, I32],
+    "vt_tree_merge": [P, I64, PI64, PI32, PI32, P, I32, I64],
     "vt_tree_wait_stream": [P, P],
     "vt_tree_finalize": [P],
     "vt_tree_fill_borders": [P],

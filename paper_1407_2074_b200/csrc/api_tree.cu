@@ -12,14 +12,6 @@ const char* last_error();
 
 namespace {
 
-__global__ void k_scatter_stats(const int64_t* __restrict__ nodes, int n,
-                                const int32_t* __restrict__ in, int32_t* stats) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n * ST_N * kMaxC) return;
-  int r = i / (ST_N * kMaxC), w = i % (ST_N * kMaxC);
-  stats[nodes[r] * ST_N * kMaxC + w] = in[i];
-}
-
 // standalone halfsample_block (octree.py:58-92) on int32 values
 __global__ void k_halfsample(const int32_t* __restrict__ v, int mz, int my, int mx, int C, int cx,
                              int cy, int cz, int kx, int ky, int kz, int bg, int32_t* out) {
@@ -284,6 +276,65 @@ vt_status vt_tree_export(vt_tree* tree, int64_t n, const int64_t* indices, int32
   });
 }
 
+vt_status vt_tree_export_nodes(vt_tree* tree, int64_t n, const int64_t* indices, int32_t* nflags,
+                               int32_t* stats, void* bricks, int32_t bricks_mem_kind) {
+  return guarded([&] {
+    Tree& t = tree->t;
+    t.flush();
+    std::vector<int64_t> nodes(indices, indices + n);
+    std::vector<int32_t> slots;
+    for (int64_t r = 0; r < n; ++r) {
+      const int64_t i = nodes[r];
+      VT_REQUIRE(i >= 0 && i < t.g.capacity && (t.flags[i] & NF_EXISTS), VT_EINVAL,
+                 "export of a node that does not exist");
+      const uint8_t f = t.flags[i];
+      if (nflags)
+        nflags[r] = VT_NODE_EXISTS | ((f & NF_CHILDREN) ? VT_NODE_CHILDREN : 0) |
+                    ((f & NF_INVOL) ? VT_NODE_IN_VOLUME : 0) | ((f & NF_BRICK) ? VT_NODE_BRICK : 0);
+      if (f & NF_BRICK) slots.push_back(t.slot[i]);
+    }
+    if (stats) {
+      t.gather_stats(nodes);
+      const int C = t.g.C;
+      for (int64_t r = 0; r < n; ++r)
+        for (int c = 0; c < C; ++c)
+          for (int s2 = 0; s2 < ST_N; ++s2) stats[(r * C + c) * ST_N + s2] = t.stat(nodes[r], s2, c);
+    }
+    if (!bricks || slots.empty()) return;
+    const int64_t bb = t.g.brick_elems * t.g.sb;
+    if (bricks_mem_kind == VT_MEM_DEVICE) {
+      int32_t* ds = upload(t, slots);
+      launch_gather_bricks(t, ds, (int)slots.size(), (uint8_t*)bricks);
+      release(t, ds);
+      VT_CUDA(cudaStreamSynchronize(t.stream));
+      return;
+    }
+    const int64_t batch = std::max<int64_t>(1, (256LL << 20) / bb);
+    uint8_t* dbuf = nullptr;
+    VT_CUDA(cudaMallocAsync(&dbuf, std::min<int64_t>(batch, (int64_t)slots.size()) * bb, t.stream));
+    for (size_t o = 0; o < slots.size(); o += batch) {
+      const int m = (int)std::min<int64_t>(batch, slots.size() - o);
+      std::vector<int32_t> part(slots.begin() + o, slots.begin() + o + m);
+      int32_t* ds = upload(t, part);
+      launch_gather_bricks(t, ds, m, dbuf);
+      VT_CUDA(cudaMemcpyAsync((uint8_t*)bricks + o * bb, dbuf, m * bb, cudaMemcpyDeviceToHost,
+                              t.stream));
+      release(t, ds);
+      VT_CUDA(cudaStreamSynchronize(t.stream));
+    }
+    release(t, dbuf);
+    VT_CUDA(cudaStreamSynchronize(t.stream));
+  });
+}
+
+vt_status vt_tree_merge(vt_tree* tree, int64_t n, const int64_t* indices, const int32_t* nflags,
+                        const int32_t* stats, const void* bricks, int32_t bricks_mem_kind,
+                        int64_t inserted_voxels) {
+  return guarded([&] {
+    tree->t.merge(n, indices, nflags, stats, bricks, bricks_mem_kind, inserted_voxels);
+  });
+}
+
 vt_status vt_tree_import(vt_tree* tree, int64_t n, const int64_t* indices, const int32_t* nflags,
                          const int32_t* stats, const void* bricks, int32_t finished,
                          int32_t borders_filled, int64_t pruned_bricks) {
@@ -323,11 +374,7 @@ vt_status vt_tree_import(vt_tree* tree, int64_t n, const int64_t* indices, const
     t.flush_structure();
     int64_t* dn = upload(t, nodes);
     int32_t* dst = upload(t, st);
-    if (n) {
-      int work = (int)(n * ST_N * kMaxC);
-      k_scatter_stats<<<(work + 255) / 256, 256, 0, t.stream>>>(dn, (int)n, dst, t.d_stats);
-      VT_CUDA(cudaGetLastError());
-    }
+    launch_set_stats(t, dn, (int)n, dst);
     release(t, dn);
     release(t, dst);
     const int64_t bb = t.g.brick_elems * t.g.sb;

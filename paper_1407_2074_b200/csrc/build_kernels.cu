@@ -485,6 +485,14 @@ __global__ void k_borders(const BorderJob* __restrict__ jobs, Geo g, T* pool,
   }
 }
 
+__global__ void k_set_stats(const int64_t* __restrict__ nodes, int n,
+                            const int32_t* __restrict__ in, int32_t* stats) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n * ST_N * kMaxC) return;
+  int r = i / (ST_N * kMaxC), w = i % (ST_N * kMaxC);
+  stats[nodes[r] * ST_N * kMaxC + w] = in[i];
+}
+
 __global__ void k_gather_stats(const int64_t* __restrict__ nodes, int n,
                                const int32_t* __restrict__ stats, int32_t* out) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -625,6 +633,14 @@ void launch_gather_stats(const Tree& t, const int64_t* d_nodes, int n, int32_t* 
   int work = n * ST_N * kMaxC;
   k_gather_stats<<<(work + kThreads - 1) / kThreads, kThreads, 0, t.stream>>>(d_nodes, n,
                                                                                t.d_stats, d_out);
+  VT_CHECK_LAUNCH();
+}
+
+void launch_set_stats(const Tree& t, const int64_t* d_nodes, int n, const int32_t* d_rows) {
+  if (n <= 0) return;
+  const int work = n * ST_N * kMaxC;
+  k_set_stats<<<(work + kThreads - 1) / kThreads, kThreads, 0, t.stream>>>(d_nodes, n, d_rows,
+                                                                          t.d_stats);
   VT_CHECK_LAUNCH();
 }
 

@@ -735,6 +735,147 @@ void Tree::fill_borders() {
   borders = true;
 }
 
+// ---------------------------------------------------------------------------
+// z-slab sharded build: merge node records of complete subtrees
+// ---------------------------------------------------------------------------
+
+void Tree::merge(int64_t n, const int64_t* idx, const int32_t* nflags, const int32_t* stats_in,
+                 const void* bricks, int mem_kind, int64_t inserted_voxels) {
+  flush();
+  ++data_version;
+  const int C = g.C;
+  std::vector<int64_t> order(n);
+  for (int64_t r = 0; r < n; ++r) order[r] = r;
+  // parents before children (BFS order)
+  std::sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return idx[a] < idx[b]; });
+  creates.clear();
+  seeds.clear();
+  created_seed.clear();
+  std::vector<int64_t> rec_nodes;
+  std::vector<int32_t> rec_stats;
+  std::vector<int32_t> brick_slots;
+  std::vector<int64_t> brick_src;  // record row of each incoming brick
+  std::vector<int64_t> brick_row(n, -1);
+  int64_t nb = 0;
+  for (int64_t r = 0; r < n; ++r)
+    if (nflags[r] & VT_NODE_BRICK) brick_row[r] = nb++;
+  int top = -1;  // highest level among the records
+  for (int64_t q = 0; q < n; ++q) {
+    const int64_t r = order[q];
+    const int64_t i = idx[r];
+    VT_REQUIRE(i > 0 && i < g.capacity, VT_EINVAL, "merge: node index outside the tree");
+    const int lvl = g.level_of(i);
+    top = std::max(top, lvl);
+    // the ancestor chain exists exactly as an insertion walk would leave it
+    {
+      std::vector<int64_t> chain;
+      for (int64_t a = (i - 1) >> 3; ; a = (a - 1) >> 3) {
+        chain.push_back(a);
+        if (a == 0) break;
+      }
+      for (auto it = chain.rbegin(); it != chain.rend(); ++it) ensure_children(*it);
+    }
+    VT_REQUIRE(flags[i] & NF_EXISTS, VT_EINVAL, "merge: record is not a real octant");
+    // the record replaces the placeholder that stood here (a brick-less,
+    // childless sibling created by an insertion walk elsewhere)
+    const int f = nflags[r];
+    VT_REQUIRE(!(flags[i] & NF_CHILDREN) || (f & VT_NODE_CHILDREN), VT_EINVAL,
+               "merge: record would drop an existing subtree");
+    if (f & VT_NODE_CHILDREN) ensure_children(i);  // children records follow
+    const bool want_brick = f & VT_NODE_BRICK;
+    if (want_brick && !(flags[i] & NF_BRICK)) {
+      const int32_t s = alloc_slot();
+      flags[i] |= NF_BRICK;
+      slot[i] = s;
+      ++brick_count;
+    } else if (!want_brick && (flags[i] & NF_BRICK)) {
+      free_slots.push(slot[i]);
+      flags[i] &= ~NF_BRICK;
+      slot[i] = -1;
+      --brick_count;
+    }
+    mark_struct(i);
+    if (want_brick) {
+      brick_slots.push_back(slot[i]);
+      brick_src.push_back(brick_row[r]);
+    }
+    rec_nodes.push_back(i);
+    for (int s2 = 0; s2 < ST_N; ++s2)
+      for (int c = 0; c < kMaxC; ++c) {
+        const int v = c < C ? stats_in[(r * C + c) * ST_N + s2] : 0;
+        rec_stats.push_back(v);
+        h_stats[st_index(i, s2, c)] = v;
+      }
+  }
+  // ancestors above the merged subtrees: bricks, then a fresh recompute of
+  // every real octant, level by level (octree.py:372-387 with fresh parents)
+  std::vector<int64_t> anc;
+  for (int64_t i : rec_nodes)
+    for (int64_t a = (i - 1) >> 3; ; a = (a - 1) >> 3) {
+      if (g.level_of(a) > top) anc.push_back(a);
+      if (a == 0) break;
+    }
+  std::sort(anc.begin(), anc.end());
+  anc.erase(std::unique(anc.begin(), anc.end()), anc.end());
+  for (int64_t a : anc) {
+    if (ensure_brick(a)) {
+      SeedJob& sj = seeds.back();
+      for (int d = 0; d < 3; ++d) {
+        sj.cov_lo[d] = 0;
+        sj.cov_hi[d] = g.brick[d];
+      }
+    }
+    Pending& p = pend(g.level_of(a), a);
+    p.fresh = true;
+    has_pending = true;
+  }
+  flush_structure();
+  CreateJob* dc = upload(*this, creates);
+  launch_create(*this, dc, (int)creates.size());
+  release(*this, dc);
+  SeedJob* ds = upload(*this, seeds);
+  launch_seed(*this, ds, (int)seeds.size());
+  release(*this, ds);
+  // record stats + bricks
+  if (!rec_nodes.empty()) {
+    int64_t* dn = upload(*this, rec_nodes);
+    int32_t* dst = upload(*this, rec_stats);
+    launch_set_stats(*this, dn, (int)rec_nodes.size(), dst);
+    release(*this, dn);
+    release(*this, dst);
+  }
+  if (!brick_slots.empty()) {
+    const int64_t bb = g.brick_elems * g.sb;
+    const uint8_t* src = static_cast<const uint8_t*>(bricks);
+    uint8_t* staged = nullptr;
+    if (mem_kind == VT_MEM_HOST) {
+      VT_CUDA(cudaMallocAsync(&staged, nb * bb, stream));
+      VT_CUDA(cudaMemcpyAsync(staged, bricks, nb * bb, cudaMemcpyHostToDevice, stream));
+      src = staged;
+    }
+    // incoming bricks are in record order; scatter row brick_src[j] -> slot
+    std::vector<int32_t> slots_by_row(nb, -1);
+    for (size_t j = 0; j < brick_slots.size(); ++j) slots_by_row[brick_src[j]] = brick_slots[j];
+    int32_t* dsl = upload(*this, slots_by_row);
+    launch_scatter_bricks(*this, dsl, (int)nb, src);
+    release(*this, dsl);
+    if (staged) release(*this, staged);
+    std::vector<PlaneJob> planes;
+    for (int64_t i : rec_nodes)
+      if (flags[i] & NF_BRICK) {
+        int ce[3];
+        node_in_extent(i, ce);
+        if (ce[0] > 0 && ce[1] > 0 && ce[2] > 0) planes.push_back({slot[i], 0, ce[2], ce[0], ce[1]});
+      }
+    PlaneJob* dp = upload(*this, planes);
+    launch_plane(*this, dp, (int)planes.size());
+    release(*this, dp);
+    if (mem_kind == VT_MEM_HOST) VT_CUDA(cudaStreamSynchronize(stream));
+  }
+  inserted += inserted_voxels;
+  propagate();
+}
+
 int64_t Tree::find_node(const double pt[3], int target) const {
   int64_t idx = 0;
   int lvl = g.depth;

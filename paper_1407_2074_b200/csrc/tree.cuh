@@ -166,6 +166,10 @@ struct Tree {
   void free_brick(int64_t n);
   void fill_borders();
   int64_t find_node(const double pt[3], int target) const;
+  // z-slab sharded build: splice complete subtrees built elsewhere into this
+  // tree, then recompute every ancestor level from its children
+  void merge(int64_t n, const int64_t* idx, const int32_t* nflags, const int32_t* stats,
+             const void* bricks, int mem_kind, int64_t inserted_voxels);
 
   int32_t stat(int64_t node, int s, int c) const { return h_stats[st_index(node, s, c)]; }
 };
@@ -188,6 +192,8 @@ void launch_gather_stats(const Tree& t, const int64_t* d_nodes, int n, int32_t* 
 void launch_gather_bricks(const Tree& t, const int32_t* d_slots, int n, uint8_t* d_out);
 void launch_scatter_bricks(const Tree& t, const int32_t* d_slots, int n, const uint8_t* d_in);
 void launch_pool_fill(const Tree& t, int64_t first_slot, int64_t n_slots);
+// stats rows [n][ST_N][kMaxC] -> node stats
+void launch_set_stats(const Tree& t, const int64_t* d_nodes, int n, const int32_t* d_rows);
 
 // device scratch: stream-ordered allocation of a host vector's copy
 template <class T>
