@@ -188,24 +188,28 @@ def run_ours(args):
     def tree_on_stream(t):
         _lib.call("vt_tree_set_stream", t.handle, ct.c_void_p(stream.cuda_stream))
 
-    # ---- synthetic volume, device resident (replicated pool: every rank
-    # builds the full tree; the z-slab sharded build is SURVEY 8e / next) ----
+    # ---- synthetic volume: each rank synthesises (untimed) only the z-slab
+    # it ingests; the z-slab sharded build (slab_build.py) inserts it, one
+    # all-gather exchanges level <= k node records and every rank ends with
+    # the full tree (the replicated pool the sort-first render reads) ----
+    from paper_1407_2074_b200.slab_build import build_sharded, slab_plan
     Z, Y, X = dims[2], dims[1], dims[0]
-    vol = torch.empty((Z, Y, X, CHANNELS), dtype=torch.uint16, device="cuda")
-    _lib.call("vt_synth", ct.c_void_p(vol.data_ptr()), 1, _lib.i32x3(dims), CHANNELS, 2, 0, 0, Z,
-              ct.c_void_p(stream.cuda_stream))
-    raw_bytes = vol.numel() * 2
+    plan = slab_plan(expected_geometry(dims, BRICK), world)
+    sz0, sz1 = plan.slabs[rank]
+    vol = torch.empty((max(0, sz1 - sz0), Y, X, CHANNELS), dtype=torch.uint16, device="cuda")
+    if sz1 > sz0:
+        _lib.call("vt_synth", ct.c_void_p(vol.data_ptr()), 1, _lib.i32x3(dims), CHANNELS, 2, 0,
+                  sz0, sz1, ct.c_void_p(stream.cuda_stream))
+    raw_bytes = X * Y * Z * CHANNELS * 2  # whole job (all ranks)
 
-    def build(src, tag):
+    def build(src):
         tree = Octree(desc, cfg, reserve_slots=geo_bricks)
         tree_on_stream(tree)
         torch.cuda.synchronize()
         barrier()
         e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         e0.record(stream)
-        for z0 in range(0, Z, BRICK):
-            tree.insert_channels((0, 0, z0), src[z0:z0 + BRICK])
-        tree.sync()
+        build_sharded(tree, lambda a, b: src[a - sz0:b - sz0], slab_z=BRICK, fill_borders=False)
         e1.record(stream)
         tree.finalize()
         tree.fill_borders()
@@ -214,7 +218,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         return tree, e0.elapsed_time(e1), e1.elapsed_time(e2)
 
-    tree, build_ms, border_ms = build(vol, "device")
+    tree, build_ms, border_ms = build(vol)
     pool_bytes = tree.brick_count * cfg.brick_nbytes(desc)
     # host-slab (pinned) build through the same public call: e2e ingest
     host = vol.cpu().pin_memory() if args.build_e2e else None
@@ -222,7 +226,7 @@ def run_ours(args):
     torch.cuda.empty_cache()
     build_e2e_ms = None
     if host is not None:
-        t2, build_e2e_ms, _ = build(host.numpy(), "host")
+        t2, build_e2e_ms, _ = build(host.numpy())
         t2.close()
         del t2, host
         torch.cuda.empty_cache()
@@ -372,7 +376,9 @@ def run_ours(args):
                                    "model": "(raw + pool bytes) / insert time"},
                       "e2e_gbs_raw": round(raw_bytes / (build_e2e_ms * 1e-3) / 1e9, 2)
                       if build_e2e_ms else None,
-                      "e2e_api": "Octree.insert_channels(pinned host slabs, 32 z each)"},
+                      "e2e_api": "Octree.insert_channels(pinned host slabs, 32 z each)",
+                      "sharding": f"z-slab x{world}, level-k={plan.level} records all-gathered"
+                      if world > 1 else "single GPU"},
             "lod_sweep": sweep,
             "clocks": clocks,
         }
@@ -382,6 +388,12 @@ def run_ours(args):
     if world > 1:
         dist.barrier(device_ids=[local])
         dist.destroy_process_group()
+
+
+def expected_geometry(dims, m):
+    from paper_1407_2074_b200 import BrickPoolConfig, TreeGeometry, VolumeDescriptor
+    desc = VolumeDescriptor(dims=dims, channels=CHANNELS, sample_format=FMT)
+    return TreeGeometry.build(desc, BrickPoolConfig(brick_dims=(m,) * 3))
 
 
 def expected_bricks(dims, m):

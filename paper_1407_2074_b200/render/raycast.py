@@ -20,6 +20,21 @@ from .settings import Scene
 OUT_F64, OUT_F32, OUT_RGBA8 = 0, 1, 2
 
 
+def host_image(shape, dtype):
+    """Output array for a frame: page-locked when torch is present (its
+    caching host allocator recycles the block once the array is dropped), so
+    the device-to-host copy runs at full PCIe speed."""
+    try:
+        import torch
+        if torch.cuda.is_available():
+            tdt = {np.float64: torch.float64, np.float32: torch.float32,
+                   np.uint8: torch.uint8}[dtype]
+            return torch.empty(shape, dtype=tdt, pin_memory=True).numpy()
+    except ImportError:
+        pass
+    return np.empty(shape, dtype=dtype)
+
+
 def scene_to_vt(scene: Scene, descriptor) -> _lib.vt_scene:
     """Pack a Scene for the kernel.  Transcendental / BLAS-dependent camera
     constants are computed with numpy exactly as the reference computes them
@@ -80,7 +95,7 @@ class OutOfCoreRenderer:
         s = scene_to_vt(scene, self.descriptor)
         cam = scene.camera
         dtype = {OUT_F64: np.float64, OUT_F32: np.float32, OUT_RGBA8: np.uint8}[out_kind]
-        img = np.empty((cam.height, cam.width, 4), dtype=dtype)
+        img = host_image((cam.height, cam.width, 4), dtype)
         cnt = _lib.vt_counters()
         _lib.call("vt_render_fullframe", self.device.handle, ct.byref(s),
                   ct.c_void_p(img.ctypes.data), out_kind, 0, ct.byref(cnt))

@@ -189,12 +189,14 @@ def _all_gather_records(idx, flags, stats, bricks, inserted, tree, group):
         rec[:n, 0] = torch.as_tensor(idx, device=dev)
         rec[:n, 1] = torch.as_tensor(flags.astype(np.int64), device=dev)
         rec[:n, 2:] = torch.as_tensor(stats.reshape(n, -1).astype(np.int64), device=dev)
-    recs = torch.empty((world,) + tuple(rec.shape), dtype=rec.dtype, device=dev)
+    recs = torch.empty((world * rec.shape[0], rec.shape[1]), dtype=rec.dtype, device=dev)
     dist.all_gather_into_tensor(recs, rec, group=group)
+    recs = recs.reshape((world,) + tuple(rec.shape))
     pad = torch.zeros(max(1, bmax) * bb, dtype=torch.uint8, device=dev)
     pad[:bricks.numel()] = bricks
-    allb = torch.empty((world, pad.numel()), dtype=torch.uint8, device=dev)
+    allb = torch.empty(world * pad.numel(), dtype=torch.uint8, device=dev)
     dist.all_gather_into_tensor(allb, pad, group=group)
+    allb = allb.reshape(world, pad.numel())
     out = []
     recs = recs.cpu().numpy()
     for r, (nr, br, ins) in enumerate(metas):

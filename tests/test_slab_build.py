@@ -91,3 +91,63 @@ def test_sharded_build_matches_single_gpu(dims, brick, world, channels, fmt, tmp
         assert t.brick_count == ref.brick_count
         assert t.inserted_voxels == ref.inserted_voxels
         assert digest(t, tmp_path, f"r{r}") == want, f"rank {r} differs"
+
+
+class _Desc:
+    channels = 2
+
+
+class _Cfg:
+    @staticmethod
+    def brick_nbytes(desc):
+        return 6
+
+
+class _FakeTree:
+    descriptor = _Desc()
+    config = _Cfg()
+
+
+def _gather_worker(rank, world, port, q):
+    import os
+    import torch
+    import torch.distributed as dist
+    from paper_1407_2074_b200.slab_build import _all_gather_records
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n = 2 + rank  # ragged record counts
+        idx = np.arange(n, dtype=np.int64) + 100 * rank
+        flags = np.full(n, 9 + rank, np.int32)
+        stats = np.arange(n * 2 * 5, dtype=np.int32).reshape(n, 2, 5) + rank
+        nb = rank + 1
+        bricks = torch.arange(nb * 6, dtype=torch.uint8) + rank
+        parts = _all_gather_records(idx, flags, stats, bricks, 1000 + rank, _FakeTree(), None)
+        ok = len(parts) == world
+        for r, (i, f, s, b, ins) in enumerate(parts):
+            ok &= np.array_equal(i, np.arange(2 + r) + 100 * r)
+            ok &= bool(np.all(f == 9 + r)) and s.shape == (2 + r, 2, 5)
+            ok &= np.array_equal(s, np.arange((2 + r) * 10).reshape(2 + r, 2, 5) + r)
+            ok &= torch.equal(b, torch.arange((r + 1) * 6, dtype=torch.uint8) + r)
+            ok &= ins == 1000 + r
+        q.put(bool(ok))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_record_all_gather_gloo():
+    """the one exchange step: ragged per-rank records over a world-3 group"""
+    import socket
+    import torch.multiprocessing as mp
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gather_worker, args=(r, 3, port, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    assert all(q.get(timeout=5) for _ in range(3))
