@@ -56,7 +56,7 @@ WORKLOAD = ("cfg2: synthetic SPIM-shaped 3-ch 1024^3 uint16 volume, 32^3 bricks,
             "1 clip plane, ET 0.99, step 0.5 voxel, LOD bias 0")
 
 
-def scene_for(mod, dims, viewport, lod_bias=0.0, mode="dvr"):
+def scene_for(mod, dims, viewport, lod_bias=0.0, mode="dvr", precision=None):
     """The bench scene, built from either our package's or the reference's
     render module (identical constructors, render/settings.py:70-84)."""
     cx, cy, cz = (d / 2.0 for d in dims)
@@ -67,6 +67,8 @@ def scene_for(mod, dims, viewport, lod_bias=0.0, mode="dvr"):
            for col in COLORS[:CHANNELS]]
     clips = mod.ClipSet((mod.ClipPlane((0.0, 0.0, 1.0), CLIP_FRAC * dims[2]),))
     st = mod.RenderSettings(mode=mode, early_termination_alpha=0.99, lod_bias=lod_bias)
+    if precision is not None:  # B200 extension of RenderSettings
+        st.precision = precision
     return mod.Scene(cam, st, tfs, clips)
 
 
@@ -232,7 +234,7 @@ def run_ours(args):
         torch.cuda.empty_cache()
 
     dev = DeviceState(tree, resident_all=True)
-    scene = scene_for(R, dims, tuple(args.viewport))
+    scene = scene_for(R, dims, tuple(args.viewport), precision=args.precision)
     sfr = SortFirstRenderer(dev, strip_rows=args.strip_rows)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device="cuda")
 
@@ -275,7 +277,7 @@ def run_ours(args):
     # LOD sweep (one flushed frame each, rank-max)
     sweep = {}
     for bias in (-1.0, 0.0, 1.0, 2.0, 3.0):
-        sc = scene_for(R, dims, tuple(args.viewport), lod_bias=bias)
+        sc = scene_for(R, dims, tuple(args.viewport), lod_bias=bias, precision=args.precision)
         flush.zero_()
         torch.cuda.synchronize()
         barrier()
@@ -342,7 +344,7 @@ def run_ours(args):
             "higher_is_better": True,
             "scaling": "strong",
             "vs_baseline": None,
-            "dtype": "f64",
+            "dtype": "f64" if args.precision == "fp64" else "f32 reconstruction / f64 accumulation",
             "data": "synthetic (SPIM-shaped S volume, generated on device, seed 0)",
             "config": {"workload": WORKLOAD, "dims": list(dims), "channels": CHANNELS,
                        "sample_format": FMT, "brick": BRICK, "viewport": list(args.viewport),
@@ -566,6 +568,8 @@ def main():
     ap.add_argument("--dims", type=int, nargs=3, default=list(DIMS))
     ap.add_argument("--viewport", type=int, nargs=2, default=list(VIEWPORT))
     ap.add_argument("--strip-rows", type=int, default=8)
+    ap.add_argument("--precision", choices=("fp64", "fp32"), default="fp64",
+                    help="sample reconstruction precision (RenderSettings.precision)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-build-e2e", dest="build_e2e", action="store_false")
     args = ap.parse_args()

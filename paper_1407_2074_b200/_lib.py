@@ -55,7 +55,8 @@ class vt_scene(ct.Structure):
                 ("tf_rgba", ((ct.c_double * 4) * MAX_TF_POINTS) * 4),
                 ("n_clips", ct.c_int32), ("clip_normal", (ct.c_double * 3) * 3),
                 ("clip_offset", ct.c_double * 3), ("spacing", ct.c_double * 3),
-                ("has_transforms", ct.c_int32), ("transforms", (ct.c_double * 12) * 4)]
+                ("has_transforms", ct.c_int32), ("transforms", (ct.c_double * 12) * 4),
+                ("precision", ct.c_int32)]
 
 
 class vt_counters(ct.Structure):

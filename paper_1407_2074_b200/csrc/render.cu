@@ -88,6 +88,7 @@ struct RenderParams {
   // alpha exactly 0 and composites to a no-op
   int ess;
   int ess_thr[kMaxC];
+  int fast;                    // FP32 sample reconstruction (vt_scene.precision)
   const uint16_t* bmax;        // [slot][nsb][kMaxC] sub-brick maxima
   const uint16_t* bmax_brick;  // [slot][kMaxC] whole-brick maxima
   double inv_step;
@@ -125,6 +126,11 @@ struct TFTable {
   double v[kMaxC][VT_MAX_TF_POINTS][4];
   double s[kMaxC][VT_MAX_TF_POINTS][4];
   int n[kMaxC];
+  // FP32 copies for the float reconstruction path
+  float xzf[kMaxC];
+  float xf[kMaxC][VT_MAX_TF_POINTS];
+  float vf[kMaxC][VT_MAX_TF_POINTS][4];
+  float sf[kMaxC][VT_MAX_TF_POINTS][4];
 };
 
 __device__ void load_tf(TFTable& T) {
@@ -132,14 +138,20 @@ __device__ void load_tf(TFTable& T) {
   const double* src_x = &P.tf_x[0][0];
   const double* src_v = &P.tf_v[0][0][0];
   const double* src_s = &P.tf_s[0][0][0];
-  for (int e = threadIdx.x; e < kMaxC * VT_MAX_TF_POINTS; e += blockDim.x) (&T.x[0][0])[e] = src_x[e];
+  for (int e = threadIdx.x; e < kMaxC * VT_MAX_TF_POINTS; e += blockDim.x) {
+    (&T.x[0][0])[e] = src_x[e];
+    (&T.xf[0][0])[e] = (float)src_x[e];
+  }
   for (int e = threadIdx.x; e < kMaxC * VT_MAX_TF_POINTS * 4; e += blockDim.x) {
     (&T.v[0][0][0])[e] = src_v[e];
     (&T.s[0][0][0])[e] = src_s[e];
+    (&T.vf[0][0][0])[e] = (float)src_v[e];
+    (&T.sf[0][0][0])[e] = (float)src_s[e];
   }
   if (threadIdx.x < kMaxC) {
     T.n[threadIdx.x] = P.tf_n[threadIdx.x];
     T.xzero[threadIdx.x] = P.tf_xzero[threadIdx.x];
+    T.xzf[threadIdx.x] = (float)P.tf_xzero[threadIdx.x];
   }
   __syncthreads();
 }
@@ -226,6 +238,33 @@ __device__ __forceinline__ void interp4(const TFTable& T, int c, double x, doubl
   }
 }
 
+// the same on FP32 tables (float reconstruction path)
+__device__ __forceinline__ void interp4(const TFTable& T, int c, float x, float out[4]) {
+  const int n = T.n[c];
+  const float* xp = T.xf[c];
+  if (!(x >= xp[0])) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) out[q] = x != x ? x : T.vf[c][0][q];
+    return;
+  }
+  if (x >= xp[n - 1]) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) out[q] = T.vf[c][n - 1][q];
+    return;
+  }
+  int j = 0;
+  while (j + 2 < n && !(x < xp[j + 1])) ++j;
+  const float dx = x - xp[j];
+  const bool exact = x == xp[j];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float y0 = T.vf[c][j][q];
+    float r = exact ? y0 : fmaf(T.sf[c][j][q], dx, y0);
+    if (r != r) r = y0;
+    out[q] = r;
+  }
+}
+
 struct DescentCache {
   int target;
   int clear;  // the node is transparent for the scene (empty-space skip)
@@ -243,8 +282,12 @@ __device__ __forceinline__ int floor_log2(double v) {
 }
 
 #define P c_P
-template <class T, int NC, bool TR>
+// FAST: sample reconstruction (trilinear) and transfer functions in FP32 —
+// the north-star's "float accumulation" model; positions, LOD, descent and
+// compositing stay FP64
+template <class T, int NC, bool TR, bool FAST = false>
 struct Sampler {
+  using V = typename std::conditional<FAST, float, double>::type;
   const uint64_t* __restrict__ nb;
   uint8_t* fb;
   const T* __restrict__ bb;
@@ -286,7 +329,7 @@ struct Sampler {
   // _trilerp (raycast.py:133-159) for channels [c0, c1): cell index and
   // weights once per sample, then the 8 corners of every channel
   __device__ void trilerp(uint64_t e, int lvl, const double lo[3], const double pv[3], int c0,
-                          int c1, double* out, int* cell = nullptr) const {
+                          int c1, V* out, int* cell = nullptr) const {
     const long long slot = (long long)((e >> 24) & 0xFFFFFFFFULL);
     int i0[3];
     double w1[3], w0[3];
@@ -306,6 +349,25 @@ struct Sampler {
     constexpr int C = NC;
     const int64_t sxC = (int64_t)P.g.stored[0] * C, sxyC = sxC * P.g.stored[1];
     const T* p = bb + slot * P.g.brick_elems + i0[2] * sxyC + i0[1] * sxC + (int64_t)i0[0] * C;
+    if (FAST) {
+      // FP32: lerp along x, then y, then z (7 FMAs per channel)
+      float fx = (float)w1[0], fy = (float)w1[1], fz = (float)w1[2];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        if (c < c0 || c >= c1) continue;
+        float r[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int dz = q >> 1, dy = q & 1;
+          const T* row = p + dz * sxyC + dy * sxC + c;
+          const float a0 = (float)__ldg(row), a1 = (float)__ldg(row + C);
+          r[q] = fmaf(fx, a1 - a0, a0);
+        }
+        const float y0 = fmaf(fy, r[1] - r[0], r[0]), y1 = fmaf(fy, r[3] - r[2], r[2]);
+        out[c] = (V)fmaf(fz, y1 - y0, y0);
+      }
+      return;
+    }
     // the 8 weight products in the reference's order: (wz * wy) * wx
     double w[8];
 #pragma unroll
@@ -326,7 +388,7 @@ struct Sampler {
         const double corner = (double)__ldg(p + dz * sxyC + dy * sxC + dx * C + c);
         v = v + w[q] * corner;
       }
-      out[c] = v;
+      out[c] = (V)v;
     }
   }
 
@@ -429,7 +491,7 @@ struct Sampler {
   }
 
   // _resolve + _fullframe_fallback (raycast.py:167-238) for channels [c0, c1)
-  __device__ bool resolve(const double pv[3], int target, int c0, int c1, double* out,
+  __device__ bool resolve(const double pv[3], int target, int c0, int c1, V* out,
                           DescentCache& dc) {
     const bool moved = descend(pv, target, dc);
     const uint64_t e = __ldg(nb + dc.idx);
@@ -444,7 +506,7 @@ struct Sampler {
       }
 #pragma unroll
       for (int c = 0; c < NC; ++c)
-        if (c >= c0 && c < c1) out[c] = avg_of(e, c);
+        if (c >= c0 && c < c1) out[c] = (V)avg_of(e, c);
       return false;
     }
     if (resident) {
@@ -511,7 +573,7 @@ struct Sampler {
     }
 #pragma unroll
     for (int c = 0; c < NC; ++c)
-      if (c >= c0 && c < c1) out[c] = avg_of(e, c);
+      if (c >= c0 && c < c1) out[c] = (V)avg_of(e, c);
     cnt.avgfb++;
     return false;
   }
@@ -567,11 +629,11 @@ struct Sampler {
   }
 
   // sampler (raycast.py:242-278); returns missing
-  __device__ bool sample(const double p[3], double* vals) {
+  __device__ bool sample(const double p[3], V* vals) {
     constexpr int C = NC;
     hint = 0;
 #pragma unroll
-    for (int c = 0; c < C; ++c) vals[c] = (double)P.g.bg;
+    for (int c = 0; c < C; ++c) vals[c] = (V)P.g.bg;
     if (!TR) {
       double pv[3];
       to_voxels(p, pv);
@@ -606,6 +668,42 @@ struct Sampler {
 #undef P
 
 // composite_step (core.py:110-134); returns terminated
+template <int NC>
+__device__ bool composite(const TFTable& T, const float* vals, RayOut& o, Counters& cnt) {
+  // float reconstruction path: per-sample TF / intermix in FP32, the ray's
+  // front-to-back accumulation in FP64
+  const RenderParams& P = c_P;
+  constexpr int C = NC;
+  if (P.mip) {
+#pragma unroll
+    for (int c = 0; c < C; ++c) o.mip[c] = fmax(o.mip[c], (double)vals[c]);
+    return false;
+  }
+  float srgb[3] = {0.f, 0.f, 0.f};
+  float trans = 1.f;
+  bool any = false;
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    const float x = vals[c] * (float)P.inv_fmax;
+    cnt.tf++;
+    if (x <= T.xzf[c]) continue;
+    any = true;
+    float rgba[4];
+    interp4(T, c, x, rgba);
+    const float alpha =
+        1.f - (P.corr == 1.0 ? (1.f - rgba[3]) : powf(1.f - rgba[3], (float)P.corr));
+#pragma unroll
+    for (int a = 0; a < 3; ++a) srgb[a] = fmaf(rgba[a], alpha, srgb[a]);
+    trans = trans * (1.f - alpha);
+  }
+  if (!any) return false;
+  const double w = 1.0 - o.a;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) o.rgb[a] = o.rgb[a] + w * (double)fminf(fmaxf(srgb[a], 0.f), 1.f);
+  o.a = o.a + w * (double)(1.f - trans);
+  return P.has_et && o.a >= P.et;
+}
+
 template <int NC>
 __device__ bool composite(const TFTable& T, const double* vals, RayOut& o, Counters& cnt) {
   const RenderParams& P = c_P;
@@ -713,7 +811,7 @@ __device__ void store_px(void* out, int kind, int64_t r, const double px[4]) {
 #ifndef VT_RENDER_MINB
 #define VT_RENDER_MINB 4
 #endif
-template <class T, int NC, bool TR>
+template <class T, int NC, bool TR, bool FAST>
 __global__ void __launch_bounds__(128, VT_RENDER_MINB) k_render_fullframe(const uint64_t* __restrict__ nb,
                                                           uint8_t* fb, const T* __restrict__ bb,
                                                           void* out, int out_kind, int out_w,
@@ -722,7 +820,7 @@ __global__ void __launch_bounds__(128, VT_RENDER_MINB) k_render_fullframe(const 
   const RenderParams& P = c_P;
   __shared__ TFTable tf;
   load_tf(tf);
-  Sampler<T, NC, TR> s(nb, fb, bb, true);
+  Sampler<T, NC, TR, FAST> s(nb, fb, bb, true);
   Counters& cnt = s.cnt;
   int i, j, jl;
   bool active = pixel_of(i, j, jl);
@@ -733,7 +831,7 @@ __global__ void __launch_bounds__(128, VT_RENDER_MINB) k_render_fullframe(const 
     long long n;
     ray_setup(d, t0, n);
     RayOut o{};
-    double vals[NC];
+    typename Sampler<T, NC, TR, FAST>::V vals[NC];
     if (P.ess) s.set_ray(d);
     for (long long k = 0; k < n; ++k) {
       double t = t0 + (double)k * P.step;
@@ -1123,6 +1221,7 @@ void fill_params(const vt_mirror* m, const vt_scene* s, RenderParams& P) {
   // empty-space skip thresholds: x*_c = sup{x : TF alpha == 0 on [0, x]};
   // a sample value v is transparent when v + 0.5 <= x*_c * fmax
   P.ess = (!P.mip && !P.has_tr && m->bmax_valid && m->d_bmax) ? ess_level() : 0;
+  P.fast = s->precision == 1 ? 1 : 0;
   P.bmax = m->d_bmax;
   P.bmax_brick = m->d_bmax_brick;
   P.inv_step = 1.0 / P.step;
@@ -1147,7 +1246,8 @@ void fill_params(const vt_mirror* m, const vt_scene* s, RenderParams& P) {
     P.tf_xzero[c] = xs < 0.0 ? -INFINITY : xs;
     if (xs < 0.0) P.ess_thr[c] = -1;
     else if (!std::isfinite(xs)) P.ess_thr[c] = t.fmax;
-    else P.ess_thr[c] = (int)std::max(-1.0, std::floor(xs * P.fmax - 0.5));
+    // the float path needs a whole sample value of margin for its roundings
+    else P.ess_thr[c] = (int)std::max(-1.0, std::floor(xs * P.fmax - (P.fast ? 1.0 : 0.5)));
   }
   P.strip_rows = P.H > 0 ? P.H : 1;
   P.n_parts = 1;
@@ -1382,8 +1482,14 @@ static void render_rect(vt_mirror* m, const vt_scene* scene, const int32_t* rect
   if (px > 0) {
     dispatch(t.g.sb, t.g.C, P.has_tr != 0, [&](auto tag, auto nc, auto tr) {
       using T = decltype(tag);
-      k_render_fullframe<T, decltype(nc)::value, decltype(tr)::value><<<grid, 128, 0, t.stream>>>(
-          m->d_nb, m->d_fb, (const T*)brick_ptr(m), dout, out_kind, rw, rh, dc);
+      if (P.fast)
+        k_render_fullframe<T, decltype(nc)::value, decltype(tr)::value, true>
+            <<<grid, 128, 0, t.stream>>>(m->d_nb, m->d_fb, (const T*)brick_ptr(m), dout, out_kind,
+                                         rw, rh, dc);
+      else
+        k_render_fullframe<T, decltype(nc)::value, decltype(tr)::value, false>
+            <<<grid, 128, 0, t.stream>>>(m->d_nb, m->d_fb, (const T*)brick_ptr(m), dout, out_kind,
+                                         rw, rh, dc);
     });
     VT_CUDA(cudaGetLastError());
   }

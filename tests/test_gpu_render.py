@@ -196,3 +196,26 @@ def test_strip_partition_equals_fullframe(G, strip):
     img = assemble(torch.stack(parts), H, strip).cpu().numpy()
     assert np.array_equal(img, full)
     assert total == fcnt.samples
+
+
+@pytest.mark.parametrize("name", [n for n in scenarios.RENDER_CASES])
+def test_fp32_reconstruction_within_tolerance(name):
+    """RenderSettings.precision = "fp32" (FP32 trilinear + TFs, FP64 ray
+    accumulation) stays within the north-star tolerance of 1/255 of the
+    reference image; sample counts agree (an early-termination flip could
+    move a ray by one sample, so allow a 1e-3 relative slack)."""
+    from paper_1407_2074_b200 import DeviceState
+    from paper_1407_2074_b200.render import OutOfCoreRenderer
+    rc = scenarios.render_case(name)
+    if rc["strategy"] != "fullframe" or rc["resident"] != "all":
+        pytest.skip("fp32 applies to full-frame passes")
+    gold = GOLDEN["renders"][name]
+    _, tree, _ = build_scenario(rc["build"], borders=True)
+    scene = to_scene(rc["scene"], rc["strategy"])
+    scene.settings.precision = "fp32"
+    dev = DeviceState(tree, resident_all=True)
+    img, cnt = OutOfCoreRenderer(dev).render_fullframe(scene)
+    err = float(np.max(np.abs(img - RENDERS[name + "/image"])))
+    assert err <= TOL, f"{name}: fp32 max err {err}"
+    want = gold["counters"]["samples"]
+    assert abs(cnt.samples - want) <= max(1, 1e-3 * want)
