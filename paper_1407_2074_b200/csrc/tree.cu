@@ -284,7 +284,7 @@ void Tree::ensure_children(int64_t p) {
   }
 }
 
-bool Tree::ensure_brick(int64_t n) {
+bool Tree::ensure_brick(int64_t n, const int* cext) {
   if (flags[n] & NF_BRICK) return false;
   int32_t s = alloc_slot();
   flags[n] |= NF_BRICK;
@@ -293,7 +293,11 @@ bool Tree::ensure_brick(int64_t n) {
   SeedJob j{};
   j.node = n;
   j.slot = s;
-  node_in_extent(n, j.cext);
+  if (cext) {
+    for (int a = 0; a < 3; ++a) j.cext[a] = cext[a];
+  } else {
+    node_in_extent(n, j.cext);
+  }
   // no cover by default (set by the caller when it overwrites a region)
   seeds.push_back(j);
   ++brick_count;
@@ -414,13 +418,26 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
         int gg[3] = {gx, gy, gz};
         int64_t idx = 0;
         for (int lvl = g.depth; lvl > 0; --lvl) {
-          ensure_children(idx);
           int k = 0;
           for (int a = 0; a < 3; ++a)
             if (g.split[a] && ((gg[a] >> (lvl - 1)) & 1)) k |= 1 << a;
           idx = 8 * idx + 1 + k;
         }
-        bool fresh = ensure_brick(idx);
+        if (!(flags[idx] & NF_EXISTS)) {
+          // create the missing part of the chain, top down (creation order
+          // and seeds exactly as the reference's descent)
+          int64_t a = 0;
+          for (int lvl = g.depth; lvl > 0; --lvl) {
+            ensure_children(a);
+            int k = 0;
+            for (int q = 0; q < 3; ++q)
+              if (g.split[q] && ((gg[q] >> (lvl - 1)) & 1)) k |= 1 << q;
+            a = 8 * a + 1 + k;
+          }
+        }
+        int ce[3];
+        for (int a = 0; a < 3; ++a) ce[a] = std::max(0, std::min(M[a], g.dims[a] - gg[a] * M[a]));
+        bool fresh = ensure_brick(idx, ce);
         leaf_slots[((size_t)(gz - g0[2]) * gn[1] + (gy - g0[1])) * gn[0] + (gx - g0[0])] =
             slot[idx];
         Box b;
@@ -442,8 +459,6 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
         box_union(p, b);
         p.fresh |= fresh;
         if (g.brick[2] <= 128) {
-          int ce[3];
-          node_in_extent(idx, ce);
           if (!p.masked) {
             // first touch since the last propagation: nothing owed yet
             p.masked = true;

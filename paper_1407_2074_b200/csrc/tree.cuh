@@ -147,7 +147,7 @@ struct Tree {
   int32_t alloc_slot();
   void ensure_pool(int64_t slots_needed);
   void ensure_children(int64_t p);
-  bool ensure_brick(int64_t n);
+  bool ensure_brick(int64_t n, const int* cext = nullptr);
   void node_in_extent(int64_t idx, int c[3]) const;
 
   // insertion / propagation
