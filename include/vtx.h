@@ -106,6 +106,9 @@ vt_status vt_tree_set_stream(vt_tree* tree, void* stream);
  * `stream` (e.g. the producer of a device-resident block), without a host
  * synchronisation */
 vt_status vt_tree_wait_stream(vt_tree* tree, void* stream);
+/* the converse: make `stream` wait for everything queued on the tree so far
+ * (a caller-owned device block may then be freed or reused in stream order) */
+vt_status vt_tree_signal_stream(vt_tree* tree, void* stream);
 /* Octree.insert_block (octree.py:323-397): one channel, values (dz,dy,dx)
  * x-fastest.  Errors exactly as octree.py:331-341 (VT_EINVAL). */
 vt_status vt_tree_insert(vt_tree* tree, int32_t channel, const int32_t origin[3],
@@ -147,6 +150,12 @@ vt_status vt_tree_export(vt_tree* tree, int64_t n, const int64_t* indices, int32
 vt_status vt_tree_import(vt_tree* tree, int64_t n, const int64_t* indices,
                          const int32_t* flags, const int32_t* stats, const void* bricks,
                          int32_t finished, int32_t borders_filled, int64_t pruned_bricks);
+
+/* 64-bit digest of the whole tree computed on the device: structure, node
+ * statistics and a position-dependent hash of every brick, in BFS order.
+ * Equal trees give equal digests: the size-independent stand-in for the
+ * VXOC/VXBP sha256 at sizes where serialising tens of GB is impractical. */
+vt_status vt_tree_checksum(vt_tree* tree, uint64_t* out);
 
 /* z-slab sharded build (no reference counterpart).  Export the
  * records of the given nodes: VT_NODE_* flags, stats as vt_tree_export, and
@@ -226,6 +235,10 @@ typedef struct {
    * ~1e-15), 1 FP32 trilinear + transfer functions with FP64 ray
    * accumulation (within the 1/255 tolerance) */
   int32_t precision;
+  /* exact empty-space skipping: 0 library default (bricks), 1 off,
+   * 2 whole bricks, 3 bricks + sub-bricks.  Never changes images or
+   * counters, only how many samples are reconstructed. */
+  int32_t empty_skip;
 } vt_scene;
 
 typedef struct {

@@ -56,7 +56,7 @@ class vt_scene(ct.Structure):
                 ("n_clips", ct.c_int32), ("clip_normal", (ct.c_double * 3) * 3),
                 ("clip_offset", ct.c_double * 3), ("spacing", ct.c_double * 3),
                 ("has_transforms", ct.c_int32), ("transforms", (ct.c_double * 12) * 4),
-                ("precision", ct.c_int32)]
+                ("precision", ct.c_int32), ("empty_skip", ct.c_int32)]
 
 
 class vt_counters(ct.Structure):
@@ -79,9 +79,11 @@ SIGNATURES = {
     "vt_tree_insert_channels": [P, PI32, PI32, P, I32],
     "vt_tree_take_events": [P, PI32, PI64, I64, PI64, PI32],
     "vt_tree_event_count": [P, PI64],
+    "vt_tree_checksum": [P, ct.POINTER(ct.c_uint64)],
     "vt_tree_export_nodes": [P, I64, PI64, PI32, PI32, P, I32],
     "vt_tree_merge": [P, I64, PI64, PI32, PI32, P, I32, I64],
     "vt_tree_wait_stream": [P, P],
+    "vt_tree_signal_stream": [P, P],
     "vt_tree_finalize": [P],
     "vt_tree_fill_borders": [P],
     "vt_tree_sync": [P],

@@ -155,6 +155,16 @@ vt_status vt_tree_wait_stream(vt_tree* tree, void* stream) {
   });
 }
 
+vt_status vt_tree_signal_stream(vt_tree* tree, void* stream) {
+  return guarded([&] {
+    Tree& t = tree->t;
+    if ((cudaStream_t)stream == t.stream) return;
+    if (!t.ev_signal) VT_CUDA(cudaEventCreateWithFlags(&t.ev_signal, cudaEventDisableTiming));
+    VT_CUDA(cudaEventRecord(t.ev_signal, t.stream));
+    VT_CUDA(cudaStreamWaitEvent((cudaStream_t)stream, t.ev_signal, 0));
+  });
+}
+
 vt_status vt_tree_event_count(vt_tree* tree, int64_t* n) {
   return guarded([&] { *n = (int64_t)tree->t.events.size(); });
 }
@@ -273,6 +283,51 @@ vt_status vt_tree_export(vt_tree* tree, int64_t n, const int64_t* indices, int32
     }
     release(t, dbuf);
     VT_CUDA(cudaStreamSynchronize(t.stream));
+  });
+}
+
+vt_status vt_tree_checksum(vt_tree* tree, uint64_t* out) {
+  return guarded([&] {
+    Tree& t = tree->t;
+    t.flush();
+    std::vector<int64_t> nodes;
+    std::vector<int32_t> slots;
+    for (int64_t i = 0; i < t.g.capacity; ++i)
+      if (t.flags[i] & NF_EXISTS) {
+        nodes.push_back(i);
+        if (t.flags[i] & NF_BRICK) slots.push_back(t.slot[i]);
+      }
+    std::vector<unsigned long long> bh(slots.size());
+    if (!slots.empty()) {
+      int32_t* ds = upload(t, slots);
+      unsigned long long* dh = nullptr;
+      VT_CUDA(cudaMallocAsync(&dh, slots.size() * sizeof(unsigned long long), t.stream));
+      launch_brick_hash(t, ds, (int)slots.size(), dh);
+      VT_CUDA(cudaMemcpyAsync(bh.data(), dh, bh.size() * sizeof(unsigned long long),
+                              cudaMemcpyDeviceToHost, t.stream));
+      release(t, ds);
+      release(t, dh);
+    }
+    t.gather_stats(nodes);
+    // FNV-1a over (index, flags, stats, brick hash) in BFS order
+    uint64_t h = 1469598103934665603ULL;
+    auto eat = [&](uint64_t v) {
+      for (int b = 0; b < 8; ++b) {
+        h ^= (v >> (8 * b)) & 0xFF;
+        h *= 1099511628211ULL;
+      }
+    };
+    size_t bi = 0;
+    for (int64_t i : nodes) {
+      const uint8_t f = t.flags[i];
+      eat((uint64_t)i);
+      eat((uint64_t)(f & (NF_EXISTS | NF_CHILDREN | NF_INVOL | NF_BRICK)));
+      for (int c = 0; c < t.g.C; ++c)
+        for (int s2 = 0; s2 < ST_N; ++s2) eat((uint64_t)(uint32_t)t.stat(i, s2, c));
+      if (f & NF_BRICK) eat(bh[bi++]);
+    }
+    eat((uint64_t)t.pruned);
+    *out = h;
   });
 }
 

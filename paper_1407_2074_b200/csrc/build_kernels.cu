@@ -501,6 +501,51 @@ __global__ void k_gather_stats(const int64_t* __restrict__ nodes, int n,
   out[i] = stats[nodes[r] * ST_N * kMaxC + w];
 }
 
+// position-dependent 64-bit hash of one brick's bytes (sum of mixed words,
+// so a parallel reduction gives the same value for any thread order)
+__device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
+  x ^= x >> 33;
+  x *= 0xff51afd7ed558ccdULL;
+  x ^= x >> 33;
+  x *= 0xc4ceb9fe1a85ec53ULL;
+  x ^= x >> 33;
+  return x;
+}
+
+__global__ void __launch_bounds__(256) k_brick_hash(const int32_t* __restrict__ slots, int n,
+                                                    const uint8_t* __restrict__ pool, int64_t bytes,
+                                                    unsigned long long* out) {
+  __shared__ unsigned long long red[8];
+  for (int b = blockIdx.x; b < n; b += gridDim.x) {
+    const uint8_t* src = pool + (int64_t)slots[b] * bytes;
+    unsigned long long h = 0;
+    const int64_t words = bytes / 4;
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(src);
+    const bool aligned = ((uintptr_t)src & 3) == 0;
+    for (int64_t k = threadIdx.x; k < words; k += blockDim.x) {
+      uint32_t v;
+      if (aligned) {
+        v = w[k];
+      } else {
+        v = (uint32_t)src[4 * k] | ((uint32_t)src[4 * k + 1] << 8) |
+            ((uint32_t)src[4 * k + 2] << 16) | ((uint32_t)src[4 * k + 3] << 24);
+      }
+      h += mix64(((unsigned long long)k << 32) ^ v);
+    }
+    for (int64_t k = words * 4 + threadIdx.x; k < bytes; k += blockDim.x)
+      h += mix64((0xABCDULL << 48) ^ ((unsigned long long)k << 8) ^ src[k]);
+    for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = h;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long t = 0;
+      for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += red[q];
+      out[b] = t;
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void k_copy_bricks(const int32_t* __restrict__ slots, int n, const uint8_t* src_pool,
                               uint8_t* dst_pool, int64_t bytes, int gather) {
   int b = blockIdx.y;
@@ -633,6 +678,13 @@ void launch_gather_stats(const Tree& t, const int64_t* d_nodes, int n, int32_t* 
   int work = n * ST_N * kMaxC;
   k_gather_stats<<<(work + kThreads - 1) / kThreads, kThreads, 0, t.stream>>>(d_nodes, n,
                                                                                t.d_stats, d_out);
+  VT_CHECK_LAUNCH();
+}
+
+void launch_brick_hash(const Tree& t, const int32_t* d_slots, int n, unsigned long long* d_out) {
+  if (n <= 0) return;
+  const unsigned grid = (unsigned)std::min<int64_t>(n, 148 * 16);
+  k_brick_hash<<<grid, 256, 0, t.stream>>>(d_slots, n, t.d_pool, t.g.brick_elems * t.g.sb, d_out);
   VT_CHECK_LAUNCH();
 }
 

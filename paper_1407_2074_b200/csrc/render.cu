@@ -1220,7 +1220,8 @@ void fill_params(const vt_mirror* m, const vt_scene* s, RenderParams& P) {
   P.rect[3] = P.H;
   // empty-space skip thresholds: x*_c = sup{x : TF alpha == 0 on [0, x]};
   // a sample value v is transparent when v + 0.5 <= x*_c * fmax
-  P.ess = (!P.mip && !P.has_tr && m->bmax_valid && m->d_bmax) ? ess_level() : 0;
+  const int want_ess = s->empty_skip == 0 ? ess_level() : s->empty_skip - 1;
+  P.ess = (!P.mip && !P.has_tr && m->bmax_valid && m->d_bmax) ? want_ess : 0;
   P.fast = s->precision == 1 ? 1 : 0;
   P.bmax = m->d_bmax;
   P.bmax_brick = m->d_bmax_brick;
@@ -1295,6 +1296,7 @@ static void update_bmax(vt_mirror* m, const int32_t* d_slots, int n) {
 
 struct vt_rays {
   vt_mirror* m;
+  int ess_want = 1;
   RenderParams P;
   RayState S{};
   int64_t n = 0;
@@ -1537,6 +1539,7 @@ vt_status vt_rays_create(vt_mirror* m, const vt_scene* scene, const int32_t* til
     Tree& t = m->tree->t;
     auto* r = new vt_rays();
     r->m = m;
+    r->ess_want = scene->empty_skip == 0 ? ess_level() : scene->empty_skip - 1;
     m->refs.fetch_add(1);
     fill_params(m, scene, r->P);
     if (tile)
@@ -1583,7 +1586,7 @@ vt_status vt_rays_march(vt_rays* r, int32_t strategy, vt_counters* cnt, int64_t*
     P.borders_filled = t.borders ? 1 : 0;
     P.bmax = m->d_bmax;
     P.bmax_brick = m->d_bmax_brick;
-    P.ess = (!P.mip && !P.has_tr && m->bmax_valid && m->d_bmax) ? ess_level() : 0;
+    P.ess = (!P.mip && !P.has_tr && m->bmax_valid && m->d_bmax) ? r->ess_want : 0;
     P.rect[0] = 0;
     P.rect[1] = 0;
     P.rect[2] = P.W;

@@ -174,7 +174,7 @@ void* Tree::stage_copy(const void* src, size_t bytes) const {
 Tree::~Tree() {
   if (prof.on) {
     std::fprintf(stderr, "[vtx host profile ms]");
-    for (int i = 0; i < 8; ++i) std::fprintf(stderr, " %s=%.2f", HostProf::name(i), prof.t[i]);
+    for (int i = 0; i < 12; ++i) std::fprintf(stderr, " %s=%.2f", HostProf::name(i), prof.t[i]);
     std::fprintf(stderr, "\n");
   }
   if (stream) cudaStreamSynchronize(stream);
@@ -190,6 +190,7 @@ Tree::~Tree() {
   if (ev0) cudaEventDestroy(ev0);
   if (ev1) cudaEventDestroy(ev1);
   if (ev_wait) cudaEventDestroy(ev_wait);
+  if (ev_signal) cudaEventDestroy(ev_signal);
   if (own_stream && stream) cudaStreamDestroy(stream);
 }
 
@@ -412,6 +413,7 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
   auto* walk_scope = new ProfScope(prof, 1);
 
   // leaves (octree.py:351-360): descend, create, ensure brick, dirty box
+  auto* leaf_scope = new ProfScope(prof, 8);
   for (int gz = g0[2]; gz <= g1[2]; ++gz)
     for (int gy = g0[1]; gy <= g1[1]; ++gy)
       for (int gx = g0[0]; gx <= g1[0]; ++gx) {
@@ -464,15 +466,16 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
             p.masked = true;
             p.need[0] = p.need[1] = 0;
           }
-          if (fresh)
-            for (int z = 0; z < ce[2]; ++z) p.set_need(z, true);
+          if (fresh) p.set_need_range(0, ce[2], true);
           const bool own = scatter_owns_stats(g, channel, origin, dims, gx, gy);
           const int z0 = std::max(origin[2], gz * M[2]) - gz * M[2];
           const int z1 = std::min(std::min(origin[2] + dims[2], (gz + 1) * M[2]) - gz * M[2], ce[2]);
-          for (int z = z0; z < z1; ++z) p.set_need(z, !own);
+          p.set_need_range(z0, z1, !own);
         }
         touched[0].push_back(idx);
       }
+  delete leaf_scope;
+  auto* anc_scope = new ProfScope(prof, 9);
   // ancestors (octree.py:363-387): ensure parent bricks, record freshness
   for (int lvl = 1; lvl <= g.depth; ++lvl) {
     std::vector<int64_t>& par = touched[lvl];
@@ -494,6 +497,7 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
   }
   std::sort(touched[0].begin(), touched[0].end());
   has_pending = true;
+  delete anc_scope;
   delete walk_scope;
   ProfScope enq_scope(prof, 2);
 
@@ -601,6 +605,7 @@ void Tree::propagate() {
           }
         }
       }
+      ProfScope ql(prof, 11);
       OctJob* d = upload(*this, oct);
       launch_octant(*this, d, (int)oct.size());
       release(*this, d);
@@ -620,16 +625,18 @@ void Tree::propagate() {
       if (p.has_box && r.cext[0] > 0 && r.cext[1] > 0) {
         if (lvl == 0 && p.masked) {
           // runs of planes whose stats the scatter did not compute
-          int z = 0;
-          while (z < r.cext[2]) {
-            if (!p.needs(z)) {
-              ++z;
-              continue;
+          if (p.need[0] | p.need[1]) {
+            int z = 0;
+            while (z < r.cext[2]) {
+              if (!p.needs(z)) {
+                ++z;
+                continue;
+              }
+              int e = z;
+              while (e < r.cext[2] && p.needs(e)) ++e;
+              planes.push_back({r.slot, z, e, r.cext[0], r.cext[1]});
+              z = e;
             }
-            int e = z;
-            while (e < r.cext[2] && p.needs(e)) ++e;
-            planes.push_back({r.slot, z, e, r.cext[0], r.cext[1]});
-            z = e;
           }
         } else {
           int z1 = std::min(p.box.hi[2], r.cext[2]);
@@ -638,6 +645,7 @@ void Tree::propagate() {
       }
       reds.push_back(r);
     }
+    ProfScope ql(prof, 11);
     PlaneJob* dp = upload(*this, planes);
     launch_plane(*this, dp, (int)planes.size());
     ReduceJob* dr = upload(*this, reds);

@@ -3,6 +3,7 @@
 // Octree (octree.py:143-614) + BrickStore (paging.py) for the hot path.
 #pragma once
 
+#include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <queue>
@@ -30,6 +31,17 @@ struct Pending {
     if (v) need[z >> 6] |= bit;
     else need[z >> 6] &= ~bit;
   }
+  // planes [z0, z1) at once
+  void set_need_range(int z0, int z1, bool v) {
+    for (int w = 0; w < 2; ++w) {
+      const int lo = std::max(z0, w * 64), hi = std::min(z1, w * 64 + 64);
+      if (lo >= hi) continue;
+      const int n = hi - lo;
+      const uint64_t m = (n == 64 ? ~0ULL : ((1ULL << n) - 1)) << (lo - w * 64);
+      if (v) need[w] |= m;
+      else need[w] &= ~m;
+    }
+  }
   bool needs(int z) const { return (need[z >> 6] >> (z & 63)) & 1; }
 };
 
@@ -37,10 +49,10 @@ struct Pending {
 // tree is destroyed
 struct HostProf {
   bool on = false;
-  double t[8] = {0};
+  double t[12] = {0};
   static const char* name(int i) {
-    static const char* n[8] = {"insert", "walk", "enqueue", "events", "propagate", "prop_jobs",
-                               "borders", "other"};
+    static const char* n[12] = {"insert", "walk", "enqueue", "events", "propagate", "flush_struct",
+                                "seed", "scatter", "leaves", "ancestors", "prop_build", "prop_launch"};
     return n[i];
   }
 };
@@ -135,7 +147,8 @@ struct Tree {
 
   // timing of the last build flush (CUDA events)
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  cudaEvent_t ev_wait = nullptr;  // cross-stream ordering (vt_tree_wait_stream)
+  cudaEvent_t ev_wait = nullptr;    // cross-stream ordering (vt_tree_wait_stream)
+  cudaEvent_t ev_signal = nullptr;  // (vt_tree_signal_stream)
   double last_build_ms = 0, last_render_ms = 0;
 
   Tree(const vt_tree_desc& d);
@@ -192,6 +205,7 @@ void launch_gather_stats(const Tree& t, const int64_t* d_nodes, int n, int32_t* 
 void launch_gather_bricks(const Tree& t, const int32_t* d_slots, int n, uint8_t* d_out);
 void launch_scatter_bricks(const Tree& t, const int32_t* d_slots, int n, const uint8_t* d_in);
 void launch_pool_fill(const Tree& t, int64_t first_slot, int64_t n_slots);
+void launch_brick_hash(const Tree& t, const int32_t* d_slots, int n, unsigned long long* d_out);
 // stats rows [n][ST_N][kMaxC] -> node stats
 void launch_set_stats(const Tree& t, const int64_t* d_nodes, int n, const int32_t* d_rows);
 

@@ -74,8 +74,8 @@ def classify_homogeneous(smin, smax, threshold: float):
 
 
 class _Pinned:
-    """Keeps a converted device temporary alive until every stream is done
-    with it (released through a device synchronisation)."""
+    """A converted device temporary of an insertion (released in stream
+    order after the tree's reads, see Octree._release_source)."""
 
     def __init__(self, t):
         self.t = t
@@ -86,13 +86,6 @@ class _Pinned:
     @property
     def shape(self):
         return self.t.shape
-
-    def __del__(self):
-        try:
-            import torch
-            torch.cuda.synchronize(self.t.device)
-        except Exception:
-            pass
 
 
 class EventBatch(Sequence):
@@ -297,7 +290,7 @@ class Octree:
         with self.lock:
             _lib.call("vt_tree_insert", self._h, int(channel), _lib.i32x3(origin),
                       _lib.i32x3(bdims), src, kind)
-            del keep
+            self._release_source(keep, kind)
             return self._collect()
 
     def insert_channels(self, origin, values) -> EventBatch:
@@ -315,8 +308,19 @@ class Octree:
         with self.lock:
             _lib.call("vt_tree_insert_channels", self._h, _lib.i32x3(origin),
                       _lib.i32x3(bdims), src, kind)
-            del keep
+            self._release_source(keep, kind)
             return self._collect()
+
+    def _release_source(self, keep, kind):
+        """Borrow contract for device blocks (the reference copies the block
+        before insert_block returns): the tree reads it asynchronously, so
+        the producing torch stream is made to wait for those reads — the
+        caching allocator may then recycle the block in stream order."""
+        if kind == _lib.VT_MEM_DEVICE:
+            import torch
+            dev = keep.t.device if isinstance(keep, _Pinned) else keep.device
+            _lib.call("vt_tree_signal_stream", self._h,
+                      ct.c_void_p(torch.cuda.current_stream(dev).cuda_stream))
 
     def _source(self, values, ndim):
         dt = self.descriptor.dtype
@@ -378,6 +382,13 @@ class Octree:
     @property
     def root(self) -> OctreeNode:
         return self.node_by_index(0)
+
+    def checksum(self) -> int:
+        """Device-computed 64-bit digest of structure, statistics and every
+        brick (vt_tree_checksum) — equal trees, equal digests."""
+        out = ct.c_uint64()
+        _lib.call("vt_tree_checksum", self._h, ct.byref(out))
+        return int(out.value)
 
     def use_stream(self, stream) -> None:
         """Run this tree's device work on ``stream`` (a torch.cuda.Stream or

@@ -55,6 +55,8 @@ def scene_to_vt(scene: Scene, descriptor) -> _lib.vt_scene:
     s.width, s.height = int(cam.width), int(cam.height)
     s.mode_mip = 1 if st.mode == "mip" else 0
     s.precision = 1 if getattr(st, "precision", "fp64") == "fp32" else 0
+    s.empty_skip = {None: 0, "off": 1, "bricks": 2, "subbricks": 3}[
+        getattr(st, "empty_space_skip", None)]
     step = st.resolve_step(descriptor.spacing)
     s.step = step
     s.corr_exp = st.opacity_exponent(step)
