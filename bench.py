@@ -51,7 +51,7 @@ COLORS = ((1.0, 0.25, 0.2), (0.2, 1.0, 0.3), (0.25, 0.45, 1.0))
 BYTES_PER_POS_SAMPLE = 8 * CHANNELS * 2  # 8 trilinear corners x C x uint16
 L2_FLUSH_BYTES = 512 << 20
 FALLBACK_HBM_GBS = 6650.0
-WORKLOAD = ("cfg2: synthetic SPIM-shaped 3-ch 1024^3 uint16 volume, 32^3 bricks, tau=0, "
+WORKLOAD = ("cfg2: synthetic SPIM-shaped 3-ch uint16 volume (1024^3 by default), 32^3 bricks, tau=0, "
             "full octree build + fill_borders; 1920x1080 DVR frame, per-channel TFs, "
             "1 clip plane, ET 0.99, step 0.5 voxel, LOD bias 0")
 
@@ -168,9 +168,16 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # VT_DIST_BACKEND=gloo (test only): several ranks may share one GPU, so
+    # the multi-rank path can be exercised on a single-GPU box
+    backend = os.environ.get("VT_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     from paper_1407_2074_b200 import (BrickPoolConfig, DeviceState, Octree, VolumeDescriptor,
                                       _lib)
@@ -185,7 +192,10 @@ def run_ours(args):
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            if backend == "nccl":
+                dist.barrier(device_ids=[local])
+            else:
+                dist.barrier()
 
     def tree_on_stream(t):
         _lib.call("vt_tree_set_stream", t.handle, ct.c_void_p(stream.cuda_stream))
@@ -222,6 +232,13 @@ def run_ours(args):
 
     tree, build_ms, border_ms = build(vol)
     pool_bytes = tree.brick_count * cfg.brick_nbytes(desc)
+    # every rank must hold the same tree after the sharded build
+    ck = tree.checksum()
+    replicas_identical = True
+    if world > 1:
+        cks = [None] * world
+        dist.all_gather_object(cks, ck)
+        replicas_identical = all(c == ck for c in cks)
     # host-slab (pinned) build through the same public call: e2e ingest
     host = vol.cpu().pin_memory() if args.build_e2e else None
     del vol
@@ -264,7 +281,8 @@ def run_ours(args):
                 skipped += cnt.samples_skipped
                 launches += 1
     clocks = clk.summary()
-    t = torch.tensor(times, dtype=torch.float64, device="cuda")
+    rdev = "cuda" if backend == "nccl" else "cpu"
+    t = torch.tensor(times, dtype=torch.float64, device=rdev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.sum())
@@ -287,7 +305,7 @@ def run_ours(args):
         cnt = frame(sc)
         e1.record(stream)
         torch.cuda.synchronize()
-        tt = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+        tt = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=rdev)
         if world > 1:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt[0])
@@ -314,14 +332,14 @@ def run_ours(args):
         if it >= args.warmup:
             e2e_times.append(e0.elapsed_time(e1))
             e2e_samples += cnt.samples
-    t = torch.tensor(e2e_times, dtype=torch.float64, device="cuda")
+    t = torch.tensor(e2e_times, dtype=torch.float64, device=rdev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_value = e2e_samples / (float(t.sum()) * 1e-3) / 1e9
 
     # build numbers: max over ranks (each rank builds its replica)
     bt = torch.tensor([build_ms, border_ms, build_e2e_ms or 0.0], dtype=torch.float64,
-                      device="cuda")
+                      device=rdev)
     if world > 1:
         dist.all_reduce(bt, op=dist.ReduceOp.MAX)
     build_ms, border_ms, build_e2e_ms = (float(v) for v in bt.tolist())
@@ -350,7 +368,8 @@ def run_ours(args):
                        "sample_format": FMT, "brick": BRICK, "viewport": list(args.viewport),
                        "parallelism": f"sort-first strips x{world} (strip_rows={args.strip_rows})"
                        if world > 1 else "single GPU",
-                       "l2": "flushed between frames (512 MB write); pool 8.8 GB > L2"},
+                       "l2": f"flushed between frames (512 MB write); pool "
+                             f"{pool_bytes / 1e9:.1f} GB vs 126 MB L2"},
             "samples_per_frame": int(samples_per_frame),
             "samples_computed_per_frame": int(computed_per_frame),
             "samples_note": "samples = the reference's RenderCounters.samples (identical); "
@@ -380,7 +399,8 @@ def run_ours(args):
                       if build_e2e_ms else None,
                       "e2e_api": "Octree.insert_channels(pinned host slabs, 32 z each)",
                       "sharding": f"z-slab x{world}, level-k={plan.level} records all-gathered"
-                      if world > 1 else "single GPU"},
+                      if world > 1 else "single GPU",
+                      "tree_checksum": f"{ck:016x}", "replicas_identical": replicas_identical},
             "lod_sweep": sweep,
             "clocks": clocks,
         }
@@ -388,7 +408,7 @@ def run_ours(args):
             out["cpu_baseline"] = cpu_baseline(args)
         print(json.dumps(out), flush=True)
     if world > 1:
-        dist.barrier(device_ids=[local])
+        barrier()
         dist.destroy_process_group()
 
 

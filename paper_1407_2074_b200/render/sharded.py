@@ -107,15 +107,17 @@ class SortFirstRenderer:
         if self.world == 1:
             return local
         parts = None
+        # NCCL gathers device buffers directly; other backends stage via host
+        src = local if dist.get_backend(self.group) == "nccl" else local.cpu()
         if self.rank == self.root:
-            parts = self._buffer("parts", (self.world,) + tuple(local.shape), local.dtype,
-                                 local.device)
+            parts = self._buffer("parts", (self.world,) + tuple(src.shape), src.dtype,
+                                 src.device)
             plist = list(parts.unbind(0))
-        dist.gather(local, plist if self.rank == self.root else None, dst=self.root,
+        dist.gather(src, plist if self.rank == self.root else None, dst=self.root,
                     group=self.group)
         if self.rank != self.root:
             return None
-        return parts
+        return parts.to(local.device)
 
     def reduce_counters(self, cnt: RenderCounters) -> RenderCounters:
         import torch

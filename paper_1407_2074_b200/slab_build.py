@@ -174,7 +174,10 @@ def _all_gather_records(idx, flags, stats, bricks, inserted, tree, group):
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
-    dev = bricks.device
+    out_dev = bricks.device
+    # NCCL exchanges device buffers; other backends (gloo tests) via host
+    dev = out_dev if dist.get_backend(group) == "nccl" else torch.device("cpu")
+    bricks = bricks.to(dev)
     C = tree.descriptor.channels
     bb = tree.config.brick_nbytes(tree.descriptor)
     meta = torch.tensor([len(idx), bricks.numel() // bb, inserted], dtype=torch.int64, device=dev)
@@ -202,5 +205,6 @@ def _all_gather_records(idx, flags, stats, bricks, inserted, tree, group):
     for r, (nr, br, ins) in enumerate(metas):
         rr = recs[r, :nr]
         out.append((rr[:, 0].astype(np.int64), rr[:, 1].astype(np.int32),
-                    rr[:, 2:].astype(np.int32).reshape(nr, C, _STATS), allb[r, :br * bb], ins))
+                    rr[:, 2:].astype(np.int32).reshape(nr, C, _STATS),
+                    allb[r, :br * bb].to(out_dev), ins))
     return out
