@@ -115,7 +115,9 @@ __device__ __forceinline__ double clampd(double v, double lo, double hi) {
 // np.clip(a, lo, hi) == minimum(maximum(a, lo), hi) for non-NaN a (every
 // clipped quantity on the sampling path is finite)
 __device__ __forceinline__ double npclip(double v, double lo, double hi) {
-  return fmin(fmax(v, lo), hi);
+  // two compares + selects (no DMNMX on sm_100; fmin/fmax add NaN handling)
+  v = v < lo ? lo : v;
+  return v > hi ? hi : v;
 }
 
 // transfer-function tables staged in shared memory per block: lanes index
@@ -288,6 +290,7 @@ __device__ __forceinline__ int floor_log2(double v) {
 template <class T, int NC, bool TR, bool FAST = false>
 struct Sampler {
   using V = typename std::conditional<FAST, float, double>::type;
+  static constexpr int kC = NC;
   const uint64_t* __restrict__ nb;
   uint8_t* fb;
   const T* __restrict__ bb;
@@ -347,8 +350,9 @@ struct Sampler {
       w0[a] = 1.0 - w1[a];
     }
     constexpr int C = NC;
-    const int64_t sxC = (int64_t)P.g.stored[0] * C, sxyC = sxC * P.g.stored[1];
-    const T* p = bb + slot * P.g.brick_elems + i0[2] * sxyC + i0[1] * sxC + (int64_t)i0[0] * C;
+    // 32-bit offsets inside a brick (a stored brick is < 2^31 samples)
+    const int sxC = P.g.stored[0] * C, sxyC = sxC * P.g.stored[1];
+    const T* p = bb + slot * P.g.brick_elems + (i0[2] * sxyC + i0[1] * sxC + i0[0] * C);
     if (FAST) {
       // FP32: lerp along x, then y, then z (7 FMAs per channel)
       float fx = (float)w1[0], fy = (float)w1[1], fz = (float)w1[2];
@@ -579,8 +583,14 @@ struct Sampler {
   }
 
   __device__ __forceinline__ void to_voxels(const double q[3], double pv[3]) const {
+    // a uniform branch, so the division is not if-converted into every sample
+    if (P.unit_spacing) {
 #pragma unroll
-    for (int a = 0; a < 3; ++a) pv[a] = P.unit_spacing ? q[a] : q[a] / P.spacing[a];
+      for (int a = 0; a < 3; ++a) pv[a] = q[a];
+    } else {
+#pragma unroll
+      for (int a = 0; a < 3; ++a) pv[a] = q[a] / P.spacing[a];
+    }
   }
 
   // samples k+1 .. k+m provably resolve to the same transparent node with
@@ -668,13 +678,14 @@ struct Sampler {
 #undef P
 
 // composite_step (core.py:110-134); returns terminated
-template <int NC>
+// MODE: 0 DVR, 1 MIP, -1 read P.mip at run time
+template <int NC, int MODE = -1>
 __device__ bool composite(const TFTable& T, const float* vals, RayOut& o, Counters& cnt) {
   // float reconstruction path: per-sample TF / intermix in FP32, the ray's
   // front-to-back accumulation in FP64
   const RenderParams& P = c_P;
   constexpr int C = NC;
-  if (P.mip) {
+  if (MODE == 1 || (MODE < 0 && P.mip)) {
 #pragma unroll
     for (int c = 0; c < C; ++c) o.mip[c] = fmax(o.mip[c], (double)vals[c]);
     return false;
@@ -704,11 +715,11 @@ __device__ bool composite(const TFTable& T, const float* vals, RayOut& o, Counte
   return P.has_et && o.a >= P.et;
 }
 
-template <int NC>
+template <int NC, int MODE = -1>
 __device__ bool composite(const TFTable& T, const double* vals, RayOut& o, Counters& cnt) {
   const RenderParams& P = c_P;
   constexpr int C = NC;
-  if (P.mip) {
+  if (MODE == 1 || (MODE < 0 && P.mip)) {
 #pragma unroll
     for (int c = 0; c < C; ++c) o.mip[c] = fmax(o.mip[c], vals[c]);
     return false;
@@ -808,6 +819,37 @@ __device__ void store_px(void* out, int kind, int64_t r, const double px[4]) {
 }
 
 // fused full-frame pass: ray setup + march + finalize, no per-ray state
+// the full-frame march of one ray (render/core.py:162-187): sample,
+// composite, early termination; transparent runs skipped exactly
+template <int MODE, class S>
+__device__ __forceinline__ void march_ray(S& s, const TFTable& tf, const double d[3], double t0,
+                                          long long n, RayOut& o) {
+  const RenderParams& P = c_P;
+  constexpr int NC = S::kC;
+  typename S::V vals[NC];
+  Counters& cnt = s.cnt;
+  for (long long k = 0; k < n; ++k) {
+    double t = t0 + (double)k * P.step;
+    double p[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) p[a] = P.cam[a] + t * d[a];
+    s.sample(p, vals);
+    cnt.samples++;
+    if (MODE == 0 && s.hint) {
+      // transparent (TF alpha exactly 0): compositing is a no-op; account
+      // this sample and the provably transparent run after it
+      const long long m = s.skip_count(k, n, t0, d);
+      cnt.samples += m;
+      cnt.skipped += m;
+      cnt.tf += (m + 1) * NC;
+      if (s.hint == 1) cnt.used += m;
+      k += m;
+      continue;
+    }
+    if (composite<NC, MODE>(tf, vals, o, cnt)) break;
+  }
+}
+
 #ifndef VT_RENDER_MINB
 #define VT_RENDER_MINB 4
 #endif
@@ -831,28 +873,10 @@ __global__ void __launch_bounds__(128, VT_RENDER_MINB) k_render_fullframe(const 
     long long n;
     ray_setup(d, t0, n);
     RayOut o{};
-    typename Sampler<T, NC, TR, FAST>::V vals[NC];
     if (P.ess) s.set_ray(d);
-    for (long long k = 0; k < n; ++k) {
-      double t = t0 + (double)k * P.step;
-      double p[3];
-#pragma unroll
-      for (int a = 0; a < 3; ++a) p[a] = P.cam[a] + t * d[a];
-      s.sample(p, vals);
-      cnt.samples++;
-      if (s.hint) {
-        // transparent (TF alpha exactly 0): compositing is a no-op; account
-        // this sample and the provably transparent run after it
-        const long long m = s.skip_count(k, n, t0, d);
-        cnt.samples += m;
-        cnt.skipped += m;
-        cnt.tf += (m + 1) * NC;
-        if (s.hint == 1) cnt.used += m;
-        k += m;
-        continue;
-      }
-      if (composite<NC>(tf, vals, o, cnt)) break;
-    }
+    // one uniform branch per ray instead of a mode test per sample
+    if (P.mip) march_ray<1>(s, tf, d, t0, n, o);
+    else march_ray<0>(s, tf, d, t0, n, o);
     double px[4];
     finalize<NC>(tf, o, px, cnt);
     store_px<T>(out, out_kind, (int64_t)jl * out_w + (i - P.rect[0]), px);
