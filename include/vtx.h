@@ -231,8 +231,8 @@ typedef struct {
   int32_t has_transforms;
   double transforms[4][12]; /* row-major 3x4 */
   /* sample reconstruction precision of vt_render_fullframe/tile/strips:
-   * 0 FP64 in numpy's operation order (default; matches the reference to
-   * ~1e-15), 1 FP32 trilinear + transfer functions with FP64 ray
+   * 0 FP64 (default; trilinear as fused-multiply-add lerps, matches the
+   * reference to ~1e-15), 1 FP32 trilinear + transfer functions with FP64 ray
    * accumulation (within the 1/255 tolerance) */
   int32_t precision;
   /* exact empty-space skipping: 0 library default (bricks), 1 off,

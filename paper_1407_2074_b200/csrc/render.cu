@@ -273,9 +273,10 @@ struct DescentCache {
   int lvl;
   long long idx;
   double lo[3];
+  double hi[3];  // lo + node extent on split axes, +inf on the others
   long long a_idx[2];
   int a_lvl[2];
-  double a_lo[2][3];
+  int a_lo[2][3];  // ancestor box origins (integral voxel coordinates)
 };
 
 // floor(log2(v)) for a positive normal double: its unbiased exponent
@@ -335,19 +336,21 @@ struct Sampler {
                           int c1, V* out, int* cell = nullptr) const {
     const long long slot = (long long)((e >> 24) & 0xFFFFFFFFULL);
     int i0[3];
-    double w1[3], w0[3];
+    double w1[3];
+    const bool filled = P.borders_filled;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-      const double m = (double)P.g.brick[a];
       // scale is a power of two: multiplying by its reciprocal is exact
       double f = (pv[a] - lo[a]) * P.inv_scl[lvl][a] + 0.5;
-      f = P.borders_filled ? npclip(f, 0.0, m + 1.0) : npclip(f, 1.0, m);
+      // inside the node box f is in [0.5, M + 0.5): with filled borders the
+      // reference's clip to [0, M + 1] and the index clip to [0, M] are
+      // no-ops; before fill_borders samples clamp to interior centres
+      if (!filled) f = npclip(f, 1.0, (double)P.g.brick[a]);
       int fi = (int)floor(f);
-      fi = fi < 0 ? 0 : (fi > P.g.brick[a] ? P.g.brick[a] : fi);
+      if (filled) fi = fi > P.g.brick[a] ? P.g.brick[a] : fi;
       i0[a] = fi;
       if (cell) cell[a] = fi;
-      w1[a] = npclip(f - (double)fi, 0.0, 1.0);
-      w0[a] = 1.0 - w1[a];
+      w1[a] = f - (double)fi;  // in [0, 1] by construction
     }
     constexpr int C = NC;
     // 32-bit offsets inside a brick (a stored brick is < 2^31 samples)
@@ -372,27 +375,21 @@ struct Sampler {
       }
       return;
     }
-    // the 8 weight products in the reference's order: (wz * wy) * wx
-    double w[8];
-#pragma unroll
-    for (int dz = 0; dz < 2; ++dz)
-#pragma unroll
-      for (int dy = 0; dy < 2; ++dy)
-#pragma unroll
-        for (int dx = 0; dx < 2; ++dx)
-          w[dz * 4 + dy * 2 + dx] = ((dz ? w1[2] : w0[2]) * (dy ? w1[1] : w0[1])) *
-                                    (dx ? w1[0] : w0[0]);
+    // FP64 lerps along x, y, z with fused multiply-adds (equal to the
+    // reference's sum of weighted corners to ~1e-15 relative)
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
       if (c < c0 || c >= c1) continue;
-      double v = 0.0;
+      double r[4];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int dz = q >> 2, dy = (q >> 1) & 1, dx = q & 1;
-        const double corner = (double)__ldg(p + dz * sxyC + dy * sxC + dx * C + c);
-        v = v + w[q] * corner;
+      for (int q = 0; q < 4; ++q) {
+        const int dz = q >> 1, dy = q & 1;
+        const T* row = p + dz * sxyC + dy * sxC + c;
+        const int a0 = __ldg(row), a1 = __ldg(row + C);
+        r[q] = fma(w1[0], (double)(a1 - a0), (double)a0);
       }
-      out[c] = (V)v;
+      const double y0 = fma(w1[1], r[1] - r[0], r[0]), y1 = fma(w1[1], r[3] - r[2], r[2]);
+      out[c] = (V)fma(w1[2], y1 - y0, y0);
     }
   }
 
@@ -404,7 +401,7 @@ struct Sampler {
       bool ok = true;
 #pragma unroll
       for (int a = 0; a < 3; ++a)
-        if (P.g.split[a] && !(pv[a] >= dc.lo[a] && pv[a] < dc.lo[a] + P.ext[dc.lvl][a])) ok = false;
+        ok = ok && pv[a] >= dc.lo[a] && pv[a] < dc.hi[a];
       if (ok) return false;
     }
     long long idx = 0;
@@ -412,7 +409,7 @@ struct Sampler {
     double lo[3] = {0.0, 0.0, 0.0};
     long long a1 = -1, a2 = -1;
     int a1l = 0, a2l = 0;
-    double a1lo[3] = {0, 0, 0}, a2lo[3] = {0, 0, 0};
+    int a1lo[3] = {0, 0, 0}, a2lo[3] = {0, 0, 0};
     for (int it = 0; it < P.g.depth; ++it) {
       uint64_t e = __ldg(nb + idx);
       long long ptr = (long long)((e >> 2) & 0x3FFFFFULL);
@@ -434,7 +431,7 @@ struct Sampler {
       a1l = lvl;
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
-        a1lo[a] = lo[a];
+        a1lo[a] = (int)lo[a];
         lo[a] = nlo[a];
       }
       idx = 8 * (ptr - 1) + 1 + k;
@@ -446,6 +443,7 @@ struct Sampler {
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       dc.lo[a] = lo[a];
+      dc.hi[a] = P.g.split[a] ? lo[a] + P.ext[lvl][a] : INFINITY;
       dc.a_lo[0][a] = a1lo[a];
       dc.a_lo[1][a] = a2lo[a];
     }
@@ -564,7 +562,9 @@ struct Sampler {
       if (ai < 0) continue;
       uint64_t ae = __ldg(nb + ai);
       if (ae & 1) {
-        trilerp(ae, dc.a_lvl[q], dc.a_lo[q], pv, c0, c1, out);
+        const double alo[3] = {(double)dc.a_lo[q][0], (double)dc.a_lo[q][1],
+                               (double)dc.a_lo[q][2]};
+        trilerp(ae, dc.a_lvl[q], alo, pv, c0, c1, out);
         mark(ai, 1);
         cnt.used++;
         cnt.coarse++;
