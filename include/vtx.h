@@ -130,6 +130,15 @@ vt_status vt_tree_fill_borders(vt_tree* tree);
 /* complete all deferred device work and wait for it */
 vt_status vt_tree_sync(vt_tree* tree);
 vt_status vt_tree_info_get(vt_tree* tree, vt_tree_info* out);
+/* B200 extension: threshold-0 dense build (dense_build.cu).  A fused
+ * all-channel block spanning the full x/y extent and whole brick layers over
+ * brick-less leaves (ingest_bulk's z-slabs, ingest.py:182-224) writes its
+ * leaf bricks and statistics outright, and parents whose in-volume children
+ * are all complete are recomputed in one pass; results, events and slots are
+ * identical to the general path.  Enabled by default (env VT_DENSE=0 or
+ * enabled = 0 turns it off); counts = dense leaf insertions / dense parents. */
+vt_status vt_tree_set_dense(vt_tree* tree, int32_t enabled);
+vt_status vt_tree_dense_counts(vt_tree* tree, int64_t* leaf_inserts, int64_t* level_nodes);
 /* Octree.node_by_index (octree.py:515-528): *exists = 0 when absent */
 vt_status vt_tree_node(vt_tree* tree, int64_t index, vt_node* out, int32_t* exists);
 /* Octree.iter_nodes order (BFS == ascending index, octree.py:507-513);

@@ -169,6 +169,20 @@ vt_status vt_tree_event_count(vt_tree* tree, int64_t* n) {
   return guarded([&] { *n = (int64_t)tree->t.events.size(); });
 }
 
+vt_status vt_tree_set_dense(vt_tree* tree, int32_t enabled) {
+  return guarded([&] {
+    tree->t.flush();
+    tree->t.dense_enabled = enabled != 0;
+  });
+}
+
+vt_status vt_tree_dense_counts(vt_tree* tree, int64_t* leaf_inserts, int64_t* level_nodes) {
+  return guarded([&] {
+    if (leaf_inserts) *leaf_inserts = tree->t.dense_leaf_inserts;
+    if (level_nodes) *level_nodes = tree->t.dense_level_nodes;
+  });
+}
+
 vt_status vt_tree_finalize(vt_tree* tree) {
   return guarded([&] { tree->t.finished = true; });
 }

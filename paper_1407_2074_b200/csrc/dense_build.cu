@@ -1,0 +1,856 @@
+// Dense (pyramid) build kernels for homogeneity threshold 0.
+//
+// At tau == 0 nothing is ever pruned and every brick whose in-volume leaves
+// are fully covered by inserted data is a pure function of that data
+// (SURVEY 7.3.1): a leaf brick is the block copied at +1 with a background
+// shell, a parent brick the 2x2x2 integer half-sample of its children
+// (halfsample_block, octree.py:58-92).  When an insertion covers whole brick
+// layers over the full x/y extent (ingest_bulk's z-slabs, ingest.py:182-224,
+// or a VSTR layer), the tree control plane (tree.cu) routes its device work
+// here instead of the general seed -> scatter -> octant-job pipeline:
+//
+//   k_dense_leaf   one CTA per leaf brick: writes the WHOLE stored brick
+//                  (shell + interior, one coalesced pass), the per-plane
+//                  partial statistics and the leaf's final statistics
+//                  (_write_leaf + _ensure_brick + _recompute_stats,
+//                  octree.py:225-263, 420-442)
+//   k_dense_level  one CTA per parent whose in-volume children are all
+//                  complete: its whole interior from the children
+//                  (_update_parent_octant for every real octant,
+//                  octree.py:281-319), plane partials, final statistics and
+//                  _aggregate_subtree_extrema (octree.py:265-277)
+//
+// Results are byte-identical to the general path (tests/test_gpu_dense.py);
+// the host emits the same events, slots and structure either way.
+#include <algorithm>
+#include <climits>
+#include <cstdlib>
+
+#include <cuda.h>
+
+#include "tree.cuh"
+
+namespace vtx {
+
+namespace {
+
+template <int C>
+struct Acc {
+  int mn[C], mx[C];
+  unsigned long long sm[C];
+  __device__ void init() {
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      mn[c] = INT_MAX;
+      mx[c] = INT_MIN;
+      sm[c] = 0;
+    }
+  }
+  __device__ void add(int c, int v) {
+#pragma unroll
+    for (int q = 0; q < C; ++q)
+      if (q == c) {
+        mn[q] = min(mn[q], v);
+        mx[q] = max(mx[q], v);
+        sm[q] += (unsigned)v;
+      }
+  }
+  __device__ void add_all(const int* v) {
+#pragma unroll
+    for (int q = 0; q < C; ++q) {
+      mn[q] = min(mn[q], v[q]);
+      mx[q] = max(mx[q], v[q]);
+      sm[q] += (unsigned)v[q];
+    }
+  }
+  __device__ void warp_reduce() {
+#pragma unroll
+    for (int c = 0; c < C; ++c)
+      for (int o = 16; o > 0; o >>= 1) {
+        mn[c] = min(mn[c], __shfl_xor_sync(0xffffffffu, mn[c], o));
+        mx[c] = max(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], o));
+        sm[c] += __shfl_xor_sync(0xffffffffu, sm[c], o);
+      }
+  }
+  __device__ void merge(const Acc& o) {
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      mn[c] = min(mn[c], o.mn[c]);
+      mx[c] = max(mx[c], o.mx[c]);
+      sm[c] += o.sm[c];
+    }
+  }
+};
+
+constexpr int kMaxWarps = 17;
+
+// CTA-wide reduction of the per-warp totals (held by lane 0 of each warp),
+// then the node's final statistics: avg (round_mean, octree.py:53-55),
+// smin, smax; sub extrema = own for leaves / childless nodes, else the
+// aggregate over existing in-volume children (octree.py:265-277)
+template <int C>
+__device__ void finish_stats(Acc<C>& tot, int64_t node, int64_t nvox, bool leafish, const Geo& g,
+                             const uint8_t* __restrict__ flags, int32_t* stats) {
+  __shared__ int s_mn[kMaxWarps][C], s_mx[kMaxWarps][C];
+  __shared__ unsigned long long s_sm[kMaxWarps][C];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (lane == 0)
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      s_mn[warp][c] = tot.mn[c];
+      s_mx[warp][c] = tot.mx[c];
+      s_sm[warp][c] = tot.sm[c];
+    }
+  __syncthreads();
+  if (threadIdx.x >= C) return;
+  const int c = threadIdx.x;
+  if (nvox > 0) {
+    int a = INT_MAX, b = INT_MIN;
+    unsigned long long s = 0;
+    for (int w = 0; w < nw; ++w) {
+      a = min(a, s_mn[w][c]);
+      b = max(b, s_mx[w][c]);
+      s += s_sm[w][c];
+    }
+    const long long avg = (2 * (long long)s + nvox) / (2 * nvox);
+    stats[st_index(node, ST_AVG, c)] = (int)avg;
+    stats[st_index(node, ST_MIN, c)] = a;
+    stats[st_index(node, ST_MAX, c)] = b;
+    if (leafish) {
+      stats[st_index(node, ST_SUBMIN, c)] = a;
+      stats[st_index(node, ST_SUBMAX, c)] = b;
+    }
+  }
+  if (!leafish) {
+    bool any = false;
+    int lo = 0, hi = 0;
+    for (int k = 0; k < 8; ++k) {
+      if (!g.octant_real(k)) continue;
+      const int64_t ch = 8 * node + 1 + k;
+      const uint8_t f = flags[ch];
+      if (!(f & NF_EXISTS) || !(f & NF_INVOL)) continue;
+      const int a = stats[st_index(ch, ST_SUBMIN, c)], b = stats[st_index(ch, ST_SUBMAX, c)];
+      lo = any ? min(lo, a) : a;
+      hi = any ? max(hi, b) : b;
+      any = true;
+    }
+    if (any) {
+      stats[st_index(node, ST_SUBMIN, c)] = lo;
+      stats[st_index(node, ST_SUBMAX, c)] = hi;
+    }
+  }
+}
+
+// lane 0 of a warp: write one plane's partials (layout of k_plane) and fold
+// them into the warp's running total
+template <int C>
+__device__ void emit_plane(Acc<C>& pl, Acc<C>& tot, int64_t slot, int mz, int z, int32_t* pmin,
+                           int32_t* pmax, unsigned long long* psum) {
+  pl.warp_reduce();
+  if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      const int64_t off = (slot * mz + z) * C + c;
+      pmin[off] = pl.mn[c];
+      pmax[off] = pl.mx[c];
+      psum[off] = pl.sm[c];
+    }
+    tot.merge(pl);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// leaves
+// ---------------------------------------------------------------------------
+// One CTA per leaf brick of a block that spans the volume's full x/y extent
+// and whole brick layers in z.  Warps own stored planes; a plane is written
+// as one linear run (rows are contiguous in the stored brick), so stores are
+// fully coalesced.  Generic per-sample version (8-bit samples, odd rows).
+template <class T, int C>
+__global__ void __launch_bounds__(384, 2) k_dense_leaf(const T* __restrict__ src, int oz,
+                                                    const DenseJob* __restrict__ jobs, int gnx,
+                                                    int gny, int g0z, Geo g, T* __restrict__ pool,
+                                                    int32_t* pmin, int32_t* pmax,
+                                                    unsigned long long* psum, int32_t* stats,
+                                                    const uint8_t* __restrict__ flags,
+                                                    int planes_per_warp) {
+  const DenseJob j = jobs[blockIdx.x];
+  const int gx = (int)(blockIdx.x % gnx);
+  const int gy = (int)((blockIdx.x / gnx) % gny);
+  const int gz = g0z + (int)(blockIdx.x / (gnx * gny));
+  const int Mx = g.brick[0], My = g.brick[1], Mz = g.brick[2];
+  const int Sx = g.stored[0], Sy = g.stored[1], Sz = g.stored[2];
+  const int X = g.dims[0], Y = g.dims[1];
+  const int cx = min(Mx, X - gx * Mx), cy = min(My, Y - gy * My), cz = min(Mz, g.dims[2] - gz * Mz);
+  const int rowlen = Sx * C;  // samples per stored row
+  T* brick = pool + (int64_t)j.slot * g.brick_elems;
+  const T bg = (T)g.bg;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  Acc<C> tot;
+  tot.init();
+  const int zp0 = warp * planes_per_warp;
+  for (int zs = zp0; zs < min(Sz, zp0 + planes_per_warp); ++zs) {
+    const int zi = zs - 1;
+    const bool zdata = zi >= 0 && zi < cz;
+    // block row of stored row ys: sample s of the stored row <-> block sample
+    // rb + s - C, rb = first sample of voxel x = gx*Mx in that block row
+    const int64_t zrow = zdata ? (int64_t)(gz * Mz + zi - oz) * Y : 0;
+    T* plane = brick + (int64_t)zs * Sy * rowlen;
+    Acc<C> pl;
+    pl.init();
+    const int n = Sy * rowlen;
+#pragma unroll 4
+    for (int e = lane; e < n; e += 32) {
+      const int ys = e / rowlen;
+      const int s = e - ys * rowlen;
+      const int x = s / C;
+      const bool v = zdata && ys >= 1 && ys <= cy && x >= 1 && x <= cx;
+      T val = bg;
+      if (v) {
+        val = __ldg(src + ((zrow + gy * My + ys - 1) * X + (int64_t)gx * Mx) * C + s - C);
+        pl.add(s % C, (int)val);
+      }
+      plane[e] = val;
+    }
+    if (zdata) emit_plane<C>(pl, tot, j.slot, Mz, zi, pmin, pmax, psum);
+  }
+  finish_stats<C>(tot, j.node, (int64_t)cx * cy * cz, true, g, flags, stats);
+}
+
+// 16-bit samples, rows of an even number of samples: 32-bit words.  A warp
+// owns a stored plane and walks its rows; lane l owns words l, l+32, ... of
+// every row, so each lane's x positions, channels and halo flags are
+// constants and the per-word work is two aligned loads (one when the row is
+// even-aligned in the block), a byte permute, one store and the statistics.
+// A stored row is the run of block samples starting one voxel left of the
+// brick (+1 interior offset, octree.py:420-442); halo / out-of-volume samples
+// are the background (fresh-brick seeding, octree.py:225-241).
+template <int C, int WPL>
+__global__ void __launch_bounds__(544, 1) k_dense_leaf16(
+    const uint16_t* __restrict__ src, int oz, const DenseJob* __restrict__ jobs, int gnx, int gny,
+    int g0z, Geo g, uint16_t* __restrict__ pool, int32_t* pmin, int32_t* pmax,
+    unsigned long long* psum, int32_t* stats, const uint8_t* __restrict__ flags,
+    int planes_per_warp, int64_t nsrc) {
+  constexpr int R = 2;  // rows per iteration (all their loads in flight together)
+  const DenseJob j = jobs[blockIdx.x];
+  const int gx = (int)(blockIdx.x % gnx);
+  const int gy = (int)((blockIdx.x / gnx) % gny);
+  const int gz = g0z + (int)(blockIdx.x / (gnx * gny));
+  const int Mx = g.brick[0], My = g.brick[1], Mz = g.brick[2];
+  const int Sx = g.stored[0], Sy = g.stored[1], Sz = g.stored[2];
+  const int X = g.dims[0], Y = g.dims[1];
+  const int cx = min(Mx, X - gx * Mx), cy = min(My, Y - gy * My), cz = min(Mz, g.dims[2] - gz * Mz);
+  const int wpr = Sx * C / 2;  // words per stored row
+  const uint32_t* src32 = reinterpret_cast<const uint32_t*>(src);
+  uint32_t* brick = reinterpret_cast<uint32_t*>(pool + (int64_t)j.slot * g.brick_elems);
+  const uint32_t bgw = (uint32_t)g.bg | ((uint32_t)g.bg << 16);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // lane constants
+  bool has[WPL], in0[WPL], in1[WPL];
+  int ch[2 * WPL];
+#pragma unroll
+  for (int q = 0; q < WPL; ++q) {
+    const int wl = lane + 32 * q;
+    const int s0 = 2 * wl;
+    has[q] = wl < wpr;
+    const int x0 = s0 / C, x1 = (s0 + 1) / C;
+    in0[q] = has[q] && x0 >= 1 && x0 <= cx;
+    in1[q] = has[q] && x1 >= 1 && x1 <= cx;
+    ch[2 * q] = s0 % C;
+    ch[2 * q + 1] = (s0 + 1) % C;
+  }
+  Acc<C> tot;
+  tot.init();
+  const int zp0 = warp * planes_per_warp;
+  for (int zs = zp0; zs < min(Sz, zp0 + planes_per_warp); ++zs) {
+    const int zi = zs - 1;
+    const bool zdata = zi >= 0 && zi < cz;
+    const int64_t zrow = zdata ? (int64_t)(gz * Mz + zi - oz) * Y : 0;
+    uint32_t* plane = brick + (int64_t)zs * Sy * wpr;
+    unsigned smn[2 * WPL], smx[2 * WPL], ssm[2 * WPL];
+#pragma unroll
+    for (int q = 0; q < 2 * WPL; ++q) {
+      smn[q] = 0xFFFFFFFFu;
+      smx[q] = 0;
+      ssm[q] = 0;
+    }
+    for (int y0 = 0; y0 < Sy; y0 += R) {
+      uint32_t A[R][WPL], B[R][WPL];
+      bool full[R], odd[R], rd[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int y = y0 + r;
+        rd[r] = zdata && y >= 1 && y <= cy;
+        // block sample index of stored sample 0 of this row (x = gx*Mx - 1)
+        const int64_t rb = ((zrow + gy * My + y - 1) * X + (int64_t)gx * Mx - 1) * C;
+        odd[r] = rb & 1;
+        const int64_t ib = (rb - (rb & 1)) >> 1;
+        full[r] = rd[r] && rb + 2 * wpr + 1 < nsrc;
+#pragma unroll
+        for (int q = 0; q < WPL; ++q) {
+          const int wl = lane + 32 * q;
+          if (full[r] && in0[q] && in1[q]) {
+            A[r][q] = __ldg(src32 + ib + wl);
+            B[r][q] = odd[r] ? __ldg(src32 + ib + wl + 1) : 0u;
+          } else {
+            A[r][q] = (rd[r] && in0[q]) ? (uint32_t)__ldg(src + rb + 2 * wl) : bgw & 0xFFFFu;
+            B[r][q] = (rd[r] && in1[q]) ? (uint32_t)__ldg(src + rb + 2 * wl + 1) : bgw & 0xFFFFu;
+          }
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int y = y0 + r;
+        if (y >= Sy) break;
+#pragma unroll
+        for (int q = 0; q < WPL; ++q) {
+          if (!has[q]) continue;
+          uint32_t out;
+          if (full[r] && in0[q] && in1[q])
+            out = odd[r] ? __byte_perm(A[r][q], B[r][q], 0x5432) : A[r][q];
+          else
+            out = A[r][q] | (B[r][q] << 16);
+          plane[y * wpr + lane + 32 * q] = out;
+          if (rd[r] && in0[q]) {
+            const unsigned v = out & 0xFFFFu;
+            smn[2 * q] = min(smn[2 * q], v);
+            smx[2 * q] = max(smx[2 * q], v);
+            ssm[2 * q] += v;
+          }
+          if (rd[r] && in1[q]) {
+            const unsigned v = out >> 16;
+            smn[2 * q + 1] = min(smn[2 * q + 1], v);
+            smx[2 * q + 1] = max(smx[2 * q + 1], v);
+            ssm[2 * q + 1] += v;
+          }
+        }
+      }
+    }
+    if (zdata) {
+      Acc<C> pl;
+      pl.init();
+#pragma unroll
+      for (int q = 0; q < 2 * WPL; ++q)
+#pragma unroll
+        for (int c = 0; c < C; ++c)
+          if (ch[q] == c && smx[q] >= smn[q]) {
+            pl.mn[c] = min(pl.mn[c], (int)smn[q]);
+            pl.mx[c] = max(pl.mx[c], (int)smx[q]);
+            pl.sm[c] += ssm[q];
+          }
+      emit_plane<C>(pl, tot, j.slot, Mz, zi, pmin, pmax, psum);
+    }
+  }
+  finish_stats<C>(tot, j.node, (int64_t)cx * cy * cz, true, g, flags, stats);
+}
+
+// ---------------------------------------------------------------------------
+// TMA-staged leaves (16-bit samples, 16-byte aligned block rows)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "VT_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra VT_WAIT_%=;\n"
+      "}\n" ::"r"(smem_addr(b)),
+      "r"(parity)
+      : "memory");
+}
+// 3-D tensor tile (TMA) global -> shared, completion on an mbarrier
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z,
+                                            uint64_t* b) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], "
+      "[%1, {%2, %3, %4}], [%5];" ::"r"(smem_addr(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_addr(b))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_addr(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// One CTA (8 warps) per leaf brick, stored planes in stages of P = 2.  The
+// TMA engine streams the block rows of a stage (one bulk copy per row) into
+// a 3-deep shared-memory input ring; the warps move every interior voxel
+// (C samples) from its staged row into a shared-memory image of the stored
+// planes (shell pre-filled with the background, octree.py:234-237, never
+// rewritten), accumulating per-plane statistics with compile-time channel
+// indices; one bulk copy then writes the stage's planes (P x (Mx+2)(My+2)C
+// samples, contiguous in the brick) to HBM from a 3-deep output ring.  Data
+// in flight lives in shared memory, not registers.
+constexpr int kTmaStages = 3;
+constexpr int kTmaWarps = 8;
+constexpr int kTmaP = 2;
+
+template <int C>
+__global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
+    const __grid_constant__ CUtensorMap map, int oz, const DenseJob* __restrict__ jobs, int gnx, int gny,
+    int g0z, Geo g, uint16_t* __restrict__ pool, int32_t* pmin, int32_t* pmax,
+    unsigned long long* psum, int32_t* stats, const uint8_t* __restrict__ flags) {
+  constexpr int P = kTmaP;
+  constexpr int WPP = kTmaWarps / P;  // warps per plane
+  extern __shared__ __align__(128) unsigned char s_dyn[];
+  __shared__ uint64_t s_bar[kTmaStages];
+  __shared__ int s_pmn[2][kTmaWarps][C], s_pmx[2][kTmaWarps][C];
+  __shared__ unsigned long long s_psm[2][kTmaWarps][C];
+  __shared__ int s_tmn[C], s_tmx[C];
+  __shared__ unsigned long long s_tsm[C];
+  const DenseJob j = jobs[blockIdx.x];
+  const int gx = (int)(blockIdx.x % gnx);
+  const int gy = (int)((blockIdx.x / gnx) % gny);
+  const int gz = g0z + (int)(blockIdx.x / (gnx * gny));
+  const int Mx = g.brick[0], My = g.brick[1], Mz = g.brick[2];
+  const int Sx = g.stored[0], Sy = g.stored[1], Sz = g.stored[2];
+  const int X = g.dims[0], Y = g.dims[1];
+  const int cx = min(Mx, X - gx * Mx), cy = min(My, Y - gy * My), cz = min(Mz, g.dims[2] - gz * Mz);
+  const uint32_t rowbytes = (uint32_t)Mx * C * 2;           // staged block row
+  const uint32_t in_bytes = (uint32_t)P * My * rowbytes;    // one input stage
+  const uint32_t plane_elems = (uint32_t)Sx * Sy * C;       // one stored plane
+  const uint32_t out_bytes = (uint32_t)P * plane_elems * 2;  // one output stage
+  unsigned char* s_in = s_dyn;
+  uint16_t* s_out = reinterpret_cast<uint16_t*>(s_dyn + (size_t)kTmaStages * in_bytes);
+  const int nstages = Sz / P;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint16_t* brick = pool + (int64_t)j.slot * g.brick_elems;
+  const uint16_t bg = (uint16_t)g.bg;
+
+  if (tid == 0) {
+    for (int b = 0; b < kTmaStages; ++b) mbar_init(&s_bar[b], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (tid < C) {
+    s_tmn[tid] = INT_MAX;
+    s_tmx[tid] = INT_MIN;
+    s_tsm[tid] = 0;
+  }
+  // output ring: background everywhere (the shell and anything outside the
+  // in-volume extent stay background; only in-volume interiors are written)
+  {
+    uint32_t* o = reinterpret_cast<uint32_t*>(s_out);
+    const uint32_t bgw = (uint32_t)bg | ((uint32_t)bg << 16);
+    for (uint32_t i = tid; i < kTmaStages * out_bytes / 4; i += blockDim.x) o[i] = bgw;
+  }
+  __syncthreads();
+
+  // one 3-D tensor tile per stage: Mx*C samples x My rows x P planes of the
+  // block, out-of-range rows/planes zero-filled by the TMA unit (never read)
+  auto issue = [&](int s) {  // one thread
+    const int b = s % kTmaStages;
+    mbar_expect_tx(&s_bar[b], in_bytes);
+    tma_load_3d(s_in + (size_t)b * in_bytes, &map, gx * Mx * C, gy * My, gz * Mz - oz + P * s - 1,
+                &s_bar[b]);
+  };
+  if (tid == 0)
+    for (int s = 0; s < min(kTmaStages, nstages); ++s) issue(s);
+
+  const int pw = warp / WPP;  // plane of the stage this warp builds
+  const int rw = warp % WPP;  // its row phase
+  for (int s = 0; s < nstages; ++s) {
+    const int b = s % kTmaStages;
+    const int zs = P * s + pw;
+    const int zi = zs - 1;
+    const bool zdata = zi >= 0 && zi < cz;
+    uint16_t* oplane = s_out + (size_t)b * (out_bytes / 2) + (size_t)pw * plane_elems;
+    if (!zdata) {
+      // a shell plane or one past the in-volume extent: all background (the
+      // ring slot may hold an interior plane from an earlier stage)
+      if (s >= kTmaStages || zs == 0)
+        for (uint32_t i = rw * 32 + lane; i < plane_elems; i += WPP * 32) oplane[i] = bg;
+    }
+    mbar_wait(&s_bar[b], (uint32_t)(s / kTmaStages) & 1u);
+    int mn[C], mx[C];
+    unsigned sm[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      mn[c] = INT_MAX;
+      mx[c] = INT_MIN;
+      sm[c] = 0;
+    }
+    if (zdata) {
+      const uint16_t* iplane =
+          reinterpret_cast<const uint16_t*>(s_in + (size_t)b * in_bytes + (size_t)pw * My * rowbytes);
+      for (int y = rw; y < cy; y += WPP) {
+        const uint16_t* irow = iplane + (size_t)y * Mx * C;
+        uint16_t* orow = oplane + ((size_t)(y + 1) * Sx + 1) * C;
+        for (int x = lane; x < cx; x += 32) {
+#pragma unroll
+          for (int c = 0; c < C; ++c) {
+            const uint16_t v = irow[x * C + c];
+            orow[x * C + c] = v;
+            mn[c] = min(mn[c], (int)v);
+            mx[c] = max(mx[c], (int)v);
+            sm[c] += v;
+          }
+        }
+      }
+    }
+    // per-warp partials of its plane -> shared (double buffered by stage parity)
+#pragma unroll
+    for (int c = 0; c < C; ++c)
+      for (int o = 16; o > 0; o >>= 1) {
+        mn[c] = min(mn[c], __shfl_xor_sync(0xffffffffu, mn[c], o));
+        mx[c] = max(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], o));
+        sm[c] += __shfl_xor_sync(0xffffffffu, sm[c], o);
+      }
+    if (lane == 0)
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        s_pmn[s & 1][warp][c] = mn[c];
+        s_pmx[s & 1][warp][c] = mx[c];
+        s_psm[s & 1][warp][c] = sm[c];
+      }
+    __syncthreads();  // input slot consumed, output image complete, partials visible
+    if (warp == 0) {
+      if (lane == 0) {
+        // stage image -> HBM (the P stored planes are contiguous in the brick)
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        bulk_s2g(brick + (size_t)P * s * plane_elems, s_out + (size_t)b * (out_bytes / 2),
+                 out_bytes);
+        bulk_commit();
+        // the output slot of stage s+1 was last read by the store of stage
+        // s+1-kTmaStages: keep at most kTmaStages-2 stores pending
+        bulk_wait_read<kTmaStages - 2>();
+        if (s + kTmaStages < nstages) issue(s + kTmaStages);
+      }
+    }
+    if (tid < C) {
+      const int c = tid;
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        const int zi2 = P * s + p - 1;
+        if (zi2 < 0 || zi2 >= cz) continue;
+        int a = INT_MAX, bmx = INT_MIN;
+        unsigned long long t = 0;
+        for (int w = p * WPP; w < (p + 1) * WPP; ++w) {
+          a = min(a, s_pmn[s & 1][w][c]);
+          bmx = max(bmx, s_pmx[s & 1][w][c]);
+          t += s_psm[s & 1][w][c];
+        }
+        const int64_t off = ((int64_t)j.slot * Mz + zi2) * C + c;
+        pmin[off] = a;
+        pmax[off] = bmx;
+        psum[off] = t;
+        s_tmn[c] = min(s_tmn[c], a);
+        s_tmx[c] = max(s_tmx[c], bmx);
+        s_tsm[c] += t;
+      }
+    }
+  }
+  if (tid == 0) bulk_wait<0>();  // every store complete before the CTA exits
+  if (tid < C) {
+    const int c = tid;
+    const long long n = (long long)cx * cy * cz;
+    const long long avg = (2 * (long long)s_tsm[c] + n) / (2 * n);
+    stats[st_index(j.node, ST_AVG, c)] = (int)avg;
+    stats[st_index(j.node, ST_MIN, c)] = s_tmn[c];
+    stats[st_index(j.node, ST_MAX, c)] = s_tmx[c];
+    stats[st_index(j.node, ST_SUBMIN, c)] = s_tmn[c];
+    stats[st_index(j.node, ST_SUBMAX, c)] = s_tmx[c];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// parents
+// ---------------------------------------------------------------------------
+// One CTA per parent; warps own interior planes, lanes the voxels of a row.
+// Every interior voxel is the half-sample of its child octant (counts over
+// the child's in-volume voxels, background where none, octree.py:83-92); an
+// out-of-volume child contributes background (its AVG is the background and
+// it covers no in-volume parent voxel, octree.py:296-306).
+template <class T, int C>
+__global__ void __launch_bounds__(256) k_dense_level(const int64_t* __restrict__ nodes, Geo g,
+                                                     T* pool, const int32_t* __restrict__ slots,
+                                                     const uint8_t* __restrict__ flags,
+                                                     int32_t* pmin, int32_t* pmax,
+                                                     unsigned long long* psum, int32_t* stats) {
+  const int64_t node = nodes[blockIdx.x];
+  const int level = g.level_of(node);
+  const int Mx = g.brick[0], My = g.brick[1], Mz = g.brick[2];
+  __shared__ int s_cslot[8];
+  __shared__ int s_cext[8][3];
+  __shared__ int s_pext[3];
+  __shared__ int s_pslot;
+  if (threadIdx.x < 8) {
+    const int k = threadIdx.x;
+    int sl = -1, ce[3] = {0, 0, 0};
+    if (g.octant_real(k)) {
+      const int64_t ch = 8 * node + 1 + k;
+      if ((flags[ch] & NF_EXISTS) && (flags[ch] & NF_BRICK)) sl = slots[ch];
+      int lo[3];
+      g.box_lo(ch, lo);
+      g.in_extent(lo, level - 1, ce);
+    }
+    s_cslot[k] = sl;
+    for (int a = 0; a < 3; ++a) s_cext[k][a] = ce[a];
+  } else if (threadIdx.x == 8) {
+    int lo[3], ce[3];
+    g.box_lo(node, lo);
+    g.in_extent(lo, level, ce);
+    for (int a = 0; a < 3; ++a) s_pext[a] = ce[a];
+    s_pslot = slots[node];
+  }
+  __syncthreads();
+  const int kx = g.split[0] ? 2 : 1, ky = g.split[1] ? 2 : 1, kz = g.split[2] ? 2 : 1;
+  const int hx = Mx / kx, hy = My / ky, hz = Mz / kz;  // octant extents
+  const int pcx = s_pext[0], pcy = s_pext[1], pcz = s_pext[2];
+  T* parent = pool + (int64_t)s_pslot * g.brick_elems;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  Acc<C> tot;
+  tot.init();
+  const int64_t rs = (int64_t)g.stored[0] * C, ps = rs * g.stored[1];  // row / plane stride
+  // value of parent interior voxel (x, y, z): loads only, no stores, so the
+  // two rows of an iteration keep all their gathers in flight together
+  struct Vox {
+    int v[C];
+  };
+  auto voxel = [&](int x, int y, int z) -> Vox {
+    Vox r;
+    int* v = r.v;
+    const int bz = z / hz, oz = z - bz * hz;
+    const int by = y / hy, oy = y - by * hy;
+    const int bx = x / hx, ox = x - bx * hx;
+    const int k = bx | (by << 1) | (bz << 2);
+    const int cs = s_cslot[k];
+    if (cs < 0) {
+#pragma unroll
+      for (int c = 0; c < C; ++c) v[c] = g.bg;
+      return r;
+    }
+    const T* child = pool + (int64_t)cs * g.brick_elems;
+    const int ex = s_cext[k][0], ey = s_cext[k][1], ez = s_cext[k][2];
+    if (kx == 2 && ky == 2 && kz == 2 && 2 * ox + 1 < ex && 2 * oy + 1 < ey && 2 * oz + 1 < ez) {
+      // full 2x2x2 block: 8 voxels = 4 runs of 2*C contiguous samples
+      const T* q = child + g.voxel_offset(1 + 2 * oz, 1 + 2 * oy, 1 + 2 * ox);
+      unsigned sum[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c)
+        sum[c] = (unsigned)__ldg(q + c) + __ldg(q + C + c) + __ldg(q + rs + c) +
+                 __ldg(q + rs + C + c) + __ldg(q + ps + c) + __ldg(q + ps + C + c) +
+                 __ldg(q + ps + rs + c) + __ldg(q + ps + rs + C + c);
+#pragma unroll
+      for (int c = 0; c < C; ++c) v[c] = (int)((2 * sum[c] + 8) / 16);
+      return r;
+    }
+    long long sum[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) sum[c] = 0;
+    int cnt = 0;
+    for (int dz = 0; dz < kz; ++dz) {
+      const int sz = kz * oz + dz;
+      if (sz >= ez) continue;
+      for (int dy = 0; dy < ky; ++dy) {
+        const int sy = ky * oy + dy;
+        if (sy >= ey) continue;
+        const T* row = child + g.voxel_offset(1 + sz, 1 + sy, 1);
+        for (int dx = 0; dx < kx; ++dx) {
+          const int sx = kx * ox + dx;
+          if (sx >= ex) continue;
+#pragma unroll
+          for (int c = 0; c < C; ++c) sum[c] += __ldg(row + sx * C + c);
+          ++cnt;
+        }
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < C; ++c) v[c] = cnt ? (int)((2 * sum[c] + cnt) / (2 * cnt)) : g.bg;
+    return r;
+  };
+  for (int z = warp; z < Mz; z += nw) {
+    Acc<C> pl;
+    pl.init();
+    for (int y = 0; y < My; y += 2) {
+      for (int x = lane; x < Mx; x += 32) {
+        const bool two = y + 1 < My;
+        const Vox a = voxel(x, y, z);
+        const Vox b = two ? voxel(x, y + 1, z) : a;
+        const int* v0 = a.v;
+        const int* v1 = b.v;
+        T* dst = parent + g.voxel_offset(1 + z, 1 + y, 1 + x);
+#pragma unroll
+        for (int c = 0; c < C; ++c) dst[c] = (T)v0[c];
+        if (x < pcx && y < pcy && z < pcz) pl.add_all(v0);
+        if (two) {
+#pragma unroll
+          for (int c = 0; c < C; ++c) dst[rs + c] = (T)v1[c];
+          if (x < pcx && y + 1 < pcy && z < pcz) pl.add_all(v1);
+        }
+      }
+    }
+    if (z < pcz && pcx > 0 && pcy > 0) emit_plane<C>(pl, tot, s_pslot, Mz, z, pmin, pmax, psum);
+  }
+  finish_stats<C>(tot, node, (int64_t)pcx * pcy * pcz, false, g, flags, stats);
+}
+
+int planes_per_warp(int sz) { return (sz + 11) / 12; }  // <= 12 warps per CTA
+
+}  // namespace
+
+#define VT_CHECK_LAUNCH() VT_CUDA(cudaGetLastError())
+
+// TMA tensor tiles need a 16-byte aligned block, row pitches and box rows
+// that are multiples of 16 bytes, and 128-byte aligned shared stages
+static bool tma_ok(const Tree& t, const void* src, int64_t rowbytes) {
+  if (std::getenv("VT_DENSE_TMA") && std::getenv("VT_DENSE_TMA")[0] == '0') return false;
+  const int64_t stride = (int64_t)t.g.dims[0] * t.g.C * 2;
+  return ((uintptr_t)src & 15) == 0 && rowbytes % 16 == 0 && stride % 16 == 0 &&
+         (rowbytes * t.g.brick[1] * kTmaP) % 128 == 0 &&
+         (int64_t)kTmaStages * kTmaP *
+                 (rowbytes * t.g.brick[1] + (int64_t)t.g.stored[0] * t.g.stored[1] * t.g.C * 2) <=
+             200 * 1024;
+}
+
+// 3-D tensor map of a (dz, Y, X*C) u16 block for the TMA unit; the encoder
+// comes from the driver through the runtime (no libcuda link)
+static bool encode_block_map(const Tree& t, const void* src, int64_t nsrc, CUtensorMap* map) {
+  using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static Encode enc = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      enc = (Encode)fn;
+    cudaGetLastError();
+  }
+  if (!enc) return false;
+  const int C = t.g.C;
+  const int64_t row = (int64_t)t.g.dims[0] * C;
+  const int64_t dz = nsrc / (row * t.g.dims[1]);
+  cuuint64_t dims[3] = {(cuuint64_t)row, (cuuint64_t)t.g.dims[1], (cuuint64_t)dz};
+  cuuint64_t strides[2] = {(cuuint64_t)row * 2, (cuuint64_t)row * 2 * t.g.dims[1]};
+  cuuint32_t box[3] = {(cuuint32_t)(t.g.brick[0] * C), (cuuint32_t)t.g.brick[1],
+                       (cuuint32_t)kTmaP};
+  cuuint32_t es[3] = {1, 1, 1};
+  if (box[0] > 256 || box[1] > 256) return false;
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, const_cast<void*>(src), dims, strides, box,
+             es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <class T, int C>
+static void leaf_launch(const Tree& t, const void* src, int64_t nsrc, int oz,
+                        const DenseJob* jobs, int n, const int gn[3], int g0z) {
+  const int sz = t.g.stored[2];
+  const int rowlen = t.g.stored[0] * C;
+  const int wpl = (rowlen / 2 + 31) / 32;
+  const int64_t rowbytes = (int64_t)t.g.brick[0] * C * 2;
+  CUtensorMap map;
+  if (sizeof(T) == 2 && tma_ok(t, src, rowbytes) && encode_block_map(t, src, nsrc, &map)) {
+    const size_t smem = (size_t)kTmaStages * kTmaP *
+                        (rowbytes * t.g.brick[1] + (size_t)t.g.stored[0] * t.g.stored[1] * C * 2);
+    auto k = k_dense_leaf_tma<C>;
+    VT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k<<<n, kTmaWarps * 32, smem, t.stream>>>(map, oz, jobs, gn[0], gn[1], g0z, t.g,
+                                            (uint16_t*)t.d_pool, t.d_pmin, t.d_pmax, t.d_psum,
+                                            t.d_stats, t.d_flags);
+    VT_CHECK_LAUNCH();
+    return;
+  }
+  if (sizeof(T) == 2 && rowlen % 2 == 0 && wpl <= 4) {
+    // warps own ceil(Sz / 17) planes each (<= 17 warps)
+    const int ppw = (sz + 16) / 17;
+    const int warps = (sz + ppw - 1) / ppw;
+    auto* p = (const uint16_t*)src;
+    auto* pool = (uint16_t*)t.d_pool;
+#define VT_LEAF16(W)                                                                      \
+  k_dense_leaf16<C, W><<<n, 32 * warps, 0, t.stream>>>(p, oz, jobs, gn[0], gn[1], g0z, t.g, \
+                                                       pool, t.d_pmin, t.d_pmax, t.d_psum, \
+                                                       t.d_stats, t.d_flags, ppw, nsrc)
+    switch (wpl) {
+      case 1: VT_LEAF16(1); break;
+      case 2: VT_LEAF16(2); break;
+      case 3: VT_LEAF16(3); break;
+      default: VT_LEAF16(4); break;
+    }
+#undef VT_LEAF16
+    VT_CHECK_LAUNCH();
+    return;
+  }
+  const int ppw = planes_per_warp(sz);
+  const int warps = (sz + ppw - 1) / ppw;
+  k_dense_leaf<T, C><<<n, 32 * warps, 0, t.stream>>>(
+      (const T*)src, oz, jobs, gn[0], gn[1], g0z, t.g, (T*)t.d_pool, t.d_pmin, t.d_pmax, t.d_psum,
+      t.d_stats, t.d_flags, ppw);
+  VT_CHECK_LAUNCH();
+}
+
+template <class T>
+static void leaf_dispatch(const Tree& t, const void* src, int64_t nsrc, int oz,
+                          const DenseJob* jobs, int n, const int gn[3], int g0z) {
+  switch (t.g.C) {
+    case 1: leaf_launch<T, 1>(t, src, nsrc, oz, jobs, n, gn, g0z); break;
+    case 2: leaf_launch<T, 2>(t, src, nsrc, oz, jobs, n, gn, g0z); break;
+    case 3: leaf_launch<T, 3>(t, src, nsrc, oz, jobs, n, gn, g0z); break;
+    default: leaf_launch<T, 4>(t, src, nsrc, oz, jobs, n, gn, g0z); break;
+  }
+}
+
+void launch_dense_leaf(const Tree& t, const void* src, int64_t nsrc, int oz, const DenseJob* jobs,
+                       int n, const int gn[3], int g0z) {
+  if (n <= 0) return;
+  if (t.g.sb == 1)
+    leaf_dispatch<uint8_t>(t, src, nsrc, oz, jobs, n, gn, g0z);
+  else
+    leaf_dispatch<uint16_t>(t, src, nsrc, oz, jobs, n, gn, g0z);
+}
+
+template <class T, int C>
+static void level_launch(const Tree& t, const int64_t* nodes, int n) {
+  const int warps = std::min(8, std::max(1, t.g.brick[2]));
+  k_dense_level<T, C><<<n, 32 * warps, 0, t.stream>>>(nodes, t.g, (T*)t.d_pool, t.d_slot,
+                                                      t.d_flags, t.d_pmin, t.d_pmax, t.d_psum,
+                                                      t.d_stats);
+  VT_CHECK_LAUNCH();
+}
+
+template <class T>
+static void level_dispatch(const Tree& t, const int64_t* nodes, int n) {
+  switch (t.g.C) {
+    case 1: level_launch<T, 1>(t, nodes, n); break;
+    case 2: level_launch<T, 2>(t, nodes, n); break;
+    case 3: level_launch<T, 3>(t, nodes, n); break;
+    default: level_launch<T, 4>(t, nodes, n); break;
+  }
+}
+
+void launch_dense_level(const Tree& t, const int64_t* nodes, int n) {
+  if (n <= 0) return;
+  if (t.g.sb == 1)
+    level_dispatch<uint8_t>(t, nodes, n);
+  else
+    level_dispatch<uint16_t>(t, nodes, n);
+}
+
+}  // namespace vtx

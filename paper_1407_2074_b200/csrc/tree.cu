@@ -95,6 +95,8 @@ Tree::Tree(const vt_tree_desc& d) {
   flags.assign(cap, 0);
   slot.assign(cap, -1);
   struct_mark.assign(cap, 0);
+  complete.assign(cap, 0);
+  if (const char* e = std::getenv("VT_DENSE")) dense_enabled = e[0] != '0';
   h_stats.assign(cap * ST_N * kMaxC, 0);
   flags[0] = NF_EXISTS | NF_INVOL;
   for (int c = 0; c < g.C; ++c)
@@ -394,10 +396,44 @@ void Tree::insert(int channel, const int origin[3], const int dims[3], const voi
   }
 }
 
+// A block that spans the full x/y extent and whole brick layers in z, every
+// channel at once, at threshold 0, over leaves that own no brick yet: its
+// leaves end fully covered, so the dense kernels (dense_build.cu) can write
+// their bricks and statistics outright.
+bool Tree::dense_eligible(int channel, const int origin[3], const int dims[3], const void* dsrc,
+                          int src_stride, int src_off) const {
+  if (!dense_enabled || tau != 0) return false;
+  if (!(channel < 0 || g.C == 1) || src_stride != g.C || src_off != 0) return false;
+  if (g.sb == 2 && ((uintptr_t)dsrc & 3)) return false;
+  if (origin[0] != 0 || origin[1] != 0 || dims[0] != g.dims[0] || dims[1] != g.dims[1])
+    return false;
+  const int* M = g.brick;
+  const int z1 = origin[2] + dims[2];
+  if (origin[2] % M[2] != 0 || (z1 % M[2] != 0 && z1 != g.dims[2])) return false;
+  const int gz1 = (z1 - 1) / M[2];
+  const int gx1 = (g.dims[0] - 1) / M[0], gy1 = (g.dims[1] - 1) / M[1];
+  for (int gz = origin[2] / M[2]; gz <= gz1; ++gz)
+    for (int gy = 0; gy <= gy1; ++gy)
+      for (int gx = 0; gx <= gx1; ++gx) {
+        const int gg[3] = {gx, gy, gz};
+        int64_t idx = 0;
+        for (int lvl = g.depth; lvl > 0; --lvl) {
+          int k = 0;
+          for (int a = 0; a < 3; ++a)
+            if (g.split[a] && ((gg[a] >> (lvl - 1)) & 1)) k |= 1 << a;
+          idx = 8 * idx + 1 + k;
+        }
+        if (flags[idx] & NF_BRICK) return false;
+      }
+  return true;
+}
+
 void Tree::insert_staged(int channel, const int origin[3], const int dims[3], const void* dsrc,
                          int src_stride, int src_off, int reps) {
   const int64_t nvox = (int64_t)dims[0] * dims[1] * dims[2];
   ++data_version;
+  const bool dense = dense_eligible(channel, origin, dims, dsrc, src_stride, src_off);
+  std::vector<DenseJob> djobs;
   creates.clear();
   seeds.clear();
   created_seed.clear();
@@ -440,6 +476,22 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
         int ce[3];
         for (int a = 0; a < 3; ++a) ce[a] = std::max(0, std::min(M[a], g.dims[a] - gg[a] * M[a]));
         bool fresh = ensure_brick(idx, ce);
+        if (dense) {
+          // the dense kernel writes the whole stored brick and its final
+          // statistics: no seed, no owed planes, no reduce
+          seeds.pop_back();
+          djobs.push_back({idx, slot[idx], 0});
+          Pending& p = pend(0, idx);
+          p.box = Box{{0, 0, 0}, {M[0], M[1], M[2]}};
+          p.has_box = true;
+          p.fresh = true;
+          p.masked = true;
+          p.need[0] = p.need[1] = 0;
+          p.dense = true;
+          complete[idx] = 1;
+          touched[0].push_back(idx);
+          continue;
+        }
         leaf_slots[((size_t)(gz - g0[2]) * gn[1] + (gy - g0[1])) * gn[0] + (gx - g0[0])] =
             slot[idx];
         Box b;
@@ -460,6 +512,7 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
         Pending& p = pend(0, idx);
         box_union(p, b);
         p.fresh |= fresh;
+        p.dense = false;
         if (g.brick[2] <= 128) {
           if (!p.masked) {
             // first touch since the last propagation: nothing owed yet
@@ -512,8 +565,14 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
     ds = upload(*this, seeds);
     launch_seed(*this, ds, (int)seeds.size());
   }
-  int32_t* dl;
-  {
+  int32_t* dl = nullptr;
+  if (dense) {
+    ProfScope q(prof, 7);
+    DenseJob* dj = upload(*this, djobs);
+    launch_dense_leaf(*this, dsrc, nvox * src_stride, origin[2], dj, (int)djobs.size(), gn, g0[2]);
+    release(*this, dj);
+    ++dense_leaf_inserts;
+  } else {
     ProfScope q(prof, 7);
     dl = upload(*this, leaf_slots);
     launch_scatter(*this, dsrc, channel, src_stride, src_off, origin, dims, g0, gn, dl);
@@ -547,6 +606,18 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
 // propagation of dirty boxes up the tree
 // ---------------------------------------------------------------------------
 
+bool Tree::dense_parent(int64_t p) const {
+  if (!dense_enabled || tau != 0) return false;
+  if (!(flags[p] & NF_BRICK) || !(flags[p] & NF_CHILDREN)) return false;
+  for (int k = 0; k < 8; ++k) {
+    if (!g.octant_real(k)) continue;
+    const int64_t c = 8 * p + 1 + k;
+    if (!(flags[c] & NF_INVOL)) continue;
+    if (!(flags[c] & NF_EXISTS) || !(flags[c] & NF_BRICK) || !complete[c]) return false;
+  }
+  return true;
+}
+
 void Tree::propagate() {
   if (!has_pending) return;
   ProfScope ps(prof, 4);
@@ -557,12 +628,24 @@ void Tree::propagate() {
     if (nodes.empty()) continue;
     std::sort(nodes.begin(), nodes.end());
     std::vector<OctJob> oct;
+    std::vector<int64_t> dense_nodes;
     if (lvl > 0) {
       // dirty children are sorted: those of parent p are a contiguous run
       const std::vector<int64_t>& kids = pend_nodes[lvl - 1];
       size_t ci = 0;
       for (int64_t p : nodes) {
         Pending& pp = *pend_find(p, lvl);
+        if (dense_parent(p)) {
+          // every in-volume child complete: recompute the whole interior and
+          // the statistics in one dense pass (dense_build.cu)
+          dense_nodes.push_back(p);
+          pp.box = Box{{0, 0, 0}, {M[0], M[1], M[2]}};
+          pp.has_box = true;
+          pp.dense = true;
+          complete[p] = 1;
+          continue;
+        }
+        complete[p] = 0;
         auto emit = [&](int64_t c, const Box* cb) {
           OctJob j{};
           j.pslot = slot[p];
@@ -609,6 +692,10 @@ void Tree::propagate() {
       OctJob* d = upload(*this, oct);
       launch_octant(*this, d, (int)oct.size());
       release(*this, d);
+      int64_t* dd = upload(*this, dense_nodes);
+      launch_dense_level(*this, dd, (int)dense_nodes.size());
+      release(*this, dd);
+      dense_level_nodes += (int64_t)dense_nodes.size();
     }
     // stats of this level's dirty nodes
     std::vector<PlaneJob> planes;
@@ -617,6 +704,7 @@ void Tree::propagate() {
     reds.reserve(nodes.size());
     for (int64_t n : nodes) {
       const Pending& p = *pend_find(n, lvl);
+      if (p.dense) continue;  // statistics written by the dense kernel
       ReduceJob r{};
       r.node = n;
       r.slot = slot[n];
@@ -823,6 +911,7 @@ void Tree::merge(int64_t n, const int64_t* idx, const int32_t* nflags, const int
       brick_src.push_back(brick_row[r]);
     }
     rec_nodes.push_back(i);
+    complete[i] = 0;
     for (int s2 = 0; s2 < ST_N; ++s2)
       for (int c = 0; c < kMaxC; ++c) {
         const int v = c < C ? stats_in[(r * C + c) * ST_N + s2] : 0;

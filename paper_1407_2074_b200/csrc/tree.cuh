@@ -22,6 +22,9 @@ struct Pending {
   Box box;
   bool has_box = false;
   bool fresh = false;
+  // statistics already final (written by a dense-build kernel): no plane /
+  // reduce work owed.  Any later general-path touch clears it.
+  bool dense = false;
   // leaves: planes whose partial stats are still owed (bit z); planes whose
   // stats the scatter computed in-kernel are cleared (requires Mz <= 128)
   bool masked = false;
@@ -87,6 +90,12 @@ struct Tree {
   std::priority_queue<int32_t, std::vector<int32_t>, std::greater<int32_t>> free_slots;
   int64_t cursor = 0;
   int64_t data_version = 0;  // bumped by every pool mutation
+  // tau == 0 dense build (dense_build.cu): complete[n] = every in-volume leaf
+  // under n was fully covered by one dense insertion, so n's brick is a pure
+  // function of the data; VT_DENSE=0 disables the path (A/B testing)
+  bool dense_enabled = true;
+  std::vector<uint8_t> complete;
+  int64_t dense_leaf_inserts = 0, dense_level_nodes = 0;
 
   // -- device state --
   uint8_t* d_pool = nullptr;  // [pool_slots][Sz][Sy][Sx][C] samples
@@ -166,10 +175,13 @@ struct Tree {
   // insertion / propagation
   void insert(int channel, const int origin[3], const int dims[3], const void* samples,
               int mem_kind);
+  bool dense_eligible(int channel, const int origin[3], const int dims[3], const void* dsrc,
+                      int src_stride, int src_off) const;
   void insert_staged(int channel, const int origin[3], const int dims[3], const void* dsrc,
                      int src_stride, int src_off, int reps);
   void flush_structure();
   void propagate();
+  bool dense_parent(int64_t p) const;
   void flush();  // propagate pending + structure
   void sync();
   void gather_stats(const std::vector<int64_t>& nodes);
@@ -198,6 +210,10 @@ void launch_scatter(const Tree& t, const void* src, int channel, int src_stride,
 bool scatter_owns_stats(const Geo& g, int channel, const int origin[3], const int dims[3], int gx,
                         int gy);
 void launch_octant(const Tree& t, const OctJob* d_jobs, int n);
+// dense_build.cu
+void launch_dense_leaf(const Tree& t, const void* src, int64_t nsrc, int oz, const DenseJob* jobs,
+                       int n, const int gn[3], int g0z);
+void launch_dense_level(const Tree& t, const int64_t* nodes, int n);
 void launch_plane(const Tree& t, const PlaneJob* d_jobs, int n);
 void launch_reduce(const Tree& t, const ReduceJob* d_jobs, int n);
 void launch_borders(const Tree& t, const BorderJob* d_jobs, int n);

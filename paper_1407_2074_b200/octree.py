@@ -13,6 +13,7 @@ reference only read them).
 from __future__ import annotations
 
 import ctypes as ct
+import os
 import threading
 from collections.abc import Sequence
 from dataclasses import dataclass
@@ -228,6 +229,7 @@ class Octree:
         h = ct.c_void_p()
         _lib.call("vt_tree_create", ct.byref(d), ct.byref(h))
         self._h = h
+        self._dense = os.environ.get("VT_DENSE", "1") != "0"
         self.store = _PoolView(self)
 
     # -- factories ---------------------------------------------------------
@@ -389,6 +391,24 @@ class Octree:
         out = ct.c_uint64()
         _lib.call("vt_tree_checksum", self._h, ct.byref(out))
         return int(out.value)
+
+    @property
+    def dense_build(self) -> bool:
+        """B200 extension: threshold-0 dense build on (default) / off
+        (vt_tree_set_dense).  Results are identical either way."""
+        return self._dense
+
+    @dense_build.setter
+    def dense_build(self, on: bool) -> None:
+        with self.lock:
+            _lib.call("vt_tree_set_dense", self._h, 1 if on else 0)
+            self._dense = bool(on)
+
+    def dense_counts(self) -> tuple[int, int]:
+        """(dense leaf insertions, dense parent recomputes) so far."""
+        a, b = ct.c_int64(), ct.c_int64()
+        _lib.call("vt_tree_dense_counts", self._h, ct.byref(a), ct.byref(b))
+        return int(a.value), int(b.value)
 
     def use_stream(self, stream) -> None:
         """Run this tree's device work on ``stream`` (a torch.cuda.Stream or
