@@ -69,6 +69,10 @@ static void build_geo(const vt_tree_desc& d, Geo& g) {
   g.brick_elems = (int64_t)g.stored[0] * g.stored[1] * g.stored[2] * g.C;
 }
 
+namespace {
+uint8_t* pinned_get(size_t& cap);
+}
+
 Tree::Tree(const vt_tree_desc& d) {
   if (const char* e = std::getenv("VT_HOST_PROFILE")) prof.on = e[0] == '1';
   VT_REQUIRE(d.channels >= 1 && d.channels <= kMaxC, VT_EINVAL, "channels must be in [1, 4]");
@@ -96,6 +100,28 @@ Tree::Tree(const vt_tree_desc& d) {
   slot.assign(cap, -1);
   struct_mark.assign(cap, 0);
   complete.assign(cap, 0);
+  seed_of.assign(cap, -1);
+  anc_mark.assign(cap, 0);
+  {
+    // staging ring up front: its first allocation syncs the stream
+    size_t sc = (size_t)8 << 20;
+    stage.h = pinned_get(sc);
+    VT_CUDA(cudaMalloc(&stage.d, sc));
+    stage.cap = sc;
+  }
+  // leaf BFS index = first index of the leaf depth + Morton interleave of the
+  // split axes' brick coordinates (child_index, volume.py:252-254)
+  for (int a = 0; a < 3; ++a) {
+    const int n = (g.dims[a] + g.brick[a] - 1) / g.brick[a];
+    morton[a].assign(n, 0);
+    if (!g.split[a]) continue;
+    for (int v = 0; v < n; ++v) {
+      int64_t m = 0;
+      for (int b = 0; b < g.depth; ++b)
+        if ((v >> b) & 1) m |= (int64_t)1 << (3 * b + a);
+      morton[a][v] = m;
+    }
+  }
   if (const char* e = std::getenv("VT_DENSE")) dense_enabled = e[0] != '0';
   h_stats.assign(cap * ST_N * kMaxC, 0);
   flags[0] = NF_EXISTS | NF_INVOL;
@@ -245,6 +271,29 @@ void Tree::node_in_extent(int64_t idx, int c[3]) const {
   g.in_extent(lo, g.level_of(idx), c);
 }
 
+void Tree::clear_seed_of() {
+  for (int64_t c : seed_marked) seed_of[c] = -1;
+  seed_marked.clear();
+}
+
+// ascending sort of node indices (< 2^32): two 16-bit LSD radix passes for
+// large lists (a whole slab's leaves), std::sort otherwise
+void sort_indices(std::vector<int64_t>& v) {
+  if (v.size() < 2048) {
+    std::sort(v.begin(), v.end());
+    return;
+  }
+  std::vector<int64_t> tmp(v.size());
+  for (int pass = 0; pass < 2; ++pass) {
+    const int sh = 16 * pass;
+    std::vector<uint32_t> cnt(65537, 0);
+    for (int64_t x : v) ++cnt[((x >> sh) & 0xFFFF) + 1];
+    for (int i = 0; i < 65536; ++i) cnt[i + 1] += cnt[i];
+    for (int64_t x : v) tmp[cnt[(x >> sh) & 0xFFFF]++] = x;
+    v.swap(tmp);
+  }
+}
+
 void Tree::mark_struct(int64_t idx) {
   if (!struct_mark[idx]) {
     struct_mark[idx] = 1;
@@ -271,28 +320,38 @@ void Tree::ensure_children(int64_t p) {
   if (flags[p] & NF_CHILDREN) return;
   flags[p] |= NF_CHILDREN;
   mark_struct(p);
-  auto it = created_seed.find(p);
-  int64_t src = it == created_seed.end() ? p : it->second;
+  const int64_t src = seed_of[p] >= 0 ? seed_of[p] : p;
   creates.push_back({p, src});
+  int plo[3];
+  g.box_lo(p, plo);
+  const int clvl = g.level_of(p) - 1;
   for (int k = 0; k < 8; ++k) {
     if (!g.octant_real(k)) continue;
     int64_t c = 8 * p + 1 + k;
-    bool inv = in_volume(c);
+    bool inv = true;
+    for (int a = 0; a < 3; ++a) {
+      const int ext = g.extent(a, clvl);
+      const int lo = plo[a] + (((k >> a) & 1) ? ext : 0);
+      inv = inv && lo < g.dims[a] && lo + ext > 0;
+    }
     flags[c] = NF_EXISTS | (inv ? NF_INVOL : 0);
     slot[c] = -1;
     mark_struct(c);
-    created_seed[c] = src;
+    if (seed_of[c] < 0) seed_marked.push_back(c);
+    seed_of[c] = src;
     ++node_count;
     events.emplace_back(VT_EV_CREATED, c);
   }
 }
 
-bool Tree::ensure_brick(int64_t n, const int* cext) {
+bool Tree::ensure_brick(int64_t n, const int* cext, bool seed) {
   if (flags[n] & NF_BRICK) return false;
   int32_t s = alloc_slot();
   flags[n] |= NF_BRICK;
   slot[n] = s;
   mark_struct(n);
+  ++brick_count;
+  if (!seed) return true;
   SeedJob j{};
   j.node = n;
   j.slot = s;
@@ -303,7 +362,6 @@ bool Tree::ensure_brick(int64_t n, const int* cext) {
   }
   // no cover by default (set by the caller when it overwrites a region)
   seeds.push_back(j);
-  ++brick_count;
   return true;
 }
 
@@ -319,6 +377,24 @@ void Tree::free_brick(int64_t n) {
 
 void Tree::flush_structure() {
   if (struct_dirty.empty()) return;
+  int64_t lo = g.capacity, hi = -1;
+  for (int64_t i : struct_dirty) {
+    lo = std::min(lo, i);
+    hi = std::max(hi, i);
+  }
+  const int64_t span = hi - lo + 1;
+  if (span * 5 <= (int64_t)(struct_dirty.size() * sizeof(StructUpd) * 16)) {
+    // dense dirty range (bulk / slab insertions): copy the flag and slot
+    // ranges outright instead of per-node records
+    for (int64_t i : struct_dirty) struct_mark[i] = 0;
+    struct_dirty.clear();
+    void* df = stage_copy(flags.data() + lo, span);
+    VT_CUDA(cudaMemcpyAsync(d_flags + lo, df, span, cudaMemcpyDeviceToDevice, stream));
+    void* ds = stage_copy(slot.data() + lo, span * sizeof(int32_t));
+    VT_CUDA(cudaMemcpyAsync(d_slot + lo, ds, span * sizeof(int32_t), cudaMemcpyDeviceToDevice,
+                            stream));
+    return;
+  }
   std::vector<StructUpd> upd;
   upd.reserve(struct_dirty.size());
   for (int64_t i : struct_dirty) {
@@ -415,15 +491,7 @@ bool Tree::dense_eligible(int channel, const int origin[3], const int dims[3], c
   for (int gz = origin[2] / M[2]; gz <= gz1; ++gz)
     for (int gy = 0; gy <= gy1; ++gy)
       for (int gx = 0; gx <= gx1; ++gx) {
-        const int gg[3] = {gx, gy, gz};
-        int64_t idx = 0;
-        for (int lvl = g.depth; lvl > 0; --lvl) {
-          int k = 0;
-          for (int a = 0; a < 3; ++a)
-            if (g.split[a] && ((gg[a] >> (lvl - 1)) & 1)) k |= 1 << a;
-          idx = 8 * idx + 1 + k;
-        }
-        if (flags[idx] & NF_BRICK) return false;
+        if (flags[leaf_index(gx, gy, gz)] & NF_BRICK) return false;
       }
   return true;
 }
@@ -436,7 +504,7 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
   std::vector<DenseJob> djobs;
   creates.clear();
   seeds.clear();
-  created_seed.clear();
+  clear_seed_of();
   const int* M = g.brick;
   int g0[3], g1[3], gn[3];
   for (int a = 0; a < 3; ++a) {
@@ -454,13 +522,7 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
     for (int gy = g0[1]; gy <= g1[1]; ++gy)
       for (int gx = g0[0]; gx <= g1[0]; ++gx) {
         int gg[3] = {gx, gy, gz};
-        int64_t idx = 0;
-        for (int lvl = g.depth; lvl > 0; --lvl) {
-          int k = 0;
-          for (int a = 0; a < 3; ++a)
-            if (g.split[a] && ((gg[a] >> (lvl - 1)) & 1)) k |= 1 << a;
-          idx = 8 * idx + 1 + k;
-        }
+        const int64_t idx = leaf_index(gx, gy, gz);
         if (!(flags[idx] & NF_EXISTS)) {
           // create the missing part of the chain, top down (creation order
           // and seeds exactly as the reference's descent)
@@ -475,11 +537,10 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
         }
         int ce[3];
         for (int a = 0; a < 3; ++a) ce[a] = std::max(0, std::min(M[a], g.dims[a] - gg[a] * M[a]));
-        bool fresh = ensure_brick(idx, ce);
+        bool fresh = ensure_brick(idx, ce, !dense);
         if (dense) {
           // the dense kernel writes the whole stored brick and its final
           // statistics: no seed, no owed planes, no reduce
-          seeds.pop_back();
           djobs.push_back({idx, slot[idx], 0});
           Pending& p = pend(0, idx);
           p.box = Box{{0, 0, 0}, {M[0], M[1], M[2]}};
@@ -532,9 +593,15 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
   // ancestors (octree.py:363-387): ensure parent bricks, record freshness
   for (int lvl = 1; lvl <= g.depth; ++lvl) {
     std::vector<int64_t>& par = touched[lvl];
-    for (int64_t c : touched[lvl - 1]) par.push_back((c - 1) >> 3);
+    ++anc_gen;
+    for (int64_t c : touched[lvl - 1]) {
+      const int64_t q = (c - 1) >> 3;
+      if (anc_mark[q] != anc_gen) {
+        anc_mark[q] = anc_gen;
+        par.push_back(q);
+      }
+    }
     std::sort(par.begin(), par.end());
-    par.erase(std::unique(par.begin(), par.end()), par.end());
     for (int64_t p : par) {
       bool fresh = ensure_brick(p);
       if (fresh) {
@@ -548,7 +615,7 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
       pend(lvl, p).fresh |= fresh;
     }
   }
-  std::sort(touched[0].begin(), touched[0].end());
+  sort_indices(touched[0]);
   has_pending = true;
   delete anc_scope;
   delete walk_scope;
@@ -593,10 +660,11 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
     flush_structure();
   }
   // NODE_UPDATED for every touched, non-deleted node, sorted (octree.py:393-395)
+  // every level's list is sorted and unique and higher levels hold smaller
+  // BFS indices, so root-first concatenation is the sorted union
   std::vector<int64_t> upd;
-  for (auto& v : touched) upd.insert(upd.end(), v.begin(), v.end());
-  std::sort(upd.begin(), upd.end());
-  upd.erase(std::unique(upd.begin(), upd.end()), upd.end());
+  for (int lvl = g.depth; lvl >= 0; --lvl) upd.insert(upd.end(), touched[lvl].begin(), touched[lvl].end());
+  events.reserve(events.size() + upd.size() * reps);
   for (int r = 0; r < reps; ++r)
     for (int64_t i : upd)
       if (flags[i] & NF_EXISTS) events.emplace_back(VT_EV_UPDATED, i);
@@ -861,7 +929,7 @@ void Tree::merge(int64_t n, const int64_t* idx, const int32_t* nflags, const int
   std::sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return idx[a] < idx[b]; });
   creates.clear();
   seeds.clear();
-  created_seed.clear();
+  clear_seed_of();
   std::vector<int64_t> rec_nodes;
   std::vector<int32_t> rec_stats;
   std::vector<int32_t> brick_slots;

@@ -95,6 +95,10 @@ struct Tree {
   // function of the data; VT_DENSE=0 disables the path (A/B testing)
   bool dense_enabled = true;
   std::vector<uint8_t> complete;
+  std::vector<int64_t> morton[3];
+  int64_t leaf_index(int gx, int gy, int gz) const {
+    return g.level_start[g.depth] + morton[0][gx] + morton[1][gy] + morton[2][gz];
+  }
   int64_t dense_leaf_inserts = 0, dense_level_nodes = 0;
 
   // -- device state --
@@ -139,7 +143,11 @@ struct Tree {
   std::vector<uint8_t> struct_mark;
   std::vector<CreateJob> creates;
   std::vector<SeedJob> seeds;
-  std::unordered_map<int64_t, int64_t> created_seed;  // node created this insertion -> seed src
+  // node created this insertion -> its seed source (flat, reset per insertion)
+  std::vector<int64_t> seed_of, seed_marked;
+  void clear_seed_of();
+  std::vector<uint32_t> anc_mark;  // ancestor dedupe, generation stamped
+  uint32_t anc_gen = 0;
 
   // pinned host -> device staging ring for job lists (no implicit syncs of
   // pageable copies; wraps only after the stream has drained the old data)
@@ -169,7 +177,7 @@ struct Tree {
   int32_t alloc_slot();
   void ensure_pool(int64_t slots_needed);
   void ensure_children(int64_t p);
-  bool ensure_brick(int64_t n, const int* cext = nullptr);
+  bool ensure_brick(int64_t n, const int* cext = nullptr, bool seed = true);
   void node_in_extent(int64_t idx, int c[3]) const;
 
   // insertion / propagation
@@ -198,6 +206,8 @@ struct Tree {
 
   int32_t stat(int64_t node, int s, int c) const { return h_stats[st_index(node, s, c)]; }
 };
+
+void sort_indices(std::vector<int64_t>& v);
 
 // launch helpers implemented in build_kernels.cu
 void launch_struct_update(const Tree& t, const StructUpd* d_upd, int n);
