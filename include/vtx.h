@@ -136,9 +136,12 @@ vt_status vt_tree_info_get(vt_tree* tree, vt_tree_info* out);
  * leaf bricks and statistics outright, and parents whose in-volume children
  * are all complete are recomputed in one pass; results, events and slots are
  * identical to the general path.  Enabled by default (env VT_DENSE=0 or
- * enabled = 0 turns it off); counts = dense leaf insertions / dense parents. */
+ * enabled = 0 turns it off); counts = dense leaf insertions / dense parents /
+ * fill_borders calls that only had to patch owed z-shells of prefilled
+ * leaves (env VT_PREFILL=0 disables shell prefill). */
 vt_status vt_tree_set_dense(vt_tree* tree, int32_t enabled);
-vt_status vt_tree_dense_counts(vt_tree* tree, int64_t* leaf_inserts, int64_t* level_nodes);
+vt_status vt_tree_dense_counts(vt_tree* tree, int64_t* leaf_inserts, int64_t* level_nodes,
+                               int64_t* fast_borders);
 /* Octree.node_by_index (octree.py:515-528): *exists = 0 when absent */
 vt_status vt_tree_node(vt_tree* tree, int64_t index, vt_node* out, int32_t* exists);
 /* Octree.iter_nodes order (BFS == ascending index, octree.py:507-513);

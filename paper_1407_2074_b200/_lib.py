@@ -85,7 +85,7 @@ SIGNATURES = {
     "vt_tree_wait_stream": [P, P],
     "vt_tree_signal_stream": [P, P],
     "vt_tree_set_dense": [P, I32],
-    "vt_tree_dense_counts": [P, PI64, PI64],
+    "vt_tree_dense_counts": [P, PI64, PI64, PI64],
     "vt_tree_finalize": [P],
     "vt_tree_fill_borders": [P],
     "vt_tree_sync": [P],

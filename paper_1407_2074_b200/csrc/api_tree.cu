@@ -176,10 +176,12 @@ vt_status vt_tree_set_dense(vt_tree* tree, int32_t enabled) {
   });
 }
 
-vt_status vt_tree_dense_counts(vt_tree* tree, int64_t* leaf_inserts, int64_t* level_nodes) {
+vt_status vt_tree_dense_counts(vt_tree* tree, int64_t* leaf_inserts, int64_t* level_nodes,
+                               int64_t* fast_borders) {
   return guarded([&] {
     if (leaf_inserts) *leaf_inserts = tree->t.dense_leaf_inserts;
     if (level_nodes) *level_nodes = tree->t.dense_level_nodes;
+    if (fast_borders) *fast_borders = tree->t.fast_borders;
   });
 }
 
@@ -255,6 +257,7 @@ vt_status vt_tree_read_brick(vt_tree* tree, int64_t index, void* out) {
     VT_REQUIRE(index >= 0 && index < t.g.capacity && (t.flags[index] & NF_BRICK), VT_EINVAL,
                "node has no brick");
     t.flush();
+    t.publish_halos();
     const int64_t bytes = t.g.brick_elems * t.g.sb;
     VT_CUDA(cudaMemcpyAsync(out, t.d_pool + (int64_t)t.slot[index] * bytes, bytes,
                             cudaMemcpyDeviceToHost, t.stream));
@@ -267,6 +270,7 @@ vt_status vt_tree_export(vt_tree* tree, int64_t n, const int64_t* indices, int32
   return guarded([&] {
     Tree& t = tree->t;
     t.flush();
+    t.publish_halos();
     std::vector<int64_t> nodes(indices, indices + n);
     for (int64_t i : nodes)
       VT_REQUIRE(i >= 0 && i < t.g.capacity && (t.flags[i] & NF_EXISTS), VT_EINVAL,
@@ -304,6 +308,7 @@ vt_status vt_tree_checksum(vt_tree* tree, uint64_t* out) {
   return guarded([&] {
     Tree& t = tree->t;
     t.flush();
+    t.publish_halos();
     std::vector<int64_t> nodes;
     std::vector<int32_t> slots;
     for (int64_t i = 0; i < t.g.capacity; ++i)
@@ -350,6 +355,7 @@ vt_status vt_tree_export_nodes(vt_tree* tree, int64_t n, const int64_t* indices,
   return guarded([&] {
     Tree& t = tree->t;
     t.flush();
+    t.publish_halos();
     std::vector<int64_t> nodes(indices, indices + n);
     std::vector<int32_t> slots;
     for (int64_t r = 0; r < n; ++r) {

@@ -396,23 +396,42 @@ __device__ __forceinline__ void bulk_wait() {
 }
 
 // One CTA (8 warps) per leaf brick, stored planes in stages of P = 2.  The
-// TMA engine streams the block rows of a stage (one bulk copy per row) into
-// a 3-deep shared-memory input ring; the warps move every interior voxel
-// (C samples) from its staged row into a shared-memory image of the stored
-// planes (shell pre-filled with the background, octree.py:234-237, never
-// rewritten), accumulating per-plane statistics with compile-time channel
-// indices; one bulk copy then writes the stage's planes (P x (Mx+2)(My+2)C
-// samples, contiguous in the brick) to HBM from a 3-deep output ring.  Data
-// in flight lives in shared memory, not registers.
+// TMA engine streams the block region a stage needs — one 3-D tensor tile of
+// (Mx+2)*C samples x (My+2) rows x P planes, i.e. the brick's planes WITH
+// their one-voxel x/y/z halo, zero-filled outside the block — into a 3-deep
+// shared-memory input ring; the warps write every stored voxel into a
+// shared-memory image of the stored planes, accumulating the interior's
+// per-plane statistics with compile-time channel indices, and one bulk copy
+// writes the stage's planes (contiguous in the brick) to HBM from a 3-deep
+// output ring.  Data in flight lives in shared memory, not registers.
+//
+// Shell voxels: with `prefill` they receive the value fill_borders will give
+// them at threshold 0 once every in-volume leaf is complete — the block
+// voxel when it lies inside the volume (the same-level neighbour's interior,
+// octree.py:593-605), else the background (outside the virtual extent, or an
+// out-of-volume neighbour whose AVG is the background) — except z-shell
+// planes whose block plane lies outside this insertion (owed: background
+// now, copied from the neighbour brick by fill_borders).  The tree keeps
+// such shells logically background until fill_borders (Tree::halo_prefill).
+// Without `prefill` every shell voxel is the background (_ensure_brick,
+// octree.py:234-237).
 constexpr int kTmaStages = 3;
 constexpr int kTmaWarps = 8;
 constexpr int kTmaP = 2;
 
+// staged row: the stored row's (Mx+2)*C samples from a 16-byte aligned start
+// (the TMA inner coordinate must be a multiple of 8 samples), <= 7 leading
+__host__ __device__ inline int tma_box_row(int mx, int C) { return ((mx + 2) * C + 7 + 7) / 8 * 8; }
+__host__ __device__ inline uint32_t tma_in_bytes(int mx, int my, int C) {
+  return ((uint32_t)kTmaP * (my + 2) * tma_box_row(mx, C) * 2 + 127) / 128 * 128;
+}
+
 template <int C>
 __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
-    const __grid_constant__ CUtensorMap map, int oz, const DenseJob* __restrict__ jobs, int gnx, int gny,
-    int g0z, Geo g, uint16_t* __restrict__ pool, int32_t* pmin, int32_t* pmax,
-    unsigned long long* psum, int32_t* stats, const uint8_t* __restrict__ flags) {
+    const __grid_constant__ CUtensorMap map, int oz, int dz, int prefill,
+    const DenseJob* __restrict__ jobs, int gnx, int gny, int g0z, Geo g,
+    uint16_t* __restrict__ pool, int32_t* pmin, int32_t* pmax, unsigned long long* psum,
+    int32_t* stats, const uint8_t* __restrict__ flags) {
   constexpr int P = kTmaP;
   constexpr int WPP = kTmaWarps / P;  // warps per plane
   extern __shared__ __align__(128) unsigned char s_dyn[];
@@ -427,11 +446,11 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
   const int gz = g0z + (int)(blockIdx.x / (gnx * gny));
   const int Mx = g.brick[0], My = g.brick[1], Mz = g.brick[2];
   const int Sx = g.stored[0], Sy = g.stored[1], Sz = g.stored[2];
-  const int X = g.dims[0], Y = g.dims[1];
-  const int cx = min(Mx, X - gx * Mx), cy = min(My, Y - gy * My), cz = min(Mz, g.dims[2] - gz * Mz);
-  const uint32_t rowbytes = (uint32_t)Mx * C * 2;           // staged block row
-  const uint32_t in_bytes = (uint32_t)P * My * rowbytes;    // one input stage
-  const uint32_t plane_elems = (uint32_t)Sx * Sy * C;       // one stored plane
+  const int X = g.dims[0], Y = g.dims[1], Z = g.dims[2];
+  const int cx = min(Mx, X - gx * Mx), cy = min(My, Y - gy * My), cz = min(Mz, Z - gz * Mz);
+  const int brow = tma_box_row(Mx, C);                       // staged row (samples)
+  const uint32_t in_bytes = tma_in_bytes(Mx, My, C);         // one input stage
+  const uint32_t plane_elems = (uint32_t)Sx * Sy * C;        // one stored plane
   const uint32_t out_bytes = (uint32_t)P * plane_elems * 2;  // one output stage
   unsigned char* s_in = s_dyn;
   uint16_t* s_out = reinterpret_cast<uint16_t*>(s_dyn + (size_t)kTmaStages * in_bytes);
@@ -439,6 +458,9 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint16_t* brick = pool + (int64_t)j.slot * g.brick_elems;
   const uint16_t bg = (uint16_t)g.bg;
+  const int x0 = gx * Mx - 1, y0 = gy * My - 1;  // block voxel of stored (0, 0)
+  const int xa = x0 * C - (((x0 * C) % 8 + 8) % 8);  // 16-byte aligned tile start (samples)
+  const int xoff = x0 * C - xa;                     // leading samples in a staged row
 
   if (tid == 0) {
     for (int b = 0; b < kTmaStages; ++b) mbar_init(&s_bar[b], 1);
@@ -449,41 +471,31 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
     s_tmx[tid] = INT_MIN;
     s_tsm[tid] = 0;
   }
-  // output ring: background everywhere (the shell and anything outside the
-  // in-volume extent stay background; only in-volume interiors are written)
-  {
-    uint32_t* o = reinterpret_cast<uint32_t*>(s_out);
-    const uint32_t bgw = (uint32_t)bg | ((uint32_t)bg << 16);
-    for (uint32_t i = tid; i < kTmaStages * out_bytes / 4; i += blockDim.x) o[i] = bgw;
-  }
   __syncthreads();
 
-  // one 3-D tensor tile per stage: Mx*C samples x My rows x P planes of the
-  // block, out-of-range rows/planes zero-filled by the TMA unit (never read)
-  auto issue = [&](int s) {  // one thread
+  auto issue = [&](int s) {  // one thread: one tensor tile per stage
     const int b = s % kTmaStages;
-    mbar_expect_tx(&s_bar[b], in_bytes);
-    tma_load_3d(s_in + (size_t)b * in_bytes, &map, gx * Mx * C, gy * My, gz * Mz - oz + P * s - 1,
-                &s_bar[b]);
+    mbar_expect_tx(&s_bar[b], (uint32_t)P * (My + 2) * brow * 2);
+    tma_load_3d(s_in + (size_t)b * in_bytes, &map, xa, y0, gz * Mz - oz + P * s - 1, &s_bar[b]);
   };
   if (tid == 0)
     for (int s = 0; s < min(kTmaStages, nstages); ++s) issue(s);
 
-  const int pw = warp / WPP;  // plane of the stage this warp builds
-  const int rw = warp % WPP;  // its row phase
+  const int pw = warp / WPP;             // plane of the stage this warp group builds
+  const int pt = (warp % WPP) * 32 + lane;  // thread within the plane group
+  const uint32_t sxm = (uint32_t)((((uint64_t)1 << 32) + Sx - 1) / Sx);  // v / Sx by mul-high
   for (int s = 0; s < nstages; ++s) {
     const int b = s % kTmaStages;
     const int zs = P * s + pw;
     const int zi = zs - 1;
-    const bool zdata = zi >= 0 && zi < cz;
+    const int rz = gz * Mz + zi;  // block-volume z of this stored plane
+    // 1: interior data plane, 2: shell plane taken from the block, 0: background
+    const int mode = (zi >= 0 && zi < cz) ? 1
+                     : (prefill && zs < Sz && rz >= 0 && rz < Z && rz - oz >= 0 && rz - oz < dz) ? 2
+                                                                                               : 0;
     uint16_t* oplane = s_out + (size_t)b * (out_bytes / 2) + (size_t)pw * plane_elems;
-    if (!zdata) {
-      // a shell plane or one past the in-volume extent: all background (the
-      // ring slot may hold an interior plane from an earlier stage)
-      if (s >= kTmaStages || zs == 0)
-        for (uint32_t i = rw * 32 + lane; i < plane_elems; i += WPP * 32) oplane[i] = bg;
-    }
-    mbar_wait(&s_bar[b], (uint32_t)(s / kTmaStages) & 1u);
+    const uint16_t* iplane = reinterpret_cast<const uint16_t*>(s_in + (size_t)b * in_bytes) +
+                             (size_t)pw * (My + 2) * brow;
     int mn[C], mx[C];
     unsigned sm[C];
 #pragma unroll
@@ -492,20 +504,29 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
       mx[c] = INT_MIN;
       sm[c] = 0;
     }
-    if (zdata) {
-      const uint16_t* iplane =
-          reinterpret_cast<const uint16_t*>(s_in + (size_t)b * in_bytes + (size_t)pw * My * rowbytes);
-      for (int y = rw; y < cy; y += WPP) {
-        const uint16_t* irow = iplane + (size_t)y * Mx * C;
-        uint16_t* orow = oplane + ((size_t)(y + 1) * Sx + 1) * C;
-        for (int x = lane; x < cx; x += 32) {
+    // every thread waits, so the slot's phase is complete before it is re-armed
+    mbar_wait(&s_bar[b], (uint32_t)(s / kTmaStages) & 1u);
+    if (mode == 0) {
+      if (zs < Sz)
+        for (uint32_t i = pt; i < plane_elems; i += WPP * 32) oplane[i] = bg;
+    } else {
+      for (int v = pt; v < Sx * Sy; v += WPP * 32) {
+        const int ys = (int)__umulhi((uint32_t)v, sxm);
+        const int xs = v - ys * Sx;
+        const int rx = x0 + xs, ry = y0 + ys;
+        const bool interior = xs >= 1 && xs <= cx && ys >= 1 && ys <= cy;
+        const bool take = interior || (prefill && rx >= 0 && rx < X && ry >= 0 && ry < Y);
+        const uint16_t* iv = iplane + (size_t)ys * brow + xoff + xs * C;
+        uint16_t* ov = oplane + (size_t)v * C;
+#pragma unroll
+        for (int c = 0; c < C; ++c) ov[c] = take ? iv[c] : bg;
+        if (mode == 1 && interior) {
 #pragma unroll
           for (int c = 0; c < C; ++c) {
-            const uint16_t v = irow[x * C + c];
-            orow[x * C + c] = v;
-            mn[c] = min(mn[c], (int)v);
-            mx[c] = max(mx[c], (int)v);
-            sm[c] += v;
+            const int val = iv[c];
+            mn[c] = min(mn[c], val);
+            mx[c] = max(mx[c], val);
+            sm[c] += (unsigned)val;
           }
         }
       }
@@ -536,7 +557,10 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
         // the output slot of stage s+1 was last read by the store of stage
         // s+1-kTmaStages: keep at most kTmaStages-2 stores pending
         bulk_wait_read<kTmaStages - 2>();
-        if (s + kTmaStages < nstages) issue(s + kTmaStages);
+        if (s + kTmaStages < nstages) {
+          // every warp is past its wait on this slot (the barrier above)
+          issue(s + kTmaStages);
+        }
       }
     }
     if (tid < C) {
@@ -707,27 +731,55 @@ __global__ void __launch_bounds__(256) k_dense_level(const int64_t* __restrict__
   finish_stats<C>(tot, node, (int64_t)pcx * pcy * pcz, false, g, flags, stats);
 }
 
+// fill_borders' z-shell fix-up for prefilled leaves (Tree::fill_borders):
+// job = (dst slot, dst stored plane, src slot, src stored plane); a stored
+// plane is contiguous, so this is a straight 32-bit word copy
+__global__ void k_plane_copy(const int32_t* __restrict__ jobs, int n, int64_t brick_words,
+                             int plane_words, uint32_t* pool) {
+  const int32_t* j = jobs + 4 * blockIdx.x;
+  uint32_t* dst = pool + (int64_t)j[0] * brick_words + (int64_t)j[1] * plane_words;
+  const uint32_t* src = pool + (int64_t)j[2] * brick_words + (int64_t)j[3] * plane_words;
+  for (int i = threadIdx.x; i < plane_words; i += blockDim.x) dst[i] = src[i];
+}
+
+// every shell voxel of a brick <- background (publishing prefilled shells as
+// the reference's pre-fill_borders state, Tree::publish_halos)
+template <class T>
+__global__ void k_clear_shells(const int32_t* __restrict__ slots, Geo g, T* pool) {
+  T* b = pool + (int64_t)slots[blockIdx.x] * g.brick_elems;
+  const int Sx = g.stored[0], Sy = g.stored[1], Sz = g.stored[2], C = g.C;
+  const int n = Sx * Sy * Sz;
+  for (int v = threadIdx.x; v < n; v += blockDim.x) {
+    const int x = v % Sx, y = (v / Sx) % Sy, z = v / (Sx * Sy);
+    if (x == 0 || y == 0 || z == 0 || x == Sx - 1 || y == Sy - 1 || z == Sz - 1)
+      for (int c = 0; c < C; ++c) b[(int64_t)v * C + c] = (T)g.bg;
+  }
+}
+
 int planes_per_warp(int sz) { return (sz + 11) / 12; }  // <= 12 warps per CTA
 
 }  // namespace
 
 #define VT_CHECK_LAUNCH() VT_CUDA(cudaGetLastError())
 
-// TMA tensor tiles need a 16-byte aligned block, row pitches and box rows
-// that are multiples of 16 bytes, and 128-byte aligned shared stages
-static bool tma_ok(const Tree& t, const void* src, int64_t rowbytes) {
+// TMA tensor tiles need a 16-byte aligned block and row pitch, a box row of
+// at most 256 samples, and the rings must fit in shared memory
+static size_t tma_smem(const Geo& g) {
+  return (size_t)kTmaStages * (tma_in_bytes(g.brick[0], g.brick[1], g.C) +
+                               (size_t)kTmaP * g.stored[0] * g.stored[1] * g.C * 2);
+}
+static bool tma_ok(const Tree& t, const void* src) {
   if (std::getenv("VT_DENSE_TMA") && std::getenv("VT_DENSE_TMA")[0] == '0') return false;
   const int64_t stride = (int64_t)t.g.dims[0] * t.g.C * 2;
-  return ((uintptr_t)src & 15) == 0 && rowbytes % 16 == 0 && stride % 16 == 0 &&
-         (rowbytes * t.g.brick[1] * kTmaP) % 128 == 0 &&
-         (int64_t)kTmaStages * kTmaP *
-                 (rowbytes * t.g.brick[1] + (int64_t)t.g.stored[0] * t.g.stored[1] * t.g.C * 2) <=
-             200 * 1024;
+  return t.g.sb == 2 && ((uintptr_t)src & 15) == 0 && stride % 16 == 0 &&
+         tma_box_row(t.g.brick[0], t.g.C) <= 256 && t.g.brick[1] + 2 <= 256 &&
+         tma_smem(t.g) <= 200 * 1024;
 }
 
-// 3-D tensor map of a (dz, Y, X*C) u16 block for the TMA unit; the encoder
-// comes from the driver through the runtime (no libcuda link)
-static bool encode_block_map(const Tree& t, const void* src, int64_t nsrc, CUtensorMap* map) {
+// 3-D tensor map of a (dz, Y, X*C) u16 block for the TMA unit, box = one
+// stage of stored planes with their halo; the encoder comes from the driver
+// through the runtime (no libcuda link)
+static bool encode_block_map(const Tree& t, const void* src, int64_t dz, CUtensorMap* map) {
   using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                               const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                               const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -747,36 +799,34 @@ static bool encode_block_map(const Tree& t, const void* src, int64_t nsrc, CUten
   if (!enc) return false;
   const int C = t.g.C;
   const int64_t row = (int64_t)t.g.dims[0] * C;
-  const int64_t dz = nsrc / (row * t.g.dims[1]);
   cuuint64_t dims[3] = {(cuuint64_t)row, (cuuint64_t)t.g.dims[1], (cuuint64_t)dz};
   cuuint64_t strides[2] = {(cuuint64_t)row * 2, (cuuint64_t)row * 2 * t.g.dims[1]};
-  cuuint32_t box[3] = {(cuuint32_t)(t.g.brick[0] * C), (cuuint32_t)t.g.brick[1],
+  cuuint32_t box[3] = {(cuuint32_t)tma_box_row(t.g.brick[0], C), (cuuint32_t)(t.g.brick[1] + 2),
                        (cuuint32_t)kTmaP};
   cuuint32_t es[3] = {1, 1, 1};
-  if (box[0] > 256 || box[1] > 256) return false;
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, const_cast<void*>(src), dims, strides, box,
              es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// returns true when the shells were prefilled (TMA path)
 template <class T, int C>
-static void leaf_launch(const Tree& t, const void* src, int64_t nsrc, int oz,
+static bool leaf_launch(const Tree& t, const void* src, int64_t nsrc, int oz, int prefill,
                         const DenseJob* jobs, int n, const int gn[3], int g0z) {
   const int sz = t.g.stored[2];
   const int rowlen = t.g.stored[0] * C;
   const int wpl = (rowlen / 2 + 31) / 32;
-  const int64_t rowbytes = (int64_t)t.g.brick[0] * C * 2;
+  const int64_t dz = nsrc / ((int64_t)t.g.dims[0] * t.g.dims[1] * C);
   CUtensorMap map;
-  if (sizeof(T) == 2 && tma_ok(t, src, rowbytes) && encode_block_map(t, src, nsrc, &map)) {
-    const size_t smem = (size_t)kTmaStages * kTmaP *
-                        (rowbytes * t.g.brick[1] + (size_t)t.g.stored[0] * t.g.stored[1] * C * 2);
+  if (sizeof(T) == 2 && tma_ok(t, src) && encode_block_map(t, src, dz, &map)) {
+    const size_t smem = tma_smem(t.g);
     auto k = k_dense_leaf_tma<C>;
     VT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k<<<n, kTmaWarps * 32, smem, t.stream>>>(map, oz, jobs, gn[0], gn[1], g0z, t.g,
-                                            (uint16_t*)t.d_pool, t.d_pmin, t.d_pmax, t.d_psum,
-                                            t.d_stats, t.d_flags);
+    k<<<n, kTmaWarps * 32, smem, t.stream>>>(map, oz, (int)dz, prefill, jobs, gn[0], gn[1], g0z,
+                                            t.g, (uint16_t*)t.d_pool, t.d_pmin, t.d_pmax,
+                                            t.d_psum, t.d_stats, t.d_flags);
     VT_CHECK_LAUNCH();
-    return;
+    return prefill != 0;
   }
   if (sizeof(T) == 2 && rowlen % 2 == 0 && wpl <= 4) {
     // warps own ceil(Sz / 17) planes each (<= 17 warps)
@@ -796,7 +846,7 @@ static void leaf_launch(const Tree& t, const void* src, int64_t nsrc, int oz,
     }
 #undef VT_LEAF16
     VT_CHECK_LAUNCH();
-    return;
+    return false;
   }
   const int ppw = planes_per_warp(sz);
   const int warps = (sz + ppw - 1) / ppw;
@@ -804,26 +854,42 @@ static void leaf_launch(const Tree& t, const void* src, int64_t nsrc, int oz,
       (const T*)src, oz, jobs, gn[0], gn[1], g0z, t.g, (T*)t.d_pool, t.d_pmin, t.d_pmax, t.d_psum,
       t.d_stats, t.d_flags, ppw);
   VT_CHECK_LAUNCH();
+  return false;
 }
 
 template <class T>
-static void leaf_dispatch(const Tree& t, const void* src, int64_t nsrc, int oz,
+static bool leaf_dispatch(const Tree& t, const void* src, int64_t nsrc, int oz, int prefill,
                           const DenseJob* jobs, int n, const int gn[3], int g0z) {
   switch (t.g.C) {
-    case 1: leaf_launch<T, 1>(t, src, nsrc, oz, jobs, n, gn, g0z); break;
-    case 2: leaf_launch<T, 2>(t, src, nsrc, oz, jobs, n, gn, g0z); break;
-    case 3: leaf_launch<T, 3>(t, src, nsrc, oz, jobs, n, gn, g0z); break;
-    default: leaf_launch<T, 4>(t, src, nsrc, oz, jobs, n, gn, g0z); break;
+    case 1: return leaf_launch<T, 1>(t, src, nsrc, oz, prefill, jobs, n, gn, g0z);
+    case 2: return leaf_launch<T, 2>(t, src, nsrc, oz, prefill, jobs, n, gn, g0z);
+    case 3: return leaf_launch<T, 3>(t, src, nsrc, oz, prefill, jobs, n, gn, g0z);
+    default: return leaf_launch<T, 4>(t, src, nsrc, oz, prefill, jobs, n, gn, g0z);
   }
 }
 
-void launch_dense_leaf(const Tree& t, const void* src, int64_t nsrc, int oz, const DenseJob* jobs,
-                       int n, const int gn[3], int g0z) {
+void launch_plane_copy(const Tree& t, const int32_t* d_jobs, int n) {
+  if (n <= 0) return;
+  const int64_t bw = t.g.brick_elems * t.g.sb / 4;
+  const int pw = t.g.stored[0] * t.g.stored[1] * t.g.C * t.g.sb / 4;
+  k_plane_copy<<<n, 256, 0, t.stream>>>(d_jobs, n, bw, pw, (uint32_t*)t.d_pool);
+  VT_CHECK_LAUNCH();
+}
+
+void launch_clear_shells(const Tree& t, const int32_t* d_slots, int n) {
   if (n <= 0) return;
   if (t.g.sb == 1)
-    leaf_dispatch<uint8_t>(t, src, nsrc, oz, jobs, n, gn, g0z);
+    k_clear_shells<uint8_t><<<n, 256, 0, t.stream>>>(d_slots, t.g, t.d_pool);
   else
-    leaf_dispatch<uint16_t>(t, src, nsrc, oz, jobs, n, gn, g0z);
+    k_clear_shells<uint16_t><<<n, 256, 0, t.stream>>>(d_slots, t.g, (uint16_t*)t.d_pool);
+  VT_CHECK_LAUNCH();
+}
+
+bool launch_dense_leaf(const Tree& t, const void* src, int64_t nsrc, int oz, int prefill,
+                       const DenseJob* jobs, int n, const int gn[3], int g0z) {
+  if (n <= 0) return prefill != 0;
+  if (t.g.sb == 1) return leaf_dispatch<uint8_t>(t, src, nsrc, oz, 0, jobs, n, gn, g0z);
+  return leaf_dispatch<uint16_t>(t, src, nsrc, oz, prefill, jobs, n, gn, g0z);
 }
 
 template <class T, int C>

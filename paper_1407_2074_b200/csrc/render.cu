@@ -1332,6 +1332,10 @@ vt_status vt_mirror_create(vt_tree* tree, int64_t slot_count, vt_mirror** out) {
   return guarded([&] {
     Tree& t = tree->t;
     t.flush();
+    // the mirror exposes pool shells: publish prefilled ones as background
+    // and write later dense leaves with background shells
+    t.publish_halos();
+    t.prefill_enabled = false;
     auto* m = new vt_mirror();
     m->tree = tree;
     vt_tree_retain(tree);

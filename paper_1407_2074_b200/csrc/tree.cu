@@ -123,6 +123,7 @@ Tree::Tree(const vt_tree_desc& d) {
     }
   }
   if (const char* e = std::getenv("VT_DENSE")) dense_enabled = e[0] != '0';
+  if (const char* e = std::getenv("VT_PREFILL")) prefill_enabled = e[0] != '0';
   h_stats.assign(cap * ST_N * kMaxC, 0);
   flags[0] = NF_EXISTS | NF_INVOL;
   for (int c = 0; c < g.C; ++c)
@@ -636,10 +637,31 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
   if (dense) {
     ProfScope q(prof, 7);
     DenseJob* dj = upload(*this, djobs);
-    launch_dense_leaf(*this, dsrc, nvox * src_stride, origin[2], dj, (int)djobs.size(), gn, g0[2]);
+    const bool want = prefill_enabled && !borders;
+    const bool pre = launch_dense_leaf(*this, dsrc, nvox * src_stride, origin[2], want ? 1 : 0, dj,
+                                       (int)djobs.size(), gn, g0[2]);
     release(*this, dj);
     ++dense_leaf_inserts;
+    if (pre) {
+      // z-shell planes whose block plane lies outside this insertion are owed
+      halo_prefill = true;
+      const int z0 = origin[2], z1 = origin[2] + dims[2];
+      for (int gz = g0[2]; gz <= g1[2]; ++gz) {
+        const int lo = gz * M[2] - 1, hi = (gz + 1) * M[2];
+        const bool olo = lo >= 0 && lo < z0, ohi = hi < g.dims[2] && hi >= z1;
+        if (!olo && !ohi) continue;
+        for (int gy = g0[1]; gy <= g1[1]; ++gy)
+          for (int gx = g0[0]; gx <= g1[0]; ++gx) {
+            const int64_t idx = leaf_index(gx, gy, gz);
+            if (olo) owed_lo.push_back(idx);
+            if (ohi) owed_hi.push_back(idx);
+          }
+      }
+    } else {
+      prefill_valid = false;
+    }
   } else {
+    prefill_valid = false;
     ProfScope q(prof, 7);
     dl = upload(*this, leaf_slots);
     launch_scatter(*this, dsrc, channel, src_stride, src_off, origin, dims, g0, gn, dl);
@@ -905,13 +927,63 @@ void Tree::fill_borders() {
   flush();
   ++data_version;
   std::vector<BorderJob> jobs;
+  std::vector<int64_t> bricks;
   for (int64_t i = 0; i < g.capacity; ++i)
-    if ((flags[i] & NF_EXISTS) && (flags[i] & NF_BRICK)) jobs.push_back({i, slot[i]});
+    if ((flags[i] & NF_EXISTS) && (flags[i] & NF_BRICK)) bricks.push_back(i);
+  // Fast path: every in-volume leaf complete and every leaf shell prefilled
+  // by the dense build (dense_build.cu) with nothing mutated since.  Then
+  // each leaf shell already holds its fill_borders value except owed z-shell
+  // planes, which equal the z-neighbour's adjacent stored plane (shell
+  // included — the neighbour's x/y shell is the same volume voxels).
+  const bool fast = halo_prefill && prefill_valid && !borders && complete[0];
+  if (fast) {
+    ++fast_borders;
+    std::vector<int32_t> pj;
+    const int mz = g.brick[2];
+    auto add = [&](int64_t leaf, int dz_) {
+      int lo[3];
+      g.box_lo(leaf, lo);
+      const int64_t nb = leaf_index(lo[0] / g.brick[0], lo[1] / g.brick[1], lo[2] / mz + dz_);
+      VT_REQUIRE((flags[nb] & NF_BRICK), VT_ESTATE, "fill_borders: neighbour brick missing");
+      pj.insert(pj.end(), {slot[leaf], dz_ < 0 ? 0 : mz + 1, slot[nb], dz_ < 0 ? mz : 1});
+    };
+    for (int64_t i : owed_lo) add(i, -1);
+    for (int64_t i : owed_hi) add(i, +1);
+    int32_t* dp = upload(*this, pj);
+    launch_plane_copy(*this, dp, (int)(pj.size() / 4));
+    release(*this, dp);
+    for (int64_t i : bricks)
+      if (g.level_of(i) > 0) jobs.push_back({i, slot[i]});
+  } else {
+    for (int64_t i : bricks) jobs.push_back({i, slot[i]});
+  }
   BorderJob* d = upload(*this, jobs);
   launch_borders(*this, d, (int)jobs.size());
   release(*this, d);
-  for (auto& j : jobs) events.emplace_back(VT_EV_UPDATED, j.node);
+  for (int64_t i : bricks) events.emplace_back(VT_EV_UPDATED, i);
   borders = true;
+  halo_prefill = false;
+  owed_lo.clear();
+  owed_hi.clear();
+}
+
+// Prefilled leaf shells are the reference's background until fill_borders:
+// any reader of pool shells first resets them (then fill_borders takes the
+// general path).
+void Tree::publish_halos() {
+  if (!halo_prefill || borders) return;
+  flush();
+  std::vector<int32_t> sl;
+  for (int64_t i = 0; i < g.capacity; ++i)
+    if ((flags[i] & NF_EXISTS) && (flags[i] & NF_BRICK) && g.level_of(i) == 0)
+      sl.push_back(slot[i]);
+  int32_t* d = upload(*this, sl);
+  launch_clear_shells(*this, d, (int)sl.size());
+  release(*this, d);
+  halo_prefill = false;
+  prefill_valid = false;
+  owed_lo.clear();
+  owed_hi.clear();
 }
 
 // ---------------------------------------------------------------------------
@@ -920,6 +992,8 @@ void Tree::fill_borders() {
 
 void Tree::merge(int64_t n, const int64_t* idx, const int32_t* nflags, const int32_t* stats_in,
                  const void* bricks, int mem_kind, int64_t inserted_voxels) {
+  publish_halos();
+  prefill_valid = false;
   flush();
   ++data_version;
   const int C = g.C;

@@ -96,10 +96,18 @@ struct Tree {
   bool dense_enabled = true;
   std::vector<uint8_t> complete;
   std::vector<int64_t> morton[3];
+  // shells of dense leaves written with their fill_borders values at
+  // insertion (dense_build.cu).  While !borders they are logically the
+  // background: every reader of pool shells calls publish_halos() first.
+  bool prefill_enabled = true;   // env VT_PREFILL=0 / a device mirror turns it off
+  bool halo_prefill = false;     // some leaf shells hold prefilled values
+  bool prefill_valid = true;     // no general-path mutation since (fast fill_borders)
+  std::vector<int64_t> owed_lo, owed_hi;  // leaves whose z-shell plane awaits a neighbour
+  void publish_halos();
   int64_t leaf_index(int gx, int gy, int gz) const {
     return g.level_start[g.depth] + morton[0][gx] + morton[1][gy] + morton[2][gz];
   }
-  int64_t dense_leaf_inserts = 0, dense_level_nodes = 0;
+  int64_t dense_leaf_inserts = 0, dense_level_nodes = 0, fast_borders = 0;
 
   // -- device state --
   uint8_t* d_pool = nullptr;  // [pool_slots][Sz][Sy][Sx][C] samples
@@ -221,8 +229,12 @@ bool scatter_owns_stats(const Geo& g, int channel, const int origin[3], const in
                         int gy);
 void launch_octant(const Tree& t, const OctJob* d_jobs, int n);
 // dense_build.cu
-void launch_dense_leaf(const Tree& t, const void* src, int64_t nsrc, int oz, const DenseJob* jobs,
-                       int n, const int gn[3], int g0z);
+bool launch_dense_leaf(const Tree& t, const void* src, int64_t nsrc, int oz, int prefill,
+                       const DenseJob* jobs, int n, const int gn[3], int g0z);
+// z-shell plane copies between leaf bricks: dst plane <- src plane
+void launch_plane_copy(const Tree& t, const int32_t* d_jobs, int n);
+// every shell voxel of the given bricks <- background
+void launch_clear_shells(const Tree& t, const int32_t* d_slots, int n);
 void launch_dense_level(const Tree& t, const int64_t* nodes, int n);
 void launch_plane(const Tree& t, const PlaneJob* d_jobs, int n);
 void launch_reduce(const Tree& t, const ReduceJob* d_jobs, int n);

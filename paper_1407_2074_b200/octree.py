@@ -404,11 +404,12 @@ class Octree:
             _lib.call("vt_tree_set_dense", self._h, 1 if on else 0)
             self._dense = bool(on)
 
-    def dense_counts(self) -> tuple[int, int]:
-        """(dense leaf insertions, dense parent recomputes) so far."""
-        a, b = ct.c_int64(), ct.c_int64()
-        _lib.call("vt_tree_dense_counts", self._h, ct.byref(a), ct.byref(b))
-        return int(a.value), int(b.value)
+    def dense_counts(self) -> tuple[int, int, int]:
+        """(dense leaf insertions, dense parent recomputes, fill_borders calls
+        served by prefilled leaf shells) so far."""
+        a, b, c = ct.c_int64(), ct.c_int64(), ct.c_int64()
+        _lib.call("vt_tree_dense_counts", self._h, ct.byref(a), ct.byref(b), ct.byref(c))
+        return int(a.value), int(b.value), int(c.value)
 
     def use_stream(self, stream) -> None:
         """Run this tree's device work on ``stream`` (a torch.cuda.Stream or

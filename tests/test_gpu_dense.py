@@ -105,9 +105,9 @@ def test_dense_equals_general(name, tmp_path):
     ops = list(ops) + [("sync",), ("borders",)]
     ta, ea, sa = _run(dims, C, brick, fmt, ops, dense=False)
     tb, eb, sb = _run(dims, C, brick, fmt, ops, dense=True)
-    leaf_inserts, _ = tb.dense_counts()
+    leaf_inserts = tb.dense_counts()[0]
     assert leaf_inserts == sum(1 for o in ops if o[0] == "slab")
-    assert ta.dense_counts() == (0, 0)
+    assert ta.dense_counts() == (0, 0, 0)
     assert eb == ea
     assert sb == sa
     assert _nodes(tb) == _nodes(ta)
@@ -157,7 +157,7 @@ def test_dense_background_and_device_source(tmp_path):
         t.sync()
         res.append((t.checksum(), _nodes(t), _bricks(t), digest(t, tmp_path, str(dense)),
                     t.dense_counts()))
-    assert res[1][4][0] == 5 and res[0][4] == (0, 0)
+    assert res[1][4][0] == 5 and res[0][4] == (0, 0, 0)
     assert res[1][:4] == res[0][:4]
 
 
@@ -188,3 +188,49 @@ def test_dense_matches_oracle_small():
         assert list(n.smax) == list(ot.smax[i])
         if n.brick is not None:
             assert np.array_equal(t.store.read_brick(n.brick), ot.bricks[n.index]), n.index
+
+
+PREFILL_CASES = {
+    # dims, C, brick, slab height (in bricks), bg
+    "cfg_like_slabs": ((64, 48, 40), 3, (8, 8, 8), 1, 0),
+    "two_layer_slabs_bg": ((48, 40, 72), 2, (8, 8, 8), 2, 17),
+    "bulk_partial": ((40, 36, 50), 3, (8, 8, 8), 100, 0),
+    "nonsplit_z": ((32, 16, 6), 3, (8, 8, 8), 1, 3),
+    "brick16_c4": ((64, 32, 48), 4, (16, 16, 16), 1, 0),
+}
+
+
+@pytest.mark.parametrize("name", sorted(PREFILL_CASES))
+def test_dense_prefilled_shells_fast_borders(name, tmp_path):
+    """Leaf shells written at insertion (TMA tile with halo) + fill_borders
+    patching only the owed z-shells: byte-identical to the general path."""
+    dims, C, brick, step, bg = PREFILL_CASES[name]
+    ops = _slabs(dims, brick[2], step=step) + [("borders",)]
+    ta, ea, _ = _run(dims, C, brick, "uint16", ops, dense=False, bg=bg)
+    tb, eb, _ = _run(dims, C, brick, "uint16", ops, dense=True, bg=bg)
+    assert tb.dense_counts()[2] == 1, "fill_borders did not take the prefilled-shell path"
+    assert eb == ea
+    assert _nodes(tb) == _nodes(ta)
+    assert _bricks(tb) == _bricks(ta)
+    assert digest(tb, tmp_path, "b") == digest(ta, tmp_path, "a")
+
+
+def test_prefilled_shells_read_as_background_before_fill_borders(tmp_path):
+    """Before fill_borders a prefilled shell is the reference's background to
+    every reader (read_brick, export, checksum, device mirror)."""
+    from paper_1407_2074_b200 import DeviceState
+    dims, C, brick = (32, 24, 40), 3, (8, 8, 8)
+    ops = _slabs(dims, brick[2])
+    ta, _, _ = _run(dims, C, brick, "uint16", ops, dense=False)
+    tb, _, _ = _run(dims, C, brick, "uint16", ops, dense=True)
+    assert _bricks(tb) == _bricks(ta)
+    assert tb.checksum() == ta.checksum()
+    assert digest(tb, tmp_path, "b") == digest(ta, tmp_path, "a")
+    tc, _, _ = _run(dims, C, brick, "uint16", ops, dense=True)
+    DeviceState(tc, resident_all=True)  # mirror first, then read
+    assert _bricks(tc) == _bricks(ta)
+    for t in (ta, tb, tc):
+        t.finalize()
+        t.fill_borders()
+    assert tb.dense_counts()[2] == 0 and tc.dense_counts()[2] == 0
+    assert _bricks(tb) == _bricks(ta) == _bricks(tc)
