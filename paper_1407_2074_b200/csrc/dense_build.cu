@@ -378,32 +378,15 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
       "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_addr(b))
       : "memory");
 }
-__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
-               "r"(smem_addr(src)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_commit() {
-  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-}
-template <int N>
-__device__ __forceinline__ void bulk_wait_read() {
-  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
-}
-template <int N>
-__device__ __forceinline__ void bulk_wait() {
-  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
-}
-
 // One CTA (8 warps) per leaf brick, stored planes in stages of P = 2.  The
 // TMA engine streams the block region a stage needs — one 3-D tensor tile of
-// (Mx+2)*C samples x (My+2) rows x P planes, i.e. the brick's planes WITH
-// their one-voxel x/y/z halo, zero-filled outside the block — into a 3-deep
-// shared-memory input ring; the warps write every stored voxel into a
-// shared-memory image of the stored planes, accumulating the interior's
-// per-plane statistics with compile-time channel indices, and one bulk copy
-// writes the stage's planes (contiguous in the brick) to HBM from a 3-deep
-// output ring.  Data in flight lives in shared memory, not registers.
+// the brick's P stored planes WITH their one-voxel x/y/z halo, zero-filled
+// outside the block — into a 3-deep shared-memory ring (data in flight lives
+// in shared memory, not registers).  Four warps per plane then write the
+// stored plane straight to HBM as coalesced 32-bit words (a stored row is
+// one contiguous run of block samples starting one voxel left of the brick:
+// a byte permute of two aligned shared words when that start is odd) and
+// reduce the interior's per-plane statistics.
 //
 // Shell voxels: with `prefill` they receive the value fill_borders will give
 // them at threshold 0 once every in-volume leaf is complete — the block
@@ -431,10 +414,11 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
     const __grid_constant__ CUtensorMap map, int oz, int dz, int prefill,
     const DenseJob* __restrict__ jobs, int gnx, int gny, int g0z, Geo g,
     uint16_t* __restrict__ pool, int32_t* pmin, int32_t* pmax, unsigned long long* psum,
-    int32_t* stats, const uint8_t* __restrict__ flags) {
+    int32_t* stats, const uint8_t* __restrict__ flags, uint32_t wmagic) {
   constexpr int P = kTmaP;
   constexpr int WPP = kTmaWarps / P;  // warps per plane
-  extern __shared__ __align__(128) unsigned char s_dyn[];
+  constexpr int NT = WPP * 32;        // threads per plane
+  extern __shared__ __align__(128) unsigned char s_in[];
   __shared__ uint64_t s_bar[kTmaStages];
   __shared__ int s_pmn[2][kTmaWarps][C], s_pmx[2][kTmaWarps][C];
   __shared__ unsigned long long s_psm[2][kTmaWarps][C];
@@ -448,19 +432,21 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
   const int Sx = g.stored[0], Sy = g.stored[1], Sz = g.stored[2];
   const int X = g.dims[0], Y = g.dims[1], Z = g.dims[2];
   const int cx = min(Mx, X - gx * Mx), cy = min(My, Y - gy * My), cz = min(Mz, Z - gz * Mz);
-  const int brow = tma_box_row(Mx, C);                       // staged row (samples)
-  const uint32_t in_bytes = tma_in_bytes(Mx, My, C);         // one input stage
-  const uint32_t plane_elems = (uint32_t)Sx * Sy * C;        // one stored plane
-  const uint32_t out_bytes = (uint32_t)P * plane_elems * 2;  // one output stage
-  unsigned char* s_in = s_dyn;
-  uint16_t* s_out = reinterpret_cast<uint16_t*>(s_dyn + (size_t)kTmaStages * in_bytes);
+  const int brow = tma_box_row(Mx, C);                  // staged row (samples)
+  const uint32_t in_bytes = tma_in_bytes(Mx, My, C);    // one input stage
+  const uint32_t plane_elems = (uint32_t)Sx * Sy * C;   // one stored plane
+  const int wpr = Sx * C / 2;                           // 32-bit words per stored row
+  const int nwords = Sy * wpr;
   const int nstages = Sz / P;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint16_t* brick = pool + (int64_t)j.slot * g.brick_elems;
   const uint16_t bg = (uint16_t)g.bg;
-  const int x0 = gx * Mx - 1, y0 = gy * My - 1;  // block voxel of stored (0, 0)
+  const uint32_t bgw = (uint32_t)bg | ((uint32_t)bg << 16);
+  const int x0 = gx * Mx - 1, y0 = gy * My - 1;     // block voxel of stored (0, 0)
   const int xa = x0 * C - (((x0 * C) % 8 + 8) % 8);  // 16-byte aligned tile start (samples)
-  const int xoff = x0 * C - xa;                     // leading samples in a staged row
+  const int xoff = x0 * C - xa;                     // leading samples of a staged row
+  const bool xfull = prefill && x0 >= 0 && x0 + Sx <= X;  // every stored x inside the volume
+  const uint32_t cxmagic = (uint32_t)((((uint64_t)1 << 32) + cx - 1) / cx);  // v / cx by mul-high
 
   if (tid == 0) {
     for (int b = 0; b < kTmaStages; ++b) mbar_init(&s_bar[b], 1);
@@ -481,21 +467,20 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
   if (tid == 0)
     for (int s = 0; s < min(kTmaStages, nstages); ++s) issue(s);
 
-  const int pw = warp / WPP;             // plane of the stage this warp group builds
+  const int pw = warp / WPP;                // plane of the stage this warp group builds
   const int pt = (warp % WPP) * 32 + lane;  // thread within the plane group
-  const uint32_t sxm = (uint32_t)((((uint64_t)1 << 32) + Sx - 1) / Sx);  // v / Sx by mul-high
   for (int s = 0; s < nstages; ++s) {
     const int b = s % kTmaStages;
     const int zs = P * s + pw;
     const int zi = zs - 1;
-    const int rz = gz * Mz + zi;  // block-volume z of this stored plane
+    const int rz = gz * Mz + zi;  // volume z of this stored plane
     // 1: interior data plane, 2: shell plane taken from the block, 0: background
     const int mode = (zi >= 0 && zi < cz) ? 1
                      : (prefill && zs < Sz && rz >= 0 && rz < Z && rz - oz >= 0 && rz - oz < dz) ? 2
                                                                                                : 0;
-    uint16_t* oplane = s_out + (size_t)b * (out_bytes / 2) + (size_t)pw * plane_elems;
     const uint16_t* iplane = reinterpret_cast<const uint16_t*>(s_in + (size_t)b * in_bytes) +
                              (size_t)pw * (My + 2) * brow;
+    uint32_t* oplane = reinterpret_cast<uint32_t*>(brick + (size_t)zs * plane_elems);
     int mn[C], mx[C];
     unsigned sm[C];
 #pragma unroll
@@ -506,21 +491,43 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
     }
     // every thread waits, so the slot's phase is complete before it is re-armed
     mbar_wait(&s_bar[b], (uint32_t)(s / kTmaStages) & 1u);
-    if (mode == 0) {
-      if (zs < Sz)
-        for (uint32_t i = pt; i < plane_elems; i += WPP * 32) oplane[i] = bg;
-    } else {
-      for (int v = pt; v < Sx * Sy; v += WPP * 32) {
-        const int ys = (int)__umulhi((uint32_t)v, sxm);
-        const int xs = v - ys * Sx;
-        const int rx = x0 + xs, ry = y0 + ys;
-        const bool interior = xs >= 1 && xs <= cx && ys >= 1 && ys <= cy;
-        const bool take = interior || (prefill && rx >= 0 && rx < X && ry >= 0 && ry < Y);
-        const uint16_t* iv = iplane + (size_t)ys * brow + xoff + xs * C;
-        uint16_t* ov = oplane + (size_t)v * C;
-#pragma unroll
-        for (int c = 0; c < C; ++c) ov[c] = take ? iv[c] : bg;
-        if (mode == 1 && interior) {
+    if (zs < Sz) {
+      if (mode == 0) {
+#pragma unroll 4
+        for (int w = pt; w < nwords; w += NT) oplane[w] = bgw;
+      } else if (xfull) {
+        // the common case: 32-bit words, stored sample e <-> staged sample
+        // xoff + e of the same row (rows outside the volume: background)
+        const uint32_t* iw = reinterpret_cast<const uint32_t*>(iplane) + (xoff >> 1);
+#pragma unroll 4
+        for (int w = pt; w < nwords; w += NT) {
+          const int ys = (int)__umulhi((uint32_t)w, wmagic);
+          const int wr = w - ys * wpr;
+          const int ry = y0 + ys;
+          const uint32_t* q = iw + ys * (brow >> 1) + wr;
+          uint32_t out = (xoff & 1) ? __byte_perm(q[0], q[1], 0x5432) : q[0];
+          oplane[w] = (ry >= 0 && ry < Y) ? out : bgw;
+        }
+      } else {
+        // bricks on the volume's x boundary, or shells not prefilled
+        uint16_t* o16 = reinterpret_cast<uint16_t*>(oplane);
+        for (int e = pt; e < (int)plane_elems; e += NT) {
+          const int ys = e / (Sx * C);
+          const int es = e - ys * Sx * C;
+          const int xs = es / C;
+          const int rx = x0 + xs, ry = y0 + ys;
+          const bool take = prefill ? (rx >= 0 && rx < X && ry >= 0 && ry < Y)
+                                    : (mode == 1 && xs >= 1 && xs <= cx && ys >= 1 && ys <= cy);
+          o16[e] = take ? iplane[(size_t)ys * brow + xoff + es] : bg;
+        }
+      }
+      if (mode == 1) {
+        // interior statistics: voxel v of the cx x cy interior plane
+#pragma unroll 2
+        for (int v = pt; v < cx * cy; v += NT) {
+          const int y = (int)__umulhi((uint32_t)v, cxmagic);
+          const int x = v - y * cx;
+          const uint16_t* iv = iplane + (size_t)(y + 1) * brow + xoff + (x + 1) * C;
 #pragma unroll
           for (int c = 0; c < C; ++c) {
             const int val = iv[c];
@@ -546,23 +553,8 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
         s_pmx[s & 1][warp][c] = mx[c];
         s_psm[s & 1][warp][c] = sm[c];
       }
-    __syncthreads();  // input slot consumed, output image complete, partials visible
-    if (warp == 0) {
-      if (lane == 0) {
-        // stage image -> HBM (the P stored planes are contiguous in the brick)
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        bulk_s2g(brick + (size_t)P * s * plane_elems, s_out + (size_t)b * (out_bytes / 2),
-                 out_bytes);
-        bulk_commit();
-        // the output slot of stage s+1 was last read by the store of stage
-        // s+1-kTmaStages: keep at most kTmaStages-2 stores pending
-        bulk_wait_read<kTmaStages - 2>();
-        if (s + kTmaStages < nstages) {
-          // every warp is past its wait on this slot (the barrier above)
-          issue(s + kTmaStages);
-        }
-      }
-    }
+    __syncthreads();  // input slot consumed, partials visible
+    if (tid == 0 && s + kTmaStages < nstages) issue(s + kTmaStages);
     if (tid < C) {
       const int c = tid;
 #pragma unroll
@@ -586,7 +578,6 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
       }
     }
   }
-  if (tid == 0) bulk_wait<0>();  // every store complete before the CTA exits
   if (tid < C) {
     const int c = tid;
     const long long n = (long long)cx * cy * cz;
@@ -765,8 +756,7 @@ int planes_per_warp(int sz) { return (sz + 11) / 12; }  // <= 12 warps per CTA
 // TMA tensor tiles need a 16-byte aligned block and row pitch, a box row of
 // at most 256 samples, and the rings must fit in shared memory
 static size_t tma_smem(const Geo& g) {
-  return (size_t)kTmaStages * (tma_in_bytes(g.brick[0], g.brick[1], g.C) +
-                               (size_t)kTmaP * g.stored[0] * g.stored[1] * g.C * 2);
+  return (size_t)kTmaStages * tma_in_bytes(g.brick[0], g.brick[1], g.C);
 }
 static bool tma_ok(const Tree& t, const void* src) {
   if (std::getenv("VT_DENSE_TMA") && std::getenv("VT_DENSE_TMA")[0] == '0') return false;
@@ -822,9 +812,12 @@ static bool leaf_launch(const Tree& t, const void* src, int64_t nsrc, int oz, in
     const size_t smem = tma_smem(t.g);
     auto k = k_dense_leaf_tma<C>;
     VT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    // y = w / words-per-row by multiply-high (exact for w < 2^32 / wpr)
+    const uint32_t wpr = (uint32_t)(t.g.stored[0] * C / 2);
+    auto magic = [](uint32_t d) { return (uint32_t)((((uint64_t)1 << 32) + d - 1) / d); };
     k<<<n, kTmaWarps * 32, smem, t.stream>>>(map, oz, (int)dz, prefill, jobs, gn[0], gn[1], g0z,
                                             t.g, (uint16_t*)t.d_pool, t.d_pmin, t.d_pmax,
-                                            t.d_psum, t.d_stats, t.d_flags);
+                                            t.d_psum, t.d_stats, t.d_flags, magic(wpr));
     VT_CHECK_LAUNCH();
     return prefill != 0;
   }
