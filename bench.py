@@ -233,6 +233,12 @@ def run_ours(args):
         torch.cuda.synchronize()
         return tree, e0.elapsed_time(e1), e1.elapsed_time(e2)
 
+    # untimed warm-up build (first launches load kernel modules, encode
+    # tensor maps, page-lock staging), then the timed build
+    wt, _, _ = build(vol)
+    wt.close()
+    del wt
+    torch.cuda.empty_cache()
     tree, build_ms, border_ms = build(vol)
     pool_bytes = tree.brick_count * cfg.brick_nbytes(desc)
     # every rank must hold the same tree after the sharded build
@@ -351,8 +357,10 @@ def run_ours(args):
         peak, peak_kind = hbm_peak()
         # only the samples the kernel actually reconstructs gather bricks
         achieved = computed_per_frame / max(world, 1) * BYTES_PER_POS_SAMPLE / (kernel_ms * 1e-3) / 1e9
-        build_gbs = raw_bytes / (build_ms * 1e-3) / 1e9
-        build_alg = (raw_bytes + pool_bytes) / (build_ms * 1e-3) / 1e9
+        # the build = insertion + fill_borders (ingest_bulk, ingest.py:182-224)
+        total_build_ms = build_ms + border_ms
+        build_gbs = raw_bytes / (total_build_ms * 1e-3) / 1e9
+        build_alg = (raw_bytes + pool_bytes) / (total_build_ms * 1e-3) / 1e9
         out = {
             "metric": "Gsamples/s (3-ch pos-samples, 1920x1080 frame); frame ms; octree build GB/s",
             "value": round(value, 4),
@@ -392,12 +400,13 @@ def run_ours(args):
                     "api": "OutOfCoreRenderer.render_fullframe -> float64 (H,W,4) host"
                     if world == 1 else "SortFirstRenderer.render_fullframe(to_host=True)"},
             "build": {"raw_gb": round(raw_bytes / 1e9, 3), "pool_gb": round(pool_bytes / 1e9, 3),
-                      "bricks": tree.brick_count, "insert_ms": round(build_ms, 2),
+                      "bricks": tree.brick_count, "build_ms": round(total_build_ms, 2),
+                      "insert_ms": round(build_ms, 2),
                       "fill_borders_ms": round(border_ms, 2),
                       "gbs_raw": round(build_gbs, 2),
                       "roofline": {"achieved": round(build_alg, 2), "peak": peak,
                                    "frac": round(build_alg / peak, 4), "unit": "GB/s",
-                                   "model": "(raw + pool bytes) / insert time"},
+                                   "model": "(raw + pool bytes) / (insert + fill_borders) time"},
                       "e2e_gbs_raw": round(raw_bytes / (build_e2e_ms * 1e-3) / 1e9, 2)
                       if build_e2e_ms else None,
                       "e2e_api": "Octree.insert_channels(pinned host slabs, 32 z each)",

@@ -398,7 +398,10 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
 // such shells logically background until fill_borders (Tree::halo_prefill).
 // Without `prefill` every shell voxel is the background (_ensure_brick,
 // octree.py:234-237).
-constexpr int kTmaStages = 3;
+// ring slots: the stage being built, the previous one (its second plane
+// pairs with this stage's first for the fused parent octant) and two in flight
+constexpr int kTmaStages = 4;
+constexpr int kTmaAhead = 3;  // stages in flight ahead of the one being built
 constexpr int kTmaWarps = 8;
 constexpr int kTmaP = 2;
 
@@ -465,7 +468,24 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
     tma_load_3d(s_in + (size_t)b * in_bytes, &map, xa, y0, gz * Mz - oz + P * s - 1, &s_bar[b]);
   };
   if (tid == 0)
-    for (int s = 0; s < min(kTmaStages, nstages); ++s) issue(s);
+    for (int s = 0; s < min(kTmaAhead, nstages); ++s) issue(s);
+
+  // fused parent octant (j.pad = parent slot, else -1): the 2x2x2 integer
+  // half-sample of this leaf (halfsample_block, octree.py:58-92) written into
+  // the parent's octant (_update_parent_octant, octree.py:308-319); the
+  // parent's per-plane statistics are folded in with atomics and reduced
+  // when the tree propagates (k_reduce)
+  const int pslot = j.pad;
+  const int hx = Mx / 2, hy = My / 2;
+  const int offx = (gx & 1) * hx, offy = (gy & 1) * hy, offz = (gz & 1) * (Mz / 2);
+  int pcx = 0, pcy = 0, pcz = 0;  // the parent's in-volume extent (octree.py:190-199)
+  {
+    const int plx = (gx >> 1) * 2 * Mx, ply = (gy >> 1) * 2 * My, plz = (gz >> 1) * 2 * Mz;
+    pcx = min(Mx, max(0, (X - plx + 1) / 2));
+    pcy = min(My, max(0, (Y - ply + 1) / 2));
+    pcz = min(Mz, max(0, (Z - plz + 1) / 2));
+  }
+  uint16_t* parent = pslot >= 0 ? pool + (int64_t)pslot * g.brick_elems : nullptr;
 
   const int pw = warp / WPP;                // plane of the stage this warp group builds
   const int pt = (warp % WPP) * 32 + lane;  // thread within the plane group
@@ -553,8 +573,93 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
         s_pmx[s & 1][warp][c] = mx[c];
         s_psm[s & 1][warp][c] = sm[c];
       }
-    __syncthreads();  // input slot consumed, partials visible
-    if (tid == 0 && s + kTmaStages < nstages) issue(s + kTmaStages);
+    // fused octant plane k = s - 1 from interior planes 2k (previous stage,
+    // second plane) and 2k + 1 (this stage, first plane)
+    if (parent && s >= 1 && 2 * (s - 1) < cz) {
+      const int k = s - 1;
+      const uint16_t* pa = reinterpret_cast<const uint16_t*>(
+                               s_in + (size_t)((s - 1) % kTmaStages) * in_bytes) +
+                           (size_t)(My + 2) * brow;  // previous stage, plane 1
+      const uint16_t* pb = reinterpret_cast<const uint16_t*>(s_in + (size_t)b * in_bytes);
+      int omn[C], omx[C];
+      unsigned osm[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        omn[c] = INT_MAX;
+        omx[c] = INT_MIN;
+        osm[c] = 0;
+      }
+      const bool zfull = 2 * k + 1 < cz;
+      for (int v = tid; v < hx * hy; v += kTmaWarps * 32) {
+        const int oy = v / hx, ox = v - oy * hx;
+        int val[C];
+        if (zfull && 2 * ox + 1 < cx && 2 * oy + 1 < cy) {
+          const int o00 = (1 + 2 * oy) * brow + xoff + (1 + 2 * ox) * C;
+#pragma unroll
+          for (int c = 0; c < C; ++c) {
+            const unsigned sum = (unsigned)pa[o00 + c] + pa[o00 + C + c] + pa[o00 + brow + c] +
+                                 pa[o00 + brow + C + c] + pb[o00 + c] + pb[o00 + C + c] +
+                                 pb[o00 + brow + c] + pb[o00 + brow + C + c];
+            val[c] = (int)((2 * sum + 8) / 16);
+          }
+        } else {
+          // partial leaf: mean over its in-volume voxels, background if none
+          unsigned sum[C];
+#pragma unroll
+          for (int c = 0; c < C; ++c) sum[c] = 0;
+          int cnt = 0;
+          for (int dz = 0; dz < 2; ++dz) {
+            if (2 * k + dz >= cz) continue;
+            const uint16_t* pl = dz ? pb : pa;
+            for (int dy = 0; dy < 2; ++dy) {
+              if (2 * oy + dy >= cy) continue;
+              for (int dx = 0; dx < 2; ++dx) {
+                if (2 * ox + dx >= cx) continue;
+                const int o = (1 + 2 * oy + dy) * brow + xoff + (1 + 2 * ox + dx) * C;
+#pragma unroll
+                for (int c = 0; c < C; ++c) sum[c] += pl[o + c];
+                ++cnt;
+              }
+            }
+          }
+#pragma unroll
+          for (int c = 0; c < C; ++c)
+            val[c] = cnt ? (int)((2 * (unsigned long long)sum[c] + cnt) / (2 * cnt)) : (int)bg;
+        }
+        uint16_t* dst = parent + g.voxel_offset(1 + offz + k, 1 + offy + oy, 1 + offx + ox);
+#pragma unroll
+        for (int c = 0; c < C; ++c) dst[c] = (uint16_t)val[c];
+        if (offx + ox < pcx && offy + oy < pcy && offz + k < pcz) {
+#pragma unroll
+          for (int c = 0; c < C; ++c) {
+            omn[c] = min(omn[c], val[c]);
+            omx[c] = max(omx[c], val[c]);
+            osm[c] += (unsigned)val[c];
+          }
+        }
+      }
+      if (offz + k < pcz) {
+#pragma unroll
+        for (int c = 0; c < C; ++c)
+          for (int o = 16; o > 0; o >>= 1) {
+            omn[c] = min(omn[c], __shfl_xor_sync(0xffffffffu, omn[c], o));
+            omx[c] = max(omx[c], __shfl_xor_sync(0xffffffffu, omx[c], o));
+            osm[c] += __shfl_xor_sync(0xffffffffu, osm[c], o);
+          }
+        if (lane == 0 && omx[0] != INT_MIN) {
+#pragma unroll
+          for (int c = 0; c < C; ++c) {
+            const int64_t off = ((int64_t)pslot * Mz + offz + k) * C + c;
+            atomicMin(pmin + off, omn[c]);
+            atomicMax(pmax + off, omx[c]);
+            atomicAdd(psum + off, (unsigned long long)osm[c]);
+          }
+        }
+      }
+    }
+    __syncthreads();  // input slots consumed, partials visible
+    // the previous stage's slot is free now: refill it kernel-ahead
+    if (tid == 0 && s + kTmaAhead < nstages) issue(s + kTmaAhead);
     if (tid < C) {
       const int c = tid;
 #pragma unroll
@@ -733,6 +838,16 @@ __global__ void k_plane_copy(const int32_t* __restrict__ jobs, int n, int64_t br
   for (int i = threadIdx.x; i < plane_words; i += blockDim.x) dst[i] = src[i];
 }
 
+__global__ void k_init_partials(const int32_t* __restrict__ slots, int n, int per, int32_t* pmin,
+                                int32_t* pmax, unsigned long long* psum) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)n * per) return;
+  const int64_t off = (int64_t)slots[i / per] * per + i % per;
+  pmin[off] = INT_MAX;
+  pmax[off] = INT_MIN;
+  psum[off] = 0;
+}
+
 // every shell voxel of a brick <- background (publishing prefilled shells as
 // the reference's pre-fill_borders state, Tree::publish_halos)
 template <class T>
@@ -799,9 +914,9 @@ static bool encode_block_map(const Tree& t, const void* src, int64_t dz, CUtenso
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// returns true when the shells were prefilled (TMA path)
+// returns kLeafPrefilled | kLeafTma as applicable
 template <class T, int C>
-static bool leaf_launch(const Tree& t, const void* src, int64_t nsrc, int oz, int prefill,
+static int leaf_launch(const Tree& t, const void* src, int64_t nsrc, int oz, int prefill,
                         const DenseJob* jobs, int n, const int gn[3], int g0z) {
   const int sz = t.g.stored[2];
   const int rowlen = t.g.stored[0] * C;
@@ -819,7 +934,7 @@ static bool leaf_launch(const Tree& t, const void* src, int64_t nsrc, int oz, in
                                             t.g, (uint16_t*)t.d_pool, t.d_pmin, t.d_pmax,
                                             t.d_psum, t.d_stats, t.d_flags, magic(wpr));
     VT_CHECK_LAUNCH();
-    return prefill != 0;
+    return kLeafTma | (prefill ? kLeafPrefilled : 0);
   }
   if (sizeof(T) == 2 && rowlen % 2 == 0 && wpl <= 4) {
     // warps own ceil(Sz / 17) planes each (<= 17 warps)
@@ -839,7 +954,7 @@ static bool leaf_launch(const Tree& t, const void* src, int64_t nsrc, int oz, in
     }
 #undef VT_LEAF16
     VT_CHECK_LAUNCH();
-    return false;
+    return 0;
   }
   const int ppw = planes_per_warp(sz);
   const int warps = (sz + ppw - 1) / ppw;
@@ -847,11 +962,11 @@ static bool leaf_launch(const Tree& t, const void* src, int64_t nsrc, int oz, in
       (const T*)src, oz, jobs, gn[0], gn[1], g0z, t.g, (T*)t.d_pool, t.d_pmin, t.d_pmax, t.d_psum,
       t.d_stats, t.d_flags, ppw);
   VT_CHECK_LAUNCH();
-  return false;
+  return 0;
 }
 
 template <class T>
-static bool leaf_dispatch(const Tree& t, const void* src, int64_t nsrc, int oz, int prefill,
+static int leaf_dispatch(const Tree& t, const void* src, int64_t nsrc, int oz, int prefill,
                           const DenseJob* jobs, int n, const int gn[3], int g0z) {
   switch (t.g.C) {
     case 1: return leaf_launch<T, 1>(t, src, nsrc, oz, prefill, jobs, n, gn, g0z);
@@ -869,6 +984,15 @@ void launch_plane_copy(const Tree& t, const int32_t* d_jobs, int n) {
   VT_CHECK_LAUNCH();
 }
 
+void launch_init_partials(const Tree& t, const int32_t* d_slots, int n) {
+  if (n <= 0) return;
+  const int per = t.g.brick[2] * t.g.C;
+  const int64_t work = (int64_t)n * per;
+  k_init_partials<<<(unsigned)((work + 255) / 256), 256, 0, t.stream>>>(d_slots, n, per, t.d_pmin,
+                                                                       t.d_pmax, t.d_psum);
+  VT_CHECK_LAUNCH();
+}
+
 void launch_clear_shells(const Tree& t, const int32_t* d_slots, int n) {
   if (n <= 0) return;
   if (t.g.sb == 1)
@@ -878,9 +1002,9 @@ void launch_clear_shells(const Tree& t, const int32_t* d_slots, int n) {
   VT_CHECK_LAUNCH();
 }
 
-bool launch_dense_leaf(const Tree& t, const void* src, int64_t nsrc, int oz, int prefill,
-                       const DenseJob* jobs, int n, const int gn[3], int g0z) {
-  if (n <= 0) return prefill != 0;
+int launch_dense_leaf(const Tree& t, const void* src, int64_t nsrc, int oz, int prefill,
+                      const DenseJob* jobs, int n, const int gn[3], int g0z) {
+  if (n <= 0) return 0;
   if (t.g.sb == 1) return leaf_dispatch<uint8_t>(t, src, nsrc, oz, 0, jobs, n, gn, g0z);
   return leaf_dispatch<uint16_t>(t, src, nsrc, oz, prefill, jobs, n, gn, g0z);
 }

@@ -100,11 +100,12 @@ Tree::Tree(const vt_tree_desc& d) {
   slot.assign(cap, -1);
   struct_mark.assign(cap, 0);
   complete.assign(cap, 0);
+  fused1.assign(cap, 0);
   seed_of.assign(cap, -1);
   anc_mark.assign(cap, 0);
   {
     // staging ring up front: its first allocation syncs the stream
-    size_t sc = (size_t)8 << 20;
+    size_t sc = (size_t)32 << 20;
     stage.h = pinned_get(sc);
     VT_CUDA(cudaMalloc(&stage.d, sc));
     stage.cap = sc;
@@ -519,7 +520,7 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
 
   // leaves (octree.py:351-360): descend, create, ensure brick, dirty box
   auto* leaf_scope = new ProfScope(prof, 8);
-  for (int gz = g0[2]; gz <= g1[2]; ++gz)
+  for (int gz = g0[2]; gz <= g1[2]; ++gz) {
     for (int gy = g0[1]; gy <= g1[1]; ++gy)
       for (int gx = g0[0]; gx <= g1[0]; ++gx) {
         int gg[3] = {gx, gy, gz};
@@ -540,17 +541,9 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
         for (int a = 0; a < 3; ++a) ce[a] = std::max(0, std::min(M[a], g.dims[a] - gg[a] * M[a]));
         bool fresh = ensure_brick(idx, ce, !dense);
         if (dense) {
-          // the dense kernel writes the whole stored brick and its final
-          // statistics: no seed, no owed planes, no reduce
-          djobs.push_back({idx, slot[idx], 0});
-          Pending& p = pend(0, idx);
-          p.box = Box{{0, 0, 0}, {M[0], M[1], M[2]}};
-          p.has_box = true;
-          p.fresh = true;
-          p.masked = true;
-          p.need[0] = p.need[1] = 0;
-          p.dense = true;
-          complete[idx] = 1;
+          // structure only here; the dense kernel writes the whole stored
+          // brick and its final statistics (pending entries after launch)
+          djobs.push_back({idx, slot[idx], -1});
           touched[0].push_back(idx);
           continue;
         }
@@ -575,6 +568,7 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
         box_union(p, b);
         p.fresh |= fresh;
         p.dense = false;
+        fused1[(idx - 1) >> 3] = 0;  // a fused parent octant would be stale
         if (g.brick[2] <= 128) {
           if (!p.masked) {
             // first touch since the last propagation: nothing owed yet
@@ -589,6 +583,7 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
         }
         touched[0].push_back(idx);
       }
+  }
   delete leaf_scope;
   auto* anc_scope = new ProfScope(prof, 9);
   // ancestors (octree.py:363-387): ensure parent bricks, record freshness
@@ -616,6 +611,34 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
       pend(lvl, p).fresh |= fresh;
     }
   }
+  // dense: level-1 parents whose every octant is a leaf of this block get
+  // their octants from the leaf kernel (fused half-sample)
+  std::vector<int32_t> fused_slots;
+  std::vector<int64_t> fused_nodes;
+  if (dense && g.depth >= 1 && g.split[0] && g.split[1] && g.split[2]) {
+    for (int64_t p : touched[1]) {
+      bool ok = true;
+      int64_t pos[8];
+      int plo[3];
+      g.box_lo(p, plo);
+      for (int k = 0; k < 8 && ok; ++k) {
+        const int64_t c = 8 * p + 1 + k;
+        if (!(flags[c] & NF_INVOL) || !(flags[c] & NF_BRICK)) {
+          ok = false;
+          break;
+        }
+        int gg[3];
+        for (int a = 0; a < 3; ++a) gg[a] = plo[a] / M[a] + ((k >> a) & 1);
+        if (gg[2] < g0[2] || gg[2] > g1[2]) ok = false;
+        pos[k] = ((int64_t)(gg[2] - g0[2]) * gn[1] + gg[1]) * gn[0] + gg[0];
+      }
+      if (!ok) continue;
+      for (int k = 0; k < 8; ++k) djobs[pos[k]].pad = slot[p];
+      fused1[p] = 1;
+      fused_slots.push_back(slot[p]);
+      fused_nodes.push_back(p);
+    }
+  }
   sort_indices(touched[0]);
   has_pending = true;
   delete anc_scope;
@@ -636,13 +659,31 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
   int32_t* dl = nullptr;
   if (dense) {
     ProfScope q(prof, 7);
+    int32_t* dfs = upload(*this, fused_slots);
+    launch_init_partials(*this, dfs, (int)fused_slots.size());
+    release(*this, dfs);
     DenseJob* dj = upload(*this, djobs);
     const bool want = prefill_enabled && !borders;
-    const bool pre = launch_dense_leaf(*this, dsrc, nvox * src_stride, origin[2], want ? 1 : 0, dj,
-                                       (int)djobs.size(), gn, g0[2]);
+    const int lr = launch_dense_leaf(*this, dsrc, nvox * src_stride, origin[2], want ? 1 : 0, dj,
+                                     (int)djobs.size(), gn, g0[2]);
     release(*this, dj);
+    const bool prefilled = lr & kLeafPrefilled;
+    if (!(lr & kLeafTma))
+      for (int64_t p : fused_nodes) fused1[p] = 0;  // the fallback kernels do not fuse
+    // host bookkeeping overlaps the device work: pending entries of leaves
+    // whose statistics the kernel writes outright
+    for (const DenseJob& jd : djobs) {
+      Pending& p = pend(0, jd.node);
+      p.box = Box{{0, 0, 0}, {M[0], M[1], M[2]}};
+      p.has_box = true;
+      p.fresh = true;
+      p.masked = true;
+      p.need[0] = p.need[1] = 0;
+      p.dense = true;
+      complete[jd.node] = 1;
+    }
     ++dense_leaf_inserts;
-    if (pre) {
+    if (prefilled) {
       // z-shell planes whose block plane lies outside this insertion are owed
       halo_prefill = true;
       const int z0 = origin[2], z1 = origin[2] + dims[2];
@@ -716,7 +757,7 @@ void Tree::propagate() {
   for (int lvl = 0; lvl <= g.depth; ++lvl) {
     std::vector<int64_t>& nodes = pend_nodes[lvl];
     if (nodes.empty()) continue;
-    std::sort(nodes.begin(), nodes.end());
+    sort_indices(nodes);
     std::vector<OctJob> oct;
     std::vector<int64_t> dense_nodes;
     if (lvl > 0) {
@@ -725,6 +766,17 @@ void Tree::propagate() {
       size_t ci = 0;
       for (int64_t p : nodes) {
         Pending& pp = *pend_find(p, lvl);
+        if (lvl == 1 && fused1[p] && dense_parent(p)) {
+          // octants written by the leaf kernel, plane partials complete:
+          // only the reduce is owed
+          fused1[p] = 0;
+          pp.box = Box{{0, 0, 0}, {M[0], M[1], M[2]}};
+          pp.has_box = true;
+          pp.fused = true;
+          complete[p] = 1;
+          continue;
+        }
+        fused1[p] = 0;
         if (dense_parent(p)) {
           // every in-volume child complete: recompute the whole interior and
           // the statistics in one dense pass (dense_build.cu)
@@ -800,7 +852,7 @@ void Tree::propagate() {
       r.slot = slot[n];
       node_in_extent(n, r.cext);
       r.leafish = (lvl == 0 || !(flags[n] & NF_CHILDREN)) ? 1 : 0;
-      if (p.has_box && r.cext[0] > 0 && r.cext[1] > 0) {
+      if (p.has_box && r.cext[0] > 0 && r.cext[1] > 0 && !p.fused) {
         if (lvl == 0 && p.masked) {
           // runs of planes whose stats the scatter did not compute
           if (p.need[0] | p.need[1]) {

@@ -25,6 +25,8 @@ struct Pending {
   // statistics already final (written by a dense-build kernel): no plane /
   // reduce work owed.  Any later general-path touch clears it.
   bool dense = false;
+  // level-1 octants and plane partials written by the leaf kernel (fused)
+  bool fused = false;
   // leaves: planes whose partial stats are still owed (bit z); planes whose
   // stats the scatter computed in-kernel are cleared (requires Mz <= 128)
   bool masked = false;
@@ -95,6 +97,7 @@ struct Tree {
   // function of the data; VT_DENSE=0 disables the path (A/B testing)
   bool dense_enabled = true;
   std::vector<uint8_t> complete;
+  std::vector<uint8_t> fused1;  // level-1 parent whose octants the leaf kernel wrote
   std::vector<int64_t> morton[3];
   // shells of dense leaves written with their fill_borders values at
   // insertion (dense_build.cu).  While !borders they are logically the
@@ -229,8 +232,13 @@ bool scatter_owns_stats(const Geo& g, int channel, const int origin[3], const in
                         int gy);
 void launch_octant(const Tree& t, const OctJob* d_jobs, int n);
 // dense_build.cu
-bool launch_dense_leaf(const Tree& t, const void* src, int64_t nsrc, int oz, int prefill,
-                       const DenseJob* jobs, int n, const int gn[3], int g0z);
+// returns kLeafPrefilled (shells prefilled) | kLeafTma (TMA kernel: fused
+// parent octants of jobs with pad >= 0 written too)
+constexpr int kLeafPrefilled = 1, kLeafTma = 2;
+int launch_dense_leaf(const Tree& t, const void* src, int64_t nsrc, int oz, int prefill,
+                      const DenseJob* jobs, int n, const int gn[3], int g0z);
+// plane partials of the given bricks <- (INT_MAX, INT_MIN, 0) (fused parents)
+void launch_init_partials(const Tree& t, const int32_t* d_slots, int n);
 // z-shell plane copies between leaf bricks: dst plane <- src plane
 void launch_plane_copy(const Tree& t, const int32_t* d_jobs, int n);
 // every shell voxel of the given bricks <- background
