@@ -416,17 +416,14 @@ template <int C>
 __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
     const __grid_constant__ CUtensorMap map, int oz, int dz, int prefill,
     const DenseJob* __restrict__ jobs, int gnx, int gny, int g0z, Geo g,
-    uint16_t* __restrict__ pool, int32_t* pmin, int32_t* pmax, unsigned long long* psum,
-    int32_t* stats, const uint8_t* __restrict__ flags, uint32_t wmagic) {
+    uint16_t* __restrict__ pool, int32_t* stats, unsigned long long* nsum) {
   constexpr int P = kTmaP;
   constexpr int WPP = kTmaWarps / P;  // warps per plane
   constexpr int NT = WPP * 32;        // threads per plane
   extern __shared__ __align__(128) unsigned char s_in[];
   __shared__ uint64_t s_bar[kTmaStages];
-  __shared__ int s_pmn[2][kTmaWarps][C], s_pmx[2][kTmaWarps][C];
-  __shared__ unsigned long long s_psm[2][kTmaWarps][C];
-  __shared__ int s_tmn[C], s_tmx[C];
-  __shared__ unsigned long long s_tsm[C];
+  __shared__ int s_mn[2][kTmaWarps][C], s_mx[2][kTmaWarps][C];
+  __shared__ unsigned long long s_sm[2][kTmaWarps][C];
   const DenseJob j = jobs[blockIdx.x];
   const int gx = (int)(blockIdx.x % gnx);
   const int gy = (int)((blockIdx.x / gnx) % gny);
@@ -439,7 +436,6 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
   const uint32_t in_bytes = tma_in_bytes(Mx, My, C);    // one input stage
   const uint32_t plane_elems = (uint32_t)Sx * Sy * C;   // one stored plane
   const int wpr = Sx * C / 2;                           // 32-bit words per stored row
-  const int nwords = Sy * wpr;
   const int nstages = Sz / P;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint16_t* brick = pool + (int64_t)j.slot * g.brick_elems;
@@ -455,11 +451,6 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
     for (int b = 0; b < kTmaStages; ++b) mbar_init(&s_bar[b], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (tid < C) {
-    s_tmn[tid] = INT_MAX;
-    s_tmx[tid] = INT_MIN;
-    s_tsm[tid] = 0;
-  }
   __syncthreads();
 
   auto issue = [&](int s) {  // one thread: one tensor tile per stage
@@ -472,13 +463,14 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
 
   // fused parent octant (j.pad = parent slot, else -1): the 2x2x2 integer
   // half-sample of this leaf (halfsample_block, octree.py:58-92) written into
-  // the parent's octant (_update_parent_octant, octree.py:308-319); the
-  // parent's per-plane statistics are folded in with atomics and reduced
-  // when the tree propagates (k_reduce)
+  // the parent's octant (_update_parent_octant, octree.py:308-319).  That
+  // pass visits every interior voxel exactly once, so it also carries the
+  // leaf's statistics; the parent's are folded into its accumulators
+  // (stats min/max, nsum) with one atomic per channel per CTA.
   const int pslot = j.pad;
   const int hx = Mx / 2, hy = My / 2;
   const int offx = (gx & 1) * hx, offy = (gy & 1) * hy, offz = (gz & 1) * (Mz / 2);
-  int pcx = 0, pcy = 0, pcz = 0;  // the parent's in-volume extent (octree.py:190-199)
+  int pcx, pcy, pcz;  // the parent's in-volume extent (octree.py:190-199)
   {
     const int plx = (gx >> 1) * 2 * Mx, ply = (gy >> 1) * 2 * My, plz = (gz >> 1) * 2 * Mz;
     pcx = min(Mx, max(0, (X - plx + 1) / 2));
@@ -487,8 +479,26 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
   }
   uint16_t* parent = pslot >= 0 ? pool + (int64_t)pslot * g.brick_elems : nullptr;
 
+  // per-thread totals over the whole brick: the leaf (l*) and the octant (o*)
+  int lmn[C], lmx[C], omn[C], omx[C];
+  unsigned long long lsm[C], osm[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    lmn[c] = omn[c] = INT_MAX;
+    lmx[c] = omx[c] = INT_MIN;
+    lsm[c] = osm[c] = 0;
+  }
+
+  // word mapping: thread pt of a plane group owns word wr of rows rr, rr+R, ..
   const int pw = warp / WPP;                // plane of the stage this warp group builds
   const int pt = (warp % WPP) * 32 + lane;  // thread within the plane group
+  const int R = wpr <= NT ? NT / wpr : 1;   // rows per pass of the group
+  const int rr = wpr <= NT ? pt / wpr : 0;
+  const int wr0 = wpr <= NT ? pt % wpr : pt;
+  const int wstep = wpr <= NT ? wpr : NT;
+  const bool wact = rr < R;
+  const int xo = (xoff >> 1) + wr0;  // staged word of this thread's first word
+
   for (int s = 0; s < nstages; ++s) {
     const int b = s % kTmaStages;
     const int zs = P * s + pw;
@@ -501,33 +511,28 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
     const uint16_t* iplane = reinterpret_cast<const uint16_t*>(s_in + (size_t)b * in_bytes) +
                              (size_t)pw * (My + 2) * brow;
     uint32_t* oplane = reinterpret_cast<uint32_t*>(brick + (size_t)zs * plane_elems);
-    int mn[C], mx[C];
-    unsigned sm[C];
-#pragma unroll
-    for (int c = 0; c < C; ++c) {
-      mn[c] = INT_MAX;
-      mx[c] = INT_MIN;
-      sm[c] = 0;
-    }
     // every thread waits, so the slot's phase is complete before it is re-armed
     mbar_wait(&s_bar[b], (uint32_t)(s / kTmaStages) & 1u);
     if (zs < Sz) {
-      if (mode == 0) {
-#pragma unroll 4
-        for (int w = pt; w < nwords; w += NT) oplane[w] = bgw;
-      } else if (xfull) {
-        // the common case: 32-bit words, stored sample e <-> staged sample
-        // xoff + e of the same row (rows outside the volume: background)
-        const uint32_t* iw = reinterpret_cast<const uint32_t*>(iplane) + (xoff >> 1);
-#pragma unroll 4
-        for (int w = pt; w < nwords; w += NT) {
-          const int ys = (int)__umulhi((uint32_t)w, wmagic);
-          const int wr = w - ys * wpr;
-          const int ry = y0 + ys;
-          const uint32_t* q = iw + ys * (brow >> 1) + wr;
-          uint32_t out = (xoff & 1) ? __byte_perm(q[0], q[1], 0x5432) : q[0];
-          oplane[w] = (ry >= 0 && ry < Y) ? out : bgw;
+      if (mode != 0 && xfull) {
+        // the common case: stored sample e of a row <-> staged sample xoff+e
+        // of the same row (rows outside the volume: background)
+        if (wact) {
+          const uint32_t* iw = reinterpret_cast<const uint32_t*>(iplane) + xo;
+          for (int ys = rr; ys < Sy; ys += R) {
+            const bool rin = (unsigned)(y0 + ys) < (unsigned)Y;
+            const uint32_t* q = iw + ys * (brow >> 1);
+            uint32_t* o = oplane + ys * wpr + wr0;
+            for (int w = 0; w < wpr - wr0; w += wstep) {
+              const uint32_t out = (xoff & 1) ? __byte_perm(q[w], q[w + 1], 0x5432) : q[w];
+              o[w] = rin ? out : bgw;
+            }
+          }
         }
+      } else if (mode == 0) {
+        if (wact)
+          for (int ys = rr; ys < Sy; ys += R)
+            for (int w = wr0; w < wpr; w += wstep) oplane[ys * wpr + w] = bgw;
       } else {
         // bricks on the volume's x boundary, or shells not prefilled
         uint16_t* o16 = reinterpret_cast<uint16_t*>(oplane);
@@ -541,9 +546,8 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
           o16[e] = take ? iplane[(size_t)ys * brow + xoff + es] : bg;
         }
       }
-      if (mode == 1) {
-        // interior statistics: voxel v of the cx x cy interior plane
-#pragma unroll 2
+      if (mode == 1 && !parent) {
+        // interior statistics of an unfused leaf: voxel v of the interior plane
         for (int v = pt; v < cx * cy; v += NT) {
           const int y = (int)__umulhi((uint32_t)v, cxmagic);
           const int x = v - y * cx;
@@ -551,28 +555,13 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
 #pragma unroll
           for (int c = 0; c < C; ++c) {
             const int val = iv[c];
-            mn[c] = min(mn[c], val);
-            mx[c] = max(mx[c], val);
-            sm[c] += (unsigned)val;
+            lmn[c] = min(lmn[c], val);
+            lmx[c] = max(lmx[c], val);
+            lsm[c] += (unsigned)val;
           }
         }
       }
     }
-    // per-warp partials of its plane -> shared (double buffered by stage parity)
-#pragma unroll
-    for (int c = 0; c < C; ++c)
-      for (int o = 16; o > 0; o >>= 1) {
-        mn[c] = min(mn[c], __shfl_xor_sync(0xffffffffu, mn[c], o));
-        mx[c] = max(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], o));
-        sm[c] += __shfl_xor_sync(0xffffffffu, sm[c], o);
-      }
-    if (lane == 0)
-#pragma unroll
-      for (int c = 0; c < C; ++c) {
-        s_pmn[s & 1][warp][c] = mn[c];
-        s_pmx[s & 1][warp][c] = mx[c];
-        s_psm[s & 1][warp][c] = sm[c];
-      }
     // fused octant plane k = s - 1 from interior planes 2k (previous stage,
     // second plane) and 2k + 1 (this stage, first plane)
     if (parent && s >= 1 && 2 * (s - 1) < cz) {
@@ -581,15 +570,8 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
                                s_in + (size_t)((s - 1) % kTmaStages) * in_bytes) +
                            (size_t)(My + 2) * brow;  // previous stage, plane 1
       const uint16_t* pb = reinterpret_cast<const uint16_t*>(s_in + (size_t)b * in_bytes);
-      int omn[C], omx[C];
-      unsigned osm[C];
-#pragma unroll
-      for (int c = 0; c < C; ++c) {
-        omn[c] = INT_MAX;
-        omx[c] = INT_MIN;
-        osm[c] = 0;
-      }
       const bool zfull = 2 * k + 1 < cz;
+      const bool pin = offz + k < pcz;
       for (int v = tid; v < hx * hy; v += kTmaWarps * 32) {
         const int oy = v / hx, ox = v - oy * hx;
         int val[C];
@@ -597,10 +579,14 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
           const int o00 = (1 + 2 * oy) * brow + xoff + (1 + 2 * ox) * C;
 #pragma unroll
           for (int c = 0; c < C; ++c) {
-            const unsigned sum = (unsigned)pa[o00 + c] + pa[o00 + C + c] + pa[o00 + brow + c] +
-                                 pa[o00 + brow + C + c] + pb[o00 + c] + pb[o00 + C + c] +
-                                 pb[o00 + brow + c] + pb[o00 + brow + C + c];
+            const int a0 = pa[o00 + c], a1 = pa[o00 + C + c], a2 = pa[o00 + brow + c],
+                      a3 = pa[o00 + brow + C + c], b0 = pb[o00 + c], b1 = pb[o00 + C + c],
+                      b2 = pb[o00 + brow + c], b3 = pb[o00 + brow + C + c];
+            const unsigned sum = (unsigned)(a0 + a1 + a2 + a3 + b0 + b1 + b2 + b3);
             val[c] = (int)((2 * sum + 8) / 16);
+            lmn[c] = min(lmn[c], min(min(min(a0, a1), min(a2, a3)), min(min(b0, b1), min(b2, b3))));
+            lmx[c] = max(lmx[c], max(max(max(a0, a1), max(a2, a3)), max(max(b0, b1), max(b2, b3))));
+            lsm[c] += sum;
           }
         } else {
           // partial leaf: mean over its in-volume voxels, background if none
@@ -617,19 +603,26 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
                 if (2 * ox + dx >= cx) continue;
                 const int o = (1 + 2 * oy + dy) * brow + xoff + (1 + 2 * ox + dx) * C;
 #pragma unroll
-                for (int c = 0; c < C; ++c) sum[c] += pl[o + c];
+                for (int c = 0; c < C; ++c) {
+                  const int x = pl[o + c];
+                  sum[c] += x;
+                  lmn[c] = min(lmn[c], x);
+                  lmx[c] = max(lmx[c], x);
+                }
                 ++cnt;
               }
             }
           }
 #pragma unroll
-          for (int c = 0; c < C; ++c)
+          for (int c = 0; c < C; ++c) {
+            lsm[c] += sum[c];
             val[c] = cnt ? (int)((2 * (unsigned long long)sum[c] + cnt) / (2 * cnt)) : (int)bg;
+          }
         }
         uint16_t* dst = parent + g.voxel_offset(1 + offz + k, 1 + offy + oy, 1 + offx + ox);
 #pragma unroll
         for (int c = 0; c < C; ++c) dst[c] = (uint16_t)val[c];
-        if (offx + ox < pcx && offy + oy < pcy && offz + k < pcz) {
+        if (pin && offx + ox < pcx && offy + oy < pcy) {
 #pragma unroll
           for (int c = 0; c < C; ++c) {
             omn[c] = min(omn[c], val[c]);
@@ -638,60 +631,58 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
           }
         }
       }
-      if (offz + k < pcz) {
-#pragma unroll
-        for (int c = 0; c < C; ++c)
-          for (int o = 16; o > 0; o >>= 1) {
-            omn[c] = min(omn[c], __shfl_xor_sync(0xffffffffu, omn[c], o));
-            omx[c] = max(omx[c], __shfl_xor_sync(0xffffffffu, omx[c], o));
-            osm[c] += __shfl_xor_sync(0xffffffffu, osm[c], o);
-          }
-        if (lane == 0 && omx[0] != INT_MIN) {
-#pragma unroll
-          for (int c = 0; c < C; ++c) {
-            const int64_t off = ((int64_t)pslot * Mz + offz + k) * C + c;
-            atomicMin(pmin + off, omn[c]);
-            atomicMax(pmax + off, omx[c]);
-            atomicAdd(psum + off, (unsigned long long)osm[c]);
-          }
-        }
-      }
     }
-    __syncthreads();  // input slots consumed, partials visible
-    // the previous stage's slot is free now: refill it kernel-ahead
+    __syncthreads();  // input slots consumed
+    // the previous stage's slot is free now: refill it kTmaAhead stages ahead
     if (tid == 0 && s + kTmaAhead < nstages) issue(s + kTmaAhead);
-    if (tid < C) {
-      const int c = tid;
-#pragma unroll
-      for (int p = 0; p < P; ++p) {
-        const int zi2 = P * s + p - 1;
-        if (zi2 < 0 || zi2 >= cz) continue;
-        int a = INT_MAX, bmx = INT_MIN;
-        unsigned long long t = 0;
-        for (int w = p * WPP; w < (p + 1) * WPP; ++w) {
-          a = min(a, s_pmn[s & 1][w][c]);
-          bmx = max(bmx, s_pmx[s & 1][w][c]);
-          t += s_psm[s & 1][w][c];
-        }
-        const int64_t off = ((int64_t)j.slot * Mz + zi2) * C + c;
-        pmin[off] = a;
-        pmax[off] = bmx;
-        psum[off] = t;
-        s_tmn[c] = min(s_tmn[c], a);
-        s_tmx[c] = max(s_tmx[c], bmx);
-        s_tsm[c] += t;
-      }
-    }
   }
+
+  // CTA totals: warp shuffles, then one thread per channel
+#pragma unroll
+  for (int c = 0; c < C; ++c)
+    for (int o = 16; o > 0; o >>= 1) {
+      lmn[c] = min(lmn[c], __shfl_xor_sync(0xffffffffu, lmn[c], o));
+      lmx[c] = max(lmx[c], __shfl_xor_sync(0xffffffffu, lmx[c], o));
+      lsm[c] += __shfl_xor_sync(0xffffffffu, lsm[c], o);
+      omn[c] = min(omn[c], __shfl_xor_sync(0xffffffffu, omn[c], o));
+      omx[c] = max(omx[c], __shfl_xor_sync(0xffffffffu, omx[c], o));
+      osm[c] += __shfl_xor_sync(0xffffffffu, osm[c], o);
+    }
+  if (lane == 0)
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      s_mn[0][warp][c] = lmn[c];
+      s_mx[0][warp][c] = lmx[c];
+      s_sm[0][warp][c] = lsm[c];
+      s_mn[1][warp][c] = omn[c];
+      s_mx[1][warp][c] = omx[c];
+      s_sm[1][warp][c] = osm[c];
+    }
+  __syncthreads();
   if (tid < C) {
     const int c = tid;
+    int a = INT_MAX, bmx = INT_MIN, pa = INT_MAX, pb = INT_MIN;
+    unsigned long long t = 0, pt2 = 0;
+    for (int w = 0; w < kTmaWarps; ++w) {
+      a = min(a, s_mn[0][w][c]);
+      bmx = max(bmx, s_mx[0][w][c]);
+      t += s_sm[0][w][c];
+      pa = min(pa, s_mn[1][w][c]);
+      pb = max(pb, s_mx[1][w][c]);
+      pt2 += s_sm[1][w][c];
+    }
     const long long n = (long long)cx * cy * cz;
-    const long long avg = (2 * (long long)s_tsm[c] + n) / (2 * n);
-    stats[st_index(j.node, ST_AVG, c)] = (int)avg;
-    stats[st_index(j.node, ST_MIN, c)] = s_tmn[c];
-    stats[st_index(j.node, ST_MAX, c)] = s_tmx[c];
-    stats[st_index(j.node, ST_SUBMIN, c)] = s_tmn[c];
-    stats[st_index(j.node, ST_SUBMAX, c)] = s_tmx[c];
+    stats[st_index(j.node, ST_AVG, c)] = (int)((2 * (long long)t + n) / (2 * n));
+    stats[st_index(j.node, ST_MIN, c)] = a;
+    stats[st_index(j.node, ST_MAX, c)] = bmx;
+    stats[st_index(j.node, ST_SUBMIN, c)] = a;
+    stats[st_index(j.node, ST_SUBMAX, c)] = bmx;
+    if (parent && pb != INT_MIN) {
+      const int64_t pnode = (j.node - 1) >> 3;
+      atomicMin(stats + st_index(pnode, ST_MIN, c), pa);
+      atomicMax(stats + st_index(pnode, ST_MAX, c), pb);
+      atomicAdd(nsum + pnode * C + c, pt2);
+    }
   }
 }
 
@@ -708,8 +699,12 @@ __global__ void __launch_bounds__(256) k_dense_level(const int64_t* __restrict__
                                                      T* pool, const int32_t* __restrict__ slots,
                                                      const uint8_t* __restrict__ flags,
                                                      int32_t* pmin, int32_t* pmax,
-                                                     unsigned long long* psum, int32_t* stats) {
-  const int64_t node = nodes[blockIdx.x];
+                                                     unsigned long long* psum, int32_t* stats,
+                                                     int zsplit) {
+  // zsplit > 1 (small levels): CTA part p of a node builds interior planes
+  // [p*Mz/zsplit, (p+1)*Mz/zsplit); the statistics come from a k_reduce pass
+  const int64_t node = nodes[blockIdx.x / zsplit];
+  const int part = blockIdx.x % zsplit;
   const int level = g.level_of(node);
   const int Mx = g.brick[0], My = g.brick[1], Mz = g.brick[2];
   __shared__ int s_cslot[8];
@@ -801,7 +796,8 @@ __global__ void __launch_bounds__(256) k_dense_level(const int64_t* __restrict__
     for (int c = 0; c < C; ++c) v[c] = cnt ? (int)((2 * sum[c] + cnt) / (2 * cnt)) : g.bg;
     return r;
   };
-  for (int z = warp; z < Mz; z += nw) {
+  const int zb0 = part * Mz / zsplit, zb1 = (part + 1) * Mz / zsplit;
+  for (int z = zb0 + warp; z < zb1; z += nw) {
     Acc<C> pl;
     pl.init();
     for (int y = 0; y < My; y += 2) {
@@ -838,14 +834,47 @@ __global__ void k_plane_copy(const int32_t* __restrict__ jobs, int n, int64_t br
   for (int i = threadIdx.x; i < plane_words; i += blockDim.x) dst[i] = src[i];
 }
 
-__global__ void k_init_partials(const int32_t* __restrict__ slots, int n, int per, int32_t* pmin,
-                                int32_t* pmax, unsigned long long* psum) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= (int64_t)n * per) return;
-  const int64_t off = (int64_t)slots[i / per] * per + i % per;
-  pmin[off] = INT_MAX;
-  pmax[off] = INT_MIN;
-  psum[off] = 0;
+// fused level-1 parents: min/max accumulators in stats, sums in nsum
+__global__ void k_init_fused(const int64_t* __restrict__ nodes, int n, int C, int32_t* stats,
+                             unsigned long long* nsum) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n * C) return;
+  const int64_t node = nodes[i / C];
+  const int c = i % C;
+  stats[st_index(node, ST_MIN, c)] = INT_MAX;
+  stats[st_index(node, ST_MAX, c)] = INT_MIN;
+  nsum[node * C + c] = 0;
+}
+
+// fused level-1 parents after their leaves: AVG = round_mean(sum, n)
+// (octree.py:53-55) and the subtree extrema (octree.py:265-277)
+__global__ void k_finish_fused(const int64_t* __restrict__ nodes, int n, Geo g,
+                               const uint8_t* __restrict__ flags, int32_t* stats,
+                               const unsigned long long* __restrict__ nsum) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n * g.C) return;
+  const int64_t node = nodes[i / g.C];
+  const int c = i % g.C;
+  int lo[3], ce[3];
+  g.box_lo(node, lo);
+  g.in_extent(lo, 1, ce);
+  const long long cnt = (long long)ce[0] * ce[1] * ce[2];
+  stats[st_index(node, ST_AVG, c)] = (int)((2 * (long long)nsum[node * g.C + c] + cnt) / (2 * cnt));
+  bool any = false;
+  int a = 0, b = 0;
+  for (int k = 0; k < 8; ++k) {
+    if (!g.octant_real(k)) continue;
+    const int64_t ch = 8 * node + 1 + k;
+    if (!(flags[ch] & NF_EXISTS) || !(flags[ch] & NF_INVOL)) continue;
+    const int x = stats[st_index(ch, ST_SUBMIN, c)], y = stats[st_index(ch, ST_SUBMAX, c)];
+    a = any ? min(a, x) : x;
+    b = any ? max(b, y) : y;
+    any = true;
+  }
+  if (any) {
+    stats[st_index(node, ST_SUBMIN, c)] = a;
+    stats[st_index(node, ST_SUBMAX, c)] = b;
+  }
 }
 
 // every shell voxel of a brick <- background (publishing prefilled shells as
@@ -927,12 +956,8 @@ static int leaf_launch(const Tree& t, const void* src, int64_t nsrc, int oz, int
     const size_t smem = tma_smem(t.g);
     auto k = k_dense_leaf_tma<C>;
     VT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    // y = w / words-per-row by multiply-high (exact for w < 2^32 / wpr)
-    const uint32_t wpr = (uint32_t)(t.g.stored[0] * C / 2);
-    auto magic = [](uint32_t d) { return (uint32_t)((((uint64_t)1 << 32) + d - 1) / d); };
     k<<<n, kTmaWarps * 32, smem, t.stream>>>(map, oz, (int)dz, prefill, jobs, gn[0], gn[1], g0z,
-                                            t.g, (uint16_t*)t.d_pool, t.d_pmin, t.d_pmax,
-                                            t.d_psum, t.d_stats, t.d_flags, magic(wpr));
+                                            t.g, (uint16_t*)t.d_pool, t.d_stats, t.d_nsum);
     VT_CHECK_LAUNCH();
     return kLeafTma | (prefill ? kLeafPrefilled : 0);
   }
@@ -984,12 +1009,18 @@ void launch_plane_copy(const Tree& t, const int32_t* d_jobs, int n) {
   VT_CHECK_LAUNCH();
 }
 
-void launch_init_partials(const Tree& t, const int32_t* d_slots, int n) {
+void launch_init_fused(const Tree& t, const int64_t* d_nodes, int n) {
   if (n <= 0) return;
-  const int per = t.g.brick[2] * t.g.C;
-  const int64_t work = (int64_t)n * per;
-  k_init_partials<<<(unsigned)((work + 255) / 256), 256, 0, t.stream>>>(d_slots, n, per, t.d_pmin,
-                                                                       t.d_pmax, t.d_psum);
+  const int work = n * t.g.C;
+  k_init_fused<<<(work + 255) / 256, 256, 0, t.stream>>>(d_nodes, n, t.g.C, t.d_stats, t.d_nsum);
+  VT_CHECK_LAUNCH();
+}
+
+void launch_finish_fused(const Tree& t, const int64_t* d_nodes, int n) {
+  if (n <= 0) return;
+  const int work = n * t.g.C;
+  k_finish_fused<<<(work + 255) / 256, 256, 0, t.stream>>>(d_nodes, n, t.g, t.d_flags, t.d_stats,
+                                                          t.d_nsum);
   VT_CHECK_LAUNCH();
 }
 
@@ -1010,30 +1041,39 @@ int launch_dense_leaf(const Tree& t, const void* src, int64_t nsrc, int oz, int 
 }
 
 template <class T, int C>
-static void level_launch(const Tree& t, const int64_t* nodes, int n) {
+static void level_launch(const Tree& t, const int64_t* nodes, int n, int zsplit) {
   const int warps = std::min(8, std::max(1, t.g.brick[2]));
-  k_dense_level<T, C><<<n, 32 * warps, 0, t.stream>>>(nodes, t.g, (T*)t.d_pool, t.d_slot,
-                                                      t.d_flags, t.d_pmin, t.d_pmax, t.d_psum,
-                                                      t.d_stats);
+  k_dense_level<T, C><<<n * zsplit, 32 * warps, 0, t.stream>>>(
+      nodes, t.g, (T*)t.d_pool, t.d_slot, t.d_flags, t.d_pmin, t.d_pmax, t.d_psum, t.d_stats,
+      zsplit);
   VT_CHECK_LAUNCH();
 }
 
 template <class T>
-static void level_dispatch(const Tree& t, const int64_t* nodes, int n) {
+static void level_dispatch(const Tree& t, const int64_t* nodes, int n, int zs) {
   switch (t.g.C) {
-    case 1: level_launch<T, 1>(t, nodes, n); break;
-    case 2: level_launch<T, 2>(t, nodes, n); break;
-    case 3: level_launch<T, 3>(t, nodes, n); break;
-    default: level_launch<T, 4>(t, nodes, n); break;
+    case 1: level_launch<T, 1>(t, nodes, n, zs); break;
+    case 2: level_launch<T, 2>(t, nodes, n, zs); break;
+    case 3: level_launch<T, 3>(t, nodes, n, zs); break;
+    default: level_launch<T, 4>(t, nodes, n, zs); break;
   }
 }
 
-void launch_dense_level(const Tree& t, const int64_t* nodes, int n) {
+int dense_level_split(const Tree& t, int n) {
+  // few parents: split each over CTAs of 8 planes (one per warp) so the
+  // level is not the latency of a single CTA walking a whole brick
+  const int mz = t.g.brick[2];
+  int k = 1;
+  while (k * 2 * 8 <= mz && (int64_t)n * k < 2 * 148) k *= 2;
+  return k;
+}
+
+void launch_dense_level(const Tree& t, const int64_t* nodes, int n, int zsplit) {
   if (n <= 0) return;
   if (t.g.sb == 1)
-    level_dispatch<uint8_t>(t, nodes, n);
+    level_dispatch<uint8_t>(t, nodes, n, zsplit);
   else
-    level_dispatch<uint16_t>(t, nodes, n);
+    level_dispatch<uint16_t>(t, nodes, n, zsplit);
 }
 
 }  // namespace vtx

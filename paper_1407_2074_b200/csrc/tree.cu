@@ -101,6 +101,7 @@ Tree::Tree(const vt_tree_desc& d) {
   struct_mark.assign(cap, 0);
   complete.assign(cap, 0);
   fused1.assign(cap, 0);
+  pinv.assign(cap, 0);
   seed_of.assign(cap, -1);
   anc_mark.assign(cap, 0);
   {
@@ -217,6 +218,7 @@ Tree::~Tree() {
   cudaFree(d_pmin);
   cudaFree(d_pmax);
   cudaFree(d_psum);
+  cudaFree(d_nsum);
   if (ev0) cudaEventDestroy(ev0);
   if (ev1) cudaEventDestroy(ev1);
   if (ev_wait) cudaEventDestroy(ev_wait);
@@ -576,6 +578,11 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
             p.need[0] = p.need[1] = 0;
           }
           if (fresh) p.set_need_range(0, ce[2], true);
+          if (pinv[idx]) {
+            // partials never written by the dense kernel: recompute them all
+            p.set_need_range(0, ce[2], true);
+            pinv[idx] = 0;
+          }
           const bool own = scatter_owns_stats(g, channel, origin, dims, gx, gy);
           const int z0 = std::max(origin[2], gz * M[2]) - gz * M[2];
           const int z1 = std::min(std::min(origin[2] + dims[2], (gz + 1) * M[2]) - gz * M[2], ce[2]);
@@ -659,17 +666,23 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
   int32_t* dl = nullptr;
   if (dense) {
     ProfScope q(prof, 7);
-    int32_t* dfs = upload(*this, fused_slots);
-    launch_init_partials(*this, dfs, (int)fused_slots.size());
-    release(*this, dfs);
+    if (!fused_nodes.empty() && !d_nsum)
+      VT_CUDA(cudaMalloc(&d_nsum, g.capacity * g.C * sizeof(unsigned long long)));
+    int64_t* dfn = upload(*this, fused_nodes);
+    launch_init_fused(*this, dfn, (int)fused_nodes.size());
+    release(*this, dfn);
     DenseJob* dj = upload(*this, djobs);
     const bool want = prefill_enabled && !borders;
     const int lr = launch_dense_leaf(*this, dsrc, nvox * src_stride, origin[2], want ? 1 : 0, dj,
                                      (int)djobs.size(), gn, g0[2]);
     release(*this, dj);
     const bool prefilled = lr & kLeafPrefilled;
-    if (!(lr & kLeafTma))
+    if (!(lr & kLeafTma)) {
       for (int64_t p : fused_nodes) fused1[p] = 0;  // the fallback kernels do not fuse
+    } else {
+      for (const DenseJob& jd : djobs) pinv[jd.node] = 1;
+      for (int64_t p : fused_nodes) pinv[p] = 1;
+    }
     // host bookkeeping overlaps the device work: pending entries of leaves
     // whose statistics the kernel writes outright
     for (const DenseJob& jd : djobs) {
@@ -759,7 +772,7 @@ void Tree::propagate() {
     if (nodes.empty()) continue;
     sort_indices(nodes);
     std::vector<OctJob> oct;
-    std::vector<int64_t> dense_nodes;
+    std::vector<int64_t> dense_nodes, fused_done;
     if (lvl > 0) {
       // dirty children are sorted: those of parent p are a contiguous run
       const std::vector<int64_t>& kids = pend_nodes[lvl - 1];
@@ -767,17 +780,19 @@ void Tree::propagate() {
       for (int64_t p : nodes) {
         Pending& pp = *pend_find(p, lvl);
         if (lvl == 1 && fused1[p] && dense_parent(p)) {
-          // octants written by the leaf kernel, plane partials complete:
-          // only the reduce is owed
+          // octants and accumulators written by the leaf kernel: only the
+          // AVG and subtree extrema are owed (k_finish_fused)
           fused1[p] = 0;
           pp.box = Box{{0, 0, 0}, {M[0], M[1], M[2]}};
           pp.has_box = true;
-          pp.fused = true;
+          pp.dense = true;
           complete[p] = 1;
+          fused_done.push_back(p);
           continue;
         }
         fused1[p] = 0;
         if (dense_parent(p)) {
+          pinv[p] = 0;  // the dense level kernel writes every plane partial
           // every in-volume child complete: recompute the whole interior and
           // the statistics in one dense pass (dense_build.cu)
           dense_nodes.push_back(p);
@@ -788,6 +803,12 @@ void Tree::propagate() {
           continue;
         }
         complete[p] = 0;
+        if (pinv[p]) {
+          // a general-path parent over unmaintained partials: every plane
+          pinv[p] = 0;
+          pp.box = Box{{0, 0, 0}, {M[0], M[1], M[2]}};
+          pp.has_box = true;
+        }
         auto emit = [&](int64_t c, const Box* cb) {
           OctJob j{};
           j.pslot = slot[p];
@@ -834,9 +855,20 @@ void Tree::propagate() {
       OctJob* d = upload(*this, oct);
       launch_octant(*this, d, (int)oct.size());
       release(*this, d);
+      int64_t* dfd = upload(*this, fused_done);
+      launch_finish_fused(*this, dfd, (int)fused_done.size());
+      release(*this, dfd);
       int64_t* dd = upload(*this, dense_nodes);
-      launch_dense_level(*this, dd, (int)dense_nodes.size());
+      const int zsplit = dense_level_split(*this, (int)dense_nodes.size());
+      launch_dense_level(*this, dd, (int)dense_nodes.size(), zsplit);
       release(*this, dd);
+      if (zsplit > 1)
+        for (int64_t q : dense_nodes) {
+          // plane partials written, statistics owed to the reduce below
+          Pending& pq = *pend_find(q, lvl);
+          pq.dense = false;
+          pq.fused = true;
+        }
       dense_level_nodes += (int64_t)dense_nodes.size();
     }
     // stats of this level's dirty nodes
@@ -1106,6 +1138,7 @@ void Tree::merge(int64_t n, const int64_t* idx, const int32_t* nflags, const int
     }
     rec_nodes.push_back(i);
     complete[i] = 0;
+    pinv[i] = 0;  // merge recomputes every plane of incoming bricks
     for (int s2 = 0; s2 < ST_N; ++s2)
       for (int c = 0; c < kMaxC; ++c) {
         const int v = c < C ? stats_in[(r * C + c) * ST_N + s2] : 0;

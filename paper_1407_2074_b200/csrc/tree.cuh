@@ -98,6 +98,10 @@ struct Tree {
   bool dense_enabled = true;
   std::vector<uint8_t> complete;
   std::vector<uint8_t> fused1;  // level-1 parent whose octants the leaf kernel wrote
+  // per-plane partial statistics not maintained (TMA dense leaves, fused
+  // parents): a later general-path touch recomputes every plane first
+  std::vector<uint8_t> pinv;
+  unsigned long long* d_nsum = nullptr;  // [capacity][C] fused-parent sums (lazy)
   std::vector<int64_t> morton[3];
   // shells of dense leaves written with their fill_borders values at
   // insertion (dense_build.cu).  While !borders they are logically the
@@ -237,13 +241,16 @@ void launch_octant(const Tree& t, const OctJob* d_jobs, int n);
 constexpr int kLeafPrefilled = 1, kLeafTma = 2;
 int launch_dense_leaf(const Tree& t, const void* src, int64_t nsrc, int oz, int prefill,
                       const DenseJob* jobs, int n, const int gn[3], int g0z);
-// plane partials of the given bricks <- (INT_MAX, INT_MIN, 0) (fused parents)
-void launch_init_partials(const Tree& t, const int32_t* d_slots, int n);
+// fused level-1 parents: accumulators before / statistics after the leaf kernel
+void launch_init_fused(const Tree& t, const int64_t* d_nodes, int n);
+void launch_finish_fused(const Tree& t, const int64_t* d_nodes, int n);
 // z-shell plane copies between leaf bricks: dst plane <- src plane
 void launch_plane_copy(const Tree& t, const int32_t* d_jobs, int n);
 // every shell voxel of the given bricks <- background
 void launch_clear_shells(const Tree& t, const int32_t* d_slots, int n);
-void launch_dense_level(const Tree& t, const int64_t* nodes, int n);
+void launch_dense_level(const Tree& t, const int64_t* nodes, int n, int zsplit);
+// CTAs per parent for a dense level of n parents (> 1: statistics by k_reduce)
+int dense_level_split(const Tree& t, int n);
 void launch_plane(const Tree& t, const PlaneJob* d_jobs, int n);
 void launch_reduce(const Tree& t, const ReduceJob* d_jobs, int n);
 void launch_borders(const Tree& t, const BorderJob* d_jobs, int n);
