@@ -72,6 +72,29 @@ __global__ void k_seed(const SeedJob* __restrict__ jobs, int n, Geo g, T* pool,
     };
     const bool cov = j.cov_hi[0] > j.cov_lo[0] && j.cov_hi[1] > j.cov_lo[1] &&
                      j.cov_hi[2] > j.cov_lo[2];
+    if (cov && j.cov_lo[0] == 0 && j.cov_lo[1] == 0 && j.cov_lo[2] == 0 &&
+        j.cov_hi[0] == g.brick[0] && j.cov_hi[1] == g.brick[1] && j.cov_hi[2] == g.brick[2]) {
+      // the whole interior is rewritten later (fresh parent): the seed is the
+      // background shell only — two full planes, two rows per inner plane,
+      // two voxels per inner row, as flat coalesced runs
+      const int plane = sx * sy * C, inner = sz - 2;
+      const int n1 = 2 * plane, n2 = n1 + inner * 2 * rowlen, n3 = n2 + inner * (sy - 2) * 2 * C;
+      for (int e = threadIdx.x; e < n3; e += blockDim.x) {
+        int64_t off;
+        if (e < n1) {
+          off = e < plane ? e : (int64_t)(sz - 1) * plane + (e - plane);
+        } else if (e < n2) {
+          const int r = (e - n1) / rowlen, q = (e - n1) - r * rowlen;
+          off = (int64_t)(1 + r / 2) * plane + (int64_t)((r & 1) ? sy - 1 : 0) * rowlen + q;
+        } else {
+          const int r = (e - n2) / (2 * C), q = (e - n2) - r * 2 * C;
+          const int z = 1 + r / (sy - 2), y = 1 + r % (sy - 2);
+          off = (int64_t)z * plane + (int64_t)y * rowlen + (q < C ? q : (sx - 1) * C + (q - C));
+        }
+        b[off] = bg;
+      }
+      continue;
+    }
     // rows outside the cover: whole rows, one warp each
     for (int row = threadIdx.x >> 5; row < sy * sz; row += blockDim.x >> 5) {
       const int y = row % sy, z = row / sy;
@@ -396,28 +419,35 @@ __global__ void __launch_bounds__(256) k_octant(const OctJob* __restrict__ jobs,
 }
 
 // fill_borders (octree.py:540-614): 26 segments per brick from same-level
-// neighbour interiors, else neighbour AVG, bg outside the virtual extent
+// neighbour interiors, else neighbour AVG, bg outside the virtual extent.
+// One CTA per brick: 26 threads resolve the segments' neighbours at once
+// (find_node, octree.py:497-505, with exact integer compares), then the
+// whole CTA walks every shell voxel of the brick in one flat loop (a
+// thread per voxel, all channels), so the small segments do not serialise.
 template <class T>
-__global__ void k_borders(const BorderJob* __restrict__ jobs, Geo g, T* pool,
-                          const uint8_t* __restrict__ flags, const int32_t* __restrict__ slots,
-                          const int32_t* __restrict__ stats) {
+__global__ void __launch_bounds__(256) k_borders(const BorderJob* __restrict__ jobs, Geo g,
+                                                 T* pool, const uint8_t* __restrict__ flags,
+                                                 const int32_t* __restrict__ slots,
+                                                 const int32_t* __restrict__ stats) {
   const BorderJob j = jobs[blockIdx.x];
   const int level = g.level_of(j.node);
-  int lo[3], sc[3], mlo[3], mvirt[3];
-  g.box_lo(j.node, lo);
-  for (int a = 0; a < 3; ++a) {
-    sc[a] = g.scale(a, level);
-    mlo[a] = lo[a] / sc[a];
-    mvirt[a] = (g.virt[a] + sc[a] - 1) / sc[a];
-  }
-  T* dst = pool + (int64_t)j.slot * g.brick_elems;
-  __shared__ int64_t s_nb;
-  __shared__ int s_mode;  // 0 bg, 1 copy, 2 avg
-  __shared__ int s_nlo[3];
-  __shared__ int s_nslot;
-  for (int seg = 0; seg < 27; ++seg) {
-    int s3[3] = {seg % 3, (seg / 3) % 3, seg / 9};
-    if (s3[0] == 1 && s3[1] == 1 && s3[2] == 1) continue;
+  __shared__ int s_mode[27];  // 0 bg, 1 copy, 2 avg
+  __shared__ int s_src[27][3];  // copy: neighbour-interior origin of the segment
+  __shared__ int s_nslot[27];
+  __shared__ int s_avg[27][kMaxC];
+  __shared__ int s_start[28];
+  __shared__ int s_len[27][3], s_l0[27][3];
+  const int C = g.C;
+  if (threadIdx.x < 27) {
+    const int seg = threadIdx.x;
+    int lo[3], sc[3], mlo[3], mvirt[3];
+    g.box_lo(j.node, lo);
+    for (int a = 0; a < 3; ++a) {
+      sc[a] = g.scale(a, level);
+      mlo[a] = lo[a] / sc[a];
+      mvirt[a] = (g.virt[a] + sc[a] - 1) / sc[a];
+    }
+    const int s3[3] = {seg % 3, (seg / 3) % 3, seg / 9};
     int l0[3], len[3], g0[3];
     bool outside = false;
     for (int a = 0; a < 3; ++a) {
@@ -432,56 +462,69 @@ __global__ void k_borders(const BorderJob* __restrict__ jobs, Geo g, T* pool,
         if (g0[a] < 0 || g0[a] >= mvirt[a]) outside = true;
       }
     }
-    if (threadIdx.x == 0) {
-      if (outside) {
-        s_mode = 0;
-      } else {
-        // find_node((g0 + 0.5) * scale, level) with exact integer compares
-        int64_t idx = 0;
-        int lvl = g.depth;
-        int nlo[3] = {0, 0, 0};
-        while (lvl > level && (flags[idx] & NF_CHILDREN)) {
-          int k = 0;
-          for (int a = 0; a < 3; ++a) {
-            int half = g.extent(a, lvl - 1);
-            if (g.split[a] && 2LL * g0[a] * sc[a] + sc[a] >= 2LL * (nlo[a] + half)) {
-              k |= 1 << a;
-              nlo[a] += half;
-            }
+    const bool interior = s3[0] == 1 && s3[1] == 1 && s3[2] == 1;
+    for (int a = 0; a < 3; ++a) {
+      s_len[seg][a] = interior ? 0 : len[a];
+      s_l0[seg][a] = l0[a];
+    }
+    int mode = 0;
+    if (!interior && !outside) {
+      int64_t idx = 0;
+      int lvl = g.depth;
+      int nlo[3] = {0, 0, 0};
+      while (lvl > level && (flags[idx] & NF_CHILDREN)) {
+        int k = 0;
+        for (int a = 0; a < 3; ++a) {
+          const int half = g.extent(a, lvl - 1);
+          if (g.split[a] && 2LL * g0[a] * sc[a] + sc[a] >= 2LL * (nlo[a] + half)) {
+            k |= 1 << a;
+            nlo[a] += half;
           }
-          idx = 8 * idx + 1 + k;
-          --lvl;
         }
-        s_nb = idx;
-        if (lvl == level && (flags[idx] & NF_BRICK)) {
-          s_mode = 1;
-          s_nslot = slots[idx];
-          for (int a = 0; a < 3; ++a) s_nlo[a] = nlo[a] / sc[a];
-        } else {
-          s_mode = 2;
-        }
+        idx = 8 * idx + 1 + k;
+        --lvl;
       }
-    }
-    __syncthreads();
-    const int mode = s_mode;
-    const int n = len[0] * len[1] * len[2] * g.C;
-    for (int e = threadIdx.x; e < n; e += blockDim.x) {
-      int c = e % g.C;
-      int v = e / g.C;
-      int x = v % len[0], y = (v / len[0]) % len[1], z = v / (len[0] * len[1]);
-      T val;
-      if (mode == 0) {
-        val = (T)g.bg;
-      } else if (mode == 1) {
-        const T* src = pool + (int64_t)s_nslot * g.brick_elems;
-        val = src[g.voxel_offset(1 + g0[2] + z - s_nlo[2], 1 + g0[1] + y - s_nlo[1],
-                                 1 + g0[0] + x - s_nlo[0]) + c];
+      if (lvl == level && (flags[idx] & NF_BRICK)) {
+        mode = 1;
+        s_nslot[seg] = slots[idx];
+        // stored coords in the neighbour of the segment's first voxel
+        for (int a = 0; a < 3; ++a) s_src[seg][a] = 1 + g0[a] - nlo[a] / sc[a];
       } else {
-        val = (T)stats[st_index(s_nb, ST_AVG, c)];
+        mode = 2;
+        for (int c = 0; c < kMaxC; ++c) s_avg[seg][c] = c < C ? stats[st_index(idx, ST_AVG, c)] : 0;
       }
-      dst[g.voxel_offset(l0[2] + z, l0[1] + y, l0[0] + x) + c] = val;
     }
-    __syncthreads();
+    s_mode[seg] = mode;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int seg = 0; seg < 27; ++seg) {
+      s_start[seg] = acc;
+      acc += s_len[seg][0] * s_len[seg][1] * s_len[seg][2];
+    }
+    s_start[27] = acc;
+  }
+  __syncthreads();
+  T* dst = pool + (int64_t)j.slot * g.brick_elems;
+  const int total = s_start[27];
+  int seg = 0;
+  for (int e = threadIdx.x; e < total; e += blockDim.x) {
+    while (e >= s_start[seg + 1]) ++seg;  // e only grows per thread
+    const int v = e - s_start[seg];
+    const int lx = s_len[seg][0], ly = s_len[seg][1];
+    const int x = v % lx, y = (v / lx) % ly, z = v / (lx * ly);
+    T* d = dst + g.voxel_offset(s_l0[seg][2] + z, s_l0[seg][1] + y, s_l0[seg][0] + x);
+    const int mode = s_mode[seg];
+    if (mode == 1) {
+      const T* src = pool + (int64_t)s_nslot[seg] * g.brick_elems +
+                     g.voxel_offset(s_src[seg][2] + z, s_src[seg][1] + y, s_src[seg][0] + x);
+      for (int c = 0; c < C; ++c) d[c] = src[c];
+    } else if (mode == 2) {
+      for (int c = 0; c < C; ++c) d[c] = (T)s_avg[seg][c];
+    } else {
+      for (int c = 0; c < C; ++c) d[c] = (T)g.bg;
+    }
   }
 }
 
@@ -666,9 +709,9 @@ void launch_reduce(const Tree& t, const ReduceJob* d, int n) {
 void launch_borders(const Tree& t, const BorderJob* d, int n) {
   if (n <= 0) return;
   if (t.g.sb == 1)
-    k_borders<uint8_t><<<n, 128, 0, t.stream>>>(d, t.g, t.d_pool, t.d_flags, t.d_slot, t.d_stats);
+    k_borders<uint8_t><<<n, 256, 0, t.stream>>>(d, t.g, t.d_pool, t.d_flags, t.d_slot, t.d_stats);
   else
-    k_borders<uint16_t><<<n, 128, 0, t.stream>>>(d, t.g, (uint16_t*)t.d_pool, t.d_flags,
+    k_borders<uint16_t><<<n, 256, 0, t.stream>>>(d, t.g, (uint16_t*)t.d_pool, t.d_flags,
                                                  t.d_slot, t.d_stats);
   VT_CHECK_LAUNCH();
 }
