@@ -35,6 +35,12 @@ __global__ void k_create(const CreateJob* __restrict__ jobs, int n, Geo g,
   if (!g.octant_real(k)) return;
   int64_t child = 8 * jobs[job].parent + 1 + k;
   bool inv = flags[child] & NF_INVOL;
+  if (inv && jobs[job].skip_z1 >= jobs[job].skip_z0 && g.level_of(child) == 0) {
+    int lo[3];
+    g.box_lo(child, lo);
+    const int gz = lo[2] / g.brick[2];
+    if (gz >= jobs[job].skip_z0 && gz <= jobs[job].skip_z1) return;
+  }
   int v = inv ? stats[st_index(jobs[job].seed_src, ST_AVG, c)] : g.bg;
   stats[st_index(child, ST_AVG, c)] = v;
   stats[st_index(child, ST_MIN, c)] = v;

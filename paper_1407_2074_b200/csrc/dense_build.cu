@@ -416,7 +416,8 @@ template <int C>
 __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
     const __grid_constant__ CUtensorMap map, int oz, int dz, int prefill,
     const DenseJob* __restrict__ jobs, int gnx, int gny, int g0z, Geo g,
-    uint16_t* __restrict__ pool, int32_t* stats, unsigned long long* nsum) {
+    uint16_t* __restrict__ pool, int32_t* stats, int32_t* nmin, int32_t* nmax,
+    unsigned long long* nsum) {
   constexpr int P = kTmaP;
   constexpr int WPP = kTmaWarps / P;  // warps per plane
   constexpr int NT = WPP * 32;        // threads per plane
@@ -466,7 +467,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
   // the parent's octant (_update_parent_octant, octree.py:308-319).  That
   // pass visits every interior voxel exactly once, so it also carries the
   // leaf's statistics; the parent's are folded into its accumulators
-  // (stats min/max, nsum) with one atomic per channel per CTA.
+  // (nmin, nmax, nsum) with one atomic per channel per CTA.
   const int pslot = j.pad;
   const int hx = Mx / 2, hy = My / 2;
   const int offx = (gx & 1) * hx, offy = (gy & 1) * hy, offz = (gz & 1) * (Mz / 2);
@@ -679,8 +680,8 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
     stats[st_index(j.node, ST_SUBMAX, c)] = bmx;
     if (parent && pb != INT_MIN) {
       const int64_t pnode = (j.node - 1) >> 3;
-      atomicMin(stats + st_index(pnode, ST_MIN, c), pa);
-      atomicMax(stats + st_index(pnode, ST_MAX, c), pb);
+      atomicMin(nmin + pnode * C + c, pa);
+      atomicMax(nmax + pnode * C + c, pb);
       atomicAdd(nsum + pnode * C + c, pt2);
     }
   }
@@ -834,15 +835,15 @@ __global__ void k_plane_copy(const int32_t* __restrict__ jobs, int n, int64_t br
   for (int i = threadIdx.x; i < plane_words; i += blockDim.x) dst[i] = src[i];
 }
 
-// fused level-1 parents: min/max accumulators in stats, sums in nsum
-__global__ void k_init_fused(const int64_t* __restrict__ nodes, int n, int C, int32_t* stats,
-                             unsigned long long* nsum) {
+// fused level-1 parents: min / max / sum accumulators (nmin, nmax, nsum)
+__global__ void k_init_fused(const int64_t* __restrict__ nodes, int n, int C, int32_t* nmin,
+                             int32_t* nmax, unsigned long long* nsum) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n * C) return;
   const int64_t node = nodes[i / C];
   const int c = i % C;
-  stats[st_index(node, ST_MIN, c)] = INT_MAX;
-  stats[st_index(node, ST_MAX, c)] = INT_MIN;
+  nmin[node * C + c] = INT_MAX;
+  nmax[node * C + c] = INT_MIN;
   nsum[node * C + c] = 0;
 }
 
@@ -850,6 +851,7 @@ __global__ void k_init_fused(const int64_t* __restrict__ nodes, int n, int C, in
 // (octree.py:53-55) and the subtree extrema (octree.py:265-277)
 __global__ void k_finish_fused(const int64_t* __restrict__ nodes, int n, Geo g,
                                const uint8_t* __restrict__ flags, int32_t* stats,
+                               const int32_t* __restrict__ nmin, const int32_t* __restrict__ nmax,
                                const unsigned long long* __restrict__ nsum) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n * g.C) return;
@@ -860,6 +862,8 @@ __global__ void k_finish_fused(const int64_t* __restrict__ nodes, int n, Geo g,
   g.in_extent(lo, 1, ce);
   const long long cnt = (long long)ce[0] * ce[1] * ce[2];
   stats[st_index(node, ST_AVG, c)] = (int)((2 * (long long)nsum[node * g.C + c] + cnt) / (2 * cnt));
+  stats[st_index(node, ST_MIN, c)] = nmin[node * g.C + c];
+  stats[st_index(node, ST_MAX, c)] = nmax[node * g.C + c];
   bool any = false;
   int a = 0, b = 0;
   for (int k = 0; k < 8; ++k) {
@@ -957,7 +961,8 @@ static int leaf_launch(const Tree& t, const void* src, int64_t nsrc, int oz, int
     auto k = k_dense_leaf_tma<C>;
     VT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k<<<n, kTmaWarps * 32, smem, t.stream>>>(map, oz, (int)dz, prefill, jobs, gn[0], gn[1], g0z,
-                                            t.g, (uint16_t*)t.d_pool, t.d_stats, t.d_nsum);
+                                            t.g, (uint16_t*)t.d_pool, t.d_stats, t.d_nmin,
+                                            t.d_nmax, t.d_nsum);
     VT_CHECK_LAUNCH();
     return kLeafTma | (prefill ? kLeafPrefilled : 0);
   }
@@ -1012,7 +1017,8 @@ void launch_plane_copy(const Tree& t, const int32_t* d_jobs, int n) {
 void launch_init_fused(const Tree& t, const int64_t* d_nodes, int n) {
   if (n <= 0) return;
   const int work = n * t.g.C;
-  k_init_fused<<<(work + 255) / 256, 256, 0, t.stream>>>(d_nodes, n, t.g.C, t.d_stats, t.d_nsum);
+  k_init_fused<<<(work + 255) / 256, 256, 0, t.stream>>>(d_nodes, n, t.g.C, t.d_nmin, t.d_nmax,
+                                                        t.d_nsum);
   VT_CHECK_LAUNCH();
 }
 
@@ -1020,7 +1026,7 @@ void launch_finish_fused(const Tree& t, const int64_t* d_nodes, int n) {
   if (n <= 0) return;
   const int work = n * t.g.C;
   k_finish_fused<<<(work + 255) / 256, 256, 0, t.stream>>>(d_nodes, n, t.g, t.d_flags, t.d_stats,
-                                                          t.d_nsum);
+                                                          t.d_nmin, t.d_nmax, t.d_nsum);
   VT_CHECK_LAUNCH();
 }
 

@@ -219,6 +219,8 @@ Tree::~Tree() {
   cudaFree(d_pmax);
   cudaFree(d_psum);
   cudaFree(d_nsum);
+  cudaFree(d_nmin);
+  cudaFree(d_nmax);
   if (ev0) cudaEventDestroy(ev0);
   if (ev1) cudaEventDestroy(ev1);
   if (ev_wait) cudaEventDestroy(ev_wait);
@@ -325,7 +327,7 @@ void Tree::ensure_children(int64_t p) {
   flags[p] |= NF_CHILDREN;
   mark_struct(p);
   const int64_t src = seed_of[p] >= 0 ? seed_of[p] : p;
-  creates.push_back({p, src});
+  creates.push_back({p, src, create_skip_z0, create_skip_z1});
   int plo[3];
   g.box_lo(p, plo);
   const int clvl = g.level_of(p) - 1;
@@ -518,6 +520,91 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
   }
   std::vector<int32_t> leaf_slots((size_t)gn[0] * gn[1] * gn[2]);
   std::vector<std::vector<int64_t>> touched(g.depth + 1);
+  std::vector<int32_t> fused_slots;
+  std::vector<int64_t> fused_nodes;
+  // Dense early launch: with no recycled slots the reference's allocation
+  // order is known up front — the block's leaves take cursor + (grid order),
+  // then the fresh level-1 parents cursor + n_leaves + (BFS order) — so the
+  // leaf kernel (with fused level-1 octants) is launched BEFORE the host walk
+  // and the walk overlaps it; the walk re-derives every slot and checks.
+  const bool early = dense && free_slots.empty();
+  int launch_result = 0;
+  if (early) {
+    ProfScope q(prof, 7);
+    const int64_t cur0 = cursor;
+    const int64_t nleaves = (int64_t)gn[0] * gn[1] * gn[2];
+    djobs.reserve(nleaves);
+    for (int gz = g0[2]; gz <= g1[2]; ++gz)
+      for (int gy = g0[1]; gy <= g1[1]; ++gy)
+        for (int gx = g0[0]; gx <= g1[0]; ++gx)
+          djobs.push_back({leaf_index(gx, gy, gz), (int32_t)(cur0 + (int64_t)djobs.size()), -1});
+    if (g.depth >= 1 && g.split[0] && g.split[1] && g.split[2]) {
+      struct P1 { int64_t idx; int px, py, pz; };
+      std::vector<P1> par;
+      const int64_t base1 = g.level_start[g.depth - 1];
+      for (int pz = g0[2] >> 1; pz <= g1[2] >> 1; ++pz)
+        for (int py = 0; py <= g1[1] >> 1; ++py)
+          for (int px = 0; px <= g1[0] >> 1; ++px)
+            par.push_back({base1 + morton[0][px] + morton[1][py] + morton[2][pz], px, py, pz});
+      std::sort(par.begin(), par.end(), [](const P1& a, const P1& b) { return a.idx < b.idx; });
+      int64_t next = cur0 + nleaves;
+      for (const P1& q1 : par) {
+        if (flags[q1.idx] & NF_BRICK) continue;  // existing brick: no new slot
+        const int32_t ps = (int32_t)next++;
+        bool ok = true;
+        int64_t pos[8];
+        for (int k = 0; k < 8 && ok; ++k) {
+          const int gg[3] = {2 * q1.px + (k & 1), 2 * q1.py + ((k >> 1) & 1),
+                             2 * q1.pz + ((k >> 2) & 1)};
+          if (gg[0] > g1[0] || gg[1] > g1[1] || gg[2] < g0[2] || gg[2] > g1[2]) ok = false;
+          pos[k] = ((int64_t)(gg[2] - g0[2]) * gn[1] + gg[1]) * gn[0] + gg[0];
+        }
+        if (!ok) continue;
+        for (int k = 0; k < 8; ++k) djobs[pos[k]].pad = ps;
+        fused_nodes.push_back(q1.idx);
+        fused_slots.push_back(ps);
+      }
+    }
+    // every slot this insertion can allocate exists before the kernel runs:
+    // the block's leaves plus every ancestor its leaves can touch
+    int64_t nanc = 0;
+    for (int l = 1; l <= g.depth; ++l) {
+      int lo[3], hi[3];
+      for (int a = 0; a < 3; ++a) {
+        lo[a] = g.split[a] ? g0[a] >> l : 0;
+        hi[a] = g.split[a] ? g1[a] >> l : 0;
+      }
+      const int64_t base = g.level_start[g.depth - l];
+      for (int z = lo[2]; z <= hi[2]; ++z)
+        for (int y = lo[1]; y <= hi[1]; ++y)
+          for (int x = lo[0]; x <= hi[0]; ++x)
+            if (!(flags[base + morton[0][x] + morton[1][y] + morton[2][z]] & NF_BRICK)) ++nanc;
+    }
+    ensure_pool(cur0 + nleaves + nanc);
+    if (!fused_nodes.empty() && !d_nsum) {
+      VT_CUDA(cudaMalloc(&d_nsum, g.capacity * g.C * sizeof(unsigned long long)));
+      VT_CUDA(cudaMalloc(&d_nmin, g.capacity * g.C * sizeof(int32_t)));
+      VT_CUDA(cudaMalloc(&d_nmax, g.capacity * g.C * sizeof(int32_t)));
+    }
+    int64_t* dfn = upload(*this, fused_nodes);
+    launch_init_fused(*this, dfn, (int)fused_nodes.size());
+    release(*this, dfn);
+    DenseJob* dj;
+    {
+      ProfScope q2(prof, 10);
+      dj = upload(*this, djobs);
+    }
+    const bool want = prefill_enabled && !borders;
+    {
+      ProfScope q3(prof, 11);
+      launch_result = launch_dense_leaf(*this, dsrc, nvox * src_stride, origin[2], want ? 1 : 0,
+                                        dj, (int)djobs.size(), gn, g0[2]);
+    }
+    release(*this, dj);
+    // chain creation below must not seed the statistics the kernel writes
+    create_skip_z0 = g0[2];
+    create_skip_z1 = g1[2];
+  }
   auto* walk_scope = new ProfScope(prof, 1);
 
   // leaves (octree.py:351-360): descend, create, ensure brick, dirty box
@@ -545,7 +632,13 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
         if (dense) {
           // structure only here; the dense kernel writes the whole stored
           // brick and its final statistics (pending entries after launch)
-          djobs.push_back({idx, slot[idx], -1});
+          if (early) {
+            const int64_t i = ((int64_t)(gz - g0[2]) * gn[1] + (gy - g0[1])) * gn[0] + (gx - g0[0]);
+            VT_REQUIRE(djobs[i].node == idx && djobs[i].slot == slot[idx], VT_ESTATE,
+                       "dense build: leaf slot order diverged from the precomputed one");
+          } else {
+            djobs.push_back({idx, slot[idx], -1});
+          }
           touched[0].push_back(idx);
           continue;
         }
@@ -620,9 +713,15 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
   }
   // dense: level-1 parents whose every octant is a leaf of this block get
   // their octants from the leaf kernel (fused half-sample)
-  std::vector<int32_t> fused_slots;
-  std::vector<int64_t> fused_nodes;
-  if (dense && g.depth >= 1 && g.split[0] && g.split[1] && g.split[2]) {
+  create_skip_z0 = 0;
+  create_skip_z1 = -1;
+  if (early) {
+    for (size_t i = 0; i < fused_nodes.size(); ++i)
+      VT_REQUIRE(slot[fused_nodes[i]] == fused_slots[i], VT_ESTATE,
+                 "dense build: parent slot order diverged from the precomputed one");
+    for (int64_t p : fused_nodes) fused1[p] = 1;
+  }
+  if (dense && !early && g.depth >= 1 && g.split[0] && g.split[1] && g.split[2]) {
     for (int64_t p : touched[1]) {
       bool ok = true;
       int64_t pos[8];
@@ -666,16 +765,23 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
   int32_t* dl = nullptr;
   if (dense) {
     ProfScope q(prof, 7);
-    if (!fused_nodes.empty() && !d_nsum)
-      VT_CUDA(cudaMalloc(&d_nsum, g.capacity * g.C * sizeof(unsigned long long)));
-    int64_t* dfn = upload(*this, fused_nodes);
-    launch_init_fused(*this, dfn, (int)fused_nodes.size());
-    release(*this, dfn);
-    DenseJob* dj = upload(*this, djobs);
-    const bool want = prefill_enabled && !borders;
-    const int lr = launch_dense_leaf(*this, dsrc, nvox * src_stride, origin[2], want ? 1 : 0, dj,
-                                     (int)djobs.size(), gn, g0[2]);
-    release(*this, dj);
+    int lr = launch_result;
+    if (!early) {
+      // recycled slots: launch after the walk, with the walk's slots
+      if (!fused_nodes.empty() && !d_nsum) {
+        VT_CUDA(cudaMalloc(&d_nsum, g.capacity * g.C * sizeof(unsigned long long)));
+        VT_CUDA(cudaMalloc(&d_nmin, g.capacity * g.C * sizeof(int32_t)));
+        VT_CUDA(cudaMalloc(&d_nmax, g.capacity * g.C * sizeof(int32_t)));
+      }
+      int64_t* dfn = upload(*this, fused_nodes);
+      launch_init_fused(*this, dfn, (int)fused_nodes.size());
+      release(*this, dfn);
+      DenseJob* dj = upload(*this, djobs);
+      const bool want = prefill_enabled && !borders;
+      lr = launch_dense_leaf(*this, dsrc, nvox * src_stride, origin[2], want ? 1 : 0, dj,
+                             (int)djobs.size(), gn, g0[2]);
+      release(*this, dj);
+    }
     const bool prefilled = lr & kLeafPrefilled;
     if (!(lr & kLeafTma)) {
       for (int64_t p : fused_nodes) fused1[p] = 0;  // the fallback kernels do not fuse

@@ -101,7 +101,10 @@ struct Tree {
   // per-plane partial statistics not maintained (TMA dense leaves, fused
   // parents): a later general-path touch recomputes every plane first
   std::vector<uint8_t> pinv;
-  unsigned long long* d_nsum = nullptr;  // [capacity][C] fused-parent sums (lazy)
+  // [capacity][C] fused-parent accumulators (lazy)
+  unsigned long long* d_nsum = nullptr;
+  int32_t *d_nmin = nullptr, *d_nmax = nullptr;
+  int32_t create_skip_z0 = 0, create_skip_z1 = -1;  // CreateJob skip range (dense)
   std::vector<int64_t> morton[3];
   // shells of dense leaves written with their fill_borders values at
   // insertion (dense_build.cu).  While !borders they are logically the

@@ -123,7 +123,9 @@ __host__ __device__ inline int64_t st_index(int64_t node, int stat, int c) {
 // build job records (host builds them, kernels consume them)
 // ---------------------------------------------------------------------------
 struct StructUpd { int64_t node; int32_t flags; int32_t slot; };
-struct CreateJob { int64_t parent; int64_t seed_src; };   // seed children of parent
+// seed children of parent; leaves in grid layers [skip_z0, skip_z1] are left
+// alone (a dense insertion's leaf kernel writes their statistics)
+struct CreateJob { int64_t parent; int64_t seed_src; int32_t skip_z0, skip_z1; };
 // cov_lo/cov_hi: interior box [lo, hi) that later work of the same insertion
 // overwrites with every channel (scatter of a fused all-channel block, or the
 // octant rewrite of a fresh parent) — the seed skips it
