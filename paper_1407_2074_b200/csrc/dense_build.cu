@@ -1014,6 +1014,25 @@ void launch_plane_copy(const Tree& t, const int32_t* d_jobs, int n) {
   VT_CHECK_LAUNCH();
 }
 
+template <class T>
+__global__ void k_interleave(const T* __restrict__ src, int64_t n, int C, int c, T* dst) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i * C + c] = src[i];
+}
+
+void launch_interleave(const Tree& t, const void* src, int64_t n, int c, void* dst) {
+  if (n <= 0) return;
+  const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32);
+  if (t.g.sb == 1)
+    k_interleave<uint8_t><<<grid, 256, 0, t.stream>>>((const uint8_t*)src, n, t.g.C, c,
+                                                       (uint8_t*)dst);
+  else
+    k_interleave<uint16_t><<<grid, 256, 0, t.stream>>>((const uint16_t*)src, n, t.g.C, c,
+                                                        (uint16_t*)dst);
+  VT_CHECK_LAUNCH();
+}
+
 void launch_init_fused(const Tree& t, const int64_t* d_nodes, int n) {
   if (n <= 0) return;
   const int work = n * t.g.C;

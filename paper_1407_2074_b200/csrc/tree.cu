@@ -126,6 +126,7 @@ Tree::Tree(const vt_tree_desc& d) {
   }
   if (const char* e = std::getenv("VT_DENSE")) dense_enabled = e[0] != '0';
   if (const char* e = std::getenv("VT_PREFILL")) prefill_enabled = e[0] != '0';
+  if (const char* e = std::getenv("VT_DEFER")) defer_enabled = e[0] != '0';
   h_stats.assign(cap * ST_N * kMaxC, 0);
   flags[0] = NF_EXISTS | NF_INVOL;
   for (int c = 0; c < g.C; ++c)
@@ -219,6 +220,7 @@ Tree::~Tree() {
   cudaFree(d_pmax);
   cudaFree(d_psum);
   cudaFree(d_nsum);
+  cudaFree(d_acc);
   cudaFree(d_nmin);
   cudaFree(d_nmax);
   if (ev0) cudaEventDestroy(ev0);
@@ -505,6 +507,9 @@ bool Tree::dense_eligible(int channel, const int origin[3], const int dims[3], c
 void Tree::insert_staged(int channel, const int origin[3], const int dims[3], const void* dsrc,
                          int src_stride, int src_off, int reps) {
   const int64_t nvox = (int64_t)dims[0] * dims[1] * dims[2];
+  if (try_defer(channel, origin, dims, dsrc, src_stride, src_off)) return;
+  const bool starting = defer_start;  // this insertion opens a deferred layer
+  defer_start = false;
   ++data_version;
   const bool dense = dense_eligible(channel, origin, dims, dsrc, src_stride, src_off);
   std::vector<DenseJob> djobs;
@@ -759,10 +764,18 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
     ProfScope q(prof, 6);
     dc = upload(*this, creates);
     launch_create(*this, dc, (int)creates.size());
+    if (starting) {
+      // leaf seeds are held (the dense kernel writes whole leaf bricks, a
+      // materialisation launches them); ancestor shells go out now
+      dl.seeds.clear();
+      std::vector<SeedJob> now;
+      for (const SeedJob& sj : seeds) (g.level_of(sj.node) == 0 ? dl.seeds : now).push_back(sj);
+      seeds.swap(now);
+    }
     ds = upload(*this, seeds);
     launch_seed(*this, ds, (int)seeds.size());
   }
-  int32_t* dl = nullptr;
+  int32_t* dlp = nullptr;
   if (dense) {
     ProfScope q(prof, 7);
     int lr = launch_result;
@@ -820,15 +833,35 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
     } else {
       prefill_valid = false;
     }
+  } else if (starting) {
+    // open the deferred layer: slots and events are final, data waits
+    ProfScope q(prof, 7);
+    dl.active = true;
+    dl.gz = g0[2];
+    dl.z0 = g0[2] * M[2];
+    dl.nz = std::min(M[2], g.dims[2] - dl.z0);
+    dl.got.assign((size_t)dl.nz * g.C, 0);
+    dl.remaining = dl.nz * g.C;
+    dl.order.clear();
+    dl.leaf_slots = leaf_slots;
+    dl.djobs.clear();
+    for (int gy = g0[1]; gy <= g1[1]; ++gy)
+      for (int gx = g0[0]; gx <= g1[0]; ++gx) {
+        const int64_t idx = leaf_index(gx, gy, g0[2]);
+        dl.djobs.push_back({idx, slot[idx], -1});
+      }
+    if (!d_acc)
+      VT_CUDA(cudaMalloc(&d_acc, (size_t)M[2] * g.dims[1] * g.dims[0] * g.C * g.sb));
+    defer_copy(channel, origin, dims, dsrc);
   } else {
     prefill_valid = false;
     ProfScope q(prof, 7);
-    dl = upload(*this, leaf_slots);
-    launch_scatter(*this, dsrc, channel, src_stride, src_off, origin, dims, g0, gn, dl);
+    dlp = upload(*this, leaf_slots);
+    launch_scatter(*this, dsrc, channel, src_stride, src_off, origin, dims, g0, gn, dlp);
   }
   release(*this, dc);
   release(*this, ds);
-  release(*this, dl);
+  release(*this, dlp);
   inserted += nvox * reps;
 
   std::vector<char> dmark;
@@ -850,6 +883,118 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
   for (int r = 0; r < reps; ++r)
     for (int64_t i : upd)
       if (flags[i] & NF_EXISTS) events.emplace_back(VT_EV_UPDATED, i);
+  if (starting) {
+    dl.upd = upd;  // every later block of the layer touches the same nodes
+    if (dl.remaining == 0) finish_layer();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// deferred brick layers of slice streams (see Tree::DeferredLayer)
+// ---------------------------------------------------------------------------
+
+bool Tree::try_defer(int channel, const int origin[3], const int dims[3], const void* dsrc,
+                     int src_stride, int src_off) {
+  defer_start = false;
+  const int* M = g.brick;
+  const int64_t nvox = (int64_t)dims[0] * dims[1] * dims[2];
+  const bool shape = defer_enabled && dense_enabled && tau == 0 && channel >= 0 && g.C > 1 && src_stride == 1 &&
+                     src_off == 0 && nvox > 0 && origin[0] == 0 && origin[1] == 0 &&
+                     dims[0] == g.dims[0] && dims[1] == g.dims[1] &&
+                     origin[2] / M[2] == (origin[2] + dims[2] - 1) / M[2];
+  const int layer = origin[2] / M[2];
+  if (dl.active) {
+    bool cont = shape && layer == dl.gz;
+    for (int z = origin[2]; cont && z < origin[2] + dims[2]; ++z)
+      cont = !dl.got[(size_t)(z - dl.z0) * g.C + channel];
+    if (cont) {
+      ++data_version;
+      defer_copy(channel, origin, dims, dsrc);
+      events.reserve(events.size() + dl.upd.size());
+      for (int64_t i : dl.upd) events.emplace_back(VT_EV_UPDATED, i);
+      inserted += nvox;
+      if (dl.remaining == 0) finish_layer();
+      return true;
+    }
+    materialize_layer();
+  }
+  if (!shape) return false;
+  // open a layer only over brick-less leaves (its leaf bricks are fresh)
+  const int gx1 = (g.dims[0] - 1) / M[0], gy1 = (g.dims[1] - 1) / M[1];
+  for (int gy = 0; gy <= gy1; ++gy)
+    for (int gx = 0; gx <= gx1; ++gx)
+      if (flags[leaf_index(gx, gy, layer)] & NF_BRICK) return false;
+  defer_start = true;
+  return false;  // the caller runs the walk in opening mode
+}
+
+void Tree::defer_copy(int channel, const int origin[3], const int dims[3], const void* dsrc) {
+  const int64_t plane = (int64_t)g.dims[0] * g.dims[1];
+  uint8_t* dst = d_acc + (size_t)(origin[2] - dl.z0) * plane * g.C * g.sb;
+  launch_interleave(*this, dsrc, plane * dims[2], channel, dst);
+  for (int z = origin[2]; z < origin[2] + dims[2]; ++z) dl.got[(size_t)(z - dl.z0) * g.C + channel] = 1;
+  dl.remaining -= dims[2];
+  dl.order.push_back({origin[2], dims[2], channel});
+}
+
+// the layer is complete: one dense leaf kernel over the layer buffer
+void Tree::finish_layer() {
+  const int* M = g.brick;
+  const int gn[3] = {(g.dims[0] - 1) / M[0] + 1, (g.dims[1] - 1) / M[1] + 1, 1};
+  DenseJob* dj = upload(*this, dl.djobs);
+  const bool want = prefill_enabled && !borders;
+  const int64_t nsrc = (int64_t)dl.nz * g.dims[1] * g.dims[0] * g.C;
+  const int lr = launch_dense_leaf(*this, d_acc, nsrc, dl.z0, want ? 1 : 0, dj,
+                                   (int)dl.djobs.size(), gn, dl.gz);
+  release(*this, dj);
+  for (const DenseJob& jd : dl.djobs) {
+    Pending& p = pend(0, jd.node);
+    p.box = Box{{0, 0, 0}, {M[0], M[1], M[2]}};
+    p.has_box = true;
+    p.fresh = true;
+    p.masked = true;
+    p.need[0] = p.need[1] = 0;
+    p.dense = true;
+    complete[jd.node] = 1;
+    if (lr & kLeafTma) pinv[jd.node] = 1;
+  }
+  if (lr & kLeafPrefilled) {
+    halo_prefill = true;
+    const int lo = dl.z0 - 1, hi = dl.z0 + M[2];
+    for (const DenseJob& jd : dl.djobs) {
+      if (lo >= 0) owed_lo.push_back(jd.node);
+      if (hi < g.dims[2]) owed_hi.push_back(jd.node);
+    }
+  } else {
+    prefill_valid = false;
+  }
+  ++deferred_layers;
+  ++dense_leaf_inserts;
+  dl.active = false;
+  dl.seeds.clear();
+}
+
+// a reader needs the tree now: the general path's device work for the
+// blocks received so far (held leaf seeds, then one scatter per block)
+void Tree::materialize_layer() {
+  if (!dl.active) return;
+  dl.active = false;
+  prefill_valid = false;
+  const int* M = g.brick;
+  SeedJob* ds = upload(*this, dl.seeds);
+  launch_seed(*this, ds, (int)dl.seeds.size());
+  release(*this, ds);
+  int32_t* dls = upload(*this, dl.leaf_slots);
+  const int64_t plane = (int64_t)g.dims[0] * g.dims[1];
+  const int g0[3] = {0, 0, dl.gz};
+  const int gn[3] = {(g.dims[0] - 1) / M[0] + 1, (g.dims[1] - 1) / M[1] + 1, 1};
+  for (const auto& b : dl.order) {
+    const int o[3] = {0, 0, b[0]}, d[3] = {g.dims[0], g.dims[1], b[1]};
+    const uint8_t* src = d_acc + (size_t)(b[0] - dl.z0) * plane * g.C * g.sb;
+    launch_scatter(*this, src, b[2], g.C, b[2], o, d, g0, gn, dls);
+  }
+  release(*this, dls);
+  dl.seeds.clear();
 }
 
 // ---------------------------------------------------------------------------
@@ -1032,6 +1177,7 @@ void Tree::propagate() {
 
 void Tree::flush() {
   VT_CUDA(cudaSetDevice(device));
+  materialize_layer();
   flush_structure();
   propagate();
 }

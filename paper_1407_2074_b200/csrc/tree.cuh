@@ -4,6 +4,7 @@
 #pragma once
 
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <chrono>
 #include <queue>
@@ -114,6 +115,35 @@ struct Tree {
   bool prefill_valid = true;     // no general-path mutation since (fast fill_borders)
   std::vector<int64_t> owed_lo, owed_hi;  // leaves whose z-shell plane awaits a neighbour
   void publish_halos();
+
+  // Threshold-0 slice streams (ingest_stream's VSTR order: per z, one
+  // single-channel full-x/y block per channel).  The first block of a fresh
+  // brick layer runs the ordinary host walk (structure, slots, events) with
+  // its leaf seeds and scatter held back; later blocks of that layer only
+  // append the same UPDATED events and land in a device layer buffer; a
+  // complete layer is built by the dense leaf kernel.  Any reader (flush)
+  // first materialises a partial layer through the general path: the held
+  // seeds and one scatter per received block, in arrival order — exactly
+  // the device work the general path would have done.
+  struct DeferredLayer {
+    bool active = false;
+    int gz = 0, z0 = 0, nz = 0, remaining = 0;
+    std::vector<uint8_t> got;                // [nz][C] blocks received
+    std::vector<SeedJob> seeds;              // held leaf seeds
+    std::vector<int32_t> leaf_slots;         // (gy, gx) order
+    std::vector<DenseJob> djobs;             // (gy, gx) order
+    std::vector<std::array<int, 3>> order;   // (z, dz, channel) in arrival order
+    std::vector<int64_t> upd;                // one block's UPDATED list
+  } dl;
+  bool defer_enabled = true;    // env VT_DEFER=0 turns it off
+  bool defer_start = false;     // set by try_defer: this insertion opens a layer
+  uint8_t* d_acc = nullptr;     // [Mz][Y][X][C] layer buffer (lazy)
+  int64_t deferred_layers = 0;
+  bool try_defer(int channel, const int origin[3], const int dims[3], const void* dsrc,
+                 int src_stride, int src_off);
+  void defer_copy(int channel, const int origin[3], const int dims[3], const void* dsrc);
+  void materialize_layer();
+  void finish_layer();
   int64_t leaf_index(int gx, int gy, int gz) const {
     return g.level_start[g.depth] + morton[0][gx] + morton[1][gy] + morton[2][gz];
   }
@@ -246,6 +276,8 @@ int launch_dense_leaf(const Tree& t, const void* src, int64_t nsrc, int oz, int 
                       const DenseJob* jobs, int n, const int gn[3], int g0z);
 // fused level-1 parents: accumulators before / statistics after the leaf kernel
 void launch_init_fused(const Tree& t, const int64_t* d_nodes, int n);
+// channel `c` of an n-voxel single-channel block into an interleaved buffer
+void launch_interleave(const Tree& t, const void* src, int64_t n, int c, void* dst);
 void launch_finish_fused(const Tree& t, const int64_t* d_nodes, int n);
 // z-shell plane copies between leaf bricks: dst plane <- src plane
 void launch_plane_copy(const Tree& t, const int32_t* d_jobs, int n);

@@ -234,3 +234,77 @@ def test_prefilled_shells_read_as_background_before_fill_borders(tmp_path):
         t.fill_borders()
     assert tb.dense_counts()[2] == 0 and tc.dense_counts()[2] == 0
     assert _bricks(tb) == _bricks(ta) == _bricks(tc)
+
+
+def _run_stream(dims, C, brick, blocks, dense, snap_at=(), bg=0):
+    """blocks: (z, dz, channel) single-channel full-x/y blocks in order, or
+    ("box", c, origin, size) general blocks; a checksum read after the block
+    indices in snap_at (a reader materialises a partial deferred layer)."""
+    t = _tree(dims, C, brick, "uint16", dense, bg)
+    vol = _volume(dims, C, "uint16", seed=11)
+    evs, snaps = [], []
+    for i, b in enumerate(blocks):
+        if b[0] == "box":
+            _, c, o, sz = b
+            blk = vol[o[2]:o[2] + sz[2], o[1]:o[1] + sz[1], o[0]:o[0] + sz[0], c]
+            evs.append(_events(t.insert_block(c, o, np.ascontiguousarray(blk))))
+        else:
+            z, dz, c = b
+            evs.append(_events(t.insert_block(c, (0, 0, z),
+                                              np.ascontiguousarray(vol[z:z + dz, :, :, c]))))
+        if i in snap_at:
+            snaps.append((t.checksum(), _nodes(t)))
+    t.finalize()
+    t.fill_borders()
+    t.sync()
+    return t, evs, snaps
+
+
+def _vstr_order(dims, C, dz=1):
+    return [(z, min(dz, dims[2] - z), c) for z in range(0, dims[2], dz) for c in range(C)]
+
+
+STREAM_CASES = {
+    "vstr_slices": ((48, 40, 50), 3, (8, 8, 8), "vstr", ()),
+    "vstr_slices_reads": ((40, 32, 40), 3, (8, 8, 8), "vstr", (5, 40, 41, 77)),
+    "vstr_two_slice_blocks": ((32, 24, 36), 2, (8, 8, 8), "vstr2", (9,)),
+    "channel_major": ((32, 24, 24), 3, (8, 8, 8), "chmajor", ()),
+    "shuffled_in_layer": ((32, 32, 32), 3, (8, 8, 8), "shuffled", (30,)),
+    "general_block_between": ((32, 32, 24), 3, (8, 8, 8), "mixed", ()),
+    "brick16_c4": ((64, 32, 40), 4, (16, 16, 16), "vstr", (70,)),
+}
+
+
+@pytest.mark.parametrize("name", sorted(STREAM_CASES))
+def test_deferred_stream_layers_equal_general(name, tmp_path):
+    """Slice streams (ingest_stream's VSTR order) through the deferred
+    brick-layer path == the general path, with reads in the middle of layers
+    (materialisation), other orders and general blocks in between."""
+    dims, C, brick, kind, snaps = STREAM_CASES[name]
+    if kind == "vstr":
+        blocks = _vstr_order(dims, C)
+    elif kind == "vstr2":
+        blocks = _vstr_order(dims, C, dz=2)
+    elif kind == "chmajor":
+        blocks = [(z, 1, c) for c in range(C) for z in range(dims[2])]
+    elif kind == "shuffled":
+        rng = np.random.default_rng(5)
+        blocks = []
+        for z0 in range(0, dims[2], brick[2]):
+            layer = [(z, 1, c) for z in range(z0, min(dims[2], z0 + brick[2])) for c in range(C)]
+            rng.shuffle(layer)
+            blocks += [tuple(int(v) for v in b) for b in layer]
+    else:
+        blocks = _vstr_order(dims, C)
+        blocks.insert(13, ("box", 1, (3, 4, 2), (9, 7, 3)))
+        blocks.insert(40, ("box", 0, (0, 0, 9), (32, 32, 1)))
+    ta, ea, sa = _run_stream(dims, C, brick, blocks, dense=False, snap_at=snaps)
+    tb, eb, sb = _run_stream(dims, C, brick, blocks, dense=True, snap_at=snaps)
+    assert eb == ea
+    assert sb == sa
+    assert _nodes(tb) == _nodes(ta)
+    assert _bricks(tb) == _bricks(ta)
+    assert digest(tb, tmp_path, "b") == digest(ta, tmp_path, "a")
+    if kind in ("vstr", "vstr2") and not snaps:
+        # every layer completed without a reader: all built by the dense kernel
+        assert tb.dense_counts()[0] == -(-dims[2] // brick[2])
