@@ -416,12 +416,68 @@ def run_ours(args):
             "lod_sweep": sweep,
             "clocks": clocks,
         }
+        if world == 1 and args.stream:
+            out["stream"] = stream_ingest(args, peak)
         if world == 1 and not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(args)
         print(json.dumps(out), flush=True)
     if world > 1:
         barrier()
         dist.destroy_process_group()
+
+
+STREAM_DIMS = (2048, 2048, 64)  # cfg3's slice shape, two brick layers
+
+
+def stream_ingest(args, peak):
+    """cfg3-shaped slice stream (ingest_stream's VSTR order: per z, one
+    single-channel 2048x2048 block per channel) through Octree.insert_block
+    from device-resident slices, then finalize + fill_borders; CUDA events on
+    the tree's stream around the whole sequence (host gaps included)."""
+    import torch
+    from paper_1407_2074_b200 import BrickPoolConfig, Octree, VolumeDescriptor, _lib
+    dims = STREAM_DIMS
+    X, Y, Z = dims
+    st = torch.cuda.current_stream()
+    vol = torch.empty((Z, Y, X, CHANNELS), dtype=torch.uint16, device="cuda")
+    _lib.call("vt_synth", ct.c_void_p(vol.data_ptr()), 1, _lib.i32x3(dims), CHANNELS, 2, 0, 0, Z,
+              ct.c_void_p(st.cuda_stream))
+    planes = [vol[..., c].contiguous() for c in range(CHANNELS)]
+    del vol
+    desc = VolumeDescriptor(dims=dims, channels=CHANNELS, sample_format=FMT)
+    cfg = BrickPoolConfig(brick_dims=(BRICK,) * 3, homogeneity_threshold=0)
+    res = None
+    for rep in range(2):  # warm-up, then timed
+        tree = Octree(desc, cfg, reserve_slots=expected_bricks(dims, BRICK))
+        _lib.call("vt_tree_set_stream", tree.handle, ct.c_void_p(st.cuda_stream))
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for z in range(Z):
+            for c in range(CHANNELS):
+                tree.insert_block(c, (0, 0, z), planes[c][z:z + 1])
+        tree.finalize()
+        tree.fill_borders()
+        tree.sync()
+        e1.record(st)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        raw = X * Y * Z * CHANNELS * 2
+        pool = tree.brick_count * cfg.brick_nbytes(desc)
+        res = {"workload": f"cfg3-shaped slice stream {X}x{Y}x{Z} x{CHANNELS} uint16, one "
+                           "single-channel slice per insert_block (VSTR order), device-resident "
+                           "slices, + finalize + fill_borders",
+               "inserts": Z * CHANNELS, "ms": round(ms, 2),
+               "gbs_raw": round(raw / (ms * 1e-3) / 1e9, 2),
+               "roofline": {"achieved": round((raw + pool) / (ms * 1e-3) / 1e9, 2), "peak": peak,
+                            "frac": round((raw + pool) / (ms * 1e-3) / 1e9 / peak, 4),
+                            "unit": "GB/s", "model": "(raw + pool bytes) / stream time"},
+               "tree_checksum": f"{tree.checksum():016x}"}
+        tree.close()
+        del tree
+    del planes
+    torch.cuda.empty_cache()
+    return res
 
 
 def expected_geometry(dims, m):
@@ -604,6 +660,8 @@ def main():
                     help="sample reconstruction precision (RenderSettings.precision)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-build-e2e", dest="build_e2e", action="store_false")
+    ap.add_argument("--no-stream", dest="stream", action="store_false",
+                    help="skip the cfg3-shaped slice-stream ingest measurement")
     args = ap.parse_args()
     if args.warmup < 3:  # timing rule: at least 3 untimed warm-up steps
         args.warmup = 3
