@@ -111,6 +111,16 @@ vt_status vt_tree_wait_stream(vt_tree* tree, void* stream);
 vt_status vt_tree_signal_stream(vt_tree* tree, void* stream);
 /* Octree.insert_block (octree.py:323-397): one channel, values (dz,dy,dx)
  * x-fastest.  Errors exactly as octree.py:331-341 (VT_EINVAL). */
+/* B200 extension: vt_tree_insert (channel -1 = vt_tree_insert_channels) in
+ * one call with the caller-stream ordering of a device block (wait on
+ * caller_stream before reading it, make caller_stream wait for the reads;
+ * a null caller_stream is the legacy default stream)
+ * and the first `cap` pending change events copied out; *n_events = how
+ * many were pending (the rest stay for vt_tree_take_events) */
+vt_status vt_tree_insert_ev(vt_tree* tree, int32_t channel, const int32_t origin[3],
+                            const int32_t dims[3], const void* samples, int32_t mem_kind,
+                            void* caller_stream, int32_t* kinds, int64_t* indices, int64_t cap,
+                            int64_t* n_events);
 vt_status vt_tree_insert(vt_tree* tree, int32_t channel, const int32_t origin[3],
                          const int32_t dims[3], const void* samples, int32_t mem_kind);
 /* fused multi-channel variant: values (dz,dy,dx,C) channel-interleaved; the

@@ -77,6 +77,7 @@ SIGNATURES = {
     "vt_tree_set_stream": [P, P],
     "vt_tree_insert": [P, I32, PI32, PI32, P, I32],
     "vt_tree_insert_channels": [P, PI32, PI32, P, I32],
+    "vt_tree_insert_ev": [P, I32, PI32, PI32, P, I32, P, PI32, PI64, I64, PI64],
     "vt_tree_take_events": [P, PI32, PI64, I64, PI64, PI32],
     "vt_tree_event_count": [P, PI64],
     "vt_tree_checksum": [P, ct.POINTER(ct.c_uint64)],

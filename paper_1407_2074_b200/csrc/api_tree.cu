@@ -125,6 +125,42 @@ vt_status vt_tree_insert(vt_tree* tree, int32_t channel, const int32_t origin[3]
   });
 }
 
+// one call per insertion (B200 extension): caller-stream ordering of a
+// device block, the insertion, and the first `cap` change events
+vt_status vt_tree_insert_ev(vt_tree* tree, int32_t channel, const int32_t origin[3],
+                            const int32_t dims[3], const void* samples, int32_t mem_kind,
+                            void* caller_stream, int32_t* kinds, int64_t* indices, int64_t cap,
+                            int64_t* n_events) {
+  return guarded([&] {
+    Tree& t = tree->t;
+    VT_REQUIRE(channel >= -1, VT_EINVAL, "channel " + std::to_string(channel) + " out of range");
+    // a device block is ordered against the caller's stream; a null handle
+    // is the legacy default stream (torch's default), not "no stream"
+    cudaStream_t cs = (cudaStream_t)caller_stream;
+    const bool order = mem_kind == VT_MEM_DEVICE && cs != t.stream;
+    if (order) {
+      if (!t.ev_wait) VT_CUDA(cudaEventCreateWithFlags(&t.ev_wait, cudaEventDisableTiming));
+      VT_CUDA(cudaEventRecord(t.ev_wait, cs));
+      VT_CUDA(cudaStreamWaitEvent(t.stream, t.ev_wait, 0));
+    }
+    t.insert(channel, origin, dims, samples, mem_kind);
+    if (order) {
+      // the caller's allocator may recycle the block only after our reads
+      if (!t.ev_signal) VT_CUDA(cudaEventCreateWithFlags(&t.ev_signal, cudaEventDisableTiming));
+      VT_CUDA(cudaEventRecord(t.ev_signal, t.stream));
+      VT_CUDA(cudaStreamWaitEvent(cs, t.ev_signal, 0));
+    }
+    auto& ev = t.events;
+    *n_events = (int64_t)ev.size();
+    const int64_t m = std::min<int64_t>(cap, (int64_t)ev.size());
+    for (int64_t i = 0; i < m; ++i) {
+      kinds[i] = ev[i].first;
+      indices[i] = ev[i].second;
+    }
+    ev.erase(ev.begin(), ev.begin() + m);
+  });
+}
+
 vt_status vt_tree_insert_channels(vt_tree* tree, const int32_t origin[3], const int32_t dims[3],
                                   const void* samples, int32_t mem_kind) {
   return guarded([&] { tree->t.insert(-1, origin, dims, samples, mem_kind); });

@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import ctypes as ct
 import os
+import sys
 import threading
 from collections.abc import Sequence
 from dataclasses import dataclass
@@ -72,21 +73,6 @@ def classify_homogeneous(smin, smax, threshold: float):
     (octree.py:95-99)."""
     per = [(hi - lo) < threshold for lo, hi in zip(smin, smax)]
     return per, all(per)
-
-
-class _Pinned:
-    """A converted device temporary of an insertion (released in stream
-    order after the tree's reads, see Octree._release_source)."""
-
-    def __init__(self, t):
-        self.t = t
-
-    def data_ptr(self):
-        return self.t.data_ptr()
-
-    @property
-    def shape(self):
-        return self.t.shape
 
 
 class EventBatch(Sequence):
@@ -230,6 +216,7 @@ class Octree:
         _lib.call("vt_tree_create", ct.byref(d), ct.byref(h))
         self._h = h
         self._dense = os.environ.get("VT_DENSE", "1") != "0"
+        self._ev_cap = 4096
         self.store = _PoolView(self)
 
     # -- factories ---------------------------------------------------------
@@ -283,73 +270,76 @@ class Octree:
         desc = self.descriptor
         if not 0 <= channel < desc.channels:
             raise ValueError(f"channel {channel} out of range")
-        origin = tuple(int(v) for v in origin)
-        src, kind, shape, keep = self._source(values, 3)
-        bdims = (shape[2], shape[1], shape[0])
-        for a in range(3):
-            if origin[a] < 0 or origin[a] + bdims[a] > desc.dims[a]:
-                raise ValueError(f"block [{origin} + {bdims}) outside volume {desc.dims}")
-        with self.lock:
-            _lib.call("vt_tree_insert", self._h, int(channel), _lib.i32x3(origin),
-                      _lib.i32x3(bdims), src, kind)
-            self._release_source(keep, kind)
-            return self._collect()
+        return self._insert(int(channel), origin, values, 3)
 
     def insert_channels(self, origin, values) -> EventBatch:
         """All channels at once: values (dz, dy, dx, C) interleaved; same
         tree and events as C successive insert_block calls."""
+        return self._insert(-1, origin, values, 4)
+
+    def _insert(self, channel: int, origin, values, ndim: int) -> EventBatch:
         desc = self.descriptor
         origin = tuple(int(v) for v in origin)
-        src, kind, shape, keep = self._source(values, 4)
-        if shape[3] != desc.channels:
+        src, kind, shape, keep, cstream = self._source(values, ndim)
+        if ndim == 4 and shape[3] != desc.channels:
             raise ValueError("last axis must hold every channel")
         bdims = (shape[2], shape[1], shape[0])
         for a in range(3):
             if origin[a] < 0 or origin[a] + bdims[a] > desc.dims[a]:
                 raise ValueError(f"block [{origin} + {bdims}) outside volume {desc.dims}")
         with self.lock:
-            _lib.call("vt_tree_insert_channels", self._h, _lib.i32x3(origin),
-                      _lib.i32x3(bdims), src, kind)
-            self._release_source(keep, kind)
-            return self._collect()
-
-    def _release_source(self, keep, kind):
-        """Borrow contract for device blocks (the reference copies the block
-        before insert_block returns): the tree reads it asynchronously, so
-        the producing torch stream is made to wait for those reads — the
-        caching allocator may then recycle the block in stream order."""
-        if kind == _lib.VT_MEM_DEVICE:
-            import torch
-            dev = keep.t.device if isinstance(keep, _Pinned) else keep.device
-            _lib.call("vt_tree_signal_stream", self._h,
-                      ct.c_void_p(torch.cuda.current_stream(dev).cuda_stream))
+            # one library call: stream ordering, the insertion, its events
+            cap = self._ev_cap
+            kinds = np.empty(cap, np.int32)
+            idx = np.empty(cap, np.int64)
+            n = ct.c_int64()
+            _lib.call("vt_tree_insert_ev", self._h, channel, _lib.i32x3(origin),
+                      _lib.i32x3(bdims), src, kind, ct.c_void_p(cstream),
+                      _lib.ptr(kinds, ct.c_int32), _lib.ptr(idx, ct.c_int64), cap,
+                      ct.byref(n))
+            total = int(n.value)
+            if total > cap:
+                rk = np.empty(total - cap, np.int32)
+                ri = np.empty(total - cap, np.int64)
+                got, more = ct.c_int64(), ct.c_int32()
+                _lib.call("vt_tree_take_events", self._h, _lib.ptr(rk, ct.c_int32),
+                          _lib.ptr(ri, ct.c_int64), total - cap, ct.byref(got), ct.byref(more))
+                kinds, idx = np.concatenate([kinds, rk]), np.concatenate([idx, ri])
+                self._ev_cap = 1 << (total - 1).bit_length()
+            else:
+                kinds, idx = kinds[:total], idx[:total]
+            del keep  # device blocks: the caller's stream waits for our reads
+            out = EventBatch(kinds, idx)
+            if total:
+                self._events.append(out)
+            return out
 
     def _source(self, values, ndim):
+        """(pointer, memory kind, shape, keep-alive, caller stream handle)."""
         dt = self.descriptor.dtype
-        cai = getattr(values, "__cuda_array_interface__", None)
-        if cai is not None:
+        torch = sys.modules.get("torch")
+        is_tensor = torch is not None and isinstance(values, torch.Tensor)
+        if is_tensor or getattr(values, "__cuda_array_interface__", None) is not None:
             import torch
-            t = torch.as_tensor(values, device="cuda") if not isinstance(values, torch.Tensor) \
-                else values
-            if t.dim() != ndim:
-                raise ValueError(f"block values must be {ndim}-D")
-            want = torch.uint8 if dt == np.uint8 else torch.uint16
-            orig = t
-            t = t.to(want).contiguous()
-            if t.data_ptr() != orig.data_ptr():
-                # a converted temporary must outlive the tree stream's reads
-                t = _Pinned(t)
-            # device work runs on the tree's stream: order it after torch's
-            # current stream (event wait, no host synchronisation)
-            _lib.call("vt_tree_wait_stream", self._h,
-                      ct.c_void_p(torch.cuda.current_stream(t.device).cuda_stream))
-            return ct.c_void_p(t.data_ptr()), _lib.VT_MEM_DEVICE, tuple(t.shape), t
+            t = values if is_tensor else torch.as_tensor(values, device="cuda")
+            if not t.is_cuda:
+                values = t.numpy()
+            else:
+                if t.dim() != ndim:
+                    raise ValueError(f"block values must be {ndim}-D")
+                want = torch.uint8 if dt == np.uint8 else torch.uint16
+                if t.dtype != want or not t.is_contiguous():
+                    t = t.to(want).contiguous()
+                # device work runs on the tree's stream, ordered after torch's
+                # current stream (event wait, no host synchronisation)
+                cs = torch.cuda.current_stream(t.device).cuda_stream
+                return ct.c_void_p(t.data_ptr()), _lib.VT_MEM_DEVICE, tuple(t.shape), t, cs
         arr = np.asarray(values)
         if arr.ndim != ndim:
             raise ValueError("block values must be 3-D (z, y, x)" if ndim == 3 else
                              "block values must be 4-D (z, y, x, c)")
         arr = np.ascontiguousarray(arr.astype(dt, copy=False))
-        return ct.c_void_p(arr.ctypes.data), _lib.VT_MEM_HOST, arr.shape, arr
+        return ct.c_void_p(arr.ctypes.data), _lib.VT_MEM_HOST, arr.shape, arr, 0
 
     # -- state ---------------------------------------------------------------
     def _info(self) -> _lib.vt_tree_info:
