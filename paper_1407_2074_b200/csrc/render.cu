@@ -1534,6 +1534,7 @@ static void render_rect(vt_mirror* m, const vt_scene* scene, const int32_t* rect
   VT_CUDA(cudaStreamSynchronize(t.stream));
   float ms = 0;
   if (cudaEventElapsedTime(&ms, t.ev0, t.ev1) == cudaSuccess) t.last_render_ms = ms;
+  else cudaGetLastError();  // not a render error
   add_counters(cnt, h);
 }
 

@@ -1187,6 +1187,7 @@ void Tree::sync() {
   VT_CUDA(cudaStreamSynchronize(stream));
   float ms = 0;
   if (cudaEventElapsedTime(&ms, ev0, ev1) == cudaSuccess) last_build_ms = ms;
+  else cudaGetLastError();  // events never recorded (nothing ran): not an error
 }
 
 void Tree::gather_stats(const std::vector<int64_t>& nodes) {
