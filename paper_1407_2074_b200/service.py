@@ -49,21 +49,26 @@ FRAME_HEADER = struct.Struct("<IIII")  # frame id, width, height, pixel format
 PIXEL_FORMAT_PNG_RGBA = 1
 
 
+def _png(rgba: np.ndarray) -> bytes:
+    from PIL import Image
+    sink = io.BytesIO()
+    Image.fromarray(rgba, "RGBA").save(sink, format="PNG")
+    return sink.getvalue()
+
+
 def encode_frame(frame_id: int, image: np.ndarray) -> bytes:
     """Header + PNG of the RGBA8 conversion of a float (H, W, 4) image."""
-    from PIL import Image
     rgba = image_to_rgba8(image)
-    png = io.BytesIO()
-    Image.fromarray(rgba, "RGBA").save(png, format="PNG")
-    h, w = rgba.shape[:2]
-    return FRAME_HEADER.pack(frame_id, w, h, PIXEL_FORMAT_PNG_RGBA) + png.getvalue()
+    head = FRAME_HEADER.pack(frame_id, rgba.shape[1], rgba.shape[0], PIXEL_FORMAT_PNG_RGBA)
+    return head + _png(rgba)
 
 
 def decode_frame(blob: bytes):
     """(frame_id, width, height, format, RGBA8 array) of an encoded frame."""
     from PIL import Image
-    fid, w, h, fmt = FRAME_HEADER.unpack_from(blob, 0)
-    return fid, w, h, fmt, np.asarray(Image.open(io.BytesIO(blob[FRAME_HEADER.size:])))
+    head = FRAME_HEADER.unpack_from(blob, 0)
+    pixels = np.asarray(Image.open(io.BytesIO(memoryview(blob)[FRAME_HEADER.size:])))
+    return (*head, pixels)
 
 
 @dataclass
@@ -86,6 +91,35 @@ def _default_camera(desc, viewport) -> Camera:
                   width=viewport[0], height=viewport[1])
 
 
+@dataclass
+class _SceneState:
+    """What a viewer controls; ``version`` counts accepted changes."""
+    camera: Camera
+    tfs: list
+    clips: ClipSet
+    settings: RenderSettings
+    version: int = 0
+
+    def as_scene(self) -> Scene:
+        return Scene(camera=self.camera, settings=self.settings,
+                     transfer_functions=list(self.tfs), clips=self.clips)
+
+    def restyled(self, **changes) -> RenderSettings:
+        s = self.settings
+        base = {f: getattr(s, f) for f in ("mode", "strategy", "sampling_step",
+                                            "early_termination_alpha", "lod_bias")}
+        base.update(changes)
+        return RenderSettings(**base)
+
+    def describe(self) -> dict:
+        c = self.camera
+        cam = {"position": list(c.position), "look_at": list(c.look_at), "up": list(c.up),
+               "fov_deg": float(np.rad2deg(c.fov_y)), "viewport": [c.width, c.height]}
+        return {"camera": cam, "mode": self.settings.mode, "strategy": self.settings.strategy,
+                "transfer_functions": [tf.control_points() for tf in self.tfs],
+                "clip_planes": [[*p.normal, p.offset] for p in self.clips]}
+
+
 class FrameService:
     """Render loop + session state, independent of the transport."""
 
@@ -104,15 +138,13 @@ class FrameService:
         self.renderer = OutOfCoreRenderer(self.device)
         self.upload_budget_ms = upload_budget_ms
         self.idle_sleep = idle_sleep
-        desc = tree.descriptor
+        nch = tree.descriptor.channels
         self._lock = threading.Lock()
-        self._camera = _default_camera(desc, viewport)
-        self._tfs = [TransferFunction.ramp(max_alpha=0.8) for _ in range(desc.channels)]
-        self._clips = ClipSet()
-        self._settings = RenderSettings(strategy="refinement")
-        self._version = 0          # bumped by every accepted control
-        self._shown_version = -1   # the version the loop last restarted for
-        self._session = None
+        self._state = _SceneState(camera=_default_camera(tree.descriptor, viewport),
+                                  tfs=[TransferFunction.ramp(max_alpha=0.8) for _ in range(nch)],
+                                  clips=ClipSet(), settings=RenderSettings(strategy="refinement"))
+        self._shown_version = -1   # the scene version the loop last restarted for
+        self._session = None       # refinement session of the shown scene
         self._stable = False       # a full-frame pass requested / uploaded nothing
         self.frame_id = 0
         self.refinement_complete = False
@@ -122,50 +154,44 @@ class FrameService:
         self._ingest_thread: threading.Thread | None = None
         self._render_thread: threading.Thread | None = None
 
-    # -- scene ----------------------------------------------------------------
+    @property
+    def _settings(self) -> RenderSettings:
+        return self._state.settings
+
     def current_scene(self) -> Scene:
         with self._lock:
-            return Scene(camera=self._camera, settings=self._settings,
-                         transfer_functions=list(self._tfs), clips=self._clips)
+            return self._state.as_scene()
 
-    def _with_settings(self, **changes) -> RenderSettings:
-        s = self._settings
-        kw = dict(mode=s.mode, strategy=s.strategy, sampling_step=s.sampling_step,
-                  early_termination_alpha=s.early_termination_alpha, lod_bias=s.lod_bias)
-        kw.update(changes)
-        return RenderSettings(**kw)
+    # -- control messages (one handler per message type) ---------------------
+    def _on_camera(self, m):
+        cam = self._state.camera
+        w, h = m.get("viewport", [cam.width, cam.height])
+        fov = float(np.deg2rad(m["fov_deg"])) if "fov_deg" in m else cam.fov_y
+        self._state.camera = Camera(position=tuple(m.get("position", cam.position)),
+                                    look_at=tuple(m.get("look_at", cam.look_at)),
+                                    up=tuple(m.get("up", cam.up)), fov_y=fov,
+                                    width=int(w), height=int(h))
 
-    # -- control messages -----------------------------------------------------
-    def _ctl_camera(self, m):
-        cam = self._camera
-        vp = m.get("viewport", [cam.width, cam.height])
-        self._camera = Camera(position=tuple(m.get("position", cam.position)),
-                              look_at=tuple(m.get("look_at", cam.look_at)),
-                              up=tuple(m.get("up", cam.up)),
-                              fov_y=float(np.deg2rad(m["fov_deg"])) if "fov_deg" in m
-                              else cam.fov_y,
-                              width=int(vp[0]), height=int(vp[1]))
+    def _on_transfer_function(self, m):
+        ch = int(m["channel"])
+        if ch < 0 or ch >= self.tree.descriptor.channels:
+            raise ValueError(f"channel {ch} out of range")
+        self._state.tfs[ch] = TransferFunction(m["points"])
 
-    def _ctl_transfer_function(self, m):
-        c = int(m["channel"])
-        if not 0 <= c < self.tree.descriptor.channels:
-            raise ValueError(f"channel {c} out of range")
-        self._tfs[c] = TransferFunction(m["points"])
+    def _on_clip_planes(self, m):
+        planes = [ClipPlane(tuple(q[:3]), float(q[3])) for q in m.get("planes", [])]
+        self._state.clips = ClipSet(tuple(planes))
 
-    def _ctl_clip_planes(self, m):
-        self._clips = ClipSet(tuple(ClipPlane(tuple(p[:3]), float(p[3]))
-                                    for p in m.get("planes", [])))
+    def _on_mode(self, m):
+        self._state.settings = self._state.restyled(mode=m["mode"])
 
-    def _ctl_mode(self, m):
-        self._settings = self._with_settings(mode=m["mode"])
+    def _on_strategy(self, m):
+        self._state.settings = self._state.restyled(strategy=m["strategy"])
 
-    def _ctl_strategy(self, m):
-        self._settings = self._with_settings(strategy=m["strategy"])
+    def _on_reset_refinement(self, m):
+        """Nothing to change: the version bump restarts the loop."""
 
-    def _ctl_reset_refinement(self, m):
-        pass  # the version bump restarts the loop
-
-    def _ctl_abort_ingest(self, m):
+    def _on_abort_ingest(self, m):
         self._ingest_abort.set()
 
     def handle_control(self, message: str) -> dict:
@@ -175,83 +201,85 @@ class FrameService:
             msg = json.loads(message)
             if not isinstance(msg, dict) or "type" not in msg:
                 raise ValueError("control message must be an object with a type")
-            kind = msg["type"]
+            kind, mid = msg["type"], msg.get("id")
             if kind == "ping":
-                return {"type": "ack", "id": msg.get("id")}
+                return {"type": "ack", "id": mid}
             if kind == "get_settings":
                 with self._lock:
-                    return {"type": "settings", "id": msg.get("id"), **self._settings_dict()}
-            handler = getattr(self, f"_ctl_{kind}", None) if isinstance(kind, str) else None
-            if handler is None:
+                    return {"type": "settings", "id": mid, **self._state.describe()}
+            apply = getattr(self, f"_on_{kind}", None) if isinstance(kind, str) else None
+            if apply is None:
                 raise ValueError(f"unknown control type {kind!r}")
             with self._lock:
-                handler(msg)
-                self._version += 1
-            return {"type": "ack", "id": msg.get("id")}
+                apply(msg)
+                self._state.version += 1
+            return {"type": "ack", "id": mid}
         except Exception as exc:  # a bad message is answered, never fatal
-            mid = msg.get("id") if isinstance(msg, dict) else None
-            return {"type": "nack", "id": mid, "error": str(exc)}
-
-    def _settings_dict(self) -> dict:
-        cam = self._camera
-        return {"camera": {"position": list(cam.position), "look_at": list(cam.look_at),
-                           "up": list(cam.up), "fov_deg": float(np.rad2deg(cam.fov_y)),
-                           "viewport": [cam.width, cam.height]},
-                "mode": self._settings.mode, "strategy": self._settings.strategy,
-                "transfer_functions": [tf.control_points() for tf in self._tfs],
-                "clip_planes": [[*p.normal, p.offset] for p in self._clips]}
+            return {"type": "nack", "id": msg.get("id") if isinstance(msg, dict) else None,
+                    "error": str(exc)}
 
     # -- live ingest ------------------------------------------------------------
     def attach_ingest(self, stream) -> threading.Thread:
         """Consume a VSTR stream (after its handshake) while rendering."""
-        t = threading.Thread(target=lambda: ingest_stream(
-            stream, self.tree, should_stop=self._ingest_abort.is_set), name="ingest", daemon=True)
-        self._ingest_thread = t
-        t.start()
-        return t
+        def consume():
+            ingest_stream(stream, self.tree, should_stop=self._ingest_abort.is_set)
+
+        self._ingest_thread = threading.Thread(target=consume, name="ingest", daemon=True)
+        self._ingest_thread.start()
+        return self._ingest_thread
 
     @property
     def ingest_active(self) -> bool:
-        return self._ingest_thread is not None and self._ingest_thread.is_alive()
+        th = self._ingest_thread
+        return bool(th and th.is_alive())
 
     def construction_progress(self) -> float:
-        desc = self.tree.descriptor
-        return min(100.0, 100.0 * self.tree.inserted_voxels / (desc.voxel_count * desc.channels))
+        d = self.tree.descriptor
+        done = self.tree.inserted_voxels / float(d.voxel_count * d.channels)
+        return min(100.0, 100.0 * done)
 
     # -- render loop -------------------------------------------------------------
-    def step(self) -> bool:
-        """One loop iteration; True when a frame was broadcast."""
+    def _sync_changes(self) -> Scene:
+        """Apply pending tree events to the mirror; a scene or data change
+        restarts the loop.  Returns the scene to draw."""
         events = self.tree.drain_events()
-        if len(events):
+        changed = len(events) > 0
+        if changed:
             self.device.apply_events(events)
-        scene = self.current_scene()
         with self._lock:
-            version = self._version
-        if len(events) or version != self._shown_version:
+            scene, version = self._state.as_scene(), self._state.version
+        if changed or version != self._shown_version:
             self._shown_version = version
-            self._session = None
-            self._stable = False
-            self.refinement_complete = False
+            self._session, self._stable, self.refinement_complete = None, False, False
+        return scene
 
-        if not self._stable:
-            image, counters = self.renderer.render_fullframe(scene)
-            plan = self.device.process_flags(RenderMode.FULLFRAME)
-            uploaded = self.device.upload_bricks(plan, self.upload_budget_ms)
-            self._stable = counters.bricks_requested == 0 and uploaded == 0
-            self._broadcast(image)
-            return True
+    def _fullframe(self, scene: Scene) -> None:
+        image, counters = self.renderer.render_fullframe(scene)
+        uploaded = self.device.upload_bricks(self.device.process_flags(RenderMode.FULLFRAME),
+                                             self.upload_budget_ms)
+        self._stable = counters.bricks_requested == 0 and uploaded == 0
+        self._broadcast(image)
 
-        if self._settings.strategy != "refinement" or self.refinement_complete:
-            return False
+    def _refine(self, scene: Scene) -> bool:
         if self._session is None:
             self._session = self.renderer.start_refinement(scene)
-        if self._session.run_pass():
-            self.refinement_complete = True
-            self._broadcast(self._session.image())
+        if not self._session.run_pass():
+            self.device.upload_bricks(self.device.process_flags(RenderMode.REFINEMENT),
+                                      self.upload_budget_ms)
+            self._push_all(self._status_json())
+            return False
+        self.refinement_complete = True
+        self._broadcast(self._session.image())
+        return True
+
+    def step(self) -> bool:
+        """One loop iteration; True when a frame was broadcast."""
+        scene = self._sync_changes()
+        if not self._stable:
+            self._fullframe(scene)
             return True
-        self.device.upload_bricks(self.device.process_flags(RenderMode.REFINEMENT),
-                                  self.upload_budget_ms)
-        self._push_all(self._status_json())
+        if self._settings.strategy == "refinement" and not self.refinement_complete:
+            return self._refine(scene)
         return False
 
     def _push_all(self, payload) -> None:
@@ -260,19 +288,17 @@ class FrameService:
 
     def _broadcast(self, image: np.ndarray) -> None:
         self.frame_id += 1
-        frame = encode_frame(self.frame_id, image)
-        status = self._status_json()
-        for client in list(self._clients):
-            client.push(frame)
-            client.push(status)
+        for payload in (encode_frame(self.frame_id, image), self._status_json()):
+            self._push_all(payload)
 
     def _status_json(self) -> str:
+        s = self._settings
         return json.dumps({"type": "status", "frame_id": self.frame_id,
                            "construction_pct": round(self.construction_progress(), 2),
                            "bricks_resident": self.device.resident_bricks,
                            "refinement_complete": self.refinement_complete,
-                           "ingest_active": self.ingest_active,
-                           "mode": self._settings.mode, "strategy": self._settings.strategy})
+                           "ingest_active": self.ingest_active, "mode": s.mode,
+                           "strategy": s.strategy})
 
     def run(self) -> None:
         while not self._stop.is_set():
@@ -294,7 +320,7 @@ class FrameService:
         client = _Client()
         self._clients.append(client)
         with self._lock:
-            self._version += 1  # a new viewer gets a fresh frame
+            self._state.version += 1  # a new viewer gets a fresh frame
         return client
 
     def unregister_client(self, client: _Client) -> None:
@@ -304,26 +330,25 @@ class FrameService:
 
 
 def serve(service: FrameService, host: str = "127.0.0.1", port: int = 8765):
-    """Websocket transport (service.py:320-349): binary frames and status
-    JSON out, control JSON in, one sender thread per viewer."""
+    """Websocket transport (service.py:320-349): per viewer, a sender thread
+    drains its outbox (binary frames, status text) while the connection's
+    text messages are answered as controls."""
     from websockets.sync.server import serve as ws_serve
 
-    def handler(conn):
-        client = service.register_client()
-
-        def sender():
-            while not client.closed:
-                client.ready.wait(0.25)
-                client.ready.clear()
+    def pump(conn, client: _Client) -> None:
+        while not client.closed:
+            if not client.ready.wait(0.25):
+                continue
+            client.ready.clear()
+            try:
                 while client.queue:
-                    try:
-                        conn.send(client.queue.popleft())
-                    except Exception:
-                        client.closed = True
-                        return
+                    conn.send(client.queue.popleft())
+            except Exception:  # the viewer went away
+                client.closed = True
 
-        out = threading.Thread(target=sender, daemon=True)
-        out.start()
+    def session(conn) -> None:
+        client = service.register_client()
+        threading.Thread(target=pump, args=(conn, client), daemon=True).start()
         try:
             for message in conn:
                 if isinstance(message, str):
@@ -333,7 +358,7 @@ def serve(service: FrameService, host: str = "127.0.0.1", port: int = 8765):
 
     service.start()
     try:
-        with ws_serve(handler, host, port) as server:
+        with ws_serve(session, host, port) as server:
             server.serve_forever()
     finally:
         service.stop()
@@ -356,14 +381,16 @@ def orbit_bench(tree: Octree, *, frames: int = 100, orbit_degrees: float = 360.0
     if scene is None:
         scene = Scene(_default_camera(desc, (vw, vh)), RenderSettings(),
                       [TransferFunction.ramp(max_alpha=0.8) for _ in range(desc.channels)])
-    centre = np.array([d * s / 2.0 for d, s in zip(desc.dims, desc.spacing)])
-    radius = 2.5 * max(d * s for d, s in zip(desc.dims, desc.spacing))
+    extent = np.asarray(desc.dims, np.float64) * np.asarray(desc.spacing, np.float64)
+    centre = extent / 2.0
+    angles = np.deg2rad(orbit_degrees) * np.arange(frames) / frames
+    ring = centre + 2.5 * extent.max() * np.stack(
+        [np.sin(angles), np.zeros_like(angles), -np.cos(angles)], axis=1)
     times, fallbacks = [], []
     uploads0 = device.uploads
-    for i in range(frames):
-        a = np.deg2rad(orbit_degrees) * i / frames
-        pos = centre + radius * np.array([np.sin(a), 0.0, -np.cos(a)])
-        scene.camera = Camera(position=tuple(pos), look_at=tuple(centre), up=(0, 1, 0),
+    for pos in ring:
+        scene.camera = Camera(position=tuple(float(v) for v in pos),
+                              look_at=tuple(float(v) for v in centre), up=(0, 1, 0),
                               fov_y=scene.camera.fov_y, width=vw, height=vh)
         t0 = time.perf_counter()
         _, counters = renderer.render_fullframe(scene)
