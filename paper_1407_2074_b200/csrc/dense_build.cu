@@ -520,13 +520,26 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
         // of the same row (rows outside the volume: background)
         if (wact) {
           const uint32_t* iw = reinterpret_cast<const uint32_t*>(iplane) + xo;
-          for (int ys = rr; ys < Sy; ys += R) {
-            const bool rin = (unsigned)(y0 + ys) < (unsigned)Y;
-            const uint32_t* q = iw + ys * (brow >> 1);
-            uint32_t* o = oplane + ys * wpr + wr0;
-            for (int w = 0; w < wpr - wr0; w += wstep) {
-              const uint32_t out = (xoff & 1) ? __byte_perm(q[w], q[w + 1], 0x5432) : q[w];
-              o[w] = rin ? out : bgw;
+          const int qs = brow >> 1;
+          if (wpr <= NT) {
+            // one word per row per thread: a flat, unrollable row loop
+            uint32_t* o = oplane + wr0;
+            const bool odd = xoff & 1;
+#pragma unroll 4
+            for (int ys = rr; ys < Sy; ys += R) {
+              const uint32_t* q = iw + ys * qs;
+              const uint32_t out = odd ? __byte_perm(q[0], q[1], 0x5432) : q[0];
+              o[ys * wpr] = (unsigned)(y0 + ys) < (unsigned)Y ? out : bgw;
+            }
+          } else {
+            for (int ys = rr; ys < Sy; ys += R) {
+              const bool rin = (unsigned)(y0 + ys) < (unsigned)Y;
+              const uint32_t* q = iw + ys * qs;
+              uint32_t* o = oplane + ys * wpr + wr0;
+              for (int w = 0; w < wpr - wr0; w += wstep) {
+                const uint32_t out = (xoff & 1) ? __byte_perm(q[w], q[w + 1], 0x5432) : q[w];
+                o[w] = rin ? out : bgw;
+              }
             }
           }
         }
