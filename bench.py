@@ -234,12 +234,21 @@ def run_ours(args):
         return tree, e0.elapsed_time(e1), e1.elapsed_time(e2)
 
     # untimed warm-up build (first launches load kernel modules, encode
-    # tensor maps, page-lock staging), then the timed build
+    # tensor maps, page-lock staging), then three timed builds: the median
+    # (by total time) is reported, the last tree is kept for rendering
     wt, _, _ = build(vol)
     wt.close()
     del wt
     torch.cuda.empty_cache()
-    tree, build_ms, border_ms = build(vol)
+    runs = []
+    for rep in range(3):
+        tree, b_ms, f_ms = build(vol)
+        runs.append((b_ms + f_ms, b_ms, f_ms))
+        if rep < 2:
+            tree.close()
+            del tree
+            torch.cuda.empty_cache()
+    _, build_ms, border_ms = sorted(runs)[1]
     pool_bytes = tree.brick_count * cfg.brick_nbytes(desc)
     # every rank must hold the same tree after the sharded build
     ck = tree.checksum()
@@ -401,6 +410,7 @@ def run_ours(args):
                     if world == 1 else "SortFirstRenderer.render_fullframe(to_host=True)"},
             "build": {"raw_gb": round(raw_bytes / 1e9, 3), "pool_gb": round(pool_bytes / 1e9, 3),
                       "bricks": tree.brick_count, "build_ms": round(total_build_ms, 2),
+                      "build_runs_ms": [round(r[0], 2) for r in runs],
                       "insert_ms": round(build_ms, 2),
                       "fill_borders_ms": round(border_ms, 2),
                       "gbs_raw": round(build_gbs, 2),

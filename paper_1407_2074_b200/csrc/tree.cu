@@ -525,6 +525,7 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
   }
   std::vector<int32_t> leaf_slots((size_t)gn[0] * gn[1] * gn[2]);
   std::vector<std::vector<int64_t>> touched(g.depth + 1);
+  touched[0].reserve(leaf_slots.size());
   std::vector<int32_t> fused_slots;
   std::vector<int64_t> fused_nodes;
   // Dense early launch: with no recycled slots the reference's allocation
@@ -804,6 +805,8 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
     }
     // host bookkeeping overlaps the device work: pending entries of leaves
     // whose statistics the kernel writes outright
+    pend_pool[0].reserve(pend_pool[0].size() + djobs.size());
+    pend_nodes[0].reserve(pend_nodes[0].size() + djobs.size());
     for (const DenseJob& jd : djobs) {
       Pending& p = pend(0, jd.node);
       p.box = Box{{0, 0, 0}, {M[0], M[1], M[2]}};
