@@ -139,6 +139,11 @@ Tree::Tree(const vt_tree_desc& d) {
   VT_CUDA(cudaMemcpy(d_flags, flags.data(), 1, cudaMemcpyHostToDevice));
   VT_CUDA(cudaMemcpy(d_stats, h_stats.data(), ST_N * kMaxC * sizeof(int32_t),
                      cudaMemcpyHostToDevice));
+  dense_pending.box = Box{{0, 0, 0}, {g.brick[0], g.brick[1], g.brick[2]}};
+  dense_pending.has_box = true;
+  dense_pending.fresh = true;
+  dense_pending.masked = true;
+  dense_pending.dense = true;
   pend_nodes.assign(g.depth + 1, {});
   pend_pool.assign(g.depth + 1, {});
   pend_slot.assign(cap, -1);
@@ -805,16 +810,9 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
     }
     // host bookkeeping overlaps the device work: pending entries of leaves
     // whose statistics the kernel writes outright
-    pend_pool[0].reserve(pend_pool[0].size() + djobs.size());
     pend_nodes[0].reserve(pend_nodes[0].size() + djobs.size());
     for (const DenseJob& jd : djobs) {
-      Pending& p = pend(0, jd.node);
-      p.box = Box{{0, 0, 0}, {M[0], M[1], M[2]}};
-      p.has_box = true;
-      p.fresh = true;
-      p.masked = true;
-      p.need[0] = p.need[1] = 0;
-      p.dense = true;
+      pend_dense(jd.node);
       complete[jd.node] = 1;
     }
     ++dense_leaf_inserts;
@@ -951,13 +949,7 @@ void Tree::finish_layer() {
                                    (int)dl.djobs.size(), gn, dl.gz);
   release(*this, dj);
   for (const DenseJob& jd : dl.djobs) {
-    Pending& p = pend(0, jd.node);
-    p.box = Box{{0, 0, 0}, {M[0], M[1], M[2]}};
-    p.has_box = true;
-    p.fresh = true;
-    p.masked = true;
-    p.need[0] = p.need[1] = 0;
-    p.dense = true;
+    pend_dense(jd.node);
     complete[jd.node] = 1;
     if (lr & kLeafTma) pinv[jd.node] = 1;
   }

@@ -172,18 +172,32 @@ struct Tree {
   std::vector<std::vector<Pending>> pend_pool;
   std::vector<int32_t> pend_slot;
   bool has_pending = false;
+  // Leaves a dense kernel wrote share one pending state (full box, fresh,
+  // statistics final): pend_slot = -2, no per-leaf entry unless a general
+  // insertion touches the leaf before the next propagation.
+  Pending dense_pending;
+  void pend_dense(int64_t idx) {  // level 0
+    int32_t& k = pend_slot[idx];
+    if (k == -1) {
+      k = -2;
+      pend_nodes[0].push_back(idx);
+    } else if (k >= 0) {
+      pend_pool[0][k] = dense_pending;
+    }
+  }
   Pending& pend(int lvl, int64_t idx) {
     int32_t& k = pend_slot[idx];
     if (k < 0) {
+      const bool was_dense = k == -2;
       k = (int32_t)pend_pool[lvl].size();
-      pend_pool[lvl].emplace_back();
-      pend_nodes[lvl].push_back(idx);
+      pend_pool[lvl].push_back(was_dense ? dense_pending : Pending{});
+      if (!was_dense) pend_nodes[lvl].push_back(idx);
     }
     return pend_pool[lvl][k];
   }
   Pending* pend_find(int64_t idx, int lvl) {
-    int32_t k = pend_slot[idx];
-    return k < 0 ? nullptr : &pend_pool[lvl][k];
+    const int32_t k = pend_slot[idx];
+    return k >= 0 ? &pend_pool[lvl][k] : (k == -2 ? &dense_pending : nullptr);
   }
 
   // -- per-insertion device work lists --
