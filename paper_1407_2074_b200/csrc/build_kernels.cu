@@ -443,6 +443,7 @@ __global__ void __launch_bounds__(256) k_borders(const BorderJob* __restrict__ j
   __shared__ int s_avg[27][kMaxC];
   __shared__ int s_start[28];
   __shared__ int s_len[27][3], s_l0[27][3];
+  __shared__ uint32_t s_mg[27][2];  // v / lx and v / (lx * ly) by multiply-high
   const int C = g.C;
   if (threadIdx.x < 27) {
     const int seg = threadIdx.x;
@@ -472,6 +473,11 @@ __global__ void __launch_bounds__(256) k_borders(const BorderJob* __restrict__ j
     for (int a = 0; a < 3; ++a) {
       s_len[seg][a] = interior ? 0 : len[a];
       s_l0[seg][a] = l0[a];
+    }
+    {
+      const uint64_t dx = (uint64_t)(len[0] > 0 ? len[0] : 1), dxy = dx * (len[1] > 0 ? len[1] : 1);
+      s_mg[seg][0] = (uint32_t)((((uint64_t)1 << 32) + dx - 1) / dx);
+      s_mg[seg][1] = (uint32_t)((((uint64_t)1 << 32) + dxy - 1) / dxy);
     }
     int mode = 0;
     if (!interior && !outside) {
@@ -514,23 +520,46 @@ __global__ void __launch_bounds__(256) k_borders(const BorderJob* __restrict__ j
   __syncthreads();
   T* dst = pool + (int64_t)j.slot * g.brick_elems;
   const int total = s_start[27];
-  int seg = 0;
-  for (int e = threadIdx.x; e < total; e += blockDim.x) {
-    while (e >= s_start[seg + 1]) ++seg;  // e only grows per thread
-    const int v = e - s_start[seg];
-    const int lx = s_len[seg][0], ly = s_len[seg][1];
-    const int x = v % lx, y = (v / lx) % ly, z = v / (lx * ly);
-    T* d = dst + g.voxel_offset(s_l0[seg][2] + z, s_l0[seg][1] + y, s_l0[seg][0] + x);
-    const int mode = s_mode[seg];
-    if (mode == 1) {
-      const T* src = pool + (int64_t)s_nslot[seg] * g.brick_elems +
-                     g.voxel_offset(s_src[seg][2] + z, s_src[seg][1] + y, s_src[seg][0] + x);
-      for (int c = 0; c < C; ++c) d[c] = src[c];
-    } else if (mode == 2) {
-      for (int c = 0; c < C; ++c) d[c] = (T)s_avg[seg][c];
-    } else {
-      for (int c = 0; c < C; ++c) d[c] = (T)g.bg;
+  // batches of K shell voxels per thread: every source of a batch is read
+  // before any destination is written (the reads are strided neighbour
+  // columns: latency, not bandwidth, bounds this loop)
+  constexpr int K = 4;
+  for (int e0 = threadIdx.x; e0 < total; e0 += K * blockDim.x) {
+    int64_t doff[K];
+    T val[K][kMaxC];
+    bool live[K];
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+      const int e = e0 + q * blockDim.x;
+      live[q] = e < total;
+      if (!live[q]) continue;
+      int seg = 0;  // binary search of the segment prefix sums
+#pragma unroll
+      for (int step = 16; step >= 1; step >>= 1)
+        if (seg + step < 27 && e >= s_start[seg + step]) seg += step;
+      const int v = e - s_start[seg];
+      const uint32_t lxly = (uint32_t)(s_len[seg][0] * s_len[seg][1]);
+      // (a divisor of 1 has no 32-bit magic: 2^32 does not fit)
+      const int z = lxly == 1 ? v : (int)__umulhi((uint32_t)v, s_mg[seg][1]);
+      const int r = v - z * (int)lxly;
+      const int y = s_len[seg][0] == 1 ? r : (int)__umulhi((uint32_t)r, s_mg[seg][0]);
+      const int x = r - y * s_len[seg][0];
+      doff[q] = g.voxel_offset(s_l0[seg][2] + z, s_l0[seg][1] + y, s_l0[seg][0] + x);
+      const int mode = s_mode[seg];
+      if (mode == 1) {
+        const T* src = pool + (int64_t)s_nslot[seg] * g.brick_elems +
+                       g.voxel_offset(s_src[seg][2] + z, s_src[seg][1] + y, s_src[seg][0] + x);
+#pragma unroll
+        for (int c = 0; c < kMaxC; ++c) val[q][c] = c < C ? src[c] : (T)0;
+      } else {
+#pragma unroll
+        for (int c = 0; c < kMaxC; ++c) val[q][c] = mode == 2 ? (T)s_avg[seg][c] : (T)g.bg;
+      }
     }
+#pragma unroll
+    for (int q = 0; q < K; ++q)
+      if (live[q])
+        for (int c = 0; c < C; ++c) dst[doff[q] + c] = val[q][c];
   }
 }
 

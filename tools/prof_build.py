@@ -36,6 +36,10 @@ for rep in range(2):
     a = time.perf_counter()
     tree.sync()
     tsync = time.perf_counter() - a
+    if os.environ.get("PROF_BORDERS", "0") == "1":
+        tree.finalize()
+        tree.fill_borders()
+        tree.sync()
     pr.disable()
     t1 = time.perf_counter()
     print(f"rep {rep}: total {1e3*(t1-t0):.1f} ms  inserts {1e3*tins:.1f} ms  final sync {1e3*tsync:.1f} ms")
