@@ -115,8 +115,9 @@ vt_status vt_tree_signal_stream(vt_tree* tree, void* stream);
  * one call with the caller-stream ordering of a device block (wait on
  * caller_stream before reading it, make caller_stream wait for the reads;
  * a null caller_stream is the legacy default stream)
- * and the first `cap` pending change events copied out; *n_events = how
- * many were pending (the rest stay for vt_tree_take_events) */
+ * and the pending change events copied out when they fit in `cap`;
+ * *n_events = how many were pending (more than cap: none copied, take them
+ * with vt_tree_take_events) */
 vt_status vt_tree_insert_ev(vt_tree* tree, int32_t channel, const int32_t origin[3],
                             const int32_t dims[3], const void* samples, int32_t mem_kind,
                             void* caller_stream, int32_t* kinds, int64_t* indices, int64_t cap,

@@ -152,12 +152,12 @@ vt_status vt_tree_insert_ev(vt_tree* tree, int32_t channel, const int32_t origin
     }
     auto& ev = t.events;
     *n_events = (int64_t)ev.size();
-    const int64_t m = std::min<int64_t>(cap, (int64_t)ev.size());
-    for (int64_t i = 0; i < m; ++i) {
+    if ((int64_t)ev.size() > cap) return;  // too many: the caller takes them all at once
+    for (size_t i = 0; i < ev.size(); ++i) {
       kinds[i] = ev[i].first;
       indices[i] = ev[i].second;
     }
-    ev.erase(ev.begin(), ev.begin() + m);
+    ev.clear();
   });
 }
 
@@ -175,7 +175,10 @@ vt_status vt_tree_take_events(vt_tree* tree, int32_t* kinds, int64_t* indices, i
       kinds[i] = ev[i].first;
       indices[i] = ev[i].second;
     }
-    ev.erase(ev.begin(), ev.begin() + m);
+    if (m == (int64_t)ev.size())
+      ev.clear();
+    else
+      ev.erase(ev.begin(), ev.begin() + m);
     *n = m;
     *more = ev.empty() ? 0 : 1;
   });

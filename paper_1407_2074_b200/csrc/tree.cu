@@ -616,6 +616,13 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
     create_skip_z0 = g0[2];
     create_skip_z1 = g1[2];
   }
+  if (dense) {
+    // the events and dirty lists of a whole-layer block: created nodes, then
+    // C reps of every touched node
+    const size_t nl = leaf_slots.size();
+    events.reserve(events.size() + nl * (2 + reps) + 64);
+    struct_dirty.reserve(struct_dirty.size() + nl * 2 + 64);
+  }
   auto* walk_scope = new ProfScope(prof, 1);
 
   // leaves (octree.py:351-360): descend, create, ensure brick, dirty box

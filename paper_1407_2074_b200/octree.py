@@ -299,13 +299,13 @@ class Octree:
                       ct.byref(n))
             total = int(n.value)
             if total > cap:
-                rk = np.empty(total - cap, np.int32)
-                ri = np.empty(total - cap, np.int64)
+                # more events than the guess: all of them in one take
+                kinds = np.empty(total, np.int32)
+                idx = np.empty(total, np.int64)
                 got, more = ct.c_int64(), ct.c_int32()
-                _lib.call("vt_tree_take_events", self._h, _lib.ptr(rk, ct.c_int32),
-                          _lib.ptr(ri, ct.c_int64), total - cap, ct.byref(got), ct.byref(more))
-                kinds, idx = np.concatenate([kinds, rk]), np.concatenate([idx, ri])
-                self._ev_cap = 1 << (total - 1).bit_length()
+                _lib.call("vt_tree_take_events", self._h, _lib.ptr(kinds, ct.c_int32),
+                          _lib.ptr(idx, ct.c_int64), total, ct.byref(got), ct.byref(more))
+                self._ev_cap = min(1 << 20, 1 << (total - 1).bit_length())
             else:
                 kinds, idx = kinds[:total], idx[:total]
             del keep  # device blocks: the caller's stream waits for our reads
