@@ -103,9 +103,11 @@ struct RayOut {
   double mip[kMaxC];
 };
 
+// per-thread (per-ray) counts fit 32 bits (a ray takes at most a few
+// thousand samples); warp sums go to 64-bit device counters
 struct Counters {
-  long long samples, tf, avgfb, coarse, req, used;
-  long long skipped;  // samples accounted by the empty-space skip (not computed)
+  int samples, tf, avgfb, coarse, req, used;
+  int skipped;  // samples accounted by the empty-space skip (not computed)
 };
 
 __device__ __forceinline__ double clampd(double v, double lo, double hi) {
@@ -778,7 +780,7 @@ __device__ void finalize(const TFTable& T, const RayOut& o, double px[4], Counte
 }
 
 __device__ void warp_add_counters(const Counters& c, unsigned long long* out) {
-  long long v[7] = {c.samples, c.tf, c.avgfb, c.coarse, c.req, c.used, c.skipped};
+  const long long v[7] = {c.samples, c.tf, c.avgfb, c.coarse, c.req, c.used, c.skipped};
 #pragma unroll
   for (int i = 0; i < 7; ++i) {
     long long x = v[i];
@@ -839,10 +841,10 @@ __device__ __forceinline__ void march_ray(S& s, const TFTable& tf, const double 
       // transparent (TF alpha exactly 0): compositing is a no-op; account
       // this sample and the provably transparent run after it
       const long long m = s.skip_count(k, n, t0, d);
-      cnt.samples += m;
-      cnt.skipped += m;
-      cnt.tf += (m + 1) * NC;
-      if (s.hint == 1) cnt.used += m;
+      cnt.samples += (int)m;
+      cnt.skipped += (int)m;
+      cnt.tf += (int)(m + 1) * NC;
+      if (s.hint == 1) cnt.used += (int)m;
       k += m;
       continue;
     }
@@ -964,10 +966,10 @@ __global__ void __launch_bounds__(128) k_rays_march(RayState S,
         }
         if (s.hint) {
           const long long m = s.skip_count(k, n, t0, d);
-          cnt.samples += m;
-          cnt.skipped += m;
-          cnt.tf += (m + 1) * NC;
-          if (s.hint == 1) cnt.used += m;
+          cnt.samples += (int)m;
+          cnt.skipped += (int)m;
+          cnt.tf += (int)(m + 1) * NC;
+          if (s.hint == 1) cnt.used += (int)m;
           k += m;
           continue;
         }
