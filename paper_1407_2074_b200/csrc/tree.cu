@@ -12,6 +12,8 @@
 // and batched across insertions until something reads the tree.  With
 // tau > 0 it runs per insertion, followed by a stats gather and the exact
 // reference prune (octree.py:456-493).
+#include <memory>
+
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -71,7 +73,8 @@ static void build_geo(const vt_tree_desc& d, Geo& g) {
 
 namespace {
 uint8_t* pinned_get(size_t& cap);
-}
+
+}  // namespace
 
 Tree::Tree(const vt_tree_desc& d) {
   if (const char* e = std::getenv("VT_HOST_PROFILE")) prof.on = e[0] == '1';
@@ -149,6 +152,20 @@ Tree::Tree(const vt_tree_desc& d) {
   pend_slot.assign(cap, -1);
   VT_CUDA(cudaEventCreate(&ev0));
   VT_CUDA(cudaEventCreate(&ev1));
+  {
+    // highest priority: its few CTAs are scheduled as leaf-kernel CTAs retire
+    int lo = 0, hi = 0;
+    VT_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    VT_CUDA(cudaStreamCreateWithPriority(&aux, cudaStreamNonBlocking, hi));
+  }
+  VT_CUDA(cudaEventCreateWithFlags(&ev_pre, cudaEventDisableTiming));
+  VT_CUDA(cudaEventCreateWithFlags(&ev_aux, cudaEventDisableTiming));
+  if (tau == 0 && dense_enabled) {
+    // fused level-1 accumulators of the dense build, allocated up front
+    VT_CUDA(cudaMalloc(&d_nsum, g.capacity * g.C * sizeof(unsigned long long)));
+    VT_CUDA(cudaMalloc(&d_nmin, g.capacity * g.C * sizeof(int32_t)));
+    VT_CUDA(cudaMalloc(&d_nmax, g.capacity * g.C * sizeof(int32_t)));
+  }
   int64_t reserve = d.reserve_slots > 0 ? d.reserve_slots : 64;
   ensure_pool(reserve);
 }
@@ -184,8 +201,14 @@ void pinned_put(uint8_t* p, size_t cap) {
 
 void* Tree::stage_copy(const void* src, size_t bytes) const {
   const size_t need = (bytes + 255) & ~(size_t)255;
-  if (need > stage.cap) {
+  // ring readers may sit on the tree stream and the side stream
+  auto drain = [&] {
     VT_CUDA(cudaStreamSynchronize(stream));
+    if (main_saved) VT_CUDA(cudaStreamSynchronize(main_saved));
+    if (aux && aux != stream) VT_CUDA(cudaStreamSynchronize(aux));
+  };
+  if (need > stage.cap) {
+    drain();
     pinned_put(stage.h, stage.cap);
     if (stage.d) cudaFree(stage.d);
     stage.h = nullptr;
@@ -197,7 +220,7 @@ void* Tree::stage_copy(const void* src, size_t bytes) const {
     stage.head = 0;
   } else if (stage.head + need > stage.cap) {
     // wrap: every earlier copy (and kernel reading the ring) must be done
-    VT_CUDA(cudaStreamSynchronize(stream));
+    drain();
     stage.head = 0;
   }
   uint8_t* h = stage.h + stage.head;
@@ -211,10 +234,12 @@ void* Tree::stage_copy(const void* src, size_t bytes) const {
 Tree::~Tree() {
   if (prof.on) {
     std::fprintf(stderr, "[vtx host profile ms]");
-    for (int i = 0; i < 12; ++i) std::fprintf(stderr, " %s=%.2f", HostProf::name(i), prof.t[i]);
+    for (int i = 0; i < HostProf::kN; ++i) std::fprintf(stderr, " %s=%.2f", HostProf::name(i), prof.t[i]);
     std::fprintf(stderr, "\n");
   }
   if (stream) cudaStreamSynchronize(stream);
+  for (auto& e : prof.ev)
+    if (e) cudaEventDestroy(e);
   pinned_put(stage.h, stage.cap);
   if (stage.d) cudaFree(stage.d);
   cudaFree(d_pool);
@@ -232,6 +257,12 @@ Tree::~Tree() {
   if (ev1) cudaEventDestroy(ev1);
   if (ev_wait) cudaEventDestroy(ev_wait);
   if (ev_signal) cudaEventDestroy(ev_signal);
+  if (ev_pre) cudaEventDestroy(ev_pre);
+  if (ev_aux) cudaEventDestroy(ev_aux);
+  if (aux) {
+    cudaStreamSynchronize(aux);
+    cudaStreamDestroy(aux);
+  }
   if (own_stream && stream) cudaStreamDestroy(stream);
 }
 
@@ -289,20 +320,25 @@ void Tree::clear_seed_of() {
   seed_marked.clear();
 }
 
-// ascending sort of node indices (< 2^32): two 16-bit LSD radix passes for
-// large lists (a whole slab's leaves), std::sort otherwise
+// ascending sort of node indices: LSD radix on 8-bit digits over the bits
+// the maximum needs (two passes below 65,536 nodes) for large lists (a whole
+// slab's leaves), std::sort otherwise
 void sort_indices(std::vector<int64_t>& v) {
   if (v.size() < 2048) {
     std::sort(v.begin(), v.end());
     return;
   }
-  std::vector<int64_t> tmp(v.size());
-  for (int pass = 0; pass < 2; ++pass) {
-    const int sh = 16 * pass;
-    std::vector<uint32_t> cnt(65537, 0);
-    for (int64_t x : v) ++cnt[((x >> sh) & 0xFFFF) + 1];
-    for (int i = 0; i < 65536; ++i) cnt[i + 1] += cnt[i];
-    for (int64_t x : v) tmp[cnt[(x >> sh) & 0xFFFF]++] = x;
+  int64_t mx = 0;
+  for (int64_t x : v) mx = std::max(mx, x);
+  int bits = 0;
+  while (bits < 63 && (mx >> bits)) bits += 8;
+  static thread_local std::vector<int64_t> tmp;
+  tmp.resize(v.size());
+  for (int sh = 0; sh < bits; sh += 8) {
+    uint32_t cnt[257] = {0};
+    for (int64_t x : v) ++cnt[((x >> sh) & 0xFF) + 1];
+    for (int i = 0; i < 256; ++i) cnt[i + 1] += cnt[i];
+    for (int64_t x : v) tmp[cnt[(x >> sh) & 0xFF]++] = x;
     v.swap(tmp);
   }
 }
@@ -451,6 +487,12 @@ void Tree::insert(int channel, const int origin[3], const int dims[3], const voi
   const int64_t nvox = (int64_t)dims[0] * dims[1] * dims[2];
   VT_CUDA(cudaSetDevice(device));
   const int nch = channel < 0 ? g.C : 1;
+  if (prof.on) {
+    for (auto& e : prof.ev)
+      if (!e) VT_CUDA(cudaEventCreate(&e));
+    VT_CUDA(cudaEventRecord(prof.ev[0], stream));
+    prof.ev_armed = false;
+  }
   if (nvox == 0) {
     // an empty block touches nothing: the reference still emits no events
     return;
@@ -474,6 +516,18 @@ void Tree::insert(int channel, const int origin[3], const int dims[3], const voi
     insert_staged(-1, origin, dims, dsrc, g.C, 0, g.C);
   }
   if (staged) release(*this, staged);
+  if (prof.on && prof.ev_armed) {
+    // device-side split of this insertion (profiling only: synchronises)
+    VT_CUDA(cudaEventRecord(prof.ev[3], stream));
+    VT_CUDA(cudaEventSynchronize(prof.ev[3]));
+    float a = 0, b = 0, c = 0;
+    cudaEventElapsedTime(&a, prof.ev[0], prof.ev[1]);
+    cudaEventElapsedTime(&b, prof.ev[1], prof.ev[2]);
+    cudaEventElapsedTime(&c, prof.ev[2], prof.ev[3]);
+    prof.t[20] += a;
+    prof.t[21] += b;
+    prof.t[22] += c;
+  }
   if (mem_kind == VT_MEM_HOST) {
     // a pinned source is read asynchronously: keep the borrow contract
     cudaPointerAttributes attr{};
@@ -512,11 +566,16 @@ bool Tree::dense_eligible(int channel, const int origin[3], const int dims[3], c
 void Tree::insert_staged(int channel, const int origin[3], const int dims[3], const void* dsrc,
                          int src_stride, int src_off, int reps) {
   const int64_t nvox = (int64_t)dims[0] * dims[1] * dims[2];
-  if (try_defer(channel, origin, dims, dsrc, src_stride, src_off)) return;
+  {
+    ProfScope qd(prof, 18);
+    if (try_defer(channel, origin, dims, dsrc, src_stride, src_off)) return;
+  }
   const bool starting = defer_start;  // this insertion opens a deferred layer
   defer_start = false;
   ++data_version;
+  ProfScope* qel = new ProfScope(prof, 23);
   const bool dense = dense_eligible(channel, origin, dims, dsrc, src_stride, src_off);
+  delete qel;
   std::vector<DenseJob> djobs;
   creates.clear();
   seeds.clear();
@@ -542,6 +601,7 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
   int launch_result = 0;
   if (early) {
     ProfScope q(prof, 7);
+    ProfScope qe(prof, 12);
     const int64_t cur0 = cursor;
     const int64_t nleaves = (int64_t)gn[0] * gn[1] * gn[2];
     djobs.reserve(nleaves);
@@ -549,15 +609,24 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
       for (int gy = g0[1]; gy <= g1[1]; ++gy)
         for (int gx = g0[0]; gx <= g1[0]; ++gx)
           djobs.push_back({leaf_index(gx, gy, gz), (int32_t)(cur0 + (int64_t)djobs.size()), -1});
+    ProfScope* qpp = new ProfScope(prof, 24);
     if (g.depth >= 1 && g.split[0] && g.split[1] && g.split[2]) {
       struct P1 { int64_t idx; int px, py, pz; };
-      std::vector<P1> par;
+      std::vector<int64_t> pidx;
       const int64_t base1 = g.level_start[g.depth - 1];
       for (int pz = g0[2] >> 1; pz <= g1[2] >> 1; ++pz)
         for (int py = 0; py <= g1[1] >> 1; ++py)
           for (int px = 0; px <= g1[0] >> 1; ++px)
-            par.push_back({base1 + morton[0][px] + morton[1][py] + morton[2][pz], px, py, pz});
-      std::sort(par.begin(), par.end(), [](const P1& a, const P1& b) { return a.idx < b.idx; });
+            pidx.push_back(morton[0][px] + morton[1][py] + morton[2][pz]);
+      sort_indices(pidx);
+      std::vector<P1> par(pidx.size());
+      for (size_t i = 0; i < pidx.size(); ++i) {
+        // all three axes split: bit 3b + a of the Morton code is bit b of axis a
+        int c[3] = {0, 0, 0};
+        for (int b = 0; b < g.depth - 1; ++b)
+          for (int a = 0; a < 3; ++a) c[a] |= (int)((pidx[i] >> (3 * b + a)) & 1) << b;
+        par[i] = {base1 + pidx[i], c[0], c[1], c[2]};
+      }
       int64_t next = cur0 + nleaves;
       for (const P1& q1 : par) {
         if (flags[q1.idx] & NF_BRICK) continue;  // existing brick: no new slot
@@ -576,6 +645,8 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
         fused_slots.push_back(ps);
       }
     }
+    delete qpp;
+    ProfScope* qpa = new ProfScope(prof, 25);
     // every slot this insertion can allocate exists before the kernel runs:
     // the block's leaves plus every ancestor its leaves can touch
     int64_t nanc = 0;
@@ -591,7 +662,11 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
           for (int x = lo[0]; x <= hi[0]; ++x)
             if (!(flags[base + morton[0][x] + morton[1][y] + morton[2][z]] & NF_BRICK)) ++nanc;
     }
-    ensure_pool(cur0 + nleaves + nanc);
+    delete qpa;
+    {
+      ProfScope qp(prof, 19);
+      ensure_pool(cur0 + nleaves + nanc);
+    }
     if (!fused_nodes.empty() && !d_nsum) {
       VT_CUDA(cudaMalloc(&d_nsum, g.capacity * g.C * sizeof(unsigned long long)));
       VT_CUDA(cudaMalloc(&d_nmin, g.capacity * g.C * sizeof(int32_t)));
@@ -608,8 +683,14 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
     const bool want = prefill_enabled && !borders;
     {
       ProfScope q3(prof, 11);
+      if (prof.on) VT_CUDA(cudaEventRecord(prof.ev[1], stream));
+      VT_CUDA(cudaEventRecord(ev_pre, stream));
       launch_result = launch_dense_leaf(*this, dsrc, nvox * src_stride, origin[2], want ? 1 : 0,
                                         dj, (int)djobs.size(), gn, g0[2]);
+      if (prof.on) {
+        VT_CUDA(cudaEventRecord(prof.ev[2], stream));
+        prof.ev_armed = true;
+      }
     }
     release(*this, dj);
     // chain creation below must not seed the statistics the kernel writes
@@ -708,14 +789,18 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
   for (int lvl = 1; lvl <= g.depth; ++lvl) {
     std::vector<int64_t>& par = touched[lvl];
     ++anc_gen;
-    for (int64_t c : touched[lvl - 1]) {
-      const int64_t q = (c - 1) >> 3;
-      if (anc_mark[q] != anc_gen) {
-        anc_mark[q] = anc_gen;
-        par.push_back(q);
+    {
+      ProfScope qa(prof, 13);
+      for (int64_t c : touched[lvl - 1]) {
+        const int64_t q = (c - 1) >> 3;
+        if (anc_mark[q] != anc_gen) {
+          anc_mark[q] = anc_gen;
+          par.push_back(q);
+        }
       }
+      std::sort(par.begin(), par.end());
     }
-    std::sort(par.begin(), par.end());
+    ProfScope qb(prof, 14);
     for (int64_t p : par) {
       bool fresh = ensure_brick(p);
       if (fresh) {
@@ -763,13 +848,40 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
       fused_nodes.push_back(p);
     }
   }
-  sort_indices(touched[0]);
+  {
+    ProfScope qs(prof, 15);
+    sort_indices(touched[0]);
+  }
   has_pending = true;
   delete anc_scope;
   delete walk_scope;
   ProfScope enq_scope(prof, 2);
 
-  // device pre-work for this insertion
+  // device pre-work for this insertion; behind an early dense launch it goes
+  // to the side stream (ordered after everything before the leaf kernel) so
+  // it runs alongside the leaf kernel rather than after it
+  struct SideJoin {
+    Tree& t;
+    bool on;
+    ~SideJoin() {  // back to the tree stream, which waits for the side work
+      if (!on) return;
+      t.stream = t.main_saved;
+      t.main_saved = nullptr;
+      cudaEventRecord(t.ev_aux, t.aux);
+      cudaStreamWaitEvent(t.stream, t.ev_aux, 0);
+    }
+  };
+  static const bool side_on = [] {
+    const char* e = std::getenv("VT_SIDE_STREAM");
+    return !(e && e[0] == '0');
+  }();
+  const bool side = side_on && early && (launch_result & kLeafTma) && aux;
+  if (side) {
+    VT_CUDA(cudaStreamWaitEvent(aux, ev_pre, 0));
+    main_saved = stream;
+    stream = aux;
+  }
+  std::unique_ptr<SideJoin> side_join(new SideJoin{*this, side});
   { ProfScope q(prof, 5); flush_structure(); }
   CreateJob* dc;
   SeedJob* ds;
@@ -788,6 +900,7 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
     ds = upload(*this, seeds);
     launch_seed(*this, ds, (int)seeds.size());
   }
+  side_join.reset();
   int32_t* dlp = nullptr;
   if (dense) {
     ProfScope q(prof, 7);
@@ -817,11 +930,12 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
     }
     // host bookkeeping overlaps the device work: pending entries of leaves
     // whose statistics the kernel writes outright
+    ProfScope qd(prof, 16);
     pend_nodes[0].reserve(pend_nodes[0].size() + djobs.size());
-    for (const DenseJob& jd : djobs) {
-      pend_dense(jd.node);
-      complete[jd.node] = 1;
-    }
+    // touched[0] holds the same leaves, already in BFS order: propagate
+    // then finds the list sorted
+    for (int64_t n : touched[0]) pend_dense(n);
+    for (const DenseJob& jd : djobs) complete[jd.node] = 1;
     ++dense_leaf_inserts;
     if (prefilled) {
       // z-shell planes whose block plane lies outside this insertion are owed
@@ -885,12 +999,17 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
   // NODE_UPDATED for every touched, non-deleted node, sorted (octree.py:393-395)
   // every level's list is sorted and unique and higher levels hold smaller
   // BFS indices, so root-first concatenation is the sorted union
+  ProfScope qu(prof, 17);
   std::vector<int64_t> upd;
   for (int lvl = g.depth; lvl >= 0; --lvl) upd.insert(upd.end(), touched[lvl].begin(), touched[lvl].end());
   events.reserve(events.size() + upd.size() * reps);
-  for (int r = 0; r < reps; ++r)
-    for (int64_t i : upd)
-      if (flags[i] & NF_EXISTS) events.emplace_back(VT_EV_UPDATED, i);
+  const size_t ev0 = events.size();
+  for (int64_t i : upd)
+    if (flags[i] & NF_EXISTS) events.emplace_back(VT_EV_UPDATED, i);
+  const size_t ev1 = events.size(), nev = ev1 - ev0;
+  events.resize(ev1 + nev * (reps - 1));
+  for (int r = 1; r < reps; ++r)
+    std::copy(events.begin() + ev0, events.begin() + ev1, events.begin() + ev0 + r * nev);
   if (starting) {
     dl.upd = upd;  // every later block of the layer touches the same nodes
     if (dl.remaining == 0) finish_layer();
@@ -1023,7 +1142,7 @@ void Tree::propagate() {
   for (int lvl = 0; lvl <= g.depth; ++lvl) {
     std::vector<int64_t>& nodes = pend_nodes[lvl];
     if (nodes.empty()) continue;
-    sort_indices(nodes);
+    if (!std::is_sorted(nodes.begin(), nodes.end())) sort_indices(nodes);
     std::vector<OctJob> oct;
     std::vector<int64_t> dense_nodes, fused_done;
     if (lvl > 0) {

@@ -55,10 +55,17 @@ struct Pending {
 // tree is destroyed
 struct HostProf {
   bool on = false;
-  double t[12] = {0};
+  static constexpr int kN = 26;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // insert entry, leaf launch, leaf end, insert end
+  bool ev_armed = false;
+  double t[kN] = {0};
   static const char* name(int i) {
-    static const char* n[12] = {"insert", "walk", "enqueue", "events", "propagate", "flush_struct",
-                                "seed", "scatter", "leaves", "ancestors", "prop_build", "prop_launch"};
+    static const char* n[kN] = {"insert", "walk", "enqueue", "events", "propagate", "flush_struct",
+                                "seed", "scatter", "leaves", "ancestors", "prop_build", "prop_launch",
+                                "early_pre", "anc_collect", "anc_brick", "sort_leaves",
+                                "dense_book", "updated_ev", "defer", "pool",
+                                "gpu_entry_to_leaf", "gpu_leaf", "gpu_leaf_to_end",
+                                "eligible", "pre_parents", "pre_anc"};
     return n[i];
   }
 };
@@ -226,6 +233,12 @@ struct Tree {
 
   // timing of the last build flush (CUDA events)
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // side stream for the small structure kernels of an early dense launch
+  // (flags/slots, chain creation, ancestor shells): they overlap the leaf
+  // kernel instead of queueing behind it; the main stream joins right after
+  cudaStream_t aux = nullptr;
+  cudaStream_t main_saved = nullptr;  // the tree stream while `stream` is aux
+  cudaEvent_t ev_pre = nullptr, ev_aux = nullptr;
   cudaEvent_t ev_wait = nullptr;    // cross-stream ordering (vt_tree_wait_stream)
   cudaEvent_t ev_signal = nullptr;  // (vt_tree_signal_stream)
   double last_build_ms = 0, last_render_ms = 0;

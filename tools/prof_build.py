@@ -3,6 +3,7 @@ import cProfile
 import ctypes as ct
 import os
 import pstats
+import resource
 import sys
 import time
 
@@ -11,6 +12,10 @@ import torch  # noqa: E402
 
 from paper_1407_2074_b200 import BrickPoolConfig, Octree, VolumeDescriptor, _lib  # noqa: E402
 
+if os.environ.get("PROF_MALLOPT", "0") == "1":
+    libc = ct.CDLL("libc.so.6")
+    libc.mallopt(-3, 32 << 20)   # M_MMAP_THRESHOLD
+    libc.mallopt(-1, 512 << 20)  # M_TRIM_THRESHOLD
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
 SLAB = int(sys.argv[2]) if len(sys.argv) > 2 else 32
 dims = (N, N, N)
@@ -29,10 +34,12 @@ for rep in range(2):
     t0 = time.perf_counter()
     pr.enable()
     tins = 0.0
+    f0 = resource.getrusage(resource.RUSAGE_SELF).ru_minflt
     for z0 in range(0, N, SLAB):
         a = time.perf_counter()
         tree.insert_channels((0, 0, z0), vol[z0:z0 + SLAB])
         tins += time.perf_counter() - a
+    print(f"minor faults during inserts: {resource.getrusage(resource.RUSAGE_SELF).ru_minflt - f0}")
     a = time.perf_counter()
     tree.sync()
     tsync = time.perf_counter() - a
