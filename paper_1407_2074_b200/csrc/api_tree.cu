@@ -154,8 +154,8 @@ vt_status vt_tree_insert_ev(vt_tree* tree, int32_t channel, const int32_t origin
     *n_events = (int64_t)ev.size();
     if ((int64_t)ev.size() > cap) return;  // too many: the caller takes them all at once
     for (size_t i = 0; i < ev.size(); ++i) {
-      kinds[i] = ev[i].first;
-      indices[i] = ev[i].second;
+      kinds[i] = Tree::ev_kind(ev[i]);
+      indices[i] = Tree::ev_index(ev[i]);
     }
     ev.clear();
   });
@@ -172,8 +172,8 @@ vt_status vt_tree_take_events(vt_tree* tree, int32_t* kinds, int64_t* indices, i
     auto& ev = tree->t.events;
     int64_t m = std::min<int64_t>(cap, (int64_t)ev.size());
     for (int64_t i = 0; i < m; ++i) {
-      kinds[i] = ev[i].first;
-      indices[i] = ev[i].second;
+      kinds[i] = Tree::ev_kind(ev[i]);
+      indices[i] = Tree::ev_index(ev[i]);
     }
     if (m == (int64_t)ev.size())
       ev.clear();

@@ -389,7 +389,7 @@ void Tree::ensure_children(int64_t p) {
     if (seed_of[c] < 0) seed_marked.push_back(c);
     seed_of[c] = src;
     ++node_count;
-    events.emplace_back(VT_EV_CREATED, c);
+    events.push_back(ev_pack(VT_EV_CREATED, c));
   }
 }
 
@@ -576,7 +576,10 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
   ProfScope* qel = new ProfScope(prof, 23);
   const bool dense = dense_eligible(channel, origin, dims, dsrc, src_stride, src_off);
   delete qel;
-  std::vector<DenseJob> djobs;
+  // per-thread scratch: a whole-volume job table is ~0.5 MB, and a fresh
+  // allocation of it page-faults on first touch every insertion
+  static thread_local std::vector<DenseJob> djobs;
+  djobs.clear();
   creates.clear();
   seeds.clear();
   clear_seed_of();
@@ -587,9 +590,13 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
     g1[a] = (origin[a] + dims[a] - 1) / M[a];
     gn[a] = g1[a] - g0[a] + 1;
   }
-  std::vector<int32_t> leaf_slots((size_t)gn[0] * gn[1] * gn[2]);
-  std::vector<std::vector<int64_t>> touched(g.depth + 1);
-  touched[0].reserve(leaf_slots.size());
+  const size_t nblock = (size_t)gn[0] * gn[1] * gn[2];
+  // brick slot per block leaf (general path only)
+  std::vector<int32_t> leaf_slots(dense ? 0 : nblock);
+  static thread_local std::vector<std::vector<int64_t>> touched;  // scratch, as djobs
+  touched.resize(g.depth + 1);
+  for (auto& v : touched) v.clear();
+  touched[0].reserve(nblock);
   std::vector<int32_t> fused_slots;
   std::vector<int64_t> fused_nodes;
   // Dense early launch: with no recycled slots the reference's allocation
@@ -604,11 +611,21 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
     ProfScope qe(prof, 12);
     const int64_t cur0 = cursor;
     const int64_t nleaves = (int64_t)gn[0] * gn[1] * gn[2];
-    djobs.reserve(nleaves);
-    for (int gz = g0[2]; gz <= g1[2]; ++gz)
-      for (int gy = g0[1]; gy <= g1[1]; ++gy)
-        for (int gx = g0[0]; gx <= g1[0]; ++gx)
-          djobs.push_back({leaf_index(gx, gy, gz), (int32_t)(cur0 + (int64_t)djobs.size()), -1});
+    ProfScope* qdj = new ProfScope(prof, 26);
+    djobs.resize(nleaves);
+    {
+      DenseJob* out = djobs.data();
+      int64_t i = 0;
+      for (int gz = g0[2]; gz <= g1[2]; ++gz) {
+        const int64_t mz = g.level_start[g.depth] + morton[2][gz];
+        for (int gy = g0[1]; gy <= g1[1]; ++gy) {
+          const int64_t myz = mz + morton[1][gy];
+          for (int gx = g0[0]; gx <= g1[0]; ++gx, ++i)
+            out[i] = {myz + morton[0][gx], (int32_t)(cur0 + i), -1};
+        }
+      }
+    }
+    delete qdj;
     ProfScope* qpp = new ProfScope(prof, 24);
     if (g.depth >= 1 && g.split[0] && g.split[1] && g.split[2]) {
       struct P1 { int64_t idx; int px, py, pz; };
@@ -628,6 +645,7 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
         par[i] = {base1 + pidx[i], c[0], c[1], c[2]};
       }
       int64_t next = cur0 + nleaves;
+      ProfScope qpd(prof, 27);
       for (const P1& q1 : par) {
         if (flags[q1.idx] & NF_BRICK) continue;  // existing brick: no new slot
         const int32_t ps = (int32_t)next++;
@@ -672,12 +690,15 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
       VT_CUDA(cudaMalloc(&d_nmin, g.capacity * g.C * sizeof(int32_t)));
       VT_CUDA(cudaMalloc(&d_nmax, g.capacity * g.C * sizeof(int32_t)));
     }
-    int64_t* dfn = upload(*this, fused_nodes);
-    launch_init_fused(*this, dfn, (int)fused_nodes.size());
-    release(*this, dfn);
+    {
+      ProfScope qf(prof, 28);
+      int64_t* dfn = upload(*this, fused_nodes);
+      launch_init_fused(*this, dfn, (int)fused_nodes.size());
+      release(*this, dfn);
+    }
     DenseJob* dj;
     {
-      ProfScope q2(prof, 10);
+      ProfScope q2(prof, 29);
       dj = upload(*this, djobs);
     }
     const bool want = prefill_enabled && !borders;
@@ -685,6 +706,7 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
       ProfScope q3(prof, 11);
       if (prof.on) VT_CUDA(cudaEventRecord(prof.ev[1], stream));
       VT_CUDA(cudaEventRecord(ev_pre, stream));
+      ProfScope qll(prof, 30);
       launch_result = launch_dense_leaf(*this, dsrc, nvox * src_stride, origin[2], want ? 1 : 0,
                                         dj, (int)djobs.size(), gn, g0[2]);
       if (prof.on) {
@@ -700,7 +722,7 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
   if (dense) {
     // the events and dirty lists of a whole-layer block: created nodes, then
     // C reps of every touched node
-    const size_t nl = leaf_slots.size();
+    const size_t nl = nblock;
     events.reserve(events.size() + nl * (2 + reps) + 64);
     struct_dirty.reserve(struct_dirty.size() + nl * 2 + 64);
   }
@@ -985,6 +1007,14 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
   release(*this, ds);
   release(*this, dlp);
   inserted += nvox * reps;
+  if (early && tau == 0 && origin[0] == 0 && origin[1] == 0 && origin[2] == 0 &&
+      dims[0] == g.dims[0] && dims[1] == g.dims[1] && dims[2] == g.dims[2]) {
+    // the whole volume in one dense insertion: no later block of a batch can
+    // share these parents, so the pyramid is queued now, right behind the
+    // leaf kernel, instead of at the next flush (the host work overlaps the
+    // leaf kernel; the result is the one flush would compute)
+    propagate();
+  }
 
   std::vector<char> dmark;
   std::vector<int64_t> deleted;
@@ -1000,12 +1030,13 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
   // every level's list is sorted and unique and higher levels hold smaller
   // BFS indices, so root-first concatenation is the sorted union
   ProfScope qu(prof, 17);
-  std::vector<int64_t> upd;
+  static thread_local std::vector<int64_t> upd;
+  upd.clear();
   for (int lvl = g.depth; lvl >= 0; --lvl) upd.insert(upd.end(), touched[lvl].begin(), touched[lvl].end());
   events.reserve(events.size() + upd.size() * reps);
   const size_t ev0 = events.size();
   for (int64_t i : upd)
-    if (flags[i] & NF_EXISTS) events.emplace_back(VT_EV_UPDATED, i);
+    if (flags[i] & NF_EXISTS) events.push_back(ev_pack(VT_EV_UPDATED, i));
   const size_t ev1 = events.size(), nev = ev1 - ev0;
   events.resize(ev1 + nev * (reps - 1));
   for (int r = 1; r < reps; ++r)
@@ -1038,7 +1069,7 @@ bool Tree::try_defer(int channel, const int origin[3], const int dims[3], const 
       ++data_version;
       defer_copy(channel, origin, dims, dsrc);
       events.reserve(events.size() + dl.upd.size());
-      for (int64_t i : dl.upd) events.emplace_back(VT_EV_UPDATED, i);
+      for (int64_t i : dl.upd) events.push_back(ev_pack(VT_EV_UPDATED, i));
       inserted += nvox;
       if (dl.remaining == 0) finish_layer();
       return true;
@@ -1344,7 +1375,7 @@ void Tree::delete_below(int64_t p, std::vector<char>& mark, std::vector<int64_t>
     slot[c] = -1;
     mark_struct(c);
     deleted.push_back(c);
-    events.emplace_back(VT_EV_DELETED, c);
+    events.push_back(ev_pack(VT_EV_DELETED, c));
   }
   flags[p] &= ~NF_CHILDREN;
   mark_struct(p);
@@ -1418,7 +1449,7 @@ void Tree::fill_borders() {
   BorderJob* d = upload(*this, jobs);
   launch_borders(*this, d, (int)jobs.size());
   release(*this, d);
-  for (int64_t i : bricks) events.emplace_back(VT_EV_UPDATED, i);
+  for (int64_t i : bricks) events.push_back(ev_pack(VT_EV_UPDATED, i));
   borders = true;
   halo_prefill = false;
   owed_lo.clear();

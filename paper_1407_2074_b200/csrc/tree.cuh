@@ -55,7 +55,7 @@ struct Pending {
 // tree is destroyed
 struct HostProf {
   bool on = false;
-  static constexpr int kN = 26;
+  static constexpr int kN = 31;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // insert entry, leaf launch, leaf end, insert end
   bool ev_armed = false;
   double t[kN] = {0};
@@ -65,7 +65,8 @@ struct HostProf {
                                 "early_pre", "anc_collect", "anc_brick", "sort_leaves",
                                 "dense_book", "updated_ev", "defer", "pool",
                                 "gpu_entry_to_leaf", "gpu_leaf", "gpu_leaf_to_end",
-                                "eligible", "pre_parents", "pre_anc"};
+                                "eligible", "pre_parents", "pre_anc", "pre_djobs",
+                                "pre_pads", "pre_fused_up", "pre_djob_up", "pre_leaf_launch"};
     return n[i];
   }
 };
@@ -170,7 +171,14 @@ struct Tree {
   std::vector<int32_t> h_stats;
 
   // -- events (octree.py:41-50) --
-  std::vector<std::pair<int32_t, int64_t>> events;
+  // packed (kind << 56 | node index): 8 bytes per event, a whole-volume
+  // insertion emits ~4 per node
+  std::vector<uint64_t> events;
+  static uint64_t ev_pack(int32_t kind, int64_t idx) {
+    return ((uint64_t)(uint32_t)kind << 56) | (uint64_t)idx;
+  }
+  static int32_t ev_kind(uint64_t e) { return (int32_t)(e >> 56); }
+  static int64_t ev_index(uint64_t e) { return (int64_t)(e & ((1ULL << 56) - 1)); }
 
   // -- deferred propagation (tau == 0 batches; tau > 0 per insertion) --
   // dirty nodes per level: pend_nodes[lvl] lists them, pend_slot[node]
