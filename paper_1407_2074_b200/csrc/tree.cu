@@ -919,6 +919,17 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
       for (const SeedJob& sj : seeds) (g.level_of(sj.node) == 0 ? dl.seeds : now).push_back(sj);
       seeds.swap(now);
     }
+    if (early && prefill_enabled && !borders) {
+      size_t w = 0;
+      for (const SeedJob& sj : seeds) {
+        bool full = g.level_of(sj.node) > 0;
+        for (int a = 0; a < 3; ++a)
+          full = full && sj.cov_lo[a] == 0 && sj.cov_hi[a] == M[a];
+        if (full) owed_shells.push_back(sj.slot);
+        else seeds[w++] = sj;
+      }
+      seeds.resize(w);
+    }
     ds = upload(*this, seeds);
     launch_seed(*this, ds, (int)seeds.size());
   }
@@ -1014,6 +1025,20 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
     // leaf kernel, instead of at the next flush (the host work overlaps the
     // leaf kernel; the result is the one flush would compute)
     propagate();
+    if (halo_prefill && prefill_valid && owed_lo.empty() && owed_hi.empty() && !borders &&
+        complete[0]) {
+      // and the shells of every level > 0 brick, as fill_borders' fast path
+      // would write them (leaf shells came prefilled from the leaf kernel)
+      std::vector<BorderJob> bj;
+      for (int64_t i = 0; i < g.capacity; ++i)
+        if ((flags[i] & NF_EXISTS) && (flags[i] & NF_BRICK) && g.level_of(i) > 0)
+          bj.push_back({i, slot[i]});
+      BorderJob* d = upload(*this, bj);
+      launch_borders(*this, d, (int)bj.size());
+      release(*this, d);
+      upper_borders = true;
+      owed_shells.clear();
+    }
   }
 
   std::vector<char> dmark;
@@ -1441,8 +1466,9 @@ void Tree::fill_borders() {
     int32_t* dp = upload(*this, pj);
     launch_plane_copy(*this, dp, (int)(pj.size() / 4));
     release(*this, dp);
-    for (int64_t i : bricks)
-      if (g.level_of(i) > 0) jobs.push_back({i, slot[i]});
+    if (!upper_borders)
+      for (int64_t i : bricks)
+        if (g.level_of(i) > 0) jobs.push_back({i, slot[i]});
   } else {
     for (int64_t i : bricks) jobs.push_back({i, slot[i]});
   }
@@ -1452,6 +1478,8 @@ void Tree::fill_borders() {
   for (int64_t i : bricks) events.push_back(ev_pack(VT_EV_UPDATED, i));
   borders = true;
   halo_prefill = false;
+  owed_shells.clear();  // every level > 0 brick's shell was just written
+  upper_borders = false;
   owed_lo.clear();
   owed_hi.clear();
 }
@@ -1460,12 +1488,17 @@ void Tree::fill_borders() {
 // any reader of pool shells first resets them (then fill_borders takes the
 // general path).
 void Tree::publish_halos() {
-  if (!halo_prefill || borders) return;
+  if ((!halo_prefill && owed_shells.empty() && !upper_borders) || borders) return;
   flush();
   std::vector<int32_t> sl;
-  for (int64_t i = 0; i < g.capacity; ++i)
-    if ((flags[i] & NF_EXISTS) && (flags[i] & NF_BRICK) && g.level_of(i) == 0)
-      sl.push_back(slot[i]);
+  if (halo_prefill || upper_borders)
+    for (int64_t i = 0; i < g.capacity; ++i)
+      if ((flags[i] & NF_EXISTS) && (flags[i] & NF_BRICK) &&
+          (g.level_of(i) == 0 ? halo_prefill : upper_borders))
+        sl.push_back(slot[i]);
+  upper_borders = false;
+  sl.insert(sl.end(), owed_shells.begin(), owed_shells.end());
+  owed_shells.clear();
   int32_t* d = upload(*this, sl);
   launch_clear_shells(*this, d, (int)sl.size());
   release(*this, d);

@@ -122,6 +122,15 @@ struct Tree {
   bool halo_prefill = false;     // some leaf shells hold prefilled values
   bool prefill_valid = true;     // no general-path mutation since (fast fill_borders)
   std::vector<int64_t> owed_lo, owed_hi;  // leaves whose z-shell plane awaits a neighbour
+  // fresh level >= 1 bricks of an early dense launch whose background shell
+  // is not written at insertion: fill_borders overwrites every shell voxel
+  // of those bricks anyway, and publish_halos() writes the background first
+  // if anything reads the pool before it
+  std::vector<int32_t> owed_shells;
+  // level > 0 shells already hold their fill_borders values (computed right
+  // after a whole-volume dense insertion, overlapping its host epilogue);
+  // logically background until fill_borders, as halo_prefill
+  bool upper_borders = false;
   void publish_halos();
 
   // Threshold-0 slice streams (ingest_stream's VSTR order: per z, one
