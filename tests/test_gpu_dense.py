@@ -195,6 +195,7 @@ PREFILL_CASES = {
     "cfg_like_slabs": ((64, 48, 40), 3, (8, 8, 8), 1, 0),
     "two_layer_slabs_bg": ((48, 40, 72), 2, (8, 8, 8), 2, 17),
     "bulk_partial": ((40, 36, 50), 3, (8, 8, 8), 100, 0),
+    "bulk_pow2_bg": ((64, 64, 64), 3, (8, 8, 8), 100, 5),
     "nonsplit_z": ((32, 16, 6), 3, (8, 8, 8), 1, 3),
     "brick16_c4": ((64, 32, 48), 4, (16, 16, 16), 1, 0),
 }
@@ -215,12 +216,16 @@ def test_dense_prefilled_shells_fast_borders(name, tmp_path):
     assert digest(tb, tmp_path, "b") == digest(ta, tmp_path, "a")
 
 
-def test_prefilled_shells_read_as_background_before_fill_borders(tmp_path):
+@pytest.mark.parametrize("dims,whole", [((32, 24, 40), False), ((32, 24, 40), True),
+                                        ((40, 36, 50), True), ((64, 64, 64), True)])
+def test_prefilled_shells_read_as_background_before_fill_borders(tmp_path, dims, whole):
     """Before fill_borders a prefilled shell is the reference's background to
-    every reader (read_brick, export, checksum, device mirror)."""
+    every reader (read_brick, export, checksum, device mirror).  A whole-volume
+    insertion also computes the parents' shells and owes their background
+    (Tree::upper_borders / owed_shells): the same contract."""
     from paper_1407_2074_b200 import DeviceState
-    dims, C, brick = (32, 24, 40), 3, (8, 8, 8)
-    ops = _slabs(dims, brick[2])
+    C, brick = 3, (8, 8, 8)
+    ops = [("slab", 0, dims[2])] if whole else _slabs(dims, brick[2])
     ta, _, _ = _run(dims, C, brick, "uint16", ops, dense=False)
     tb, _, _ = _run(dims, C, brick, "uint16", ops, dense=True)
     assert _bricks(tb) == _bricks(ta)
