@@ -808,15 +808,20 @@ __device__ __forceinline__ bool pixel_of(int& i, int& j, int& jl) {
 
 template <class T>
 __device__ void store_px(void* out, int kind, int64_t r, const double px[4]) {
+  // whole-pixel vector stores (the frame may be page-locked host memory
+  // written over PCIe, where narrow scattered stores are expensive)
   if (kind == 0) {
-    double* o = (double*)out + r * 4;
-    for (int a = 0; a < 4; ++a) o[a] = px[a];
+    double2* o = reinterpret_cast<double2*>((double*)out + r * 4);
+    o[0] = make_double2(px[0], px[1]);
+    o[1] = make_double2(px[2], px[3]);
   } else if (kind == 1) {
-    float* o = (float*)out + r * 4;
-    for (int a = 0; a < 4; ++a) o[a] = (float)px[a];
+    *reinterpret_cast<float4*>((float*)out + r * 4) =
+        make_float4((float)px[0], (float)px[1], (float)px[2], (float)px[3]);
   } else {
-    uint8_t* o = (uint8_t*)out + r * 4;
-    for (int a = 0; a < 4; ++a) o[a] = (uint8_t)npclip(rint(px[a] * 255.0), 0.0, 255.0);
+    uint32_t v = 0;
+    for (int a = 0; a < 4; ++a)
+      v |= (uint32_t)(uint8_t)npclip(rint(px[a] * 255.0), 0.0, 255.0) << (8 * a);
+    *reinterpret_cast<uint32_t*>((uint8_t*)out + r * 4) = v;
   }
 }
 
@@ -868,6 +873,8 @@ __global__ void __launch_bounds__(128, VT_RENDER_MINB) k_render_fullframe(const 
   Counters& cnt = s.cnt;
   int i, j, jl;
   bool active = pixel_of(i, j, jl);
+  bool write = false;
+  double px[4] = {0.0, 0.0, 0.0, 0.0};
   if (active) {
     double d[3];
     ray_dir(i, j, d);
@@ -879,13 +886,34 @@ __global__ void __launch_bounds__(128, VT_RENDER_MINB) k_render_fullframe(const 
     // one uniform branch per ray instead of a mode test per sample
     if (P.mip) march_ray<1>(s, tf, d, t0, n, o);
     else march_ray<0>(s, tf, d, t0, n, o);
-    double px[4];
     finalize<NC>(tf, o, px, cnt);
-    store_px<T>(out, out_kind, (int64_t)jl * out_w + (i - P.rect[0]), px);
+    write = true;
   } else if (P.n_parts > 1 && i < P.rect[2] && jl < out_rows) {
     // padding rows of the last strip: deterministic zeros
-    const double z[4] = {0.0, 0.0, 0.0, 0.0};
-    store_px<T>(out, out_kind, (int64_t)jl * out_w + (i - P.rect[0]), z);
+    write = true;
+  }
+  if (out_kind == 0) {
+    // FP64 frames: the warp's 8x4 patch leaves as two instructions of two
+    // contiguous 256-byte rows each (16-byte chunks gathered by shuffles)
+    // rather than four half-sector scatters — the frame may be page-locked
+    // host memory written over PCIe
+    const int lane = threadIdx.x & 31;
+    const int64_t base = (int64_t)(jl - (lane >> 3)) * out_w + (i - (lane & 7) - P.rect[0]);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int src = (2 * h + (lane >> 4)) * 8 + ((lane & 15) >> 1);
+      double q[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) q[a] = __shfl_sync(0xffffffffu, px[a], src);
+      const bool w = __shfl_sync(0xffffffffu, write, src);
+      if (w) {
+        const int64_t r = base + (int64_t)(2 * h + (lane >> 4)) * out_w + ((lane & 15) >> 1);
+        reinterpret_cast<double2*>((double*)out + r * 4)[lane & 1] =
+            (lane & 1) ? make_double2(q[2], q[3]) : make_double2(q[0], q[1]);
+      }
+    }
+  } else if (write) {
+    store_px<T>(out, out_kind, (int64_t)jl * out_w + (i - P.rect[0]), px);
   }
   warp_add_counters(cnt, counters);
 }
@@ -1503,8 +1531,29 @@ static void render_rect(vt_mirror* m, const vt_scene* scene, const int32_t* rect
   }
   const int64_t px = (int64_t)rw * rh;
   const int esz = out_kind == 0 ? 8 : (out_kind == 1 ? 4 : 1);
+  VT_REQUIRE(((uintptr_t)out & (out_kind == 2 ? 3 : 15)) == 0, VT_EINVAL,
+             "output frame must be 16-byte aligned (4-byte for RGBA8)");
   void* dout = out;
-  if (!out_on_device) VT_CUDA(cudaMallocAsync(&dout, std::max<int64_t>(1, px) * 4 * esz, t.stream));
+  // a page-locked host frame (the Python API's frames are) is written by the
+  // kernel itself over PCIe as the rays finish — the 66 MB float64 1080p
+  // frame's transfer hides under the render instead of following it
+  bool direct = false;
+  if (!out_on_device && px > 0) {
+    static const bool zc = [] {
+      const char* e = std::getenv("VT_RENDER_DIRECT_HOST");
+      return !(e && e[0] == '0');
+    }();
+    cudaPointerAttributes attr{};
+    if (zc && cudaPointerGetAttributes(&attr, out) == cudaSuccess &&
+        attr.type == cudaMemoryTypeHost && attr.devicePointer != nullptr) {
+      dout = attr.devicePointer;
+      direct = true;
+    } else {
+      cudaGetLastError();  // pageable memory: not an error
+    }
+  }
+  if (!out_on_device && !direct)
+    VT_CUDA(cudaMallocAsync(&dout, std::max<int64_t>(1, px) * 4 * esz, t.stream));
   unsigned long long* dc = nullptr;
   VT_CUDA(cudaMallocAsync(&dc, 7 * sizeof(unsigned long long), t.stream));
   VT_CUDA(cudaMemsetAsync(dc, 0, 7 * sizeof(unsigned long long), t.stream));
@@ -1528,7 +1577,7 @@ static void render_rect(vt_mirror* m, const vt_scene* scene, const int32_t* rect
   VT_CUDA(cudaEventRecord(t.ev1, t.stream));
   unsigned long long h[7];
   VT_CUDA(cudaMemcpyAsync(h, dc, sizeof(h), cudaMemcpyDeviceToHost, t.stream));
-  if (!out_on_device) {
+  if (!out_on_device && !direct) {
     VT_CUDA(cudaMemcpyAsync(out, dout, px * 4 * esz, cudaMemcpyDeviceToHost, t.stream));
     release(t, dout);
   }
