@@ -406,7 +406,8 @@ def run_ours(args):
             "e2e": {"value": round(e2e_value, 4), "unit": "Gsamples/s",
                     "h2d_bytes_per_step": ct.sizeof(_lib.vt_scene),
                     "d2h_bytes_per_step": W * H * 4 * 8 + 48,
-                    "api": "OutOfCoreRenderer.render_fullframe -> float64 (H,W,4) host"
+                    "api": "OutOfCoreRenderer.render_fullframe -> float64 (H,W,4) page-locked host "
+                           "frame (N=1: the kernel writes it over PCIe)"
                     if world == 1 else "SortFirstRenderer.render_fullframe(to_host=True)"},
             "build": {"raw_gb": round(raw_bytes / 1e9, 3), "pool_gb": round(pool_bytes / 1e9, 3),
                       "bricks": tree.brick_count, "build_ms": round(total_build_ms, 2),
