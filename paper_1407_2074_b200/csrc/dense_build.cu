@@ -412,7 +412,10 @@ __host__ __device__ inline uint32_t tma_in_bytes(int mx, int my, int C) {
   return ((uint32_t)kTmaP * (my + 2) * tma_box_row(mx, C) * 2 + 127) / 128 * 128;
 }
 
-template <int C>
+// MX, MY: brick x/y edge fixed at compile time (0 = from g) — with them the
+// stored-row word copy has constant strides and trip counts (immediate
+// offsets, full unrolling)
+template <int C, int MX = 0, int MY = 0>
 __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
     const __grid_constant__ CUtensorMap map, int oz, int dz, int prefill,
     const DenseJob* __restrict__ jobs, int gnx, int gny, int g0z, Geo g,
@@ -429,8 +432,8 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
   const int gx = (int)(blockIdx.x % gnx);
   const int gy = (int)((blockIdx.x / gnx) % gny);
   const int gz = g0z + (int)(blockIdx.x / (gnx * gny));
-  const int Mx = g.brick[0], My = g.brick[1], Mz = g.brick[2];
-  const int Sx = g.stored[0], Sy = g.stored[1], Sz = g.stored[2];
+  const int Mx = MX ? MX : g.brick[0], My = MY ? MY : g.brick[1], Mz = g.brick[2];
+  const int Sx = Mx + 2, Sy = My + 2, Sz = g.stored[2];
   const int X = g.dims[0], Y = g.dims[1], Z = g.dims[2];
   const int cx = min(Mx, X - gx * Mx), cy = min(My, Y - gy * My), cz = min(Mz, Z - gz * Mz);
   const int brow = tma_box_row(Mx, C);                  // staged row (samples)
@@ -446,6 +449,11 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
   const int xa = x0 * C - (((x0 * C) % 8 + 8) % 8);  // 16-byte aligned tile start (samples)
   const int xoff = x0 * C - xa;                     // leading samples of a staged row
   const bool xfull = prefill && x0 >= 0 && x0 + Sx <= X;  // every stored x inside the volume
+  const bool yfull = y0 >= 0 && y0 + Sy <= Y;              // every stored row inside it
+  // e / (Sx * C) and e / C by multiply-high (e < 2^16; a divisor of 1 has no
+  // 32-bit magic)
+  const uint32_t rowmagic = (uint32_t)((((uint64_t)1 << 32) + Sx * C - 1) / (Sx * C));
+  const uint32_t cmagic = C == 1 ? 0u : (uint32_t)((((uint64_t)1 << 32) + C - 1) / C);
   const uint32_t cxmagic = (uint32_t)((((uint64_t)1 << 32) + cx - 1) / cx);  // v / cx by mul-high
 
   if (tid == 0) {
@@ -500,8 +508,9 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
   const bool wact = rr < R;
   const int xo = (xoff >> 1) + wr0;  // staged word of this thread's first word
 
+  const int toy = hx > 0 ? tid / hx : 0;  // octant row of this thread's first octant voxel
   for (int s = 0; s < nstages; ++s) {
-    const int b = s % kTmaStages;
+    const int b = (unsigned)s % kTmaStages;
     const int zs = P * s + pw;
     const int zi = zs - 1;
     const int rz = gz * Mz + zi;  // volume z of this stored plane
@@ -521,7 +530,40 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
         if (wact) {
           const uint32_t* iw = reinterpret_cast<const uint32_t*>(iplane) + xo;
           const int qs = brow >> 1;
-          if (wpr <= NT) {
+          if (wpr <= NT && yfull) {
+            // one word per row per thread, every stored row inside the
+            // volume: a flat loop of load(s), permute, store with running
+            // 32-bit offsets (the parity of the row start is per brick)
+            uint32_t* o = oplane + wr0 + rr * wpr;
+            const uint32_t* q = iw + rr * qs;
+            if (MX && MY) {
+              // constant strides: rows rr, rr + R, ... (the last pass may
+              // hold one row fewer for some threads)
+              constexpr int kWpr = (MX + 2) * C / 2, kQs = ((MX + 2) * C + 14) / 8 * 8 / 2;
+              constexpr int kR = kWpr <= NT ? NT / kWpr : 1, kN = (MY + 2 + kR - 1) / kR;
+              const int nrow = (Sy - rr + kR - 1) / kR;
+              if (xoff & 1) {
+#pragma unroll
+                for (int t = 0; t < kN; ++t)
+                  if (t < nrow) o[t * kR * kWpr] = __byte_perm(q[t * kR * kQs], q[t * kR * kQs + 1], 0x5432);
+              } else {
+#pragma unroll
+                for (int t = 0; t < kN; ++t)
+                  if (t < nrow) o[t * kR * kWpr] = q[t * kR * kQs];
+              }
+            } else {
+              int oo = 0, qo = 0;
+              const int ostep = R * wpr, qstep = R * qs;
+              if (xoff & 1) {
+#pragma unroll 4
+                for (int ys = rr; ys < Sy; ys += R, oo += ostep, qo += qstep)
+                  o[oo] = __byte_perm(q[qo], q[qo + 1], 0x5432);
+              } else {
+#pragma unroll 4
+                for (int ys = rr; ys < Sy; ys += R, oo += ostep, qo += qstep) o[oo] = q[qo];
+              }
+            }
+          } else if (wpr <= NT) {
             // one word per row per thread: a flat, unrollable row loop
             uint32_t* o = oplane + wr0;
             const bool odd = xoff & 1;
@@ -551,9 +593,9 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
         // bricks on the volume's x boundary, or shells not prefilled
         uint16_t* o16 = reinterpret_cast<uint16_t*>(oplane);
         for (int e = pt; e < (int)plane_elems; e += NT) {
-          const int ys = e / (Sx * C);
+          const int ys = (int)__umulhi((uint32_t)e, rowmagic);
           const int es = e - ys * Sx * C;
-          const int xs = es / C;
+          const int xs = C == 1 ? es : (int)__umulhi((uint32_t)es, cmagic);
           const int rx = x0 + xs, ry = y0 + ys;
           const bool take = prefill ? (rx >= 0 && rx < X && ry >= 0 && ry < Y)
                                     : (mode == 1 && xs >= 1 && xs <= cx && ys >= 1 && ys <= cy);
@@ -581,13 +623,14 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
     if (parent && s >= 1 && 2 * (s - 1) < cz) {
       const int k = s - 1;
       const uint16_t* pa = reinterpret_cast<const uint16_t*>(
-                               s_in + (size_t)((s - 1) % kTmaStages) * in_bytes) +
+                               s_in + (size_t)((unsigned)(s - 1) % kTmaStages) * in_bytes) +
                            (size_t)(My + 2) * brow;  // previous stage, plane 1
       const uint16_t* pb = reinterpret_cast<const uint16_t*>(s_in + (size_t)b * in_bytes);
       const bool zfull = 2 * k + 1 < cz;
       const bool pin = offz + k < pcz;
       for (int v = tid; v < hx * hy; v += kTmaWarps * 32) {
-        const int oy = v / hx, ox = v - oy * hx;
+        // the first pass (all of it for 32x32 leaves) uses the hoisted split
+        const int oy = v == tid ? toy : v / hx, ox = v - oy * hx;
         int val[C];
         if (zfull && 2 * ox + 1 < cx && 2 * oy + 1 < cy) {
           const int o00 = (1 + 2 * oy) * brow + xoff + (1 + 2 * ox) * C;
@@ -971,7 +1014,8 @@ static int leaf_launch(const Tree& t, const void* src, int64_t nsrc, int oz, int
   CUtensorMap map;
   if (sizeof(T) == 2 && tma_ok(t, src) && encode_block_map(t, src, dz, &map)) {
     const size_t smem = tma_smem(t.g);
-    auto k = k_dense_leaf_tma<C>;
+    auto k = t.g.brick[0] == 32 && t.g.brick[1] == 32 ? k_dense_leaf_tma<C, 32, 32>
+                                                      : k_dense_leaf_tma<C>;
     VT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k<<<n, kTmaWarps * 32, smem, t.stream>>>(map, oz, (int)dz, prefill, jobs, gn[0], gn[1], g0z,
                                             t.g, (uint16_t*)t.d_pool, t.d_stats, t.d_nmin,
