@@ -563,6 +563,10 @@ bool Tree::dense_eligible(int channel, const int origin[3], const int dims[3], c
   return true;
 }
 
+namespace {
+struct ParentCoord { int64_t idx; int px, py, pz; };
+}  // namespace
+
 void Tree::insert_staged(int channel, const int origin[3], const int dims[3], const void* dsrc,
                          int src_stride, int src_off, int reps) {
   const int64_t nvox = (int64_t)dims[0] * dims[1] * dims[2];
@@ -594,6 +598,9 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
   // brick slot per block leaf (general path only)
   std::vector<int32_t> leaf_slots(dense ? 0 : nblock);
   static thread_local std::vector<std::vector<int64_t>> touched;  // scratch, as djobs
+  // early path: the sorted level-1 parents (BFS order of the block's leaves)
+  static thread_local std::vector<ParentCoord> early_par;
+  early_par.clear();
   touched.resize(g.depth + 1);
   for (auto& v : touched) v.clear();
   touched[0].reserve(nblock);
@@ -628,7 +635,7 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
     delete qdj;
     ProfScope* qpp = new ProfScope(prof, 24);
     if (g.depth >= 1 && g.split[0] && g.split[1] && g.split[2]) {
-      struct P1 { int64_t idx; int px, py, pz; };
+      using P1 = ParentCoord;
       std::vector<int64_t> pidx;
       const int64_t base1 = g.level_start[g.depth - 1];
       for (int pz = g0[2] >> 1; pz <= g1[2] >> 1; ++pz)
@@ -644,6 +651,7 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
           for (int a = 0; a < 3; ++a) c[a] |= (int)((pidx[i] >> (3 * b + a)) & 1) << b;
         par[i] = {base1 + pidx[i], c[0], c[1], c[2]};
       }
+      early_par.assign(par.begin(), par.end());  // for the leaves' BFS order, after launch
       int64_t next = cur0 + nleaves;
       ProfScope qpd(prof, 27);
       for (const P1& q1 : par) {
@@ -872,7 +880,22 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
   }
   {
     ProfScope qs(prof, 15);
-    sort_indices(touched[0]);
+    // early path: the block's leaves in BFS order are the children of the
+    // sorted parents — no sort
+    static thread_local std::vector<int64_t> sorted_leaves;
+    sorted_leaves.clear();
+    for (const ParentCoord& q1 : early_par)
+      for (int k = 0; k < 8; ++k) {
+        const int cgx = 2 * q1.px + (k & 1), cgy = 2 * q1.py + ((k >> 1) & 1),
+                  cgz = 2 * q1.pz + ((k >> 2) & 1);
+        if (cgx >= g0[0] && cgx <= g1[0] && cgy >= g0[1] && cgy <= g1[1] && cgz >= g0[2] &&
+            cgz <= g1[2])
+          sorted_leaves.push_back(8 * q1.idx + 1 + k);
+      }
+    if (!sorted_leaves.empty() && sorted_leaves.size() == touched[0].size())
+      touched[0].swap(sorted_leaves);  // the same set, already ordered
+    else
+      sort_indices(touched[0]);
   }
   has_pending = true;
   delete anc_scope;
