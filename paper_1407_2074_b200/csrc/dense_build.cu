@@ -857,21 +857,22 @@ __global__ void __launch_bounds__(256) k_dense_level(const int64_t* __restrict__
   for (int z = zb0 + warp; z < zb1; z += nw) {
     Acc<C> pl;
     pl.init();
-    for (int y = 0; y < My; y += 2) {
+    // kRows rows per iteration: their gathers are all in flight together
+    // (the small top levels are latency bound: few CTAs, a serial row chain)
+    constexpr int kRows = 4;
+    for (int y = 0; y < My; y += kRows) {
       for (int x = lane; x < Mx; x += 32) {
-        const bool two = y + 1 < My;
-        const Vox a = voxel(x, y, z);
-        const Vox b = two ? voxel(x, y + 1, z) : a;
-        const int* v0 = a.v;
-        const int* v1 = b.v;
+        Vox vv[kRows];
+#pragma unroll
+        for (int r = 0; r < kRows; ++r)
+          if (y + r < My) vv[r] = voxel(x, y + r, z);
         T* dst = parent + g.voxel_offset(1 + z, 1 + y, 1 + x);
 #pragma unroll
-        for (int c = 0; c < C; ++c) dst[c] = (T)v0[c];
-        if (x < pcx && y < pcy && z < pcz) pl.add_all(v0);
-        if (two) {
+        for (int r = 0; r < kRows; ++r) {
+          if (y + r >= My) continue;
 #pragma unroll
-          for (int c = 0; c < C; ++c) dst[rs + c] = (T)v1[c];
-          if (x < pcx && y + 1 < pcy && z < pcz) pl.add_all(v1);
+          for (int c = 0; c < C; ++c) dst[r * rs + c] = (T)vv[r].v[c];
+          if (x < pcx && y + r < pcy && z < pcz) pl.add_all(vv[r].v);
         }
       }
     }
@@ -1144,9 +1145,13 @@ static void level_dispatch(const Tree& t, const int64_t* nodes, int n, int zs) {
 int dense_level_split(const Tree& t, int n) {
   // few parents: split each over CTAs of 8 planes (one per warp) so the
   // level is not the latency of a single CTA walking a whole brick
+  static const int target = [] {
+    const char* e = std::getenv("VT_LEVEL_CTAS");
+    return e ? std::max(1, atoi(e)) : 2 * 148;
+  }();
   const int mz = t.g.brick[2];
   int k = 1;
-  while (k * 2 * 8 <= mz && (int64_t)n * k < 2 * 148) k *= 2;
+  while (k * 2 * 8 <= mz && (int64_t)n * k < target) k *= 2;
   return k;
 }
 
