@@ -601,6 +601,7 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
   // early path: the sorted level-1 parents (BFS order of the block's leaves)
   static thread_local std::vector<ParentCoord> early_par;
   early_par.clear();
+  bool early_full = false;  // early launch over the complete leaf grid
   touched.resize(g.depth + 1);
   for (auto& v : touched) v.clear();
   touched[0].reserve(nblock);
@@ -634,7 +635,26 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
     }
     delete qdj;
     ProfScope* qpp = new ProfScope(prof, 24);
-    if (g.depth >= 1 && g.split[0] && g.split[1] && g.split[2]) {
+    // complete grid (every leaf of the tree in this block, no brick yet): the
+    // block's parents are every level-1 node, in BFS order, so parent p takes
+    // slot cur0 + n_leaves + (p - first level-1 index) — no sort
+    const int64_t n1 = g.depth >= 1 ? g.level_start[g.depth] - g.level_start[g.depth - 1] : 0;
+    bool complete_grid = g.depth >= 1 && g.split[0] && g.split[1] && g.split[2] &&
+                         nleaves == ((int64_t)1 << (3 * g.depth)) && n1 * 8 == nleaves;
+    for (int64_t p = 0; complete_grid && p < n1; ++p)
+      if (flags[g.level_start[g.depth - 1] + p] & NF_BRICK) complete_grid = false;
+    if (complete_grid) {
+      early_full = true;
+      const int64_t base1 = g.level_start[g.depth - 1];
+      for (DenseJob& jd : djobs)
+        jd.pad = (int32_t)(cur0 + nleaves + (((jd.node - 1) >> 3) - base1));
+      fused_nodes.resize(n1);
+      fused_slots.resize(n1);
+      for (int64_t p = 0; p < n1; ++p) {
+        fused_nodes[p] = base1 + p;
+        fused_slots[p] = (int32_t)(cur0 + nleaves + p);
+      }
+    } else if (g.depth >= 1 && g.split[0] && g.split[1] && g.split[2]) {
       using P1 = ParentCoord;
       std::vector<int64_t> pidx;
       const int64_t base1 = g.level_start[g.depth - 1];
@@ -884,6 +904,12 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
     // sorted parents — no sort
     static thread_local std::vector<int64_t> sorted_leaves;
     sorted_leaves.clear();
+    if (early_full) {
+      // complete grid: the leaves are the whole last BFS level
+      sorted_leaves.resize(touched[0].size());
+      for (size_t i = 0; i < sorted_leaves.size(); ++i)
+        sorted_leaves[i] = g.level_start[g.depth] + (int64_t)i;
+    }
     for (const ParentCoord& q1 : early_par)
       for (int k = 0; k < 8; ++k) {
         const int cgx = 2 * q1.px + (k & 1), cgy = 2 * q1.py + ((k >> 1) & 1),
