@@ -219,3 +219,34 @@ def test_fp32_reconstruction_within_tolerance(name):
     assert err <= TOL, f"{name}: fp32 max err {err}"
     want = gold["counters"]["samples"]
     assert abs(cnt.samples - want) <= max(1, 1e-3 * want)
+
+
+@pytest.mark.parametrize("kind", [0, 1, 2])
+@pytest.mark.parametrize("wh", [(37, 29), (64, 48), (9, 5)])
+def test_host_frame_direct_write_equals_copy(kind, wh):
+    """A page-locked host frame is written by the kernel itself over PCIe
+    (warp patches as contiguous rows, shuffle-gathered); a pageable one goes
+    through a device frame and a copy.  Same bytes, partial warp patches at
+    the frame's right and bottom edges included."""
+    import ctypes as ct
+    import torch
+    from paper_1407_2074_b200 import DeviceState, _lib
+    from paper_1407_2074_b200.render.raycast import scene_to_vt
+    rc = scenarios.render_case("spim_u8_dvr")
+    spec = dict(rc["scene"], width=wh[0], height=wh[1])
+    _, tree, _ = build_scenario(rc["build"], borders=True)
+    dev = DeviceState(tree, resident_all=True)
+    scene = to_scene(spec)
+    dt = {0: np.float64, 1: np.float32, 2: np.uint8}[kind]
+    tdt = {0: torch.float64, 1: torch.float32, 2: torch.uint8}[kind]
+    out = {}
+    for name, arr in (("pinned", torch.full((wh[1], wh[0], 4), 7, dtype=tdt,
+                                            pin_memory=True).numpy()),
+                      ("pageable", np.full((wh[1], wh[0], 4), 7, dtype=dt))):
+        cnt = _lib.vt_counters()
+        s = scene_to_vt(scene, tree.descriptor)
+        _lib.call("vt_render_fullframe", dev.handle, ct.byref(s), ct.c_void_p(arr.ctypes.data),
+                  kind, 0, ct.byref(cnt))
+        out[name] = (arr.copy(), cnt.samples)
+    assert np.array_equal(out["pinned"][0], out["pageable"][0])
+    assert out["pinned"][1] == out["pageable"][1]
