@@ -305,6 +305,7 @@ __global__ void k_reduce(const ReduceJob* __restrict__ jobs, int n, Geo g,
   if (cx > 0 && cy > 0 && cz > 0) {
     int mn = INT_MAX, mx = INT_MIN;
     unsigned long long s = 0;
+#pragma unroll 8
     for (int z = 0; z < cz; ++z) {
       int64_t o = ((int64_t)j.slot * g.brick[2] + z) * g.C + c;
       mn = min(mn, pmin[o]);

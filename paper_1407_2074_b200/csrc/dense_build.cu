@@ -804,9 +804,10 @@ __global__ void __launch_bounds__(256) k_dense_level(const int64_t* __restrict__
   auto voxel = [&](int x, int y, int z) -> Vox {
     Vox r;
     int* v = r.v;
-    const int bz = z / hz, oz = z - bz * hz;
-    const int by = y / hy, oy = y - by * hy;
-    const int bx = x / hx, ox = x - bx * hx;
+    // coordinates are below 2 * half-extent: the octant bit is a compare
+    const int bz = z >= hz ? 1 : 0, oz = z - bz * hz;
+    const int by = y >= hy ? 1 : 0, oy = y - by * hy;
+    const int bx = x >= hx ? 1 : 0, ox = x - bx * hx;
     const int k = bx | (by << 1) | (bz << 2);
     const int cs = s_cslot[k];
     if (cs < 0) {
@@ -854,13 +855,22 @@ __global__ void __launch_bounds__(256) k_dense_level(const int64_t* __restrict__
     return r;
   };
   const int zb0 = part * Mz / zsplit, zb1 = (part + 1) * Mz / zsplit;
-  for (int z = zb0 + warp; z < zb1; z += nw) {
+  // fewer planes than warps (small levels split finely): wpp warps share a
+  // plane, each taking every wpp-th group of rows; their plane partials are
+  // combined in shared memory before the first of them emits the plane
+  const int nplanes = zb1 - zb0;
+  const int wpp = nplanes >= nw ? 1 : nw / nplanes;
+  const int pz = warp / wpp, wy = warp % wpp, ppass = nw / wpp;
+  __shared__ int s_pmn[kMaxWarps][C], s_pmx[kMaxWarps][C];
+  __shared__ unsigned long long s_psm[kMaxWarps][C];
+  const int zend = zb0 + (nplanes + ppass - 1) / ppass * ppass;  // uniform trip count
+  for (int z = zb0 + pz; z < zend; z += ppass) {
     Acc<C> pl;
     pl.init();
     // kRows rows per iteration: their gathers are all in flight together
     // (the small top levels are latency bound: few CTAs, a serial row chain)
     constexpr int kRows = 4;
-    for (int y = 0; y < My; y += kRows) {
+    for (int y = wy * kRows; y < My && z < zb1; y += kRows * wpp) {
       for (int x = lane; x < Mx; x += 32) {
         Vox vv[kRows];
 #pragma unroll
@@ -876,7 +886,29 @@ __global__ void __launch_bounds__(256) k_dense_level(const int64_t* __restrict__
         }
       }
     }
-    if (z < pcz && pcx > 0 && pcy > 0) emit_plane<C>(pl, tot, s_pslot, Mz, z, pmin, pmax, psum);
+    if (wpp > 1) {
+      pl.warp_reduce();
+      if (lane == 0)
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          s_pmn[warp][c] = pl.mn[c];
+          s_pmx[warp][c] = pl.mx[c];
+          s_psm[warp][c] = pl.sm[c];
+        }
+      __syncthreads();
+      pl.init();
+      if (wy == 0 && lane == 0)
+        for (int w = warp; w < warp + wpp; ++w)
+#pragma unroll
+          for (int c = 0; c < C; ++c) {
+            pl.mn[c] = min(pl.mn[c], s_pmn[w][c]);
+            pl.mx[c] = max(pl.mx[c], s_pmx[w][c]);
+            pl.sm[c] += s_psm[w][c];
+          }
+      __syncthreads();
+    }
+    if (wy == 0 && z < zb1 && z < pcz && pcx > 0 && pcy > 0)
+      emit_plane<C>(pl, tot, s_pslot, Mz, z, pmin, pmax, psum);
   }
   finish_stats<C>(tot, node, (int64_t)pcx * pcy * pcz, false, g, flags, stats);
 }
@@ -1143,15 +1175,16 @@ static void level_dispatch(const Tree& t, const int64_t* nodes, int n, int zs) {
 }
 
 int dense_level_split(const Tree& t, int n) {
-  // few parents: split each over CTAs of 8 planes (one per warp) so the
-  // level is not the latency of a single CTA walking a whole brick
+  // few parents: split each over CTAs of fewer planes (down to one plane per
+  // CTA, its warps sharing the rows) so the level is not the latency of a
+  // single CTA walking a whole brick
   static const int target = [] {
     const char* e = std::getenv("VT_LEVEL_CTAS");
     return e ? std::max(1, atoi(e)) : 2 * 148;
   }();
   const int mz = t.g.brick[2];
   int k = 1;
-  while (k * 2 * 8 <= mz && (int64_t)n * k < target) k *= 2;
+  while (k * 2 <= mz && (int64_t)n * k * 2 <= target) k *= 2;
   return k;
 }
 
