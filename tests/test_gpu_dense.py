@@ -196,6 +196,12 @@ PREFILL_CASES = {
     "two_layer_slabs_bg": ((48, 40, 72), 2, (8, 8, 8), 2, 17),
     "bulk_partial": ((40, 36, 50), 3, (8, 8, 8), 100, 0),
     "bulk_pow2_bg": ((64, 64, 64), 3, (8, 8, 8), 100, 5),
+    # complete leaf grids in one insertion (parent slots by BFS rank, leaves
+    # as one BFS range), incl. the compile-time 32x32 copy for C = 1, 2, 4
+    "grid_b32_c1": ((128, 128, 64), 1, (32, 32, 32), 100, 0),
+    "grid_b32_c2": ((64, 64, 64), 2, (32, 32, 32), 100, 9),
+    "grid_b32_c4": ((64, 64, 128), 4, (32, 32, 32), 100, 0),
+    "grid_b16_c2": ((64, 64, 64), 2, (16, 16, 16), 100, 0),
     "nonsplit_z": ((32, 16, 6), 3, (8, 8, 8), 1, 3),
     "brick16_c4": ((64, 32, 48), 4, (16, 16, 16), 1, 0),
 }
