@@ -431,6 +431,9 @@ __global__ void __launch_bounds__(256) k_octant(const OctJob* __restrict__ jobs,
 // (find_node, octree.py:497-505, with exact integer compares), then the
 // whole CTA walks every shell voxel of the brick in one flat loop (a
 // thread per voxel, all channels), so the small segments do not serialise.
+#ifndef VT_BORDER_K
+#define VT_BORDER_K 4
+#endif
 template <class T>
 __global__ void __launch_bounds__(256) k_borders(const BorderJob* __restrict__ jobs, Geo g,
                                                  T* pool, const uint8_t* __restrict__ flags,
@@ -524,7 +527,7 @@ __global__ void __launch_bounds__(256) k_borders(const BorderJob* __restrict__ j
   // batches of K shell voxels per thread: every source of a batch is read
   // before any destination is written (the reads are strided neighbour
   // columns: latency, not bandwidth, bounds this loop)
-  constexpr int K = 4;
+  constexpr int K = VT_BORDER_K;
   for (int e0 = threadIdx.x; e0 < total; e0 += K * blockDim.x) {
     int64_t doff[K];
     T val[K][kMaxC];
@@ -560,7 +563,9 @@ __global__ void __launch_bounds__(256) k_borders(const BorderJob* __restrict__ j
 #pragma unroll
     for (int q = 0; q < K; ++q)
       if (live[q])
-        for (int c = 0; c < C; ++c) dst[doff[q] + c] = val[q][c];
+#pragma unroll
+        for (int c = 0; c < kMaxC; ++c)
+          if (c < C) dst[doff[q] + c] = val[q][c];
   }
 }
 
