@@ -17,7 +17,7 @@ dims = (N, N, N)
 desc = VolumeDescriptor(dims=dims, channels=3, sample_format="uint16")
 cfg = BrickPoolConfig(brick_dims=(32,) * 3, homogeneity_threshold=0)
 vol = torch.empty((N, N, N, 3), dtype=torch.uint16, device="cuda")
-st = torch.cuda.Stream()
+st = torch.cuda.current_stream() if os.environ.get("AB_DEFAULT_STREAM") == "1" else torch.cuda.Stream()
 _lib.call("vt_synth", ct.c_void_p(vol.data_ptr()), 1, _lib.i32x3(dims), 3, 2, 0, 0, N,
           ct.c_void_p(st.cuda_stream))
 torch.cuda.synchronize()
