@@ -1088,6 +1088,68 @@ __global__ void __launch_bounds__(256) k_brick_max(const T* __restrict__ bb, con
   }
 }
 
+// The same maxima for 16-bit pools in two passes over shared memory: (1)
+// every (stored row, sub-brick x-range) task reduces its run of samples —
+// consecutive tasks read consecutive, overlapping runs of 32-bit words, so
+// the brick streams through coalesced — into a row-maximum table; (2) one
+// thread per (sub-brick, channel) reduces its rows of that table.  No
+// atomics, no per-voxel index arithmetic.
+constexpr int kBmaxSmemBytes = 40 * 1024;
+constexpr int kBmaxWords = 20;  // one task's run: (sub-brick edge + 2) * C / 2 words
+template <int C>
+__global__ void __launch_bounds__(256) k_brick_max16(const uint16_t* __restrict__ bb,
+                                                     const int32_t* slots, int n, Geo g, int sb0,
+                                                     int sb1, int sb2, int nx, int ny, int nz,
+                                                     uint16_t* bmax, uint16_t* bmax_brick) {
+  extern __shared__ uint16_t s_rm[];  // [Sz][Sy][nx][C] row maxima
+  __shared__ int s_all[kMaxC];
+  const int Sx = g.stored[0], Sy = g.stored[1], Sz = g.stored[2];
+  const int nsb = nx * ny * nz;
+  const int ntask = Sz * Sy * nx;
+  for (int job = blockIdx.x; job < n; job += gridDim.x) {
+    const int64_t slot = slots ? slots[job] : job;
+    if (slot < 0) continue;
+    const uint16_t* b = bb + slot * g.brick_elems;
+    if (threadIdx.x < kMaxC) s_all[threadIdx.x] = 0;
+    for (int t = threadIdx.x; t < ntask; t += blockDim.x) {
+      const int qx = t % nx, row = t / nx;  // row = z * Sy + y
+      const int x0 = qx * sb0, x1 = min(x0 + sb0 + 2, Sx);
+      const uint32_t* w = reinterpret_cast<const uint32_t*>(b + (int64_t)row * Sx * C + x0 * C);
+      int mx[kMaxC] = {0, 0, 0, 0};
+      const int nw = (x1 - x0) * C / 2;
+      // every word of the run in flight at once (<= kBmaxWords), then reduce
+      uint32_t v[kBmaxWords];
+#pragma unroll
+      for (int k = 0; k < kBmaxWords; ++k) v[k] = k < nw ? __ldg(w + k) : 0u;
+      // sample 2k + h has channel (2k + h) % C: static after unrolling
+#pragma unroll
+      for (int k = 0; k < kBmaxWords; ++k) {
+        if (k < nw) {
+          mx[(2 * k) % C] = max(mx[(2 * k) % C], (int)(v[k] & 0xFFFF));
+          mx[(2 * k + 1) % C] = max(mx[(2 * k + 1) % C], (int)(v[k] >> 16));
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < kMaxC; ++q)
+        if (q < C) s_rm[(int64_t)t * C + q] = (uint16_t)mx[q];
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < nsb * C; r += blockDim.x) {
+      const int q = r / C, c = r - q * C;
+      const int qx = q % nx, qy = (q / nx) % ny, qz = q / (nx * ny);
+      const int y0 = qy * sb1, y1 = min(y0 + sb1 + 2, Sy), z0 = qz * sb2, z1 = min(z0 + sb2 + 2, Sz);
+      int m = 0;
+      for (int z = z0; z < z1; ++z)
+        for (int y = y0; y < y1; ++y) m = max(m, (int)s_rm[((z * Sy + y) * nx + qx) * C + c]);
+      bmax[(slot * nsb + q) * kMaxC + c] = (uint16_t)m;
+      atomicMax(&s_all[c], m);
+    }
+    __syncthreads();
+    if (threadIdx.x < kMaxC) bmax_brick[slot * kMaxC + threadIdx.x] = (uint16_t)s_all[threadIdx.x];
+    __syncthreads();
+  }
+}
+
 // sub-brick edge per axis: a quarter of the brick when that divides evenly
 // into edges of at least 2 voxels, else the whole brick
 inline void sub_bricks(const Geo& g, int sbk[3], int nsub[3]) {
@@ -1338,6 +1400,23 @@ static void update_bmax(vt_mirror* m, const int32_t* d_slots, int n) {
       k_brick_max<uint8_t><<<grid, 256, 0, t.stream>>>((const uint8_t*)bb, d_slots, jobs, t.g,
                                                        sbk[0], sbk[1], sbk[2], nsub[0], nsub[1],
                                                        nsub[2], m->d_bmax, m->d_bmax_brick);
+    else if (sbk[0] % 2 == 0 && t.g.stored[0] % 2 == 0 &&
+             (sbk[0] + 2) * t.g.C / 2 <= kBmaxWords &&
+             (size_t)t.g.stored[2] * t.g.stored[1] * nsub[0] * t.g.C * sizeof(uint16_t) <=
+                 (size_t)kBmaxSmemBytes)
+      switch (t.g.C) {
+#define VT_BMAX16(CC)                                                                          \
+  case CC:                                                                                     \
+    k_brick_max16<CC><<<grid, 256, kBmaxSmemBytes, t.stream>>>(                                \
+        (const uint16_t*)bb, d_slots, jobs, t.g, sbk[0], sbk[1], sbk[2], nsub[0], nsub[1],     \
+        nsub[2], m->d_bmax, m->d_bmax_brick);                                                  \
+    break;
+        VT_BMAX16(1)
+        VT_BMAX16(2)
+        VT_BMAX16(3)
+        VT_BMAX16(4)
+#undef VT_BMAX16
+      }
     else
       k_brick_max<uint16_t><<<grid, 256, 0, t.stream>>>((const uint16_t*)bb, d_slots, jobs, t.g,
                                                         sbk[0], sbk[1], sbk[2], nsub[0], nsub[1],
