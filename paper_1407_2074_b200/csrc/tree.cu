@@ -1487,12 +1487,18 @@ void Tree::prune(std::vector<std::vector<int64_t>>& touched, std::vector<char>& 
 // ---------------------------------------------------------------------------
 
 void Tree::fill_borders() {
+  ProfScope pf(prof, 3);
   flush();
   ++data_version;
   std::vector<BorderJob> jobs;
-  std::vector<int64_t> bricks;
-  for (int64_t i = 0; i < g.capacity; ++i)
-    if ((flags[i] & NF_EXISTS) && (flags[i] & NF_BRICK)) bricks.push_back(i);
+  static thread_local std::vector<int64_t> bricks;  // scratch: every brick, BFS order
+  bricks.resize(g.capacity);  // an upper bound; the scratch keeps its pages
+  {
+    size_t nb = 0;
+    for (int64_t i = 0; i < g.capacity; ++i)
+      if ((flags[i] & (NF_EXISTS | NF_BRICK)) == (NF_EXISTS | NF_BRICK)) bricks[nb++] = i;
+    bricks.resize(nb);
+  }
   // Fast path: every in-volume leaf complete and every leaf shell prefilled
   // by the dense build (dense_build.cu) with nothing mutated since.  Then
   // each leaf shell already holds its fill_borders value except owed z-shell
@@ -1524,7 +1530,12 @@ void Tree::fill_borders() {
   BorderJob* d = upload(*this, jobs);
   launch_borders(*this, d, (int)jobs.size());
   release(*this, d);
-  for (int64_t i : bricks) events.push_back(ev_pack(VT_EV_UPDATED, i));
+  {
+    const size_t e0 = events.size();
+    events.resize(e0 + bricks.size());
+    uint64_t* ev = events.data() + e0;
+    for (size_t k = 0; k < bricks.size(); ++k) ev[k] = ev_pack(VT_EV_UPDATED, bricks[k]);
+  }
   borders = true;
   halo_prefill = false;
   owed_shells.clear();  // every level > 0 brick's shell was just written

@@ -60,7 +60,7 @@ struct HostProf {
   bool ev_armed = false;
   double t[kN] = {0};
   static const char* name(int i) {
-    static const char* n[kN] = {"insert", "walk", "enqueue", "events", "propagate", "flush_struct",
+    static const char* n[kN] = {"insert", "walk", "enqueue", "fill_borders", "propagate", "flush_struct",
                                 "seed", "scatter", "leaves", "ancestors", "prop_build", "prop_launch",
                                 "early_pre", "anc_collect", "anc_brick", "sort_leaves",
                                 "dense_book", "updated_ev", "defer", "pool",
