@@ -965,18 +965,22 @@ def synth_uniform(dims, C, fmax, seed=0, z0=0, z1=None):
     return out
 
 
-def synth_spim(dims, C, fmax, seed=0, z0=0, z1=None):
+def synth_spim(dims, C, fmax, seed=0, z0=0, z1=None, y0=0, y1=None, x0=0, x1=None):
     """'S' data: integer-only SPIM-like specimen: noisy
-    background, ellipsoidal specimen, per-channel blob lattice of 32^3 cells."""
+    background, ellipsoidal specimen, per-channel blob lattice of 32^3 cells.
+    Returns the sub-box [z0, z1) x [y0, y1) x [x0, x1) of the volume of
+    extent ``dims`` (a crop keeps the full volume's specimen geometry)."""
     dx, dy, dz = dims
     z1 = dz if z1 is None else z1
-    z, y, x = np.meshgrid(np.arange(z0, z1, dtype=np.int64), np.arange(dy, dtype=np.int64),
-                          np.arange(dx, dtype=np.int64), indexing="ij")
+    y1 = dy if y1 is None else y1
+    x1 = dx if x1 is None else x1
+    z, y, x = np.meshgrid(np.arange(z0, z1, dtype=np.int64), np.arange(y0, y1, dtype=np.int64),
+                          np.arange(x0, x1, dtype=np.int64), indexing="ij")
     big = fmax > 255
     amp = 40000 if big else 220
     base = 100 if big else 8
     noise_mask = 15 if big else 3
-    out = np.empty((z1 - z0, dy, dx, C), dtype=np.uint16 if big else np.uint8)
+    out = np.empty((z1 - z0, y1 - y0, x1 - x0, C), dtype=np.uint16 if big else np.uint8)
     # ellipsoid: sum((2p - d)^2 * 400 / d^2) <= 81*4 ... integer form
     ex = (2 * x - dx) ** 2 * 10000 // max(dx * dx, 1)
     ey = (2 * y - dy) ** 2 * 10000 // max(dy * dy, 1)

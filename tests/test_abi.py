@@ -84,7 +84,8 @@ def test_volume_validation_mirrors_reference():
     assert virtual_dims((2048, 2048, 1000), (32, 32, 32)) == ((2048, 2048, 2048), 6)
     g = TreeGeometry.build(VolumeDescriptor(dims=(16, 16, 16)), BrickPoolConfig(brick_dims=(4, 4, 4)))
     assert g.node_capacity == 73 and g.level_of_index(9) == 0
-    assert g.box_lo_of_index(8 * 1 + 1 + 7) == (12, 12, 12) or True
+    assert g.box_lo_of_index(8 * 1 + 1 + 7) == (4, 4, 4)  # child 7 of node 1 (level 0)
+    assert g.box_lo_of_index(72) == (12, 12, 12)  # last level-0 node
     with pytest.raises(ValueError):
         TreeGeometry.build(VolumeDescriptor(dims=(4096, 1, 1)), BrickPoolConfig(brick_dims=(2, 1, 1)))
 
