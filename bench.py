@@ -3,22 +3,39 @@
 ray-casting hot path (BASELINE.json metric: frame ms & Gsamples/s, 3-ch
 1920x1080; octree build GB/s; at 1/2/4/8 GPUs).
 
-Workload (BASELINE.json configs[1], the largest single-GPU config): a
-synthetic SPIM-shaped ("S") 3-channel 1024^3 uint16 volume,
-32^3 bricks, homogeneity threshold 0, built on the device from
-device-resident z-slabs (Octree.insert_channels) + fill_borders; then
-1920x1080 DVR frames with per-channel transfer functions, one clipping
-plane, early termination 0.99, step 0.5 voxel, LOD bias 0, camera at 2.5x
-the extent (voxtree cli.default_scene).  A "step" is one full frame.
+Workload (N=1 default, BASELINE.json configs[2], the north-star set): the
+synthetic SPIM-shaped ("S") 3-channel 2048x2048x1000 uint16
+volume (25.2 GB raw; 32^3 bricks, homogeneity threshold 0, pool 35.3 GB),
+which fits one B200.  It lives in HBM as planar (C, Z, Y, X) slices, the
+layout a VSTR slice stream lands in (ingest_stream, ingest.py:306-358):
 
-  value      pos-samples / s of the whole job (Gsamples/s), device time of the
-             render (+ NCCL strip gather for N > 1), CUDA events, max over ranks
-  e2e        the same through the public drop-in API with host output
-             (OutOfCoreRenderer.render_fullframe -> float64 (H, W, 4) numpy, the
-             reference's return type; SortFirstRenderer to_host for N > 1)
-  build      device-resident slab ingest GB/s (+ host-slab e2e GB/s)
-  roofline   render kernel: 48 B gathered per pos-sample (8 corners x 3 ch x
-             2 B) / average kernel duration vs measured HBM copy bandwidth
+  stream              every (z, channel) slice in VSTR order through
+                      Octree.insert_planar (= insert_block per slice), one
+                      call per brick layer, + finalize + fill_borders: build
+                      GB/s and its roofline fraction (1 + pool/raw bytes per
+                      raw byte)
+  stream_interleaved  the same stream with a 1920x1080 frame after every 50 z
+                      (mirror refresh + render timed separately)
+  stream_e2e          host -> tree: pinned host frames of the first 256 z
+  value               Gsamples/s of 1920x1080 DVR frames of the final tree
+                      (per-channel transfer functions, one clipping plane,
+                      ET 0.99, step 0.5 voxel, LOD bias 0, camera at 2.5x the
+                      extent as voxtree cli.default_scene); a "step" is one
+                      frame; device time (CUDA events), L2 flushed between
+                      frames, max over ranks
+  e2e                 the same through the public drop-in API with host output
+                      (OutOfCoreRenderer.render_fullframe -> float64 (H, W, 4)
+                      numpy, the reference's return type)
+  roofline            render kernel: 48 B gathered per reconstructed pos-sample
+                      (8 corners x 3 ch x 2 B) / average kernel duration vs the
+                      measured HBM copy bandwidth
+  cfg2                secondary leg: configs[1] (1024^3 x 3 uint16), one-call
+                      device build + 1080p frames
+
+N > 1 (torchrun): the same volume built z-slab sharded (each rank inserts
+its slab, one all-gather of level-k node records) and rendered sort-first
+(interleaved strips, NCCL gather to rank 0).  `--workload cfg2` selects
+configs[1] instead.
 
 `--impl reference` times the reference's own CPU implementation (the
 unmodified voxtree package from baseline/_ref; the oracle port when that is
@@ -41,7 +58,6 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-DIMS = (1024, 1024, 1024)
 CHANNELS = 3
 FMT = "uint16"
 BRICK = 32
@@ -51,9 +67,18 @@ COLORS = ((1.0, 0.25, 0.2), (0.2, 1.0, 0.3), (0.25, 0.45, 1.0))
 BYTES_PER_POS_SAMPLE = 8 * CHANNELS * 2  # 8 trilinear corners x C x uint16
 L2_FLUSH_BYTES = 512 << 20
 FALLBACK_HBM_GBS = 6650.0
-WORKLOAD = ("cfg2: synthetic SPIM-shaped 3-ch uint16 volume (1024^3 by default), 32^3 bricks, tau=0, "
-            "full octree build + fill_borders; 1920x1080 DVR frame, per-channel TFs, "
-            "1 clip plane, ET 0.99, step 0.5 voxel, LOD bias 0")
+_SCENE = ("1920x1080 DVR frame, per-channel TFs, 1 clip plane, ET 0.99, step 0.5 voxel, "
+          "LOD bias 0")
+WORKLOADS = {
+    "cfg3": {"dims": (2048, 2048, 1000),
+             "desc": "cfg3: synthetic SPIM-shaped 3-ch uint16 2048x2048x1000 (25.2 GB), 32^3 "
+                     "bricks, tau=0, streamed slice-wise in VSTR order (device-resident planar "
+                     "slices) + fill_borders, interleaved 1080p renders every 50 z; " + _SCENE},
+    "cfg2": {"dims": (1024, 1024, 1024),
+             "desc": "cfg2: synthetic SPIM-shaped 3-ch uint16 1024^3, 32^3 bricks, tau=0, "
+                     "full octree build + fill_borders; " + _SCENE},
+}
+WORKLOAD = WORKLOADS["cfg3"]["desc"]
 
 
 def scene_for(mod, dims, viewport, lod_bias=0.0, mode="dvr", precision=None):
@@ -161,10 +186,9 @@ def traffic_from_profiles(kernel):
 # our arm
 # ---------------------------------------------------------------------------
 
-def run_ours(args):
+def _setup_dist():
     import torch
     import torch.distributed as dist
-
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -179,17 +203,6 @@ def run_ours(args):
         else:
             dist.init_process_group(backend)
 
-    from paper_1407_2074_b200 import (BrickPoolConfig, DeviceState, Octree, VolumeDescriptor,
-                                      _lib)
-    from paper_1407_2074_b200 import render as R
-    from paper_1407_2074_b200.render.sharded import SortFirstRenderer
-
-    dims = tuple(args.dims)
-    desc = VolumeDescriptor(dims=dims, channels=CHANNELS, sample_format=FMT)
-    cfg = BrickPoolConfig(brick_dims=(BRICK,) * 3, homogeneity_threshold=0)
-    geo_bricks = expected_bricks(dims, BRICK)
-    stream = torch.cuda.current_stream()
-
     def barrier():
         if world > 1:
             if backend == "nccl":
@@ -197,45 +210,289 @@ def run_ours(args):
             else:
                 dist.barrier()
 
-    def tree_on_stream(t):
-        _lib.call("vt_tree_set_stream", t.handle, ct.c_void_p(stream.cuda_stream))
+    return world, rank, local, backend, barrier
 
-    # ---- synthetic volume: each rank synthesises (untimed) only the z-slab
-    # it ingests; the z-slab sharded build (slab_build.py) inserts it, one
-    # all-gather exchanges level <= k node records and every rank ends with
-    # the full tree (the replicated pool the sort-first render reads) ----
-    from paper_1407_2074_b200.slab_build import build_sharded, slab_plan
-    Z, Y, X = dims[2], dims[1], dims[0]
-    plan = slab_plan(expected_geometry(dims, BRICK), world)
-    sz0, sz1 = plan.slabs[rank]
-    vol = torch.empty((max(0, sz1 - sz0), Y, X, CHANNELS), dtype=torch.uint16, device="cuda")
-    if sz1 > sz0:
-        _lib.call("vt_synth", ct.c_void_p(vol.data_ptr()), 1, _lib.i32x3(dims), CHANNELS, 2, 0,
-                  sz0, sz1, ct.c_void_p(stream.cuda_stream))
-    raw_bytes = X * Y * Z * CHANNELS * 2  # whole job (all ranks)
 
-    def build(src):
-        tree = Octree(desc, cfg, reserve_slots=geo_bricks)
-        tree_on_stream(tree)
+def _rank_max(vals, world, backend):
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(vals, dtype=torch.float64, device="cuda" if backend == "nccl" else "cpu")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(v) for v in t.tolist()]
+
+
+def _synth(dims, z0, z1, stream):
+    """(z1 - z0, Y, X, C) interleaved S volume on the device (vt_synth ==
+    oracle synth_spim, hash-checked in tests/test_gpu_build.py)."""
+    import torch
+    from paper_1407_2074_b200 import _lib
+    v = torch.empty((max(0, z1 - z0), dims[1], dims[0], CHANNELS), dtype=torch.uint16,
+                    device="cuda")
+    if z1 > z0:
+        _lib.call("vt_synth", ct.c_void_p(v.data_ptr()), 1, _lib.i32x3(dims), CHANNELS, 2, 0,
+                  z0, z1, ct.c_void_p(stream.cuda_stream))
+    return v
+
+
+def _synth_planar(dims, stream, z0=0, z1=None, pin=False):
+    """(C, z1 - z0, Y, X) planar S volume: the layout a VSTR slice stream
+    lands in (one frame per channel per z); device, or pinned host."""
+    import torch
+    z1 = dims[2] if z1 is None else z1
+    X, Y = dims[0], dims[1]
+    if pin:
+        out = torch.empty((CHANNELS, z1 - z0, Y, X), dtype=torch.uint16, pin_memory=True)
+    else:
+        out = torch.empty((CHANNELS, z1 - z0, Y, X), dtype=torch.uint16, device="cuda")
+    step = 64
+    for a in range(z0, z1, step):
+        b = min(z1, a + step)
+        tmp = _synth(dims, a, b, stream)
+        out[:, a - z0:b - z0].copy_(tmp.permute(3, 0, 1, 2))
+        del tmp
+    torch.cuda.synchronize()
+    return out
+
+
+class _Ev:
+    """CUDA events on the bench stream around a region (device time)."""
+
+    def __init__(self, stream):
+        import torch
+        self.s = stream
+        self.a = torch.cuda.Event(enable_timing=True)
+        self.b = torch.cuda.Event(enable_timing=True)
+
+    def __enter__(self):
+        self.a.record(self.s)
+        return self
+
+    def __exit__(self, *exc):
+        self.b.record(self.s)
+
+    def ms(self):
+        return self.a.elapsed_time(self.b)
+
+
+def leg_stream(P, dims, stream, peak):
+    """Device-resident VSTR slice stream: every (z, channel) frame of the
+    planar volume P through Octree.insert_planar, one call per brick layer,
+    then finalize + fill_borders (ingest_stream, ingest.py:306-358); CUDA
+    events around the whole sequence (host gaps included)."""
+    import torch
+    from paper_1407_2074_b200 import BrickPoolConfig, Octree, VolumeDescriptor, _lib
+    desc = VolumeDescriptor(dims=dims, channels=CHANNELS, sample_format=FMT)
+    cfg = BrickPoolConfig(brick_dims=(BRICK,) * 3, homogeneity_threshold=0)
+    Z = dims[2]
+    raw = dims[0] * dims[1] * Z * CHANNELS * 2
+    res = None
+    for rep in range(3):  # warm-up, then two timed runs (best reported, both listed)
+        tree = Octree(desc, cfg, reserve_slots=expected_bricks(dims, BRICK))
+        _lib.call("vt_tree_set_stream", tree.handle, ct.c_void_p(stream.cuda_stream))
         torch.cuda.synchronize()
-        barrier()
-        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
-        e0.record(stream)
-        # device-resident volume: the rank's whole slab is one insertion;
-        # host (pinned) volume: brick-layer slabs, so H2D overlaps the build
-        slab = max(BRICK, sz1 - sz0) if hasattr(src, "is_cuda") else BRICK
-        build_sharded(tree, lambda a, b: src[a - sz0:b - sz0], slab_z=slab, fill_borders=False)
-        e1.record(stream)
+        with _Ev(stream) as ev:
+            for z0 in range(0, Z, BRICK):
+                tree.insert_planar(P[:, z0:min(Z, z0 + BRICK)], z0)
+            with _Ev(stream) as evb:
+                tree.finalize()
+                tree.fill_borders()
+                tree.sync()
+        torch.cuda.synchronize()
+        ms = ev.ms()
+        pool = tree.brick_count * cfg.brick_nbytes(desc)
+        groups, in_place, _ = tree.stream_counts()
+        run = {"ms": round(ms, 3), "fill_borders_ms": round(evb.ms(), 3)}
+        if rep == 0:
+            tree.close()
+            del tree
+            continue
+        if res is None or ms < res["ms"]:
+            alg = (raw + pool) / (ms * 1e-3) / 1e9
+            res = {"workload": f"{dims[0]}x{dims[1]}x{Z} x{CHANNELS} uint16 S volume, planar "
+                               "(C, Z, Y, X) in HBM, every (z, channel) slice in VSTR order "
+                               "through Octree.insert_planar (= insert_block per slice), one "
+                               "call per brick layer, + finalize + fill_borders",
+                   "slices": Z * CHANNELS, "ms": round(ms, 3),
+                   "fill_borders_ms": round(evb.ms(), 3),
+                   "raw_gb": round(raw / 1e9, 3), "pool_gb": round(pool / 1e9, 3),
+                   "gbs_raw": round(raw / (ms * 1e-3) / 1e9, 2),
+                   "layer_groups": groups, "layers_read_in_place": in_place,
+                   "roofline": {"achieved": round(alg, 2), "peak": peak,
+                                "frac": round(alg / peak, 4), "unit": "GB/s",
+                                "model": "(raw + pool bytes) / stream time (SURVEY 8d: "
+                                         "1 + pool/raw B per raw byte)"},
+                   "tree_checksum": f"{tree.checksum():016x}"}
+        res.setdefault("runs_ms", []).append(round(ms, 3))
+        tree.close()
+        del tree
+        torch.cuda.empty_cache()
+    return res
+
+
+def leg_stream_interleaved(P, dims, stream, viewport, every_z, precision):
+    """The stream again with a 1920x1080 frame after every `every_z` slices
+    (a FrameService-style live view: refresh the mirror — flush, incremental
+    brick maxima — then render); returns the numbers and the final tree."""
+    import torch
+    from paper_1407_2074_b200 import (BrickPoolConfig, DeviceState, Octree, VolumeDescriptor,
+                                      _lib)
+    from paper_1407_2074_b200 import render as R
+    desc = VolumeDescriptor(dims=dims, channels=CHANNELS, sample_format=FMT)
+    cfg = BrickPoolConfig(brick_dims=(BRICK,) * 3, homogeneity_threshold=0)
+    Z = dims[2]
+    tree = Octree(desc, cfg, reserve_slots=expected_bricks(dims, BRICK))
+    _lib.call("vt_tree_set_stream", tree.handle, ct.c_void_p(stream.cuda_stream))
+    dev = DeviceState(tree, resident_all=True)
+    rr = R.OutOfCoreRenderer(dev)
+    scene = scene_for(R, dims, viewport, precision=precision)
+    ins, ref, fr, slots = [], [], [], []
+    torch.cuda.synchronize()
+    with _Ev(stream) as tot:
+        for z0 in range(0, Z, every_z):
+            z1 = min(Z, z0 + every_z)
+            with _Ev(stream) as e1:
+                tree.insert_planar(P[:, z0:z1], z0)
+            with _Ev(stream) as e2:
+                dev.refresh()
+            with _Ev(stream) as e3:
+                img, cnt = rr.render_fullframe(scene, out_kind=R.raycast.OUT_RGBA8)
+            ins.append(e1)
+            ref.append(e2)
+            fr.append((e3, cnt.samples))
+            slots.append(dev.bmax_stats()[1])
         tree.finalize()
         tree.fill_borders()
         tree.sync()
-        e2.record(stream)
-        torch.cuda.synchronize()
-        return tree, e0.elapsed_time(e1), e1.elapsed_time(e2)
+    torch.cuda.synchronize()
+    ins_ms = [e.ms() for e in ins]
+    ref_ms = [e.ms() for e in ref]
+    fr_ms = [e.ms() for e, _ in fr]
+    out = {"every_z": every_z, "frames": len(fr_ms),
+           "total_ms": round(tot.ms(), 2),
+           "ingest_ms": round(sum(ins_ms), 2),
+           "mirror_refresh_ms_mean": round(statistics.mean(ref_ms), 3),
+           "mirror_refresh_ms_max": round(max(ref_ms), 3),
+           "bmax_slots_per_refresh_mean": int(statistics.mean(slots)),
+           "frame_ms_mean": round(statistics.mean(fr_ms), 3),
+           "frame_ms_max": round(max(fr_ms), 3),
+           "samples_last_frame": int(fr[-1][1]),
+           "note": "refresh = drain events + node-buffer repack + brick maxima of the slots "
+                   "written since the last frame (flushing any partial brick layer); frame = "
+                   "render kernel + RGBA8 copy-out"}
+    dev.close()
+    return out, tree
 
-    # untimed warm-up build (first launches load kernel modules, encode
-    # tensor maps, page-lock staging), then three timed builds: the median
-    # (by total time) is reported, the last tree is kept for rendering
+
+def leg_frames(tree, dims, viewport, args, stream, barrier, world, rank, backend, sweep=True):
+    """K flushed 1080p frames (sort-first strips over the ranks), the LOD
+    sweep and the e2e frames through the public API."""
+    import torch
+    from paper_1407_2074_b200 import DeviceState, _lib
+    from paper_1407_2074_b200 import render as R
+    from paper_1407_2074_b200.render.sharded import SortFirstRenderer
+    dev = DeviceState(tree, resident_all=True)
+    scene = scene_for(R, dims, tuple(viewport), precision=args.precision)
+    sfr = SortFirstRenderer(dev, strip_rows=args.strip_rows)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device="cuda")
+
+    def frame(sc):
+        img, cnt = sfr.render_fullframe(sc, out_kind=R.raycast.OUT_RGBA8)
+        return cnt
+
+    times, kms, samples, skipped, launches = [], [], 0, 0, 0
+    with Clocks(torch.cuda.current_device()) as clk:
+        for it in range(args.warmup + args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            barrier()
+            with _Ev(stream) as ev:
+                cnt = frame(scene)
+            torch.cuda.synchronize()
+            if it >= args.warmup:
+                times.append(ev.ms())
+                rms = ct.c_double()
+                _lib.call("vt_last_kernel_ms", tree.handle, ct.byref(rms), None)
+                kms.append(rms.value)
+                samples += cnt.samples
+                skipped += cnt.samples_skipped
+                launches += 1
+    clocks = clk.summary()
+    t = _rank_max(times, world, backend)
+    total_ms = sum(t)
+    out = {"frame_ms": total_ms / args.steps,
+           "value": samples / (total_ms * 1e-3) / 1e9,
+           "kernel_ms": statistics.mean(kms),
+           "samples_per_frame": samples / args.steps,
+           "computed_per_frame": (samples - skipped) / args.steps,
+           "launches": launches, "clocks": clocks}
+    if sweep:
+        sw = {}
+        for bias in (-1.0, 0.0, 1.0, 2.0, 3.0):
+            sc = scene_for(R, dims, tuple(viewport), lod_bias=bias, precision=args.precision)
+            flush.zero_()
+            torch.cuda.synchronize()
+            barrier()
+            with _Ev(stream) as ev:
+                cnt = frame(sc)
+            torch.cuda.synchronize()
+            ms = _rank_max([ev.ms()], world, backend)[0]
+            sw[f"{bias:+.0f}"] = {"frame_ms": round(ms, 3), "samples": cnt.samples,
+                                  "gsamples_s": round(cnt.samples / (ms * 1e-3) / 1e9, 3)}
+        out["lod_sweep"] = sw
+    # e2e: public drop-in API, float64 image to host every frame
+    e2e_times, e2e_samples = [], 0
+    rr = R.OutOfCoreRenderer(dev)
+    for it in range(args.warmup + args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        barrier()
+        with _Ev(stream) as ev:
+            if world == 1:
+                img, cnt = rr.render_fullframe(scene)
+            else:
+                img, cnt = sfr.render_fullframe(scene, out_kind=R.raycast.OUT_F64, to_host=True)
+        torch.cuda.synchronize()
+        if it >= args.warmup:
+            e2e_times.append(ev.ms())
+            e2e_samples += cnt.samples
+    t = _rank_max(e2e_times, world, backend)
+    out["e2e_value"] = e2e_samples / (sum(t) * 1e-3) / 1e9
+    dev.close()
+    return out
+
+
+def leg_whole_build(dims, stream, barrier, world, rank, backend, host_e2e):
+    """Whole-volume device build (z-slab sharded over the ranks): each rank
+    inserts its slab in one Octree.insert_channels call (ingest_bulk),
+    one all-gather of level-k records, fill_borders; median of three."""
+    import torch
+    import torch.distributed as dist
+    from paper_1407_2074_b200 import BrickPoolConfig, Octree, VolumeDescriptor, _lib
+    from paper_1407_2074_b200.slab_build import build_sharded, slab_plan
+    desc = VolumeDescriptor(dims=dims, channels=CHANNELS, sample_format=FMT)
+    cfg = BrickPoolConfig(brick_dims=(BRICK,) * 3, homogeneity_threshold=0)
+    plan = slab_plan(expected_geometry(dims, BRICK), world)
+    sz0, sz1 = plan.slabs[rank]
+    vol = _synth(dims, sz0, sz1, stream)
+    raw_bytes = dims[0] * dims[1] * dims[2] * CHANNELS * 2
+
+    def build(src):
+        tree = Octree(desc, cfg, reserve_slots=expected_bricks(dims, BRICK))
+        _lib.call("vt_tree_set_stream", tree.handle, ct.c_void_p(stream.cuda_stream))
+        torch.cuda.synchronize()
+        barrier()
+        with _Ev(stream) as e1:
+            slab = max(BRICK, sz1 - sz0) if hasattr(src, "is_cuda") else BRICK
+            build_sharded(tree, lambda a, b: src[a - sz0:b - sz0], slab_z=slab,
+                          fill_borders=False)
+        with _Ev(stream) as e2:
+            tree.finalize()
+            tree.fill_borders()
+            tree.sync()
+        torch.cuda.synchronize()
+        return tree, e1.ms(), e2.ms()
+
     wt, _, _ = build(vol)
     wt.close()
     del wt
@@ -250,249 +507,185 @@ def run_ours(args):
             torch.cuda.empty_cache()
     _, build_ms, border_ms = sorted(runs)[1]
     pool_bytes = tree.brick_count * cfg.brick_nbytes(desc)
-    # every rank must hold the same tree after the sharded build
     ck = tree.checksum()
     replicas_identical = True
     if world > 1:
         cks = [None] * world
         dist.all_gather_object(cks, ck)
         replicas_identical = all(c == ck for c in cks)
-    # host-slab (pinned) build through the same public call: e2e ingest
-    host = vol.cpu().pin_memory() if args.build_e2e else None
-    del vol
-    torch.cuda.empty_cache()
     build_e2e_ms = None
-    if host is not None:
-        # one untimed pass first (staging-pool growth, first H2D of the
-        # pinned block), then the timed one, as for the device builds
+    if host_e2e:
+        host = vol.cpu().pin_memory()
+        del vol
+        torch.cuda.empty_cache()
         for _ in range(2):
             t2, build_e2e_ms, _ = build(host.numpy())
             t2.close()
             del t2
         del host
+    else:
+        del vol
+    torch.cuda.empty_cache()
+    build_ms, border_ms, build_e2e_ms = _rank_max([build_ms, border_ms, build_e2e_ms or 0.0],
+                                                  world, backend)
+    total = build_ms + border_ms
+    alg = (raw_bytes + pool_bytes) / (total * 1e-3) / 1e9
+    peak, _ = hbm_peak()
+    info = {"raw_gb": round(raw_bytes / 1e9, 3), "pool_gb": round(pool_bytes / 1e9, 3),
+            "bricks": tree.brick_count, "build_ms": round(total, 2),
+            "build_runs_ms": [round(r[0], 2) for r in runs],
+            "insert_ms": round(build_ms, 2), "fill_borders_ms": round(border_ms, 2),
+            "gbs_raw": round(raw_bytes / (total * 1e-3) / 1e9, 2),
+            "roofline": {"achieved": round(alg, 2), "peak": peak, "frac": round(alg / peak, 4),
+                         "unit": "GB/s",
+                         "model": "(raw + pool bytes) / (insert + fill_borders) time"},
+            "e2e_gbs_raw": round(raw_bytes / (build_e2e_ms * 1e-3) / 1e9, 2)
+            if build_e2e_ms else None,
+            "e2e_api": "Octree.insert_channels(pinned host slabs, 32 z each)",
+            "api": "Octree.insert_channels(device-resident slab) [z-slab sharded: "
+                   "slab_build.build_sharded]",
+            "sharding": f"z-slab x{world}, level-k={plan.level} records all-gathered"
+            if world > 1 else "single GPU",
+            "tree_checksum": f"{ck:016x}", "replicas_identical": replicas_identical}
+    return tree, info
+
+
+def leg_stream_host(dims, stream, nz):
+    """End-to-end host -> tree ingest of the first nz slices: pinned planar
+    host frames through Octree.insert_planar (H2D inside the timed region)."""
+    import torch
+    from paper_1407_2074_b200 import BrickPoolConfig, Octree, VolumeDescriptor, _lib
+    H = _synth_planar(dims, stream, 0, nz, pin=True)
+    desc = VolumeDescriptor(dims=dims, channels=CHANNELS, sample_format=FMT)
+    cfg = BrickPoolConfig(brick_dims=(BRICK,) * 3, homogeneity_threshold=0)
+    raw = dims[0] * dims[1] * nz * CHANNELS * 2
+    best = None
+    for rep in range(2):
+        tree = Octree(desc, cfg, reserve_slots=expected_bricks(dims, BRICK))
+        _lib.call("vt_tree_set_stream", tree.handle, ct.c_void_p(stream.cuda_stream))
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        with _Ev(stream) as ev:
+            for z0 in range(0, nz, BRICK):
+                tree.insert_planar(H[:, z0:min(nz, z0 + BRICK)].numpy(), z0)
+            tree.sync()
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        if rep and (best is None or ev.ms() < best[0]):
+            best = (ev.ms(), wall)
+        tree.close()
+        del tree
+    del H
+    torch.cuda.empty_cache()
+    return {"sample": f"first {nz} slices x {CHANNELS} channels ({raw / 1e9:.2f} GB), pinned "
+                      "host planar frames, one insert_planar call per brick layer",
+            "ms": round(best[0], 2), "gbs_raw": round(raw / (best[0] * 1e-3) / 1e9, 2),
+            "wall_ms": round(best[1] * 1e3, 2),
+            "h2d_bytes": raw}
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    world, rank, local, backend, barrier = _setup_dist()
+    from paper_1407_2074_b200 import _lib
+    stream = torch.cuda.current_stream()
+    peak, peak_kind = hbm_peak()
+    wl = WORKLOADS[args.workload]
+    dims = tuple(args.dims) if args.dims else wl["dims"]
+    viewport = tuple(args.viewport)
+    extra = {}
+    if world == 1 and args.workload == "cfg3":
+        P = _synth_planar(dims, stream)
+        stream_res = leg_stream(P, dims, stream, peak) if args.stream else None
+        inter, tree = leg_stream_interleaved(P, dims, stream, viewport, args.render_every,
+                                             args.precision)
+        del P
         torch.cuda.empty_cache()
-
-    dev = DeviceState(tree, resident_all=True)
-    scene = scene_for(R, dims, tuple(args.viewport), precision=args.precision)
-    sfr = SortFirstRenderer(dev, strip_rows=args.strip_rows)
-    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device="cuda")
-
-    def frame(sc):
-        img, cnt = sfr.render_fullframe(sc, out_kind=R.raycast.OUT_RGBA8)
-        return cnt
-
-    times, kms, samples, skipped = [], [], 0, 0
-    launches = 0
-    with Clocks(local) as clk:
-        for it in range(args.warmup + args.steps):
-            flush.zero_()
-            torch.cuda.synchronize()
-            barrier()
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            cnt = frame(scene)
-            e1.record(stream)
-            torch.cuda.synchronize()
-            if it >= args.warmup:
-                times.append(e0.elapsed_time(e1))
-                rms = ct.c_double()
-                _lib.call("vt_last_kernel_ms", tree.handle, ct.byref(rms), None)
-                kms.append(rms.value)
-                samples += cnt.samples
-                skipped += cnt.samples_skipped
-                launches += 1
-    clocks = clk.summary()
-    rdev = "cuda" if backend == "nccl" else "cpu"
-    t = torch.tensor(times, dtype=torch.float64, device=rdev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t.sum())
-    frame_ms = total_ms / args.steps
-    value = samples / (total_ms * 1e-3) / 1e9
-    kernel_ms = statistics.mean(kms)
-    samples_per_frame = samples / args.steps
-    computed_per_frame = (samples - skipped) / args.steps
-
-    # LOD sweep (one flushed frame each, rank-max)
-    sweep = {}
-    for bias in (-1.0, 0.0, 1.0, 2.0, 3.0):
-        sc = scene_for(R, dims, tuple(args.viewport), lod_bias=bias, precision=args.precision)
-        flush.zero_()
-        torch.cuda.synchronize()
-        barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        cnt = frame(sc)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        tt = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=rdev)
-        if world > 1:
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt[0])
-        sweep[f"{bias:+.0f}"] = {"frame_ms": round(ms, 3), "samples": cnt.samples,
-                                 "gsamples_s": round(cnt.samples / (ms * 1e-3) / 1e9, 3)}
-
-    # e2e: public drop-in API, float64 image to host every frame
-    W, H = args.viewport
-    e2e_times, e2e_samples = [], 0
-    rr = R.OutOfCoreRenderer(dev)
-    for it in range(args.warmup + args.steps):
-        flush.zero_()
-        torch.cuda.synchronize()
-        barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        if world == 1:
-            img, cnt = rr.render_fullframe(scene)
-        else:
-            img, cnt = sfr.render_fullframe(scene, out_kind=R.raycast.OUT_F64, to_host=True)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        if it >= args.warmup:
-            e2e_times.append(e0.elapsed_time(e1))
-            e2e_samples += cnt.samples
-    t = torch.tensor(e2e_times, dtype=torch.float64, device=rdev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    e2e_value = e2e_samples / (float(t.sum()) * 1e-3) / 1e9
-
-    # build numbers: max over ranks (each rank builds its replica)
-    bt = torch.tensor([build_ms, border_ms, build_e2e_ms or 0.0], dtype=torch.float64,
-                      device=rdev)
-    if world > 1:
-        dist.all_reduce(bt, op=dist.ReduceOp.MAX)
-    build_ms, border_ms, build_e2e_ms = (float(v) for v in bt.tolist())
-
+        build_info = None
+        extra["stream"] = stream_res
+        extra["stream_interleaved"] = inter
+    else:
+        tree, build_info = leg_whole_build(dims, stream, barrier, world, rank, backend,
+                                           host_e2e=args.build_e2e)
+    fr = leg_frames(tree, dims, viewport, args, stream, barrier, world, rank, backend)
+    pool_bytes = tree.brick_count * tree.config.brick_nbytes(tree.descriptor)
+    tree_ck = f"{tree.checksum():016x}"
+    tree.close()
+    del tree
+    torch.cuda.empty_cache()
+    if world == 1 and args.workload == "cfg3" and args.build_e2e:
+        extra["stream_e2e"] = leg_stream_host(dims, stream, min(dims[2], 256))
+    if world == 1 and args.workload == "cfg3" and args.secondary:
+        d2 = WORKLOADS["cfg2"]["dims"]
+        t2, b2 = leg_whole_build(d2, stream, barrier, world, rank, backend, host_e2e=False)
+        f2 = leg_frames(t2, d2, viewport, args, stream, barrier, world, rank, backend,
+                        sweep=False)
+        t2.close()
+        del t2
+        torch.cuda.empty_cache()
+        extra["cfg2"] = {"workload": WORKLOADS["cfg2"]["desc"], "frame_ms": round(f2["frame_ms"], 4),
+                         "gsamples_s": round(f2["value"], 3),
+                         "render_kernel_ms": round(f2["kernel_ms"], 4),
+                         "samples_per_frame": int(f2["samples_per_frame"]),
+                         "samples_computed_per_frame": int(f2["computed_per_frame"]),
+                         "e2e_gsamples_s": round(f2["e2e_value"], 3), "build": b2}
     if rank == 0:
-        peak, peak_kind = hbm_peak()
-        # only the samples the kernel actually reconstructs gather bricks
-        achieved = computed_per_frame / max(world, 1) * BYTES_PER_POS_SAMPLE / (kernel_ms * 1e-3) / 1e9
-        # the build = insertion + fill_borders (ingest_bulk, ingest.py:182-224)
-        total_build_ms = build_ms + border_ms
-        build_gbs = raw_bytes / (total_build_ms * 1e-3) / 1e9
-        build_alg = (raw_bytes + pool_bytes) / (total_build_ms * 1e-3) / 1e9
+        achieved = fr["computed_per_frame"] / max(world, 1) * BYTES_PER_POS_SAMPLE / (
+            fr["kernel_ms"] * 1e-3) / 1e9
+        W, H = viewport
         out = {
             "metric": "Gsamples/s (3-ch pos-samples, 1920x1080 frame); frame ms; octree build GB/s",
-            "value": round(value, 4),
+            "value": round(fr["value"], 4),
             "unit": "Gsamples/s",
             "n_gpus": world,
             "steps": args.steps,
             "warmup": args.warmup,
-            "ms_per_step": round(frame_ms, 4),
-            "frame_ms": round(frame_ms, 4),
+            "ms_per_step": round(fr["frame_ms"], 4),
+            "frame_ms": round(fr["frame_ms"], 4),
             "higher_is_better": True,
             "scaling": "strong",
             "vs_baseline": None,
             "dtype": "f64" if args.precision == "fp64" else "f32 reconstruction / f64 accumulation",
             "data": "synthetic (SPIM-shaped S volume, generated on device, seed 0)",
-            "config": {"workload": WORKLOAD, "dims": list(dims), "channels": CHANNELS,
-                       "sample_format": FMT, "brick": BRICK, "viewport": list(args.viewport),
+            "config": {"workload": wl["desc"], "dims": list(dims), "channels": CHANNELS,
+                       "sample_format": FMT, "brick": BRICK, "viewport": list(viewport),
                        "parallelism": f"sort-first strips x{world} (strip_rows={args.strip_rows})"
                        if world > 1 else "single GPU",
                        "l2": f"flushed between frames (512 MB write); pool "
                              f"{pool_bytes / 1e9:.1f} GB vs 126 MB L2"},
-            "samples_per_frame": int(samples_per_frame),
-            "samples_computed_per_frame": int(computed_per_frame),
+            "samples_per_frame": int(fr["samples_per_frame"]),
+            "samples_computed_per_frame": int(fr["computed_per_frame"]),
             "samples_note": "samples = the reference's RenderCounters.samples (identical); "
                             "computed = samples minus those the exact empty-space skip "
                             "accounted without reconstructing (TF alpha provably 0)",
-            "render_kernel_ms": round(kernel_ms, 4),
-            "gpu_launches": launches,
+            "render_kernel_ms": round(fr["kernel_ms"], 4),
+            "gpu_launches": fr["launches"],
             "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": round(achieved / peak, 4),
                          "traffic": traffic_from_profiles("k_render_fullframe"),
                          "model": "48 B gathered per computed pos-sample / avg render kernel "
                                   "ms (rank 0)"},
-            "e2e": {"value": round(e2e_value, 4), "unit": "Gsamples/s",
+            "e2e": {"value": round(fr["e2e_value"], 4), "unit": "Gsamples/s",
                     "h2d_bytes_per_step": ct.sizeof(_lib.vt_scene),
                     "d2h_bytes_per_step": W * H * 4 * 8 + 48,
                     "api": "OutOfCoreRenderer.render_fullframe -> float64 (H,W,4) page-locked host "
                            "frame (N=1: the kernel writes it over PCIe)"
                     if world == 1 else "SortFirstRenderer.render_fullframe(to_host=True)"},
-            "build": {"raw_gb": round(raw_bytes / 1e9, 3), "pool_gb": round(pool_bytes / 1e9, 3),
-                      "bricks": tree.brick_count, "build_ms": round(total_build_ms, 2),
-                      "build_runs_ms": [round(r[0], 2) for r in runs],
-                      "insert_ms": round(build_ms, 2),
-                      "fill_borders_ms": round(border_ms, 2),
-                      "gbs_raw": round(build_gbs, 2),
-                      "roofline": {"achieved": round(build_alg, 2), "peak": peak,
-                                   "frac": round(build_alg / peak, 4), "unit": "GB/s",
-                                   "model": "(raw + pool bytes) / (insert + fill_borders) time"},
-                      "e2e_gbs_raw": round(raw_bytes / (build_e2e_ms * 1e-3) / 1e9, 2)
-                      if build_e2e_ms else None,
-                      "e2e_api": "Octree.insert_channels(pinned host slabs, 32 z each)",
-                      "sharding": f"z-slab x{world}, level-k={plan.level} records all-gathered"
-                      if world > 1 else "single GPU",
-                      "tree_checksum": f"{ck:016x}", "replicas_identical": replicas_identical},
-            "lod_sweep": sweep,
-            "clocks": clocks,
+            "tree_checksum": tree_ck,
+            "lod_sweep": fr.get("lod_sweep"),
+            "clocks": fr["clocks"],
         }
-        if world == 1 and args.stream:
-            out["stream"] = stream_ingest(args, peak)
+        if build_info is not None:
+            out["build"] = build_info
+        out.update(extra)
         if world == 1 and not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(args)
         print(json.dumps(out), flush=True)
     if world > 1:
         barrier()
         dist.destroy_process_group()
-
-
-STREAM_DIMS = (2048, 2048, 64)  # cfg3's slice shape, two brick layers
-
-
-def stream_ingest(args, peak):
-    """cfg3-shaped slice stream (ingest_stream's VSTR order: per z, one
-    single-channel 2048x2048 block per channel) through Octree.insert_block
-    from device-resident slices, then finalize + fill_borders; CUDA events on
-    the tree's stream around the whole sequence (host gaps included)."""
-    import torch
-    from paper_1407_2074_b200 import BrickPoolConfig, Octree, VolumeDescriptor, _lib
-    dims = STREAM_DIMS
-    X, Y, Z = dims
-    st = torch.cuda.current_stream()
-    vol = torch.empty((Z, Y, X, CHANNELS), dtype=torch.uint16, device="cuda")
-    _lib.call("vt_synth", ct.c_void_p(vol.data_ptr()), 1, _lib.i32x3(dims), CHANNELS, 2, 0, 0, Z,
-              ct.c_void_p(st.cuda_stream))
-    planes = [vol[..., c].contiguous() for c in range(CHANNELS)]
-    del vol
-    desc = VolumeDescriptor(dims=dims, channels=CHANNELS, sample_format=FMT)
-    cfg = BrickPoolConfig(brick_dims=(BRICK,) * 3, homogeneity_threshold=0)
-    res = None
-    for rep in range(2):  # warm-up, then timed
-        tree = Octree(desc, cfg, reserve_slots=expected_bricks(dims, BRICK))
-        _lib.call("vt_tree_set_stream", tree.handle, ct.c_void_p(st.cuda_stream))
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(st)
-        for z in range(Z):
-            for c in range(CHANNELS):
-                tree.insert_block(c, (0, 0, z), planes[c][z:z + 1])
-        tree.finalize()
-        tree.fill_borders()
-        tree.sync()
-        e1.record(st)
-        torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1)
-        raw = X * Y * Z * CHANNELS * 2
-        pool = tree.brick_count * cfg.brick_nbytes(desc)
-        res = {"workload": f"cfg3-shaped slice stream {X}x{Y}x{Z} x{CHANNELS} uint16, one "
-                           "single-channel slice per insert_block (VSTR order), device-resident "
-                           "slices, + finalize + fill_borders",
-               "inserts": Z * CHANNELS, "ms": round(ms, 2),
-               "gbs_raw": round(raw / (ms * 1e-3) / 1e9, 2),
-               "roofline": {"achieved": round((raw + pool) / (ms * 1e-3) / 1e9, 2), "peak": peak,
-                            "frac": round((raw + pool) / (ms * 1e-3) / 1e9 / peak, 4),
-                            "unit": "GB/s", "model": "(raw + pool bytes) / stream time"},
-               "tree_checksum": f"{tree.checksum():016x}"}
-        tree.close()
-        del tree
-    del planes
-    torch.cuda.empty_cache()
-    return res
 
 
 def expected_geometry(dims, m):
@@ -516,8 +709,37 @@ def expected_bricks(dims, m):
 # reference (CPU) arm and the cpu_baseline leg
 # ---------------------------------------------------------------------------
 
+# bounded sample of the workload for the CPU reference: the central 128^3
+# sub-box of the cfg3 S volume (the same voxel values), the bench scene
+# around it
 CPU_DIMS = (128, 128, 128)
+CPU_CROP = (960, 960, 436)  # x, y, z origin of the sub-box in the 2048x2048x1000 volume
 CPU_VIEW_BASE = (192, 108)
+
+
+def _cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return None
+
+
+def _cpu_volume():
+    import voxtree_oracle as vo
+    x0, y0, z0 = CPU_CROP
+    d = WORKLOADS["cfg3"]["dims"]
+    return vo.synth_spim(d, CHANNELS, 65535, seed=0, z0=z0, z1=z0 + CPU_DIMS[2], y0=y0,
+                         y1=y0 + CPU_DIMS[1], x0=x0, x1=x0 + CPU_DIMS[0])
+
+
+def _cpu_sample_text(view, extra=""):
+    return (f"central {CPU_DIMS[0]}^3 sub-box of the cfg3 S volume (origin {CPU_CROP}), 32^3 "
+            f"bricks, tau 0, the bench scene around it at {view[0]}x{view[1]}, all bricks "
+            f"resident{extra}")
 
 
 def _reference_modules():
@@ -545,7 +767,7 @@ def _cpu_setup():
     import numpy as np
     import voxtree_oracle as vo
     kind, vr = _reference_modules()
-    vol = vo.synth_spim(CPU_DIMS, CHANNELS, 65535, seed=0)
+    vol = _cpu_volume()
     t0 = time.perf_counter()
     if kind == "reference":
         from voxtree.device import DeviceState, RenderMode
@@ -615,10 +837,8 @@ def cpu_baseline(args):
     samples = _cpu_render(view, (0, 0, view[0], view[1]))
     dt = time.perf_counter() - t0
     return {"value": round(samples / dt / 1e9, 8), "unit": "Gsamples/s", "cores": 1,
-            "kind": st["kind"],
-            "sample": f"S volume {CPU_DIMS[0]}^3 x3 uint16, 32^3 bricks, same scene at "
-                      f"{view[0]}x{view[1]}, all bricks resident: {samples} pos-samples "
-                      f"in {dt:.2f} s",
+            "kind": st["kind"], "cpu_model": _cpu_model(), "nproc": os.cpu_count(),
+            "sample": _cpu_sample_text(view, f": {samples} pos-samples in {dt:.2f} s"),
             "build_gbs_raw": round(st["build_gbs"], 5)}
 
 
@@ -646,17 +866,21 @@ def run_reference(args):
     total = sum(times)
     v = samples / total / 1e9
     st = _CPU_STATE
-    sample = (f"S volume {CPU_DIMS[0]}^3 x3 uint16, 32^3 bricks, same scene at {view[0]}x{view[1]} "
-              f"split in {len(jobs)} row tiles over {cores} processes, all bricks resident")
+    wl = WORKLOADS[args.workload]
+    dims = tuple(args.dims) if args.dims else wl["dims"]
+    sample = _cpu_sample_text(view, f", split in {len(jobs)} row tiles over {cores} processes "
+                                    "(tile-restricted RefinementSession each)")
     print(json.dumps({
         "impl": "reference", "metric": "Gsamples/s (3-ch pos-samples, 1920x1080 frame); frame ms; "
         "octree build GB/s", "value": round(v, 8), "unit": "Gsamples/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(total / args.steps * 1e3, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "sample": sample},
+        "config": {"workload": wl["desc"], "dims": list(dims), "channels": CHANNELS,
+                   "sample_format": FMT, "brick": BRICK, "viewport": list(args.viewport),
+                   "sample": sample},
         "cpu_baseline": {"value": round(v, 8), "unit": "Gsamples/s", "cores": cores,
-                         "kind": st["kind"], "sample": sample},
+                         "kind": st["kind"], "cpu_model": _cpu_model(), "sample": sample},
         "e2e": {"value": round(v, 8), "unit": "Gsamples/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "build_gbs_raw": round(st["build_gbs"], 5)}), flush=True)
@@ -668,15 +892,21 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--dims", type=int, nargs=3, default=list(DIMS))
+    ap.add_argument("--workload", choices=tuple(WORKLOADS), default="cfg3")
+    ap.add_argument("--dims", type=int, nargs=3, default=None,
+                    help="override the workload's volume extent (x y z)")
     ap.add_argument("--viewport", type=int, nargs=2, default=list(VIEWPORT))
     ap.add_argument("--strip-rows", type=int, default=8)
+    ap.add_argument("--render-every", type=int, default=50,
+                    help="slices between the interleaved renders of the stream leg")
     ap.add_argument("--precision", choices=("fp64", "fp32"), default="fp64",
                     help="sample reconstruction precision (RenderSettings.precision)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-build-e2e", dest="build_e2e", action="store_false")
     ap.add_argument("--no-stream", dest="stream", action="store_false",
-                    help="skip the cfg3-shaped slice-stream ingest measurement")
+                    help="skip the pure stream-ingest measurement")
+    ap.add_argument("--no-secondary", dest="secondary", action="store_false",
+                    help="skip the cfg2 secondary leg")
     args = ap.parse_args()
     if args.warmup < 3:  # timing rule: at least 3 untimed warm-up steps
         args.warmup = 3

@@ -129,6 +129,27 @@ vt_status vt_tree_insert(vt_tree* tree, int32_t channel, const int32_t origin[3]
 vt_status vt_tree_insert_channels(vt_tree* tree, const int32_t origin[3],
                                   const int32_t dims[3], const void* samples,
                                   int32_t mem_kind);
+/* B200 extension: a batch of insertions in one call — the same tree and the
+ * same queued change events (drained with vt_tree_take_events) as n
+ * successive vt_tree_insert calls in order; what ingest_stream's frame loop
+ * (ingest.py:306-358) does per VSTR frame.  All blocks share `mem_kind` and
+ * are borrowed for the duration of the call (device blocks: ordered after
+ * caller_stream, which waits for the reads).  At threshold 0, consecutive
+ * single-channel blocks spanning the full x/y extent that cover every
+ * (z, channel) of one brick layer exactly once become one dense insertion
+ * (a device layer whose blocks sit at an affine stride, e.g. slices of a
+ * planar (C, Z, Y, X) volume, is read in place through a 4-D TMA tensor
+ * map).  An invalid block raises after the blocks before it are inserted,
+ * as the loop would. */
+typedef struct {
+  int32_t channel;   /* 0..C-1 */
+  int32_t origin[3]; /* x, y, z */
+  int32_t dims[3];   /* x, y, z extent of values (dz, dy, dx), x-fastest */
+  int32_t pad;
+  const void* samples;
+} vt_block;
+vt_status vt_tree_insert_many(vt_tree* tree, int64_t n, const vt_block* blocks, int32_t mem_kind,
+                              void* caller_stream);
 /* move pending change events out (Octree.drain_events, octree.py:180-183);
  * *n returns the number written (<= cap); call again while *more != 0 */
 vt_status vt_tree_take_events(vt_tree* tree, int32_t* kinds, int64_t* indices, int64_t cap,
@@ -153,6 +174,16 @@ vt_status vt_tree_info_get(vt_tree* tree, vt_tree_info* out);
 vt_status vt_tree_set_dense(vt_tree* tree, int32_t enabled);
 vt_status vt_tree_dense_counts(vt_tree* tree, int64_t* leaf_inserts, int64_t* level_nodes,
                                int64_t* fast_borders);
+/* B200 extension: brick layers built as one dense insertion by
+ * vt_tree_insert_many (of which read in place), and deferred layers of
+ * per-block slice streams (diagnostics for tests and the bench) */
+vt_status vt_tree_stream_counts(vt_tree* tree, int64_t* layer_groups, int64_t* zero_copy_layers,
+                                int64_t* deferred_layers);
+/* B200 extension: leaf shells the dense build prefilled with their
+ * fill_borders values are the reference's background until fill_borders
+ * (octree.py:234-237); every pool reader publishes them first — call this
+ * before reading the pool through a zero-copy alias */
+vt_status vt_tree_publish_halos(vt_tree* tree);
 /* Octree.node_by_index (octree.py:515-528): *exists = 0 when absent */
 vt_status vt_tree_node(vt_tree* tree, int64_t index, vt_node* out, int32_t* exists);
 /* Octree.iter_nodes order (BFS == ascending index, octree.py:507-513);
@@ -210,6 +241,10 @@ vt_status vt_mirror_create(vt_tree* tree, int64_t slot_count, vt_mirror** out);
 vt_status vt_mirror_destroy(vt_mirror* m);
 /* device pointers + sizes of node_buffer (u64[capacity]), flag_buffer
  * (u8[capacity]) and brick_buffer ([slots, bz, by, bx, C]) */
+/* B200 extension: brick-maxima refreshes of a zero-copy mirror done
+ * incrementally (only pool slots written since the last refresh) and the
+ * slot count of the last refresh */
+vt_status vt_mirror_bmax_stats(vt_mirror* m, int64_t* incremental, int64_t* last_slots);
 vt_status vt_mirror_buffers(vt_mirror* m, void** node_buffer, void** flag_buffer,
                             void** brick_buffer, int64_t* capacity, int64_t* slots);
 /* residency edits: slot >= 0 copies the node's pool brick into brick_buffer

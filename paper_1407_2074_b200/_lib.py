@@ -66,6 +66,11 @@ class vt_counters(ct.Structure):
                 ("samples_skipped", ct.c_int64)]
 
 
+class vt_block(ct.Structure):
+    _fields_ = [("channel", ct.c_int32), ("origin", ct.c_int32 * 3), ("dims", ct.c_int32 * 3),
+                ("pad", ct.c_int32), ("samples", ct.c_void_p)]
+
+
 P = ct.c_void_p
 I32, I64, U32 = ct.c_int32, ct.c_int64, ct.c_uint32
 PI32, PI64 = ct.POINTER(ct.c_int32), ct.POINTER(ct.c_int64)
@@ -78,6 +83,10 @@ SIGNATURES = {
     "vt_tree_insert": [P, I32, PI32, PI32, P, I32],
     "vt_tree_insert_channels": [P, PI32, PI32, P, I32],
     "vt_tree_insert_ev": [P, I32, PI32, PI32, P, I32, P, PI32, PI64, I64, PI64],
+    "vt_tree_insert_many": [P, I64, ct.POINTER(vt_block), I32, P],
+    "vt_tree_stream_counts": [P, PI64, PI64, PI64],
+    "vt_tree_publish_halos": [P],
+    "vt_mirror_bmax_stats": [P, PI64, PI64],
     "vt_tree_take_events": [P, PI32, PI64, I64, PI64, PI32],
     "vt_tree_event_count": [P, PI64],
     "vt_tree_checksum": [P, ct.POINTER(ct.c_uint64)],

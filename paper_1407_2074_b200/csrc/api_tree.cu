@@ -150,6 +150,7 @@ vt_status vt_tree_insert_ev(vt_tree* tree, int32_t channel, const int32_t origin
       VT_CUDA(cudaEventRecord(t.ev_signal, t.stream));
       VT_CUDA(cudaStreamWaitEvent(cs, t.ev_signal, 0));
     }
+    t.flush_replays();
     auto& ev = t.events;
     *n_events = (int64_t)ev.size();
     if ((int64_t)ev.size() > cap) return;  // too many: the caller takes them all at once
@@ -161,6 +162,37 @@ vt_status vt_tree_insert_ev(vt_tree* tree, int32_t channel, const int32_t origin
   });
 }
 
+vt_status vt_tree_insert_many(vt_tree* tree, int64_t n, const vt_block* blocks, int32_t mem_kind,
+                              void* caller_stream) {
+  return guarded([&] {
+    Tree& t = tree->t;
+    VT_REQUIRE(n >= 0 && (n == 0 || blocks), VT_EINVAL, "null block list");
+    VT_REQUIRE(mem_kind == VT_MEM_HOST || mem_kind == VT_MEM_DEVICE, VT_EINVAL, "bad memory kind");
+    VT_CUDA(cudaSetDevice(t.device));
+    cudaStream_t cs = (cudaStream_t)caller_stream;
+    const bool order = mem_kind == VT_MEM_DEVICE && cs != t.stream;
+    if (order) {
+      if (!t.ev_wait) VT_CUDA(cudaEventCreateWithFlags(&t.ev_wait, cudaEventDisableTiming));
+      VT_CUDA(cudaEventRecord(t.ev_wait, cs));
+      VT_CUDA(cudaStreamWaitEvent(t.stream, t.ev_wait, 0));
+    }
+    struct Signal {  // also on error: blocks inserted before it were read
+      Tree& t;
+      cudaStream_t cs;
+      bool on;
+      ~Signal() {
+        if (!on) return;
+        if (!t.ev_signal && cudaEventCreateWithFlags(&t.ev_signal, cudaEventDisableTiming) != cudaSuccess)
+          return;
+        cudaEventRecord(t.ev_signal, t.stream);
+        cudaStreamWaitEvent(cs, t.ev_signal, 0);
+      }
+    } sig{t, cs, order};
+    t.insert_many(n, blocks, mem_kind);
+    if (mem_kind == VT_MEM_HOST) VT_CUDA(cudaStreamSynchronize(t.stream));  // host borrow
+  });
+}
+
 vt_status vt_tree_insert_channels(vt_tree* tree, const int32_t origin[3], const int32_t dims[3],
                                   const void* samples, int32_t mem_kind) {
   return guarded([&] { tree->t.insert(-1, origin, dims, samples, mem_kind); });
@@ -169,6 +201,7 @@ vt_status vt_tree_insert_channels(vt_tree* tree, const int32_t origin[3], const 
 vt_status vt_tree_take_events(vt_tree* tree, int32_t* kinds, int64_t* indices, int64_t cap,
                               int64_t* n, int32_t* more) {
   return guarded([&] {
+    tree->t.flush_replays();
     auto& ev = tree->t.events;
     int64_t m = std::min<int64_t>(cap, (int64_t)ev.size());
     for (int64_t i = 0; i < m; ++i) {
@@ -205,7 +238,7 @@ vt_status vt_tree_signal_stream(vt_tree* tree, void* stream) {
 }
 
 vt_status vt_tree_event_count(vt_tree* tree, int64_t* n) {
-  return guarded([&] { *n = (int64_t)tree->t.events.size(); });
+  return guarded([&] { *n = tree->t.event_total(); });
 }
 
 vt_status vt_tree_set_dense(vt_tree* tree, int32_t enabled) {
@@ -222,6 +255,19 @@ vt_status vt_tree_dense_counts(vt_tree* tree, int64_t* leaf_inserts, int64_t* le
     if (level_nodes) *level_nodes = tree->t.dense_level_nodes;
     if (fast_borders) *fast_borders = tree->t.fast_borders;
   });
+}
+
+vt_status vt_tree_stream_counts(vt_tree* tree, int64_t* layer_groups, int64_t* zero_copy_layers,
+                                int64_t* deferred_layers) {
+  return guarded([&] {
+    if (layer_groups) *layer_groups = tree->t.layer_groups;
+    if (zero_copy_layers) *zero_copy_layers = tree->t.zero_copy_layers;
+    if (deferred_layers) *deferred_layers = tree->t.deferred_layers;
+  });
+}
+
+vt_status vt_tree_publish_halos(vt_tree* tree) {
+  return guarded([&] { tree->t.publish_halos(); });
 }
 
 vt_status vt_tree_finalize(vt_tree* tree) {
@@ -454,6 +500,7 @@ vt_status vt_tree_import(vt_tree* tree, int64_t n, const int64_t* indices, const
                          int32_t borders_filled, int64_t pruned_bricks) {
   return guarded([&] {
     ++tree->t.data_version;
+    tree->t.touch_all();
     Tree& t = tree->t;
     VT_REQUIRE(t.node_count == 1 && t.brick_count == 0, VT_ESTATE, "import into a non-empty tree");
     const int C = t.g.C;

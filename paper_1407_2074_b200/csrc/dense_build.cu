@@ -744,6 +744,292 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
 }
 
 // ---------------------------------------------------------------------------
+// TMA-staged leaves from a PLANAR source (16-bit samples)
+// ---------------------------------------------------------------------------
+// The layer of a slice stream arrives channel by channel (ingest_stream's
+// VSTR order: per z one single-channel frame per channel), so its natural
+// device layout is planar: sample (x, y, z, c) at
+// base + c*cstride + (z - oz)*zstride + (y*X + x)*2 bytes.  The TMA engine
+// streams one 4-D tensor tile per stage — P stored planes x (My+2) rows x
+// the aligned row span, for every channel — into [C][P][Sy][bx] shared
+// memory, and the warps interleave channels on the way out: thread v of a
+// plane group owns stored voxel v of the plane (consecutive lanes read
+// consecutive x of a channel row: no bank conflicts), loads its C samples
+// and writes them as 32-bit words of the channel-fastest stored row; for odd
+// C an even voxel completes its last word with the next voxel's first sample
+// (one shuffle, the pair is always in the same warp since rows are even).
+// The stored brick, statistics and fused parent octant are exactly those of
+// k_dense_leaf_tma (same shells, prefill rules and rounding); only the
+// source layout differs.  Reference: _write_leaf + _ensure_brick +
+// _recompute_stats (octree.py:225-263, 420-442), halfsample_block
+// (octree.py:58-92), _update_parent_octant (octree.py:308-319).
+__host__ __device__ inline int tma_box_row_planar(int mx) { return (mx + 2 + 7 + 7) / 8 * 8; }
+__host__ __device__ inline uint32_t tma_in_bytes_planar(int mx, int my, int C) {
+  return ((uint32_t)C * kTmaP * (my + 2) * tma_box_row_planar(mx) * 2 + 127) / 128 * 128;
+}
+
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int x, int y, int z,
+                                            int c, uint64_t* b) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], "
+      "[%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_addr(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(z), "r"(c), "r"(smem_addr(b))
+      : "memory");
+}
+
+template <int C, int MX = 0, int MY = 0>
+__global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma_planar(
+    const __grid_constant__ CUtensorMap map, int oz, int dz, int prefill,
+    const DenseJob* __restrict__ jobs, int gnx, int gny, int g0z, Geo g,
+    uint16_t* __restrict__ pool, int32_t* stats, int32_t* nmin, int32_t* nmax,
+    unsigned long long* nsum) {
+  constexpr int P = kTmaP;
+  constexpr int WPP = kTmaWarps / P;  // warps per plane
+  constexpr int NT = WPP * 32;        // threads per plane
+  extern __shared__ __align__(128) unsigned char s_in[];
+  __shared__ uint64_t s_bar[kTmaStages];
+  __shared__ int s_mn[2][kTmaWarps][C], s_mx[2][kTmaWarps][C];
+  __shared__ unsigned long long s_sm[2][kTmaWarps][C];
+  const DenseJob j = jobs[blockIdx.x];
+  const int gx = (int)(blockIdx.x % gnx);
+  const int gy = (int)((blockIdx.x / gnx) % gny);
+  const int gz = g0z + (int)(blockIdx.x / (gnx * gny));
+  const int Mx = MX ? MX : g.brick[0], My = MY ? MY : g.brick[1], Mz = g.brick[2];
+  const int Sx = MX ? MX + 2 : Mx + 2, Sy = MY ? MY + 2 : My + 2, Sz = g.stored[2];
+  const int X = g.dims[0], Y = g.dims[1], Z = g.dims[2];
+  const int cx = min(Mx, X - gx * Mx), cy = min(My, Y - gy * My), cz = min(Mz, Z - gz * Mz);
+  const int bx = tma_box_row_planar(Mx);             // staged row (samples, one channel)
+  const int rows = P * Sy;                           // staged rows per channel
+  const uint32_t in_bytes = tma_in_bytes_planar(Mx, My, C);
+  const uint32_t plane_elems = (uint32_t)Sx * Sy * C;
+  const int nvox = Sx * Sy;                          // stored voxels per plane
+  const int nstages = Sz / P;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint16_t* brick = pool + (int64_t)j.slot * g.brick_elems;
+  const uint16_t bg = (uint16_t)g.bg;
+  const int x0 = gx * Mx - 1, y0 = gy * My - 1;  // block voxel of stored (0, 0)
+  const int xa = x0 - ((x0 % 8 + 8) % 8);        // 16-byte aligned tile start (samples)
+  const int xoff = x0 - xa;                      // leading samples of a staged row
+
+  if (tid == 0) {
+    for (int b = 0; b < kTmaStages; ++b) mbar_init(&s_bar[b], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  auto issue = [&](int s) {  // one thread: one 4-D tensor tile per stage
+    const int b = s % kTmaStages;
+    mbar_expect_tx(&s_bar[b], (uint32_t)C * rows * bx * 2);
+    tma_load_4d(s_in + (size_t)b * in_bytes, &map, xa, y0, gz * Mz - oz + P * s - 1, 0, &s_bar[b]);
+  };
+  if (tid == 0)
+    for (int s = 0; s < min(kTmaAhead, nstages); ++s) issue(s);
+
+  const int pslot = j.pad;
+  const int hx = Mx / 2, hy = My / 2;
+  const int offx = (gx & 1) * hx, offy = (gy & 1) * hy, offz = (gz & 1) * (Mz / 2);
+  int pcx, pcy, pcz;  // the parent's in-volume extent (octree.py:190-199)
+  {
+    const int plx = (gx >> 1) * 2 * Mx, ply = (gy >> 1) * 2 * My, plz = (gz >> 1) * 2 * Mz;
+    pcx = min(Mx, max(0, (X - plx + 1) / 2));
+    pcy = min(My, max(0, (Y - ply + 1) / 2));
+    pcz = min(Mz, max(0, (Z - plz + 1) / 2));
+  }
+  uint16_t* parent = pslot >= 0 ? pool + (int64_t)pslot * g.brick_elems : nullptr;
+
+  int lmn[C], lmx[C], omn[C], omx[C];
+  unsigned long long lsm[C], osm[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    lmn[c] = omn[c] = INT_MAX;
+    lmx[c] = omx[c] = INT_MIN;
+    lsm[c] = osm[c] = 0;
+  }
+  const int pw = warp / WPP;                // plane of the stage this warp group builds
+  const int cstr = rows * bx;               // staged channel stride (samples)
+
+  for (int s = 0; s < nstages; ++s) {
+    const int b = (unsigned)s % kTmaStages;
+    const int zs = P * s + pw;
+    const int zi = zs - 1;
+    const int rz = gz * Mz + zi;
+    const int mode = (zi >= 0 && zi < cz) ? 1
+                     : (prefill && zs < Sz && rz >= 0 && rz < Z && rz - oz >= 0 && rz - oz < dz) ? 2
+                                                                                               : 0;
+    const uint16_t* stage = reinterpret_cast<const uint16_t*>(s_in + (size_t)b * in_bytes);
+    const uint16_t* iplane = stage + (size_t)pw * Sy * bx + xoff;  // channel 0, stored (0, 0)
+    uint32_t* oplane = reinterpret_cast<uint32_t*>(brick + (size_t)zs * plane_elems);
+    mbar_wait(&s_bar[b], (uint32_t)(s / kTmaStages) & 1u);
+    if (zs < Sz) {
+      const bool stat_plane = mode == 1 && !parent;
+      // every lane runs the same trip count (shuffles below)
+      for (int v0 = (warp % WPP) * 32; v0 < nvox; v0 += NT) {
+        const int v = v0 + lane;
+        const bool act = v < nvox;
+        const int ys = v / Sx, xs = v - ys * Sx;
+        const int rx = x0 + xs, ry = y0 + ys;
+        const bool take = act && mode != 0 &&
+                          (prefill ? ((unsigned)rx < (unsigned)X && (unsigned)ry < (unsigned)Y)
+                                   : (xs >= 1 && xs <= cx && ys >= 1 && ys <= cy));
+        uint32_t val[C];
+        const uint16_t* q = iplane + ys * bx + xs;
+#pragma unroll
+        for (int c = 0; c < C; ++c) val[c] = take ? (uint32_t)q[c * cstr] : (uint32_t)bg;
+        if (stat_plane && xs >= 1 && xs <= cx && ys >= 1 && ys <= cy && act) {
+#pragma unroll
+          for (int c = 0; c < C; ++c) {
+            lmn[c] = min(lmn[c], (int)val[c]);
+            lmx[c] = max(lmx[c], (int)val[c]);
+            lsm[c] += val[c];
+          }
+        }
+        if ((C & 1) == 0) {
+          if (act) {
+            uint32_t* o = oplane + (size_t)v * (C / 2);
+#pragma unroll
+            for (int w = 0; w < C / 2; ++w) o[w] = val[2 * w] | (val[2 * w + 1] << 16);
+          }
+        } else {
+          const uint32_t nb = __shfl_down_sync(0xffffffffu, val[0], 1);
+          if (act) {
+            const uint32_t e = (uint32_t)v * C;  // first sample of this voxel
+            if ((v & 1) == 0) {
+              // even voxel: its samples start a word; the last pairs with nb
+#pragma unroll
+              for (int w = 0; w < C / 2; ++w) oplane[e / 2 + w] = val[2 * w] | (val[2 * w + 1] << 16);
+              oplane[e / 2 + C / 2] = val[C - 1] | (nb << 16);
+            } else {
+              // odd voxel: sample 0 completed the previous voxel's word
+#pragma unroll
+              for (int w = 0; w < C / 2; ++w)
+                oplane[(e + 1) / 2 + w] = val[2 * w + 1] | (val[2 * w + 2] << 16);
+            }
+          }
+        }
+      }
+    }
+    // fused octant plane k = s - 1 from interior planes 2k (previous stage,
+    // second plane) and 2k + 1 (this stage, first plane)
+    if (parent && s >= 1 && 2 * (s - 1) < cz) {
+      const int k = s - 1;
+      const uint16_t* pa = reinterpret_cast<const uint16_t*>(
+                               s_in + (size_t)((unsigned)(s - 1) % kTmaStages) * in_bytes) +
+                           (size_t)Sy * bx + xoff;  // previous stage, plane 1
+      const uint16_t* pb = stage + xoff;             // this stage, plane 0
+      const bool zfull = 2 * k + 1 < cz;
+      const bool pin = offz + k < pcz;
+      for (int v = tid; v < hx * hy; v += kTmaWarps * 32) {
+        const int oy = v / hx, ox = v - oy * hx;
+        int val[C];
+        if (zfull && 2 * ox + 1 < cx && 2 * oy + 1 < cy) {
+          const int o00 = (1 + 2 * oy) * bx + 1 + 2 * ox;
+#pragma unroll
+          for (int c = 0; c < C; ++c) {
+            const int oc = o00 + c * cstr;
+            const int a0 = pa[oc], a1 = pa[oc + 1], a2 = pa[oc + bx], a3 = pa[oc + bx + 1];
+            const int b0 = pb[oc], b1 = pb[oc + 1], b2 = pb[oc + bx], b3 = pb[oc + bx + 1];
+            const unsigned sum = (unsigned)(a0 + a1 + a2 + a3 + b0 + b1 + b2 + b3);
+            val[c] = (int)((2 * sum + 8) / 16);
+            lmn[c] = min(lmn[c], min(min(min(a0, a1), min(a2, a3)), min(min(b0, b1), min(b2, b3))));
+            lmx[c] = max(lmx[c], max(max(max(a0, a1), max(a2, a3)), max(max(b0, b1), max(b2, b3))));
+            lsm[c] += sum;
+          }
+        } else {
+          unsigned sum[C];
+#pragma unroll
+          for (int c = 0; c < C; ++c) sum[c] = 0;
+          int cnt = 0;
+          for (int dz2 = 0; dz2 < 2; ++dz2) {
+            if (2 * k + dz2 >= cz) continue;
+            const uint16_t* pl = dz2 ? pb : pa;
+            for (int dy = 0; dy < 2; ++dy) {
+              if (2 * oy + dy >= cy) continue;
+              for (int dx = 0; dx < 2; ++dx) {
+                if (2 * ox + dx >= cx) continue;
+                const int o = (1 + 2 * oy + dy) * bx + 1 + 2 * ox + dx;
+#pragma unroll
+                for (int c = 0; c < C; ++c) {
+                  const int x = pl[o + c * cstr];
+                  sum[c] += x;
+                  lmn[c] = min(lmn[c], x);
+                  lmx[c] = max(lmx[c], x);
+                }
+                ++cnt;
+              }
+            }
+          }
+#pragma unroll
+          for (int c = 0; c < C; ++c) {
+            lsm[c] += sum[c];
+            val[c] = cnt ? (int)((2 * (unsigned long long)sum[c] + cnt) / (2 * cnt)) : (int)bg;
+          }
+        }
+        uint16_t* dst = parent + g.voxel_offset(1 + offz + k, 1 + offy + oy, 1 + offx + ox);
+#pragma unroll
+        for (int c = 0; c < C; ++c) dst[c] = (uint16_t)val[c];
+        if (pin && offx + ox < pcx && offy + oy < pcy) {
+#pragma unroll
+          for (int c = 0; c < C; ++c) {
+            omn[c] = min(omn[c], val[c]);
+            omx[c] = max(omx[c], val[c]);
+            osm[c] += (unsigned)val[c];
+          }
+        }
+      }
+    }
+    __syncthreads();  // input slots consumed
+    if (tid == 0 && s + kTmaAhead < nstages) issue(s + kTmaAhead);
+  }
+
+#pragma unroll
+  for (int c = 0; c < C; ++c)
+    for (int o = 16; o > 0; o >>= 1) {
+      lmn[c] = min(lmn[c], __shfl_xor_sync(0xffffffffu, lmn[c], o));
+      lmx[c] = max(lmx[c], __shfl_xor_sync(0xffffffffu, lmx[c], o));
+      lsm[c] += __shfl_xor_sync(0xffffffffu, lsm[c], o);
+      omn[c] = min(omn[c], __shfl_xor_sync(0xffffffffu, omn[c], o));
+      omx[c] = max(omx[c], __shfl_xor_sync(0xffffffffu, omx[c], o));
+      osm[c] += __shfl_xor_sync(0xffffffffu, osm[c], o);
+    }
+  if (lane == 0)
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      s_mn[0][warp][c] = lmn[c];
+      s_mx[0][warp][c] = lmx[c];
+      s_sm[0][warp][c] = lsm[c];
+      s_mn[1][warp][c] = omn[c];
+      s_mx[1][warp][c] = omx[c];
+      s_sm[1][warp][c] = osm[c];
+    }
+  __syncthreads();
+  if (tid < C) {
+    const int c = tid;
+    int a = INT_MAX, bmx = INT_MIN, pa = INT_MAX, pb = INT_MIN;
+    unsigned long long t = 0, pt2 = 0;
+    for (int w = 0; w < kTmaWarps; ++w) {
+      a = min(a, s_mn[0][w][c]);
+      bmx = max(bmx, s_mx[0][w][c]);
+      t += s_sm[0][w][c];
+      pa = min(pa, s_mn[1][w][c]);
+      pb = max(pb, s_mx[1][w][c]);
+      pt2 += s_sm[1][w][c];
+    }
+    const long long n = (long long)cx * cy * cz;
+    stats[st_index(j.node, ST_AVG, c)] = (int)((2 * (long long)t + n) / (2 * n));
+    stats[st_index(j.node, ST_MIN, c)] = a;
+    stats[st_index(j.node, ST_MAX, c)] = bmx;
+    stats[st_index(j.node, ST_SUBMIN, c)] = a;
+    stats[st_index(j.node, ST_SUBMAX, c)] = bmx;
+    if (parent && pb != INT_MIN) {
+      const int64_t pnode = (j.node - 1) >> 3;
+      atomicMin(nmin + pnode * C + c, pa);
+      atomicMax(nmax + pnode * C + c, pb);
+      atomicAdd(nsum + pnode * C + c, pt2);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // parents
 // ---------------------------------------------------------------------------
 // One CTA per parent; warps own interior planes, lanes the voxels of a row.
@@ -1145,6 +1431,128 @@ void launch_clear_shells(const Tree& t, const int32_t* d_slots, int n) {
     k_clear_shells<uint8_t><<<n, 256, 0, t.stream>>>(d_slots, t.g, t.d_pool);
   else
     k_clear_shells<uint16_t><<<n, 256, 0, t.stream>>>(d_slots, t.g, (uint16_t*)t.d_pool);
+  VT_CHECK_LAUNCH();
+}
+
+static size_t tma_smem_planar(const Geo& g) {
+  return (size_t)kTmaStages * tma_in_bytes_planar(g.brick[0], g.brick[1], g.C);
+}
+
+bool planar_leaf_ok(const Tree& t, const void* base, int64_t zstride, int64_t cstride) {
+  if (std::getenv("VT_DENSE_TMA") && std::getenv("VT_DENSE_TMA")[0] == '0') return false;
+  const Geo& g = t.g;
+  return g.sb == 2 && ((uintptr_t)base & 15) == 0 && ((int64_t)g.dims[0] * 2) % 16 == 0 &&
+         zstride > 0 && zstride % 16 == 0 && (g.C == 1 || (cstride > 0 && cstride % 16 == 0)) &&
+         tma_box_row_planar(g.brick[0]) <= 256 && g.brick[1] + 2 <= 256 &&
+         ((g.brick[0] + 2) * (g.brick[1] + 2)) % 2 == 0 && tma_smem_planar(g) <= 200 * 1024;
+}
+
+// 4-D tensor map (x, y, z, c) of a planar u16 block of dz planes per channel
+static bool encode_planar_map(const Tree& t, const void* base, int64_t zstride, int64_t cstride,
+                              int64_t dz, CUtensorMap* map) {
+  using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static Encode enc = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      enc = (Encode)fn;
+    cudaGetLastError();
+  }
+  if (!enc) return false;
+  const Geo& g = t.g;
+  cuuint64_t dims[4] = {(cuuint64_t)g.dims[0], (cuuint64_t)g.dims[1], (cuuint64_t)dz,
+                        (cuuint64_t)g.C};
+  cuuint64_t strides[3] = {(cuuint64_t)g.dims[0] * 2, (cuuint64_t)zstride,
+                           (cuuint64_t)(g.C == 1 ? zstride * dz : cstride)};
+  cuuint32_t box[4] = {(cuuint32_t)tma_box_row_planar(g.brick[0]), (cuuint32_t)(g.brick[1] + 2),
+                       (cuuint32_t)kTmaP, (cuuint32_t)g.C};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 4, const_cast<void*>(base), dims, strides, box,
+             es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int C>
+static int leaf_launch_planar(const Tree& t, const void* base, int64_t zstride, int64_t cstride,
+                              int oz, int64_t dz, int prefill, const DenseJob* jobs, int n,
+                              const int gn[3], int g0z) {
+  CUtensorMap map;
+  if (!encode_planar_map(t, base, zstride, cstride, dz, &map)) return -1;
+  const size_t smem = tma_smem_planar(t.g);
+  auto k = t.g.brick[0] == 32 && t.g.brick[1] == 32 ? k_dense_leaf_tma_planar<C, 32, 32>
+                                                    : k_dense_leaf_tma_planar<C>;
+  VT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k<<<n, kTmaWarps * 32, smem, t.stream>>>(map, oz, (int)dz, prefill, jobs, gn[0], gn[1], g0z, t.g,
+                                          (uint16_t*)t.d_pool, t.d_stats, t.d_nmin, t.d_nmax,
+                                          t.d_nsum);
+  VT_CHECK_LAUNCH();
+  return kLeafTma | (prefill ? kLeafPrefilled : 0);
+}
+
+int launch_dense_leaf_planar(const Tree& t, const void* base, int64_t zstride, int64_t cstride,
+                             int oz, int64_t dz, int prefill, const DenseJob* jobs, int n,
+                             const int gn[3], int g0z) {
+  if (n <= 0) return 0;
+  if (!planar_leaf_ok(t, base, zstride, cstride)) return -1;
+  switch (t.g.C) {
+    case 1: return leaf_launch_planar<1>(t, base, zstride, cstride, oz, dz, prefill, jobs, n, gn, g0z);
+    case 2: return leaf_launch_planar<2>(t, base, zstride, cstride, oz, dz, prefill, jobs, n, gn, g0z);
+    case 3: return leaf_launch_planar<3>(t, base, zstride, cstride, oz, dz, prefill, jobs, n, gn, g0z);
+    default: return leaf_launch_planar<4>(t, base, zstride, cstride, oz, dz, prefill, jobs, n, gn, g0z);
+  }
+}
+
+// planar (c, z, y, x) block -> interleaved (z, y, x, c) (fallback for the
+// kernels that read interleaved blocks)
+template <class T>
+__global__ void k_planar_to_interleaved(const unsigned char* __restrict__ base, int64_t zstride,
+                                        int64_t cstride, int64_t plane, int dz, int C, T* dst) {
+  const int64_t n = plane * dz;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t z = i / plane, r = i - z * plane;
+    for (int c = 0; c < C; ++c)
+      dst[i * C + c] = *reinterpret_cast<const T*>(base + c * cstride + z * zstride + r * sizeof(T));
+  }
+}
+
+void launch_planar_to_interleaved(const Tree& t, const void* base, int64_t zstride,
+                                  int64_t cstride, int dz, void* dst) {
+  const int64_t plane = (int64_t)t.g.dims[0] * t.g.dims[1];
+  const int64_t n = plane * dz;
+  if (n <= 0) return;
+  const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32);
+  if (t.g.sb == 1)
+    k_planar_to_interleaved<uint8_t><<<grid, 256, 0, t.stream>>>(
+        (const unsigned char*)base, zstride, cstride, plane, dz, t.g.C, (uint8_t*)dst);
+  else
+    k_planar_to_interleaved<uint16_t><<<grid, 256, 0, t.stream>>>(
+        (const unsigned char*)base, zstride, cstride, plane, dz, t.g.C, (uint16_t*)dst);
+  VT_CHECK_LAUNCH();
+}
+
+template <class T>
+__global__ void k_fill_value(T* dst, int64_t n, T v) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = v;
+}
+
+void launch_fill_bg(const Tree& t, void* dst, int64_t n) {
+  if (n <= 0) return;
+  const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  if (t.g.sb == 1)
+    k_fill_value<uint8_t><<<grid, 256, 0, t.stream>>>((uint8_t*)dst, n, (uint8_t)t.g.bg);
+  else
+    k_fill_value<uint16_t><<<grid, 256, 0, t.stream>>>((uint16_t*)dst, n, (uint16_t)t.g.bg);
   VT_CHECK_LAUNCH();
 }
 

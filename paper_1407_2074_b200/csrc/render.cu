@@ -41,6 +41,7 @@ struct vt_mirror {
   int64_t bmax_cap = 0;
   bool bmax_valid = false;
   int64_t bmax_version = -1;  // tree data_version the zero-copy maxima reflect
+  int64_t bmax_incremental = 0, bmax_last_slots = 0;  // refresh statistics
 };
 
 namespace {
@@ -1382,6 +1383,25 @@ static void update_bmax(vt_mirror* m, const int32_t* d_slots, int n) {
   const int64_t nsb = (int64_t)nsub[0] * nsub[1] * nsub[2];
   const int64_t nslots = std::max<int64_t>(1, m->zero_copy ? t.pool_slots : m->slots);
   const int64_t need = nslots * nsb;
+  // zero copy: only the pool slots written since the maxima were last
+  // computed (Tree::slot_ver), unless everything changed or the table grows
+  std::vector<int32_t> dirty;
+  int32_t* d_dirty = nullptr;
+  if (m->zero_copy && !d_slots && m->bmax_version >= 0 && need <= m->bmax_cap &&
+      t.all_ver <= m->bmax_version) {
+    const int64_t used = std::min<int64_t>(t.cursor, (int64_t)t.slot_ver.size());
+    for (int64_t s = 0; s < used; ++s)
+      if (t.slot_ver[s] > m->bmax_version) dirty.push_back((int32_t)s);
+    m->bmax_incremental += 1;
+    m->bmax_last_slots = (int64_t)dirty.size();
+    m->bmax_version = t.data_version;
+    if (dirty.empty()) return;
+    d_dirty = upload(t, dirty);
+    d_slots = d_dirty;
+    n = (int)dirty.size();
+  } else if (m->zero_copy && !d_slots) {
+    m->bmax_last_slots = t.cursor;
+  }
   if (need > m->bmax_cap) {
     VT_CUDA(cudaStreamSynchronize(t.stream));
     cudaFree(m->d_bmax);
@@ -1423,6 +1443,7 @@ static void update_bmax(vt_mirror* m, const int32_t* d_slots, int n) {
                                                         nsub[2], m->d_bmax, m->d_bmax_brick);
     VT_CUDA(cudaGetLastError());
   }
+  release(t, d_dirty);
   m->bmax_valid = true;
   if (m->zero_copy) m->bmax_version = t.data_version;
 }
@@ -1441,10 +1462,16 @@ vt_status vt_mirror_create(vt_tree* tree, int64_t slot_count, vt_mirror** out) {
   return guarded([&] {
     Tree& t = tree->t;
     t.flush();
-    // the mirror exposes pool shells: publish prefilled ones as background
-    // and write later dense leaves with background shells
-    t.publish_halos();
-    t.prefill_enabled = false;
+    if (slot_count >= 0) {
+      // a bounded mirror copies whole bricks (shells included) into its own
+      // buffer: publish prefilled shells as background and write later dense
+      // leaves with background shells.  A zero-copy mirror reads the pool in
+      // place, where prefilled shells stay invisible: before fill_borders the
+      // sampler clamps to the interior (render/raycast.py:141-144) and the
+      // brick maxima only bound what may be read.
+      t.publish_halos();
+      t.prefill_enabled = false;
+    }
     auto* m = new vt_mirror();
     m->tree = tree;
     vt_tree_retain(tree);
@@ -1491,6 +1518,13 @@ static void mirror_release(vt_mirror* m) {
 
 vt_status vt_mirror_destroy(vt_mirror* m) {
   return guarded([&] { mirror_release(m); });
+}
+
+vt_status vt_mirror_bmax_stats(vt_mirror* m, int64_t* incremental, int64_t* last_slots) {
+  return guarded([&] {
+    if (incremental) *incremental = m->bmax_incremental;
+    if (last_slots) *last_slots = m->bmax_last_slots;
+  });
 }
 
 vt_status vt_mirror_buffers(vt_mirror* m, void** nbp, void** fbp, void** bbp, int64_t* cap,

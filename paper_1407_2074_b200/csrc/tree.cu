@@ -251,6 +251,7 @@ Tree::~Tree() {
   cudaFree(d_psum);
   cudaFree(d_nsum);
   cudaFree(d_acc);
+  cudaFree(d_acc_il);
   cudaFree(d_nmin);
   cudaFree(d_nmax);
   if (ev0) cudaEventDestroy(ev0);
@@ -294,6 +295,7 @@ void Tree::ensure_pool(int64_t need) {
   d_pmax = nmax;
   d_psum = nsum;
   pool_slots = n;
+  slot_ver.resize(n, data_version);
 }
 
 // ---------------------------------------------------------------------------
@@ -568,12 +570,14 @@ struct ParentCoord { int64_t idx; int px, py, pz; };
 }  // namespace
 
 void Tree::insert_staged(int channel, const int origin[3], const int dims[3], const void* dsrc,
-                         int src_stride, int src_off, int reps) {
+                         int src_stride, int src_off, int reps, int64_t ev_reps) {
   const int64_t nvox = (int64_t)dims[0] * dims[1] * dims[2];
+  if (ev_reps <= 0) ev_reps = reps;
   {
     ProfScope qd(prof, 18);
     if (try_defer(channel, origin, dims, dsrc, src_stride, src_off)) return;
   }
+  flush_replays();  // this insertion's events follow every earlier one
   const bool starting = defer_start;  // this insertion opens a deferred layer
   defer_start = false;
   ++data_version;
@@ -735,8 +739,8 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
       if (prof.on) VT_CUDA(cudaEventRecord(prof.ev[1], stream));
       VT_CUDA(cudaEventRecord(ev_pre, stream));
       ProfScope qll(prof, 30);
-      launch_result = launch_dense_leaf(*this, dsrc, nvox * src_stride, origin[2], want ? 1 : 0,
-                                        dj, (int)djobs.size(), gn, g0[2]);
+      launch_result = leaf_launch(dsrc, nvox * src_stride, origin[2], dims[2], want ? 1 : 0, dj,
+                                  (int)djobs.size(), gn, g0[2]);
       if (prof.on) {
         VT_CUDA(cudaEventRecord(prof.ev[2], stream));
         prof.ev_armed = true;
@@ -751,7 +755,7 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
     // the events and dirty lists of a whole-layer block: created nodes, then
     // C reps of every touched node
     const size_t nl = nblock;
-    events.reserve(events.size() + nl * (2 + reps) + 64);
+    events.reserve(events.size() + nl * 3 + 64);
     struct_dirty.reserve(struct_dirty.size() + nl * 2 + 64);
   }
   auto* walk_scope = new ProfScope(prof, 1);
@@ -924,6 +928,9 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
       sort_indices(touched[0]);
   }
   has_pending = true;
+  for (const auto& lv : touched)
+    for (int64_t n : lv)
+      if (flags[n] & NF_BRICK) touch_slot(slot[n]);
   delete anc_scope;
   delete walk_scope;
   ProfScope enq_scope(prof, 2);
@@ -999,8 +1006,8 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
       release(*this, dfn);
       DenseJob* dj = upload(*this, djobs);
       const bool want = prefill_enabled && !borders;
-      lr = launch_dense_leaf(*this, dsrc, nvox * src_stride, origin[2], want ? 1 : 0, dj,
-                             (int)djobs.size(), gn, g0[2]);
+      lr = leaf_launch(dsrc, nvox * src_stride, origin[2], dims[2], want ? 1 : 0, dj,
+                       (int)djobs.size(), gn, g0[2]);
       release(*this, dj);
     }
     const bool prefilled = lr & kLeafPrefilled;
@@ -1049,6 +1056,8 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
     dl.order.clear();
     dl.leaf_slots = leaf_slots;
     dl.djobs.clear();
+    dl.seeds.clear();  // the leaf kernel writes whole bricks: no seeds owed
+    dl.prefilled = false;
     for (int gy = g0[1]; gy <= g1[1]; ++gy)
       for (int gx = g0[0]; gx <= g1[0]; ++gx) {
         const int64_t idx = leaf_index(gx, gy, g0[2]);
@@ -1107,14 +1116,15 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
   static thread_local std::vector<int64_t> upd;
   upd.clear();
   for (int lvl = g.depth; lvl >= 0; --lvl) upd.insert(upd.end(), touched[lvl].begin(), touched[lvl].end());
-  events.reserve(events.size() + upd.size() * reps);
+  events.reserve(events.size() + upd.size());
   const size_t ev0 = events.size();
   for (int64_t i : upd)
     if (flags[i] & NF_EXISTS) events.push_back(ev_pack(VT_EV_UPDATED, i));
-  const size_t ev1 = events.size(), nev = ev1 - ev0;
-  events.resize(ev1 + nev * (reps - 1));
-  for (int r = 1; r < reps; ++r)
-    std::copy(events.begin() + ev0, events.begin() + ev1, events.begin() + ev0 + r * nev);
+  if (ev_reps > 1) {
+    // the later blocks' lists are replayed when something reads the events
+    rep_list.assign(events.begin() + ev0, events.end());
+    rep_count = ev_reps - 1;
+  }
   if (starting) {
     dl.upd = upd;  // every later block of the layer touches the same nodes
     if (dl.remaining == 0) finish_layer();
@@ -1142,13 +1152,19 @@ bool Tree::try_defer(int channel, const int origin[3], const int dims[3], const 
     if (cont) {
       ++data_version;
       defer_copy(channel, origin, dims, dsrc);
-      events.reserve(events.size() + dl.upd.size());
-      for (int64_t i : dl.upd) events.push_back(ev_pack(VT_EV_UPDATED, i));
+      // this block's events: the layer's UPDATED list once more (replayed
+      // lazily: a 2048^2 slice of 32^3 bricks updates ~5.5k nodes)
+      if (rep_count > 0 && rep_list.size() != dl.upd.size()) flush_replays();
+      if (rep_count == 0) {
+        rep_list.clear();
+        for (int64_t i : dl.upd) rep_list.push_back(ev_pack(VT_EV_UPDATED, i));
+      }
+      ++rep_count;
       inserted += nvox;
       if (dl.remaining == 0) finish_layer();
       return true;
     }
-    materialize_layer();
+    materialize_layer(true);
   }
   if (!shape) return false;
   // open a layer only over brick-less leaves (its leaf bricks are fresh)
@@ -1160,39 +1176,65 @@ bool Tree::try_defer(int channel, const int origin[3], const int dims[3], const 
   return false;  // the caller runs the walk in opening mode
 }
 
+// the block's planes into the planar layer buffer [C][Mz][Y][X]
 void Tree::defer_copy(int channel, const int origin[3], const int dims[3], const void* dsrc) {
-  const int64_t plane = (int64_t)g.dims[0] * g.dims[1];
-  uint8_t* dst = d_acc + (size_t)(origin[2] - dl.z0) * plane * g.C * g.sb;
-  launch_interleave(*this, dsrc, plane * dims[2], channel, dst);
+  const int64_t plane = (int64_t)g.dims[0] * g.dims[1] * g.sb;
+  uint8_t* dst = d_acc + ((size_t)channel * g.brick[2] + (origin[2] - dl.z0)) * plane;
+  VT_CUDA(cudaMemcpyAsync(dst, dsrc, plane * dims[2], cudaMemcpyDeviceToDevice, stream));
   for (int z = origin[2]; z < origin[2] + dims[2]; ++z) dl.got[(size_t)(z - dl.z0) * g.C + channel] = 1;
   dl.remaining -= dims[2];
+  dl.dirty = true;
   dl.order.push_back({origin[2], dims[2], channel});
 }
 
-// the layer is complete: one dense leaf kernel over the layer buffer
-void Tree::finish_layer() {
+// the dense leaf kernel over the layer buffer; `partial`: planes not received
+// yet hold the leaves' seed value (the background at threshold 0: every
+// fresh leaf brick is seeded with its AVG = the background, octree.py:225-241)
+void Tree::run_layer(bool partial) {
   const int* M = g.brick;
+  const int64_t plane = (int64_t)g.dims[0] * g.dims[1];
+  if (partial)
+    for (int zi = 0; zi < dl.nz; ++zi)
+      for (int c = 0; c < g.C; ++c)
+        if (!dl.got[(size_t)zi * g.C + c])
+          launch_fill_bg(*this, d_acc + ((size_t)c * M[2] + zi) * plane * g.sb, plane);
   const int gn[3] = {(g.dims[0] - 1) / M[0] + 1, (g.dims[1] - 1) / M[1] + 1, 1};
   DenseJob* dj = upload(*this, dl.djobs);
   const bool want = prefill_enabled && !borders;
-  const int64_t nsrc = (int64_t)dl.nz * g.dims[1] * g.dims[0] * g.C;
-  const int lr = launch_dense_leaf(*this, d_acc, nsrc, dl.z0, want ? 1 : 0, dj,
-                                   (int)dl.djobs.size(), gn, dl.gz);
+  PlanarSrc saved = planar;
+  planar = {true, d_acc, plane * g.sb, (int64_t)M[2] * plane * g.sb};
+  const int lr = leaf_launch(nullptr, 0, dl.z0, dl.nz, want ? 1 : 0, dj, (int)dl.djobs.size(), gn,
+                             dl.gz);
+  planar = saved;
   release(*this, dj);
   for (const DenseJob& jd : dl.djobs) {
     pend_dense(jd.node);
     complete[jd.node] = 1;
     if (lr & kLeafTma) pinv[jd.node] = 1;
   }
-  if (lr & kLeafPrefilled) {
-    halo_prefill = true;
-    const int lo = dl.z0 - 1, hi = dl.z0 + M[2];
+  // the layer's ancestors are owed a recompute: pending since the opening
+  // walk, or again when a reader's flush already consumed that entry
+  ++data_version;
+  for (int64_t p : dl.upd) {
+    const int lvl = g.level_of(p);
+    if (lvl > 0) pend(lvl, p);
+    if (flags[p] & NF_BRICK) touch_slot(slot[p]);
+  }
+  has_pending = true;
+  dl.prefilled = (lr & kLeafPrefilled) != 0;
+  if (dl.prefilled) halo_prefill = true;
+  else prefill_valid = false;
+  dl.dirty = false;
+}
+
+void Tree::close_layer() {
+  if (dl.prefilled) {
+    // z-shell planes of the neighbouring layers are owed to fill_borders
+    const int lo = dl.z0 - 1, hi = dl.z0 + g.brick[2];
     for (const DenseJob& jd : dl.djobs) {
       if (lo >= 0) owed_lo.push_back(jd.node);
       if (hi < g.dims[2]) owed_hi.push_back(jd.node);
     }
-  } else {
-    prefill_valid = false;
   }
   ++deferred_layers;
   ++dense_leaf_inserts;
@@ -1200,27 +1242,161 @@ void Tree::finish_layer() {
   dl.seeds.clear();
 }
 
-// a reader needs the tree now: the general path's device work for the
-// blocks received so far (held leaf seeds, then one scatter per block)
-void Tree::materialize_layer() {
+// the layer is complete: one dense leaf kernel over the layer buffer
+void Tree::finish_layer() {
+  run_layer(false);
+  close_layer();
+}
+
+// a reader needs the tree now: the leaves as the blocks received so far
+// leave them (the same bytes the general path's held seeds + one scatter per
+// block produce); the layer stays open for its remaining blocks unless
+// `close` (a non-follower insertion arrives)
+void Tree::materialize_layer(bool close) {
   if (!dl.active) return;
-  dl.active = false;
-  prefill_valid = false;
-  const int* M = g.brick;
-  SeedJob* ds = upload(*this, dl.seeds);
-  launch_seed(*this, ds, (int)dl.seeds.size());
-  release(*this, ds);
-  int32_t* dls = upload(*this, dl.leaf_slots);
-  const int64_t plane = (int64_t)g.dims[0] * g.dims[1];
-  const int g0[3] = {0, 0, dl.gz};
-  const int gn[3] = {(g.dims[0] - 1) / M[0] + 1, (g.dims[1] - 1) / M[1] + 1, 1};
-  for (const auto& b : dl.order) {
-    const int o[3] = {0, 0, b[0]}, d[3] = {g.dims[0], g.dims[1], b[1]};
-    const uint8_t* src = d_acc + (size_t)(b[0] - dl.z0) * plane * g.C * g.sb;
-    launch_scatter(*this, src, b[2], g.C, b[2], o, d, g0, gn, dls);
+  if (dl.dirty) run_layer(true);
+  if (close) close_layer();
+}
+
+// dense leaf launch from the current source: the planar block of a layer
+// group / deferred layer (4-D TMA; 8-bit or unaligned planar sources are
+// interleaved into a scratch block first), else the interleaved block
+int Tree::leaf_launch(const void* dsrc, int64_t nsrc, int oz, int dz, int prefill,
+                      const DenseJob* dj, int n, const int gn[3], int g0z) {
+  if (!planar.active) return launch_dense_leaf(*this, dsrc, nsrc, oz, prefill, dj, n, gn, g0z);
+  const int r = launch_dense_leaf_planar(*this, planar.base, planar.zstride, planar.cstride, oz, dz,
+                                         prefill, dj, n, gn, g0z);
+  if (r >= 0) return r;
+  const int64_t need = (int64_t)dz * g.dims[1] * g.dims[0] * g.C * g.sb;
+  if (need > d_acc_il_bytes) {
+    if (d_acc_il) VT_CUDA(cudaFreeAsync(d_acc_il, stream));
+    VT_CUDA(cudaMallocAsync(&d_acc_il, need, stream));
+    d_acc_il_bytes = need;
   }
-  release(*this, dls);
-  dl.seeds.clear();
+  launch_planar_to_interleaved(*this, planar.base, planar.zstride, planar.cstride, dz, d_acc_il);
+  return launch_dense_leaf(*this, d_acc_il, need / g.sb, oz, prefill, dj, n, gn, g0z);
+}
+
+// ---------------------------------------------------------------------------
+// batched insertion (vt_tree_insert_many)
+// ---------------------------------------------------------------------------
+
+// Blocks [i, i + len) form a complete brick layer group when, at threshold
+// 0 with the dense path on and no deferred layer open, each is one channel's
+// full-x/y block inside one brick layer over brick-less leaves and together
+// they cover every (z, channel) of the layer exactly once.  Returns len, or
+// 0 when block i starts no such group.
+int64_t Tree::layer_group(int64_t i, int64_t n, const vt_block* blocks, int mem_kind) {
+  const int* M = g.brick;
+  if (!dense_enabled || tau != 0 || dl.active) return 0;
+  auto fits = [&](const vt_block& b, int layer) {
+    if (b.channel < 0 || b.channel >= g.C || !b.samples) return false;
+    if (b.origin[0] != 0 || b.origin[1] != 0 || b.dims[0] != g.dims[0] || b.dims[1] != g.dims[1])
+      return false;
+    if (b.dims[2] <= 0 || b.origin[2] < 0 || (int64_t)b.origin[2] + b.dims[2] > g.dims[2]) return false;
+    if (b.origin[2] / M[2] != (b.origin[2] + b.dims[2] - 1) / M[2]) return false;
+    return layer < 0 || b.origin[2] / M[2] == layer;
+  };
+  if (!fits(blocks[i], -1)) return 0;
+  const int layer = blocks[i].origin[2] / M[2];
+  const int z0 = layer * M[2], nz = std::min(M[2], g.dims[2] - z0);
+  const int gx1 = (g.dims[0] - 1) / M[0], gy1 = (g.dims[1] - 1) / M[1];
+  for (int gy = 0; gy <= gy1; ++gy)
+    for (int gx = 0; gx <= gx1; ++gx)
+      if (flags[leaf_index(gx, gy, layer)] & NF_BRICK) return 0;
+  std::vector<uint8_t> got((size_t)nz * g.C, 0);
+  int64_t need = (int64_t)nz * g.C, j = i;
+  while (need > 0 && j < n && fits(blocks[j], layer)) {
+    const vt_block& b = blocks[j];
+    bool fresh = true;
+    for (int z = b.origin[2]; z < b.origin[2] + b.dims[2]; ++z)
+      fresh = fresh && !got[(size_t)(z - z0) * g.C + b.channel];
+    if (!fresh) break;
+    for (int z = b.origin[2]; z < b.origin[2] + b.dims[2]; ++z) got[(size_t)(z - z0) * g.C + b.channel] = 1;
+    need -= b.dims[2];
+    ++j;
+  }
+  (void)mem_kind;
+  return need == 0 ? j - i : 0;
+}
+
+void Tree::insert_many(int64_t n, const vt_block* blocks, int mem_kind) {
+  VT_CUDA(cudaSetDevice(device));
+  const int* M = g.brick;
+  const int64_t plane = (int64_t)g.dims[0] * g.dims[1] * g.sb;
+  int64_t i = 0;
+  while (i < n) {
+    const int64_t len = layer_group(i, n, blocks, mem_kind);
+    if (len == 0) {
+      const vt_block& b = blocks[i];
+      VT_REQUIRE(b.channel >= 0, VT_EINVAL, "channel " + std::to_string(b.channel) + " out of range");
+      insert(b.channel, b.origin, b.dims, b.samples, mem_kind);
+      ++i;
+      continue;
+    }
+    // one dense insertion for the whole layer: the first block's walk and
+    // events, then the same UPDATED list for each later block
+    const int layer = blocks[i].origin[2] / M[2];
+    const int z0 = layer * M[2], nz = std::min(M[2], g.dims[2] - z0);
+    // source: in place when the blocks sit at an affine (z, channel) stride
+    const uint8_t* base = nullptr;
+    int64_t zs = 0, cs = 0;
+    bool affine = mem_kind == VT_MEM_DEVICE;
+    if (affine) {
+      auto at = [&](const vt_block& b, int z) {
+        return (const uint8_t*)b.samples + (int64_t)(z - b.origin[2]) * plane;
+      };
+      const uint8_t* p00 = nullptr;
+      const uint8_t* p10 = nullptr;
+      const uint8_t* p01 = nullptr;
+      for (int64_t k = i; k < i + len; ++k) {
+        const vt_block& b = blocks[k];
+        for (int z = b.origin[2]; z < b.origin[2] + b.dims[2]; ++z) {
+          if (z == z0 && b.channel == 0) p00 = at(b, z);
+          if (z == z0 + 1 && b.channel == 0) p10 = at(b, z);
+          if (z == z0 && b.channel == 1) p01 = at(b, z);
+        }
+      }
+      base = p00;
+      zs = nz > 1 ? (int64_t)(p10 - p00) : plane;
+      cs = g.C > 1 ? (int64_t)(p01 - p00) : (int64_t)nz * plane;
+      for (int64_t k = i; k < i + len && affine; ++k) {
+        const vt_block& b = blocks[k];
+        for (int z = b.origin[2]; z < b.origin[2] + b.dims[2] && affine; ++z)
+          affine = at(b, z) == p00 + (int64_t)(z - z0) * zs + (int64_t)b.channel * cs;
+      }
+      affine = affine && zs > 0 && cs > 0 && planar_leaf_ok(*this, base, zs, cs);
+    }
+    if (!affine) {
+      // gather the layer into the planar layer buffer
+      if (!d_acc)
+        VT_CUDA(cudaMalloc(&d_acc, (size_t)M[2] * g.dims[1] * g.dims[0] * g.C * g.sb));
+      for (int64_t k = i; k < i + len; ++k) {
+        const vt_block& b = blocks[k];
+        uint8_t* dst = d_acc + ((size_t)b.channel * M[2] + (b.origin[2] - z0)) * plane;
+        VT_CUDA(cudaMemcpyAsync(dst, b.samples, plane * b.dims[2],
+                                mem_kind == VT_MEM_DEVICE ? cudaMemcpyDeviceToDevice
+                                                          : cudaMemcpyHostToDevice,
+                                stream));
+      }
+      base = d_acc;
+      zs = plane;
+      cs = (int64_t)M[2] * plane;
+    } else {
+      ++zero_copy_layers;
+    }
+    planar = {true, base, zs, cs};
+    const int o[3] = {0, 0, z0}, d[3] = {g.dims[0], g.dims[1], nz};
+    try {
+      insert_staged(-1, o, d, base, g.C, 0, g.C, len);
+    } catch (...) {
+      planar = PlanarSrc{};
+      throw;
+    }
+    planar = PlanarSrc{};
+    ++layer_groups;
+    i += len;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1403,7 +1579,7 @@ void Tree::propagate() {
 
 void Tree::flush() {
   VT_CUDA(cudaSetDevice(device));
-  materialize_layer();
+  materialize_layer(false);
   flush_structure();
   propagate();
 }
@@ -1487,9 +1663,11 @@ void Tree::prune(std::vector<std::vector<int64_t>>& touched, std::vector<char>& 
 // ---------------------------------------------------------------------------
 
 void Tree::fill_borders() {
+  flush_replays();
   ProfScope pf(prof, 3);
   flush();
   ++data_version;
+  touch_all();
   std::vector<BorderJob> jobs;
   static thread_local std::vector<int64_t> bricks;  // scratch: every brick, BFS order
   bricks.resize(g.capacity);  // an upper bound; the scratch keeps its pages
@@ -1562,6 +1740,8 @@ void Tree::publish_halos() {
   int32_t* d = upload(*this, sl);
   launch_clear_shells(*this, d, (int)sl.size());
   release(*this, d);
+  ++data_version;
+  touch_all();
   halo_prefill = false;
   prefill_valid = false;
   owed_lo.clear();
@@ -1574,10 +1754,12 @@ void Tree::publish_halos() {
 
 void Tree::merge(int64_t n, const int64_t* idx, const int32_t* nflags, const int32_t* stats_in,
                  const void* bricks, int mem_kind, int64_t inserted_voxels) {
+  flush_replays();
   publish_halos();
   prefill_valid = false;
   flush();
   ++data_version;
+  touch_all();
   const int C = g.C;
   std::vector<int64_t> order(n);
   for (int64_t r = 0; r < n; ++r) order[r] = r;

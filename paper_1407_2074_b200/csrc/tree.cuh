@@ -101,6 +101,15 @@ struct Tree {
   std::priority_queue<int32_t, std::vector<int32_t>, std::greater<int32_t>> free_slots;
   int64_t cursor = 0;
   int64_t data_version = 0;  // bumped by every pool mutation
+  // data_version of each pool slot's last write (every slot changed at
+  // all_ver or later): renderers refresh derived per-brick data (brick
+  // maxima) for the changed slots only
+  std::vector<int64_t> slot_ver;
+  int64_t all_ver = 0;
+  void touch_slot(int32_t s) {
+    if (s >= 0 && (size_t)s < slot_ver.size()) slot_ver[s] = data_version;
+  }
+  void touch_all() { all_ver = data_version; }
   // tau == 0 dense build (dense_build.cu): complete[n] = every in-volume leaf
   // under n was fully covered by one dense insertion, so n's brick is a pure
   // function of the data; VT_DENSE=0 disables the path (A/B testing)
@@ -151,16 +160,41 @@ struct Tree {
     std::vector<DenseJob> djobs;             // (gy, gx) order
     std::vector<std::array<int, 3>> order;   // (z, dz, channel) in arrival order
     std::vector<int64_t> upd;                // one block's UPDATED list
+    bool dirty = false;                      // blocks received since the last leaf launch
+    bool prefilled = false;                  // the last leaf launch prefilled shells
   } dl;
   bool defer_enabled = true;    // env VT_DEFER=0 turns it off
   bool defer_start = false;     // set by try_defer: this insertion opens a layer
-  uint8_t* d_acc = nullptr;     // [Mz][Y][X][C] layer buffer (lazy)
-  int64_t deferred_layers = 0;
+  uint8_t* d_acc = nullptr;     // [C][Mz][Y][X] planar layer buffer (lazy)
+  uint8_t* d_acc_il = nullptr;  // interleaved scratch for the non-TMA leaf kernels (lazy)
+  int64_t d_acc_il_bytes = 0;
+  int64_t deferred_layers = 0, layer_groups = 0, zero_copy_layers = 0;
   bool try_defer(int channel, const int origin[3], const int dims[3], const void* dsrc,
                  int src_stride, int src_off);
   void defer_copy(int channel, const int origin[3], const int dims[3], const void* dsrc);
-  void materialize_layer();
+  // a reader needs the tree: launch the leaf kernel over the received planes
+  // (missing ones are the background seeds); `close` ends the layer (a
+  // non-follower insertion arrives)
+  void materialize_layer(bool close = false);
+  void run_layer(bool partial);
+  void close_layer();
   void finish_layer();
+  // planar source of the current dense insertion (insert_many layer groups):
+  // sample (x, y, z, c) at base + c*cstride + (z - oz)*zstride + (y*X + x)*sb
+  struct PlanarSrc {
+    bool active = false;
+    const uint8_t* base = nullptr;
+    int64_t zstride = 0, cstride = 0;
+  } planar;
+  // dense leaf launch from the current source (planar if set, else the
+  // interleaved block at dsrc)
+  int leaf_launch(const void* dsrc, int64_t nsrc, int oz, int dz, int prefill, const DenseJob* dj,
+                  int n, const int gn[3], int g0z);
+  // B200 batched insertion: same tree and queued events as n successive
+  // insert() calls; whole brick layers of single-channel full-x/y blocks
+  // become one dense insertion
+  void insert_many(int64_t n, const vt_block* blocks, int mem_kind);
+  int64_t layer_group(int64_t i, int64_t n, const vt_block* blocks, int mem_kind);
   int64_t leaf_index(int gx, int gy, int gz) const {
     return g.level_start[g.depth] + morton[0][gx] + morton[1][gy] + morton[2][gz];
   }
@@ -183,6 +217,19 @@ struct Tree {
   // packed (kind << 56 | node index): 8 bytes per event, a whole-volume
   // insertion emits ~4 per node
   std::vector<uint64_t> events;
+  // lazily replayed tail: rep_list appended rep_count more times (the
+  // UPDATED list every later block of a brick layer repeats)
+  std::vector<uint64_t> rep_list;
+  int64_t rep_count = 0;
+  void flush_replays() {
+    if (rep_count <= 0) return;
+    const size_t e0 = events.size(), nl = rep_list.size();
+    events.resize(e0 + nl * (size_t)rep_count);
+    for (int64_t r = 0; r < rep_count; ++r)
+      std::copy(rep_list.begin(), rep_list.end(), events.begin() + e0 + r * nl);
+    rep_count = 0;
+  }
+  int64_t event_total() const { return (int64_t)events.size() + (int64_t)rep_list.size() * rep_count; }
   static uint64_t ev_pack(int32_t kind, int64_t idx) {
     return ((uint64_t)(uint32_t)kind << 56) | (uint64_t)idx;
   }
@@ -278,7 +325,7 @@ struct Tree {
   bool dense_eligible(int channel, const int origin[3], const int dims[3], const void* dsrc,
                       int src_stride, int src_off) const;
   void insert_staged(int channel, const int origin[3], const int dims[3], const void* dsrc,
-                     int src_stride, int src_off, int reps);
+                     int src_stride, int src_off, int reps, int64_t ev_reps = 0);
   void flush_structure();
   void propagate();
   bool dense_parent(int64_t p) const;
@@ -318,6 +365,15 @@ void launch_octant(const Tree& t, const OctJob* d_jobs, int n);
 constexpr int kLeafPrefilled = 1, kLeafTma = 2;
 int launch_dense_leaf(const Tree& t, const void* src, int64_t nsrc, int oz, int prefill,
                       const DenseJob* jobs, int n, const int gn[3], int g0z);
+// planar (c, z, y, x) source through a 4-D TMA tensor map; -1 = unsupported
+// here (8-bit samples, unaligned strides, oversized bricks)
+bool planar_leaf_ok(const Tree& t, const void* base, int64_t zstride, int64_t cstride);
+int launch_dense_leaf_planar(const Tree& t, const void* base, int64_t zstride, int64_t cstride,
+                             int oz, int64_t dz, int prefill, const DenseJob* jobs, int n,
+                             const int gn[3], int g0z);
+void launch_planar_to_interleaved(const Tree& t, const void* base, int64_t zstride,
+                                  int64_t cstride, int dz, void* dst);
+void launch_fill_bg(const Tree& t, void* dst, int64_t n);
 // fused level-1 parents: accumulators before / statistics after the leaf kernel
 void launch_init_fused(const Tree& t, const int64_t* d_nodes, int n);
 // channel `c` of an n-voxel single-channel block into an interleaved buffer

@@ -16,7 +16,6 @@ import ctypes as ct
 import os
 import sys
 import threading
-from collections.abc import Sequence
 from dataclasses import dataclass
 from enum import IntEnum
 
@@ -75,48 +74,106 @@ def classify_homogeneous(smin, smax, threshold: float):
     return per, all(per)
 
 
-class EventBatch(Sequence):
-    """The change events of one or more insertions, in order: a read-only
-    sequence of ChangeEvent (what insert_block / drain_events return in the
-    reference, octree.py:180-183, 393-395) backed by two arrays, so a slab
-    that creates and updates thousands of nodes costs no Python objects
-    until a caller indexes it.  ``kinds`` / ``indices`` expose the arrays."""
+_EV_TABLES: dict = {}  # ChangeKind value -> object array of interned events by node index
 
-    __slots__ = ("kinds", "indices")
 
-    def __init__(self, kinds, indices):
-        self.kinds = np.asarray(kinds, np.int32)
-        self.indices = np.asarray(indices, np.int64)
+def _event_table(kind: int, n: int) -> np.ndarray:
+    tbl = _EV_TABLES.get(kind)
+    if tbl is None or len(tbl) < n:
+        new = np.empty(max(n, 2 * (0 if tbl is None else len(tbl)), 1024), dtype=object)
+        if tbl is not None:
+            new[:len(tbl)] = tbl
+        _EV_TABLES[kind] = tbl = new
+    return tbl
+
+
+def _events_from_arrays(kinds: np.ndarray, idx: np.ndarray) -> list:
+    """ChangeEvent objects for packed (kind, index) arrays.  ChangeEvent is a
+    frozen dataclass, so equal events can be shared: each (kind, index) is
+    built once per process and a batch is a vectorised gather."""
+    n = len(kinds)
+    if n == 0:
+        return []
+    out = np.empty(n, dtype=object)
+    for k in np.unique(kinds).tolist():
+        m = kinds == k
+        ii = idx[m]
+        tbl = _event_table(k, int(ii.max()) + 1)
+        vals = tbl[ii]
+        miss = np.flatnonzero(np.equal(vals, None))
+        if miss.size:
+            kind = ChangeKind(k)
+            for u in np.unique(ii[miss]).tolist():
+                tbl[u] = ChangeEvent(kind, u)
+            vals = tbl[ii]
+        out[m] = vals
+    return out.tolist()
+
+
+class EventList(list):
+    """What insert_block / drain_events return (octree.py:180-183, 393-395):
+    a real ``list`` of ChangeEvent.  The library's packed form is kept as
+    ``kinds`` / ``indices`` numpy arrays (B200 extension for bulk consumers
+    such as DeviceState.apply_events); any in-place change of the list
+    recomputes them from the elements."""
+
+    def __init__(self, items=(), *, kinds=None, indices=None):
+        if kinds is not None:
+            kinds = np.asarray(kinds, np.int32)
+            indices = np.asarray(indices, np.int64)
+            super().__init__(_events_from_arrays(kinds, indices))
+            self._arr = (kinds, indices)
+        else:
+            super().__init__(items)
+            self._arr = None
+
+    @classmethod
+    def from_arrays(cls, kinds, indices) -> "EventList":
+        return cls(kinds=kinds, indices=indices)
 
     @staticmethod
-    def concat(batches) -> "EventBatch":
-        batches = list(batches)
+    def concat(batches) -> "EventList":
+        batches = [b for b in batches if len(b)]
         if not batches:
-            return EventBatch(np.empty(0, np.int32), np.empty(0, np.int64))
+            return EventList()
         if len(batches) == 1:
             return batches[0]
-        return EventBatch(np.concatenate([b.kinds for b in batches]),
-                          np.concatenate([b.indices for b in batches]))
+        return EventList.from_arrays(np.concatenate([b.kinds for b in batches]),
+                                     np.concatenate([b.indices for b in batches]))
 
-    def __len__(self):
-        return len(self.kinds)
+    def _arrays(self):
+        if self._arr is None or len(self._arr[0]) != len(self):
+            self._arr = (np.fromiter((int(e.kind) for e in self), np.int32, len(self)),
+                         np.fromiter((int(e.node_index) for e in self), np.int64, len(self)))
+        return self._arr
 
-    def __getitem__(self, i):
-        if isinstance(i, slice):
-            return EventBatch(self.kinds[i], self.indices[i])
-        return ChangeEvent(ChangeKind(int(self.kinds[i])), int(self.indices[i]))
+    @property
+    def kinds(self) -> np.ndarray:
+        return self._arrays()[0]
 
-    def __eq__(self, other):
-        if isinstance(other, EventBatch):
-            return (np.array_equal(self.kinds, other.kinds)
-                    and np.array_equal(self.indices, other.indices))
-        try:
-            return list(self) == list(other)
-        except TypeError:
-            return NotImplemented
+    @property
+    def indices(self) -> np.ndarray:
+        return self._arrays()[1]
 
-    def __repr__(self):
-        return f"EventBatch({len(self)} events)"
+    def _dirty(self):
+        self._arr = None
+
+
+def _mutator(name):
+    base = getattr(list, name)
+
+    def fn(self, *a, **kw):
+        self._arr = None
+        return base(self, *a, **kw)
+    fn.__name__ = name
+    return fn
+
+
+for _m in ("__setitem__", "__delitem__", "__iadd__", "__imul__", "append", "extend", "insert",
+           "pop", "remove", "clear", "sort", "reverse"):
+    setattr(EventList, _m, _mutator(_m))
+
+EventBatch = EventList  # round-1 name
 
 
 class OctreeNode:
@@ -200,7 +257,7 @@ class Octree:
         self.geometry = TreeGeometry.build(desc, cfg)
         self.threshold = cfg.resolve_threshold(desc)
         self.lock = threading.RLock()
-        self._events: list[EventBatch] = []
+        self._events: list[EventList] = []
         self._closed = False
         d = _lib.vt_tree_desc()
         d.dims[:] = list(desc.dims)
@@ -242,7 +299,7 @@ class Octree:
         return self._h
 
     # -- events --------------------------------------------------------------
-    def _collect(self) -> "EventBatch":
+    def _collect(self) -> "EventList":
         n = ct.c_int64()
         _lib.call("vt_tree_event_count", self._h, ct.byref(n))
         kinds = np.empty(n.value, np.int32)
@@ -251,19 +308,29 @@ class Octree:
             got, more = ct.c_int64(), ct.c_int32()
             _lib.call("vt_tree_take_events", self._h, _lib.ptr(kinds, ct.c_int32),
                       _lib.ptr(idx, ct.c_int64), n.value, ct.byref(got), ct.byref(more))
-        out = EventBatch(kinds, idx)
-        if len(out):
+        out = (kinds, idx)
+        if n.value:
             self._events.append(out)
         return out
 
-    def drain_events(self) -> "EventBatch":
+    def drain_event_arrays(self) -> tuple[np.ndarray, np.ndarray]:
+        """B200 extension: drain_events as packed (kinds int32, indices
+        int64) arrays — no Python object per event (a 2048^2 slice of 32^3
+        bricks updates ~5.5k nodes)."""
         with self.lock:
             self._collect()
-            ev, self._events = EventBatch.concat(self._events), []
-            return ev
+            parts, self._events = self._events, []
+            if not parts:
+                return np.empty(0, np.int32), np.empty(0, np.int64)
+            return (np.concatenate([p[0] for p in parts]),
+                    np.concatenate([p[1] for p in parts]))
+
+    def drain_events(self) -> "EventList":
+        """Every queued change event, oldest first (octree.py:180-183)."""
+        return EventList.from_arrays(*self.drain_event_arrays())
 
     # -- insertion -------------------------------------------------------------
-    def insert_block(self, channel: int, origin, values) -> EventBatch:
+    def insert_block(self, channel: int, origin, values) -> EventList:
         """Octree.insert_block (octree.py:323-397).  ``values`` (dz, dy, dx)
         numpy array (host) or a CUDA tensor/array exposing
         ``__cuda_array_interface__`` (device, stream-ordered)."""
@@ -272,12 +339,107 @@ class Octree:
             raise ValueError(f"channel {channel} out of range")
         return self._insert(int(channel), origin, values, 3)
 
-    def insert_channels(self, origin, values) -> EventBatch:
+    def insert_channels(self, origin, values) -> EventList:
         """All channels at once: values (dz, dy, dx, C) interleaved; same
         tree and events as C successive insert_block calls."""
         return self._insert(-1, origin, values, 4)
 
-    def _insert(self, channel: int, origin, values, ndim: int) -> EventBatch:
+    def insert_many(self, blocks) -> None:
+        """B200 extension (vt_tree_insert_many): insert ``blocks`` — an
+        iterable of ``(channel, origin, values)`` as insert_block takes them —
+        in one library call.  The tree and the queued change events
+        (drain_events) are exactly those of calling insert_block on each in
+        order (ingest_stream's frame loop, ingest.py:306-358); only the
+        per-call return lists are not built.  Consecutive device or host
+        blocks are batched; at threshold 0 the single-channel full-x/y blocks
+        that complete a brick layer become one dense insertion, read in place
+        when they are slices of one planar (C, Z, Y, X) device array."""
+        desc = self.descriptor
+        run, run_kind, keep, cstream = [], None, [], 0
+
+        def flush_run():
+            nonlocal run, keep
+            if not run:
+                return
+            arr = (_lib.vt_block * len(run))(*run)
+            _lib.call("vt_tree_insert_many", self._h, len(run), arr, run_kind,
+                      ct.c_void_p(cstream))
+            run, keep = [], []
+
+        with self.lock:
+            for channel, origin, values in blocks:
+                if not 0 <= int(channel) < desc.channels:
+                    flush_run()
+                    raise ValueError(f"channel {channel} out of range")
+                src, kind, shape, k, cs = self._source(values, 3)
+                if run and kind != run_kind:
+                    flush_run()
+                run_kind, cstream = kind, cs
+                o = [int(v) for v in origin]
+                b = _lib.vt_block()
+                b.channel = int(channel)
+                b.origin[:] = o
+                b.dims[:] = [shape[2], shape[1], shape[0]]
+                b.samples = src
+                run.append(b)
+                keep.append(k)
+            flush_run()
+
+    _BLOCK_DTYPE = np.dtype([("channel", "<i4"), ("origin", "<i4", 3), ("dims", "<i4", 3),
+                             ("pad", "<i4"), ("samples", "<u8")])
+
+    def insert_planar(self, values, z0: int = 0) -> None:
+        """B200 extension: a slab of a slice stream in VSTR order.  ``values``
+        is a (C, dz, Y, X) planar block (CUDA tensor or host array) holding
+        planes z0 .. z0+dz of every channel over the full x/y extent; the
+        tree and queued events are those of
+        ``insert_block(c, (0, 0, z0 + z), values[c, z:z + 1])`` for each z,
+        for each channel c (ingest_stream's frame order, ingest.py:306-358),
+        issued as one vt_tree_insert_many call without per-slice Python work."""
+        desc = self.descriptor
+        torch = sys.modules.get("torch")
+        if torch is not None and isinstance(values, torch.Tensor) and values.is_cuda:
+            want = torch.uint8 if desc.dtype == np.uint8 else torch.uint16
+            if values.dtype != want:
+                raise ValueError(f"planar block must be {want}")
+            if values.dim() != 4 or values.stride(3) != 1 or values.stride(2) != values.shape[3]:
+                raise ValueError("planar block must be (C, dz, Y, X) with contiguous planes")
+            C, dz, Y, X = values.shape
+            base, es = values.data_ptr(), values.element_size()
+            cstr, zstr = values.stride(0) * es, values.stride(1) * es
+            kind = _lib.VT_MEM_DEVICE
+            cs = torch.cuda.current_stream(values.device).cuda_stream
+            keep = values
+        else:
+            arr = np.ascontiguousarray(np.asarray(values).astype(desc.dtype, copy=False))
+            if arr.ndim != 4:
+                raise ValueError("planar block must be (C, dz, Y, X)")
+            C, dz, Y, X = arr.shape
+            base, cstr, zstr = arr.ctypes.data, arr.strides[0], arr.strides[1]
+            kind, cs, keep = _lib.VT_MEM_HOST, 0, arr
+        if C != desc.channels:
+            raise ValueError("planar block must hold every channel")
+        n = dz * C
+        blk = np.zeros(n, self._BLOCK_DTYPE)
+        z = np.repeat(np.arange(dz, dtype=np.int64), C)
+        c = np.tile(np.arange(C, dtype=np.int64), dz)
+        blk["channel"] = c
+        blk["origin"][:, 2] = z0 + z
+        blk["dims"][:] = (X, Y, 1)
+        blk["samples"] = (base + c * cstr + z * zstr).astype(np.uint64)
+        with self.lock:
+            _lib.call("vt_tree_insert_many", self._h, n,
+                      blk.ctypes.data_as(ct.POINTER(_lib.vt_block)), kind, ct.c_void_p(cs))
+        del keep
+
+    def stream_counts(self) -> tuple[int, int, int]:
+        """(brick layers built by insert_many as one dense insertion, of which
+        read in place, deferred layers of per-block slice streams)."""
+        a, b, c = ct.c_int64(), ct.c_int64(), ct.c_int64()
+        _lib.call("vt_tree_stream_counts", self._h, ct.byref(a), ct.byref(b), ct.byref(c))
+        return int(a.value), int(b.value), int(c.value)
+
+    def _insert(self, channel: int, origin, values, ndim: int) -> EventList:
         desc = self.descriptor
         origin = tuple(int(v) for v in origin)
         src, kind, shape, keep, cstream = self._source(values, ndim)
@@ -309,10 +471,9 @@ class Octree:
             else:
                 kinds, idx = kinds[:total], idx[:total]
             del keep  # device blocks: the caller's stream waits for our reads
-            out = EventBatch(kinds, idx)
             if total:
-                self._events.append(out)
-            return out
+                self._events.append((kinds, idx))
+            return EventList.from_arrays(kinds, idx)
 
     def _source(self, values, ndim):
         """(pointer, memory kind, shape, keep-alive, caller stream handle)."""

@@ -119,6 +119,7 @@ class OutOfCoreRenderer:
         dtype = {OUT_F64: np.float64, OUT_F32: np.float32, OUT_RGBA8: np.uint8}[out_kind]
         img = host_image((cam.height, cam.width, 4), dtype)
         cnt = _lib.vt_counters()
+        self.device.order_after_torch()
         _lib.call("vt_render_fullframe", self.device.handle, ct.byref(s),
                   ct.c_void_p(img.ctypes.data), out_kind, 0, ct.byref(cnt))
         return img, RenderCounters.from_vt(cnt)
@@ -131,6 +132,7 @@ class OutOfCoreRenderer:
         img = np.empty((y1 - y0, x1 - x0, 4), dtype=dtype)
         cnt = _lib.vt_counters()
         r = (ct.c_int32 * 4)(x0, y0, x1, y1)
+        self.device.order_after_torch()
         _lib.call("vt_render_tile", self.device.handle, ct.byref(s), r,
                   ct.c_void_p(img.ctypes.data), out_kind, 0, ct.byref(cnt))
         return img, RenderCounters.from_vt(cnt)
@@ -183,6 +185,7 @@ class RefinementSession:
         if tile is not None:
             x0, y0, x1, y1 = (int(v) for v in tile)
             t = (ct.c_int32 * 4)(max(0, x0), max(0, y0), min(cam.width, x1), min(cam.height, y1))
+        renderer.device.order_after_torch()
         _lib.call("vt_rays_create", renderer.device.handle, ct.byref(s), t, ct.byref(h))
         self._h = h
         self.rays = _RayView(self)
@@ -204,6 +207,7 @@ class RefinementSession:
             return True
         cnt = _lib.vt_counters()
         sus = ct.c_int64()
+        self.renderer.device.order_after_torch()
         _lib.call("vt_rays_march", self._h, 1, ct.byref(cnt), ct.byref(sus))
         self.passes += 1
         pc = RenderCounters.from_vt(cnt)

@@ -94,10 +94,15 @@ class SortFirstRenderer:
         local = self._buffer("local", (rows, cam.width, 4), dtype)
         s = scene_to_vt(scene, self.descriptor)
         cnt = _lib.vt_counters()
-        torch.cuda.current_stream().synchronize()
+        # stream ordering both ways, no host synchronisation: the tree's
+        # stream after torch's (the buffer), torch's after the render (the
+        # gather reads it)
+        self.device.order_after_torch()
         _lib.call("vt_render_strips", self.device.handle, ct.byref(s), self.strip_rows,
                   self.world, self.rank, ct.c_void_p(local.data_ptr()), out_kind, 1,
                   ct.byref(cnt))
+        _lib.call("vt_tree_signal_stream", self.device.octree.handle,
+                  ct.c_void_p(torch.cuda.current_stream().cuda_stream))
         return local, RenderCounters.from_vt(cnt)
 
     def gather(self, local):

@@ -57,73 +57,121 @@ def _write_atomic(path, chunks) -> None:
         raise
 
 
-def pool_bytes(bricks: np.ndarray, page_bricks: int, brick_shape, channels: int, dtype):
-    """Chunks of a freshly written, flushed VXBP holding ``bricks`` in order
-    (BrickStore.create + allocate/write_brick + flush, paging.py:120-380)."""
+def _pool_chunks(n, batches, page_bricks: int, brick_shape, channels: int, dtype):
+    """Chunks of a freshly written, flushed VXBP holding n bricks, taken in
+    order from ``batches`` (arrays of whole bricks) — BrickStore.create +
+    allocate/write_brick + flush, paging.py:120-380."""
     dt = np.dtype(dtype).newbyteorder("<")
-    n = len(bricks)
     nbytes = int(np.prod(brick_shape)) * channels * dt.itemsize
     pages = -(-n // page_bricks)
     stride = page_bricks * nbytes + _CRC.size
     footer = _POOL_HEAD.size + pages * stride if pages else 0
-    out = [_POOL_HEAD.pack(POOL_MAGIC, 1, page_bricks, nbytes, *brick_shape, channels,
-                           _FMT_CODES[np.dtype(dtype).name], pages, footer)]
-    flat = np.ascontiguousarray(bricks, dtype=dt).reshape(n, -1).view(np.uint8) if n else None
-    for p in range(pages):
-        body = bytearray(page_bricks * nbytes)
-        part = flat[p * page_bricks:(p + 1) * page_bricks]
-        body[:part.size] = part.tobytes()
-        body = bytes(body)
-        out += [body, _CRC.pack(zlib.crc32(body))]
+    yield _POOL_HEAD.pack(POOL_MAGIC, 1, page_bricks, nbytes, *brick_shape, channels,
+                          _FMT_CODES[np.dtype(dtype).name], pages, footer)
+    page, cur, done = bytearray(), 0, 0
+    for b in batches:
+        flat = np.ascontiguousarray(b, dtype=dt).reshape(len(b), -1).view(np.uint8)
+        pos = 0
+        while pos < len(flat):
+            take = min(page_bricks - cur, len(flat) - pos)
+            page += flat[pos:pos + take].tobytes()
+            cur += take
+            pos += take
+            done += take
+            if cur == page_bricks:
+                yield bytes(page)
+                yield _CRC.pack(zlib.crc32(page))
+                page, cur = bytearray(), 0
+    if page:
+        page += bytes(page_bricks * nbytes - len(page))
+        yield bytes(page)
+        yield _CRC.pack(zlib.crc32(page))
+    assert done == n, (done, n)
     if pages:
         bits = np.zeros(pages * page_bricks, np.uint8)
         bits[:n] = 1
-        out.append(np.packbits(bits, bitorder="little").tobytes())
-    return out
+        yield np.packbits(bits, bitorder="little").tobytes()
 
 
-def save_octree(tree: Octree, octree_path, pool_path) -> None:
+def pool_bytes(bricks: np.ndarray, page_bricks: int, brick_shape, channels: int, dtype):
+    """Chunks of a freshly written, flushed VXBP holding ``bricks`` in order."""
+    return list(_pool_chunks(len(bricks), [bricks] if len(bricks) else [], page_bricks,
+                             brick_shape, channels, dtype))
+
+
+def _octree_chunks(tree: Octree, idx, flags, stats):
+    """VXOC metadata chunks (serialize.py:92-124)."""
+    desc, cfg = tree.descriptor, tree.config
+    hdr = 0
+    if desc.channel_transforms is not None:
+        hdr |= _F_TRANSFORMS
+    if tree.construction_finished:
+        hdr |= _F_FINISHED
+    if tree.borders_filled:
+        hdr |= _F_BORDERS
+    parts = [_HEAD.pack(MAGIC, VERSION),
+             _DESC.pack(*desc.dims, desc.channels, _FMT_CODES[desc.sample_format],
+                        *desc.spacing, desc.background_value, hdr)]
+    if desc.channel_transforms is not None:
+        parts.append(np.asarray(desc.channel_transforms, dtype="<f8").tobytes())
+    parts.append(_CONF.pack(*cfg.brick_dims, tree.threshold, cfg.overlap,
+                            cfg.page_bricks, cfg.ram_page_limit))
+    parts.append(_TREE.pack(tree.geometry.depth, len(idx)))
+    geo = tree.geometry
+    canon = 0
+    for r, i in enumerate(idx):
+        f = int(flags[r])
+        nf = (_N_BRICK if f & _lib.NODE_BRICK else 0) | \
+            (_N_CHILDREN if f & _lib.NODE_CHILDREN else 0) | \
+            (_N_INVOL if f & _lib.NODE_IN_VOLUME else 0)
+        parts.append(_NODE.pack(int(i), geo.level_of_index(int(i)), nf))
+        inv = bool(f & _lib.NODE_IN_VOLUME)
+        for c in range(desc.channels):
+            a, lo, hi, slo, shi = (int(v) for v in stats[r, c])
+            parts.append(_CHAN.pack(lo, hi, a, slo if inv else 0, shi if inv else 0))
+        if f & _lib.NODE_BRICK:
+            parts.append(_LOC.pack(*divmod(canon, cfg.page_bricks)))
+            canon += 1
+        else:
+            parts.append(_LOC.pack(_NO_BRICK, _NO_BRICK))
+    return parts
+
+
+def _brick_batches(tree: Octree, bricked, batch: int):
+    for k in range(0, len(bricked), batch):
+        yield tree.export(indices=bricked[k:k + batch])[3]
+
+
+def save_octree(tree: Octree, octree_path, pool_path, *, batch: int = 4096) -> None:
     """Persist the tree and a canonically compacted copy of its pool
-    (serialize.py:61-125)."""
+    (serialize.py:61-125); bricks leave HBM in batches."""
     desc, cfg = tree.descriptor, tree.config
     with tree.lock:
-        idx, flags, stats, bricks = tree.export()
-        _write_atomic(pool_path, pool_bytes(bricks, cfg.page_bricks,
-                                            tuple(reversed(cfg.stored_brick_dims)),
-                                            desc.channels, desc.dtype))
-        hdr = 0
-        if desc.channel_transforms is not None:
-            hdr |= _F_TRANSFORMS
-        if tree.construction_finished:
-            hdr |= _F_FINISHED
-        if tree.borders_filled:
-            hdr |= _F_BORDERS
-        parts = [_HEAD.pack(MAGIC, VERSION),
-                 _DESC.pack(*desc.dims, desc.channels, _FMT_CODES[desc.sample_format],
-                            *desc.spacing, desc.background_value, hdr)]
-        if desc.channel_transforms is not None:
-            parts.append(np.asarray(desc.channel_transforms, dtype="<f8").tobytes())
-        parts.append(_CONF.pack(*cfg.brick_dims, tree.threshold, cfg.overlap,
-                                cfg.page_bricks, cfg.ram_page_limit))
-        parts.append(_TREE.pack(tree.geometry.depth, len(idx)))
-        geo = tree.geometry
-        canon = 0
-        for r, i in enumerate(idx):
-            f = int(flags[r])
-            nf = (_N_BRICK if f & _lib.NODE_BRICK else 0) | \
-                (_N_CHILDREN if f & _lib.NODE_CHILDREN else 0) | \
-                (_N_INVOL if f & _lib.NODE_IN_VOLUME else 0)
-            parts.append(_NODE.pack(int(i), geo.level_of_index(int(i)), nf))
-            inv = bool(f & _lib.NODE_IN_VOLUME)
-            for c in range(desc.channels):
-                a, lo, hi, slo, shi = (int(v) for v in stats[r, c])
-                parts.append(_CHAN.pack(lo, hi, a, slo if inv else 0, shi if inv else 0))
-            if f & _lib.NODE_BRICK:
-                parts.append(_LOC.pack(*divmod(canon, cfg.page_bricks)))
-                canon += 1
-            else:
-                parts.append(_LOC.pack(_NO_BRICK, _NO_BRICK))
-        _write_atomic(octree_path, parts)
+        idx, flags, stats, _ = tree.export(with_bricks=False)
+        bricked = idx[(flags & _lib.NODE_BRICK) != 0]
+        _write_atomic(pool_path, _pool_chunks(len(bricked), _brick_batches(tree, bricked, batch),
+                                              cfg.page_bricks,
+                                              tuple(reversed(cfg.stored_brick_dims)),
+                                              desc.channels, desc.dtype))
+        _write_atomic(octree_path, _octree_chunks(tree, idx, flags, stats))
+
+
+def octree_digests(tree: Octree, *, batch: int = 4096) -> tuple[str, str]:
+    """sha256 of the VXOC and VXBP files save_octree would write, without
+    writing them (the digest parity harness at BASELINE sizes)."""
+    import hashlib
+    desc, cfg = tree.descriptor, tree.config
+    with tree.lock:
+        idx, flags, stats, _ = tree.export(with_bricks=False)
+        bricked = idx[(flags & _lib.NODE_BRICK) != 0]
+        hp = hashlib.sha256()
+        for c in _pool_chunks(len(bricked), _brick_batches(tree, bricked, batch), cfg.page_bricks,
+                              tuple(reversed(cfg.stored_brick_dims)), desc.channels, desc.dtype):
+            hp.update(c)
+        ho = hashlib.sha256()
+        for c in _octree_chunks(tree, idx, flags, stats):
+            ho.update(c)
+        return ho.hexdigest(), hp.hexdigest()
 
 
 def load_octree(octree_path, pool_path, *, ram_page_limit: int | None = None,
@@ -149,9 +197,13 @@ def load_octree(octree_path, pool_path, *, ram_page_limit: int | None = None,
                             channel_transforms=transforms)
     bx, by, bz, thr, overlap, page_bricks, ram_pages = _CONF.unpack_from(raw, off)
     off += _CONF.size
+    # the file's ram_page_limit is kept (it is part of the VXOC header); the
+    # reference passes an override only to its paging store's RAM cache
+    # (serialize.py:128-206), which the HBM pool does not have, so the
+    # argument is accepted and ignored
+    del ram_page_limit
     cfg = BrickPoolConfig(brick_dims=(bx, by, bz), homogeneity_threshold=thr, overlap=overlap,
-                          page_bricks=page_bricks,
-                          ram_page_limit=ram_pages if ram_page_limit is None else ram_pages)
+                          page_bricks=page_bricks, ram_page_limit=ram_pages)
     depth, count = _TREE.unpack_from(raw, off)
     off += _TREE.size
     idx = np.empty(count, np.int64)

@@ -132,7 +132,9 @@ def test_dense_interleaved_flushes_and_general_inserts(tmp_path):
            ("borders",)]
     ta, ea, sa = _run(dims, C, brick, fmt, ops, dense=False)
     tb, eb, sb = _run(dims, C, brick, fmt, ops, dense=True)
-    assert tb.dense_counts()[0] == 4
+    # 4 dense slabs + the partial single-channel layer a later slab closes
+    # (materialised by the dense leaf kernel, missing planes = seeds)
+    assert tb.dense_counts()[0] == 5
     assert eb == ea
     assert sb == sa
     assert _nodes(tb) == _nodes(ta)
