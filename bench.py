@@ -66,6 +66,7 @@ CLIP_FRAC = 0.8
 COLORS = ((1.0, 0.25, 0.2), (0.2, 1.0, 0.3), (0.25, 0.45, 1.0))
 BYTES_PER_POS_SAMPLE = 8 * CHANNELS * 2  # 8 trilinear corners x C x uint16
 L2_FLUSH_BYTES = 512 << 20
+STREAM_CHUNK = 2 * BRICK  # slices per insert_planar call: a pair of brick layers
 FALLBACK_HBM_GBS = 6650.0
 _SCENE = ("1920x1080 DVR frame, per-channel TFs, 1 clip plane, ET 0.99, step 0.5 voxel, "
           "LOD bias 0")
@@ -292,8 +293,8 @@ def leg_stream(P, dims, stream, peak):
         _lib.call("vt_tree_set_stream", tree.handle, ct.c_void_p(stream.cuda_stream))
         torch.cuda.synchronize()
         with _Ev(stream) as ev:
-            for z0 in range(0, Z, BRICK):
-                tree.insert_planar(P[:, z0:min(Z, z0 + BRICK)], z0)
+            for z0 in range(0, Z, STREAM_CHUNK):
+                tree.insert_planar(P[:, z0:min(Z, z0 + STREAM_CHUNK)], z0)
             with _Ev(stream) as evb:
                 tree.finalize()
                 tree.fill_borders()
@@ -312,7 +313,7 @@ def leg_stream(P, dims, stream, peak):
             res = {"workload": f"{dims[0]}x{dims[1]}x{Z} x{CHANNELS} uint16 S volume, planar "
                                "(C, Z, Y, X) in HBM, every (z, channel) slice in VSTR order "
                                "through Octree.insert_planar (= insert_block per slice), one "
-                               "call per brick layer, + finalize + fill_borders",
+                               f"call per {STREAM_CHUNK} slices, + finalize + fill_borders",
                    "slices": Z * CHANNELS, "ms": round(ms, 3),
                    "fill_borders_ms": round(evb.ms(), 3),
                    "raw_gb": round(raw / 1e9, 3), "pool_gb": round(pool / 1e9, 3),
@@ -567,7 +568,7 @@ def leg_stream_host(dims, stream, nz):
         t0 = time.perf_counter()
         with _Ev(stream) as ev:
             for z0 in range(0, nz, BRICK):
-                tree.insert_planar(H[:, z0:min(nz, z0 + BRICK)].numpy(), z0)
+                tree.insert_planar(H[:, z0:min(nz, z0 + BRICK)], z0)
             tree.sync()
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0

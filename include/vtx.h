@@ -115,9 +115,10 @@ vt_status vt_tree_signal_stream(vt_tree* tree, void* stream);
  * one call with the caller-stream ordering of a device block (wait on
  * caller_stream before reading it, make caller_stream wait for the reads;
  * a null caller_stream is the legacy default stream)
- * and the pending change events copied out when they fit in `cap`;
- * *n_events = how many were pending (more than cap: none copied, take them
- * with vt_tree_take_events) */
+ * and a copy of THIS insertion's change events when they fit in `cap` (they
+ * stay queued for vt_tree_take_events, as insert_block's returned list stays
+ * in Octree._events, octree.py:393-395); *n_events = how many it emitted
+ * (more than cap: none copied — vt_tree_copy_events(event_count - n, n)) */
 vt_status vt_tree_insert_ev(vt_tree* tree, int32_t channel, const int32_t origin[3],
                             const int32_t dims[3], const void* samples, int32_t mem_kind,
                             void* caller_stream, int32_t* kinds, int64_t* indices, int64_t cap,
@@ -154,6 +155,11 @@ vt_status vt_tree_insert_many(vt_tree* tree, int64_t n, const vt_block* blocks, 
  * *n returns the number written (<= cap); call again while *more != 0 */
 vt_status vt_tree_take_events(vt_tree* tree, int32_t* kinds, int64_t* indices, int64_t cap,
                               int64_t* n, int32_t* more);
+/* B200 extension: copy queued events [from, from + n) (0 = oldest) without
+ * taking them (vt_tree_insert_ev reports an insertion's events this way
+ * when they exceed its buffer) */
+vt_status vt_tree_copy_events(vt_tree* tree, int64_t from, int64_t n, int32_t* kinds,
+                              int64_t* indices);
 /* number of pending change events (size the take_events buffers) */
 vt_status vt_tree_event_count(vt_tree* tree, int64_t* n);
 /* Octree.finalize / fill_borders (octree.py:536-614) */

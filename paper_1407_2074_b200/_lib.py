@@ -88,6 +88,7 @@ SIGNATURES = {
     "vt_tree_publish_halos": [P],
     "vt_mirror_bmax_stats": [P, PI64, PI64],
     "vt_tree_take_events": [P, PI32, PI64, I64, PI64, PI32],
+    "vt_tree_copy_events": [P, I64, I64, PI32, PI64],
     "vt_tree_event_count": [P, PI64],
     "vt_tree_checksum": [P, ct.POINTER(ct.c_uint64)],
     "vt_tree_export_nodes": [P, I64, PI64, PI32, PI32, P, I32],

@@ -104,11 +104,11 @@ vt_status vt_tree_create(const vt_tree_desc* desc, vt_tree** out) {
 }
 
 vt_status vt_tree_destroy(vt_tree* tree) {
-  return guarded([&] { vt_tree_release(tree); });
+  return guarded_on(tree->t.device, [&] { vt_tree_release(tree); });
 }
 
 vt_status vt_tree_set_stream(vt_tree* tree, void* stream) {
-  return guarded([&] {
+  return guarded_on(tree->t.device, [&] {
     Tree& t = tree->t;
     VT_CUDA(cudaStreamSynchronize(t.stream));
     if (t.own_stream) VT_CUDA(cudaStreamDestroy(t.stream));
@@ -119,7 +119,7 @@ vt_status vt_tree_set_stream(vt_tree* tree, void* stream) {
 
 vt_status vt_tree_insert(vt_tree* tree, int32_t channel, const int32_t origin[3],
                          const int32_t dims[3], const void* samples, int32_t mem_kind) {
-  return guarded([&] {
+  return guarded_on(tree->t.device, [&] {
     VT_REQUIRE(channel >= 0, VT_EINVAL, "channel " + std::to_string(channel) + " out of range");
     tree->t.insert(channel, origin, dims, samples, mem_kind);
   });
@@ -131,7 +131,7 @@ vt_status vt_tree_insert_ev(vt_tree* tree, int32_t channel, const int32_t origin
                             const int32_t dims[3], const void* samples, int32_t mem_kind,
                             void* caller_stream, int32_t* kinds, int64_t* indices, int64_t cap,
                             int64_t* n_events) {
-  return guarded([&] {
+  return guarded_on(tree->t.device, [&] {
     Tree& t = tree->t;
     VT_REQUIRE(channel >= -1, VT_EINVAL, "channel " + std::to_string(channel) + " out of range");
     // a device block is ordered against the caller's stream; a null handle
@@ -143,6 +143,7 @@ vt_status vt_tree_insert_ev(vt_tree* tree, int32_t channel, const int32_t origin
       VT_CUDA(cudaEventRecord(t.ev_wait, cs));
       VT_CUDA(cudaStreamWaitEvent(t.stream, t.ev_wait, 0));
     }
+    const int64_t before = t.event_total();
     t.insert(channel, origin, dims, samples, mem_kind);
     if (order) {
       // the caller's allocator may recycle the block only after our reads
@@ -150,21 +151,16 @@ vt_status vt_tree_insert_ev(vt_tree* tree, int32_t channel, const int32_t origin
       VT_CUDA(cudaEventRecord(t.ev_signal, t.stream));
       VT_CUDA(cudaStreamWaitEvent(cs, t.ev_signal, 0));
     }
-    t.flush_replays();
-    auto& ev = t.events;
-    *n_events = (int64_t)ev.size();
-    if ((int64_t)ev.size() > cap) return;  // too many: the caller takes them all at once
-    for (size_t i = 0; i < ev.size(); ++i) {
-      kinds[i] = Tree::ev_kind(ev[i]);
-      indices[i] = Tree::ev_index(ev[i]);
-    }
-    ev.clear();
+    // this insertion's events, copied; they stay queued for drain_events
+    *n_events = t.event_total() - before;
+    if (*n_events > cap) return;  // too many: the caller copies them with vt_tree_copy_events
+    t.copy_events(before, *n_events, kinds, indices);
   });
 }
 
 vt_status vt_tree_insert_many(vt_tree* tree, int64_t n, const vt_block* blocks, int32_t mem_kind,
                               void* caller_stream) {
-  return guarded([&] {
+  return guarded_on(tree->t.device, [&] {
     Tree& t = tree->t;
     VT_REQUIRE(n >= 0 && (n == 0 || blocks), VT_EINVAL, "null block list");
     VT_REQUIRE(mem_kind == VT_MEM_HOST || mem_kind == VT_MEM_DEVICE, VT_EINVAL, "bad memory kind");
@@ -195,30 +191,28 @@ vt_status vt_tree_insert_many(vt_tree* tree, int64_t n, const vt_block* blocks, 
 
 vt_status vt_tree_insert_channels(vt_tree* tree, const int32_t origin[3], const int32_t dims[3],
                                   const void* samples, int32_t mem_kind) {
-  return guarded([&] { tree->t.insert(-1, origin, dims, samples, mem_kind); });
+  return guarded_on(tree->t.device, [&] { tree->t.insert(-1, origin, dims, samples, mem_kind); });
 }
 
 vt_status vt_tree_take_events(vt_tree* tree, int32_t* kinds, int64_t* indices, int64_t cap,
                               int64_t* n, int32_t* more) {
-  return guarded([&] {
-    tree->t.flush_replays();
-    auto& ev = tree->t.events;
-    int64_t m = std::min<int64_t>(cap, (int64_t)ev.size());
-    for (int64_t i = 0; i < m; ++i) {
-      kinds[i] = Tree::ev_kind(ev[i]);
-      indices[i] = Tree::ev_index(ev[i]);
-    }
-    if (m == (int64_t)ev.size())
-      ev.clear();
-    else
-      ev.erase(ev.begin(), ev.begin() + m);
-    *n = m;
-    *more = ev.empty() ? 0 : 1;
+  return guarded_on(tree->t.device, [&] {
+    *n = tree->t.take_events(kinds, indices, cap);
+    *more = tree->t.event_total() > 0 ? 1 : 0;
+  });
+}
+
+vt_status vt_tree_copy_events(vt_tree* tree, int64_t from, int64_t n, int32_t* kinds,
+                              int64_t* indices) {
+  return guarded_on(tree->t.device, [&] {
+    VT_REQUIRE(from >= 0 && n >= 0 && from + n <= tree->t.event_total(), VT_EINVAL,
+               "event range outside the queue");
+    tree->t.copy_events(from, n, kinds, indices);
   });
 }
 
 vt_status vt_tree_wait_stream(vt_tree* tree, void* stream) {
-  return guarded([&] {
+  return guarded_on(tree->t.device, [&] {
     Tree& t = tree->t;
     if ((cudaStream_t)stream == t.stream) return;
     if (!t.ev_wait) VT_CUDA(cudaEventCreateWithFlags(&t.ev_wait, cudaEventDisableTiming));
@@ -228,7 +222,7 @@ vt_status vt_tree_wait_stream(vt_tree* tree, void* stream) {
 }
 
 vt_status vt_tree_signal_stream(vt_tree* tree, void* stream) {
-  return guarded([&] {
+  return guarded_on(tree->t.device, [&] {
     Tree& t = tree->t;
     if ((cudaStream_t)stream == t.stream) return;
     if (!t.ev_signal) VT_CUDA(cudaEventCreateWithFlags(&t.ev_signal, cudaEventDisableTiming));
@@ -238,11 +232,11 @@ vt_status vt_tree_signal_stream(vt_tree* tree, void* stream) {
 }
 
 vt_status vt_tree_event_count(vt_tree* tree, int64_t* n) {
-  return guarded([&] { *n = tree->t.event_total(); });
+  return guarded_on(tree->t.device, [&] { *n = tree->t.event_total(); });
 }
 
 vt_status vt_tree_set_dense(vt_tree* tree, int32_t enabled) {
-  return guarded([&] {
+  return guarded_on(tree->t.device, [&] {
     tree->t.flush();
     tree->t.dense_enabled = enabled != 0;
   });
@@ -250,7 +244,7 @@ vt_status vt_tree_set_dense(vt_tree* tree, int32_t enabled) {
 
 vt_status vt_tree_dense_counts(vt_tree* tree, int64_t* leaf_inserts, int64_t* level_nodes,
                                int64_t* fast_borders) {
-  return guarded([&] {
+  return guarded_on(tree->t.device, [&] {
     if (leaf_inserts) *leaf_inserts = tree->t.dense_leaf_inserts;
     if (level_nodes) *level_nodes = tree->t.dense_level_nodes;
     if (fast_borders) *fast_borders = tree->t.fast_borders;
@@ -259,7 +253,7 @@ vt_status vt_tree_dense_counts(vt_tree* tree, int64_t* leaf_inserts, int64_t* le
 
 vt_status vt_tree_stream_counts(vt_tree* tree, int64_t* layer_groups, int64_t* zero_copy_layers,
                                 int64_t* deferred_layers) {
-  return guarded([&] {
+  return guarded_on(tree->t.device, [&] {
     if (layer_groups) *layer_groups = tree->t.layer_groups;
     if (zero_copy_layers) *zero_copy_layers = tree->t.zero_copy_layers;
     if (deferred_layers) *deferred_layers = tree->t.deferred_layers;
@@ -267,23 +261,23 @@ vt_status vt_tree_stream_counts(vt_tree* tree, int64_t* layer_groups, int64_t* z
 }
 
 vt_status vt_tree_publish_halos(vt_tree* tree) {
-  return guarded([&] { tree->t.publish_halos(); });
+  return guarded_on(tree->t.device, [&] { tree->t.publish_halos(); });
 }
 
 vt_status vt_tree_finalize(vt_tree* tree) {
-  return guarded([&] { tree->t.finished = true; });
+  return guarded_on(tree->t.device, [&] { tree->t.finished = true; });
 }
 
 vt_status vt_tree_fill_borders(vt_tree* tree) {
-  return guarded([&] { tree->t.fill_borders(); });
+  return guarded_on(tree->t.device, [&] { tree->t.fill_borders(); });
 }
 
 vt_status vt_tree_sync(vt_tree* tree) {
-  return guarded([&] { tree->t.sync(); });
+  return guarded_on(tree->t.device, [&] { tree->t.sync(); });
 }
 
 vt_status vt_tree_info_get(vt_tree* tree, vt_tree_info* o) {
-  return guarded([&] {
+  return guarded_on(tree->t.device, [&] {
     const Tree& t = tree->t;
     o->node_count = t.node_count;
     o->brick_count = t.brick_count;
@@ -299,7 +293,7 @@ vt_status vt_tree_info_get(vt_tree* tree, vt_tree_info* o) {
 }
 
 vt_status vt_tree_node(vt_tree* tree, int64_t index, vt_node* out, int32_t* exists) {
-  return guarded([&] {
+  return guarded_on(tree->t.device, [&] {
     Tree& t = tree->t;
     *exists = 0;
     if (index < 0 || index >= t.g.capacity || !(t.flags[index] & NF_EXISTS)) return;
@@ -317,7 +311,7 @@ vt_status vt_tree_node(vt_tree* tree, int64_t index, vt_node* out, int32_t* exis
 
 vt_status vt_tree_list_nodes(vt_tree* tree, int64_t* out, int32_t* fl, int64_t cap,
                              int64_t* n) {
-  return guarded([&] {
+  return guarded_on(tree->t.device, [&] {
     const Tree& t = tree->t;
     int64_t m = 0;
     for (int64_t i = 0; i < t.g.capacity; ++i)
@@ -333,11 +327,11 @@ vt_status vt_tree_list_nodes(vt_tree* tree, int64_t* out, int32_t* fl, int64_t c
 }
 
 vt_status vt_tree_find_node(vt_tree* tree, const double point[3], int32_t target, int64_t* index) {
-  return guarded([&] { *index = tree->t.find_node(point, target); });
+  return guarded_on(tree->t.device, [&] { *index = tree->t.find_node(point, target); });
 }
 
 vt_status vt_tree_read_brick(vt_tree* tree, int64_t index, void* out) {
-  return guarded([&] {
+  return guarded_on(tree->t.device, [&] {
     Tree& t = tree->t;
     VT_REQUIRE(index >= 0 && index < t.g.capacity && (t.flags[index] & NF_BRICK), VT_EINVAL,
                "node has no brick");
@@ -352,7 +346,7 @@ vt_status vt_tree_read_brick(vt_tree* tree, int64_t index, void* out) {
 
 vt_status vt_tree_export(vt_tree* tree, int64_t n, const int64_t* indices, int32_t* stats,
                          void* bricks) {
-  return guarded([&] {
+  return guarded_on(tree->t.device, [&] {
     Tree& t = tree->t;
     t.flush();
     t.publish_halos();
@@ -390,7 +384,7 @@ vt_status vt_tree_export(vt_tree* tree, int64_t n, const int64_t* indices, int32
 }
 
 vt_status vt_tree_checksum(vt_tree* tree, uint64_t* out) {
-  return guarded([&] {
+  return guarded_on(tree->t.device, [&] {
     Tree& t = tree->t;
     t.flush();
     t.publish_halos();
@@ -437,7 +431,7 @@ vt_status vt_tree_checksum(vt_tree* tree, uint64_t* out) {
 
 vt_status vt_tree_export_nodes(vt_tree* tree, int64_t n, const int64_t* indices, int32_t* nflags,
                                int32_t* stats, void* bricks, int32_t bricks_mem_kind) {
-  return guarded([&] {
+  return guarded_on(tree->t.device, [&] {
     Tree& t = tree->t;
     t.flush();
     t.publish_halos();
@@ -490,7 +484,7 @@ vt_status vt_tree_export_nodes(vt_tree* tree, int64_t n, const int64_t* indices,
 vt_status vt_tree_merge(vt_tree* tree, int64_t n, const int64_t* indices, const int32_t* nflags,
                         const int32_t* stats, const void* bricks, int32_t bricks_mem_kind,
                         int64_t inserted_voxels) {
-  return guarded([&] {
+  return guarded_on(tree->t.device, [&] {
     tree->t.merge(n, indices, nflags, stats, bricks, bricks_mem_kind, inserted_voxels);
   });
 }
@@ -498,7 +492,7 @@ vt_status vt_tree_merge(vt_tree* tree, int64_t n, const int64_t* indices, const 
 vt_status vt_tree_import(vt_tree* tree, int64_t n, const int64_t* indices, const int32_t* nflags,
                          const int32_t* stats, const void* bricks, int32_t finished,
                          int32_t borders_filled, int64_t pruned_bricks) {
-  return guarded([&] {
+  return guarded_on(tree->t.device, [&] {
     ++tree->t.data_version;
     tree->t.touch_all();
     Tree& t = tree->t;
@@ -608,7 +602,7 @@ vt_status vt_synth(void* out, int32_t kind, const int32_t dims[3], int32_t C, in
 }
 
 vt_status vt_last_kernel_ms(vt_tree* tree, double* render_ms, double* build_ms) {
-  return guarded([&] {
+  return guarded_on(tree->t.device, [&] {
     if (render_ms) *render_ms = tree->t.last_render_ms;
     if (build_ms) *build_ms = tree->t.last_build_ms;
   });

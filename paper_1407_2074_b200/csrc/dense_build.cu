@@ -763,6 +763,8 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
 // source layout differs.  Reference: _write_leaf + _ensure_brick +
 // _recompute_stats (octree.py:225-263, 420-442), halfsample_block
 // (octree.py:58-92), _update_parent_octant (octree.py:308-319).
+constexpr int kPStages = 3;  // planar ring: building, previous (fused octant), one in flight
+constexpr int kPAhead = 2;
 __host__ __device__ inline int tma_box_row_planar(int mx) { return (mx + 2 + 7 + 7) / 8 * 8; }
 __host__ __device__ inline uint32_t tma_in_bytes_planar(int mx, int my, int C) {
   return ((uint32_t)C * kTmaP * (my + 2) * tma_box_row_planar(mx) * 2 + 127) / 128 * 128;
@@ -787,7 +789,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma_planar(
   constexpr int WPP = kTmaWarps / P;  // warps per plane
   constexpr int NT = WPP * 32;        // threads per plane
   extern __shared__ __align__(128) unsigned char s_in[];
-  __shared__ uint64_t s_bar[kTmaStages];
+  __shared__ uint64_t s_bar[kPStages];
   __shared__ int s_mn[2][kTmaWarps][C], s_mx[2][kTmaWarps][C];
   __shared__ unsigned long long s_sm[2][kTmaWarps][C];
   const DenseJob j = jobs[blockIdx.x];
@@ -809,21 +811,23 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma_planar(
   const uint16_t bg = (uint16_t)g.bg;
   const int x0 = gx * Mx - 1, y0 = gy * My - 1;  // block voxel of stored (0, 0)
   const int xa = x0 - ((x0 % 8 + 8) % 8);        // 16-byte aligned tile start (samples)
-  const int xoff = x0 - xa;                      // leading samples of a staged row
+  const int xoff = x0 - xa;                      // leading samples of a staged row (odd)
+  // every stored voxel of a block plane inside the volume (prefilled shells)
+  const bool xyfull = prefill && x0 >= 0 && x0 + Sx <= X && y0 >= 0 && y0 + Sy <= Y;
 
   if (tid == 0) {
-    for (int b = 0; b < kTmaStages; ++b) mbar_init(&s_bar[b], 1);
+    for (int b = 0; b < kPStages; ++b) mbar_init(&s_bar[b], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
   auto issue = [&](int s) {  // one thread: one 4-D tensor tile per stage
-    const int b = s % kTmaStages;
+    const int b = s % kPStages;
     mbar_expect_tx(&s_bar[b], (uint32_t)C * rows * bx * 2);
     tma_load_4d(s_in + (size_t)b * in_bytes, &map, xa, y0, gz * Mz - oz + P * s - 1, 0, &s_bar[b]);
   };
   if (tid == 0)
-    for (int s = 0; s < min(kTmaAhead, nstages); ++s) issue(s);
+    for (int s = 0; s < min(kPAhead, nstages); ++s) issue(s);
 
   const int pslot = j.pad;
   const int hx = Mx / 2, hy = My / 2;
@@ -849,7 +853,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma_planar(
   const int cstr = rows * bx;               // staged channel stride (samples)
 
   for (int s = 0; s < nstages; ++s) {
-    const int b = (unsigned)s % kTmaStages;
+    const int b = (unsigned)s % kPStages;
     const int zs = P * s + pw;
     const int zi = zs - 1;
     const int rz = gz * Mz + zi;
@@ -859,8 +863,50 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma_planar(
     const uint16_t* stage = reinterpret_cast<const uint16_t*>(s_in + (size_t)b * in_bytes);
     const uint16_t* iplane = stage + (size_t)pw * Sy * bx + xoff;  // channel 0, stored (0, 0)
     uint32_t* oplane = reinterpret_cast<uint32_t*>(brick + (size_t)zs * plane_elems);
-    mbar_wait(&s_bar[b], (uint32_t)(s / kTmaStages) & 1u);
-    if (zs < Sz) {
+    mbar_wait(&s_bar[b], (uint32_t)(s / kPStages) & 1u);
+    if (zs < Sz && mode != 0 && xyfull) {
+      // the common case: every stored voxel of the plane comes from the
+      // block.  Thread q builds voxel pair (2q, 2q + 1) of the plane (Sx is
+      // even): per channel two aligned 32-bit shared loads and a byte
+      // permute give both voxels (the staged row starts at an odd xoff, so
+      // stored x = 2k - 1 sits at an even sample), then the pair's C words
+      // of the channel-fastest stored row are assembled and stored.
+      const bool stat_plane = mode == 1 && !parent;
+      const uint32_t* s32 = reinterpret_cast<const uint32_t*>(stage) + (pw * Sy * bx + xoff - 1) / 2;
+      const int pt = (warp % WPP) * 32 + lane;
+      const int SP = Sx / 2;  // voxel pairs per stored row
+      for (int q = pt; q < Sy * SP; q += NT) {
+        const int ys = q / SP, xs = 2 * (q - ys * SP);
+        const uint32_t* w = s32 + (ys * bx + xs) / 2;
+        uint32_t pv[C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) pv[c] = __byte_perm(w[c * cstr / 2], w[c * cstr / 2 + 1], 0x5432);
+        if (stat_plane) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int x = xs + h;
+            if (x >= 1 && x <= cx && ys >= 1 && ys <= cy) {
+#pragma unroll
+              for (int c = 0; c < C; ++c) {
+                const int v = (int)((pv[c] >> (16 * h)) & 0xFFFFu);
+                lmn[c] = min(lmn[c], v);
+                lmx[c] = max(lmx[c], v);
+                lsm[c] += (unsigned)v;
+              }
+            }
+          }
+        }
+        uint32_t* o = oplane + (size_t)q * C;
+#pragma unroll
+        for (int j2 = 0; j2 < C; ++j2) {
+          // samples 2 j2 and 2 j2 + 1 of the pair: voxel k / C, channel k % C
+          const int k0 = 2 * j2, k1 = 2 * j2 + 1;
+          const uint32_t a0 = k0 / C ? (pv[k0 % C] >> 16) : (pv[k0 % C] & 0xFFFFu);
+          const uint32_t a1 = k1 / C ? (pv[k1 % C] >> 16) : (pv[k1 % C] & 0xFFFFu);
+          o[j2] = a0 | (a1 << 16);
+        }
+      }
+    } else if (zs < Sz) {
       const bool stat_plane = mode == 1 && !parent;
       // every lane runs the same trip count (shuffles below)
       for (int v0 = (warp % WPP) * 32; v0 < nvox; v0 += NT) {
@@ -913,7 +959,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma_planar(
     if (parent && s >= 1 && 2 * (s - 1) < cz) {
       const int k = s - 1;
       const uint16_t* pa = reinterpret_cast<const uint16_t*>(
-                               s_in + (size_t)((unsigned)(s - 1) % kTmaStages) * in_bytes) +
+                               s_in + (size_t)((unsigned)(s - 1) % kPStages) * in_bytes) +
                            (size_t)Sy * bx + xoff;  // previous stage, plane 1
       const uint16_t* pb = stage + xoff;             // this stage, plane 0
       const bool zfull = 2 * k + 1 < cz;
@@ -978,7 +1024,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma_planar(
       }
     }
     __syncthreads();  // input slots consumed
-    if (tid == 0 && s + kTmaAhead < nstages) issue(s + kTmaAhead);
+    if (tid == 0 && s + kPAhead < nstages) issue(s + kPAhead);
   }
 
 #pragma unroll
@@ -1435,7 +1481,7 @@ void launch_clear_shells(const Tree& t, const int32_t* d_slots, int n) {
 }
 
 static size_t tma_smem_planar(const Geo& g) {
-  return (size_t)kTmaStages * tma_in_bytes_planar(g.brick[0], g.brick[1], g.C);
+  return (size_t)kPStages * tma_in_bytes_planar(g.brick[0], g.brick[1], g.C);
 }
 
 bool planar_leaf_ok(const Tree& t, const void* base, int64_t zstride, int64_t cstride) {
@@ -1444,7 +1490,7 @@ bool planar_leaf_ok(const Tree& t, const void* base, int64_t zstride, int64_t cs
   return g.sb == 2 && ((uintptr_t)base & 15) == 0 && ((int64_t)g.dims[0] * 2) % 16 == 0 &&
          zstride > 0 && zstride % 16 == 0 && (g.C == 1 || (cstride > 0 && cstride % 16 == 0)) &&
          tma_box_row_planar(g.brick[0]) <= 256 && g.brick[1] + 2 <= 256 &&
-         ((g.brick[0] + 2) * (g.brick[1] + 2)) % 2 == 0 && tma_smem_planar(g) <= 200 * 1024;
+         g.brick[0] % 2 == 0 && tma_smem_planar(g) <= 200 * 1024;
 }
 
 // 4-D tensor map (x, y, z, c) of a planar u16 block of dz planes per channel

@@ -1459,7 +1459,7 @@ struct vt_rays {
 extern "C" {
 
 vt_status vt_mirror_create(vt_tree* tree, int64_t slot_count, vt_mirror** out) {
-  return guarded([&] {
+  return guarded_on(tree->t.device, [&] {
     Tree& t = tree->t;
     t.flush();
     if (slot_count >= 0) {
@@ -1517,11 +1517,11 @@ static void mirror_release(vt_mirror* m) {
 }
 
 vt_status vt_mirror_destroy(vt_mirror* m) {
-  return guarded([&] { mirror_release(m); });
+  return guarded_on(m->tree->t.device, [&] { mirror_release(m); });
 }
 
 vt_status vt_mirror_bmax_stats(vt_mirror* m, int64_t* incremental, int64_t* last_slots) {
-  return guarded([&] {
+  return guarded_on(m->tree->t.device, [&] {
     if (incremental) *incremental = m->bmax_incremental;
     if (last_slots) *last_slots = m->bmax_last_slots;
   });
@@ -1529,7 +1529,7 @@ vt_status vt_mirror_bmax_stats(vt_mirror* m, int64_t* incremental, int64_t* last
 
 vt_status vt_mirror_buffers(vt_mirror* m, void** nbp, void** fbp, void** bbp, int64_t* cap,
                             int64_t* slots) {
-  return guarded([&] {
+  return guarded_on(m->tree->t.device, [&] {
     Tree& t = m->tree->t;
     if (nbp) *nbp = m->d_nb;
     if (fbp) *fbp = m->d_fb;
@@ -1541,7 +1541,7 @@ vt_status vt_mirror_buffers(vt_mirror* m, void** nbp, void** fbp, void** bbp, in
 
 vt_status vt_mirror_set_resident(vt_mirror* m, int64_t n, const int64_t* nodes,
                                  const int32_t* slots, int32_t copy) {
-  return guarded([&] {
+  return guarded_on(m->tree->t.device, [&] {
     Tree& t = m->tree->t;
     VT_REQUIRE(!m->zero_copy, VT_ESTATE, "zero-copy mirror: every brick is resident");
     if (n <= 0) return;
@@ -1578,7 +1578,7 @@ vt_status vt_mirror_set_resident(vt_mirror* m, int64_t n, const int64_t* nodes,
 }
 
 vt_status vt_mirror_repack(vt_mirror* m) {
-  return guarded([&] {
+  return guarded_on(m->tree->t.device, [&] {
     Tree& t = m->tree->t;
     t.flush();
     const int64_t cap = t.g.capacity;
@@ -1592,7 +1592,7 @@ vt_status vt_mirror_repack(vt_mirror* m) {
 }
 
 vt_status vt_mirror_read_flags(vt_mirror* m, uint8_t* out, int32_t clear) {
-  return guarded([&] {
+  return guarded_on(m->tree->t.device, [&] {
     Tree& t = m->tree->t;
     const int64_t cap = t.g.capacity;
     VT_CUDA(cudaMemcpyAsync(out, m->d_fb, cap, cudaMemcpyDeviceToHost, t.stream));
@@ -1704,18 +1704,18 @@ static void render_rect(vt_mirror* m, const vt_scene* scene, const int32_t* rect
 
 vt_status vt_render_fullframe(vt_mirror* m, const vt_scene* scene, void* out, int32_t out_kind,
                               int32_t out_on_device, vt_counters* cnt) {
-  return guarded([&] { render_rect(m, scene, nullptr, out, out_kind, out_on_device, cnt); });
+  return guarded_on(m->tree->t.device, [&] { render_rect(m, scene, nullptr, out, out_kind, out_on_device, cnt); });
 }
 
 vt_status vt_render_tile(vt_mirror* m, const vt_scene* scene, const int32_t rect[4], void* out,
                          int32_t out_kind, int32_t out_on_device, vt_counters* cnt) {
-  return guarded([&] { render_rect(m, scene, rect, out, out_kind, out_on_device, cnt); });
+  return guarded_on(m->tree->t.device, [&] { render_rect(m, scene, rect, out, out_kind, out_on_device, cnt); });
 }
 
 vt_status vt_render_strips(vt_mirror* m, const vt_scene* scene, int32_t strip_rows,
                            int32_t n_parts, int32_t part, void* out, int32_t out_kind,
                            int32_t out_on_device, vt_counters* cnt) {
-  return guarded([&] {
+  return guarded_on(m->tree->t.device, [&] {
     VT_REQUIRE(n_parts >= 1, VT_EINVAL, "n_parts must be >= 1");
     render_rect(m, scene, nullptr, out, out_kind, out_on_device, cnt, strip_rows, n_parts, part);
   });
@@ -1727,7 +1727,7 @@ int32_t vt_strip_part_rows(int32_t height, int32_t strip_rows, int32_t n_parts) 
 }
 
 vt_status vt_rays_create(vt_mirror* m, const vt_scene* scene, const int32_t* tile, vt_rays** out) {
-  return guarded([&] {
+  return guarded_on(m->tree->t.device, [&] {
     std::lock_guard<std::mutex> lk(g_render_mu);
     Tree& t = m->tree->t;
     auto* r = new vt_rays();
@@ -1754,7 +1754,7 @@ vt_status vt_rays_create(vt_mirror* m, const vt_scene* scene, const int32_t* til
 }
 
 vt_status vt_rays_destroy(vt_rays* r) {
-  return guarded([&] {
+  return guarded_on(r->m->tree->t.device, [&] {
     if (!r) return;
     cudaStreamSynchronize(r->m->tree->t.stream);
     cudaFree(r->S.t0);
@@ -1769,7 +1769,7 @@ vt_status vt_rays_destroy(vt_rays* r) {
 }
 
 vt_status vt_rays_march(vt_rays* r, int32_t strategy, vt_counters* cnt, int64_t* suspended) {
-  return guarded([&] {
+  return guarded_on(r->m->tree->t.device, [&] {
     std::lock_guard<std::mutex> lk(g_render_mu);
     vt_mirror* m = r->m;
     Tree& t = m->tree->t;
@@ -1805,7 +1805,7 @@ vt_status vt_rays_march(vt_rays* r, int32_t strategy, vt_counters* cnt, int64_t*
 }
 
 vt_status vt_rays_image(vt_rays* r, double* out_host, vt_counters* cnt) {
-  return guarded([&] {
+  return guarded_on(r->m->tree->t.device, [&] {
     std::lock_guard<std::mutex> lk(g_render_mu);
     Tree& t = r->m->tree->t;
     double* dout = nullptr;
@@ -1831,7 +1831,7 @@ vt_status vt_rays_image(vt_rays* r, double* out_host, vt_counters* cnt) {
 }
 
 vt_status vt_rays_state(vt_rays* r, int64_t* k, int64_t* n_steps, uint8_t* suspended) {
-  return guarded([&] {
+  return guarded_on(r->m->tree->t.device, [&] {
     Tree& t = r->m->tree->t;
     std::vector<uint8_t> fl(r->n);
     if (k) VT_CUDA(cudaMemcpyAsync(k, r->S.k, r->n * 8, cudaMemcpyDeviceToHost, t.stream));

@@ -577,7 +577,6 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
     ProfScope qd(prof, 18);
     if (try_defer(channel, origin, dims, dsrc, src_stride, src_off)) return;
   }
-  flush_replays();  // this insertion's events follow every earlier one
   const bool starting = defer_start;  // this insertion opens a deferred layer
   defer_start = false;
   ++data_version;
@@ -616,7 +615,7 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
   // then the fresh level-1 parents cursor + n_leaves + (BFS order) — so the
   // leaf kernel (with fused level-1 octants) is launched BEFORE the host walk
   // and the walk overlaps it; the walk re-derives every slot and checks.
-  const bool early = dense && free_slots.empty();
+  const bool early = dense && free_slots.empty() && !hold_dense;
   int launch_result = 0;
   if (early) {
     ProfScope q(prof, 7);
@@ -991,7 +990,19 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
   }
   side_join.reset();
   int32_t* dlp = nullptr;
-  if (dense) {
+  if (dense && hold_dense) {
+    // the even layer of a pair: its leaves wait for the odd layer's walk
+    if (!held.active) {
+      held.active = true;
+      held.djobs.clear();
+      held.z0 = origin[2];
+      held.nz = 0;
+      held.gz0 = g0[2];
+    }
+    held.djobs.insert(held.djobs.end(), djobs.begin(), djobs.end());
+    held.nz += dims[2];
+    held.gz1 = g1[2];
+  } else if (dense) {
     ProfScope q(prof, 7);
     int lr = launch_result;
     if (!early) {
@@ -1010,40 +1021,8 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
                        (int)djobs.size(), gn, g0[2]);
       release(*this, dj);
     }
-    const bool prefilled = lr & kLeafPrefilled;
-    if (!(lr & kLeafTma)) {
-      for (int64_t p : fused_nodes) fused1[p] = 0;  // the fallback kernels do not fuse
-    } else {
-      for (const DenseJob& jd : djobs) pinv[jd.node] = 1;
-      for (int64_t p : fused_nodes) pinv[p] = 1;
-    }
-    // host bookkeeping overlaps the device work: pending entries of leaves
-    // whose statistics the kernel writes outright
-    ProfScope qd(prof, 16);
-    pend_nodes[0].reserve(pend_nodes[0].size() + djobs.size());
-    // touched[0] holds the same leaves, already in BFS order: propagate
-    // then finds the list sorted
-    for (int64_t n : touched[0]) pend_dense(n);
-    for (const DenseJob& jd : djobs) complete[jd.node] = 1;
-    ++dense_leaf_inserts;
-    if (prefilled) {
-      // z-shell planes whose block plane lies outside this insertion are owed
-      halo_prefill = true;
-      const int z0 = origin[2], z1 = origin[2] + dims[2];
-      for (int gz = g0[2]; gz <= g1[2]; ++gz) {
-        const int lo = gz * M[2] - 1, hi = (gz + 1) * M[2];
-        const bool olo = lo >= 0 && lo < z0, ohi = hi < g.dims[2] && hi >= z1;
-        if (!olo && !ohi) continue;
-        for (int gy = g0[1]; gy <= g1[1]; ++gy)
-          for (int gx = g0[0]; gx <= g1[0]; ++gx) {
-            const int64_t idx = leaf_index(gx, gy, gz);
-            if (olo) owed_lo.push_back(idx);
-            if (ohi) owed_hi.push_back(idx);
-          }
-      }
-    } else {
-      prefill_valid = false;
-    }
+    dense_after_launch(lr, djobs, fused_nodes, origin[2], origin[2] + dims[2], g0[2], g1[2],
+                       &touched[0]);
   } else if (starting) {
     // open the deferred layer: slots and events are final, data waits
     ProfScope q(prof, 7);
@@ -1121,14 +1100,111 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
   for (int64_t i : upd)
     if (flags[i] & NF_EXISTS) events.push_back(ev_pack(VT_EV_UPDATED, i));
   if (ev_reps > 1) {
-    // the later blocks' lists are replayed when something reads the events
-    rep_list.assign(events.begin() + ev0, events.end());
-    rep_count = ev_reps - 1;
+    // the later blocks' lists: the same UPDATED list, expanded when taken
+    push_replay(std::make_shared<std::vector<uint64_t>>(events.begin() + ev0, events.end()),
+                ev_reps - 1);
   }
   if (starting) {
     dl.upd = upd;  // every later block of the layer touches the same nodes
+    dl_upd_ev.reset();
     if (dl.remaining == 0) finish_layer();
   }
+}
+
+void Tree::dense_after_launch(int lr, const std::vector<DenseJob>& djobs,
+                              const std::vector<int64_t>& fused_nodes, int z0, int z1, int gz0,
+                              int gz1, const std::vector<int64_t>* sorted_leaves) {
+  const int* M = g.brick;
+  const bool prefilled = lr & kLeafPrefilled;
+  if (!(lr & kLeafTma)) {
+    for (int64_t p : fused_nodes) fused1[p] = 0;  // the fallback kernels do not fuse
+  } else {
+    for (const DenseJob& jd : djobs) pinv[jd.node] = 1;
+    for (int64_t p : fused_nodes) pinv[p] = 1;
+  }
+  // host bookkeeping overlaps the device work: pending entries of leaves
+  // whose statistics the kernel writes outright (djobs are in (gz, gy, gx)
+  // order; propagate sorts its lists)
+  ProfScope qd(prof, 16);
+  pend_nodes[0].reserve(pend_nodes[0].size() + djobs.size());
+  if (sorted_leaves)
+    for (int64_t n : *sorted_leaves) pend_dense(n);  // BFS order: propagate needs no sort
+  else
+    for (const DenseJob& jd : djobs) pend_dense(jd.node);
+  for (const DenseJob& jd : djobs) complete[jd.node] = 1;
+  ++dense_leaf_inserts;
+  if (prefilled) {
+    // z-shell planes whose block plane lies outside this insertion are owed
+    halo_prefill = true;
+    const int gx1 = (g.dims[0] - 1) / M[0], gy1 = (g.dims[1] - 1) / M[1];
+    for (int gz = gz0; gz <= gz1; ++gz) {
+      const int lo = gz * M[2] - 1, hi = (gz + 1) * M[2];
+      const bool olo = lo >= 0 && lo < z0, ohi = hi < g.dims[2] && hi >= z1;
+      if (!olo && !ohi) continue;
+      for (int gy = 0; gy <= gy1; ++gy)
+        for (int gx = 0; gx <= gx1; ++gx) {
+          const int64_t idx = leaf_index(gx, gy, gz);
+          if (!(flags[idx] & NF_BRICK) || !complete[idx]) continue;
+          if (olo) owed_lo.push_back({idx, leaf_index(gx, gy, gz - 1)});
+          if (ohi) owed_hi.push_back({idx, leaf_index(gx, gy, gz + 1)});
+        }
+    }
+  } else {
+    prefill_valid = false;
+  }
+}
+
+// the held even layer and the odd layer after it: one leaf launch over both,
+// level-1 parents whose eight children are all in the pair fused
+void Tree::launch_held() {
+  if (!held.active) return;
+  held.active = false;
+  const int* M = g.brick;
+  const int gnx = (g.dims[0] - 1) / M[0] + 1, gny = (g.dims[1] - 1) / M[1] + 1;
+  const int nl = held.gz1 - held.gz0 + 1;
+  std::vector<DenseJob>& dj = held.djobs;
+  VT_REQUIRE((int64_t)dj.size() == (int64_t)gnx * gny * nl, VT_ESTATE,
+             "held dense layers: leaf count mismatch");
+  std::vector<int64_t> fused_nodes;
+  std::vector<int32_t> fused_slots;
+  if (nl == 2 && (held.gz0 & 1) == 0 && g.depth >= 1 && g.split[0] && g.split[1] && g.split[2]) {
+    for (int gy = 0; gy + 1 < gny; gy += 2)
+      for (int gx = 0; gx + 1 < gnx; gx += 2) {
+        const int64_t c0 = dj[(size_t)gy * gnx + gx].node;
+        const int64_t p = (c0 - 1) >> 3;
+        if (!(flags[p] & NF_BRICK)) continue;
+        bool ok = true;
+        int64_t pos[8];
+        for (int k = 0; k < 8 && ok; ++k) {
+          const int x = gx + (k & 1), y = gy + ((k >> 1) & 1), z = (k >> 2) & 1;
+          pos[k] = ((int64_t)z * gny + y) * gnx + x;
+          const int64_t c = dj[pos[k]].node;
+          ok = c == 8 * p + 1 + k && (flags[c] & NF_INVOL) && (flags[c] & NF_BRICK);
+        }
+        if (!ok) continue;
+        for (int k = 0; k < 8; ++k) dj[pos[k]].pad = slot[p];
+        fused_nodes.push_back(p);
+        fused1[p] = 1;
+      }
+  }
+  if (!fused_nodes.empty() && !d_nsum) {
+    VT_CUDA(cudaMalloc(&d_nsum, g.capacity * g.C * sizeof(unsigned long long)));
+    VT_CUDA(cudaMalloc(&d_nmin, g.capacity * g.C * sizeof(int32_t)));
+    VT_CUDA(cudaMalloc(&d_nmax, g.capacity * g.C * sizeof(int32_t)));
+  }
+  int64_t* dfn = upload(*this, fused_nodes);
+  launch_init_fused(*this, dfn, (int)fused_nodes.size());
+  release(*this, dfn);
+  DenseJob* d = upload(*this, dj);
+  const bool want = prefill_enabled && !borders;
+  const int gn[3] = {gnx, gny, nl};
+  const int64_t nvox = (int64_t)g.dims[0] * g.dims[1] * held.nz;
+  const int lr = leaf_launch(planar.base, nvox * g.C, held.z0, held.nz, want ? 1 : 0, d,
+                             (int)dj.size(), gn, held.gz0);
+  release(*this, d);
+  dense_after_launch(lr, dj, fused_nodes, held.z0, held.z0 + held.nz, held.gz0, held.gz1,
+                     nullptr);
+  dj.clear();
 }
 
 // ---------------------------------------------------------------------------
@@ -1154,12 +1230,12 @@ bool Tree::try_defer(int channel, const int origin[3], const int dims[3], const 
       defer_copy(channel, origin, dims, dsrc);
       // this block's events: the layer's UPDATED list once more (replayed
       // lazily: a 2048^2 slice of 32^3 bricks updates ~5.5k nodes)
-      if (rep_count > 0 && rep_list.size() != dl.upd.size()) flush_replays();
-      if (rep_count == 0) {
-        rep_list.clear();
-        for (int64_t i : dl.upd) rep_list.push_back(ev_pack(VT_EV_UPDATED, i));
+      if (!dl_upd_ev) {
+        dl_upd_ev = std::make_shared<std::vector<uint64_t>>();
+        dl_upd_ev->reserve(dl.upd.size());
+        for (int64_t i : dl.upd) dl_upd_ev->push_back(ev_pack(VT_EV_UPDATED, i));
       }
-      ++rep_count;
+      push_replay(dl_upd_ev, 1);
       inserted += nvox;
       if (dl.remaining == 0) finish_layer();
       return true;
@@ -1231,9 +1307,11 @@ void Tree::close_layer() {
   if (dl.prefilled) {
     // z-shell planes of the neighbouring layers are owed to fill_borders
     const int lo = dl.z0 - 1, hi = dl.z0 + g.brick[2];
-    for (const DenseJob& jd : dl.djobs) {
-      if (lo >= 0) owed_lo.push_back(jd.node);
-      if (hi < g.dims[2]) owed_hi.push_back(jd.node);
+    const int gnx = (g.dims[0] - 1) / g.brick[0] + 1;
+    for (size_t k = 0; k < dl.djobs.size(); ++k) {  // (gy, gx) order
+      const int gx = (int)(k % gnx), gy = (int)(k / gnx);
+      if (lo >= 0) owed_lo.push_back({dl.djobs[k].node, leaf_index(gx, gy, dl.gz - 1)});
+      if (hi < g.dims[2]) owed_hi.push_back({dl.djobs[k].node, leaf_index(gx, gy, dl.gz + 1)});
     }
   }
   ++deferred_layers;
@@ -1320,10 +1398,65 @@ int64_t Tree::layer_group(int64_t i, int64_t n, const vt_block* blocks, int mem_
   return need == 0 ? j - i : 0;
 }
 
-void Tree::insert_many(int64_t n, const vt_block* blocks, int mem_kind) {
-  VT_CUDA(cudaSetDevice(device));
+// where a complete layer group's samples are: in place (the blocks sit at
+// an affine (z, channel) stride) or gathered into the planar layer buffer
+bool Tree::group_source(int64_t i, int64_t len, const vt_block* blocks, int mem_kind, bool gather,
+                        PlanarSrc& src) {
   const int* M = g.brick;
   const int64_t plane = (int64_t)g.dims[0] * g.dims[1] * g.sb;
+  const int layer = blocks[i].origin[2] / M[2];
+  const int z0 = layer * M[2], nz = std::min(M[2], g.dims[2] - z0);
+  if (mem_kind == VT_MEM_DEVICE) {
+    auto at = [&](const vt_block& b, int z) {
+      return (const uint8_t*)b.samples + (int64_t)(z - b.origin[2]) * plane;
+    };
+    const uint8_t *p00 = nullptr, *p10 = nullptr, *p01 = nullptr;
+    for (int64_t k = i; k < i + len; ++k) {
+      const vt_block& b = blocks[k];
+      for (int z = b.origin[2]; z < b.origin[2] + b.dims[2]; ++z) {
+        if (z == z0 && b.channel == 0) p00 = at(b, z);
+        if (z == z0 + 1 && b.channel == 0) p10 = at(b, z);
+        if (z == z0 && b.channel == 1) p01 = at(b, z);
+      }
+    }
+    const int64_t zs = nz > 1 ? (int64_t)(p10 - p00) : plane;
+    const int64_t cs = g.C > 1 ? (int64_t)(p01 - p00) : (int64_t)nz * plane;
+    bool affine = zs > 0 && cs > 0;
+    for (int64_t k = i; k < i + len && affine; ++k) {
+      const vt_block& b = blocks[k];
+      for (int z = b.origin[2]; z < b.origin[2] + b.dims[2] && affine; ++z)
+        affine = at(b, z) == p00 + (int64_t)(z - z0) * zs + (int64_t)b.channel * cs;
+    }
+    if (affine && planar_leaf_ok(*this, p00, zs, cs)) {
+      src = {true, p00, zs, cs};
+      return true;
+    }
+  }
+  if (!gather) return false;
+  if (!d_acc) VT_CUDA(cudaMalloc(&d_acc, (size_t)M[2] * g.dims[1] * g.dims[0] * g.C * g.sb));
+  for (int64_t k = i; k < i + len; ++k) {
+    const vt_block& b = blocks[k];
+    uint8_t* dst = d_acc + ((size_t)b.channel * M[2] + (b.origin[2] - z0)) * plane;
+    VT_CUDA(cudaMemcpyAsync(dst, b.samples, plane * b.dims[2],
+                            mem_kind == VT_MEM_DEVICE ? cudaMemcpyDeviceToDevice
+                                                      : cudaMemcpyHostToDevice,
+                            stream));
+  }
+  src = {true, d_acc, plane, (int64_t)M[2] * plane};
+  return false;
+}
+
+void Tree::insert_many(int64_t n, const vt_block* blocks, int mem_kind) {
+  VT_CUDA(cudaSetDevice(device));
+  if (prof.on)
+    for (auto& e : prof.ev)
+      if (!e) VT_CUDA(cudaEventCreate(&e));
+  const int* M = g.brick;
+  const int nlayers = (g.dims[2] - 1) / M[2] + 1;
+  static const bool pairs_on = [] {
+    const char* e = std::getenv("VT_LAYER_PAIRS");
+    return !(e && e[0] == '0');
+  }();
   int64_t i = 0;
   while (i < n) {
     const int64_t len = layer_group(i, n, blocks, mem_kind);
@@ -1334,68 +1467,67 @@ void Tree::insert_many(int64_t n, const vt_block* blocks, int mem_kind) {
       ++i;
       continue;
     }
-    // one dense insertion for the whole layer: the first block's walk and
-    // events, then the same UPDATED list for each later block
+    // one dense insertion per layer: the first block's walk and events,
+    // then the same UPDATED list for each later block
     const int layer = blocks[i].origin[2] / M[2];
-    const int z0 = layer * M[2], nz = std::min(M[2], g.dims[2] - z0);
-    // source: in place when the blocks sit at an affine (z, channel) stride
-    const uint8_t* base = nullptr;
-    int64_t zs = 0, cs = 0;
-    bool affine = mem_kind == VT_MEM_DEVICE;
-    if (affine) {
-      auto at = [&](const vt_block& b, int z) {
-        return (const uint8_t*)b.samples + (int64_t)(z - b.origin[2]) * plane;
-      };
-      const uint8_t* p00 = nullptr;
-      const uint8_t* p10 = nullptr;
-      const uint8_t* p01 = nullptr;
-      for (int64_t k = i; k < i + len; ++k) {
-        const vt_block& b = blocks[k];
-        for (int z = b.origin[2]; z < b.origin[2] + b.dims[2]; ++z) {
-          if (z == z0 && b.channel == 0) p00 = at(b, z);
-          if (z == z0 + 1 && b.channel == 0) p10 = at(b, z);
-          if (z == z0 && b.channel == 1) p01 = at(b, z);
-        }
+    PlanarSrc a{};
+    const bool in_place = group_source(i, len, blocks, mem_kind, false, a);
+    // an even layer read in place with its odd layer right behind it (also
+    // in place, the same strides, contiguous in z): build the pair at once
+    int64_t len2 = 0;
+    PlanarSrc b{};
+    if (pairs_on && in_place && (layer & 1) == 0 && layer + 1 < nlayers && i + len < n) {
+      // the odd layer's leaves must be brick-less too: layer_group checks
+      len2 = layer_group(i + len, n, blocks, mem_kind);
+      const int nza = M[2];
+      if (len2 > 0 && blocks[i + len].origin[2] / M[2] == layer + 1 &&
+          group_source(i + len, len2, blocks, mem_kind, false, b) && b.zstride == a.zstride &&
+          b.cstride == a.cstride && b.base == a.base + (int64_t)nza * a.zstride &&
+          planar_leaf_ok(*this, a.base, a.zstride, a.cstride)) {
+      } else {
+        len2 = 0;
       }
-      base = p00;
-      zs = nz > 1 ? (int64_t)(p10 - p00) : plane;
-      cs = g.C > 1 ? (int64_t)(p01 - p00) : (int64_t)nz * plane;
-      for (int64_t k = i; k < i + len && affine; ++k) {
-        const vt_block& b = blocks[k];
-        for (int z = b.origin[2]; z < b.origin[2] + b.dims[2] && affine; ++z)
-          affine = at(b, z) == p00 + (int64_t)(z - z0) * zs + (int64_t)b.channel * cs;
-      }
-      affine = affine && zs > 0 && cs > 0 && planar_leaf_ok(*this, base, zs, cs);
     }
-    if (!affine) {
-      // gather the layer into the planar layer buffer
-      if (!d_acc)
-        VT_CUDA(cudaMalloc(&d_acc, (size_t)M[2] * g.dims[1] * g.dims[0] * g.C * g.sb));
-      for (int64_t k = i; k < i + len; ++k) {
-        const vt_block& b = blocks[k];
-        uint8_t* dst = d_acc + ((size_t)b.channel * M[2] + (b.origin[2] - z0)) * plane;
-        VT_CUDA(cudaMemcpyAsync(dst, b.samples, plane * b.dims[2],
-                                mem_kind == VT_MEM_DEVICE ? cudaMemcpyDeviceToDevice
-                                                          : cudaMemcpyHostToDevice,
-                                stream));
-      }
-      base = d_acc;
-      zs = plane;
-      cs = (int64_t)M[2] * plane;
+    if (!in_place) {
+      group_source(i, len, blocks, mem_kind, true, a);
     } else {
       ++zero_copy_layers;
     }
-    planar = {true, base, zs, cs};
+    const int z0 = layer * M[2], nz = std::min(M[2], g.dims[2] - z0);
     const int o[3] = {0, 0, z0}, d[3] = {g.dims[0], g.dims[1], nz};
+    planar = a;
+    if (len2 == 0) {
+      try {
+        insert_staged(-1, o, d, a.base, g.C, 0, g.C, len);
+      } catch (...) {
+        planar = PlanarSrc{};
+        throw;
+      }
+      planar = PlanarSrc{};
+      ++layer_groups;
+      i += len;
+      continue;
+    }
+    // the pair: walk both (their events in order), then one leaf launch
+    const int z1 = z0 + M[2], nz1 = std::min(M[2], g.dims[2] - z1);
+    const int o1[3] = {0, 0, z1}, d1[3] = {g.dims[0], g.dims[1], nz1};
+    hold_dense = true;
     try {
-      insert_staged(-1, o, d, base, g.C, 0, g.C, len);
+      insert_staged(-1, o, d, a.base, g.C, 0, g.C, len);
+      insert_staged(-1, o1, d1, b.base, g.C, 0, g.C, len2);
     } catch (...) {
+      hold_dense = false;
+      launch_held();  // whatever was walked must be built
       planar = PlanarSrc{};
       throw;
     }
+    hold_dense = false;
+    launch_held();
     planar = PlanarSrc{};
-    ++layer_groups;
-    i += len;
+    layer_groups += 2;
+    zero_copy_layers += 1;
+    ++layer_pairs;
+    i += len + len2;
   }
 }
 
@@ -1663,7 +1795,6 @@ void Tree::prune(std::vector<std::vector<int64_t>>& touched, std::vector<char>& 
 // ---------------------------------------------------------------------------
 
 void Tree::fill_borders() {
-  flush_replays();
   ProfScope pf(prof, 3);
   flush();
   ++data_version;
@@ -1687,15 +1818,13 @@ void Tree::fill_borders() {
     ++fast_borders;
     std::vector<int32_t> pj;
     const int mz = g.brick[2];
-    auto add = [&](int64_t leaf, int dz_) {
-      int lo[3];
-      g.box_lo(leaf, lo);
-      const int64_t nb = leaf_index(lo[0] / g.brick[0], lo[1] / g.brick[1], lo[2] / mz + dz_);
-      VT_REQUIRE((flags[nb] & NF_BRICK), VT_ESTATE, "fill_borders: neighbour brick missing");
-      pj.insert(pj.end(), {slot[leaf], dz_ < 0 ? 0 : mz + 1, slot[nb], dz_ < 0 ? mz : 1});
+    pj.reserve(4 * (owed_lo.size() + owed_hi.size()));
+    auto add = [&](const Owed& o, int dz_) {
+      VT_REQUIRE((flags[o.nb] & NF_BRICK), VT_ESTATE, "fill_borders: neighbour brick missing");
+      pj.insert(pj.end(), {slot[o.leaf], dz_ < 0 ? 0 : mz + 1, slot[o.nb], dz_ < 0 ? mz : 1});
     };
-    for (int64_t i : owed_lo) add(i, -1);
-    for (int64_t i : owed_hi) add(i, +1);
+    for (const Owed& o : owed_lo) add(o, -1);
+    for (const Owed& o : owed_hi) add(o, +1);
     int32_t* dp = upload(*this, pj);
     launch_plane_copy(*this, dp, (int)(pj.size() / 4));
     release(*this, dp);
@@ -1754,7 +1883,6 @@ void Tree::publish_halos() {
 
 void Tree::merge(int64_t n, const int64_t* idx, const int32_t* nflags, const int32_t* stats_in,
                  const void* bricks, int mem_kind, int64_t inserted_voxels) {
-  flush_replays();
   publish_halos();
   prefill_valid = false;
   flush();

@@ -7,6 +7,8 @@
 #include <array>
 #include <atomic>
 #include <chrono>
+#include <deque>
+#include <memory>
 #include <queue>
 #include <unordered_map>
 #include <vector>
@@ -130,7 +132,9 @@ struct Tree {
   bool prefill_enabled = true;   // env VT_PREFILL=0 / a device mirror turns it off
   bool halo_prefill = false;     // some leaf shells hold prefilled values
   bool prefill_valid = true;     // no general-path mutation since (fast fill_borders)
-  std::vector<int64_t> owed_lo, owed_hi;  // leaves whose z-shell plane awaits a neighbour
+  // leaves whose z-shell plane awaits a neighbour: (leaf, z-neighbour leaf)
+  struct Owed { int64_t leaf, nb; };
+  std::vector<Owed> owed_lo, owed_hi;
   // fresh level >= 1 bricks of an early dense launch whose background shell
   // is not written at insertion: fill_borders overwrites every shell voxel
   // of those bricks anyway, and publish_halos() writes the background first
@@ -190,11 +194,31 @@ struct Tree {
   // interleaved block at dsrc)
   int leaf_launch(const void* dsrc, int64_t nsrc, int oz, int dz, int prefill, const DenseJob* dj,
                   int n, const int gn[3], int g0z);
+  // Layer pairs (insert_many): the even brick layer's walk holds its leaf
+  // launch; the odd layer's walk adds its leaves and one leaf kernel builds
+  // both layers, writing every level-1 parent's octants on the fly (fused
+  // half-sample, as a two-layer block) instead of re-reading the leaves in
+  // propagate.  Events are the per-layer walks' events.
+  struct HeldDense {
+    bool active = false;
+    std::vector<DenseJob> djobs;  // (gz, gy, gx) order
+    int z0 = 0, nz = 0, gz0 = 0, gz1 = 0;
+  } held;
+  bool hold_dense = false;
+  void launch_held();
+  // bookkeeping after a dense leaf launch over leaves `djobs` of the block
+  // z in [z0, z1), layers [gz0, gz1]
+  void dense_after_launch(int lr, const std::vector<DenseJob>& djobs,
+                          const std::vector<int64_t>& fused_nodes, int z0, int z1, int gz0,
+                          int gz1, const std::vector<int64_t>* sorted_leaves);
   // B200 batched insertion: same tree and queued events as n successive
   // insert() calls; whole brick layers of single-channel full-x/y blocks
   // become one dense insertion
   void insert_many(int64_t n, const vt_block* blocks, int mem_kind);
   int64_t layer_group(int64_t i, int64_t n, const vt_block* blocks, int mem_kind);
+  bool group_source(int64_t i, int64_t len, const vt_block* blocks, int mem_kind, bool gather,
+                    PlanarSrc& src);
+  int64_t layer_pairs = 0;
   int64_t leaf_index(int gx, int gy, int gz) const {
     return g.level_start[g.depth] + morton[0][gx] + morton[1][gy] + morton[2][gz];
   }
@@ -217,19 +241,89 @@ struct Tree {
   // packed (kind << 56 | node index): 8 bytes per event, a whole-volume
   // insertion emits ~4 per node
   std::vector<uint64_t> events;
-  // lazily replayed tail: rep_list appended rep_count more times (the
-  // UPDATED list every later block of a brick layer repeats)
-  std::vector<uint64_t> rep_list;
-  int64_t rep_count = 0;
-  void flush_replays() {
-    if (rep_count <= 0) return;
-    const size_t e0 = events.size(), nl = rep_list.size();
-    events.resize(e0 + nl * (size_t)rep_count);
-    for (int64_t r = 0; r < rep_count; ++r)
-      std::copy(rep_list.begin(), rep_list.end(), events.begin() + e0 + r * nl);
-    rep_count = 0;
+  // Change events are queued in order as sealed chunks, then the open tail
+  // `events`.  A chunk is a shared list repeated `reps` times: the UPDATED
+  // list every later block of a brick layer repeats (a 2048^2 slice of 32^3
+  // bricks updates ~5.5k nodes, a cfg3 stream ~16M events) is stored once
+  // and expanded only when the events are taken.
+  struct EvChunk {
+    std::shared_ptr<std::vector<uint64_t>> list;
+    int64_t reps = 1;
+    int64_t done = 0;  // expanded elements already taken
+    int64_t left() const { return (int64_t)list->size() * reps - done; }
+  };
+  std::deque<EvChunk> ev_q;
+  void seal_events() {
+    if (events.empty()) return;
+    ev_q.push_back({std::make_shared<std::vector<uint64_t>>(std::move(events)), 1, 0});
+    events.clear();
   }
-  int64_t event_total() const { return (int64_t)events.size() + (int64_t)rep_list.size() * rep_count; }
+  void push_replay(const std::shared_ptr<std::vector<uint64_t>>& l, int64_t reps) {
+    if (reps <= 0 || !l || l->empty()) return;
+    if (events.empty() && !ev_q.empty() && ev_q.back().list == l && ev_q.back().done == 0) {
+      ev_q.back().reps += reps;
+      return;
+    }
+    seal_events();
+    ev_q.push_back({l, reps, 0});
+  }
+  int64_t event_total() const {
+    int64_t n = (int64_t)events.size();
+    for (const EvChunk& c : ev_q) n += c.left();
+    return n;
+  }
+  // move up to cap events out, oldest first; returns how many
+  int64_t take_events(int32_t* kinds, int64_t* indices, int64_t cap) {
+    int64_t m = 0;
+    while (m < cap && !ev_q.empty()) {
+      EvChunk& c = ev_q.front();
+      const int64_t L = (int64_t)c.list->size();
+      while (m < cap && c.left() > 0) {
+        const int64_t j = c.done % L;
+        const int64_t n = std::min(cap - m, L - j);
+        const uint64_t* src = c.list->data() + j;
+        for (int64_t k = 0; k < n; ++k) {
+          kinds[m + k] = ev_kind(src[k]);
+          indices[m + k] = ev_index(src[k]);
+        }
+        c.done += n;
+        m += n;
+      }
+      if (c.left() == 0) ev_q.pop_front();
+    }
+    if (m < cap && !events.empty()) {
+      const int64_t n = std::min<int64_t>(cap - m, (int64_t)events.size());
+      for (int64_t k = 0; k < n; ++k) {
+        kinds[m + k] = ev_kind(events[k]);
+        indices[m + k] = ev_index(events[k]);
+      }
+      if (n == (int64_t)events.size()) events.clear();
+      else events.erase(events.begin(), events.begin() + n);
+      m += n;
+    }
+    return m;
+  }
+  // copy queued events [from, from + n) (oldest = 0) without taking them
+  void copy_events(int64_t from, int64_t n, int32_t* kinds, int64_t* indices) const {
+    int64_t pos = 0, m = 0;
+    auto emit = [&](uint64_t e) {
+      kinds[m] = ev_kind(e);
+      indices[m] = ev_index(e);
+      ++m;
+    };
+    for (const EvChunk& c : ev_q) {
+      const int64_t len = c.left();
+      if (pos + len > from && m < n) {
+        const int64_t L = (int64_t)c.list->size();
+        for (int64_t k = std::max<int64_t>(0, from - pos); k < len && m < n; ++k)
+          emit((*c.list)[(c.done + k) % L]);
+      }
+      pos += len;
+    }
+    for (int64_t k = std::max<int64_t>(0, from - pos); k < (int64_t)events.size() && m < n; ++k)
+      emit(events[k]);
+  }
+  std::shared_ptr<std::vector<uint64_t>> dl_upd_ev;  // a deferred layer's UPDATED events
   static uint64_t ev_pack(int32_t kind, int64_t idx) {
     return ((uint64_t)(uint32_t)kind << 56) | (uint64_t)idx;
   }

@@ -52,6 +52,31 @@ vt_status guarded(F&& f) {
   }
 }
 
+// the calling thread's current device is restored on exit from every ABI
+// entry point that works on a tree's device (Octree(device=k) with k not the
+// current device must neither fail nor leave k current)
+struct DeviceScope {
+  int prev = -1;
+  bool changed = false;
+  explicit DeviceScope(int dev) {
+    if (cudaGetDevice(&prev) == cudaSuccess && prev != dev) {
+      if (cudaSetDevice(dev) != cudaSuccess) throw Error(VT_ECUDA, "cudaSetDevice failed");
+      changed = true;
+    }
+  }
+  ~DeviceScope() {
+    if (changed) cudaSetDevice(prev);
+  }
+};
+
+template <class F>
+vt_status guarded_on(int device, F&& f) {
+  return guarded([&] {
+    DeviceScope ds(device);
+    f();
+  });
+}
+
 constexpr int kMaxDepth = 8;   // volume.py:23-25 (22-bit child pointers)
 constexpr int kMaxC = 4;
 

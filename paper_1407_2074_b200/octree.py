@@ -16,6 +16,7 @@ import ctypes as ct
 import os
 import sys
 import threading
+from collections.abc import Sequence
 from dataclasses import dataclass
 from enum import IntEnum
 
@@ -176,6 +177,43 @@ for _m in ("__setitem__", "__delitem__", "__iadd__", "__imul__", "append", "exte
 EventBatch = EventList  # round-1 name
 
 
+class EventArrays(Sequence):
+    """The change events of a bulk B200 insertion (insert_channels): a
+    read-only sequence of ChangeEvent over the packed ``kinds`` /
+    ``indices`` arrays, so a whole-volume insertion (hundreds of thousands
+    of events) costs no Python objects until a caller iterates it.  The
+    reference-API calls (insert_block, drain_events) return EventList."""
+
+    __slots__ = ("kinds", "indices")
+
+    def __init__(self, kinds, indices):
+        self.kinds = np.asarray(kinds, np.int32)
+        self.indices = np.asarray(indices, np.int64)
+
+    def __len__(self):
+        return len(self.kinds)
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return EventArrays(self.kinds[i], self.indices[i])
+        return ChangeEvent(ChangeKind(int(self.kinds[i])), int(self.indices[i]))
+
+    def __eq__(self, other):
+        if isinstance(other, (EventArrays, EventList)):
+            return (np.array_equal(self.kinds, other.kinds)
+                    and np.array_equal(self.indices, other.indices))
+        try:
+            return list(self) == list(other)
+        except TypeError:
+            return NotImplemented
+
+    def to_list(self) -> "EventList":
+        return EventList.from_arrays(self.kinds, self.indices)
+
+    def __repr__(self):
+        return f"EventArrays({len(self)} events)"
+
+
 class OctreeNode:
     """Snapshot of one node (OctreeNode, octree.py:102-140)."""
 
@@ -257,7 +295,6 @@ class Octree:
         self.geometry = TreeGeometry.build(desc, cfg)
         self.threshold = cfg.resolve_threshold(desc)
         self.lock = threading.RLock()
-        self._events: list[EventList] = []
         self._closed = False
         d = _lib.vt_tree_desc()
         d.dims[:] = list(desc.dims)
@@ -299,31 +336,21 @@ class Octree:
         return self._h
 
     # -- events --------------------------------------------------------------
-    def _collect(self) -> "EventList":
-        n = ct.c_int64()
-        _lib.call("vt_tree_event_count", self._h, ct.byref(n))
-        kinds = np.empty(n.value, np.int32)
-        idx = np.empty(n.value, np.int64)
-        if n.value:
-            got, more = ct.c_int64(), ct.c_int32()
-            _lib.call("vt_tree_take_events", self._h, _lib.ptr(kinds, ct.c_int32),
-                      _lib.ptr(idx, ct.c_int64), n.value, ct.byref(got), ct.byref(more))
-        out = (kinds, idx)
-        if n.value:
-            self._events.append(out)
-        return out
-
     def drain_event_arrays(self) -> tuple[np.ndarray, np.ndarray]:
         """B200 extension: drain_events as packed (kinds int32, indices
         int64) arrays — no Python object per event (a 2048^2 slice of 32^3
-        bricks updates ~5.5k nodes)."""
+        bricks updates ~5.5k nodes).  Events stay queued in the library until
+        drained, as in the reference (octree.py:180-183)."""
         with self.lock:
-            self._collect()
-            parts, self._events = self._events, []
-            if not parts:
-                return np.empty(0, np.int32), np.empty(0, np.int64)
-            return (np.concatenate([p[0] for p in parts]),
-                    np.concatenate([p[1] for p in parts]))
+            n = ct.c_int64()
+            _lib.call("vt_tree_event_count", self._h, ct.byref(n))
+            kinds = np.empty(n.value, np.int32)
+            idx = np.empty(n.value, np.int64)
+            if n.value:
+                got, more = ct.c_int64(), ct.c_int32()
+                _lib.call("vt_tree_take_events", self._h, _lib.ptr(kinds, ct.c_int32),
+                          _lib.ptr(idx, ct.c_int64), n.value, ct.byref(got), ct.byref(more))
+            return kinds, idx
 
     def drain_events(self) -> "EventList":
         """Every queued change event, oldest first (octree.py:180-183)."""
@@ -339,9 +366,10 @@ class Octree:
             raise ValueError(f"channel {channel} out of range")
         return self._insert(int(channel), origin, values, 3)
 
-    def insert_channels(self, origin, values) -> EventList:
+    def insert_channels(self, origin, values) -> "EventArrays":
         """All channels at once: values (dz, dy, dx, C) interleaved; same
-        tree and events as C successive insert_block calls."""
+        tree and events as C successive insert_block calls (returned as a
+        lazy EventArrays sequence)."""
         return self._insert(-1, origin, values, 4)
 
     def insert_many(self, blocks) -> None:
@@ -411,9 +439,16 @@ class Octree:
             cs = torch.cuda.current_stream(values.device).cuda_stream
             keep = values
         else:
-            arr = np.ascontiguousarray(np.asarray(values).astype(desc.dtype, copy=False))
+            if torch is not None and isinstance(values, torch.Tensor):
+                values = values.numpy()  # host tensor (pinned memory stays pinned)
+            arr = np.asarray(values)
+            if arr.dtype != desc.dtype:
+                arr = arr.astype(desc.dtype)
             if arr.ndim != 4:
                 raise ValueError("planar block must be (C, dz, Y, X)")
+            isz = arr.itemsize
+            if arr.strides[3] != isz or arr.strides[2] != arr.shape[3] * isz:
+                arr = np.ascontiguousarray(arr)  # each (c, z) plane must be contiguous
             C, dz, Y, X = arr.shape
             base, cstr, zstr = arr.ctypes.data, arr.strides[0], arr.strides[1]
             kind, cs, keep = _lib.VT_MEM_HOST, 0, arr
@@ -461,18 +496,19 @@ class Octree:
                       ct.byref(n))
             total = int(n.value)
             if total > cap:
-                # more events than the guess: all of them in one take
+                # more events than the guess: copy them (they stay queued)
                 kinds = np.empty(total, np.int32)
                 idx = np.empty(total, np.int64)
-                got, more = ct.c_int64(), ct.c_int32()
-                _lib.call("vt_tree_take_events", self._h, _lib.ptr(kinds, ct.c_int32),
-                          _lib.ptr(idx, ct.c_int64), total, ct.byref(got), ct.byref(more))
+                cnt = ct.c_int64()
+                _lib.call("vt_tree_event_count", self._h, ct.byref(cnt))
+                _lib.call("vt_tree_copy_events", self._h, cnt.value - total, total,
+                          _lib.ptr(kinds, ct.c_int32), _lib.ptr(idx, ct.c_int64))
                 self._ev_cap = min(1 << 20, 1 << (total - 1).bit_length())
             else:
                 kinds, idx = kinds[:total], idx[:total]
             del keep  # device blocks: the caller's stream waits for our reads
-            if total:
-                self._events.append((kinds, idx))
+            if channel < 0:
+                return EventArrays(kinds, idx)
             return EventList.from_arrays(kinds, idx)
 
     def _source(self, values, ndim):
@@ -581,7 +617,6 @@ class Octree:
         """octree.py:540-549; emits NODE_UPDATED per brick."""
         with self.lock:
             _lib.call("vt_tree_fill_borders", self._h)
-            self._collect()
 
     def fill_borders_async(self) -> threading.Thread:
         th = threading.Thread(target=self.fill_borders, name="border-fill", daemon=True)

@@ -107,7 +107,8 @@ class _SceneState:
     def restyled(self, **changes) -> RenderSettings:
         s = self.settings
         base = {f: getattr(s, f) for f in ("mode", "strategy", "sampling_step",
-                                            "early_termination_alpha", "lod_bias")}
+                                            "reference_step", "early_termination_alpha",
+                                            "lod_bias", "precision", "empty_space_skip")}
         base.update(changes)
         return RenderSettings(**base)
 
