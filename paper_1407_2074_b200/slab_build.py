@@ -131,7 +131,6 @@ def merge_records(tree, idx, flags, stats, bricks, inserted_voxels: int = 0) -> 
         _lib.call("vt_tree_merge", tree.handle, len(idx), _lib.ptr(idx, ct.c_int64),
                   _lib.ptr(flags, ct.c_int32), _lib.ptr(stats, ct.c_int32), ptr, kind,
                   int(inserted_voxels))
-        tree._collect()
 
 
 def build_sharded(tree, source, group=None, slab_z=32, fill_borders=True) -> SlabPlan:
