@@ -262,15 +262,40 @@ class OctreeNode:
         return f"<node {self.index} L{self.level} {kind} avg={self.avg}>"
 
 
+class _BrickHandle:
+    """BrickHandle (paging.py:54-60) over the HBM pool."""
+
+    __slots__ = ("_store", "loc")
+
+    def __init__(self, store: "_PoolView", loc: BrickLocator):
+        self._store, self.loc = store, loc
+
+    @property
+    def data(self) -> np.ndarray:
+        return self._store.read_brick(self.loc)
+
+
 class _PoolView:
     """``tree.store`` facade: brick reads go to HBM (BrickStore.read_brick,
     paging.py:398-403)."""
+
+    page_faults = 0  # the pool is HBM-resident: nothing is ever paged in
 
     def __init__(self, tree: "Octree"):
         self._tree = tree
 
     def read_brick(self, loc: BrickLocator) -> np.ndarray:
         return self._tree.read_brick(loc.node_index)
+
+    def acquire(self, loc: BrickLocator, blocking: bool = True) -> "_BrickHandle":
+        """BrickStore.acquire (paging.py:248-290): every brick of the HBM
+        pool is always available, so this never returns None; the handle's
+        ``data`` reads the brick on demand (DeviceState.upload_bricks copies
+        pool -> brick buffer on the device and never touches it)."""
+        return _BrickHandle(self, loc)
+
+    def release(self, handle: "_BrickHandle") -> None:
+        pass
 
     @property
     def live_bricks(self) -> int:
