@@ -167,6 +167,11 @@ vt_status vt_tree_finalize(vt_tree* tree);
 vt_status vt_tree_fill_borders(vt_tree* tree);
 /* complete all deferred device work and wait for it */
 vt_status vt_tree_sync(vt_tree* tree);
+/* B200 extension: enqueue every deferred device update (an open slice
+ * layer's received planes, pending pyramid propagation) on the tree stream
+ * without waiting for it — what any reader does first (octree.py:323-397
+ * leaves the tree complete after every insert_block). */
+vt_status vt_tree_flush(vt_tree* tree);
 vt_status vt_tree_info_get(vt_tree* tree, vt_tree_info* out);
 /* B200 extension: threshold-0 dense build (dense_build.cu).  A fused
  * all-channel block spanning the full x/y extent and whole brick layers over
@@ -259,6 +264,12 @@ vt_status vt_mirror_set_resident(vt_mirror* m, int64_t n, const int64_t* nodes,
                                  const int32_t* slots, int32_t copy);
 /* rewrite every node entry from the tree + residency (device.py:168-203) */
 vt_status vt_mirror_repack(vt_mirror* m);
+/* B200 extension for zero-copy mirrors: DeviceState.apply_events(
+ * octree.drain_events()) without moving the events to the host — every
+ * queued change event is taken inside the library, NODE_DELETED flags are
+ * cleared (device.py:214-220), node entries re-packed and brick maxima of
+ * the changed slots refreshed.  Returns the events consumed and deletions. */
+vt_status vt_mirror_apply_queued(vt_mirror* m, int64_t* n_events, int64_t* n_deleted);
 /* flag buffer transfer; clear != 0 zeroes it after reading (device.py:250-252) */
 vt_status vt_mirror_read_flags(vt_mirror* m, uint8_t* out, int32_t clear);
 

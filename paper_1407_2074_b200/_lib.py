@@ -100,6 +100,7 @@ SIGNATURES = {
     "vt_tree_finalize": [P],
     "vt_tree_fill_borders": [P],
     "vt_tree_sync": [P],
+    "vt_tree_flush": [P],
     "vt_tree_info_get": [P, ct.POINTER(vt_tree_info)],
     "vt_tree_node": [P, I64, ct.POINTER(vt_node), PI32],
     "vt_tree_list_nodes": [P, PI64, PI32, I64, PI64],
@@ -113,6 +114,7 @@ SIGNATURES = {
     "vt_mirror_buffers": [P, ct.POINTER(P), ct.POINTER(P), ct.POINTER(P), PI64, PI64],
     "vt_mirror_set_resident": [P, I64, PI64, PI32, I32],
     "vt_mirror_repack": [P],
+    "vt_mirror_apply_queued": [P, PI64, PI64],
     "vt_mirror_read_flags": [P, P, I32],
     "vt_rays_create": [P, ct.POINTER(vt_scene), PI32, ct.POINTER(P)],
     "vt_rays_destroy": [P],

@@ -276,6 +276,10 @@ vt_status vt_tree_sync(vt_tree* tree) {
   return guarded_on(tree->t.device, [&] { tree->t.sync(); });
 }
 
+vt_status vt_tree_flush(vt_tree* tree) {
+  return guarded_on(tree->t.device, [&] { tree->t.flush(); });
+}
+
 vt_status vt_tree_info_get(vt_tree* tree, vt_tree_info* o) {
   return guarded_on(tree->t.device, [&] {
     const Tree& t = tree->t;

@@ -784,13 +784,15 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma_planar(
     const __grid_constant__ CUtensorMap map, int oz, int dz, int prefill,
     const DenseJob* __restrict__ jobs, int gnx, int gny, int g0z, Geo g,
     uint16_t* __restrict__ pool, int32_t* stats, int32_t* nmin, int32_t* nmax,
-    unsigned long long* nsum) {
+    unsigned long long* nsum, uint16_t* __restrict__ bmax_sub, uint16_t* __restrict__ bmax_brick,
+    int nsb) {
   constexpr int P = kTmaP;
   constexpr int WPP = kTmaWarps / P;  // warps per plane
   constexpr int NT = WPP * 32;        // threads per plane
   extern __shared__ __align__(128) unsigned char s_in[];
   __shared__ uint64_t s_bar[kPStages];
   __shared__ int s_mn[2][kTmaWarps][C], s_mx[2][kTmaWarps][C];
+  __shared__ int s_wm[kTmaWarps][C];  // brick maxima over every stored voxel written
   __shared__ unsigned long long s_sm[2][kTmaWarps][C];
   const DenseJob j = jobs[blockIdx.x];
   const int gx = (int)(blockIdx.x % gnx);
@@ -842,12 +844,14 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma_planar(
   uint16_t* parent = pslot >= 0 ? pool + (int64_t)pslot * g.brick_elems : nullptr;
 
   int lmn[C], lmx[C], omn[C], omx[C];
+  uint32_t wmx[C];  // max of every sample this thread stores (brick maxima)
   unsigned long long lsm[C], osm[C];
 #pragma unroll
   for (int c = 0; c < C; ++c) {
     lmn[c] = omn[c] = INT_MAX;
     lmx[c] = omx[c] = INT_MIN;
     lsm[c] = osm[c] = 0;
+    wmx[c] = 0;
   }
   const int pw = warp / WPP;                // plane of the stage this warp group builds
   const int cstr = rows * bx;               // staged channel stride (samples)
@@ -880,7 +884,10 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma_planar(
         const uint32_t* w = s32 + (ys * bx + xs) / 2;
         uint32_t pv[C];
 #pragma unroll
-        for (int c = 0; c < C; ++c) pv[c] = __byte_perm(w[c * cstr / 2], w[c * cstr / 2 + 1], 0x5432);
+        for (int c = 0; c < C; ++c) {
+          pv[c] = __byte_perm(w[c * cstr / 2], w[c * cstr / 2 + 1], 0x5432);
+          wmx[c] = max(wmx[c], max(pv[c] & 0xFFFFu, pv[c] >> 16));
+        }
         if (stat_plane) {
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
@@ -920,7 +927,10 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma_planar(
         uint32_t val[C];
         const uint16_t* q = iplane + ys * bx + xs;
 #pragma unroll
-        for (int c = 0; c < C; ++c) val[c] = take ? (uint32_t)q[c * cstr] : (uint32_t)bg;
+        for (int c = 0; c < C; ++c) {
+          val[c] = take ? (uint32_t)q[c * cstr] : (uint32_t)bg;
+          if (act) wmx[c] = max(wmx[c], val[c]);
+        }
         if (stat_plane && xs >= 1 && xs <= cx && ys >= 1 && ys <= cy && act) {
 #pragma unroll
           for (int c = 0; c < C; ++c) {
@@ -1036,10 +1046,12 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma_planar(
       omn[c] = min(omn[c], __shfl_xor_sync(0xffffffffu, omn[c], o));
       omx[c] = max(omx[c], __shfl_xor_sync(0xffffffffu, omx[c], o));
       osm[c] += __shfl_xor_sync(0xffffffffu, osm[c], o);
+      wmx[c] = max(wmx[c], __shfl_xor_sync(0xffffffffu, wmx[c], o));
     }
   if (lane == 0)
 #pragma unroll
     for (int c = 0; c < C; ++c) {
+      s_wm[warp][c] = (int)wmx[c];
       s_mn[0][warp][c] = lmn[c];
       s_mx[0][warp][c] = lmx[c];
       s_sm[0][warp][c] = lsm[c];
@@ -1072,6 +1084,19 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma_planar(
       atomicMax(nmax + pnode * C + c, pb);
       atomicAdd(nsum + pnode * C + c, pt2);
     }
+  }
+  if (bmax_brick) {
+    // the stored brick is complete: its maxima over every voxel (shells as
+    // written; prefilled shells only loosen the bound before fill_borders)
+    if (tid < kMaxC) {
+      int m = 0;
+      if (tid < C)
+        for (int w = 0; w < kTmaWarps; ++w) m = max(m, s_wm[w][tid]);
+      bmax_brick[(int64_t)j.slot * kMaxC + tid] = (uint16_t)m;
+    }
+    // sub-brick maxima unknown: never skip at sub-brick granularity
+    for (int i = tid; i < nsb * kMaxC; i += kTmaWarps * 32)
+      bmax_sub[(int64_t)j.slot * nsb * kMaxC + i] = 0xFFFFu;
   }
 }
 
@@ -1536,11 +1561,12 @@ static int leaf_launch_planar(const Tree& t, const void* base, int64_t zstride, 
   auto k = t.g.brick[0] == 32 && t.g.brick[1] == 32 ? k_dense_leaf_tma_planar<C, 32, 32>
                                                     : k_dense_leaf_tma_planar<C>;
   VT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  uint16_t* bb = t.bmax_brick();
   k<<<n, kTmaWarps * 32, smem, t.stream>>>(map, oz, (int)dz, prefill, jobs, gn[0], gn[1], g0z, t.g,
                                           (uint16_t*)t.d_pool, t.d_stats, t.d_nmin, t.d_nmax,
-                                          t.d_nsum);
+                                          t.d_nsum, t.d_bmax, bb, t.bmax_nsb);
   VT_CHECK_LAUNCH();
-  return kLeafTma | (prefill ? kLeafPrefilled : 0);
+  return kLeafTma | (prefill ? kLeafPrefilled : 0) | (bb ? kLeafBmax : 0);
 }
 
 int launch_dense_leaf_planar(const Tree& t, const void* base, int64_t zstride, int64_t cstride,
@@ -1602,11 +1628,188 @@ void launch_fill_bg(const Tree& t, void* dst, int64_t n) {
   VT_CHECK_LAUNCH();
 }
 
+// background into planes base + idx[k] * plane (samples), one launch for
+// up to kMaxFillPlanes planes: 16-byte stores, grid.y = plane
+struct FillPlanes {
+  int32_t idx[kMaxFillPlanes];
+};
+__global__ void k_fill_planes(uint8_t* base, int64_t plane_bytes, FillPlanes fp, uint32_t word) {
+  uint4* dst = reinterpret_cast<uint4*>(base + (int64_t)fp.idx[blockIdx.y] * plane_bytes);
+  const int64_t n = plane_bytes / 16;
+  const uint4 v = make_uint4(word, word, word, word);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = v;
+}
+
+void launch_fill_planes(const Tree& t, void* base, int64_t plane, const int32_t* idx, int n) {
+  const int64_t pb = plane * t.g.sb;
+  if (pb % 16 != 0 || ((uintptr_t)base & 15) != 0) {
+    for (int k = 0; k < n; ++k) launch_fill_bg(t, (uint8_t*)base + (int64_t)idx[k] * pb, plane);
+    return;
+  }
+  const uint32_t bg = (uint32_t)t.g.bg;
+  const uint32_t word = t.g.sb == 1 ? bg * 0x01010101u : (bg | (bg << 16));
+  for (int k0 = 0; k0 < n; k0 += kMaxFillPlanes) {
+    FillPlanes fp{};
+    const int m = std::min(kMaxFillPlanes, n - k0);
+    for (int k = 0; k < m; ++k) fp.idx[k] = idx[k0 + k];
+    const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(pb / 16 / 256, 64));
+    k_fill_planes<<<dim3(gx, m), 256, 0, t.stream>>>((uint8_t*)base, pb, fp, word);
+    VT_CHECK_LAUNCH();
+  }
+}
+
 int launch_dense_leaf(const Tree& t, const void* src, int64_t nsrc, int oz, int prefill,
                       const DenseJob* jobs, int n, const int gn[3], int g0z) {
   if (n <= 0) return 0;
   if (t.g.sb == 1) return leaf_dispatch<uint8_t>(t, src, nsrc, oz, 0, jobs, n, gn, g0z);
   return leaf_dispatch<uint16_t>(t, src, nsrc, oz, prefill, jobs, n, gn, g0z);
+}
+
+// Shared-memory variant for 16-bit pools, all axes split, every child a
+// full in-volume brick (the bulk of every dense level): per parent interior
+// plane z, the two child planes it half-samples from each of the 4
+// children of that z-half (contiguous in the stored brick) are staged into
+// shared memory with 16-byte cp.async copies — double buffered, so the next
+// plane's copies overlap this plane's arithmetic — then every parent voxel
+// is the 2x2x2 round_mean of 8 shared samples per channel.  Same values,
+// plane partials and statistics as k_dense_level.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+inline int64_t level_s_span(const Geo& g) {
+  const int64_t pair = 2LL * g.stored[0] * g.stored[1] * g.C * 2;
+  return ((pair + 15) & ~15LL) + 16;
+}
+constexpr int64_t kLevelSmemMax = 112 * 1024;
+
+template <int C>
+__global__ void __launch_bounds__(256, 2) k_dense_level_s(
+    const int64_t* __restrict__ nodes, Geo g, uint16_t* pool, const int32_t* __restrict__ slots,
+    const uint8_t* __restrict__ flags, int32_t* pmin, int32_t* pmax, unsigned long long* psum,
+    int32_t* stats, int zsplit, int span) {
+  extern __shared__ __align__(16) unsigned char s_raw[];
+  const int64_t node = nodes[blockIdx.x / zsplit];
+  const int part = blockIdx.x % zsplit;
+  const int Mx = g.brick[0], My = g.brick[1], Mz = g.brick[2];
+  const int hx = Mx / 2, hy = My / 2, hz = Mz / 2;
+  const int Sx = g.stored[0], Sy = g.stored[1];
+  const int64_t plane_elems = (int64_t)Sx * Sy * C;
+  const int64_t pair_bytes = 2 * plane_elems * 2;
+  __shared__ const uint16_t* s_child[8];
+  __shared__ int s_pslot;
+  __shared__ int s_pmn[8][C], s_pmx[8][C];
+  __shared__ unsigned long long s_psm[8][C];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  if (tid < 8) s_child[tid] = pool + (int64_t)slots[8 * node + 1 + tid] * g.brick_elems;
+  if (tid == 8) s_pslot = slots[node];
+  __syncthreads();
+  uint16_t* parent = pool + (int64_t)s_pslot * g.brick_elems;
+  const int zb0 = part * Mz / zsplit, zb1 = (part + 1) * Mz / zsplit;
+  // copy the child plane pairs of parent plane z into buffer b
+  auto issue = [&](int z, int b) {
+    const int bz = z >= hz ? 1 : 0, oz = z - bz * hz;
+    for (int q = 0; q < 4; ++q) {
+      const uintptr_t src = (uintptr_t)(s_child[q | (bz << 2)] + (1 + 2 * oz) * plane_elems);
+      const uintptr_t a0 = src & ~(uintptr_t)15, a1 = (src + pair_bytes + 15) & ~(uintptr_t)15;
+      const int nvec = (int)((a1 - a0) / 16);
+      unsigned char* dst = s_raw + (size_t)(b * 4 + q) * span;
+      for (int i = tid; i < nvec; i += blockDim.x)
+        cp_async16(dst + 16 * i, (const void*)(a0 + 16 * (uintptr_t)i));
+    }
+    cp_async_commit();
+  };
+  Acc<C> tot;
+  tot.init();
+  if (zb0 < zb1) issue(zb0, 0);
+  for (int z = zb0; z < zb1; ++z) {
+    const int b = (z - zb0) & 1;
+    if (z + 1 < zb1) {
+      issue(z + 1, b ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const int bz = z >= hz ? 1 : 0, oz = z - bz * hz;
+    Acc<C> pl;
+    pl.init();
+    for (int v = tid; v < Mx * My; v += blockDim.x) {
+      const int y = v / Mx, x = v - y * Mx;
+      const int bx = x >= hx ? 1 : 0, by = y >= hy ? 1 : 0;
+      const int ox = x - bx * hx, oy = y - by * hy;
+      const int q = bx | (by << 1);
+      const uintptr_t src = (uintptr_t)(s_child[q | (bz << 2)] + (1 + 2 * oz) * plane_elems);
+      const uint16_t* base =
+          reinterpret_cast<const uint16_t*>(s_raw + (size_t)(b * 4 + q) * span + (src & 15));
+      const uint16_t* p0 = base + ((1 + 2 * oy) * Sx + 1 + 2 * ox) * C;
+      const uint16_t* p1 = p0 + plane_elems;
+      int val[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const unsigned sum = (unsigned)p0[c] + p0[C + c] + p0[Sx * C + c] + p0[Sx * C + C + c] +
+                             p1[c] + p1[C + c] + p1[Sx * C + c] + p1[Sx * C + C + c];
+        val[c] = (int)((2 * sum + 8) / 16);
+      }
+      uint16_t* dst = parent + g.voxel_offset(1 + z, 1 + y, 1 + x);
+#pragma unroll
+      for (int c = 0; c < C; ++c) dst[c] = (uint16_t)val[c];
+      pl.add_all(val);
+    }
+    pl.warp_reduce();
+    if (lane == 0)
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        s_pmn[warp][c] = pl.mn[c];
+        s_pmx[warp][c] = pl.mx[c];
+        s_psm[warp][c] = pl.sm[c];
+      }
+    __syncthreads();  // plane partials visible; buffer b free for reuse
+    if (tid == 0) {
+      Acc<C> a;
+      a.init();
+      for (int w = 0; w < nw; ++w)
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          a.mn[c] = min(a.mn[c], s_pmn[w][c]);
+          a.mx[c] = max(a.mx[c], s_pmx[w][c]);
+          a.sm[c] += s_psm[w][c];
+        }
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const int64_t off = ((int64_t)s_pslot * Mz + z) * C + c;
+        pmin[off] = a.mn[c];
+        pmax[off] = a.mx[c];
+        psum[off] = a.sm[c];
+      }
+      tot.merge(a);
+    }
+  }
+  finish_stats<C>(tot, node, (int64_t)Mx * My * Mz, false, g, flags, stats);
+}
+
+template <class T, int C>
+static void level_launch_s(const Tree& t, const int64_t* nodes, int n, int zsplit) {
+  const int span = (int)level_s_span(t.g);
+  const int smem = 8 * span;
+  static bool attr = false;
+  if (!attr) {
+    VT_CUDA(cudaFuncSetAttribute(k_dense_level_s<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kLevelSmemMax));
+    attr = true;
+  }
+  k_dense_level_s<C><<<n * zsplit, 256, smem, t.stream>>>(
+      nodes, t.g, (uint16_t*)t.d_pool, t.d_slot, t.d_flags, t.d_pmin, t.d_pmax, t.d_psum,
+      t.d_stats, zsplit, span);
+  VT_CHECK_LAUNCH();
 }
 
 template <class T, int C>
@@ -1642,8 +1845,29 @@ int dense_level_split(const Tree& t, int n) {
   return k;
 }
 
-void launch_dense_level(const Tree& t, const int64_t* nodes, int n, int zsplit) {
+// the shared-memory level kernel applies: 16-bit samples, all axes split,
+// even brick edges, the staged plane pairs fit
+bool level_smem_ok(const Tree& t) {
+  static const bool off = [] {
+    const char* e = std::getenv("VT_LEVEL_SMEM");
+    return e && e[0] == '0';
+  }();
+  const Geo& g = t.g;
+  return !off && g.sb == 2 && g.split[0] && g.split[1] && g.split[2] && g.brick[0] % 2 == 0 &&
+         g.brick[1] % 2 == 0 && g.brick[2] % 2 == 0 && 8 * level_s_span(g) <= kLevelSmemMax;
+}
+
+void launch_dense_level(const Tree& t, const int64_t* nodes, int n, int zsplit, bool smem) {
   if (n <= 0) return;
+  if (smem && level_smem_ok(t)) {
+    switch (t.g.C) {
+      case 1: level_launch_s<uint16_t, 1>(t, nodes, n, zsplit); break;
+      case 2: level_launch_s<uint16_t, 2>(t, nodes, n, zsplit); break;
+      case 3: level_launch_s<uint16_t, 3>(t, nodes, n, zsplit); break;
+      default: level_launch_s<uint16_t, 4>(t, nodes, n, zsplit); break;
+    }
+    return;
+  }
   if (t.g.sb == 1)
     level_dispatch<uint8_t>(t, nodes, n, zsplit);
   else

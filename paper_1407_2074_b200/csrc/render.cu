@@ -1381,45 +1381,58 @@ static void update_bmax(vt_mirror* m, const int32_t* d_slots, int n) {
   int sbk[3], nsub[3];
   sub_bricks(t.g, sbk, nsub);
   const int64_t nsb = (int64_t)nsub[0] * nsub[1] * nsub[2];
-  const int64_t nslots = std::max<int64_t>(1, m->zero_copy ? t.pool_slots : m->slots);
-  const int64_t need = nslots * nsb;
-  // zero copy: only the pool slots written since the maxima were last
-  // computed (Tree::slot_ver), unless everything changed or the table grows
   std::vector<int32_t> dirty;
   int32_t* d_dirty = nullptr;
-  if (m->zero_copy && !d_slots && m->bmax_version >= 0 && need <= m->bmax_cap &&
-      t.all_ver <= m->bmax_version) {
+  uint16_t *tab, *tab_brick;
+  int jobs;
+  if (m->zero_copy) {
+    // the tree owns the table (dense leaf kernels write their maxima into
+    // it): recompute the slots written since their maxima were last valid
+    VT_REQUIRE(!d_slots, VT_ESTATE, "zero-copy maxima are per pool slot");
+    t.enable_bmax((int)nsb);
+    m->d_bmax = t.d_bmax;
+    m->d_bmax_brick = t.bmax_brick();
+    m->bmax_cap = t.bmax_cap * nsb;
     const int64_t used = std::min<int64_t>(t.cursor, (int64_t)t.slot_ver.size());
     for (int64_t s = 0; s < used; ++s)
-      if (t.slot_ver[s] > m->bmax_version) dirty.push_back((int32_t)s);
-    m->bmax_incremental += 1;
+      if (std::max(t.slot_ver[s], t.all_ver) > t.bmax_ver[s]) dirty.push_back((int32_t)s);
+    for (int32_t s : dirty) t.bmax_ver[s] = t.data_version;
+    if (m->bmax_version >= 0) m->bmax_incremental += 1;
     m->bmax_last_slots = (int64_t)dirty.size();
     m->bmax_version = t.data_version;
+    m->bmax_valid = true;
     if (dirty.empty()) return;
-    d_dirty = upload(t, dirty);
-    d_slots = d_dirty;
-    n = (int)dirty.size();
-  } else if (m->zero_copy && !d_slots) {
-    m->bmax_last_slots = t.cursor;
+    if ((int64_t)dirty.size() < used) {
+      d_dirty = upload(t, dirty);
+      d_slots = d_dirty;
+    }
+    jobs = (int)dirty.size();
+    tab = t.d_bmax;
+    tab_brick = t.bmax_brick();
+  } else {
+    const int64_t nslots = std::max<int64_t>(1, m->slots);
+    const int64_t need = nslots * nsb;
+    if (need > m->bmax_cap) {
+      VT_CUDA(cudaStreamSynchronize(t.stream));
+      cudaFree(m->d_bmax);
+      m->d_bmax = nullptr;
+      const size_t bytes = (need + nslots) * kMaxC * sizeof(uint16_t);
+      VT_CUDA(cudaMalloc(&m->d_bmax, bytes));
+      VT_CUDA(cudaMemsetAsync(m->d_bmax, 0xFF, bytes, t.stream));  // unknown: never empty
+      m->bmax_cap = need;
+      m->d_bmax_brick = m->d_bmax + need * kMaxC;
+    }
+    jobs = d_slots ? n : (int)m->slots;
+    tab = m->d_bmax;
+    tab_brick = m->d_bmax_brick;
   }
-  if (need > m->bmax_cap) {
-    VT_CUDA(cudaStreamSynchronize(t.stream));
-    cudaFree(m->d_bmax);
-    m->d_bmax = nullptr;
-    const size_t bytes = (need + nslots) * kMaxC * sizeof(uint16_t);
-    VT_CUDA(cudaMalloc(&m->d_bmax, bytes));
-    VT_CUDA(cudaMemsetAsync(m->d_bmax, 0xFF, bytes, t.stream));  // unknown: never empty
-    m->bmax_cap = need;
-    m->d_bmax_brick = m->d_bmax + need * kMaxC;
-  }
-  const int jobs = d_slots ? n : (int)(m->zero_copy ? t.cursor : m->slots);
   if (jobs > 0) {
     const unsigned grid = (unsigned)std::min<int64_t>(jobs, 148 * 16);
     const void* bb = m->zero_copy ? (const void*)t.d_pool : (const void*)m->d_bb;
     if (t.g.sb == 1)
       k_brick_max<uint8_t><<<grid, 256, 0, t.stream>>>((const uint8_t*)bb, d_slots, jobs, t.g,
                                                        sbk[0], sbk[1], sbk[2], nsub[0], nsub[1],
-                                                       nsub[2], m->d_bmax, m->d_bmax_brick);
+                                                       nsub[2], tab, tab_brick);
     else if (sbk[0] % 2 == 0 && t.g.stored[0] % 2 == 0 &&
              (sbk[0] + 2) * t.g.C / 2 <= kBmaxWords &&
              (size_t)t.g.stored[2] * t.g.stored[1] * nsub[0] * t.g.C * sizeof(uint16_t) <=
@@ -1429,7 +1442,7 @@ static void update_bmax(vt_mirror* m, const int32_t* d_slots, int n) {
   case CC:                                                                                     \
     k_brick_max16<CC><<<grid, 256, kBmaxSmemBytes, t.stream>>>(                                \
         (const uint16_t*)bb, d_slots, jobs, t.g, sbk[0], sbk[1], sbk[2], nsub[0], nsub[1],     \
-        nsub[2], m->d_bmax, m->d_bmax_brick);                                                  \
+        nsub[2], tab, tab_brick);                                                              \
     break;
         VT_BMAX16(1)
         VT_BMAX16(2)
@@ -1440,12 +1453,17 @@ static void update_bmax(vt_mirror* m, const int32_t* d_slots, int n) {
     else
       k_brick_max<uint16_t><<<grid, 256, 0, t.stream>>>((const uint16_t*)bb, d_slots, jobs, t.g,
                                                         sbk[0], sbk[1], sbk[2], nsub[0], nsub[1],
-                                                        nsub[2], m->d_bmax, m->d_bmax_brick);
+                                                        nsub[2], tab, tab_brick);
     VT_CUDA(cudaGetLastError());
   }
   release(t, d_dirty);
   m->bmax_valid = true;
   if (m->zero_copy) m->bmax_version = t.data_version;
+}
+
+__global__ void k_clear_flags(const int64_t* __restrict__ idx, int64_t n, uint8_t* fb) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) fb[idx[i]] = 0;
 }
 
 struct vt_rays {
@@ -1511,7 +1529,7 @@ static void mirror_release(vt_mirror* m) {
   cudaFree(m->d_fb);
   cudaFree(m->d_bb);
   cudaFree(m->d_res);
-  cudaFree(m->d_bmax);
+  if (!m->zero_copy) cudaFree(m->d_bmax);  // a zero-copy mirror's table is the tree's
   vt_tree_release(m->tree);
   delete m;
 }
@@ -1588,6 +1606,31 @@ vt_status vt_mirror_repack(vt_mirror* m) {
     VT_CUDA(cudaGetLastError());
     if (m->zero_copy) update_bmax(m, nullptr, 0);
     else if (!m->bmax_valid) update_bmax(m, nullptr, 0);
+  });
+}
+
+vt_status vt_mirror_apply_queued(vt_mirror* m, int64_t* n_events, int64_t* n_deleted) {
+  return guarded_on(m->tree->t.device, [&] {
+    Tree& t = m->tree->t;
+    VT_REQUIRE(m->zero_copy, VT_ESTATE,
+               "apply_queued needs a zero-copy mirror (bounded mirrors release slots per event)");
+    t.flush();
+    std::vector<int64_t> del;
+    const int64_t n = t.discard_events(del);
+    if (!del.empty()) {
+      int64_t* d = upload(t, del);
+      k_clear_flags<<<(unsigned)((del.size() + 255) / 256), 256, 0, t.stream>>>(
+          d, (int64_t)del.size(), m->d_fb);
+      VT_CUDA(cudaGetLastError());
+      release(t, d);
+    }
+    const int64_t cap = t.g.capacity;
+    k_repack<<<(unsigned)((cap + 255) / 256), 256, 0, t.stream>>>(
+        t.g, t.d_flags, t.d_slot, t.d_stats, m->d_res, 1, (double)t.fmax, 40 / t.g.C, m->d_nb);
+    VT_CUDA(cudaGetLastError());
+    update_bmax(m, nullptr, 0);
+    if (n_events) *n_events = n;
+    if (n_deleted) *n_deleted = (int64_t)del.size();
   });
 }
 

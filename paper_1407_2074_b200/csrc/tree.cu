@@ -243,6 +243,7 @@ Tree::~Tree() {
   pinned_put(stage.h, stage.cap);
   if (stage.d) cudaFree(stage.d);
   cudaFree(d_pool);
+  cudaFree(d_bmax);
   cudaFree(d_flags);
   cudaFree(d_slot);
   cudaFree(d_stats);
@@ -296,6 +297,34 @@ void Tree::ensure_pool(int64_t need) {
   d_psum = nsum;
   pool_slots = n;
   slot_ver.resize(n, data_version);
+  if (d_bmax) enable_bmax(bmax_nsb);  // grow the maxima table with the pool
+}
+
+// (re)size the brick-maxima table to the pool; new slots are "unknown"
+// (0xFFFF: never skipped) until a kernel or a refresh computes them
+void Tree::enable_bmax(int nsb) {
+  if (d_bmax && bmax_cap >= pool_slots && nsb == bmax_nsb) return;
+  const int64_t n = std::max<int64_t>(1, pool_slots);
+  uint16_t* nb = nullptr;
+  const size_t sub = (size_t)n * nsb * kMaxC, bytes = (sub + (size_t)n * kMaxC) * sizeof(uint16_t);
+  VT_CUDA(cudaMalloc(&nb, bytes));
+  VT_CUDA(cudaMemsetAsync(nb, 0xFF, bytes, stream));
+  if (d_bmax && nsb == bmax_nsb) {
+    VT_CUDA(cudaMemcpyAsync(nb, d_bmax, (size_t)bmax_cap * nsb * kMaxC * 2,
+                            cudaMemcpyDeviceToDevice, stream));
+    VT_CUDA(cudaMemcpyAsync(nb + sub, bmax_brick(), (size_t)bmax_cap * kMaxC * 2,
+                            cudaMemcpyDeviceToDevice, stream));
+    bmax_ver.resize(n, -1);
+  } else {
+    bmax_ver.assign(n, -1);
+  }
+  if (d_bmax) {
+    VT_CUDA(cudaStreamSynchronize(stream));
+    cudaFree(d_bmax);
+  }
+  d_bmax = nb;
+  bmax_cap = n;
+  bmax_nsb = nsb;
 }
 
 // ---------------------------------------------------------------------------
@@ -1132,6 +1161,7 @@ void Tree::dense_after_launch(int lr, const std::vector<DenseJob>& djobs,
   else
     for (const DenseJob& jd : djobs) pend_dense(jd.node);
   for (const DenseJob& jd : djobs) complete[jd.node] = 1;
+  if (lr & kLeafBmax) leaves_bmax_valid(djobs);
   ++dense_leaf_inserts;
   if (prefilled) {
     // z-shell planes whose block plane lies outside this insertion are owed
@@ -1269,11 +1299,13 @@ void Tree::defer_copy(int channel, const int origin[3], const int dims[3], const
 void Tree::run_layer(bool partial) {
   const int* M = g.brick;
   const int64_t plane = (int64_t)g.dims[0] * g.dims[1];
-  if (partial)
+  if (partial) {
+    std::vector<int32_t> miss;  // planes not received yet hold the background
     for (int zi = 0; zi < dl.nz; ++zi)
       for (int c = 0; c < g.C; ++c)
-        if (!dl.got[(size_t)zi * g.C + c])
-          launch_fill_bg(*this, d_acc + ((size_t)c * M[2] + zi) * plane * g.sb, plane);
+        if (!dl.got[(size_t)zi * g.C + c]) miss.push_back(c * M[2] + zi);
+    launch_fill_planes(*this, d_acc, plane, miss.data(), (int)miss.size());
+  }
   const int gn[3] = {(g.dims[0] - 1) / M[0] + 1, (g.dims[1] - 1) / M[1] + 1, 1};
   DenseJob* dj = upload(*this, dl.djobs);
   const bool want = prefill_enabled && !borders;
@@ -1291,6 +1323,7 @@ void Tree::run_layer(bool partial) {
   // the layer's ancestors are owed a recompute: pending since the opening
   // walk, or again when a reader's flush already consumed that entry
   ++data_version;
+  if (lr & kLeafBmax) leaves_bmax_valid(dl.djobs);
   for (int64_t p : dl.upd) {
     const int lvl = g.level_of(p);
     if (lvl > 0) pend(lvl, p);
@@ -1643,9 +1676,33 @@ void Tree::propagate() {
       int64_t* dfd = upload(*this, fused_done);
       launch_finish_fused(*this, dfd, (int)fused_done.size());
       release(*this, dfd);
-      int64_t* dd = upload(*this, dense_nodes);
+      // nodes whose 8 children are full in-volume bricks take the
+      // shared-memory kernel; the rest (volume edges) the general one
+      std::vector<int64_t> dfull, dpart;
+      if (level_smem_ok(*this)) {
+        for (int64_t q : dense_nodes) {
+          bool full = true;
+          for (int k = 0; k < 8 && full; ++k) {
+            const int64_t ch = 8 * q + 1 + k;
+            if ((flags[ch] & (NF_EXISTS | NF_BRICK)) != (NF_EXISTS | NF_BRICK)) {
+              full = false;
+              break;
+            }
+            int ce[3];
+            node_in_extent(ch, ce);
+            full = ce[0] == M[0] && ce[1] == M[1] && ce[2] == M[2];
+          }
+          (full ? dfull : dpart).push_back(q);
+        }
+      } else {
+        dpart = dense_nodes;
+      }
       const int zsplit = dense_level_split(*this, (int)dense_nodes.size());
-      launch_dense_level(*this, dd, (int)dense_nodes.size(), zsplit);
+      int64_t* dd = upload(*this, dfull);
+      launch_dense_level(*this, dd, (int)dfull.size(), zsplit, true);
+      release(*this, dd);
+      dd = upload(*this, dpart);
+      launch_dense_level(*this, dd, (int)dpart.size(), zsplit, false);
       release(*this, dd);
       if (zsplit > 1)
         for (int64_t q : dense_nodes) {

@@ -112,6 +112,26 @@ struct Tree {
     if (s >= 0 && (size_t)s < slot_ver.size()) slot_ver[s] = data_version;
   }
   void touch_all() { all_ver = data_version; }
+  // Brick maxima for the renderer's exact empty-space skip (render.cu):
+  // [bmax_cap][bmax_nsb][kMaxC] sub-brick maxima, then [bmax_cap][kMaxC]
+  // whole-brick maxima, per channel, over every stored voxel a trilinear
+  // corner can touch.  Allocated by the first zero-copy mirror; the dense
+  // leaf kernels write a leaf's brick maxima as they build it (its
+  // sub-brick maxima become "unknown", 0xFFFF), so a live stream's refresh
+  // re-reads only the bricks written by other kernels.  bmax_ver[s]: the
+  // data_version at which slot s's maxima were last made valid.
+  uint16_t* d_bmax = nullptr;
+  int64_t bmax_cap = 0;
+  int bmax_nsb = 0;
+  std::vector<int64_t> bmax_ver;
+  uint16_t* bmax_brick() const {
+    return d_bmax ? d_bmax + bmax_cap * bmax_nsb * kMaxC : nullptr;
+  }
+  void enable_bmax(int nsb);
+  void leaves_bmax_valid(const std::vector<DenseJob>& djobs) {
+    for (const DenseJob& jd : djobs)
+      if (jd.slot >= 0 && (size_t)jd.slot < bmax_ver.size()) bmax_ver[jd.slot] = data_version;
+  }
   // tau == 0 dense build (dense_build.cu): complete[n] = every in-volume leaf
   // under n was fully covered by one dense insertion, so n's brick is a pure
   // function of the data; VT_DENSE=0 disables the path (A/B testing)
@@ -303,6 +323,28 @@ struct Tree {
     }
     return m;
   }
+  // take every queued event without expanding replayed lists: returns the
+  // event count, appends the NODE_DELETED indices (in order) to `deleted`
+  int64_t discard_events(std::vector<int64_t>& deleted) {
+    int64_t m = 0;
+    for (EvChunk& c : ev_q) {
+      const int64_t L = (int64_t)c.list->size(), left = c.left();
+      m += left;
+      bool any = false;  // replayed lists are UPDATED runs: usually no deletions
+      for (int64_t k = 0; k < L && !any; ++k) any = ev_kind((*c.list)[k]) == VT_EV_DELETED;
+      if (!any) continue;
+      for (int64_t k = 0; k < left; ++k) {
+        const uint64_t e = (*c.list)[(c.done + k) % L];
+        if (ev_kind(e) == VT_EV_DELETED) deleted.push_back(ev_index(e));
+      }
+    }
+    ev_q.clear();
+    for (uint64_t e : events)
+      if (ev_kind(e) == VT_EV_DELETED) deleted.push_back(ev_index(e));
+    m += (int64_t)events.size();
+    events.clear();
+    return m;
+  }
   // copy queued events [from, from + n) (oldest = 0) without taking them
   void copy_events(int64_t from, int64_t n, int32_t* kinds, int64_t* indices) const {
     int64_t pos = 0, m = 0;
@@ -456,7 +498,7 @@ void launch_octant(const Tree& t, const OctJob* d_jobs, int n);
 // dense_build.cu
 // returns kLeafPrefilled (shells prefilled) | kLeafTma (TMA kernel: fused
 // parent octants of jobs with pad >= 0 written too)
-constexpr int kLeafPrefilled = 1, kLeafTma = 2;
+constexpr int kLeafPrefilled = 1, kLeafTma = 2, kLeafBmax = 4;  // kLeafBmax: brick maxima written
 int launch_dense_leaf(const Tree& t, const void* src, int64_t nsrc, int oz, int prefill,
                       const DenseJob* jobs, int n, const int gn[3], int g0z);
 // planar (c, z, y, x) source through a 4-D TMA tensor map; -1 = unsupported
@@ -468,6 +510,9 @@ int launch_dense_leaf_planar(const Tree& t, const void* base, int64_t zstride, i
 void launch_planar_to_interleaved(const Tree& t, const void* base, int64_t zstride,
                                   int64_t cstride, int dz, void* dst);
 void launch_fill_bg(const Tree& t, void* dst, int64_t n);
+// background into n planes of `plane` samples at base + idx[k] * plane
+constexpr int kMaxFillPlanes = 128;
+void launch_fill_planes(const Tree& t, void* base, int64_t plane, const int32_t* idx, int n);
 // fused level-1 parents: accumulators before / statistics after the leaf kernel
 void launch_init_fused(const Tree& t, const int64_t* d_nodes, int n);
 // channel `c` of an n-voxel single-channel block into an interleaved buffer
@@ -477,7 +522,10 @@ void launch_finish_fused(const Tree& t, const int64_t* d_nodes, int n);
 void launch_plane_copy(const Tree& t, const int32_t* d_jobs, int n);
 // every shell voxel of the given bricks <- background
 void launch_clear_shells(const Tree& t, const int32_t* d_slots, int n);
-void launch_dense_level(const Tree& t, const int64_t* nodes, int n, int zsplit);
+// smem: every node has 8 full in-volume bricked children (the shared-memory
+// kernel, when level_smem_ok); else the general dense level kernel
+void launch_dense_level(const Tree& t, const int64_t* nodes, int n, int zsplit, bool smem = false);
+bool level_smem_ok(const Tree& t);
 // CTAs per parent for a dense level of n parents (> 1: statistics by k_reduce)
 int dense_level_split(const Tree& t, int n);
 void launch_plane(const Tree& t, const PlaneJob* d_jobs, int n);

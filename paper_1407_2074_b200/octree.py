@@ -629,6 +629,12 @@ class Octree:
         h = getattr(stream, "cuda_stream", stream)
         _lib.call("vt_tree_set_stream", self._h, ct.c_void_p(int(h)))
 
+    def flush(self) -> None:
+        """B200 extension: enqueue deferred device work (an open slice
+        layer's received planes, pending propagation) without a host wait."""
+        with self.lock:
+            _lib.call("vt_tree_flush", self._h)
+
     def sync(self) -> None:
         """Complete deferred device work (tau == 0 batches)."""
         _lib.call("vt_tree_sync", self._h)

@@ -399,3 +399,32 @@ def test_uploaded_entry_valid_before_next_pass():
     node = tree.node_by_index(9)
     assert np.array_equal(dev.brick_buffer[entry.slot].cpu().numpy(),
                           tree.store.read_brick(node.brick))
+
+
+# -- resident_all refresh consumes events in the library (vt_mirror_apply_queued) --
+
+def test_resident_all_refresh_equals_drain_and_apply():
+    """DeviceState.refresh() on a zero-copy mirror == apply_events(
+    drain_events()): same node buffer, deleted nodes' feedback flags
+    cleared, and the queue is empty afterwards (device.py:205-237)."""
+    from paper_1407_2074_b200.device import FLAG_REQUESTED, FLAG_USED, DeviceState
+    trees = []
+    for _ in range(2):
+        t = make_tree(r2.events_tree())
+        trees.append((t, DeviceState(t, resident_all=True)))
+    for step, (origin, block) in enumerate(r2.events_ops()):
+        for t, dev in trees:
+            fb = dev.flag_buffer
+            fb[:] = FLAG_USED | FLAG_REQUESTED  # every node flagged
+            t.insert_block(0, origin, block)
+        (ta, da), (tb, db) = trees
+        evs = tb.drain_events()
+        db.apply_events(evs)
+        n = da.refresh()
+        assert n == len(evs), step
+        assert len(ta.drain_events()) == 0
+        assert node_sha(da) == node_sha(db), step
+        fa, fbb = da.read_flags(), db.read_flags()
+        assert np.array_equal(fa, fbb), step
+        deleted = [int(e.node_index) for e in evs if int(e.kind) == 2]
+        assert all(fa[i] == 0 for i in deleted), step
