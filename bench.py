@@ -347,7 +347,7 @@ def leg_stream_interleaved(P, dims, stream, viewport, every_z, precision):
     dev = DeviceState(tree, resident_all=True)
     rr = R.OutOfCoreRenderer(dev)
     scene = scene_for(R, dims, viewport, precision=precision)
-    ins, ref, fr, slots = [], [], [], []
+    ins, fl, ref, fr, slots, nev = [], [], [], [], [], []
     torch.cuda.synchronize()
     with _Ev(stream) as tot:
         for z0 in range(0, Z, every_z):
@@ -355,32 +355,43 @@ def leg_stream_interleaved(P, dims, stream, viewport, every_z, precision):
             with _Ev(stream) as e1:
                 tree.insert_planar(P[:, z0:z1], z0)
             with _Ev(stream) as e2:
-                dev.refresh()
+                tree.flush()
             with _Ev(stream) as e3:
+                nev.append(dev.refresh())
+            with _Ev(stream) as e4:
                 img, cnt = rr.render_fullframe(scene, out_kind=R.raycast.OUT_RGBA8)
             ins.append(e1)
-            ref.append(e2)
-            fr.append((e3, cnt.samples))
+            fl.append(e2)
+            ref.append(e3)
+            fr.append((e4, cnt.samples))
             slots.append(dev.bmax_stats()[1])
         tree.finalize()
         tree.fill_borders()
         tree.sync()
     torch.cuda.synchronize()
     ins_ms = [e.ms() for e in ins]
+    fl_ms = [e.ms() for e in fl]
     ref_ms = [e.ms() for e in ref]
     fr_ms = [e.ms() for e, _ in fr]
     out = {"every_z": every_z, "frames": len(fr_ms),
            "total_ms": round(tot.ms(), 2),
            "ingest_ms": round(sum(ins_ms), 2),
+           "tree_flush_ms_mean": round(statistics.mean(fl_ms), 3),
+           "tree_flush_ms_max": round(max(fl_ms), 3),
            "mirror_refresh_ms_mean": round(statistics.mean(ref_ms), 3),
            "mirror_refresh_ms_max": round(max(ref_ms), 3),
+           "events_per_refresh_mean": int(statistics.mean(nev)),
            "bmax_slots_per_refresh_mean": int(statistics.mean(slots)),
            "frame_ms_mean": round(statistics.mean(fr_ms), 3),
            "frame_ms_max": round(max(fr_ms), 3),
            "samples_last_frame": int(fr[-1][1]),
-           "note": "refresh = drain events + node-buffer repack + brick maxima of the slots "
-                   "written since the last frame (flushing any partial brick layer); frame = "
-                   "render kernel + RGBA8 copy-out"}
+           "note": "tree flush = the open brick layer's received planes built by the leaf "
+                   "kernel + pyramid propagation of everything inserted since the last frame "
+                   "(what any reader of the tree pays, octree.py:323-397 leaves the tree complete "
+                   "after every insert_block); mirror refresh = apply the queued change events "
+                   "(DeviceState.refresh, in-library), node-buffer repack, brick maxima of the "
+                   "slots not written by the leaf kernel; frame = render kernel + RGBA8 "
+                   "copy-out"}
     dev.close()
     return out, tree
 

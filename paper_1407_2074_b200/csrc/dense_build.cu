@@ -785,7 +785,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma_planar(
     const DenseJob* __restrict__ jobs, int gnx, int gny, int g0z, Geo g,
     uint16_t* __restrict__ pool, int32_t* stats, int32_t* nmin, int32_t* nmax,
     unsigned long long* nsum, uint16_t* __restrict__ bmax_sub, uint16_t* __restrict__ bmax_brick,
-    int nsb) {
+    int nsb, uint8_t* __restrict__ dflags, int32_t* __restrict__ dslot) {
   constexpr int P = kTmaP;
   constexpr int WPP = kTmaWarps / P;  // warps per plane
   constexpr int NT = WPP * 32;        // threads per plane
@@ -820,6 +820,10 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma_planar(
   if (tid == 0) {
     for (int b = 0; b < kPStages; ++b) mbar_init(&s_bar[b], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (dflags) {  // structure mirror of this in-volume leaf (held pairs)
+      dflags[j.node] = NF_EXISTS | NF_INVOL | NF_BRICK;
+      dslot[j.node] = j.slot;
+    }
   }
   __syncthreads();
 
@@ -1554,7 +1558,7 @@ static bool encode_planar_map(const Tree& t, const void* base, int64_t zstride, 
 template <int C>
 static int leaf_launch_planar(const Tree& t, const void* base, int64_t zstride, int64_t cstride,
                               int oz, int64_t dz, int prefill, const DenseJob* jobs, int n,
-                              const int gn[3], int g0z) {
+                              const int gn[3], int g0z, bool write_struct) {
   CUtensorMap map;
   if (!encode_planar_map(t, base, zstride, cstride, dz, &map)) return -1;
   const size_t smem = tma_smem_planar(t.g);
@@ -1564,21 +1568,23 @@ static int leaf_launch_planar(const Tree& t, const void* base, int64_t zstride, 
   uint16_t* bb = t.bmax_brick();
   k<<<n, kTmaWarps * 32, smem, t.stream>>>(map, oz, (int)dz, prefill, jobs, gn[0], gn[1], g0z, t.g,
                                           (uint16_t*)t.d_pool, t.d_stats, t.d_nmin, t.d_nmax,
-                                          t.d_nsum, t.d_bmax, bb, t.bmax_nsb);
+                                          t.d_nsum, t.d_bmax, bb, t.bmax_nsb,
+                                          write_struct ? t.d_flags : nullptr,
+                                          write_struct ? t.d_slot : nullptr);
   VT_CHECK_LAUNCH();
   return kLeafTma | (prefill ? kLeafPrefilled : 0) | (bb ? kLeafBmax : 0);
 }
 
 int launch_dense_leaf_planar(const Tree& t, const void* base, int64_t zstride, int64_t cstride,
                              int oz, int64_t dz, int prefill, const DenseJob* jobs, int n,
-                             const int gn[3], int g0z) {
+                             const int gn[3], int g0z, bool ws) {
   if (n <= 0) return 0;
   if (!planar_leaf_ok(t, base, zstride, cstride)) return -1;
   switch (t.g.C) {
-    case 1: return leaf_launch_planar<1>(t, base, zstride, cstride, oz, dz, prefill, jobs, n, gn, g0z);
-    case 2: return leaf_launch_planar<2>(t, base, zstride, cstride, oz, dz, prefill, jobs, n, gn, g0z);
-    case 3: return leaf_launch_planar<3>(t, base, zstride, cstride, oz, dz, prefill, jobs, n, gn, g0z);
-    default: return leaf_launch_planar<4>(t, base, zstride, cstride, oz, dz, prefill, jobs, n, gn, g0z);
+    case 1: return leaf_launch_planar<1>(t, base, zstride, cstride, oz, dz, prefill, jobs, n, gn, g0z, ws);
+    case 2: return leaf_launch_planar<2>(t, base, zstride, cstride, oz, dz, prefill, jobs, n, gn, g0z, ws);
+    case 3: return leaf_launch_planar<3>(t, base, zstride, cstride, oz, dz, prefill, jobs, n, gn, g0z, ws);
+    default: return leaf_launch_planar<4>(t, base, zstride, cstride, oz, dz, prefill, jobs, n, gn, g0z, ws);
   }
 }
 

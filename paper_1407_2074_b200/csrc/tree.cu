@@ -375,6 +375,7 @@ void sort_indices(std::vector<int64_t>& v) {
 }
 
 void Tree::mark_struct(int64_t idx) {
+  if (leaf_struct_by_kernel && idx >= g.level_start[g.depth] && (flags[idx] & NF_INVOL)) return;
   if (!struct_mark[idx]) {
     struct_mark[idx] = 1;
     struct_dirty.push_back(idx);
@@ -796,6 +797,7 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
         int gg[3] = {gx, gy, gz};
         const int64_t idx = leaf_index(gx, gy, gz);
         if (!(flags[idx] & NF_EXISTS)) {
+          ProfScope qc(prof, 31);
           // create the missing part of the chain, top down (creation order
           // and seeds exactly as the reference's descent)
           int64_t a = 0;
@@ -867,20 +869,34 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
   }
   delete leaf_scope;
   auto* anc_scope = new ProfScope(prof, 9);
+  // a dense block of one whole brick layer over the full x/y extent (slice
+  // streams): its ancestors at level l are every level-l node of row z
+  // g0z >> l, listed in closed form (Morton code = BFS offset in a level)
+  const bool fullxy = dense && g.split[0] && g.split[1] && g.split[2] && origin[0] == 0 &&
+                      origin[1] == 0 && dims[0] == g.dims[0] && dims[1] == g.dims[1] &&
+                      g0[2] == g1[2];
   // ancestors (octree.py:363-387): ensure parent bricks, record freshness
   for (int lvl = 1; lvl <= g.depth; ++lvl) {
     std::vector<int64_t>& par = touched[lvl];
     ++anc_gen;
     {
       ProfScope qa(prof, 13);
-      for (int64_t c : touched[lvl - 1]) {
-        const int64_t q = (c - 1) >> 3;
-        if (anc_mark[q] != anc_gen) {
-          anc_mark[q] = anc_gen;
-          par.push_back(q);
+      if (fullxy) {
+        const int64_t base = g.level_start[g.depth - lvl];
+        const int64_t mz = morton[2][g0[2] >> lvl];
+        for (int y = 0; y <= (g1[1] >> lvl); ++y)
+          for (int x = 0; x <= (g1[0] >> lvl); ++x) par.push_back(base + morton[0][x] + morton[1][y] + mz);
+        sort_indices(par);
+      } else {
+        for (int64_t c : touched[lvl - 1]) {
+          const int64_t q = (c - 1) >> 3;
+          if (anc_mark[q] != anc_gen) {
+            anc_mark[q] = anc_gen;
+            par.push_back(q);
+          }
         }
+        std::sort(par.begin(), par.end());
       }
-      std::sort(par.begin(), par.end());
     }
     ProfScope qb(prof, 14);
     for (int64_t p : par) {
@@ -906,7 +922,9 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
                  "dense build: parent slot order diverged from the precomputed one");
     for (int64_t p : fused_nodes) fused1[p] = 1;
   }
-  if (dense && !early && g.depth >= 1 && g.split[0] && g.split[1] && g.split[2]) {
+  // (a held layer's parents are fused by launch_held, over both layers)
+  if (dense && !early && !hold_dense && g.depth >= 1 && g.split[0] && g.split[1] && g.split[2]) {
+    ProfScope qfs(prof, 33);
     for (int64_t p : touched[1]) {
       bool ok = true;
       int64_t pos[8];
@@ -950,15 +968,28 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
             cgz <= g1[2])
           sorted_leaves.push_back(8 * q1.idx + 1 + k);
       }
+    if (fullxy && early_par.empty() && g.depth >= 1) {
+      // the layer's leaves in BFS order: the in-volume children of the
+      // sorted level-1 parents on this layer's side of the z split
+      const int zb = g0[2] & 1;
+      for (int64_t p : touched[1])
+        for (int k = zb << 2; k < (zb << 2) + 4; ++k) {
+          const int64_t c = 8 * p + 1 + k;
+          if ((flags[c] & (NF_EXISTS | NF_INVOL)) == (NF_EXISTS | NF_INVOL)) sorted_leaves.push_back(c);
+        }
+    }
     if (!sorted_leaves.empty() && sorted_leaves.size() == touched[0].size())
       touched[0].swap(sorted_leaves);  // the same set, already ordered
     else
       sort_indices(touched[0]);
   }
   has_pending = true;
-  for (const auto& lv : touched)
-    for (int64_t n : lv)
-      if (flags[n] & NF_BRICK) touch_slot(slot[n]);
+  {
+    ProfScope qt(prof, 34);
+    for (const auto& lv : touched)
+      for (int64_t n : lv)
+        if (flags[n] & NF_BRICK) touch_slot(slot[n]);
+  }
   delete anc_scope;
   delete walk_scope;
   ProfScope enq_scope(prof, 2);
@@ -1164,8 +1195,30 @@ void Tree::dense_after_launch(int lr, const std::vector<DenseJob>& djobs,
   if (lr & kLeafBmax) leaves_bmax_valid(djobs);
   ++dense_leaf_inserts;
   if (prefilled) {
+    ProfScope qo(prof, 36);
     // z-shell planes whose block plane lies outside this insertion are owed
+    // to the z-neighbour's leaf; one whose neighbour is already built (a
+    // slice stream's previous layer, or this launch for an earlier owed
+    // entry) is copied right away — the plane fill_borders' fast path would
+    // copy, logically background until then like every prefilled shell
     halo_prefill = true;
+    const int mz = M[2];
+    std::vector<int32_t> pj;
+    auto built = [&](int64_t nb) { return (flags[nb] & NF_BRICK) && complete[nb]; };
+    const bool eager = prefill_valid;
+    if (eager) {
+      for (auto* v : {&owed_lo, &owed_hi}) {
+        const bool lo = v == &owed_lo;
+        size_t w = 0;
+        for (const Owed& o : *v) {
+          if (built(o.nb))
+            pj.insert(pj.end(), {slot[o.leaf], lo ? 0 : mz + 1, slot[o.nb], lo ? mz : 1});
+          else
+            (*v)[w++] = o;
+        }
+        v->resize(w);
+      }
+    }
     const int gx1 = (g.dims[0] - 1) / M[0], gy1 = (g.dims[1] - 1) / M[1];
     for (int gz = gz0; gz <= gz1; ++gz) {
       const int lo = gz * M[2] - 1, hi = (gz + 1) * M[2];
@@ -1175,9 +1228,22 @@ void Tree::dense_after_launch(int lr, const std::vector<DenseJob>& djobs,
         for (int gx = 0; gx <= gx1; ++gx) {
           const int64_t idx = leaf_index(gx, gy, gz);
           if (!(flags[idx] & NF_BRICK) || !complete[idx]) continue;
-          if (olo) owed_lo.push_back({idx, leaf_index(gx, gy, gz - 1)});
-          if (ohi) owed_hi.push_back({idx, leaf_index(gx, gy, gz + 1)});
+          if (olo) {
+            const int64_t nb = leaf_index(gx, gy, gz - 1);
+            if (eager && built(nb)) pj.insert(pj.end(), {slot[idx], 0, slot[nb], mz});
+            else owed_lo.push_back({idx, nb});
+          }
+          if (ohi) {
+            const int64_t nb = leaf_index(gx, gy, gz + 1);
+            if (eager && built(nb)) pj.insert(pj.end(), {slot[idx], mz + 1, slot[nb], 1});
+            else owed_hi.push_back({idx, nb});
+          }
         }
+    }
+    if (!pj.empty()) {
+      int32_t* dp = upload(*this, pj);
+      launch_plane_copy(*this, dp, (int)(pj.size() / 4));
+      release(*this, dp);
     }
   } else {
     prefill_valid = false;
@@ -1188,6 +1254,7 @@ void Tree::dense_after_launch(int lr, const std::vector<DenseJob>& djobs,
 // level-1 parents whose eight children are all in the pair fused
 void Tree::launch_held() {
   if (!held.active) return;
+  ProfScope qh(prof, 35);
   held.active = false;
   const int* M = g.brick;
   const int gnx = (g.dims[0] - 1) / M[0] + 1, gny = (g.dims[1] - 1) / M[1] + 1;
@@ -1229,8 +1296,26 @@ void Tree::launch_held() {
   const bool want = prefill_enabled && !borders;
   const int gn[3] = {gnx, gny, nl};
   const int64_t nvox = (int64_t)g.dims[0] * g.dims[1] * held.nz;
-  const int lr = leaf_launch(planar.base, nvox * g.C, held.z0, held.nz, want ? 1 : 0, d,
-                             (int)dj.size(), gn, held.gz0);
+  int lr;
+  if (leaf_struct_by_kernel) {
+    // the walks left the leaves' device flags / slots to this kernel
+    lr = launch_dense_leaf_planar(*this, planar.base, planar.zstride, planar.cstride, held.z0,
+                                  held.nz, want ? 1 : 0, d, (int)dj.size(), gn, held.gz0, true);
+    if (lr < 0) {
+      // no tensor-map encoder after all: the records the walks skipped
+      std::vector<StructUpd> upd;
+      upd.reserve(dj.size());
+      for (const DenseJob& jd : dj) upd.push_back({jd.node, flags[jd.node], slot[jd.node]});
+      StructUpd* du = upload(*this, upd);
+      launch_struct_update(*this, du, (int)upd.size());
+      release(*this, du);
+      lr = leaf_launch(planar.base, nvox * g.C, held.z0, held.nz, want ? 1 : 0, d,
+                       (int)dj.size(), gn, held.gz0);
+    }
+  } else {
+    lr = leaf_launch(planar.base, nvox * g.C, held.z0, held.nz, want ? 1 : 0, d, (int)dj.size(),
+                     gn, held.gz0);
+  }
   release(*this, d);
   dense_after_launch(lr, dj, fused_nodes, held.z0, held.z0 + held.nz, held.gz0, held.gz1,
                      nullptr);
@@ -1545,17 +1630,20 @@ void Tree::insert_many(int64_t n, const vt_block* blocks, int mem_kind) {
     const int z1 = z0 + M[2], nz1 = std::min(M[2], g.dims[2] - z1);
     const int o1[3] = {0, 0, z1}, d1[3] = {g.dims[0], g.dims[1], nz1};
     hold_dense = true;
+    leaf_struct_by_kernel = true;
     try {
       insert_staged(-1, o, d, a.base, g.C, 0, g.C, len);
       insert_staged(-1, o1, d1, b.base, g.C, 0, g.C, len2);
     } catch (...) {
       hold_dense = false;
       launch_held();  // whatever was walked must be built
+      leaf_struct_by_kernel = false;
       planar = PlanarSrc{};
       throw;
     }
     hold_dense = false;
     launch_held();
+    leaf_struct_by_kernel = false;
     planar = PlanarSrc{};
     layer_groups += 2;
     zero_copy_layers += 1;

@@ -57,7 +57,7 @@ struct Pending {
 // tree is destroyed
 struct HostProf {
   bool on = false;
-  static constexpr int kN = 31;
+  static constexpr int kN = 37;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // insert entry, leaf launch, leaf end, insert end
   bool ev_armed = false;
   double t[kN] = {0};
@@ -68,7 +68,8 @@ struct HostProf {
                                 "dense_book", "updated_ev", "defer", "pool",
                                 "gpu_entry_to_leaf", "gpu_leaf", "gpu_leaf_to_end",
                                 "eligible", "pre_parents", "pre_anc", "pre_djobs",
-                                "pre_pads", "pre_fused_up", "pre_djob_up", "pre_leaf_launch"};
+                                "pre_pads", "pre_fused_up", "pre_djob_up", "pre_leaf_launch",
+                                "chain", "leaf_brick", "fused_scan", "touch", "held", "owed"};
     return n[i];
   }
 };
@@ -225,6 +226,9 @@ struct Tree {
     int z0 = 0, nz = 0, gz0 = 0, gz1 = 0;
   } held;
   bool hold_dense = false;
+  // while a pair is walked: in-volume leaves get no per-node structure
+  // record — the pair's leaf kernel writes their device flags and slots
+  bool leaf_struct_by_kernel = false;
   void launch_held();
   // bookkeeping after a dense leaf launch over leaves `djobs` of the block
   // z in [z0, z1), layers [gz0, gz1]
@@ -506,7 +510,7 @@ int launch_dense_leaf(const Tree& t, const void* src, int64_t nsrc, int oz, int 
 bool planar_leaf_ok(const Tree& t, const void* base, int64_t zstride, int64_t cstride);
 int launch_dense_leaf_planar(const Tree& t, const void* base, int64_t zstride, int64_t cstride,
                              int oz, int64_t dz, int prefill, const DenseJob* jobs, int n,
-                             const int gn[3], int g0z);
+                             const int gn[3], int g0z, bool write_struct = false);
 void launch_planar_to_interleaved(const Tree& t, const void* base, int64_t zstride,
                                   int64_t cstride, int dz, void* dst);
 void launch_fill_bg(const Tree& t, void* dst, int64_t n);
