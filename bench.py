@@ -287,7 +287,7 @@ def leg_stream(P, dims, stream, peak):
     cfg = BrickPoolConfig(brick_dims=(BRICK,) * 3, homogeneity_threshold=0)
     Z = dims[2]
     raw = dims[0] * dims[1] * Z * CHANNELS * 2
-    res = None
+    res, runs = None, []
     for rep in range(3):  # warm-up, then two timed runs (best reported, both listed)
         tree = Octree(desc, cfg, reserve_slots=expected_bricks(dims, BRICK))
         _lib.call("vt_tree_set_stream", tree.handle, ct.c_void_p(stream.cuda_stream))
@@ -324,7 +324,8 @@ def leg_stream(P, dims, stream, peak):
                                 "model": "(raw + pool bytes) / stream time (SURVEY 8d: "
                                          "1 + pool/raw B per raw byte)"},
                    "tree_checksum": f"{tree.checksum():016x}"}
-        res.setdefault("runs_ms", []).append(round(ms, 3))
+        runs.append(round(ms, 3))
+        res["runs_ms"] = list(runs)
         tree.close()
         del tree
         torch.cuda.empty_cache()

@@ -1034,7 +1034,11 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
       for (const SeedJob& sj : seeds) (g.level_of(sj.node) == 0 ? dl.seeds : now).push_back(sj);
       seeds.swap(now);
     }
-    if (early && prefill_enabled && !borders) {
+    // fresh ancestors of an early launch or a held pair: their interior is
+    // rewritten whole by propagation and fill_borders overwrites every shell
+    // voxel, so the background shell is owed (publish_halos writes it for an
+    // earlier reader) instead of written
+    if ((early || hold_dense) && prefill_enabled && !borders) {
       size_t w = 0;
       for (const SeedJob& sj : seeds) {
         bool full = g.level_of(sj.node) > 0;
@@ -1173,7 +1177,8 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
 
 void Tree::dense_after_launch(int lr, const std::vector<DenseJob>& djobs,
                               const std::vector<int64_t>& fused_nodes, int z0, int z1, int gz0,
-                              int gz1, const std::vector<int64_t>* sorted_leaves) {
+                              int gz1, const std::vector<int64_t>* sorted_leaves,
+                              bool pend_leaves) {
   const int* M = g.brick;
   const bool prefilled = lr & kLeafPrefilled;
   if (!(lr & kLeafTma)) {
@@ -1186,11 +1191,13 @@ void Tree::dense_after_launch(int lr, const std::vector<DenseJob>& djobs,
   // whose statistics the kernel writes outright (djobs are in (gz, gy, gx)
   // order; propagate sorts its lists)
   ProfScope qd(prof, 16);
-  pend_nodes[0].reserve(pend_nodes[0].size() + djobs.size());
-  if (sorted_leaves)
-    for (int64_t n : *sorted_leaves) pend_dense(n);  // BFS order: propagate needs no sort
-  else
-    for (const DenseJob& jd : djobs) pend_dense(jd.node);
+  if (pend_leaves) {
+    pend_nodes[0].reserve(pend_nodes[0].size() + djobs.size());
+    if (sorted_leaves)
+      for (int64_t n : *sorted_leaves) pend_dense(n);  // BFS order: propagate needs no sort
+    else
+      for (const DenseJob& jd : djobs) pend_dense(jd.node);
+  }
   for (const DenseJob& jd : djobs) complete[jd.node] = 1;
   if (lr & kLeafBmax) leaves_bmax_valid(djobs);
   ++dense_leaf_inserts;
@@ -1317,8 +1324,19 @@ void Tree::launch_held() {
                      gn, held.gz0);
   }
   release(*this, d);
+  // No pending entries for the pair's leaves: their statistics are final
+  // and every level-1 parent over them is fresh (all octants) or dense
+  // (recomputed whole from complete children), so propagate never needs
+  // them as dirty children; a later general touch of a leaf opens its own
+  // entry (and pinv makes it recompute every plane partial).
+  bool parents_fresh = true;
+  for (int64_t i = 0; i < (int64_t)dj.size() && parents_fresh; ++i) {
+    const int64_t p = (dj[i].node - 1) >> 3;
+    const Pending* pp = pend_find(p, 1);
+    parents_fresh = pp && pp->fresh;
+  }
   dense_after_launch(lr, dj, fused_nodes, held.z0, held.z0 + held.nz, held.gz0, held.gz1,
-                     nullptr);
+                     nullptr, !parents_fresh);
   dj.clear();
 }
 

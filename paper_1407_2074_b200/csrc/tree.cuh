@@ -234,7 +234,8 @@ struct Tree {
   // z in [z0, z1), layers [gz0, gz1]
   void dense_after_launch(int lr, const std::vector<DenseJob>& djobs,
                           const std::vector<int64_t>& fused_nodes, int z0, int z1, int gz0,
-                          int gz1, const std::vector<int64_t>* sorted_leaves);
+                          int gz1, const std::vector<int64_t>* sorted_leaves,
+                          bool pend_leaves = true);
   // B200 batched insertion: same tree and queued events as n successive
   // insert() calls; whole brick layers of single-channel full-x/y blocks
   // become one dense insertion
