@@ -12,7 +12,8 @@ import ctypes as ct
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libvtx.so")
+# VT_LIB: an alternate build of the same library (A/B measurements only)
+LIB_PATH = os.environ.get("VT_LIB") or os.path.join(HERE, "libvtx.so")
 
 VT_OK, VT_EINVAL, VT_EOVERFLOW, VT_ENOMEM, VT_ECUDA, VT_ESTATE, VT_EIO = range(7)
 VT_MEM_HOST, VT_MEM_DEVICE = 0, 1

@@ -72,6 +72,7 @@ struct RenderParams {
   double tf_xzero[kMaxC];                   // alpha == 0 on [0, xzero]
   double inv_fmax;
   double inv_scl[kMaxLevels][3];  // exact: scales are powers of two
+  int exti[kMaxLevels][3];        // node extents in voxels; 1 << 30 on unsplit axes
   int unit_spacing;               // spacing == (1, 1, 1): p / spacing == p
   int base_pow2;                  // base_voxel a power of two: exact reciprocal
   double inv_base;
@@ -270,16 +271,17 @@ __device__ __forceinline__ void interp4(const TFTable& T, int c, float x, float 
   }
 }
 
+// the node a sample last resolved to, per channel group: a sample inside
+// its box at the same target level reuses it.  Node boxes have integral
+// voxel origins, and pv >= 0 on the sampling path, so the box test is an
+// integer compare of floor(pv).  The full-frame fallback's ancestors are
+// re-derived only when a sample needs them (ancestors()).
 struct DescentCache {
-  int target;
-  int clear;  // the node is transparent for the scene (empty-space skip)
+  int target;  // -1: empty
+  int clear;   // the node is transparent for the scene (empty-space skip)
   int lvl;
-  long long idx;
-  double lo[3];
-  double hi[3];  // lo + node extent on split axes, +inf on the others
-  long long a_idx[2];
-  int a_lvl[2];
-  int a_lo[2][3];  // ancestor box origins (integral voxel coordinates)
+  int idx;     // BFS node index (< 2^31: a depth-8 tree has 19.2M nodes)
+  int lo[3];   // box origin; the box is [lo, lo + exti[lvl])
 };
 
 // floor(log2(v)) for a positive normal double: its unbiased exponent
@@ -291,7 +293,9 @@ __device__ __forceinline__ int floor_log2(double v) {
 // FAST: sample reconstruction (trilinear) and transfer functions in FP32 —
 // the north-star's "float accumulation" model; positions, LOD, descent and
 // compositing stay FP64
-template <class T, int NC, bool TR, bool FAST = false>
+// FILLED: 1 / 0 = borders filled / not known at compile time (the full-frame
+// kernel is instantiated for both), -1 = read P.borders_filled
+template <class T, int NC, bool TR, bool FAST = false, int FILLED = -1>
 struct Sampler {
   using V = typename std::conditional<FAST, float, double>::type;
   static constexpr int kC = NC;
@@ -300,12 +304,13 @@ struct Sampler {
   const T* __restrict__ bb;
   bool fullframe;
   Counters cnt;  // by value: stays in registers
-  long long last_used = -1, last_req = -1;
+  int last_used = -1, last_req = -1;
   // the last sample resolved to a node that is transparent for the scene's
-  // transfer functions: 1 resident brick (sub-brick), 2 homogeneous (AVG)
-  // node; box_lo/box_hi: the voxel-space box that stays transparent
+  // transfer functions: 1 resident brick (or sub-brick), 2 homogeneous
+  // (AVG) node; the transparent box is cache[0]'s node box, or its
+  // sub-brick hint_sb (x | y << 8 | z << 16) when >= 0
   int hint = 0;
-  double box_lo[3], box_hi[3];
+  int hint_sb = -1;
   DescentCache cache[TR ? NC : 1];
 
   __device__ Sampler(const uint64_t* n, uint8_t* f, const T* b, bool ff)
@@ -319,11 +324,11 @@ struct Sampler {
 
   // feedback flag: idempotent OR into the byte of the node (device.py:35-36,
   // raycast.py:161-163); skipped when this thread already marked the node
-  __device__ void mark(long long idx, unsigned flag) {
-    long long& last = flag == 1 ? last_used : last_req;
+  __device__ void mark(int idx, unsigned flag) {
+    int& last = flag == 1 ? last_used : last_req;
     if (last == idx) return;
     last = idx;
-    unsigned* w = reinterpret_cast<unsigned*>(fb + (idx & ~3LL));
+    unsigned* w = reinterpret_cast<unsigned*>(fb + (idx & ~3));
     unsigned bit = flag << ((idx & 3) * 8);
     if (!(__ldcg(w) & bit)) atomicOr(w, bit);
   }
@@ -335,16 +340,16 @@ struct Sampler {
 
   // _trilerp (raycast.py:133-159) for channels [c0, c1): cell index and
   // weights once per sample, then the 8 corners of every channel
-  __device__ void trilerp(uint64_t e, int lvl, const double lo[3], const double pv[3], int c0,
+  __device__ void trilerp(uint64_t e, int lvl, const int lo[3], const double pv[3], int c0,
                           int c1, V* out, int* cell = nullptr) const {
     const long long slot = (long long)((e >> 24) & 0xFFFFFFFFULL);
     int i0[3];
     double w1[3];
-    const bool filled = P.borders_filled;
+    const bool filled = FILLED < 0 ? P.borders_filled != 0 : FILLED != 0;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       // scale is a power of two: multiplying by its reciprocal is exact
-      double f = (pv[a] - lo[a]) * P.inv_scl[lvl][a] + 0.5;
+      double f = (pv[a] - (double)lo[a]) * P.inv_scl[lvl][a] + 0.5;
       // inside the node box f is in [0.5, M + 0.5): with filled borders the
       // reference's clip to [0, M + 1] and the index clip to [0, M] are
       // no-ops; before fill_borders samples clamp to interior centres
@@ -400,42 +405,30 @@ struct Sampler {
   // stays inside the cached node box at the same target level reuses it
   // returns true when it re-descended (a different node than the cached one)
   __device__ bool descend(const double pv[3], int target, DescentCache& dc) {
+    int ip[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) ip[a] = (int)pv[a];  // floor: pv >= 0
     if (dc.target == target) {
       bool ok = true;
 #pragma unroll
       for (int a = 0; a < 3; ++a)
-        ok = ok && pv[a] >= dc.lo[a] && pv[a] < dc.hi[a];
+        ok = ok && ip[a] >= dc.lo[a] && ip[a] - dc.lo[a] < P.exti[dc.lvl][a];
       if (ok) return false;
     }
-    long long idx = 0;
+    int idx = 0;
     int lvl = P.g.depth;
-    double lo[3] = {0.0, 0.0, 0.0};
-    long long a1 = -1, a2 = -1;
-    int a1l = 0, a2l = 0;
-    int a1lo[3] = {0, 0, 0}, a2lo[3] = {0, 0, 0};
+    int lo[3] = {0, 0, 0};
     for (int it = 0; it < P.g.depth; ++it) {
       uint64_t e = __ldg(nb + idx);
-      long long ptr = (long long)((e >> 2) & 0x3FFFFFULL);
+      int ptr = (int)((e >> 2) & 0x3FFFFFULL);
       if (!(ptr != 0 && lvl > target)) break;
       int k = 0;
-      double nlo[3];
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
-        double half = P.ext[lvl - 1][a];
-        bool bit = (pv[a] >= lo[a] + half) && P.g.split[a];
+        const int half = P.exti[lvl - 1][a];
+        const bool bit = ip[a] >= lo[a] + half && P.g.split[a];
         k |= bit ? (1 << a) : 0;
-        nlo[a] = lo[a] + (bit ? half : 0.0);
-      }
-      a2 = a1;
-      a2l = a1l;
-#pragma unroll
-      for (int a = 0; a < 3; ++a) a2lo[a] = a1lo[a];
-      a1 = idx;
-      a1l = lvl;
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        a1lo[a] = (int)lo[a];
-        lo[a] = nlo[a];
+        lo[a] += bit ? half : 0;
       }
       idx = 8 * (ptr - 1) + 1 + k;
       --lvl;
@@ -444,17 +437,44 @@ struct Sampler {
     dc.idx = idx;
     dc.lvl = lvl;
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      dc.lo[a] = lo[a];
-      dc.hi[a] = P.g.split[a] ? lo[a] + P.ext[lvl][a] : INFINITY;
-      dc.a_lo[0][a] = a1lo[a];
-      dc.a_lo[1][a] = a2lo[a];
-    }
-    dc.a_idx[0] = a1;
-    dc.a_idx[1] = a2;
-    dc.a_lvl[0] = a1l;
-    dc.a_lvl[1] = a2l;
+    for (int a = 0; a < 3; ++a) dc.lo[a] = lo[a];
     return true;
+  }
+
+  // the two nearest ancestors of the node at level `lvl` on pv's path (the
+  // last two nodes descend() passed through): full-frame fallback only
+  __device__ void ancestors(const double pv[3], int lvl, int aidx[2], int alvl[2],
+                            int alo[2][3]) const {
+    int ip[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) ip[a] = (int)pv[a];
+    aidx[0] = aidx[1] = -1;
+    alvl[0] = alvl[1] = 0;
+    int idx = 0, l = P.g.depth;
+    int lo[3] = {0, 0, 0};
+    while (l > lvl) {
+      const uint64_t e = __ldg(nb + idx);
+      const int ptr = (int)((e >> 2) & 0x3FFFFFULL);
+      aidx[1] = aidx[0];
+      alvl[1] = alvl[0];
+      aidx[0] = idx;
+      alvl[0] = l;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        alo[1][a] = alo[0][a];
+        alo[0][a] = lo[a];
+      }
+      int k = 0;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const int half = P.exti[l - 1][a];
+        const bool bit = ip[a] >= lo[a] + half && P.g.split[a];
+        k |= bit ? (1 << a) : 0;
+        lo[a] += bit ? half : 0;
+      }
+      idx = 8 * (ptr - 1) + 1 + k;
+      --l;
+    }
   }
 
   // transparency of the node just entered: every sample in it has TF alpha 0
@@ -472,14 +492,6 @@ struct Sampler {
 #pragma unroll
     for (int c = 0; c < NC; ++c) clear = clear && (int)__ldg(bm + c) <= P.ess_thr[c];
     return clear ? 1 : 0;
-  }
-
-  __device__ void node_box(const DescentCache& dc) {
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      box_lo[a] = P.g.split[a] ? dc.lo[a] : -INFINITY;
-      box_hi[a] = P.g.split[a] ? dc.lo[a] + P.ext[dc.lvl][a] : INFINITY;
-    }
   }
 
   // optimal_lod (raycast.py:40-50): floor(log2(.)) is the exponent of the
@@ -506,7 +518,7 @@ struct Sampler {
       if (dc.clear) {
         // transparent homogeneous node: value irrelevant, skip its samples
         hint = 2;
-        node_box(dc);
+        hint_sb = -1;
         return false;
       }
 #pragma unroll
@@ -519,7 +531,7 @@ struct Sampler {
       cnt.used++;
       if (dc.clear) {
         hint = 1;
-        node_box(dc);
+        hint_sb = -1;
         return false;
       }
       int cell[3];
@@ -541,17 +553,7 @@ struct Sampler {
         for (int c = 0; c < NC; ++c) clear = clear && (int)__ldg(sm + c) <= P.ess_thr[c];
         if (clear) {
           hint = 1;
-          // cells [sB, sB + B) <=> (pv - lo) / scale in [sB - 0.5, sB + B - 0.5)
-#pragma unroll
-          for (int a = 0; a < 3; ++a) {
-            const double sc = P.scl[dc.lvl][a];
-            const double base = dc.lo[a] - 0.5 * sc;
-            box_lo[a] = sb[a] == 0 ? (P.g.split[a] ? dc.lo[a] : -INFINITY)
-                                   : base + (double)(sb[a] * P.sbk[a]) * sc;
-            box_hi[a] = sb[a] == P.nsub[a] - 1
-                            ? (P.g.split[a] ? dc.lo[a] + P.ext[dc.lvl][a] : INFINITY)
-                            : base + (double)((sb[a] + 1) * P.sbk[a]) * sc;
-          }
+          hint_sb = sb[0] | (sb[1] << 8) | (sb[2] << 16);
         }
       }
       return false;
@@ -559,15 +561,15 @@ struct Sampler {
     mark(dc.idx, 2);
     cnt.req++;
     if (!fullframe) return true;
+    int aidx[2], alvl[2], alo[2][3];
+    ancestors(pv, dc.lvl, aidx, alvl, alo);
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
-      long long ai = dc.a_idx[q];
+      const int ai = aidx[q];
       if (ai < 0) continue;
       uint64_t ae = __ldg(nb + ai);
       if (ae & 1) {
-        const double alo[3] = {(double)dc.a_lo[q][0], (double)dc.a_lo[q][1],
-                               (double)dc.a_lo[q][2]};
-        trilerp(ae, dc.a_lvl[q], alo, pv, c0, c1, out);
+        trilerp(ae, alvl[q], alo[q], pv, c0, c1, out);
         mark(ai, 1);
         cnt.used++;
         cnt.coarse++;
@@ -601,23 +603,46 @@ struct Sampler {
   // empty-space skip; each skipped sample still counts as the reference
   // counts it).  Positions are monotone in k, so checking the last one
   // suffices; the analytic estimate is verified with the sampling code.
-  // per-ray constants of the skip estimate
-  double inv_d[3], t_lod;
-  __device__ void set_ray(const double d[3]) {
+  // the voxel-space box the hint says stays transparent
+  __device__ void hint_box(double lo[3], double hi[3]) const {
+    const DescentCache& dc = cache[0];
 #pragma unroll
-    for (int a = 0; a < 3; ++a) inv_d[a] = d[a] != 0.0 ? 1.0 / d[a] : 0.0;
-    const double df = d[0] * P.fwd[0] + d[1] * P.fwd[1] + d[2] * P.fwd[2];
-    t_lod = df > 0.0 ? P.base_voxel / (P.pfs * P.lod_scale * df) : INFINITY;
+    for (int a = 0; a < 3; ++a) {
+      const bool sp = P.g.split[a];
+      const double nlo = (double)dc.lo[a];
+      const double nhi = nlo + (double)P.exti[dc.lvl][a];
+      lo[a] = sp ? nlo : -INFINITY;
+      hi[a] = sp ? nhi : INFINITY;
+      if (hint_sb >= 0) {
+        // cells [sB, sB + B) <=> (pv - lo) / scale in [sB - 0.5, sB + B - 0.5)
+        const int sb = (hint_sb >> (8 * a)) & 0xFF;
+        const double sc = P.scl[dc.lvl][a];
+        const double base = nlo - 0.5 * sc;
+        if (sb > 0) lo[a] = base + (double)(sb * P.sbk[a]) * sc;
+        if (sb < P.nsub[a] - 1) hi[a] = base + (double)((sb + 1) * P.sbk[a]) * sc;
+      }
+    }
   }
 
+  // samples k+1 .. k+m provably resolve to the same transparent node with
+  // the same target level, inside the volume and the ray: returns m (exact
+  // empty-space skip; each skipped sample still counts as the reference
+  // counts it).  Positions are monotone in k, so checking the last one
+  // suffices; the analytic estimate is verified with the sampling code.
   __device__ long long skip_count(long long k, long long n, double t0, const double d[3]) {
     const int target = cache[0].target;
-    double tl = target < P.g.depth ? ldexp(t_lod, target + 1) : INFINITY;
+    double box_lo[3], box_hi[3];
+    hint_box(box_lo, box_hi);
+    double tl = INFINITY;
+    if (target < P.g.depth) {
+      const double df = d[0] * P.fwd[0] + d[1] * P.fwd[1] + d[2] * P.fwd[2];
+      if (df > 0.0) tl = ldexp(P.base_voxel / (P.pfs * P.lod_scale * df), target + 1);
+    }
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       const double lo = fmax(0.0, box_lo[a]), hi = fmin(P.dims[a], box_hi[a]);
-      if (d[a] > 0.0) tl = fmin(tl, (hi * P.spacing[a] - P.cam[a]) * inv_d[a]);
-      else if (d[a] < 0.0) tl = fmin(tl, (lo * P.spacing[a] - P.cam[a]) * inv_d[a]);
+      if (d[a] > 0.0) tl = fmin(tl, (hi * P.spacing[a] - P.cam[a]) * (1.0 / d[a]));
+      else if (d[a] < 0.0) tl = fmin(tl, (lo * P.spacing[a] - P.cam[a]) * (1.0 / d[a]));
     }
     long long m = (long long)floor((tl - t0) * P.inv_step) - 1 - k;
     m = m < n - 1 - k ? m : n - 1 - k;
@@ -655,8 +680,9 @@ struct Sampler {
       for (int a = 0; a < 3; ++a) in = in && pv[a] >= 0.0 && pv[a] <= P.dims[a];
       if (!in) return false;
       int target = lod(p);
+      // np.clip(pv, 0, dims - 1e-9): pv >= 0 here, so only the upper bound acts
 #pragma unroll
-      for (int a = 0; a < 3; ++a) pv[a] = npclip(pv[a], 0.0, P.dims[a] - 1e-9);
+      for (int a = 0; a < 3; ++a) pv[a] = pv[a] > P.dims[a] - 1e-9 ? P.dims[a] - 1e-9 : pv[a];
       return resolve(pv, target, 0, C, vals, cache[0]);
     }
     bool missing = false;
@@ -861,7 +887,7 @@ __device__ __forceinline__ void march_ray(S& s, const TFTable& tf, const double 
 #ifndef VT_RENDER_MINB
 #define VT_RENDER_MINB 4
 #endif
-template <class T, int NC, bool TR, bool FAST>
+template <class T, int NC, bool TR, bool FAST, int FILLED>
 __global__ void __launch_bounds__(128, VT_RENDER_MINB) k_render_fullframe(const uint64_t* __restrict__ nb,
                                                           uint8_t* fb, const T* __restrict__ bb,
                                                           void* out, int out_kind, int out_w,
@@ -870,7 +896,7 @@ __global__ void __launch_bounds__(128, VT_RENDER_MINB) k_render_fullframe(const 
   const RenderParams& P = c_P;
   __shared__ TFTable tf;
   load_tf(tf);
-  Sampler<T, NC, TR, FAST> s(nb, fb, bb, true);
+  Sampler<T, NC, TR, FAST, FILLED> s(nb, fb, bb, true);
   Counters& cnt = s.cnt;
   int i, j, jl;
   bool active = pixel_of(i, j, jl);
@@ -883,7 +909,6 @@ __global__ void __launch_bounds__(128, VT_RENDER_MINB) k_render_fullframe(const 
     long long n;
     ray_setup(d, t0, n);
     RayOut o{};
-    if (P.ess) s.set_ray(d);
     // one uniform branch per ray instead of a mode test per sample
     if (P.mip) march_ray<1>(s, tf, d, t0, n, o);
     else march_ray<0>(s, tf, d, t0, n, o);
@@ -981,8 +1006,7 @@ __global__ void __launch_bounds__(128) k_rays_march(RayState S,
       for (int c = 0; c < kMaxC; ++c) o.mip[c] = S.mip[r * 4 + c];
       double vals[NC];
       const double t0 = S.t0[r];
-      if (P.ess) s.set_ray(d);
-      for (; k < n; ++k) {
+        for (; k < n; ++k) {
         double t = t0 + (double)k * P.step;
         double p[3];
         for (int a = 0; a < 3; ++a) p[a] = P.cam[a] + t * d[a];
@@ -1279,7 +1303,10 @@ void fill_params(const vt_mirror* m, const vt_scene* s, RenderParams& P) {
   P.fmax = (double)t.fmax;
   P.inv_fmax = 1.0 / P.fmax;
   for (int l = 0; l <= t.g.depth; ++l)
-    for (int a = 0; a < 3; ++a) P.inv_scl[l][a] = 1.0 / P.scl[l][a];
+    for (int a = 0; a < 3; ++a) {
+      P.inv_scl[l][a] = 1.0 / P.scl[l][a];
+      P.exti[l][a] = t.g.split[a] ? t.g.extent(a, l) : (1 << 30);
+    }
   P.unit_spacing = s->spacing[0] == 1.0 && s->spacing[1] == 1.0 && s->spacing[2] == 1.0;
   {
     int ex = 0;
@@ -1719,14 +1746,24 @@ static void render_rect(vt_mirror* m, const vt_scene* scene, const int32_t* rect
   if (px > 0) {
     dispatch(t.g.sb, t.g.C, P.has_tr != 0, [&](auto tag, auto nc, auto tr) {
       using T = decltype(tag);
-      if (P.fast)
-        k_render_fullframe<T, decltype(nc)::value, decltype(tr)::value, true>
-            <<<grid, 128, 0, t.stream>>>(m->d_nb, m->d_fb, (const T*)brick_ptr(m), dout, out_kind,
-                                         rw, rh, dc);
-      else
-        k_render_fullframe<T, decltype(nc)::value, decltype(tr)::value, false>
-            <<<grid, 128, 0, t.stream>>>(m->d_nb, m->d_fb, (const T*)brick_ptr(m), dout, out_kind,
-                                         rw, rh, dc);
+      constexpr int NCv = decltype(nc)::value;
+      constexpr bool TRv = decltype(tr)::value;
+      const T* bbp = (const T*)brick_ptr(m);
+      if (P.fast) {
+        if (P.borders_filled)
+          k_render_fullframe<T, NCv, TRv, true, 1><<<grid, 128, 0, t.stream>>>(
+              m->d_nb, m->d_fb, bbp, dout, out_kind, rw, rh, dc);
+        else
+          k_render_fullframe<T, NCv, TRv, true, 0><<<grid, 128, 0, t.stream>>>(
+              m->d_nb, m->d_fb, bbp, dout, out_kind, rw, rh, dc);
+      } else {
+        if (P.borders_filled)
+          k_render_fullframe<T, NCv, TRv, false, 1><<<grid, 128, 0, t.stream>>>(
+              m->d_nb, m->d_fb, bbp, dout, out_kind, rw, rh, dc);
+        else
+          k_render_fullframe<T, NCv, TRv, false, 0><<<grid, 128, 0, t.stream>>>(
+              m->d_nb, m->d_fb, bbp, dout, out_kind, rw, rh, dc);
+      }
     });
     VT_CUDA(cudaGetLastError());
   }
