@@ -85,7 +85,7 @@ __global__ void k_seed(const SeedJob* __restrict__ jobs, int n, Geo g, T* pool,
       // two voxels per inner row, as flat coalesced runs
       const int plane = sx * sy * C, inner = sz - 2;
       const int n1 = 2 * plane, n2 = n1 + inner * 2 * rowlen, n3 = n2 + inner * (sy - 2) * 2 * C;
-      for (int e = threadIdx.x; e < n3; e += blockDim.x) {
+      for (int e = threadIdx.x + blockIdx.y * blockDim.x; e < n3; e += blockDim.x * gridDim.y) {
         int64_t off;
         if (e < n1) {
           off = e < plane ? e : (int64_t)(sz - 1) * plane + (e - plane);
@@ -102,7 +102,8 @@ __global__ void k_seed(const SeedJob* __restrict__ jobs, int n, Geo g, T* pool,
       continue;
     }
     // rows outside the cover: whole rows, one warp each
-    for (int row = threadIdx.x >> 5; row < sy * sz; row += blockDim.x >> 5) {
+    for (int row = (threadIdx.x >> 5) + blockIdx.y * (blockDim.x >> 5); row < sy * sz;
+         row += (blockDim.x >> 5) * gridDim.y) {
       const int y = row % sy, z = row / sy;
       const bool yz_cov = cov && y >= 1 + j.cov_lo[1] && y < 1 + j.cov_hi[1] &&
                           z >= 1 + j.cov_lo[2] && z < 1 + j.cov_hi[2];
@@ -248,7 +249,7 @@ __global__ void __launch_bounds__(256) k_plane(const PlaneJob* __restrict__ jobs
   const int64_t rowstride = (int64_t)g.stored[0] * C;
   for (int job = blockIdx.x; job < n; job += gridDim.x) {
     const PlaneJob j = jobs[job];
-    for (int z = j.z0 + warp; z < j.z1; z += nw) {
+    for (int z = j.z0 + warp + blockIdx.y * nw; z < j.z1; z += nw * gridDim.y) {
       const T* base = pool + (int64_t)j.slot * g.brick_elems + g.voxel_offset(z + 1, 1, 1);
       int mn[kMaxC], mx[kMaxC];
       unsigned long long sm[kMaxC];
@@ -258,6 +259,7 @@ __global__ void __launch_bounds__(256) k_plane(const PlaneJob* __restrict__ jobs
         mx[c] = INT_MIN;
         sm[c] = 0;
       }
+#pragma unroll 4
       for (int y = 0; y < j.cy; ++y) {
         const T* row = base + y * rowstride;
         for (int x = lane; x < j.cx; x += 32) {
@@ -374,7 +376,9 @@ __global__ void __launch_bounds__(256) k_octant(const OctJob* __restrict__ jobs,
     const bool full = child && j.cext[0] >= kk[0] * j.r1[0] && j.cext[1] >= kk[1] * j.r1[1] &&
                       j.cext[2] >= kk[2] * j.r1[2];
     const int n_out = kk[0] * kk[1] * kk[2];
-    for (int e = threadIdx.x; e < per_plane * wz; e += blockDim.x) {
+#pragma unroll 2
+    for (int e = threadIdx.x + blockIdx.y * blockDim.x; e < per_plane * wz;
+         e += blockDim.x * gridDim.y) {
       const int oz = j.r0[2] + e / per_plane;
       const int rem = e - (e / per_plane) * per_plane;
       const int oy = j.r0[1] + rem / wx, ox = j.r0[0] + rem % wx;
@@ -681,9 +685,17 @@ void launch_create(const Tree& t, const CreateJob* d, int n) {
 
 constexpr int kMaxGridY = 65535;
 
+// CTAs per job for a launch of n jobs: small per-insertion launches (a
+// slice's few dozen bricks at threshold > 0) split each job so every SM works
+static unsigned split_for(int n, int max_split) {
+  int k = 1;
+  while (k < max_split && (int64_t)n * k < 2 * 148) k *= 2;
+  return (unsigned)k;
+}
+
 void launch_seed(const Tree& t, const SeedJob* d, int n) {
   if (n <= 0) return;
-  const unsigned grid = (unsigned)std::min<int64_t>(n, 148 * 64);
+  const dim3 grid((unsigned)std::min<int64_t>(n, 148 * 64), split_for(n, 16));
   if (t.g.sb == 1)
     k_seed<uint8_t><<<grid, 256, 0, t.stream>>>(d, n, t.g, t.d_pool, t.d_stats);
   else
@@ -719,7 +731,7 @@ void launch_scatter(const Tree& t, const void* src, int channel, int ss, int so,
 
 void launch_octant(const Tree& t, const OctJob* d, int n) {
   if (n <= 0) return;
-  const unsigned grid = (unsigned)std::min<int64_t>(n, 148 * 32);
+  const dim3 grid((unsigned)std::min<int64_t>(n, 148 * 32), split_for(n, 8));
   if (t.g.sb == 1)
     k_octant<uint8_t><<<grid, 256, 0, t.stream>>>(d, n, t.g, t.d_pool, t.d_stats);
   else
@@ -729,7 +741,7 @@ void launch_octant(const Tree& t, const OctJob* d, int n) {
 
 void launch_plane(const Tree& t, const PlaneJob* d, int n) {
   if (n <= 0) return;
-  const unsigned grid = (unsigned)std::min<int64_t>(n, 148 * 64);
+  const dim3 grid((unsigned)std::min<int64_t>(n, 148 * 64), split_for(n, 8));
   if (t.g.sb == 1)
     k_plane<uint8_t><<<grid, 256, 0, t.stream>>>(d, n, t.g, t.d_pool, t.d_pmin, t.d_pmax,
                                                   t.d_psum);
