@@ -323,11 +323,16 @@ struct Sampler {
   }
 
   // feedback flag: idempotent OR into the byte of the node (device.py:35-36,
-  // raycast.py:161-163); skipped when this thread already marked the node
+  // raycast.py:161-163).  Skipped when this thread already marked the node;
+  // otherwise warp-aggregated: the lanes marking the same node this step
+  // elect one leader (__match_any_sync), which writes only if the bit is
+  // not set yet — one atomic per node per warp instead of one per lane
   __device__ void mark(int idx, unsigned flag) {
     int& last = flag == 1 ? last_used : last_req;
     if (last == idx) return;
     last = idx;
+    const unsigned peers = __match_any_sync(__activemask(), idx);
+    if ((int)(threadIdx.x & 31) != __ffs(peers) - 1) return;
     unsigned* w = reinterpret_cast<unsigned*>(fb + (idx & ~3));
     unsigned bit = flag << ((idx & 3) * 8);
     if (!(__ldcg(w) & bit)) atomicOr(w, bit);
