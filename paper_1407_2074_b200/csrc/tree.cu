@@ -1271,6 +1271,7 @@ void Tree::launch_held() {
              "held dense layers: leaf count mismatch");
   std::vector<int64_t> fused_nodes;
   std::vector<int32_t> fused_slots;
+  std::vector<int64_t> shell_nodes;  // interior fused parents (x/y shells by the kernel)
   if (nl == 2 && (held.gz0 & 1) == 0 && g.depth >= 1 && g.split[0] && g.split[1] && g.split[2]) {
     for (int gy = 0; gy + 1 < gny; gy += 2)
       for (int gx = 0; gx + 1 < gnx; gx += 2) {
@@ -1289,6 +1290,11 @@ void Tree::launch_held() {
         for (int k = 0; k < 8; ++k) dj[pos[k]].pad = slot[p];
         fused_nodes.push_back(p);
         fused1[p] = 1;
+        // the kernel's interior rule (k_dense_leaf_tma_planar `pxy`)
+        const int px = gx >> 1, py = gy >> 1;
+        if (px >= 1 && py >= 1 && (px + 1) * 2 * M[0] + 2 <= g.dims[0] &&
+            (py + 1) * 2 * M[1] + 2 <= g.dims[1])
+          shell_nodes.push_back(p);
       }
   }
   if (!fused_nodes.empty() && !d_nsum) {
@@ -1307,7 +1313,8 @@ void Tree::launch_held() {
   if (leaf_struct_by_kernel) {
     // the walks left the leaves' device flags / slots to this kernel
     lr = launch_dense_leaf_planar(*this, planar.base, planar.zstride, planar.cstride, held.z0,
-                                  held.nz, want ? 1 : 0, d, (int)dj.size(), gn, held.gz0, true);
+                                  held.nz, want ? 1 : 0, d, (int)dj.size(), gn, held.gz0, true,
+                                  !shell_nodes.empty());
     if (lr < 0) {
       // no tensor-map encoder after all: the records the walks skipped
       std::vector<StructUpd> upd;
@@ -1337,6 +1344,32 @@ void Tree::launch_held() {
   }
   dense_after_launch(lr, dj, fused_nodes, held.z0, held.z0 + held.nz, held.gz0, held.gz1,
                      nullptr, !parents_fresh);
+  if (lr & kLeafParentShells) {
+    // x/y faces written (tracked even when prefill is no longer valid:
+    // publish_halos resets every tracked shell for a reader); z faces: the
+    // seam with the slab below (built earlier), both ways
+    if (pshell.empty()) pshell.assign(g.capacity, 0);
+    const int pz = held.gz0 >> 1, mz = M[2];
+    std::vector<int32_t> pj;
+    for (int64_t p : shell_nodes) {
+      pshell[p] |= 1;
+      if (pz == 0 || !prefill_valid) continue;
+      int lo[3];
+      g.box_lo(p, lo);
+      const int px = lo[0] / (2 * M[0]), py = lo[1] / (2 * M[1]);
+      const int64_t q = g.level_start[g.depth - 1] + morton[0][px] + morton[1][py] + morton[2][pz - 1];
+      if (!(flags[q] & NF_BRICK) || !(pshell[q] & 1)) continue;
+      pj.insert(pj.end(), {slot[p], 0, slot[q], mz});
+      pj.insert(pj.end(), {slot[q], mz + 1, slot[p], 1});
+      pshell[p] |= 2;
+      pshell[q] |= 4;
+    }
+    if (!pj.empty()) {
+      int32_t* dp = upload(*this, pj);
+      launch_plane_copy(*this, dp, (int)(pj.size() / 4));
+      release(*this, dp);
+    }
+  }
   dj.clear();
 }
 
@@ -1993,7 +2026,7 @@ void Tree::fill_borders() {
     release(*this, dp);
     if (!upper_borders)
       for (int64_t i : bricks)
-        if (g.level_of(i) > 0) jobs.push_back({i, slot[i]});
+        if (g.level_of(i) > 0 && !(!pshell.empty() && pshell[i] == 7)) jobs.push_back({i, slot[i]});
   } else {
     for (int64_t i : bricks) jobs.push_back({i, slot[i]});
   }
@@ -2008,6 +2041,7 @@ void Tree::fill_borders() {
   }
   borders = true;
   halo_prefill = false;
+  if (!pshell.empty()) std::fill(pshell.begin(), pshell.end(), 0);
   owed_shells.clear();  // every level > 0 brick's shell was just written
   upper_borders = false;
   owed_lo.clear();
@@ -2018,14 +2052,16 @@ void Tree::fill_borders() {
 // any reader of pool shells first resets them (then fill_borders takes the
 // general path).
 void Tree::publish_halos() {
-  if ((!halo_prefill && owed_shells.empty() && !upper_borders) || borders) return;
+  const bool ps = !pshell.empty();
+  if ((!halo_prefill && owed_shells.empty() && !upper_borders && !ps) || borders) return;
   flush();
   std::vector<int32_t> sl;
-  if (halo_prefill || upper_borders)
+  if (halo_prefill || upper_borders || ps)
     for (int64_t i = 0; i < g.capacity; ++i)
       if ((flags[i] & NF_EXISTS) && (flags[i] & NF_BRICK) &&
-          (g.level_of(i) == 0 ? halo_prefill : upper_borders))
+          (g.level_of(i) == 0 ? halo_prefill : (upper_borders || (ps && pshell[i]))))
         sl.push_back(slot[i]);
+  if (ps) pshell.clear();
   upper_borders = false;
   sl.insert(sl.end(), owed_shells.begin(), owed_shells.end());
   owed_shells.clear();

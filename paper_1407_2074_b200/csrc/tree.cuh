@@ -229,6 +229,11 @@ struct Tree {
   // while a pair is walked: in-volume leaves get no per-node structure
   // record — the pair's leaf kernel writes their device flags and slots
   bool leaf_struct_by_kernel = false;
+  // level-1 parents whose shells a held pair's leaf kernel (x/y faces) and
+  // the slab seams (z faces) already wrote with their fill_borders values:
+  // bit 1 x/y, bit 2 z-low, bit 4 z-high (7: fill_borders skips the brick);
+  // logically background until fill_borders like every prefilled shell
+  std::vector<uint8_t> pshell;
   void launch_held();
   // bookkeeping after a dense leaf launch over leaves `djobs` of the block
   // z in [z0, z1), layers [gz0, gz1]
@@ -503,7 +508,9 @@ void launch_octant(const Tree& t, const OctJob* d_jobs, int n);
 // dense_build.cu
 // returns kLeafPrefilled (shells prefilled) | kLeafTma (TMA kernel: fused
 // parent octants of jobs with pad >= 0 written too)
-constexpr int kLeafPrefilled = 1, kLeafTma = 2, kLeafBmax = 4;  // kLeafBmax: brick maxima written
+// kLeafBmax: brick maxima written; kLeafParentShells: the x/y shells of the
+// interior fused level-1 parents written (held pairs)
+constexpr int kLeafPrefilled = 1, kLeafTma = 2, kLeafBmax = 4, kLeafParentShells = 8;
 int launch_dense_leaf(const Tree& t, const void* src, int64_t nsrc, int oz, int prefill,
                       const DenseJob* jobs, int n, const int gn[3], int g0z);
 // planar (c, z, y, x) source through a 4-D TMA tensor map; -1 = unsupported
@@ -511,7 +518,8 @@ int launch_dense_leaf(const Tree& t, const void* src, int64_t nsrc, int oz, int 
 bool planar_leaf_ok(const Tree& t, const void* base, int64_t zstride, int64_t cstride);
 int launch_dense_leaf_planar(const Tree& t, const void* base, int64_t zstride, int64_t cstride,
                              int oz, int64_t dz, int prefill, const DenseJob* jobs, int n,
-                             const int gn[3], int g0z, bool write_struct = false);
+                             const int gn[3], int g0z, bool write_struct = false,
+                             bool parent_shells = false);
 void launch_planar_to_interleaved(const Tree& t, const void* base, int64_t zstride,
                                   int64_t cstride, int dz, void* dst);
 void launch_fill_bg(const Tree& t, void* dst, int64_t n);

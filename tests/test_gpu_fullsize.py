@@ -147,6 +147,19 @@ def test_cfg3_spim_slice_stream_equals_slabs():
             s.insert_block(ch, (0, 0, z), plane[..., ch].contiguous())
     assert _finish(s) == want
     s.close()
+    torch.cuda.empty_cache()
+    # the bench's stream: planar (C, Z, Y, X) slices, one insert_planar call
+    # per brick-layer pair (fused pairs, parent shells from the leaf kernel,
+    # eager z seams)
+    P = vol.permute(3, 0, 1, 2).contiguous()
+    del vol
+    torch.cuda.empty_cache()
+    s = _tree(dims, C, M)
+    for z in range(0, dims[2], 2 * M):
+        s.insert_planar(P[:, z:z + 2 * M], z)
+    assert s.stream_counts()[0] == (dims[2] + M - 1) // M
+    assert _finish(s) == want
+    s.close()
 
 
 @pytest.fixture(scope="module")

@@ -248,3 +248,33 @@ def test_insert_planar_slabs(where):
         t.insert_planar(src[:, z0:z1], z0)
     assert t.stream_counts()[0] >= 1
     assert _state(t) == want
+
+
+@pytest.mark.parametrize("reader", [False, True])
+def test_layer_pairs_with_interior_parents(reader):
+    """insert_planar in brick-layer pairs over a volume whose level-1
+    parents have interior x/y neighbours: the pair's leaf kernel writes those
+    parents' x/y shells and the slab seams their z shells; fill_borders skips
+    them.  Same tree (checksum, VXOC/VXBP after fill_borders) as the general
+    path, also with a reader (which resets every prefilled shell) mid-stream."""
+    from paper_1407_2074_b200.serialize import octree_digests
+    dims, C, brick = (224, 192, 160), 3, 16
+    vol = _vol(dims, C, "uint16", seed=9)
+    spec = _spec(dims, C, "uint16", brick)
+    pv = _planar(vol)
+    t = make_tree(spec)
+    for z in range(0, dims[2], 4 * brick):
+        t.insert_planar(pv[:, z:z + 4 * brick], z)
+        if reader and z == 4 * brick:
+            t.checksum()  # a reader between pairs: prefilled shells published
+    t.finalize()
+    t.fill_borders()
+    g = make_tree(spec)
+    g.dense_build = False
+    for z in range(dims[2]):
+        for c in range(C):
+            g.insert_block(c, (0, 0, z), vol[z:z + 1, :, :, c])
+    g.finalize()
+    g.fill_borders()
+    assert t.checksum() == g.checksum()
+    assert octree_digests(t) == octree_digests(g)
