@@ -477,7 +477,8 @@ __global__ void __launch_bounds__(256) k_borders(const BorderJob* __restrict__ j
         if (g0[a] < 0 || g0[a] >= mvirt[a]) outside = true;
       }
     }
-    const bool interior = s3[0] == 1 && s3[1] == 1 && s3[2] == 1;
+    const bool interior = (s3[0] == 1 && s3[1] == 1 && s3[2] == 1) ||
+                          (j.skipx && s3[0] != 1 && s3[1] == 1 && s3[2] == 1);
     for (int a = 0; a < 3; ++a) {
       s_len[seg][a] = interior ? 0 : len[a];
       s_l0[seg][a] = l0[a];

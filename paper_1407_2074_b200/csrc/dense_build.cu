@@ -420,7 +420,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
     const __grid_constant__ CUtensorMap map, int oz, int dz, int prefill,
     const DenseJob* __restrict__ jobs, int gnx, int gny, int g0z, Geo g,
     uint16_t* __restrict__ pool, int32_t* stats, int32_t* nmin, int32_t* nmax,
-    unsigned long long* nsum) {
+    unsigned long long* nsum, int pshell) {
   constexpr int P = kTmaP;
   constexpr int WPP = kTmaWarps / P;  // warps per plane
   constexpr int NT = WPP * 32;        // threads per plane
@@ -437,6 +437,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
   const int X = g.dims[0], Y = g.dims[1], Z = g.dims[2];
   const int cx = min(Mx, X - gx * Mx), cy = min(My, Y - gy * My), cz = min(Mz, Z - gz * Mz);
   const int brow = tma_box_row(Mx, C);                  // staged row (samples)
+  const int RS = My + 2;  // staged rows per plane
   const uint32_t in_bytes = tma_in_bytes(Mx, My, C);    // one input stage
   const uint32_t plane_elems = (uint32_t)Sx * Sy * C;   // one stored plane
   const int wpr = Sx * C / 2;                           // 32-bit words per stored row
@@ -464,7 +465,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
 
   auto issue = [&](int s) {  // one thread: one tensor tile per stage
     const int b = s % kTmaStages;
-    mbar_expect_tx(&s_bar[b], (uint32_t)P * (My + 2) * brow * 2);
+    mbar_expect_tx(&s_bar[b], (uint32_t)P * RS * brow * 2);
     tma_load_3d(s_in + (size_t)b * in_bytes, &map, xa, y0, gz * Mz - oz + P * s - 1, &s_bar[b]);
   };
   if (tid == 0)
@@ -487,6 +488,12 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
     pcz = min(Mz, max(0, (Z - plz + 1) / 2));
   }
   uint16_t* parent = pslot >= 0 ? pool + (int64_t)pslot * g.brick_elems : nullptr;
+  // interior level-1 parent: its x-face shell rows on this child's side,
+  // from the staged x halo (as k_dense_leaf_tma_planar; Tree::parent_interior
+  // mirrors the rule)
+  const bool pxy = parent && pshell && (gx >> 1) >= 1 && (gy >> 1) >= 1 &&
+                   ((gx >> 1) + 1) * 2 * Mx + 2 <= X && ((gy >> 1) + 1) * 2 * My + 2 <= Y &&
+                   xoff >= C && (Mx + 3) * C + xoff <= brow;
 
   // per-thread totals over the whole brick: the leaf (l*) and the octant (o*)
   int lmn[C], lmx[C], omn[C], omx[C];
@@ -519,7 +526,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
                      : (prefill && zs < Sz && rz >= 0 && rz < Z && rz - oz >= 0 && rz - oz < dz) ? 2
                                                                                                : 0;
     const uint16_t* iplane = reinterpret_cast<const uint16_t*>(s_in + (size_t)b * in_bytes) +
-                             (size_t)pw * (My + 2) * brow;
+                             (size_t)pw * RS * brow;
     uint32_t* oplane = reinterpret_cast<uint32_t*>(brick + (size_t)zs * plane_elems);
     // every thread waits, so the slot's phase is complete before it is re-armed
     mbar_wait(&s_bar[b], (uint32_t)(s / kTmaStages) & 1u);
@@ -624,7 +631,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
       const int k = s - 1;
       const uint16_t* pa = reinterpret_cast<const uint16_t*>(
                                s_in + (size_t)((unsigned)(s - 1) % kTmaStages) * in_bytes) +
-                           (size_t)(My + 2) * brow;  // previous stage, plane 1
+                           (size_t)RS * brow;  // previous stage, plane 1
       const uint16_t* pb = reinterpret_cast<const uint16_t*>(s_in + (size_t)b * in_bytes);
       const bool zfull = 2 * k + 1 < cz;
       const bool pin = offz + k < pcz;
@@ -686,6 +693,35 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
             omx[c] = max(omx[c], val[c]);
             osm[c] += (unsigned)val[c];
           }
+        }
+      }
+      if (pxy) {
+        // x-face voxel of parent row 1 + offy + v
+        const int lx = (gx & 1) ? Mx : -2;         // child-local raw x of the footprint
+        const int dxs = (gx & 1) ? Mx + 1 : 0;     // stored x of the shell
+        for (int v = tid; v < hy; v += kTmaWarps * 32) {
+          const int ly = 2 * v, dys = 1 + offy + v;
+          unsigned sum[C];
+#pragma unroll
+          for (int c = 0; c < C; ++c) sum[c] = 0;
+          int cnt = 0;
+          for (int dz2 = 0; dz2 < 2; ++dz2) {
+            if (2 * k + dz2 >= cz) continue;
+            const uint16_t* pl = dz2 ? pb : pa;
+#pragma unroll
+            for (int dy = 0; dy < 2; ++dy)
+#pragma unroll
+              for (int dx = 0; dx < 2; ++dx) {
+                const int o = (1 + ly + dy) * brow + xoff + (1 + lx + dx) * C;
+#pragma unroll
+                for (int c = 0; c < C; ++c) sum[c] += pl[o + c];
+                ++cnt;
+              }
+          }
+          uint16_t* dst = parent + g.voxel_offset(1 + offz + k, dys, dxs);
+#pragma unroll
+          for (int c = 0; c < C; ++c)
+            dst[c] = (uint16_t)(cnt ? (2 * (unsigned long long)sum[c] + cnt) / (2 * cnt) : bg);
         }
       }
     }
@@ -767,7 +803,7 @@ constexpr int kPStages = 3;  // planar ring: building, previous (fused octant), 
 constexpr int kPAhead = 2;
 __host__ __device__ inline int tma_box_row_planar(int mx) { return (mx + 2 + 7 + 7) / 8 * 8; }
 __host__ __device__ inline uint32_t tma_in_bytes_planar(int mx, int my, int C) {
-  return ((uint32_t)C * kTmaP * (my + 4) * tma_box_row_planar(mx) * 2 + 127) / 128 * 128;
+  return ((uint32_t)C * kTmaP * (my + 2) * tma_box_row_planar(mx) * 2 + 127) / 128 * 128;
 }
 
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int x, int y, int z,
@@ -803,9 +839,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma_planar(
   const int X = g.dims[0], Y = g.dims[1], Z = g.dims[2];
   const int cx = min(Mx, X - gx * Mx), cy = min(My, Y - gy * My), cz = min(Mz, Z - gz * Mz);
   const int bx = tma_box_row_planar(Mx);             // staged row (samples, one channel)
-  // staged rows per plane: the stored rows plus one more raw row on each
-  // side (the level-1 parent's y-shells half-sample raw rows -2 / M + 1)
-  const int RS = Sy + 2;
+  const int RS = Sy;  // staged rows per plane
   const int rows = P * RS;                           // staged rows per channel
   const uint32_t in_bytes = tma_in_bytes_planar(Mx, My, C);
   const uint32_t plane_elems = (uint32_t)Sx * Sy * C;
@@ -833,8 +867,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma_planar(
   auto issue = [&](int s) {  // one thread: one 4-D tensor tile per stage
     const int b = s % kPStages;
     mbar_expect_tx(&s_bar[b], (uint32_t)C * rows * bx * 2);
-    tma_load_4d(s_in + (size_t)b * in_bytes, &map, xa, y0 - 1, gz * Mz - oz + P * s - 1, 0,
-                &s_bar[b]);
+    tma_load_4d(s_in + (size_t)b * in_bytes, &map, xa, y0, gz * Mz - oz + P * s - 1, 0, &s_bar[b]);
   };
   if (tid == 0)
     for (int s = 0; s < min(kPAhead, nstages); ++s) issue(s);
@@ -851,9 +884,10 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma_planar(
   }
   uint16_t* parent = pslot >= 0 ? pool + (int64_t)pslot * g.brick_elems : nullptr;
   // interior level-1 parent (its x/y neighbour parents' footprints lie in
-  // the volume): this child also writes the parent's x/y shell voxels on its
-  // side — the neighbour parent's edge voxels, half-sampled from the two raw
-  // voxels beyond the child's edge that the staged halo holds
+  // the volume): this child also writes the parent's x-face shell rows on
+  // its side — the neighbour parent's edge voxels, half-sampled from the two
+  // raw voxels beyond the child's edge that the staged x halo holds (the
+  // strided x faces are k_borders' costly segments; it skips them)
   const bool pxy = parent && pshell && (gx >> 1) >= 1 && (gy >> 1) >= 1 &&
                    ((gx >> 1) + 1) * 2 * Mx + 2 <= X && ((gy >> 1) + 1) * 2 * My + 2 <= Y;
 
@@ -879,7 +913,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma_planar(
                      : (prefill && zs < Sz && rz >= 0 && rz < Z && rz - oz >= 0 && rz - oz < dz) ? 2
                                                                                                : 0;
     const uint16_t* stage = reinterpret_cast<const uint16_t*>(s_in + (size_t)b * in_bytes);
-    const uint16_t* iplane = stage + (size_t)(pw * RS + 1) * bx + xoff;  // channel 0, stored (0, 0)
+    const uint16_t* iplane = stage + (size_t)pw * RS * bx + xoff;  // channel 0, stored (0, 0)
     uint32_t* oplane = reinterpret_cast<uint32_t*>(brick + (size_t)zs * plane_elems);
     mbar_wait(&s_bar[b], (uint32_t)(s / kPStages) & 1u);
     if (zs < Sz && mode != 0 && xyfull) {
@@ -891,7 +925,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma_planar(
       // of the channel-fastest stored row are assembled and stored.
       const bool stat_plane = mode == 1 && !parent;
       const uint32_t* s32 =
-          reinterpret_cast<const uint32_t*>(stage) + ((pw * RS + 1) * bx + xoff - 1) / 2;
+          reinterpret_cast<const uint32_t*>(stage) + (pw * RS * bx + xoff - 1) / 2;
       const int pt = (warp % WPP) * 32 + lane;
       const int SP = Sx / 2;  // voxel pairs per stored row
       for (int q = pt; q < Sy * SP; q += NT) {
@@ -985,8 +1019,8 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma_planar(
       const int k = s - 1;
       const uint16_t* pa = reinterpret_cast<const uint16_t*>(
                                s_in + (size_t)((unsigned)(s - 1) % kPStages) * in_bytes) +
-                           (size_t)(RS + 1) * bx + xoff;  // previous stage, plane 1
-      const uint16_t* pb = stage + bx + xoff;              // this stage, plane 0
+                           (size_t)RS * bx + xoff;  // previous stage, plane 1
+      const uint16_t* pb = stage + xoff;             // this stage, plane 0
       const bool zfull = 2 * k + 1 < cz;
       const bool pin = offz + k < pcz;
       for (int v = tid; v < hx * hy; v += kTmaWarps * 32) {
@@ -1048,19 +1082,11 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma_planar(
         }
       }
       if (pxy) {
-        // v < hy: x-face voxel (row oy = v); v < hy + hx: y-face (column
-        // ox = v - hy); the last: the shared corner
-        const int fx = (gx & 1) ? Mx : -2, fy = (gy & 1) ? My : -2;  // child-local raw
-        const int sxf = (gx & 1) ? Mx + 1 : 0, syf = (gy & 1) ? My + 1 : 0;  // stored
-        for (int v = tid; v < hx + hy + 1; v += kTmaWarps * 32) {
-          int lx, ly, dxs, dys;
-          if (v < hy) {
-            lx = fx; ly = 2 * v; dxs = sxf; dys = 1 + offy + v;
-          } else if (v < hy + hx) {
-            lx = 2 * (v - hy); ly = fy; dxs = 1 + offx + (v - hy); dys = syf;
-          } else {
-            lx = fx; ly = fy; dxs = sxf; dys = syf;
-          }
+        // x-face voxel of parent row 1 + offy + v
+        const int lx = (gx & 1) ? Mx : -2;         // child-local raw x of the footprint
+        const int dxs = (gx & 1) ? Mx + 1 : 0;     // stored x of the shell
+        for (int v = tid; v < hy; v += kTmaWarps * 32) {
+          const int ly = 2 * v, dys = 1 + offy + v;
           unsigned sum[C];
 #pragma unroll
           for (int c = 0; c < C; ++c) sum[c] = 0;
@@ -1459,11 +1485,12 @@ static int leaf_launch(const Tree& t, const void* src, int64_t nsrc, int oz, int
     auto k = t.g.brick[0] == 32 && t.g.brick[1] == 32 ? k_dense_leaf_tma<C, 32, 32>
                                                       : k_dense_leaf_tma<C>;
     VT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int ps = t.parent_shells_next && prefill ? 1 : 0;
     k<<<n, kTmaWarps * 32, smem, t.stream>>>(map, oz, (int)dz, prefill, jobs, gn[0], gn[1], g0z,
                                             t.g, (uint16_t*)t.d_pool, t.d_stats, t.d_nmin,
-                                            t.d_nmax, t.d_nsum);
+                                            t.d_nmax, t.d_nsum, ps);
     VT_CHECK_LAUNCH();
-    return kLeafTma | (prefill ? kLeafPrefilled : 0);
+    return kLeafTma | (prefill ? kLeafPrefilled : 0) | (ps ? kLeafParentShells : 0);
   }
   if (sizeof(T) == 2 && rowlen % 2 == 0 && wpl <= 4) {
     // warps own ceil(Sz / 17) planes each (<= 17 warps)
@@ -1566,7 +1593,7 @@ bool planar_leaf_ok(const Tree& t, const void* base, int64_t zstride, int64_t cs
   const Geo& g = t.g;
   return g.sb == 2 && ((uintptr_t)base & 15) == 0 && ((int64_t)g.dims[0] * 2) % 16 == 0 &&
          zstride > 0 && zstride % 16 == 0 && (g.C == 1 || (cstride > 0 && cstride % 16 == 0)) &&
-         tma_box_row_planar(g.brick[0]) <= 256 && g.brick[1] + 4 <= 256 &&
+         tma_box_row_planar(g.brick[0]) <= 256 && g.brick[1] + 2 <= 256 &&
          g.brick[0] % 2 == 0 && tma_smem_planar(g) <= 200 * 1024;
 }
 
@@ -1595,7 +1622,7 @@ static bool encode_planar_map(const Tree& t, const void* base, int64_t zstride, 
                         (cuuint64_t)g.C};
   cuuint64_t strides[3] = {(cuuint64_t)g.dims[0] * 2, (cuuint64_t)zstride,
                            (cuuint64_t)(g.C == 1 ? zstride * dz : cstride)};
-  cuuint32_t box[4] = {(cuuint32_t)tma_box_row_planar(g.brick[0]), (cuuint32_t)(g.brick[1] + 4),
+  cuuint32_t box[4] = {(cuuint32_t)tma_box_row_planar(g.brick[0]), (cuuint32_t)(g.brick[1] + 2),
                        (cuuint32_t)kTmaP, (cuuint32_t)g.C};
   cuuint32_t es[4] = {1, 1, 1, 1};
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 4, const_cast<void*>(base), dims, strides, box,

@@ -768,8 +768,10 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
       if (prof.on) VT_CUDA(cudaEventRecord(prof.ev[1], stream));
       VT_CUDA(cudaEventRecord(ev_pre, stream));
       ProfScope qll(prof, 30);
+      parent_shells_next = !fused_nodes.empty();
       launch_result = leaf_launch(dsrc, nvox * src_stride, origin[2], dims[2], want ? 1 : 0, dj,
                                   (int)djobs.size(), gn, g0[2]);
+      parent_shells_next = false;
       if (prof.on) {
         VT_CUDA(cudaEventRecord(prof.ev[2], stream));
         prof.ev_armed = true;
@@ -1087,6 +1089,7 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
     }
     dense_after_launch(lr, djobs, fused_nodes, origin[2], origin[2] + dims[2], g0[2], g1[2],
                        &touched[0]);
+    if (lr & kLeafParentShells) mark_parent_shells(fused_nodes, true);
   } else if (starting) {
     // open the deferred layer: slots and events are final, data waits
     ProfScope q(prof, 7);
@@ -1133,7 +1136,7 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
       std::vector<BorderJob> bj;
       for (int64_t i = 0; i < g.capacity; ++i)
         if ((flags[i] & NF_EXISTS) && (flags[i] & NF_BRICK) && g.level_of(i) > 0)
-          bj.push_back({i, slot[i]});
+          bj.push_back({i, slot[i], skipx(i) ? 1 : 0});
       BorderJob* d = upload(*this, bj);
       launch_borders(*this, d, (int)bj.size());
       release(*this, d);
@@ -1257,6 +1260,33 @@ void Tree::dense_after_launch(int lr, const std::vector<DenseJob>& djobs,
   }
 }
 
+bool Tree::parent_interior(int64_t p, bool interleaved) const {
+  const int* M = g.brick;
+  int lo[3];
+  g.box_lo(p, lo);
+  const int px = lo[0] / (2 * M[0]), py = lo[1] / (2 * M[1]);
+  if (!(px >= 1 && py >= 1 && (px + 1) * 2 * M[0] + 2 <= g.dims[0] &&
+        (py + 1) * 2 * M[1] + 2 <= g.dims[1]))
+    return false;
+  if (!interleaved) return true;
+  // k_dense_leaf_tma: (Mx + 3) * C + xoff <= staged row, for both child columns
+  const int brow = ((M[0] + 2) * g.C + 14) / 8 * 8;
+  for (int gx = 2 * px; gx <= 2 * px + 1; ++gx) {
+    const int x0c = (gx * M[0] - 1) * g.C;
+    const int xoff = ((x0c % 8) + 8) % 8;
+    if (xoff < g.C || (M[0] + 3) * g.C + xoff > brow) return false;
+  }
+  return true;
+}
+
+void Tree::mark_parent_shells(const std::vector<int64_t>& nodes, bool interleaved) {
+  // tracked even when prefill is no longer valid: publish_halos resets every
+  // tracked shell for a reader
+  if (pshell.empty()) pshell.assign(g.capacity, 0);
+  for (int64_t p : nodes)
+    if (parent_interior(p, interleaved)) pshell[p] |= 1;
+}
+
 // the held even layer and the odd layer after it: one leaf launch over both,
 // level-1 parents whose eight children are all in the pair fused
 void Tree::launch_held() {
@@ -1344,32 +1374,7 @@ void Tree::launch_held() {
   }
   dense_after_launch(lr, dj, fused_nodes, held.z0, held.z0 + held.nz, held.gz0, held.gz1,
                      nullptr, !parents_fresh);
-  if (lr & kLeafParentShells) {
-    // x/y faces written (tracked even when prefill is no longer valid:
-    // publish_halos resets every tracked shell for a reader); z faces: the
-    // seam with the slab below (built earlier), both ways
-    if (pshell.empty()) pshell.assign(g.capacity, 0);
-    const int pz = held.gz0 >> 1, mz = M[2];
-    std::vector<int32_t> pj;
-    for (int64_t p : shell_nodes) {
-      pshell[p] |= 1;
-      if (pz == 0 || !prefill_valid) continue;
-      int lo[3];
-      g.box_lo(p, lo);
-      const int px = lo[0] / (2 * M[0]), py = lo[1] / (2 * M[1]);
-      const int64_t q = g.level_start[g.depth - 1] + morton[0][px] + morton[1][py] + morton[2][pz - 1];
-      if (!(flags[q] & NF_BRICK) || !(pshell[q] & 1)) continue;
-      pj.insert(pj.end(), {slot[p], 0, slot[q], mz});
-      pj.insert(pj.end(), {slot[q], mz + 1, slot[p], 1});
-      pshell[p] |= 2;
-      pshell[q] |= 4;
-    }
-    if (!pj.empty()) {
-      int32_t* dp = upload(*this, pj);
-      launch_plane_copy(*this, dp, (int)(pj.size() / 4));
-      release(*this, dp);
-    }
-  }
+  if (lr & kLeafParentShells) mark_parent_shells(shell_nodes, false);
   dj.clear();
 }
 
@@ -2026,7 +2031,7 @@ void Tree::fill_borders() {
     release(*this, dp);
     if (!upper_borders)
       for (int64_t i : bricks)
-        if (g.level_of(i) > 0 && !(!pshell.empty() && pshell[i] == 7)) jobs.push_back({i, slot[i]});
+        if (g.level_of(i) > 0) jobs.push_back({i, slot[i], skipx(i) ? 1 : 0});
   } else {
     for (int64_t i : bricks) jobs.push_back({i, slot[i]});
   }

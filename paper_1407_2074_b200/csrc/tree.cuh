@@ -229,11 +229,18 @@ struct Tree {
   // while a pair is walked: in-volume leaves get no per-node structure
   // record — the pair's leaf kernel writes their device flags and slots
   bool leaf_struct_by_kernel = false;
-  // level-1 parents whose shells a held pair's leaf kernel (x/y faces) and
-  // the slab seams (z faces) already wrote with their fill_borders values:
-  // bit 1 x/y, bit 2 z-low, bit 4 z-high (7: fill_borders skips the brick);
+  // level-1 parents whose x-face shell rows a leaf kernel already wrote with
+  // their fill_borders values (bit 1): k_borders skips those two segments;
   // logically background until fill_borders like every prefilled shell
   std::vector<uint8_t> pshell;
+  bool parent_shells_next = false;  // the next interleaved TMA leaf launch writes them
+  // interior fused level-1 parents (the leaf kernels' `pxy` rule; `xoff_ok`:
+  // the interleaved kernel's staged row also reaches two voxels past the brick)
+  bool parent_interior(int64_t p, bool interleaved) const;
+  // after a leaf launch that wrote the x-face shells of `nodes`' interior
+  // parents: mark them
+  void mark_parent_shells(const std::vector<int64_t>& nodes, bool interleaved);
+  bool skipx(int64_t i) const { return !pshell.empty() && (pshell[i] & 1); }
   void launch_held();
   // bookkeeping after a dense leaf launch over leaves `djobs` of the block
   // z in [z0, z1), layers [gz0, gz1]

@@ -164,7 +164,9 @@ struct OctJob {
 };
 struct PlaneJob { int32_t slot, z0, z1, cx, cy; };  // planes [z0, z1) of one brick
 struct ReduceJob { int64_t node; int32_t slot; int32_t cext[3]; int32_t leafish; };
-struct BorderJob { int64_t node; int32_t slot; };
+// skipx: the two x-face segments (x = 0 and x = M + 1 over the interior y/z
+// rows) were written by the leaf kernel (interior level-1 parents)
+struct BorderJob { int64_t node; int32_t slot; int32_t skipx = 0; };
 // dense (tau == 0) build: one leaf brick of a full-layer block
 struct DenseJob { int64_t node; int32_t slot; int32_t pad; };
 

@@ -205,6 +205,11 @@ PREFILL_CASES = {
     "grid_b32_c4": ((64, 64, 128), 4, (32, 32, 32), 100, 0),
     "grid_b16_c2": ((64, 64, 64), 2, (16, 16, 16), 100, 0),
     "nonsplit_z": ((32, 16, 6), 3, (8, 8, 8), 1, 3),
+    # whole volumes whose interior level-1 parents get their x/y shells from
+    # the leaf kernel and their z shells from parent seams
+    "bulk_interior_parents": ((96, 80, 64), 3, (8, 8, 8), 100, 0),
+    "bulk_interior_parents_bg": ((112, 88, 72), 2, (8, 8, 8), 100, 13),
+    "grid_b16_interior": ((160, 128, 96), 3, (16, 16, 16), 100, 0),
     "brick16_c4": ((64, 32, 48), 4, (16, 16, 16), 1, 0),
 }
 
@@ -225,7 +230,8 @@ def test_dense_prefilled_shells_fast_borders(name, tmp_path):
 
 
 @pytest.mark.parametrize("dims,whole", [((32, 24, 40), False), ((32, 24, 40), True),
-                                        ((40, 36, 50), True), ((64, 64, 64), True)])
+                                        ((40, 36, 50), True), ((64, 64, 64), True),
+                                        ((96, 80, 64), True)])
 def test_prefilled_shells_read_as_background_before_fill_borders(tmp_path, dims, whole):
     """Before fill_borders a prefilled shell is the reference's background to
     every reader (read_brick, export, checksum, device mirror).  A whole-volume
