@@ -769,12 +769,7 @@ def run_ours(args):
             "vs_baseline": None,
             "dtype": "f64" if args.precision == "fp64" else "f32 reconstruction / f64 accumulation",
             "data": "synthetic (SPIM-shaped S volume, generated on device, seed 0)",
-            "config": {"workload": wl["desc"], "dims": list(dims), "channels": CHANNELS,
-                       "sample_format": FMT, "brick": BRICK, "viewport": list(viewport),
-                       "parallelism": f"sort-first strips x{world} (strip_rows={args.strip_rows})"
-                       if world > 1 else "single GPU",
-                       "l2": f"flushed between frames (512 MB write); pool "
-                             f"{pool_bytes / 1e9:.1f} GB vs 126 MB L2"},
+            "config": arm_config(args, dims, world),
             "samples_per_frame": int(fr["samples_per_frame"]),
             "samples_computed_per_frame": int(fr["computed_per_frame"]),
             "samples_note": "samples = the reference's RenderCounters.samples (identical); "
@@ -824,6 +819,21 @@ def expected_bricks(dims, m):
         sc = 1 << lvl
         n += math.prod(-(-d // (m * sc)) for d in dims)
     return n
+
+
+def arm_config(args, dims, world):
+    """The `config` object both arms print (ours and --impl reference): the
+    workload, its shape and the frame; the reference arm's bounded CPU sample
+    is described in its cpu_baseline.sample, not here."""
+    wl = WORKLOADS[args.workload]
+    W, H = args.viewport
+    stored = (BRICK + 2) ** 3 * CHANNELS * 2
+    pool = expected_bricks(dims, BRICK) * stored
+    return {"workload": wl["desc"], "dims": list(dims), "channels": CHANNELS,
+            "sample_format": FMT, "brick": BRICK, "viewport": [W, H],
+            "parallelism": f"sort-first strips x{world} (strip_rows={args.strip_rows})"
+            if world > 1 else "single GPU",
+            "l2": f"flushed between frames (512 MB write); pool {pool / 1e9:.1f} GB vs 126 MB L2"}
 
 
 # ---------------------------------------------------------------------------
@@ -997,9 +1007,7 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(total / args.steps * 1e3, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": wl["desc"], "dims": list(dims), "channels": CHANNELS,
-                   "sample_format": FMT, "brick": BRICK, "viewport": list(args.viewport),
-                   "sample": sample},
+        "config": arm_config(args, dims, world),
         "cpu_baseline": {"value": round(v, 8), "unit": "Gsamples/s", "cores": cores,
                          "kind": st["kind"], "cpu_model": _cpu_model(), "sample": sample},
         "e2e": {"value": round(v, 8), "unit": "Gsamples/s", "h2d_bytes_per_step": 0,
