@@ -598,6 +598,49 @@ def leg_whole_build(dims, stream, barrier, world, rank, backend, host_e2e):
     return tree, info
 
 
+def leg_brick_sweep(stream, peak, dims=(1024, 1024, 1024)):
+    """configs[4] on one GPU: the whole-volume slice-ingest / downsample build
+    (one Octree.insert_channels of a device-resident volume + fill_borders)
+    at brick edges 16, 32, 64 — GB/s and roofline fraction per brick size
+    (the z-slab sharding over 8 GPUs splits exactly this work)."""
+    import torch
+    from paper_1407_2074_b200 import BrickPoolConfig, Octree, VolumeDescriptor, _lib
+    desc = VolumeDescriptor(dims=dims, channels=CHANNELS, sample_format=FMT)
+    vol = _synth(dims, 0, dims[2], stream)
+    raw = dims[0] * dims[1] * dims[2] * CHANNELS * 2
+    out = {}
+    for m in (16, 32, 64):
+        cfg = BrickPoolConfig(brick_dims=(m,) * 3, homogeneity_threshold=0)
+        runs = []
+        for rep in range(3):
+            tree = Octree(desc, cfg, reserve_slots=expected_bricks(dims, m))
+            _lib.call("vt_tree_set_stream", tree.handle, ct.c_void_p(stream.cuda_stream))
+            torch.cuda.synchronize()
+            with _Ev(stream) as ev:
+                tree.insert_channels((0, 0, 0), vol)
+                tree.finalize()
+                tree.fill_borders()
+                tree.sync()
+            torch.cuda.synchronize()
+            if rep:
+                runs.append(ev.ms())
+            pool = tree.brick_count * cfg.brick_nbytes(desc)
+            bricks = tree.brick_count
+            tree.close()
+            del tree
+            torch.cuda.empty_cache()
+        ms = min(runs)
+        out[f"{m}^3"] = {"ms": round(ms, 3), "bricks": bricks, "pool_gb": round(pool / 1e9, 3),
+                         "gbs_raw": round(raw / (ms * 1e-3) / 1e9, 1),
+                         "roofline_frac": round((raw + pool) / (ms * 1e-3) / 1e9 / peak, 4),
+                         "runs_ms": [round(r, 3) for r in runs]}
+    del vol
+    torch.cuda.empty_cache()
+    out["workload"] = (f"{dims[0]}x{dims[1]}x{dims[2]} x{CHANNELS} uint16 S volume, device "
+                       "resident, one insert_channels + fill_borders, tau 0")
+    return out
+
+
 def leg_stream_host(dims, stream, nz):
     """End-to-end host -> tree ingest of the first nz slices: pinned planar
     host frames through Octree.insert_planar (H2D inside the timed region)."""
@@ -790,6 +833,8 @@ def run_ours(args):
         extra["stream_e2e"] = leg_stream_host(dims, stream, min(dims[2], 256))
     if world == 1 and args.workload == "cfg3" and args.build_e2e:
         extra["stream_vstr_e2e"] = leg_vstr(dims, stream, min(dims[2], 128))
+    if world == 1 and args.workload == "cfg3" and args.secondary:
+        extra["cfg5_brick_sweep"] = leg_brick_sweep(stream, peak)
     if world == 1 and args.workload == "cfg3" and args.tau:
         extra["tau"] = leg_tau(stream, peak)
     if world == 1 and args.workload == "cfg3" and args.secondary:

@@ -415,7 +415,8 @@ __host__ __device__ inline uint32_t tma_in_bytes(int mx, int my, int C) {
 // MX, MY: brick x/y edge fixed at compile time (0 = from g) — with them the
 // stored-row word copy has constant strides and trip counts (immediate
 // offsets, full unrolling)
-template <int C, int MX = 0, int MY = 0>
+// ST: input stages in the shared-memory ring (4, or 3 for large bricks)
+template <int C, int MX = 0, int MY = 0, int ST = kTmaStages>
 __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
     const __grid_constant__ CUtensorMap map, int oz, int dz, int prefill,
     const DenseJob* __restrict__ jobs, int gnx, int gny, int g0z, Geo g,
@@ -425,7 +426,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
   constexpr int WPP = kTmaWarps / P;  // warps per plane
   constexpr int NT = WPP * 32;        // threads per plane
   extern __shared__ __align__(128) unsigned char s_in[];
-  __shared__ uint64_t s_bar[kTmaStages];
+  __shared__ uint64_t s_bar[ST];
   __shared__ int s_mn[2][kTmaWarps][C], s_mx[2][kTmaWarps][C];
   __shared__ unsigned long long s_sm[2][kTmaWarps][C];
   const DenseJob j = jobs[blockIdx.x];
@@ -458,18 +459,18 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
   const uint32_t cxmagic = (uint32_t)((((uint64_t)1 << 32) + cx - 1) / cx);  // v / cx by mul-high
 
   if (tid == 0) {
-    for (int b = 0; b < kTmaStages; ++b) mbar_init(&s_bar[b], 1);
+    for (int b = 0; b < ST; ++b) mbar_init(&s_bar[b], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
   auto issue = [&](int s) {  // one thread: one tensor tile per stage
-    const int b = s % kTmaStages;
+    const int b = s % ST;
     mbar_expect_tx(&s_bar[b], (uint32_t)P * RS * brow * 2);
     tma_load_3d(s_in + (size_t)b * in_bytes, &map, xa, y0, gz * Mz - oz + P * s - 1, &s_bar[b]);
   };
   if (tid == 0)
-    for (int s = 0; s < min(kTmaAhead, nstages); ++s) issue(s);
+    for (int s = 0; s < min((ST - 1), nstages); ++s) issue(s);
 
   // fused parent octant (j.pad = parent slot, else -1): the 2x2x2 integer
   // half-sample of this leaf (halfsample_block, octree.py:58-92) written into
@@ -517,7 +518,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
 
   const int toy = hx > 0 ? tid / hx : 0;  // octant row of this thread's first octant voxel
   for (int s = 0; s < nstages; ++s) {
-    const int b = (unsigned)s % kTmaStages;
+    const int b = (unsigned)s % ST;
     const int zs = P * s + pw;
     const int zi = zs - 1;
     const int rz = gz * Mz + zi;  // volume z of this stored plane
@@ -529,7 +530,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
                              (size_t)pw * RS * brow;
     uint32_t* oplane = reinterpret_cast<uint32_t*>(brick + (size_t)zs * plane_elems);
     // every thread waits, so the slot's phase is complete before it is re-armed
-    mbar_wait(&s_bar[b], (uint32_t)(s / kTmaStages) & 1u);
+    mbar_wait(&s_bar[b], (uint32_t)(s / ST) & 1u);
     if (zs < Sz) {
       if (mode != 0 && xfull) {
         // the common case: stored sample e of a row <-> staged sample xoff+e
@@ -630,7 +631,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
     if (parent && s >= 1 && 2 * (s - 1) < cz) {
       const int k = s - 1;
       const uint16_t* pa = reinterpret_cast<const uint16_t*>(
-                               s_in + (size_t)((unsigned)(s - 1) % kTmaStages) * in_bytes) +
+                               s_in + (size_t)((unsigned)(s - 1) % ST) * in_bytes) +
                            (size_t)RS * brow;  // previous stage, plane 1
       const uint16_t* pb = reinterpret_cast<const uint16_t*>(s_in + (size_t)b * in_bytes);
       const bool zfull = 2 * k + 1 < cz;
@@ -726,8 +727,8 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
       }
     }
     __syncthreads();  // input slots consumed
-    // the previous stage's slot is free now: refill it kTmaAhead stages ahead
-    if (tid == 0 && s + kTmaAhead < nstages) issue(s + kTmaAhead);
+    // the previous stage's slot is free now: refill it (ST - 1) stages ahead
+    if (tid == 0 && s + (ST - 1) < nstages) issue(s + (ST - 1));
   }
 
   // CTA totals: warp shuffles, then one thread per channel
@@ -1427,15 +1428,17 @@ int planes_per_warp(int sz) { return (sz + 11) / 12; }  // <= 12 warps per CTA
 
 // TMA tensor tiles need a 16-byte aligned block and row pitch, a box row of
 // at most 256 samples, and the rings must fit in shared memory
-static size_t tma_smem(const Geo& g) {
-  return (size_t)kTmaStages * tma_in_bytes(g.brick[0], g.brick[1], g.C);
+static size_t tma_smem(const Geo& g, int stages = kTmaStages) {
+  return (size_t)stages * tma_in_bytes(g.brick[0], g.brick[1], g.C);
 }
+// ring depth of the interleaved leaf kernel: 4 stages, 3 when 4 do not fit
+static int tma_stages(const Geo& g) { return tma_smem(g) <= 200 * 1024 ? kTmaStages : 3; }
 static bool tma_ok(const Tree& t, const void* src) {
   if (std::getenv("VT_DENSE_TMA") && std::getenv("VT_DENSE_TMA")[0] == '0') return false;
   const int64_t stride = (int64_t)t.g.dims[0] * t.g.C * 2;
   return t.g.sb == 2 && ((uintptr_t)src & 15) == 0 && stride % 16 == 0 &&
          tma_box_row(t.g.brick[0], t.g.C) <= 256 && t.g.brick[1] + 2 <= 256 &&
-         tma_smem(t.g) <= 200 * 1024;
+         tma_smem(t.g, tma_stages(t.g)) <= 200 * 1024;
 }
 
 // 3-D tensor map of a (dz, Y, X*C) u16 block for the TMA unit, box = one
@@ -1481,9 +1484,11 @@ static int leaf_launch(const Tree& t, const void* src, int64_t nsrc, int oz, int
   const int64_t dz = nsrc / ((int64_t)t.g.dims[0] * t.g.dims[1] * C);
   CUtensorMap map;
   if (sizeof(T) == 2 && tma_ok(t, src) && encode_block_map(t, src, dz, &map)) {
-    const size_t smem = tma_smem(t.g);
+    const int st = tma_stages(t.g);
+    const size_t smem = tma_smem(t.g, st);
     auto k = t.g.brick[0] == 32 && t.g.brick[1] == 32 ? k_dense_leaf_tma<C, 32, 32>
-                                                      : k_dense_leaf_tma<C>;
+             : st == kTmaStages                       ? k_dense_leaf_tma<C>
+                                                      : k_dense_leaf_tma<C, 0, 0, 3>;
     VT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int ps = t.parent_shells_next && prefill ? 1 : 0;
     k<<<n, kTmaWarps * 32, smem, t.stream>>>(map, oz, (int)dz, prefill, jobs, gn[0], gn[1], g0z,
