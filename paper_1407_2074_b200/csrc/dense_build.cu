@@ -829,7 +829,6 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma_planar(
   extern __shared__ __align__(128) unsigned char s_in[];
   __shared__ uint64_t s_bar[kPStages];
   __shared__ int s_mn[2][kTmaWarps][C], s_mx[2][kTmaWarps][C];
-  __shared__ int s_wm[kTmaWarps][C];  // brick maxima over every stored voxel written
   __shared__ unsigned long long s_sm[2][kTmaWarps][C];
   const DenseJob j = jobs[blockIdx.x];
   const int gx = (int)(blockIdx.x % gnx);
@@ -893,14 +892,12 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma_planar(
                    ((gx >> 1) + 1) * 2 * Mx + 2 <= X && ((gy >> 1) + 1) * 2 * My + 2 <= Y;
 
   int lmn[C], lmx[C], omn[C], omx[C];
-  uint32_t wmx[C];  // max of every sample this thread stores (brick maxima)
   unsigned long long lsm[C], osm[C];
 #pragma unroll
   for (int c = 0; c < C; ++c) {
     lmn[c] = omn[c] = INT_MAX;
     lmx[c] = omx[c] = INT_MIN;
     lsm[c] = osm[c] = 0;
-    wmx[c] = 0;
   }
   const int pw = warp / WPP;                // plane of the stage this warp group builds
   const int cstr = rows * bx;               // staged channel stride (samples)
@@ -934,10 +931,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma_planar(
         const uint32_t* w = s32 + (ys * bx + xs) / 2;
         uint32_t pv[C];
 #pragma unroll
-        for (int c = 0; c < C; ++c) {
-          pv[c] = __byte_perm(w[c * cstr / 2], w[c * cstr / 2 + 1], 0x5432);
-          wmx[c] = max(wmx[c], max(pv[c] & 0xFFFFu, pv[c] >> 16));
-        }
+        for (int c = 0; c < C; ++c) pv[c] = __byte_perm(w[c * cstr / 2], w[c * cstr / 2 + 1], 0x5432);
         if (stat_plane) {
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
@@ -963,6 +957,11 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma_planar(
           o[j2] = a0 | (a1 << 16);
         }
       }
+    } else if (zs < Sz && mode == 0) {
+      // a shell plane outside the volume or the insertion: background words
+      const uint32_t bgw = (uint32_t)bg | ((uint32_t)bg << 16);
+      const int words = (int)(plane_elems / 2);
+      for (int w = (warp % WPP) * 32 + lane; w < words; w += NT) oplane[w] = bgw;
     } else if (zs < Sz) {
       const bool stat_plane = mode == 1 && !parent;
       // every lane runs the same trip count (shuffles below)
@@ -977,10 +976,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma_planar(
         uint32_t val[C];
         const uint16_t* q = iplane + ys * bx + xs;
 #pragma unroll
-        for (int c = 0; c < C; ++c) {
-          val[c] = take ? (uint32_t)q[c * cstr] : (uint32_t)bg;
-          if (act) wmx[c] = max(wmx[c], val[c]);
-        }
+        for (int c = 0; c < C; ++c) val[c] = take ? (uint32_t)q[c * cstr] : (uint32_t)bg;
         if (stat_plane && xs >= 1 && xs <= cx && ys >= 1 && ys <= cy && act) {
 #pragma unroll
           for (int c = 0; c < C; ++c) {
@@ -1125,12 +1121,10 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma_planar(
       omn[c] = min(omn[c], __shfl_xor_sync(0xffffffffu, omn[c], o));
       omx[c] = max(omx[c], __shfl_xor_sync(0xffffffffu, omx[c], o));
       osm[c] += __shfl_xor_sync(0xffffffffu, osm[c], o);
-      wmx[c] = max(wmx[c], __shfl_xor_sync(0xffffffffu, wmx[c], o));
     }
   if (lane == 0)
 #pragma unroll
     for (int c = 0; c < C; ++c) {
-      s_wm[warp][c] = (int)wmx[c];
       s_mn[0][warp][c] = lmn[c];
       s_mx[0][warp][c] = lmx[c];
       s_sm[0][warp][c] = lsm[c];
@@ -1157,6 +1151,12 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma_planar(
     stats[st_index(j.node, ST_MAX, c)] = bmx;
     stats[st_index(j.node, ST_SUBMIN, c)] = a;
     stats[st_index(j.node, ST_SUBMAX, c)] = bmx;
+    // brick maxima for the empty-space skip: before fill_borders a sample's
+    // trilinear weights on shell voxels are exactly 0 (the sampler clamps to
+    // interior centres, render/raycast.py:141-144), so the interior maximum
+    // (background for interior voxels outside the volume) bounds it;
+    // fill_borders re-derives every brick's maxima with its shells
+    if (bmax_brick) bmax_brick[(int64_t)j.slot * kMaxC + c] = (uint16_t)max(bmx, (int)bg);
     if (parent && pb != INT_MIN) {
       const int64_t pnode = (j.node - 1) >> 3;
       atomicMin(nmin + pnode * C + c, pa);
@@ -1165,14 +1165,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma_planar(
     }
   }
   if (bmax_brick) {
-    // the stored brick is complete: its maxima over every voxel (shells as
-    // written; prefilled shells only loosen the bound before fill_borders)
-    if (tid < kMaxC) {
-      int m = 0;
-      if (tid < C)
-        for (int w = 0; w < kTmaWarps; ++w) m = max(m, s_wm[w][tid]);
-      bmax_brick[(int64_t)j.slot * kMaxC + tid] = (uint16_t)m;
-    }
+    if (tid >= C && tid < kMaxC) bmax_brick[(int64_t)j.slot * kMaxC + tid] = 0;
     // sub-brick maxima unknown: never skip at sub-brick granularity
     for (int i = tid; i < nsb * kMaxC; i += kTmaWarps * 32)
       bmax_sub[(int64_t)j.slot * nsb * kMaxC + i] = 0xFFFFu;
