@@ -241,15 +241,21 @@ __global__ void __launch_bounds__(256) k_scatter(const T* __restrict__ src, int 
 // _recompute_stats, octree.py:248-263): one warp per plane of a brick job,
 // one lane per voxel of a row, warp-shuffle reductions per channel
 template <class T>
-__global__ void __launch_bounds__(256) k_plane(const PlaneJob* __restrict__ jobs, int n, Geo g,
+__global__ void __launch_bounds__(128) k_plane(const PlaneJob* __restrict__ jobs, int n, Geo g,
                                                const T* __restrict__ pool, int32_t* pmin,
                                                int32_t* pmax, unsigned long long* psum) {
+  // one CTA per (job, plane): its 4 warps split the plane's rows, lanes the
+  // voxels of a row; warp partials combine in shared memory.  Small
+  // per-insertion launches (a slice at threshold > 0) are latency bound, so
+  // every plane's rows are in flight at once rather than walked by one warp.
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int C = g.C;
   const int64_t rowstride = (int64_t)g.stored[0] * C;
+  __shared__ int s_mn[4][kMaxC], s_mx[4][kMaxC];
+  __shared__ unsigned long long s_sm[4][kMaxC];
   for (int job = blockIdx.x; job < n; job += gridDim.x) {
     const PlaneJob j = jobs[job];
-    for (int z = j.z0 + warp + blockIdx.y * nw; z < j.z1; z += nw * gridDim.y) {
+    for (int z = j.z0 + blockIdx.y; z < j.z1; z += gridDim.y) {
       const T* base = pool + (int64_t)j.slot * g.brick_elems + g.voxel_offset(z + 1, 1, 1);
       int mn[kMaxC], mx[kMaxC];
       unsigned long long sm[kMaxC];
@@ -260,7 +266,7 @@ __global__ void __launch_bounds__(256) k_plane(const PlaneJob* __restrict__ jobs
         sm[c] = 0;
       }
 #pragma unroll 4
-      for (int y = 0; y < j.cy; ++y) {
+      for (int y = warp; y < j.cy; y += nw) {
         const T* row = base + y * rowstride;
         for (int x = lane; x < j.cx; x += 32) {
 #pragma unroll
@@ -283,12 +289,27 @@ __global__ void __launch_bounds__(256) k_plane(const PlaneJob* __restrict__ jobs
           sm[c] += __shfl_xor_sync(0xffffffffu, sm[c], o);
         }
         if (lane == 0) {
-          const int64_t off = ((int64_t)j.slot * g.brick[2] + z) * C + c;
-          pmin[off] = mn[c];
-          pmax[off] = mx[c];
-          psum[off] = sm[c];
+          s_mn[warp][c] = mn[c];
+          s_mx[warp][c] = mx[c];
+          s_sm[warp][c] = sm[c];
         }
       }
+      __syncthreads();
+      if (threadIdx.x < C) {
+        const int c = threadIdx.x;
+        int a = INT_MAX, b = INT_MIN;
+        unsigned long long t = 0;
+        for (int w = 0; w < nw; ++w) {
+          a = min(a, s_mn[w][c]);
+          b = max(b, s_mx[w][c]);
+          t += s_sm[w][c];
+        }
+        const int64_t off = ((int64_t)j.slot * g.brick[2] + z) * C + c;
+        pmin[off] = a;
+        pmax[off] = b;
+        psum[off] = t;
+      }
+      __syncthreads();
     }
   }
 }
@@ -299,7 +320,11 @@ __global__ void k_reduce(const ReduceJob* __restrict__ jobs, int n, Geo g,
                          const int32_t* __restrict__ pmin, const int32_t* __restrict__ pmax,
                          const unsigned long long* __restrict__ psum,
                          const uint8_t* __restrict__ flags, int32_t* stats) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  // one warp per (node, channel): lanes take the plane partials and the
+  // children's subtree extrema, warp shuffles combine them (tiny launches
+  // per insertion at threshold > 0 are latency bound)
+  const int lane = threadIdx.x & 31;
+  const int i = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   if (i >= n * g.C) return;
   const ReduceJob j = jobs[i / g.C];
   const int c = i % g.C;
@@ -307,39 +332,50 @@ __global__ void k_reduce(const ReduceJob* __restrict__ jobs, int n, Geo g,
   if (cx > 0 && cy > 0 && cz > 0) {
     int mn = INT_MAX, mx = INT_MIN;
     unsigned long long s = 0;
-#pragma unroll 8
-    for (int z = 0; z < cz; ++z) {
-      int64_t o = ((int64_t)j.slot * g.brick[2] + z) * g.C + c;
+    for (int z = lane; z < cz; z += 32) {
+      const int64_t o = ((int64_t)j.slot * g.brick[2] + z) * g.C + c;
       mn = min(mn, pmin[o]);
       mx = max(mx, pmax[o]);
       s += psum[o];
     }
-    long long cnt = (long long)cx * cy * cz;
-    long long avg = (2 * (long long)s + cnt) / (2 * cnt);
-    stats[st_index(j.node, ST_AVG, c)] = (int)avg;
-    stats[st_index(j.node, ST_MIN, c)] = mn;
-    stats[st_index(j.node, ST_MAX, c)] = mx;
-    if (j.leafish) {
-      stats[st_index(j.node, ST_SUBMIN, c)] = mn;
-      stats[st_index(j.node, ST_SUBMAX, c)] = mx;
+    for (int o = 16; o > 0; o >>= 1) {
+      mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      s += __shfl_xor_sync(0xffffffffu, s, o);
+    }
+    if (lane == 0) {
+      const long long cnt = (long long)cx * cy * cz;
+      const long long avg = (2 * (long long)s + cnt) / (2 * cnt);
+      stats[st_index(j.node, ST_AVG, c)] = (int)avg;
+      stats[st_index(j.node, ST_MIN, c)] = mn;
+      stats[st_index(j.node, ST_MAX, c)] = mx;
+      if (j.leafish) {
+        stats[st_index(j.node, ST_SUBMIN, c)] = mn;
+        stats[st_index(j.node, ST_SUBMAX, c)] = mx;
+      }
     }
   }
   if (!j.leafish) {
-    bool any = false;
-    int lo = 0, hi = 0;
-    for (int k = 0; k < 8; ++k) {
-      if (!g.octant_real(k)) continue;
-      int64_t ch = 8 * j.node + 1 + k;
-      uint8_t f = flags[ch];
-      if (!(f & NF_EXISTS) || !(f & NF_INVOL)) continue;
-      int a = stats[st_index(ch, ST_SUBMIN, c)], b = stats[st_index(ch, ST_SUBMAX, c)];
-      lo = any ? min(lo, a) : a;
-      hi = any ? max(hi, b) : b;
-      any = true;
+    // lanes 0..7: the children's subtree extrema (existing, in volume)
+    bool ok = false;
+    int a = INT_MAX, b = INT_MIN;
+    if (lane < 8 && g.octant_real(lane)) {
+      const int64_t ch = 8 * j.node + 1 + lane;
+      const uint8_t f = flags[ch];
+      if ((f & NF_EXISTS) && (f & NF_INVOL)) {
+        ok = true;
+        a = stats[st_index(ch, ST_SUBMIN, c)];
+        b = stats[st_index(ch, ST_SUBMAX, c)];
+      }
     }
-    if (any) {
-      stats[st_index(j.node, ST_SUBMIN, c)] = lo;
-      stats[st_index(j.node, ST_SUBMAX, c)] = hi;
+    const bool any = __any_sync(0xffffffffu, ok);
+    for (int o = 4; o > 0; o >>= 1) {
+      a = min(a, __shfl_xor_sync(0xffffffffu, a, o));
+      b = max(b, __shfl_xor_sync(0xffffffffu, b, o));
+    }
+    if (lane == 0 && any) {
+      stats[st_index(j.node, ST_SUBMIN, c)] = a;
+      stats[st_index(j.node, ST_SUBMAX, c)] = b;
     }
   }
 }
@@ -742,20 +778,20 @@ void launch_octant(const Tree& t, const OctJob* d, int n) {
 
 void launch_plane(const Tree& t, const PlaneJob* d, int n) {
   if (n <= 0) return;
-  const dim3 grid((unsigned)std::min<int64_t>(n, 148 * 64), split_for(n, 8));
+  const dim3 grid((unsigned)std::min<int64_t>(n, 148 * 64), split_for(n, 32));
   if (t.g.sb == 1)
-    k_plane<uint8_t><<<grid, 256, 0, t.stream>>>(d, n, t.g, t.d_pool, t.d_pmin, t.d_pmax,
+    k_plane<uint8_t><<<grid, 128, 0, t.stream>>>(d, n, t.g, t.d_pool, t.d_pmin, t.d_pmax,
                                                   t.d_psum);
   else
-    k_plane<uint16_t><<<grid, 256, 0, t.stream>>>(d, n, t.g, (const uint16_t*)t.d_pool, t.d_pmin,
+    k_plane<uint16_t><<<grid, 128, 0, t.stream>>>(d, n, t.g, (const uint16_t*)t.d_pool, t.d_pmin,
                                                    t.d_pmax, t.d_psum);
   VT_CHECK_LAUNCH();
 }
 
 void launch_reduce(const Tree& t, const ReduceJob* d, int n) {
   if (n <= 0) return;
-  int work = n * t.g.C;
-  k_reduce<<<(work + kThreads - 1) / kThreads, kThreads, 0, t.stream>>>(
+  const int64_t work = (int64_t)n * t.g.C * 32;  // a warp per (node, channel)
+  k_reduce<<<(unsigned)((work + 127) / 128), 128, 0, t.stream>>>(
       d, n, t.g, t.d_pmin, t.d_pmax, t.d_psum, t.d_flags, t.d_stats);
   VT_CHECK_LAUNCH();
 }
