@@ -791,10 +791,11 @@ __device__ bool composite(const TFTable& T, const double* vals, RayOut& o, Count
 }
 
 // finalize_image (core.py:137-155)
-template <int NC>
+// MODE: 0 DVR, 1 MIP, -1 read P.mip at run time
+template <int NC, int MODE = -1>
 __device__ void finalize(const TFTable& T, const RayOut& o, double px[4], Counters& cnt) {
   const RenderParams& P = c_P;
-  if (!P.mip) {
+  if (MODE == 0 || (MODE < 0 && !P.mip)) {
     px[0] = o.rgb[0];
     px[1] = o.rgb[1];
     px[2] = o.rgb[2];
@@ -895,7 +896,7 @@ __device__ __forceinline__ void march_ray(S& s, const TFTable& tf, const double 
 }
 
 #ifndef VT_RENDER_MINB
-#define VT_RENDER_MINB 4
+#define VT_RENDER_MINB 5
 #endif
 template <class T, int NC, bool TR, bool FAST, int FILLED>
 __global__ void __launch_bounds__(128, VT_RENDER_MINB) k_render_fullframe(const uint64_t* __restrict__ nb,
@@ -919,10 +920,15 @@ __global__ void __launch_bounds__(128, VT_RENDER_MINB) k_render_fullframe(const 
     long long n;
     ray_setup(d, t0, n);
     RayOut o{};
-    // one uniform branch per ray instead of a mode test per sample
-    if (P.mip) march_ray<1>(s, tf, d, t0, n, o);
-    else march_ray<0>(s, tf, d, t0, n, o);
-    finalize<NC>(tf, o, px, cnt);
+    // one uniform branch per ray instead of a mode test per sample (the DVR
+    // branch never keeps the MIP maxima live)
+    if (P.mip) {
+      march_ray<1>(s, tf, d, t0, n, o);
+      finalize<NC, 1>(tf, o, px, cnt);
+    } else {
+      march_ray<0>(s, tf, d, t0, n, o);
+      finalize<NC, 0>(tf, o, px, cnt);
+    }
     write = true;
   } else if (P.n_parts > 1 && i < P.rect[2] && jl < out_rows) {
     // padding rows of the last strip: deterministic zeros
