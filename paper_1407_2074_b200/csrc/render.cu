@@ -717,7 +717,9 @@ struct Sampler {
 
 // composite_step (core.py:110-134); returns terminated
 // MODE: 0 DVR, 1 MIP, -1 read P.mip at run time
-template <int NC, int MODE = -1>
+// COUNT: tally the TF lookups here (false: the full-frame DVR march derives
+// them as C per counted sample once, at the end of the ray)
+template <int NC, int MODE = -1, bool COUNT = true>
 __device__ bool composite(const TFTable& T, const float* vals, RayOut& o, Counters& cnt) {
   // float reconstruction path: per-sample TF / intermix in FP32, the ray's
   // front-to-back accumulation in FP64
@@ -734,7 +736,7 @@ __device__ bool composite(const TFTable& T, const float* vals, RayOut& o, Counte
 #pragma unroll
   for (int c = 0; c < C; ++c) {
     const float x = vals[c] * (float)P.inv_fmax;
-    cnt.tf++;
+    if (COUNT) cnt.tf++;
     if (x <= T.xzf[c]) continue;
     any = true;
     float rgba[4];
@@ -753,7 +755,7 @@ __device__ bool composite(const TFTable& T, const float* vals, RayOut& o, Counte
   return P.has_et && o.a >= P.et;
 }
 
-template <int NC, int MODE = -1>
+template <int NC, int MODE = -1, bool COUNT = true>
 __device__ bool composite(const TFTable& T, const double* vals, RayOut& o, Counters& cnt) {
   const RenderParams& P = c_P;
   constexpr int C = NC;
@@ -768,7 +770,7 @@ __device__ bool composite(const TFTable& T, const double* vals, RayOut& o, Count
 #pragma unroll
   for (int c = 0; c < C; ++c) {
     const double x = vals[c] * P.inv_fmax;
-    cnt.tf++;
+    if (COUNT) cnt.tf++;
     // alpha exactly 0: rgb * 0 and (1 - 0) change nothing — skip the lookup
     if (x <= T.xzero[c]) continue;
     any = true;
@@ -868,12 +870,12 @@ __device__ void store_px(void* out, int kind, int64_t r, const double px[4]) {
 // composite, early termination; transparent runs skipped exactly
 template <int MODE, class S>
 __device__ __forceinline__ void march_ray(S& s, const TFTable& tf, const double d[3], double t0,
-                                          long long n, RayOut& o) {
+                                          int n, RayOut& o) {
   const RenderParams& P = c_P;
   constexpr int NC = S::kC;
   typename S::V vals[NC];
   Counters& cnt = s.cnt;
-  for (long long k = 0; k < n; ++k) {
+  for (int k = 0; k < n; ++k) {
     double t = t0 + (double)k * P.step;
     double p[3];
 #pragma unroll
@@ -883,16 +885,18 @@ __device__ __forceinline__ void march_ray(S& s, const TFTable& tf, const double 
     if (MODE == 0 && s.hint) {
       // transparent (TF alpha exactly 0): compositing is a no-op; account
       // this sample and the provably transparent run after it
-      const long long m = s.skip_count(k, n, t0, d);
-      cnt.samples += (int)m;
-      cnt.skipped += (int)m;
-      cnt.tf += (int)(m + 1) * NC;
-      if (s.hint == 1) cnt.used += (int)m;
+      const int m = (int)s.skip_count(k, n, t0, d);
+      cnt.samples += m;
+      cnt.skipped += m;
+      if (s.hint == 1) cnt.used += m;
       k += m;
       continue;
     }
-    if (composite<NC, MODE>(tf, vals, o, cnt)) break;
+    if (composite<NC, MODE, MODE != 0>(tf, vals, o, cnt)) break;
   }
+  // DVR: every counted sample looks up each channel's TF once (composite
+  // or the exact skip) — render/core.py:122
+  if (MODE == 0) cnt.tf += cnt.samples * NC;  // one ray per thread: its own samples
 }
 
 #ifndef VT_RENDER_MINB
@@ -923,10 +927,10 @@ __global__ void __launch_bounds__(128, VT_RENDER_MINB) k_render_fullframe(const 
     // one uniform branch per ray instead of a mode test per sample (the DVR
     // branch never keeps the MIP maxima live)
     if (P.mip) {
-      march_ray<1>(s, tf, d, t0, n, o);
+      march_ray<1>(s, tf, d, t0, (int)n, o);
       finalize<NC, 1>(tf, o, px, cnt);
     } else {
-      march_ray<0>(s, tf, d, t0, n, o);
+      march_ray<0>(s, tf, d, t0, (int)n, o);
       finalize<NC, 0>(tf, o, px, cnt);
     }
     write = true;
@@ -1387,6 +1391,14 @@ void fill_params(const vt_mirror* m, const vt_scene* s, RenderParams& P) {
   P.bmax = m->d_bmax;
   P.bmax_brick = m->d_bmax_brick;
   P.inv_step = 1.0 / P.step;
+  {
+    // the full-frame march counts samples in 32 bits: a ray through the
+    // whole box takes at most |box| / step + 1 of them
+    const double diag = std::sqrt(P.box_hi[0] * P.box_hi[0] + P.box_hi[1] * P.box_hi[1] +
+                                  P.box_hi[2] * P.box_hi[2]);
+    VT_REQUIRE(diag / P.step + 2.0 < 2147483647.0, VT_EINVAL,
+               "sampling step too small: over 2^31 samples per ray");
+  }
   sub_bricks(t.g, P.sbk, P.nsub);
   P.nsb = P.nsub[0] * P.nsub[1] * P.nsub[2];
   for (int c = 0; c < kMaxC; ++c) P.ess_thr[c] = -1;
