@@ -99,6 +99,11 @@ struct RenderParams {
   const uint16_t* bmax_brick;  // [slot][kMaxC] whole-brick maxima
   double inv_step;
   int sbk[3], nsub[3], nsb;  // sub-brick edge, count per axis, total
+  // node / flag / brick buffers of this launch: read from constant memory
+  // where used rather than held in registers for the whole ray
+  const uint64_t* buf_nb;
+  uint8_t* buf_fb;
+  const void* buf_bb;
 };
 
 // per-launch scene + geometry; render entry points serialise on g_render_mu
@@ -303,9 +308,6 @@ template <class T, int NC, bool TR, bool FAST = false, int FILLED = -1>
 struct Sampler {
   using V = typename std::conditional<FAST, float, double>::type;
   static constexpr int kC = NC;
-  const uint64_t* __restrict__ nb;
-  uint8_t* fb;
-  const T* __restrict__ bb;
   bool fullframe;
   Counters cnt;  // by value: stays in registers
   int last_used = -1, last_req = -1;
@@ -317,8 +319,11 @@ struct Sampler {
   int hint_sb = -1;
   DescentCache cache[TR ? NC : 1];
 
-  __device__ Sampler(const uint64_t* n, uint8_t* f, const T* b, bool ff)
-      : nb(n), fb(f), bb(b), fullframe(ff), cnt{0, 0, 0, 0, 0, 0, 0} {
+  __device__ static const uint64_t* nbuf() { return P.buf_nb; }
+  __device__ static uint8_t* fbuf() { return P.buf_fb; }
+  __device__ static const T* bbuf() { return static_cast<const T*>(P.buf_bb); }
+  __device__ Sampler(const uint64_t*, uint8_t*, const T*, bool ff)
+      : fullframe(ff), cnt{0, 0, 0, 0, 0, 0, 0} {
 #pragma unroll
     for (int q = 0; q < (TR ? NC : 1); ++q) {
       cache[q].target = -1;
@@ -337,7 +342,7 @@ struct Sampler {
     last = idx;
     const unsigned peers = __match_any_sync(__activemask(), idx);
     if ((int)(threadIdx.x & 31) != __ffs(peers) - 1) return;
-    unsigned* w = reinterpret_cast<unsigned*>(fb + (idx & ~3));
+    unsigned* w = reinterpret_cast<unsigned*>(fbuf() + (idx & ~3));
     unsigned bit = flag << ((idx & 3) * 8);
     if (!(__ldcg(w) & bit)) atomicOr(w, bit);
   }
@@ -372,7 +377,7 @@ struct Sampler {
     constexpr int C = NC;
     // 32-bit offsets inside a brick (a stored brick is < 2^31 samples)
     const int sxC = P.g.stored[0] * C, sxyC = sxC * P.g.stored[1];
-    const T* p = bb + slot * P.g.brick_elems + (i0[2] * sxyC + i0[1] * sxC + i0[0] * C);
+    const T* p = bbuf() + slot * P.g.brick_elems + (i0[2] * sxyC + i0[1] * sxC + i0[0] * C);
     if (FAST) {
       // FP32: lerp along x, then y, then z (7 FMAs per channel)
       float fx = (float)w1[0], fy = (float)w1[1], fz = (float)w1[2];
@@ -428,7 +433,7 @@ struct Sampler {
     int lvl = P.g.depth;
     int lo[3] = {0, 0, 0};
     for (int it = 0; it < P.g.depth; ++it) {
-      uint64_t e = __ldg(nb + idx);
+      uint64_t e = __ldg(nbuf() + idx);
       int ptr = (int)((e >> 2) & 0x3FFFFFULL);
       if (!(ptr != 0 && lvl > target)) break;
       int k = 0;
@@ -462,7 +467,7 @@ struct Sampler {
     int idx = 0, l = P.g.depth;
     int lo[3] = {0, 0, 0};
     while (l > lvl) {
-      const uint64_t e = __ldg(nb + idx);
+      const uint64_t e = __ldg(nbuf() + idx);
       const int ptr = (int)((e >> 2) & 0x3FFFFFULL);
       aidx[1] = aidx[0];
       alvl[1] = alvl[0];
@@ -520,7 +525,7 @@ struct Sampler {
   __device__ bool resolve(const double pv[3], int target, int c0, int c1, V* out,
                           DescentCache& dc) {
     const bool moved = descend(pv, target, dc);
-    const uint64_t e = __ldg(nb + dc.idx);
+    const uint64_t e = __ldg(nbuf() + dc.idx);
     const bool resident = e & 1, nh = e & 2;
     if (moved) dc.clear = node_clear(e, c0, c1);
     if (!nh) {
@@ -576,7 +581,7 @@ struct Sampler {
     for (int q = 0; q < 2; ++q) {
       const int ai = aidx[q];
       if (ai < 0) continue;
-      uint64_t ae = __ldg(nb + ai);
+      uint64_t ae = __ldg(nbuf() + ai);
       if (ae & 1) {
         trilerp(ae, alvl[q], alo[q], pv, c0, c1, out);
         mark(ai, 1);
@@ -1771,6 +1776,9 @@ static void render_rect(vt_mirror* m, const vt_scene* scene, const int32_t* rect
   VT_CUDA(cudaMemsetAsync(dc, 0, 7 * sizeof(unsigned long long), t.stream));
   dim3 grid((rw + VT_TW - 1) / VT_TW, (rh + 4 * (32 / VT_TW) - 1) / (4 * (32 / VT_TW)));
   VT_CUDA(cudaEventRecord(t.ev0, t.stream));
+  P.buf_nb = m->d_nb;
+  P.buf_fb = m->d_fb;
+  P.buf_bb = brick_ptr(m);
   set_params(P, t.stream);
   if (px > 0) {
     dispatch(t.g.sb, t.g.C, P.has_tr != 0, [&](auto tag, auto nc, auto tr) {
@@ -1897,6 +1905,9 @@ vt_status vt_rays_march(vt_rays* r, int32_t strategy, vt_counters* cnt, int64_t*
     VT_CUDA(cudaMallocAsync(&dc, 8 * sizeof(unsigned long long), t.stream));
     VT_CUDA(cudaMemsetAsync(dc, 0, 8 * sizeof(unsigned long long), t.stream));
     dim3 grid((P.W + VT_TW - 1) / VT_TW, (P.H + 4 * (32 / VT_TW) - 1) / (4 * (32 / VT_TW)));
+    P.buf_nb = m->d_nb;
+    P.buf_fb = m->d_fb;
+    P.buf_bb = brick_ptr(m);
     set_params(P, t.stream);
     dispatch(t.g.sb, t.g.C, P.has_tr != 0, [&](auto tag, auto nc, auto tr) {
       using T = decltype(tag);
