@@ -450,8 +450,10 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma(
   const int x0 = gx * Mx - 1, y0 = gy * My - 1;     // block voxel of stored (0, 0)
   const int xa = x0 * C - (((x0 * C) % 8 + 8) % 8);  // 16-byte aligned tile start (samples)
   const int xoff = x0 * C - xa;                     // leading samples of a staged row
-  const bool xfull = prefill && x0 >= 0 && x0 + Sx <= X;  // every stored x inside the volume
-  const bool yfull = y0 >= 0 && y0 + Sy <= Y;              // every stored row inside it
+  // every stored x / row inside the volume — or a zero background, which the
+  // TMA tile's zero fill outside the volume reproduces
+  const bool xfull = prefill && (bg == 0 || (x0 >= 0 && x0 + Sx <= X));
+  const bool yfull = bg == 0 || (y0 >= 0 && y0 + Sy <= Y);
   // e / (Sx * C) and e / C by multiply-high (e < 2^16; a divisor of 1 has no
   // 32-bit magic)
   const uint32_t rowmagic = (uint32_t)((((uint64_t)1 << 32) + Sx * C - 1) / (Sx * C));
@@ -852,7 +854,10 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma_planar(
   const int xa = x0 - ((x0 % 8 + 8) % 8);        // 16-byte aligned tile start (samples)
   const int xoff = x0 - xa;                      // leading samples of a staged row (odd)
   // every stored voxel of a block plane inside the volume (prefilled shells)
-  const bool xyfull = prefill && x0 >= 0 && x0 + Sx <= X && y0 >= 0 && y0 + Sy <= Y;
+  // (with a zero background the TMA tile's zero fill outside the volume IS
+  // the background, so bricks on the volume's x/y faces take this path too)
+  const bool xyfull =
+      prefill && (bg == 0 || (x0 >= 0 && x0 + Sx <= X && y0 >= 0 && y0 + Sy <= Y));
 
   if (tid == 0) {
     for (int b = 0; b < kPStages; ++b) mbar_init(&s_bar[b], 1);
