@@ -375,6 +375,11 @@ void sort_indices(std::vector<int64_t>& v) {
 }
 
 void Tree::mark_struct(int64_t idx) {
+  if (struct_range) {
+    struct_lo = std::min(struct_lo, idx);
+    struct_hi = std::max(struct_hi, idx);
+    return;
+  }
   if (leaf_struct_by_kernel && idx >= g.level_start[g.depth] && (flags[idx] & NF_INVOL)) return;
   if (!struct_mark[idx]) {
     struct_mark[idx] = 1;
@@ -395,6 +400,32 @@ int32_t Tree::alloc_slot() {
     ensure_pool(cursor);
   }
   return s;
+}
+
+// ensure_children for a node on a leaf's descent path whose box follows
+// from the leaf's grid coordinates (no index decoding); in fast_create mode
+// (complete grid) every child is in volume and needs no seed job
+void Tree::ensure_children_at(int64_t p, int lvl, const int gg[3]) {
+  if (!fast_create) {
+    ensure_children(p);
+    return;
+  }
+  if (flags[p] & NF_CHILDREN) return;
+  flags[p] |= NF_CHILDREN;
+  mark_struct(p);
+  (void)lvl;
+  (void)gg;
+  const int64_t c0 = 8 * p + 1;
+  for (int k = 0; k < 8; ++k) {
+    flags[c0 + k] = NF_EXISTS | NF_INVOL;
+    slot[c0 + k] = -1;
+  }
+  mark_struct(c0);
+  mark_struct(c0 + 7);
+  node_count += 8;
+  const size_t e0 = events.size();
+  events.resize(e0 + 8);
+  for (int k = 0; k < 8; ++k) events[e0 + k] = ev_pack(VT_EV_CREATED, c0 + k);
 }
 
 void Tree::ensure_children(int64_t p) {
@@ -457,6 +488,17 @@ void Tree::free_brick(int64_t n) {
 }
 
 void Tree::flush_structure() {
+  if (struct_hi >= struct_lo) {
+    // a range-mode insertion: one copy of the flag and slot ranges
+    const int64_t lo = struct_lo, span = struct_hi - struct_lo + 1;
+    struct_lo = INT64_MAX;
+    struct_hi = -1;
+    void* df = stage_copy(flags.data() + lo, span);
+    VT_CUDA(cudaMemcpyAsync(d_flags + lo, df, span, cudaMemcpyDeviceToDevice, stream));
+    void* ds = stage_copy(slot.data() + lo, span * sizeof(int32_t));
+    VT_CUDA(cudaMemcpyAsync(d_slot + lo, ds, span * sizeof(int32_t), cudaMemcpyDeviceToDevice,
+                            stream));
+  }
   if (struct_dirty.empty()) return;
   int64_t lo = g.capacity, hi = -1;
   for (int64_t i : struct_dirty) {
@@ -790,6 +832,7 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
     struct_dirty.reserve(struct_dirty.size() + nl * 2 + 64);
   }
   auto* walk_scope = new ProfScope(prof, 1);
+  fast_create = struct_range = early_full;
 
   // leaves (octree.py:351-360): descend, create, ensure brick, dirty box
   auto* leaf_scope = new ProfScope(prof, 8);
@@ -804,7 +847,7 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
           // and seeds exactly as the reference's descent)
           int64_t a = 0;
           for (int lvl = g.depth; lvl > 0; --lvl) {
-            ensure_children(a);
+            ensure_children_at(a, lvl, gg);
             int k = 0;
             for (int q = 0; q < 3; ++q)
               if (g.split[q] && ((gg[q] >> (lvl - 1)) & 1)) k |= 1 << q;
@@ -1022,6 +1065,7 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
   }
   std::unique_ptr<SideJoin> side_join(new SideJoin{*this, side});
   { ProfScope q(prof, 5); flush_structure(); }
+  fast_create = struct_range = false;
   CreateJob* dc;
   SeedJob* ds;
   {

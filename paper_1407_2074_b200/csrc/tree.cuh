@@ -4,6 +4,7 @@
 #pragma once
 
 #include <algorithm>
+#include <climits>
 #include <array>
 #include <atomic>
 #include <chrono>
@@ -424,6 +425,14 @@ struct Tree {
     return k >= 0 ? &pend_pool[lvl][k] : (k == -2 ? &dense_pending : nullptr);
   }
 
+  // complete-grid whole-volume insertion (every node in volume, every
+  // created node's statistics rewritten by the dense kernels before anything
+  // reads them): ensure_children skips the CreateJob / seed bookkeeping, and
+  // structure records are one dirty index range
+  bool fast_create = false;
+  bool struct_range = false;
+  int64_t struct_lo = INT64_MAX, struct_hi = -1;
+  void ensure_children_at(int64_t p, int lvl, const int gg[3]);
   // -- per-insertion device work lists --
   std::vector<int64_t> struct_dirty;
   std::vector<uint8_t> struct_mark;
