@@ -83,12 +83,113 @@ def _worker(rank, world, port, strip_rows, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("strip_rows", [8, 5])
-def test_two_ranks_sharded_build_and_sort_first_render(tmp_path, strip_rows):
-    from gpu_helpers import counters_dict
+def _reference(tmp_path):
+    """The single-process reference: one bulk build, one full frame."""
     from paper_1407_2074_b200 import DeviceState
     from paper_1407_2074_b200.render import OutOfCoreRenderer
     from paper_1407_2074_b200 import render as R
+    vol = _volume()
+    t = _tree()
+    t.insert_channels((0, 0, 0), vol)
+    t.finalize()
+    t.fill_borders()
+    img, cnt = OutOfCoreRenderer(DeviceState(t, resident_all=True)).render_fullframe(_scene(R))
+    return t.checksum(), img, cnt
+
+
+def _nccl_worker(port, q):
+    """One NCCL rank (NCCL will not put two ranks on one GPU) playing both
+    slabs of a two-slab plan: slab 1's records go through the real NCCL
+    device collectives of the sharded build (`_all_gather_records`: meta
+    all-gather, record and brick all_gather_into_tensor on device buffers)
+    and are merged into the slab-0 tree; the frame is then rendered as two
+    sort-first strip sets whose parts and counters go through NCCL gather /
+    all-reduce on device tensors."""
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path.insert(0, here)
+    sys.path.insert(0, os.path.join(os.path.dirname(here), "oracle"))
+    sys.path.insert(0, os.path.dirname(here))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        from paper_1407_2074_b200 import DeviceState
+        from paper_1407_2074_b200 import render as R
+        from paper_1407_2074_b200.render.sharded import SortFirstRenderer, assemble
+        from paper_1407_2074_b200 import slab_build as sb
+        vol = torch.from_numpy(np.ascontiguousarray(_volume())).cuda()
+        plan = sb.slab_plan(_tree().geometry, 2)
+        trees = []
+        for z0, z1 in plan.slabs:
+            t = _tree()
+            for z in range(z0, z1, 32):
+                t.insert_channels((0, 0, z), vol[z:min(z1, z + 32)].contiguous())
+            t.sync()
+            trees.append(t)
+        z0, z1 = plan.slabs[1]
+        idx, flags, stats, bricks = sb.export_records(trees[1], sb.slab_records(trees[1], plan, z0, z1))
+        parts = sb._all_gather_records(idx, flags, stats, bricks, trees[1].inserted_voxels,
+                                       trees[1], None)
+        assert len(parts) == 1 and parts[0][3].is_cuda
+        assert np.array_equal(parts[0][0], idx) and np.array_equal(parts[0][2], stats)
+        t = trees[0]
+        sb.merge_records(t, *parts[0])
+        t.finalize()
+        t.fill_borders()
+        ck = t.checksum()
+        dev = DeviceState(t, resident_all=True)
+        scene = _scene(R)
+        # two virtual ranks' strips, rendered then exchanged through NCCL
+        locs, cnts = [], []
+        for r in range(2):
+            sfr = SortFirstRenderer(dev, strip_rows=8)
+            sfr.world, sfr.rank = 2, r
+            loc, c = sfr.render_part(scene, R.raycast.OUT_F64)
+            locs.append(loc.clone())
+            cnts.append(c)
+        torch.cuda.synchronize()
+        g = torch.stack(locs)
+        out = torch.empty_like(g)
+        dist.all_gather_into_tensor(out.view(-1), g.view(-1))
+        fields = list(cnts[0].__dataclass_fields__)
+        v = torch.tensor([[getattr(c, f) for f in fields] for c in cnts], dtype=torch.int64,
+                         device="cuda").sum(0)
+        dist.all_reduce(v)
+        img = assemble(out, scene.camera.height, 8)
+        np.save(os.path.join(os.environ["VT_TEST_TMP"], "nccl.npy"), img.cpu().numpy())
+        q.put({"backend": dist.get_backend(), "checksum": ck,
+               "counters": dict(zip(fields, (int(x) for x in v.tolist())))})
+        dev.close()
+        for tt in trees:
+            tt.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nccl_sharded_build_exchange_and_sort_first_render(tmp_path):
+    from gpu_helpers import counters_dict
+    os.environ["VT_TEST_TMP"] = str(tmp_path)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_worker, args=(_free_port(), q))
+    p.start()
+    res = q.get(timeout=600)
+    p.join(timeout=120)
+    assert p.exitcode == 0
+    ref_ck, img, cnt = _reference(tmp_path)
+    assert res["backend"] == "nccl"
+    assert res["checksum"] == ref_ck
+    assert res["counters"] == counters_dict(cnt)
+    got = np.load(os.path.join(str(tmp_path), "nccl.npy"))
+    assert got.shape == img.shape and np.array_equal(got, img)
+
+
+@pytest.mark.parametrize("strip_rows", [8, 5])
+def test_two_ranks_sharded_build_and_sort_first_render(tmp_path, strip_rows):
+    from gpu_helpers import counters_dict
     os.environ["VT_TEST_TMP"] = str(tmp_path)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -103,14 +204,7 @@ def test_two_ranks_sharded_build_and_sort_first_render(tmp_path, strip_rows):
         p.join(timeout=120)
         assert p.exitcode == 0
     res.sort(key=lambda r: r["rank"])
-    # the single-process reference: one bulk build, one full frame
-    vol = _volume()
-    t = _tree()
-    t.insert_channels((0, 0, 0), vol)
-    t.finalize()
-    t.fill_borders()
-    ref_ck = t.checksum()
-    img, cnt = OutOfCoreRenderer(DeviceState(t, resident_all=True)).render_fullframe(_scene(R))
+    ref_ck, img, cnt = _reference(tmp_path)
     assert res[0]["slabs"] != [[0, DIMS[2]]]  # really split in z
     for r in res:
         assert r["checksum"] == ref_ck, r["rank"]
