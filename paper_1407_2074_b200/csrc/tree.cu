@@ -1195,9 +1195,9 @@ void Tree::insert_staged(int channel, const int origin[3], const int dims[3], co
     propagate();
     std::vector<int64_t> all;
     for (auto& v : touched) all.insert(all.end(), v.begin(), v.end());
-    gather_stats(all);
-    prune(touched, dmark, deleted);
-    flush_structure();
+    { ProfScope q(prof, 37); gather_stats(all); }
+    { ProfScope q(prof, 38); prune(touched, dmark, deleted); }
+    { ProfScope q(prof, 39); flush_structure(); }
   }
   // NODE_UPDATED for every touched, non-deleted node, sorted (octree.py:393-395)
   // every level's list is sorted and unique and higher levels hold smaller

@@ -58,7 +58,7 @@ struct Pending {
 // tree is destroyed
 struct HostProf {
   bool on = false;
-  static constexpr int kN = 37;
+  static constexpr int kN = 40;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // insert entry, leaf launch, leaf end, insert end
   bool ev_armed = false;
   double t[kN] = {0};
@@ -70,7 +70,8 @@ struct HostProf {
                                 "gpu_entry_to_leaf", "gpu_leaf", "gpu_leaf_to_end",
                                 "eligible", "pre_parents", "pre_anc", "pre_djobs",
                                 "pre_pads", "pre_fused_up", "pre_djob_up", "pre_leaf_launch",
-                                "chain", "leaf_brick", "fused_scan", "touch", "held", "owed"};
+                                "chain", "leaf_brick", "fused_scan", "touch", "held", "owed",
+                                "tau_gather", "tau_prune", "tau_flush"};
     return n[i];
   }
 };
