@@ -931,9 +931,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma_planar(
           reinterpret_cast<const uint32_t*>(stage) + (pw * RS * bx + xoff - 1) / 2;
       const int pt = (warp % WPP) * 32 + lane;
       const int SP = Sx / 2;  // voxel pairs per stored row
-      for (int q = pt; q < Sy * SP; q += NT) {
-        const int ys = q / SP, xs = 2 * (q - ys * SP);
-        const uint32_t* w = s32 + (ys * bx + xs) / 2;
+      auto pair = [&](int ys, int xs, const uint32_t* w, uint32_t* o) {
         uint32_t pv[C];
 #pragma unroll
         for (int c = 0; c < C; ++c) pv[c] = __byte_perm(w[c * cstr / 2], w[c * cstr / 2 + 1], 0x5432);
@@ -952,14 +950,39 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_dense_leaf_tma_planar(
             }
           }
         }
-        uint32_t* o = oplane + (size_t)q * C;
+        if (C == 3) {
+          // (v0c0 | v0c1), (v0c2 | v1c0), (v1c1 | v1c2): one byte permute each
+          o[0] = __byte_perm(pv[0], pv[1 % C], 0x5410);
+          o[1] = __byte_perm(pv[2 % C], pv[0], 0x7610);
+          o[2] = __byte_perm(pv[1 % C], pv[2 % C], 0x7632);
+        } else {
 #pragma unroll
-        for (int j2 = 0; j2 < C; ++j2) {
-          // samples 2 j2 and 2 j2 + 1 of the pair: voxel k / C, channel k % C
-          const int k0 = 2 * j2, k1 = 2 * j2 + 1;
-          const uint32_t a0 = k0 / C ? (pv[k0 % C] >> 16) : (pv[k0 % C] & 0xFFFFu);
-          const uint32_t a1 = k1 / C ? (pv[k1 % C] >> 16) : (pv[k1 % C] & 0xFFFFu);
-          o[j2] = a0 | (a1 << 16);
+          for (int j2 = 0; j2 < C; ++j2) {
+            // samples 2 j2 and 2 j2 + 1 of the pair: voxel k / C, channel k % C
+            const int k0 = 2 * j2, k1 = 2 * j2 + 1;
+            const uint32_t a0 = k0 / C ? (pv[k0 % C] >> 16) : (pv[k0 % C] & 0xFFFFu);
+            const uint32_t a1 = k1 / C ? (pv[k1 % C] >> 16) : (pv[k1 % C] & 0xFFFFu);
+            o[j2] = a0 | (a1 << 16);
+          }
+        }
+      };
+      // Each thread owns one pair column xp of rows y0, y0 + RSTEP, ...
+      // (RSTEP = NT / SP rows per pass: 7 x 17 of the 128 threads for 32^3
+      // bricks), so the per-pair index arithmetic reduces to two pointer
+      // increments; the staged row stride bx is even
+      const int RSTEP = NT / SP;
+      if (RSTEP > 0) {
+        if (pt < RSTEP * SP) {
+          const int y0 = pt / SP, xp = pt - y0 * SP;
+          const uint32_t* w = s32 + y0 * (bx / 2) + xp;
+          uint32_t* o = oplane + (size_t)(y0 * SP + xp) * C;
+          for (int ys = y0; ys < Sy; ys += RSTEP, w += RSTEP * (bx / 2), o += RSTEP * SP * C)
+            pair(ys, 2 * xp, w, o);
+        }
+      } else {
+        for (int q = pt; q < Sy * SP; q += NT) {
+          const int ys = q / SP, xs = 2 * (q - ys * SP);
+          pair(ys, xs, s32 + (ys * bx + xs) / 2, oplane + (size_t)q * C);
         }
       }
     } else if (zs < Sz && mode == 0) {
