@@ -293,6 +293,32 @@ struct DescentCache {
   int lo[3];   // box origin; the box is [lo, lo + exti[lvl])
 };
 
+// Exact integer <-> FP64 conversions on the FP64 pipe instead of the
+// quarter-rate conversion (XU) pipe, which the per-sample I2F/F2I ops (24
+// corner conversions, cell floors, box origins) otherwise saturate: for an
+// integer 0 <= v < 2^31 the double 2^52 + v is exact and its low word is v.
+constexpr double kMagic52 = 4503599627370496.0;  // 2^52
+__device__ __forceinline__ double magic_of(unsigned v) {
+  return __hiloint2double(0x43300000, (int)v);  // == 2^52 + v
+}
+// (double)v for 0 <= v < 2^31
+__device__ __forceinline__ double exact_d(int v) { return magic_of((unsigned)v) - kMagic52; }
+// (double)v for any 32-bit v: the double with high word 0x43380000 and low
+// word v + 2^31 is exactly 2^52 + 2^51 + 2^31 + v
+__device__ __forceinline__ double exact_sd(int v) {
+  return __hiloint2double(0x43380000, v ^ (int)0x80000000) - 6755401588539392.0;
+}
+// floor(x) for 0 <= x < 2^31, as an int and as a double (2^52 + x rounded
+// toward -inf holds floor(x) in its low word)
+__device__ __forceinline__ int floor_nonneg(double x, double& fl) {
+  const double t = __dadd_rd(x, kMagic52);
+  fl = t - kMagic52;
+  return __double2loint(t);
+}
+__device__ __forceinline__ int floor_nonneg(double x) {
+  return __double2loint(__dadd_rd(x, kMagic52));
+}
+
 // floor(log2(v)) for a positive normal double: its unbiased exponent
 __device__ __forceinline__ int floor_log2(double v) {
   return (int)((__double_as_longlong(v) >> 52) & 0x7FF) - 1023;
@@ -363,16 +389,20 @@ struct Sampler {
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       // scale is a power of two: multiplying by its reciprocal is exact
-      double f = (pv[a] - (double)lo[a]) * P.inv_scl[lvl][a] + 0.5;
+      double f = (pv[a] - exact_d(lo[a])) * P.inv_scl[lvl][a] + 0.5;
       // inside the node box f is in [0.5, M + 0.5): with filled borders the
       // reference's clip to [0, M + 1] and the index clip to [0, M] are
       // no-ops; before fill_borders samples clamp to interior centres
-      if (!filled) f = npclip(f, 1.0, (double)P.g.brick[a]);
-      int fi = (int)floor(f);
-      if (filled) fi = fi > P.g.brick[a] ? P.g.brick[a] : fi;
+      if (!filled) f = npclip(f, 1.0, exact_d(P.g.brick[a]));
+      double fl;
+      int fi = floor_nonneg(f, fl);  // f >= 0.5
+      if (filled && fi > P.g.brick[a]) {
+        fi = P.g.brick[a];
+        fl = exact_d(fi);
+      }
       i0[a] = fi;
       if (cell) cell[a] = fi;
-      w1[a] = f - (double)fi;  // in [0, 1] by construction
+      w1[a] = f - fl;  // in [0, 1] by construction
     }
     constexpr int C = NC;
     // 32-bit offsets inside a brick (a stored brick is < 2^31 samples)
@@ -408,7 +438,7 @@ struct Sampler {
         const int dz = q >> 1, dy = q & 1;
         const T* row = p + dz * sxyC + dy * sxC + c;
         const int a0 = __ldg(row), a1 = __ldg(row + C);
-        r[q] = fma(w1[0], (double)(a1 - a0), (double)a0);
+        r[q] = fma(w1[0], exact_sd(a1 - a0), exact_d(a0));
       }
       const double y0 = fma(w1[1], r[1] - r[0], r[0]), y1 = fma(w1[1], r[3] - r[2], r[2]);
       out[c] = (V)fma(w1[2], y1 - y0, y0);
@@ -421,7 +451,7 @@ struct Sampler {
   __device__ bool descend(const double pv[3], int target, DescentCache& dc) {
     int ip[3];
 #pragma unroll
-    for (int a = 0; a < 3; ++a) ip[a] = (int)pv[a];  // floor: pv >= 0
+    for (int a = 0; a < 3; ++a) ip[a] = floor_nonneg(pv[a]);  // pv >= 0
     if (dc.target == target) {
       bool ok = true;
 #pragma unroll
@@ -461,7 +491,7 @@ struct Sampler {
                             int alo[2][3]) const {
     int ip[3];
 #pragma unroll
-    for (int a = 0; a < 3; ++a) ip[a] = (int)pv[a];
+    for (int a = 0; a < 3; ++a) ip[a] = floor_nonneg(pv[a]);
     aidx[0] = aidx[1] = -1;
     alvl[0] = alvl[1] = 0;
     int idx = 0, l = P.g.depth;
@@ -881,7 +911,7 @@ __device__ __forceinline__ void march_ray(S& s, const TFTable& tf, const double 
   typename S::V vals[NC];
   Counters& cnt = s.cnt;
   for (int k = 0; k < n; ++k) {
-    double t = t0 + (double)k * P.step;
+    double t = t0 + exact_d(k) * P.step;
     double p[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) p[a] = P.cam[a] + t * d[a];
