@@ -1,3 +1,5 @@
+# Records of a reverted experiment (VT_RENDER_CARVEOUT); the committed library
+# ignores the variable, the ncu capture still applies.
 # render A/B of the shared-memory carveout + one ncu source-level capture
 for v in -1 0 10 25 50 100; do
   echo "VT_RENDER_CARVEOUT=$v" >> gpurun_out/ab_co.log

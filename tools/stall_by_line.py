@@ -21,6 +21,6 @@ base=min(samples)
 byline=collections.Counter()
 for a,(s,ins) in samples.items(): byline[addr2line.get(a-base)]+=s
 tot=sum(byline.values())
-srcl=open('/root/repo/paper_1407_2074_b200/csrc/render.cu').read().split('\n')
+srcl=open(sys.argv[5] if len(sys.argv)>5 else '/root/repo/paper_1407_2074_b200/csrc/render.cu').read().split('\n')
 for k,v in byline.most_common(int(sys.argv[4]) if len(sys.argv)>4 else 40):
     print(f"{v/tot*100:5.1f}% L{k} {srcl[k-1].strip()[:100] if k else ''}")
