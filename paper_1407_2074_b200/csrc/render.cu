@@ -293,10 +293,12 @@ struct DescentCache {
   int lo[3];   // box origin; the box is [lo, lo + exti[lvl])
 };
 
-// Exact integer <-> FP64 conversions on the FP64 pipe instead of the
-// quarter-rate conversion (XU) pipe, which the per-sample I2F/F2I ops (24
-// corner conversions, cell floors, box origins) otherwise saturate: for an
-// integer 0 <= v < 2^31 the double 2^52 + v is exact and its low word is v.
+// Exact integer -> FP64 conversions on the FP64 pipe: the per-sample
+// conversions (24 corner values, cell floors, box origins, descent floors)
+// all on the quarter-rate conversion (XU) pipe saturate it; the measured
+// fastest split puts the corner differences, box origins and the sample
+// index here and the rest on XU.  For an integer 0 <= v < 2^31 the double
+// 2^52 + v is exact.
 constexpr double kMagic52 = 4503599627370496.0;  // 2^52
 __device__ __forceinline__ double magic_of(unsigned v) {
   return __hiloint2double(0x43300000, (int)v);  // == 2^52 + v
@@ -307,11 +309,6 @@ __device__ __forceinline__ double exact_d(int v) { return magic_of((unsigned)v) 
 // word v + 2^31 is exactly 2^52 + 2^51 + 2^31 + v
 __device__ __forceinline__ double exact_sd(int v) {
   return __hiloint2double(0x43380000, v ^ (int)0x80000000) - 6755401588539392.0;
-}
-// floor(x) for 0 <= x < 2^31 (2^52 + x rounded toward -inf holds floor(x)
-// in its low word)
-__device__ __forceinline__ int floor_nonneg(double x) {
-  return __double2loint(__dadd_rd(x, kMagic52));
 }
 
 // floor(log2(v)) for a positive normal double: its unbiased exponent
@@ -448,7 +445,7 @@ struct Sampler {
   __device__ bool descend(const double pv[3], int target, DescentCache& dc) {
     int ip[3];
 #pragma unroll
-    for (int a = 0; a < 3; ++a) ip[a] = floor_nonneg(pv[a]);  // pv >= 0
+    for (int a = 0; a < 3; ++a) ip[a] = (int)pv[a];  // floor: pv >= 0
     if (dc.target == target) {
       bool ok = true;
 #pragma unroll
@@ -488,7 +485,7 @@ struct Sampler {
                             int alo[2][3]) const {
     int ip[3];
 #pragma unroll
-    for (int a = 0; a < 3; ++a) ip[a] = floor_nonneg(pv[a]);
+    for (int a = 0; a < 3; ++a) ip[a] = (int)pv[a];
     aidx[0] = aidx[1] = -1;
     alvl[0] = alvl[1] = 0;
     int idx = 0, l = P.g.depth;
